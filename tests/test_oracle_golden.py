@@ -1,0 +1,229 @@
+"""Pin the CPU oracle (oracle/port.py) to the reference's own outputs.
+
+The golden vectors were produced by the real reference (``greytrt``) by
+``tests/golden/make_golden.py``; the oracle must reproduce them to round-off
+before it is trusted as the checker of the GPU path.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+from oracle import port as P
+from oracle import runner as R
+from paper_2601_18705_b200 import problems
+from paper_2601_18705_b200.errors import ContractViolation, IterationLimitError
+
+
+def _grid(arr):
+    nx, ny, x0, y0, lx, ly = arr
+    return P.Grid(int(nx), int(ny), float(x0), float(y0), float(lx), float(ly))
+
+
+def _manual(n, sigma_t, sigma_s, q, inv_cdt):
+    return P.Step(np.asarray(sigma_t, float), np.asarray(sigma_s, float),
+                  np.asarray(sigma_t, float) - inv_cdt, np.asarray(q, float), np.zeros(n),
+                  np.ones(n), np.ones(n), 1.0, float(inv_cdt))
+
+
+def test_physics_matches_reference(golden):
+    g = golden("physics")
+    for tag in ("default", "unit"):
+        k = P.Constants(c=float(g[f"{tag}_c"]), a_r=float(g[f"{tag}_a_r"]))
+        B, dB = P.planck(g["T"], k)
+        assert rel_l2(B, g[f"{tag}_B"]) <= 1e-15 and rel_l2(dB, g[f"{tag}_dB"]) <= 1e-15
+        st = P.linearize(g["T"], g["sigma_a"], g["rho_cv"], float(g["dt"]), k)
+        for f in ("sigma_t", "sigma_s", "q", "denom"):
+            assert rel_l2(getattr(st, f), g[f"{tag}_{f}"]) <= 1e-15, f
+        assert st.inv_cdt == float(g[f"{tag}_inv_cdt"])
+        assert rel_l2(P.update_temperature(g[f"{tag}_phi"], st), g[f"{tag}_Tnew"]) <= 1e-15
+
+
+def test_physics_contract_errors():
+    with pytest.raises(ContractViolation):
+        P.planck(np.array([-1.0]))
+    with pytest.raises(ContractViolation):
+        P.linearize(np.ones(2), np.ones(2), np.ones(2), 0.0)
+    with pytest.raises(ContractViolation):
+        P.linearize(np.ones(2), -np.ones(2), np.ones(2), 1.0)
+
+
+def test_quadrature_matches_reference(golden):
+    g = golden("quadrature")
+    for npol, naz in ((2, 4), (4, 8), (16, 16), (3, 6)):
+        q = P.build_quadrature(npol, naz)
+        assert np.abs(q.omegas - g[f"om_{npol}_{naz}"]).max() <= 1e-15
+        assert np.abs(q.weights - g[f"w_{npol}_{naz}"]).max() <= 1e-15
+        assert abs(q.weights.sum() - 4 * np.pi) <= 1e-12
+
+
+@pytest.mark.parametrize("tag", ["a", "b"])
+def test_sweep_matches_reference(golden, tag):
+    g = golden("sweep")
+    grid = _grid(g[f"{tag}_grid"])
+    n = grid.n_cells
+    sig = g[f"{tag}_sigma_t"]
+    ops = P.assemble_operators(grid, _manual(n, sig, 0 * sig, np.zeros(n), 0.5))
+    psi = P.sweep_many(ops, g[f"{tag}_omegas"], g[f"{tag}_rhs"])
+    ref = g[f"{tag}_psi"]
+    for d in range(ref.shape[1]):
+        assert rel_l2(psi[:, d], ref[:, d]) <= 1e-13, d
+
+
+def test_sweep_quadrant_reflection_identity():
+    """A_c(omega) = P A_c(|omega|) P per quadrant: the basis
+    of the single-code-path GPU sweep."""
+    grid = P.Grid(3, 2, 0.0, 0.0, 1.5, 1.0)
+    n = grid.n_cells
+    st = _manual(n, np.linspace(1, 3, n), np.zeros(n), np.zeros(n), 0.2)
+    ops = P.assemble_operators(grid, st, with_matrices=False)
+    Px = np.eye(4)[[1, 0, 3, 2]]
+    Py = np.eye(4)[[2, 3, 0, 1]]
+    base = P._local_inverses(ops, np.array([[0.3, 0.5, 0.1]]))[0]
+    for sx, sy in ((-1, 1), (1, -1), (-1, -1)):
+        om = np.array([[0.3 * sx, 0.5 * sy, 0.1]])
+        got = P._local_inverses(ops, om)[0]
+        perm = (Px if sx < 0 else np.eye(4)) @ (Py if sy < 0 else np.eye(4))
+        assert np.abs(got - perm @ base @ perm).max() <= 1e-14 * np.abs(base).max()
+
+
+def test_source_iteration_matches_reference(golden):
+    g = golden("source_iteration")
+    grid = _grid(g["grid"])
+    n = grid.n_cells
+    for tag, dsa in (("plain", False), ("dsa", True)):
+        ops = P.assemble_operators(grid, _manual(n, g["sigma_t"], g["sigma_s"], g["q"], float(g["inv_cdt"])))
+        res = P.source_iteration(ops, g["omegas"], g["closure"], psi_time=g["psi_time"], use_dsa=dsa,
+                                 tol=1e-12, max_iters=400, phi_start=g["phi_start"],
+                                 extra_source=g["extra"])
+        assert res.iterations == int(g[f"{tag}_iters"])
+        assert rel_l2(res.psi, g[f"{tag}_psi"]) <= 1e-12
+        assert rel_l2(res.phi, g[f"{tag}_phi"]) <= 1e-12
+    ops = P.assemble_operators(grid, _manual(n, g["sigma_t"], 0 * g["sigma_s"], g["q"], float(g["inv_cdt"])))
+    res = P.source_iteration(ops, g["omegas"], g["closure"], psi_time=g["psi_time"], use_dsa=False, tol=1e-12)
+    assert res.iterations == int(g["absorber_iters"]) == 1
+    assert rel_l2(res.psi, g["absorber_psi"]) <= 1e-13
+
+
+def test_iteration_limit_matches_reference(golden):
+    g = golden("source_iteration")
+    grid = P.Grid(8, 8)
+    ops = P.assemble_operators(grid, _manual(64, np.full(64, 100.0), np.full(64, 99.99), np.ones(64), 0.0))
+    q = P.build_quadrature(2, 4)
+    with pytest.raises(IterationLimitError) as err:
+        P.source_iteration(ops, q.omegas, q.weights, use_dsa=False, tol=1e-8, max_iters=10)
+    assert err.value.iterations == int(g["limit_iters"])
+    assert abs(err.value.residual - float(g["limit_residual"])) <= 1e-10 * float(g["limit_residual"])
+
+
+def test_gram_schmidt_with_deficiency_matches_reference(golden):
+    g = golden("gram_schmidt")
+    grid = P.Grid(5, 4, 0.0, 0.0, 2.0, 1.0)
+    ops = P.assemble_operators(grid, _manual(20, np.full(20, 2.0), np.ones(20), np.ones(20), 0.1),
+                               with_matrices=False)
+    comp = P.spatial_monomials(P.dof_coordinates(grid), grid.extent, 6 + 8)
+    q, r, d = P.gram_schmidt(g["x_cols"], P.mass_dot(ops), comp)
+    assert list(d) == list(g["x_def"]) == [3]
+    assert np.abs(q - g["x_q"]).max() <= 1e-12
+    assert np.abs(r - g["x_r"]).max() <= 1e-12 * np.abs(g["x_r"]).max()
+    quad = P.build_quadrature(3, 6)
+    w, rr, dw = P.orthonormalize(g["w_cols"], quad)
+    assert list(dw) == list(g["w_def"])
+    assert np.abs(w - g["w_q"]).max() <= 1e-10
+    assert np.abs(rr - g["w_r"]).max() <= 1e-12
+    assert np.abs(w.T @ quad.weights - g["w_beta"]).max() <= 1e-12
+
+
+def test_deim_matches_reference(golden):
+    g = golden("deim")
+    quad = P.build_quadrature(4, 8)
+    for r in (1, 3, 6, 12):
+        W = g[f"W{r}"]
+        sel = P.deim_select(W)
+        assert list(sel.indices) == list(g[f"idx{r}"])
+        assert abs(sel.cond - float(g[f"cond{r}"])) <= 1e-12 * float(g[f"cond{r}"])
+        beta = W.T @ quad.weights
+        assert rel_l2(sel.closure_weights(beta), g[f"closure{r}"]) <= 1e-13
+        assert rel_l2(sel.interpolation_coefficients(g[f"vals{r}"]), g[f"gamma{r}"]) <= 1e-13
+
+
+def test_projections_and_row_solve_match_reference(golden):
+    g = golden("projections")
+    grid = P.Grid(6, 5, 0.0, 0.0, 1.5, 1.0)
+    st = _manual(30, g["sigma_t"], g["sigma_s"], g["q"], float(g["inv_cdt"]))
+    ops = P.assemble_operators(grid, st)
+    proj = P.project_row_operators(ops, g["x"])
+    for k in ("px", "py", "jx", "jy", "mt", "ms", "q"):
+        assert rel_l2(proj[k], g[f"p_{k}"]) <= 1e-13, k
+    old = P.State(g["old_X"], g["old_S"], g["old_W"], None)
+    assert rel_l2(P.project_initial(old, g["x"], ops), g["pinit"]) <= 1e-13
+    B = P.row_matrices(proj, g["omegas"])
+    assert rel_l2(B, g["B"]) <= 1e-13
+    L, lbar = P.solve_row_system(g["B"], g["p_ms"], g["Q"], g["closure"])
+    assert rel_l2(L, g["L"]) <= 1e-12 and rel_l2(lbar, g["lbar"]) <= 1e-12
+
+
+def _cell_step(grid, sigma_a, dt, T0):
+    n = grid.n_cells
+    return P.linearize(np.full(n, float(T0)), np.full(n, float(sigma_a)), np.ones(n), dt)
+
+
+def test_edge_cases_match_reference(golden):
+    g = golden("edge_cases")
+    grid = P.Grid(4, 4)
+    quad = P.build_quadrature(2, 4)
+    # cold empty problem: every swept column deficient -> spatial completion
+    st = P.State(g["cold_X"], g["cold_S"], g["cold_W"], g["cold_W"].T @ quad.weights)
+    new, info = P.step_collocation(grid, _cell_step(grid, 2.0, 0.2, 0.0), quad, st)
+    assert info.spatial_deficiency == int(g["cold_sdef"]) == 3
+    assert info.angular_deficiency == int(g["cold_adef"])
+    assert list(info.angle_indices) == list(g["cold_idx"])
+    assert np.abs(info.phi).max() == 0.0 and np.abs(new.S).max() == 0.0
+    assert np.abs(new.X - g["cold_newX"]).max() <= 1e-12
+    # full-rank step (r = N_Omega) reproduces the reference
+    st = P.State(g["full_X"], g["full_S"], g["full_W"], g["full_W"].T @ quad.weights)
+    new, info = P.step_collocation(grid, _cell_step(grid, 2.0, 0.3, 0.6), quad, st, si_tol=1e-13,
+                                   si_max_iters=800, use_dsa=False)
+    assert info.iterations == int(g["full_iters"])
+    assert list(info.angle_indices) == list(g["full_idx"])
+    assert rel_l2(new.reconstruct(), g["full_psi"]) <= 1e-11
+    assert rel_l2(info.phi, g["full_phi"]) <= 1e-11
+
+
+def _run_checker(g):
+    per, r, nq, seed = int(g["per"]), int(g["rank"]), int(g["nq"]), int(g["seed"])
+    spec = problems.checkerboard(per, rank=r, n_polar=nq, n_azimuthal=nq, seed=seed)
+    rng = np.random.default_rng(spec.seed)
+    Xr, Wr = problems.draw_factors(spec, rng)
+    X, W = R.orthonormal_factors(spec, Xr, Wr)
+    st0 = R.initial_state(spec, X, W)
+    return spec, st0
+
+
+@pytest.mark.parametrize("name", ["dlr_small", "dlr_c1"])
+def test_dlr_steps_match_reference(golden, name):
+    g = golden(name)
+    spec, st0 = _run_checker(g)
+    ops = P.assemble_operators(R.grid_of(spec), _cell_step(R.grid_of(spec), 1.0, 1.0, 1.0),
+                               with_matrices=False)
+    b0 = P.planck(P.cells_to_dofs(spec.T0), R.constants_of(spec))[0]
+    assert rel_l2(st0.X.T @ ops.mass_apply(b0), g["X0_mb0"]) <= 1e-13
+    assert rel_l2(st0.W, g["W0"]) <= 1e-13 and rel_l2(st0.S, g["S0"]) <= 1e-13
+    recs = []
+    R.run(spec, st0, int(g["nsteps"]), record=lambda s, i, t: recs.append((s, i, t)))
+    rng = np.random.default_rng(9)
+    for k, (s, info, T) in enumerate(recs):
+        assert list(info.angle_indices) == list(g[f"s{k}_idx"]), k
+        assert info.iterations == int(g[f"s{k}_iters"])
+        assert rel_l2(info.phi, g[f"s{k}_phi"]) <= 1e-11
+        assert rel_l2(T, g[f"s{k}_T"]) <= 1e-11
+        assert rel_l2(s.scalar_flux(), g[f"s{k}_phiq"]) <= 1e-11
+        rng = np.random.default_rng(9)
+        phi_t = rng.standard_normal((s.X.shape[0], 12))
+        om_t = rng.standard_normal((s.W.shape[0], 12))
+        sk = (phi_t.T @ s.X) @ s.S @ (s.W.T @ om_t)
+        assert rel_l2(sk, g[f"s{k}_sketch"]) <= 1e-11
+        assert abs(info.interpolation_condition - float(g[f"s{k}_cond"])) <= 1e-9 * float(g[f"s{k}_cond"])
+    if "final_X" in g:
+        s = recs[-1][0]
+        assert P.lowrank_rel_diff(s.X, s.S, s.W, g["final_X"], g["final_S"], g["final_W"]) <= 1e-11
