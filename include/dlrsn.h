@@ -1,0 +1,163 @@
+/*
+ * dlrsn.h -- C ABI of the B200 (sm_100a) SN-like DLR hot path.
+ *
+ * The reference (greytrt, Python/numpy) has no FFI: its boundary is the
+ * Python function API.  These entry points are what a maintainer would bind
+ * (ctypes / cffi) to replace the numpy kernels under
+ * that API.  Each declaration cites the reference function it replaces
+ * (paths relative to /root/reference/pkg/src/greytrt).
+ *
+ * Conventions
+ *  - All pointers are caller-owned DEVICE pointers unless the comment says
+ *    "host".  fp64 throughout ("f64"); ints are int32 unless noted.
+ *  - `stream` is a cudaStream_t passed as void*.  No entry point allocates
+ *    device memory or synchronises the host; workspaces are caller-owned.
+ *  - Return: 0 = DLRSN_OK, negative = error (see codes).  The Python shim
+ *    maps them onto the reference's exceptions (errors.py:4-41);
+ *    dlrsn_last_error() gives the message of the last failing call.
+ *  - Canonical layout = the reference's: dof = 4*cell + local,
+ *    cell = j*nx + i, local 0..3 = corners (0,0),(1,0),(0,1),(1,1)
+ *    (mesh.py:28-33,117-118); psi/X are (n_dofs, ld) row-major.
+ *  - "SK" layout (sweep-native, per direction or per quadrant): for the
+ *    quadrant (sx,sy) a cell (i,j) is addressed by oriented coordinates
+ *    i' = sx>0 ? i : nx-1-i, j' = sy>0 ? j : ny-1-j, strip s = j'/32,
+ *    lane = j'%32, step t = i' + lane; a 4-dof slab is
+ *    [n_strips][nx+31][2 dof-pairs][32 lanes][2] f64 with local dofs stored
+ *    in the oriented frame (local' = local ^ (sx<0) ^ 2*(sy<0)); a scalar
+ *    slab is [n_strips][nx+31][32].  dlrsn_sk_vec_len / dlrsn_sk_scalar_len
+ *    give the per-slab element counts.
+ */
+#ifndef DLRSN_H
+#define DLRSN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* dlrsn_stream_t;
+
+enum {
+  DLRSN_OK = 0,
+  DLRSN_EINVAL = -1,      /* ContractViolation */
+  DLRSN_ESINGULAR = -2,   /* SolverError (singular reduced operator) */
+  DLRSN_ENONFINITE = -3,  /* SolverError (non-finite values) */
+  DLRSN_ECUDA = -4,       /* CUDA runtime failure */
+  DLRSN_EINTERP = -5,     /* InterpolationError */
+  DLRSN_ECOMPLETION = -6  /* ContractViolation: ran out of completion vectors */
+};
+
+#define DLRSN_MAX_DW 8 /* directions per sweep group (one warp) */
+
+/* Per-cell reference blocks, computed on the host exactly as the reference
+ * does (mesh.py:285-313 scaled as in transport_sn.py:213-227). */
+typedef struct dlrsn_cellops {
+  int nx, ny;
+  double x0, y0, dx, dy;
+  double mass[16];   /* dx*dy*Mhat, row-major */
+  double gx[16];     /* -dy*Ghat_xi   (grad_cell[0]) */
+  double gy[16];     /* -dx*Ghat_eta  (grad_cell[1]) */
+  double e2x[4];     /* dy*Ehat (vertical faces) */
+  double e2y[4];     /* dx*Ehat (horizontal faces) */
+  double src_row[4]; /* mass.sum(axis=1) (transport_sn.py:124-127) */
+} dlrsn_cellops;
+
+/* One sweep group: up to DLRSN_MAX_DW directions of one quadrant swept by
+ * one warp per 32-row strip.  quad = (sx<0) | 2*(sy<0). */
+typedef struct dlrsn_group {
+  int32_t quad;
+  int32_t ndir;
+  int32_t slot[DLRSN_MAX_DW]; /* direction slot (column of rhs/psi) */
+  double ox[DLRSN_MAX_DW];    /* |omega_x| */
+  double oy[DLRSN_MAX_DW];    /* |omega_y| */
+  double cw[DLRSN_MAX_DW];    /* closure weight (phi = sum_d cw_d psi_d) */
+} dlrsn_group;
+
+int dlrsn_version(void);
+const char* dlrsn_last_error(void);
+int dlrsn_device_sm_count(int* out);
+
+int64_t dlrsn_sk_vec_len(int nx, int ny);
+int64_t dlrsn_sk_scalar_len(int nx, int ny);
+/* bytes of workspace dlrsn_sweep needs for G groups of width dw */
+int64_t dlrsn_sweep_workspace_bytes(int nx, int ny, int n_groups, int dw);
+
+/* ---- K4: per-cell physics (physics.py:63-132, driver.py:344-346,532-534) */
+
+/* linearize (physics.py:94-120) + BASELINE adapters: sigma_t += ss_phys,
+ * sigma_s += ss_phys, q += q_ext (nullable).  status (device int, OR-ed)
+ * gets 1 if a contract fails (T<0, sigma_a<0, rho_cv<=0). */
+int dlrsn_linearize(int n, const double* T0, const double* sigma_a, const double* rho_cv,
+                    double dt, double c, double a_r, const double* ss_phys,
+                    const double* q_ext, double* sigma_t, double* sigma_s, double* q,
+                    double* denom, int* status, dlrsn_stream_t stream);
+
+/* update_temperature (physics.py:123-132); phi is per cell, or per dof
+ * (phi_per_dof=1: cell mean of the 4 dofs first, driver.py:344-346).
+ * T = max(T0 + dt*sigma_a*(phi - 4 pi B(T0))/denom, t_floor). */
+int dlrsn_update_temperature(int n, const double* phi, int phi_per_dof, const double* T0,
+                             const double* sigma_a, const double* denom, double dt, double c,
+                             double a_r, double t_floor, double* T, dlrsn_stream_t stream);
+
+/* Fused driver step boundary: T update of the finished step followed by the
+ * linearisation of the next one (driver.py:486-487,532-534 +
+ * physics.py:94-120).  sigma_a(T) = sigma_a0 * T^opacity_power when
+ * opacity_power != 0 (Marshak), else sigma_a0. */
+int dlrsn_advance_relinearize(int n, const double* phi_dofs, double* T, double* sigma_a,
+                              const double* sigma_a0, double opacity_power,
+                              const double* rho_cv, double dt, double c, double a_r,
+                              double t_floor, const double* ss_phys, const double* q_ext,
+                              double* sigma_t, double* sigma_s, double* q, double* denom,
+                              int* status, dlrsn_stream_t stream);
+
+/* ---- K1: sweep data movement (transport_sn.py:377-450) */
+
+/* rhs_sk[d] = source_vector(q) + inv_cdt * M psi_time[:, d] + extra[:, d]
+ * (transport_sn.py:403-407) for D direction slots of quadrant quad[d]
+ * (host-built int array on device).  psi_time / extra are canonical
+ * (n_dofs, ld_*) and nullable. */
+int dlrsn_rhs_build(const dlrsn_cellops* ops, int D, const int* quad, const double* q,
+                    double inv_cdt, const double* psi_time, int ld_psi_time,
+                    const double* extra, int ld_extra, double* rhs_sk, dlrsn_stream_t stream);
+
+/* scalar per cell -> 4 quadrant SK slabs (out + k*sk_scalar_len) */
+int dlrsn_cells_to_sk4(const dlrsn_cellops* ops, const double* cell_values, double* out_sk4,
+                       dlrsn_stream_t stream);
+
+/* scatter = M (sigma_s * phi) / 4 pi (transport_sn.py:436) written to the 4
+ * quadrant SK slabs; also OR-s 1 into *any_scatter if some sigma_s != 0
+ * (transport_sn.py:410). */
+int dlrsn_scatter_source(const dlrsn_cellops* ops, const double* phi, const double* sigma_s,
+                         double* scat_sk4, int* any_scatter, dlrsn_stream_t stream);
+
+/* phi_new = sum_g phi_part[g] (fixed order), scat for the next iteration,
+ * and norms[0] = ||phi_new - phi_old||^2, norms[1] = ||phi_new||^2
+ * (deterministic reduction; transport_sn.py:438,442-446).  groups: device
+ * table; partial_ws >= 2*ceil(n_cells/256) doubles + 1 int counter. */
+int dlrsn_phi_combine(const dlrsn_cellops* ops, int G, const dlrsn_group* groups,
+                      const double* phi_part_sk, const double* phi_old, const double* sigma_s,
+                      double* phi_new, double* scat_sk4, double* norms, void* partial_ws,
+                      dlrsn_stream_t stream);
+
+/* psi (n_dofs, ld) canonical <- psi_sk[d] for d < D */
+int dlrsn_sk_to_canonical(const dlrsn_cellops* ops, int D, const int* quad,
+                          const double* psi_sk, double* psi, int ld, dlrsn_stream_t stream);
+
+/* ---- K1: the sweep (transport_sn.py:142-163,303-322 batched over
+ * directions, sweep_all :419-427, phi_half :438).
+ * One persistent launch sweeps every direction of every group: warp =
+ * (group, 32-row strip), lanes = rows, marching the oriented x axis; the
+ * strip above is fed through an L2 handoff with release/acquire progress
+ * counters.  rhs_sk / psi_sk: D slabs; sigma_t_sk4 / scat_sk4: quadrant
+ * slabs (scat nullable => no scattering term); phi_part_sk: G slabs
+ * (nullable).  dw = template width >= max group ndir (1,2,4,8). */
+int dlrsn_sweep(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int dw,
+                const double* sigma_t_sk4, const double* scat_sk4, const double* rhs_sk,
+                double* psi_sk, double* phi_part_sk, void* workspace, int64_t workspace_bytes,
+                int max_ctas, dlrsn_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DLRSN_H */

@@ -1,0 +1,66 @@
+"""Device plumbing: which CUDA device, the current stream, fp64 tensors.
+
+The B200 path is CUDA-only: ``device()`` raises when no GPU is visible
+instead of silently computing on the host.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+
+_DEV = None
+
+
+def device():
+    global _DEV
+    if _DEV is None:
+        if not torch.cuda.is_available():
+            raise RuntimeError("the B200 DLR-SN path needs a CUDA device (no CPU fallback)")
+        _DEV = torch.device("cuda", torch.cuda.current_device())
+        _lib.load()
+    return _DEV
+
+
+def set_device(index):
+    global _DEV
+    torch.cuda.set_device(index)
+    _DEV = torch.device("cuda", index)
+    _lib.load()
+
+
+def stream():
+    return ctypes.c_void_p(torch.cuda.current_stream(device()).cuda_stream)
+
+
+def as_device(x, n=None, dtype=torch.float64):
+    """fp64 contiguous CUDA tensor from numpy / torch / scalar (scalars
+    broadcast to length ``n``)."""
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=device(), dtype=dtype)
+    else:
+        a = np.asarray(x, dtype=np.float64 if dtype == torch.float64 else None)
+        if a.ndim == 0 and n is not None:
+            a = np.full(n, float(a))
+        t = torch.from_numpy(np.ascontiguousarray(a)).to(device=device(), dtype=dtype)
+    if t.ndim == 0 and n is not None:
+        t = t.expand(n)
+    return t.contiguous()
+
+
+def zeros(*shape, dtype=torch.float64):
+    return torch.zeros(*shape, dtype=dtype, device=device())
+
+
+def empty(*shape, dtype=torch.float64):
+    return torch.empty(*shape, dtype=dtype, device=device())
+
+
+def to_numpy(t):
+    if isinstance(t, torch.Tensor):
+        return t.detach().cpu().numpy()
+    return np.asarray(t)

@@ -1,0 +1,120 @@
+"""ctypes binding of the C-ABI library ``libdlrsn.so`` (include/dlrsn.h).
+
+The library is built in-tree (``paper_2601_18705_b200/build.py``) and loaded
+from the package directory; there is no fallback: if the library is missing
+or no CUDA device is visible, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .errors import ContractViolation, InterpolationError, SolverError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdlrsn.so")
+
+MAX_DW = 8
+
+c_int = ctypes.c_int
+c_i64 = ctypes.c_int64
+c_dbl = ctypes.c_double
+c_vp = ctypes.c_void_p
+
+
+class CellOps(ctypes.Structure):
+    _fields_ = [
+        ("nx", c_int), ("ny", c_int),
+        ("x0", c_dbl), ("y0", c_dbl), ("dx", c_dbl), ("dy", c_dbl),
+        ("mass", c_dbl * 16), ("gx", c_dbl * 16), ("gy", c_dbl * 16),
+        ("e2x", c_dbl * 4), ("e2y", c_dbl * 4), ("src_row", c_dbl * 4),
+    ]
+
+
+# numpy mirror of struct dlrsn_group (include/dlrsn.h)
+GROUP_DTYPE = np.dtype([
+    ("quad", np.int32), ("ndir", np.int32), ("slot", np.int32, (MAX_DW,)),
+    ("ox", np.float64, (MAX_DW,)), ("oy", np.float64, (MAX_DW,)), ("cw", np.float64, (MAX_DW,)),
+], align=True)
+
+# name -> (restype, argtypes); keep in sync with include/dlrsn.h
+_SIGNATURES = {
+    "dlrsn_version": (c_int, []),
+    "dlrsn_last_error": (ctypes.c_char_p, []),
+    "dlrsn_device_sm_count": (c_int, [c_vp]),
+    "dlrsn_sk_vec_len": (c_i64, [c_int, c_int]),
+    "dlrsn_sk_scalar_len": (c_i64, [c_int, c_int]),
+    "dlrsn_sweep_workspace_bytes": (c_i64, [c_int, c_int, c_int, c_int]),
+    "dlrsn_linearize": (c_int, [c_int, c_vp, c_vp, c_vp, c_dbl, c_dbl, c_dbl, c_vp, c_vp,
+                                c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "dlrsn_update_temperature": (c_int, [c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_dbl, c_dbl,
+                                         c_dbl, c_dbl, c_vp, c_vp]),
+    "dlrsn_advance_relinearize": (c_int, [c_int, c_vp, c_vp, c_vp, c_vp, c_dbl, c_vp, c_dbl,
+                                          c_dbl, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                          c_vp, c_vp, c_vp]),
+    "dlrsn_rhs_build": (c_int, [c_vp, c_int, c_vp, c_vp, c_dbl, c_vp, c_int, c_vp, c_int, c_vp,
+                                c_vp]),
+    "dlrsn_cells_to_sk4": (c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "dlrsn_scatter_source": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "dlrsn_phi_combine": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                  c_vp]),
+    "dlrsn_sk_to_canonical": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp, c_int, c_vp]),
+    "dlrsn_sweep": (c_int, [c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64,
+                            c_int, c_vp]),
+}
+
+_lib = None
+
+
+def exported_symbols():
+    return sorted(_SIGNATURES)
+
+
+def load(path=LIB_PATH):
+    """Load (once) and type the library; raises if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            " (the B200 path has no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(status, what=""):
+    if status == 0:
+        return
+    msg = load().dlrsn_last_error().decode(errors="replace")
+    text = f"{what}: {msg}" if what else msg
+    if status == -1 or status == -6:
+        raise ContractViolation(text)
+    if status == -5:
+        raise InterpolationError(text, column=-1)
+    if status in (-2, -3):
+        raise SolverError(text)
+    raise RuntimeError(f"dlrsn CUDA failure ({status}): {text}")
+
+
+def call(name, *args):
+    check(getattr(load(), name)(*args), name)
+
+
+def ptr(t):
+    """Device pointer of a torch tensor (None -> NULL)."""
+    return None if t is None else c_vp(t.data_ptr())
+
+
+def stream_handle(device=None):
+    import torch
+
+    return c_vp(torch.cuda.current_stream(device).cuda_stream)

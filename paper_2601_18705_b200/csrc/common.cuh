@@ -1,0 +1,110 @@
+// Shared helpers for the sm_100a DLR-SN kernels: error plumbing, the
+// sweep-native "SK" addressing (see include/dlrsn.h) and small fp64 utilities.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/dlrsn.h"
+
+namespace dlrsn {
+
+void set_error(const char* fmt, ...);
+
+#define DLRSN_TRY_CUDA(expr)                                                        \
+  do {                                                                              \
+    cudaError_t e_ = (expr);                                                        \
+    if (e_ != cudaSuccess) {                                                        \
+      ::dlrsn::set_error("%s failed: %s", #expr, cudaGetErrorString(e_));           \
+      return DLRSN_ECUDA;                                                           \
+    }                                                                               \
+  } while (0)
+
+#define DLRSN_CHECK_LAUNCH(name)                                                    \
+  do {                                                                              \
+    cudaError_t e_ = cudaGetLastError();                                            \
+    if (e_ != cudaSuccess) {                                                        \
+      ::dlrsn::set_error("launch of %s failed: %s", name, cudaGetErrorString(e_));  \
+      return DLRSN_ECUDA;                                                           \
+    }                                                                               \
+  } while (0)
+
+#define DLRSN_REQUIRE(cond, ...)                                                    \
+  do {                                                                              \
+    if (!(cond)) {                                                                  \
+      ::dlrsn::set_error(__VA_ARGS__);                                              \
+      return DLRSN_EINVAL;                                                          \
+    }                                                                               \
+  } while (0)
+
+inline cudaStream_t as_stream(dlrsn_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+constexpr double kFourPi = 12.566370614359172;  // 4*np.pi
+constexpr double kPi = 3.141592653589793;
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---- SK layout -------------------------------------------------------------
+__host__ __device__ inline int sk_strips(int ny) { return (ny + 31) >> 5; }
+__host__ __device__ inline int sk_steps(int nx) { return nx + 31; }
+__host__ __device__ inline int64_t sk_vec_len(int nx, int ny) {
+  return (int64_t)sk_strips(ny) * sk_steps(nx) * 128;
+}
+__host__ __device__ inline int64_t sk_scalar_len(int nx, int ny) {
+  return (int64_t)sk_strips(ny) * sk_steps(nx) * 32;
+}
+// offset (in doubles) of the double2 holding oriented dofs (2h, 2h+1)
+__host__ __device__ inline int64_t sk_vec_off(int T, int s, int t, int h, int lane) {
+  return ((((int64_t)s * T + t) * 2 + h) * 32 + lane) * 2;
+}
+__host__ __device__ inline int64_t sk_sc_off(int T, int s, int t, int lane) {
+  return ((int64_t)s * T + t) * 32 + lane;
+}
+// canonical cell (i,j) -> (strip, step, lane) in quadrant `quad`
+__host__ __device__ inline void sk_locate(int i, int j, int quad, int nx, int ny, int& s, int& t,
+                                          int& lane) {
+  const int ip = (quad & 1) ? nx - 1 - i : i;
+  const int jp = (quad & 2) ? ny - 1 - j : j;
+  s = jp >> 5;
+  lane = jp & 31;
+  t = ip + lane;
+}
+// oriented local dof <-> canonical local dof (an involution)
+__host__ __device__ inline int sk_flip(int quad) { return (quad & 1) | (quad & 2); }
+
+// ---- memory-model helpers ---------------------------------------------------
+__device__ inline int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ inline void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// deterministic block sum of NV doubles (fixed tree order); result in lane 0
+// of warp 0.  blockDim.x must be a multiple of 32 and <= 1024.
+template <int NV>
+__device__ inline void block_sum(double (&v)[NV], double* smem /* 32*NV */) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(kFull, v[k], o);
+  }
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) smem[w * NV + k] = v[k];
+  }
+  __syncthreads();
+  if (w == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      v[k] = lane < nw ? smem[lane * NV + k] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(kFull, v[k], o);
+    }
+  }
+}
+
+}  // namespace dlrsn

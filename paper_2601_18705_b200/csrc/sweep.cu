@@ -1,0 +1,514 @@
+// K1: the upwind DG(Q1) transport sweep and its data movement.
+//
+// Restates transport_sn.py:142-163 (local operator), :303-322 (wavefront
+// sweep), :403-407 (rhs), :419-438 (sweep_all + phi closure) for all swept
+// directions at once.  Design:
+//   * one warp = (direction group, 32-row strip); lane = row; the warp marches
+//     the quadrant-oriented x axis with a one-column skew per lane, so the
+//     x-upwind value stays in registers and the y-upwind value arrives by
+//     __shfl_up_sync from the lane below one step earlier;
+//   * data are stored in the sweep-native SK layout, so each warp-wide access
+//     is one contiguous 512 B (double2 per lane) transaction;
+//   * the strip above is fed through an L2 "handoff" column with
+//     release/acquire progress counters; warps take work tickets in strip-major
+//     order, so every wait targets a smaller, already-running ticket
+//     (deadlock-free without co-residency assumptions);
+//   * the 4x4 local operator A = sigma_t M + |wx| Gx' + |wy| Gy' is formed and
+//     solved in registers per cell-angle (no stored inverses: the reference's
+//     128 B/cell-angle cache is not materialised);
+//   * the closure phi_g = sum_d cw_d psi_d of the warp's directions is
+//     accumulated in registers (deterministic, no atomics).
+#include <cmath>
+
+#include "common.cuh"
+
+namespace dlrsn {
+
+struct SweepArgs {
+  int nx, ny, G;
+  const dlrsn_group* groups;
+  const double* sigma_sk4;
+  const double* scat_sk4;
+  const double* rhs_sk;
+  double* psi_sk;
+  double* phi_sk;
+  int* ticket;
+  int* progress;
+  double* handoff;
+  double mass[16];
+  double gxp[16];  // Gx + e2x embedded at the right edge (oriented +x outflow)
+  double gyp[16];  // Gy + e2y embedded at the top edge
+  double ex[4];    // e2x (left inflow coupling)
+  double ey[4];    // e2y (bottom inflow coupling)
+  int64_t vlen, slen;
+};
+
+__device__ __forceinline__ void solve4(double* a, double* b, double* x) {
+  // Gaussian elimination without pivoting: A has a positive-definite
+  // symmetric part (sigma_t M + upwind outflow terms), so the pivots are
+  // positive.  The reference inverts with LAPACK (transport_sn.py:158); the
+  // two differ only at round-off.
+  const double p0 = 1.0 / a[0];
+  double l = a[4] * p0;
+  a[5] -= l * a[1]; a[6] -= l * a[2]; a[7] -= l * a[3]; b[1] -= l * b[0];
+  l = a[8] * p0;
+  a[9] -= l * a[1]; a[10] -= l * a[2]; a[11] -= l * a[3]; b[2] -= l * b[0];
+  l = a[12] * p0;
+  a[13] -= l * a[1]; a[14] -= l * a[2]; a[15] -= l * a[3]; b[3] -= l * b[0];
+  const double p1 = 1.0 / a[5];
+  l = a[9] * p1;
+  a[10] -= l * a[6]; a[11] -= l * a[7]; b[2] -= l * b[1];
+  l = a[13] * p1;
+  a[14] -= l * a[6]; a[15] -= l * a[7]; b[3] -= l * b[1];
+  const double p2 = 1.0 / a[10];
+  l = a[14] * p2;
+  a[15] -= l * a[11]; b[3] -= l * b[2];
+  x[3] = b[3] / a[15];
+  x[2] = (b[2] - a[11] * x[3]) * p2;
+  x[1] = (b[1] - a[6] * x[2] - a[7] * x[3]) * p1;
+  x[0] = (b[0] - a[1] * x[1] - a[2] * x[2] - a[3] * x[3]) * p0;
+}
+
+template <int DW>
+__global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
+  __shared__ double s_S[4][DW][16];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int nx = a.nx, ny = a.ny, G = a.G;
+  const int T = nx + 31;
+  const int ns = (ny + 31) >> 5;
+  const int items = ns * G;
+
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(a.ticket, 1);
+    item = __shfl_sync(kFull, item, 0);
+    if (item >= items) break;
+    const int s = item / G;
+    const int g = item - s * G;
+    const dlrsn_group& grp = a.groups[g];
+    const int quad = grp.quad;
+    const int nd = grp.ndir;
+
+    __syncwarp();
+    for (int e = lane; e < DW * 16; e += 32) {
+      const int k = e >> 4, m = e & 15;
+      s_S[wib][k][m] = k < nd ? grp.ox[k] * a.gxp[m] + grp.oy[k] * a.gyp[m] : 0.0;
+    }
+    __syncwarp();
+
+    double ox[DW], oy[DW], cw[DW];
+    const double* rhs_base[DW];
+    double* psi_base[DW];
+#pragma unroll
+    for (int k = 0; k < DW; ++k) {
+      const bool on = k < nd;
+      ox[k] = on ? grp.ox[k] : 0.0;
+      oy[k] = on ? grp.oy[k] : 0.0;
+      cw[k] = on ? grp.cw[k] : 0.0;
+      const int slot = on ? grp.slot[k] : 0;
+      rhs_base[k] = a.rhs_sk + (int64_t)slot * a.vlen;
+      psi_base[k] = a.psi_sk + (int64_t)slot * a.vlen;
+    }
+    const double* sig = a.sigma_sk4 + (int64_t)quad * a.slen;
+    const double* scat = a.scat_sk4 ? a.scat_sk4 + (int64_t)quad * a.vlen : nullptr;
+    double* phi = a.phi_sk ? a.phi_sk + (int64_t)g * a.vlen : nullptr;
+
+    const int jp = (s << 5) + lane;
+    const bool row_ok = jp < ny;
+    const double* hin = s > 0 ? a.handoff + ((int64_t)(s - 1) * G + g) * nx * DW * 2 : nullptr;
+    double* hout = (s + 1 < ns) ? a.handoff + ((int64_t)s * G + g) * nx * DW * 2 : nullptr;
+    const int* pin = s > 0 ? a.progress + (s - 1) * G + g : nullptr;
+    int* pout = a.progress + s * G + g;
+    int avail = 0;
+
+    double xin[DW][2], yin[DW][2];
+#pragma unroll
+    for (int k = 0; k < DW; ++k) xin[k][0] = xin[k][1] = yin[k][0] = yin[k][1] = 0.0;
+
+    for (int t = 0; t < T; ++t) {
+      const int ip = t - lane;
+      const bool act = row_ok && ip >= 0 && ip < nx;
+      if (lane == 0 && act && hin) {
+        if (ip >= avail) {
+          while ((avail = ld_acquire_gpu(pin)) <= ip) __nanosleep(32);
+        }
+#pragma unroll
+        for (int k = 0; k < DW; ++k) {
+          const double2 v = __ldcg(reinterpret_cast<const double2*>(hin) + (int64_t)ip * DW + k);
+          yin[k][0] = v.x;
+          yin[k][1] = v.y;
+        }
+      }
+      double ytop[DW][2];
+#pragma unroll
+      for (int k = 0; k < DW; ++k) ytop[k][0] = ytop[k][1] = 0.0;
+      if (act) {
+        const double sigma = __ldg(sig + sk_sc_off(T, s, t, lane));
+        double sc[4] = {0.0, 0.0, 0.0, 0.0};
+        if (scat) {
+          const double2 u = __ldg(reinterpret_cast<const double2*>(scat + sk_vec_off(T, s, t, 0, lane)));
+          const double2 v = __ldg(reinterpret_cast<const double2*>(scat + sk_vec_off(T, s, t, 1, lane)));
+          sc[0] = u.x; sc[1] = u.y; sc[2] = v.x; sc[3] = v.y;
+        }
+        double ph[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < DW; ++k) {
+          if (k < nd) {
+            const double2 u = __ldg(reinterpret_cast<const double2*>(rhs_base[k] + sk_vec_off(T, s, t, 0, lane)));
+            const double2 v = __ldg(reinterpret_cast<const double2*>(rhs_base[k] + sk_vec_off(T, s, t, 1, lane)));
+            double b[4] = {u.x + sc[0], u.y + sc[1], v.x + sc[2], v.y + sc[3]};
+            // upwind couplings (transport_sn.py:312-320): x first, then y
+            b[0] += ox[k] * (a.ex[0] * xin[k][0] + a.ex[1] * xin[k][1]);
+            b[2] += ox[k] * (a.ex[2] * xin[k][0] + a.ex[3] * xin[k][1]);
+            b[0] += oy[k] * (a.ey[0] * yin[k][0] + a.ey[1] * yin[k][1]);
+            b[1] += oy[k] * (a.ey[2] * yin[k][0] + a.ey[3] * yin[k][1]);
+            double A[16];
+#pragma unroll
+            for (int m = 0; m < 16; ++m) A[m] = fma(sigma, a.mass[m], s_S[wib][k][m]);
+            double x[4];
+            solve4(A, b, x);
+            double2* po = reinterpret_cast<double2*>(psi_base[k]);
+            po[sk_vec_off(T, s, t, 0, lane) >> 1] = make_double2(x[0], x[1]);
+            po[sk_vec_off(T, s, t, 1, lane) >> 1] = make_double2(x[2], x[3]);
+            xin[k][0] = x[1]; xin[k][1] = x[3];
+            ytop[k][0] = x[2]; ytop[k][1] = x[3];
+            ph[0] += cw[k] * x[0]; ph[1] += cw[k] * x[1];
+            ph[2] += cw[k] * x[2]; ph[3] += cw[k] * x[3];
+          }
+        }
+        if (phi) {
+          double2* pp = reinterpret_cast<double2*>(phi);
+          pp[sk_vec_off(T, s, t, 0, lane) >> 1] = make_double2(ph[0], ph[1]);
+          pp[sk_vec_off(T, s, t, 1, lane) >> 1] = make_double2(ph[2], ph[3]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        const double y0 = __shfl_up_sync(kFull, ytop[k][0], 1);
+        const double y1 = __shfl_up_sync(kFull, ytop[k][1], 1);
+        if (lane > 0) { yin[k][0] = y0; yin[k][1] = y1; }
+      }
+      if (lane == 31 && act && hout) {
+        double2* ho = reinterpret_cast<double2*>(hout) + (int64_t)ip * DW;
+#pragma unroll
+        for (int k = 0; k < DW; ++k) ho[k] = make_double2(ytop[k][0], ytop[k][1]);
+        if ((ip & 7) == 7 || ip == nx - 1) st_release_gpu(pout, ip + 1);
+      }
+    }
+  }
+}
+
+// rhs_sk[d] = source_vector(q) + inv_cdt M psi_time[:, d] + extra[:, d]
+__global__ void rhs_build_kernel(int nx, int ny, int D, const int* __restrict__ quad,
+                                 const double* __restrict__ q, double inv_cdt,
+                                 const double* __restrict__ pt, int ldp,
+                                 const double* __restrict__ ex, int lde, double* __restrict__ out,
+                                 int64_t vlen, dlrsn_cellops ops) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = (int64_t)nx * ny * D;
+  if (idx >= n) return;
+  const int c = (int)(idx / D);
+  const int d = (int)(idx - (int64_t)c * D);
+  const double qc = q[c];
+  double v[4];
+#pragma unroll
+  for (int l = 0; l < 4; ++l) v[l] = qc * ops.src_row[l];
+  if (pt) {
+    double u[4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) u[l] = pt[(int64_t)(4 * c + l) * ldp + d];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const double mu = ops.mass[4 * l] * u[0] + ops.mass[4 * l + 1] * u[1] +
+                        ops.mass[4 * l + 2] * u[2] + ops.mass[4 * l + 3] * u[3];
+      v[l] += inv_cdt * mu;
+    }
+  }
+  if (ex) {
+#pragma unroll
+    for (int l = 0; l < 4; ++l) v[l] += ex[(int64_t)(4 * c + l) * lde + d];
+  }
+  const int qd = quad[d];
+  const int f = sk_flip(qd);
+  int s, t, lane;
+  sk_locate(c % nx, c / nx, qd, nx, ny, s, t, lane);
+  const int T = nx + 31;
+  double2* o = reinterpret_cast<double2*>(out + (int64_t)d * vlen);
+  o[sk_vec_off(T, s, t, 0, lane) >> 1] = make_double2(v[0 ^ f], v[1 ^ f]);
+  o[sk_vec_off(T, s, t, 1, lane) >> 1] = make_double2(v[2 ^ f], v[3 ^ f]);
+}
+
+__global__ void cells_to_sk4_kernel(int nx, int ny, const double* __restrict__ v,
+                                    double* __restrict__ out, int64_t slen) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nx * ny) return;
+  const double x = v[c];
+  const int T = nx + 31;
+#pragma unroll
+  for (int qd = 0; qd < 4; ++qd) {
+    int s, t, lane;
+    sk_locate(c % nx, c / nx, qd, nx, ny, s, t, lane);
+    out[qd * slen + sk_sc_off(T, s, t, lane)] = x;
+  }
+}
+
+__device__ inline void write_scat4(const dlrsn_cellops& ops, int c, const double* phi_c,
+                                   double ss, double* scat, int64_t vlen) {
+  // transport_sn.py:436: M (sigma_s phi) / 4 pi
+  double u[4], w[4];
+#pragma unroll
+  for (int l = 0; l < 4; ++l) u[l] = ss * phi_c[l];
+#pragma unroll
+  for (int l = 0; l < 4; ++l)
+    w[l] = (ops.mass[4 * l] * u[0] + ops.mass[4 * l + 1] * u[1] + ops.mass[4 * l + 2] * u[2] +
+            ops.mass[4 * l + 3] * u[3]) / kFourPi;
+  const int nx = ops.nx, ny = ops.ny, T = nx + 31;
+#pragma unroll
+  for (int qd = 0; qd < 4; ++qd) {
+    int s, t, lane;
+    sk_locate(c % nx, c / nx, qd, nx, ny, s, t, lane);
+    const int f = sk_flip(qd);
+    double2* o = reinterpret_cast<double2*>(scat + qd * vlen);
+    o[sk_vec_off(T, s, t, 0, lane) >> 1] = make_double2(w[0 ^ f], w[1 ^ f]);
+    o[sk_vec_off(T, s, t, 1, lane) >> 1] = make_double2(w[2 ^ f], w[3 ^ f]);
+  }
+}
+
+__global__ void scatter_source_kernel(dlrsn_cellops ops, const double* __restrict__ phi,
+                                      const double* __restrict__ ss, double* __restrict__ scat,
+                                      int64_t vlen, int* any) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ops.nx * ops.ny) return;
+  const double s = ss[c];
+  if (s != 0.0 && any) atomicOr(any, 1);
+  double p[4];
+  const double2 a = reinterpret_cast<const double2*>(phi)[2 * c];
+  const double2 b = reinterpret_cast<const double2*>(phi)[2 * c + 1];
+  p[0] = a.x; p[1] = a.y; p[2] = b.x; p[3] = b.y;
+  write_scat4(ops, c, p, s, scat, vlen);
+}
+
+__global__ void phi_combine_kernel(dlrsn_cellops ops, int G, const dlrsn_group* __restrict__ groups,
+                                   const double* __restrict__ part, const double* __restrict__ phi_old,
+                                   const double* __restrict__ ss, double* __restrict__ phi_new,
+                                   double* __restrict__ scat, int64_t vlen, double* norms,
+                                   double* partials, unsigned* counter) {
+  __shared__ double red[64];
+  __shared__ bool last;
+  const int nx = ops.nx, ny = ops.ny, T = nx + 31;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  double v[2] = {0.0, 0.0};
+  if (c < nx * ny) {
+    double p[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int g = 0; g < G; ++g) {
+      const int qd = groups[g].quad;
+      int s, t, lane;
+      sk_locate(c % nx, c / nx, qd, nx, ny, s, t, lane);
+      const double* src = part + (int64_t)g * vlen;
+      const double2 a = *reinterpret_cast<const double2*>(src + sk_vec_off(T, s, t, 0, lane));
+      const double2 b = *reinterpret_cast<const double2*>(src + sk_vec_off(T, s, t, 1, lane));
+      const double o[4] = {a.x, a.y, b.x, b.y};
+      const int f = sk_flip(qd);
+#pragma unroll
+      for (int l = 0; l < 4; ++l) p[l] += o[l ^ f];
+    }
+    const double2 oa = reinterpret_cast<const double2*>(phi_old)[2 * c];
+    const double2 ob = reinterpret_cast<const double2*>(phi_old)[2 * c + 1];
+    const double po[4] = {oa.x, oa.y, ob.x, ob.y};
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const double dlt = p[l] - po[l];
+      v[0] += dlt * dlt;
+      v[1] += p[l] * p[l];
+    }
+    reinterpret_cast<double2*>(phi_new)[2 * c] = make_double2(p[0], p[1]);
+    reinterpret_cast<double2*>(phi_new)[2 * c + 1] = make_double2(p[2], p[3]);
+    if (scat) write_scat4(ops, c, p, ss[c], scat, vlen);
+  }
+  block_sum<2>(v, red);
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = v[0];
+    partials[2 * blockIdx.x + 1] = v[1];
+    __threadfence();
+    last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    // fixed-order reduction of the per-block partials (deterministic)
+    double w[2] = {0.0, 0.0};
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+      w[0] += __ldcg(partials + 2 * b);
+      w[1] += __ldcg(partials + 2 * b + 1);
+    }
+    block_sum<2>(w, red);
+    if (threadIdx.x == 0) {
+      norms[0] = w[0];
+      norms[1] = w[1];
+      *counter = 0u;
+    }
+  }
+}
+
+__global__ void sk_to_canonical_kernel(int nx, int ny, int D, const int* __restrict__ quad,
+                                       const double* __restrict__ sk, double* __restrict__ psi,
+                                       int ld, int64_t vlen) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)nx * ny * D) return;
+  const int c = (int)(idx / D);
+  const int d = (int)(idx - (int64_t)c * D);
+  const int qd = quad[d];
+  int s, t, lane;
+  sk_locate(c % nx, c / nx, qd, nx, ny, s, t, lane);
+  const int T = nx + 31;
+  const double* src = sk + (int64_t)d * vlen;
+  const double2 a = *reinterpret_cast<const double2*>(src + sk_vec_off(T, s, t, 0, lane));
+  const double2 b = *reinterpret_cast<const double2*>(src + sk_vec_off(T, s, t, 1, lane));
+  const double o[4] = {a.x, a.y, b.x, b.y};
+  const int f = sk_flip(qd);
+#pragma unroll
+  for (int l = 0; l < 4; ++l) psi[(int64_t)(4 * c + l) * ld + d] = o[l ^ f];
+}
+
+static int64_t handoff_offset_bytes(int nx, int ny, int G) {
+  const int64_t head = 256 + (int64_t)sk_strips(ny) * G * sizeof(int);
+  return (head + 255) / 256 * 256;
+}
+
+template <int DW>
+int launch_sweep(const SweepArgs& a, int max_ctas, cudaStream_t st) {
+  int dev = 0, sms = 0, occ = 0;
+  DLRSN_TRY_CUDA(cudaGetDevice(&dev));
+  DLRSN_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  DLRSN_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_kernel<DW>, 128, 0));
+  const int items = sk_strips(a.ny) * a.G;
+  int ctas = (items + 3) / 4;
+  const int cap = sms * (occ > 0 ? occ : 1);
+  if (ctas > cap) ctas = cap;
+  if (max_ctas > 0 && ctas > max_ctas) ctas = max_ctas;
+  if (ctas < 1) ctas = 1;
+  sweep_kernel<DW><<<ctas, 128, 0, st>>>(a);
+  DLRSN_CHECK_LAUNCH("sweep_kernel");
+  return DLRSN_OK;
+}
+
+}  // namespace dlrsn
+
+using namespace dlrsn;
+
+extern "C" {
+
+int64_t dlrsn_sweep_workspace_bytes(int nx, int ny, int n_groups, int dw) {
+  return handoff_offset_bytes(nx, ny, n_groups) +
+         (int64_t)sk_strips(ny) * n_groups * nx * dw * 2 * sizeof(double);
+}
+
+int dlrsn_rhs_build(const dlrsn_cellops* ops, int D, const int* quad, const double* q,
+                    double inv_cdt, const double* psi_time, int ld_psi_time, const double* extra,
+                    int ld_extra, double* rhs_sk, dlrsn_stream_t stream) {
+  DLRSN_REQUIRE(ops && D >= 0, "bad arguments to dlrsn_rhs_build");
+  const int64_t n = (int64_t)ops->nx * ops->ny * D;
+  if (n == 0) return DLRSN_OK;
+  rhs_build_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(
+      ops->nx, ops->ny, D, quad, q, inv_cdt, psi_time, ld_psi_time, extra, ld_extra, rhs_sk,
+      sk_vec_len(ops->nx, ops->ny), *ops);
+  DLRSN_CHECK_LAUNCH("rhs_build_kernel");
+  return DLRSN_OK;
+}
+
+int dlrsn_cells_to_sk4(const dlrsn_cellops* ops, const double* cell_values, double* out_sk4,
+                       dlrsn_stream_t stream) {
+  const int n = ops->nx * ops->ny;
+  cells_to_sk4_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(
+      ops->nx, ops->ny, cell_values, out_sk4, sk_scalar_len(ops->nx, ops->ny));
+  DLRSN_CHECK_LAUNCH("cells_to_sk4_kernel");
+  return DLRSN_OK;
+}
+
+int dlrsn_scatter_source(const dlrsn_cellops* ops, const double* phi, const double* sigma_s,
+                         double* scat_sk4, int* any_scatter, dlrsn_stream_t stream) {
+  const int n = ops->nx * ops->ny;
+  scatter_source_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(
+      *ops, phi, sigma_s, scat_sk4, sk_vec_len(ops->nx, ops->ny), any_scatter);
+  DLRSN_CHECK_LAUNCH("scatter_source_kernel");
+  return DLRSN_OK;
+}
+
+int dlrsn_phi_combine(const dlrsn_cellops* ops, int G, const dlrsn_group* groups,
+                      const double* phi_part_sk, const double* phi_old, const double* sigma_s,
+                      double* phi_new, double* scat_sk4, double* norms, void* partial_ws,
+                      dlrsn_stream_t stream) {
+  const int n = ops->nx * ops->ny;
+  const int nb = (n + 255) / 256;
+  unsigned* counter = reinterpret_cast<unsigned*>(partial_ws);
+  double* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(partial_ws) + 256);
+  phi_combine_kernel<<<nb, 256, 0, as_stream(stream)>>>(*ops, G, groups, phi_part_sk, phi_old,
+                                                        sigma_s, phi_new, scat_sk4,
+                                                        sk_vec_len(ops->nx, ops->ny), norms,
+                                                        partials, counter);
+  DLRSN_CHECK_LAUNCH("phi_combine_kernel");
+  return DLRSN_OK;
+}
+
+int dlrsn_sk_to_canonical(const dlrsn_cellops* ops, int D, const int* quad, const double* psi_sk,
+                          double* psi, int ld, dlrsn_stream_t stream) {
+  const int64_t n = (int64_t)ops->nx * ops->ny * D;
+  if (n == 0) return DLRSN_OK;
+  sk_to_canonical_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(
+      ops->nx, ops->ny, D, quad, psi_sk, psi, ld, sk_vec_len(ops->nx, ops->ny));
+  DLRSN_CHECK_LAUNCH("sk_to_canonical_kernel");
+  return DLRSN_OK;
+}
+
+int dlrsn_sweep(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int dw,
+                const double* sigma_t_sk4, const double* scat_sk4, const double* rhs_sk,
+                double* psi_sk, double* phi_part_sk, void* workspace, int64_t workspace_bytes,
+                int max_ctas, dlrsn_stream_t stream) {
+  DLRSN_REQUIRE(ops && groups && sigma_t_sk4 && rhs_sk && psi_sk && workspace,
+                "null argument to dlrsn_sweep");
+  DLRSN_REQUIRE(dw == 1 || dw == 2 || dw == 4 || dw == 8, "sweep width must be 1, 2, 4 or 8");
+  const int64_t need = dlrsn_sweep_workspace_bytes(ops->nx, ops->ny, G, dw);
+  DLRSN_REQUIRE(workspace_bytes >= need, "sweep workspace too small (%lld < %lld)",
+                (long long)workspace_bytes, (long long)need);
+  if (G == 0) return DLRSN_OK;
+  cudaStream_t st = as_stream(stream);
+  const int64_t head = handoff_offset_bytes(ops->nx, ops->ny, G);
+  DLRSN_TRY_CUDA(cudaMemsetAsync(workspace, 0, head, st));
+  SweepArgs a;
+  a.nx = ops->nx; a.ny = ops->ny; a.G = G;
+  a.groups = groups;
+  a.sigma_sk4 = sigma_t_sk4;
+  a.scat_sk4 = scat_sk4;
+  a.rhs_sk = rhs_sk;
+  a.psi_sk = psi_sk;
+  a.phi_sk = phi_part_sk;
+  a.ticket = reinterpret_cast<int*>(workspace);
+  a.progress = reinterpret_cast<int*>(reinterpret_cast<char*>(workspace) + 256);
+  a.handoff = reinterpret_cast<double*>(reinterpret_cast<char*>(workspace) + head);
+  for (int m = 0; m < 16; ++m) {
+    a.mass[m] = ops->mass[m];
+    a.gxp[m] = ops->gx[m];
+    a.gyp[m] = ops->gy[m];
+  }
+  // outflow edge masses: right edge dofs (1,3), top edge dofs (2,3)
+  const int ix[2] = {1, 3}, iy[2] = {2, 3};
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 2; ++c) {
+      a.gxp[4 * ix[r] + ix[c]] += ops->e2x[2 * r + c];
+      a.gyp[4 * iy[r] + iy[c]] += ops->e2y[2 * r + c];
+    }
+  for (int m = 0; m < 4; ++m) {
+    a.ex[m] = ops->e2x[m];
+    a.ey[m] = ops->e2y[m];
+  }
+  a.vlen = sk_vec_len(ops->nx, ops->ny);
+  a.slen = sk_scalar_len(ops->nx, ops->ny);
+  switch (dw) {
+    case 1: return launch_sweep<1>(a, max_ctas, st);
+    case 2: return launch_sweep<2>(a, max_ctas, st);
+    case 4: return launch_sweep<4>(a, max_ctas, st);
+    default: return launch_sweep<8>(a, max_ctas, st);
+  }
+}
+
+}  // extern "C"

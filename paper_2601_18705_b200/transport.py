@@ -1,0 +1,310 @@
+"""Discrete-ordinates sweeps and source iteration on the B200
+(mirror of transport_sn.py:38-450).
+
+The reference assembles sparse N_x x N_x operators every step and sweeps
+with cached per-cell inverses; here the structured stencil is implicit: the
+per-step state is sigma_t / sigma_s / q per cell plus the constant reference
+blocks, and one persistent CUDA launch sweeps every direction
+(csrc/sweep.cu).  The public functions keep the reference names, arguments,
+return types and exceptions.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import as_device, device, empty, stream, zeros
+from .errors import ConfigurationError, ContractViolation, IterationLimitError
+from .mesh import DISCONTINUOUS, cellops_struct
+
+FOUR_PI = 4.0 * np.pi
+_WARPS_PER_SM_TARGET = 8
+
+
+def quadrant_code(omega):
+    """(sx<0) | 2*(sy<0); grazing components sweep as positive
+    (transport_sn.py:38-42)."""
+    return (0 if omega[0] >= 0.0 else 1) | (0 if omega[1] >= 0.0 else 2)
+
+
+def plan_groups(omegas, closure, n_strips, dw=None, sm_count=148):
+    """Partition the swept directions into warp groups (host logic).
+
+    Directions of one quadrant share the traversal order, so a group holds
+    up to ``dw`` directions of a single quadrant; the width is the largest
+    power of two that still yields enough warps (groups x strips) to fill the
+    GPU, else 1.  Returns (groups structured array, dw, quad codes per slot).
+    """
+    om = np.asarray(omegas, dtype=float)
+    clo = np.asarray(closure, dtype=float)
+    D = om.shape[0]
+    quads = np.array([quadrant_code(om[d]) for d in range(D)], dtype=np.int32)
+    members = [np.flatnonzero(quads == q) for q in range(4)]
+    if dw is None:
+        target = _WARPS_PER_SM_TARGET * sm_count
+        dw = 1
+        for cand in (8, 4, 2):
+            g = sum(math.ceil(len(m) / cand) for m in members)
+            if g * n_strips >= target:
+                dw = cand
+                break
+    biggest = max((len(m) for m in members), default=1)
+    while dw > 1 and dw // 2 >= biggest:
+        dw //= 2
+    if dw not in (1, 2, 4, 8):
+        raise ContractViolation(f"sweep group width must be 1, 2, 4 or 8, got {dw}")
+    rows = []
+    for q in range(4):
+        m = members[q]
+        for k in range(0, len(m), dw):
+            rows.append((q, m[k:k + dw]))
+    groups = np.zeros(len(rows), dtype=_lib.GROUP_DTYPE)
+    for gi, (q, slots) in enumerate(rows):
+        groups[gi]["quad"] = q
+        groups[gi]["ndir"] = len(slots)
+        groups[gi]["slot"][:len(slots)] = slots
+        groups[gi]["ox"][:len(slots)] = np.abs(om[slots, 0])
+        groups[gi]["oy"][:len(slots)] = np.abs(om[slots, 1])
+        groups[gi]["cw"][:len(slots)] = clo[slots]
+    return groups, dw, quads
+
+
+def _groups_to_device(groups):
+    raw = np.frombuffer(groups.tobytes(), dtype=np.uint8)
+    return torch.from_numpy(raw.copy()).to(device())
+
+
+@dataclass(eq=False)
+class DiscreteOperators:
+    """Per-step operator data for the sweeps (transport_sn.py:78-97).
+
+    Holds the grid, the linearised step (device tensors) and the scaled
+    reference blocks; the sparse matrices of the reference are implicit.
+    """
+
+    grid: object
+    step: object
+    cellops: object
+    dsa_penalty: str = "simplified"
+    penalty_closure: tuple | None = None
+    _sigma_sk4: torch.Tensor | None = None
+    _scratch: dict = field(default_factory=dict)
+
+    @property
+    def n_cells(self):
+        return self.grid.n_cells
+
+    @property
+    def vec_len(self):
+        return int(_lib.load().dlrsn_sk_vec_len(self.grid.nx, self.grid.ny))
+
+    @property
+    def scalar_len(self):
+        return int(_lib.load().dlrsn_sk_scalar_len(self.grid.nx, self.grid.ny))
+
+    @property
+    def cellops_ptr(self):
+        import ctypes
+
+        return ctypes.c_void_p(ctypes.addressof(self.cellops))
+
+    def sigma_t_sk4(self):
+        if self._sigma_sk4 is None:
+            out = empty(4 * self.scalar_len)
+            _lib.call("dlrsn_cells_to_sk4", self.cellops_ptr, _lib.ptr(self.step.sigma_t),
+                      _lib.ptr(out), stream())
+            self._sigma_sk4 = out
+        return self._sigma_sk4
+
+    def buffer(self, name, numel, dtype=torch.float64, zero=False):
+        """Reusable device scratch (grows on demand)."""
+        t = self._scratch.get(name)
+        if t is None or t.numel() < numel or t.dtype != dtype:
+            t = (torch.zeros if zero else torch.empty)(max(numel, 1), dtype=dtype, device=device())
+            self._scratch[name] = t
+        return t
+
+    def mass_apply(self, u, coeff=None):
+        """Block-diagonal mass times a dof vector / (n_dofs, k) block
+        (transport_sn.py:107-116)."""
+        m = torch.from_numpy(np.frombuffer(bytes(self.cellops.mass), dtype=np.float64)
+                             .reshape(4, 4).copy()).to(device())
+        u = as_device(u)
+        flat = u.ndim == 1
+        uc = u.reshape(self.n_cells, 4, -1)
+        out = torch.einsum("ij,cjk->cik", m, uc)
+        if coeff is not None:
+            out = out * as_device(coeff)[:, None, None]
+        out = out.reshape(self.grid.n_dofs, -1)
+        return out[:, 0] if flat else out
+
+    def source_vector(self, cell_values):
+        row = torch.tensor(list(self.cellops.src_row), dtype=torch.float64, device=device())
+        return (as_device(cell_values)[:, None] * row[None, :]).reshape(-1)
+
+
+def assemble_operators(grid, step, dsa_penalty="simplified", penalty_closure=None):
+    """Per-step operator data (transport_sn.py:201-300); same checks."""
+    if grid.flavor != DISCONTINUOUS:
+        raise ContractViolation("sweep transport needs the discontinuous dof layout")
+    for name in ("sigma_t", "sigma_s", "q"):
+        if tuple(getattr(step, name).shape) != (grid.n_cells,):
+            raise ContractViolation(f"step field {name} must be per-cell")
+    if bool((step.sigma_t - step.sigma_s <= 0).any()):
+        raise ContractViolation("pseudo absorption sigma_t - sigma_s must stay positive")
+    if dsa_penalty not in ("simplified", "collocation"):
+        raise ContractViolation(f"unknown dsa penalty variant {dsa_penalty!r}")
+    return DiscreteOperators(grid=grid, step=step, cellops=cellops_struct(grid),
+                             dsa_penalty=dsa_penalty, penalty_closure=penalty_closure)
+
+
+@dataclass(eq=False)
+class SourceIterationResult:
+    psi: torch.Tensor  # (n_dofs, n_angles), canonical layout, on the device
+    phi: torch.Tensor  # converged scattering scalar flux
+    iterations: int
+
+
+class _SweepPlan:
+    """Device-side tables and buffers of one set of swept directions."""
+
+    def __init__(self, ops, omegas, closure, dw=None):
+        g = ops.grid
+        sms = ctypes_int()
+        _lib.call("dlrsn_device_sm_count", sms.ptr)
+        ns = (g.ny + 31) // 32
+        self.groups, self.dw, quads = plan_groups(omegas, closure, ns, dw=dw, sm_count=sms.value)
+        self.G = len(self.groups)
+        self.D = len(quads)
+        self.groups_dev = _groups_to_device(self.groups)
+        self.quads_dev = torch.from_numpy(quads).to(device())
+        self.ws_bytes = int(_lib.load().dlrsn_sweep_workspace_bytes(g.nx, g.ny, self.G, self.dw))
+        self.workspace = ops.buffer("sweep_ws", self.ws_bytes, dtype=torch.uint8)
+
+
+class ctypes_int:
+    def __init__(self):
+        import ctypes
+
+        self._v = ctypes.c_int(0)
+        self.ptr = ctypes.byref(self._v)
+
+    @property
+    def value(self):
+        return self._v.value
+
+
+def _sweep(ops, plan, rhs_sk, psi_sk, scat_sk4=None, phi_part=None, max_ctas=0):
+    _lib.call("dlrsn_sweep", ops.cellops_ptr, plan.G, _lib.ptr(plan.groups_dev), plan.dw,
+              _lib.ptr(ops.sigma_t_sk4()), _lib.ptr(scat_sk4), _lib.ptr(rhs_sk), _lib.ptr(psi_sk),
+              _lib.ptr(phi_part), _lib.ptr(plan.workspace), plan.ws_bytes, int(max_ctas), stream())
+
+
+def _to_canonical(ops, plan, psi_sk, out=None):
+    g = ops.grid
+    psi = out if out is not None else empty(g.n_dofs, plan.D)
+    _lib.call("dlrsn_sk_to_canonical", ops.cellops_ptr, plan.D, _lib.ptr(plan.quads_dev),
+              _lib.ptr(psi_sk), _lib.ptr(psi), plan.D, stream())
+    return psi
+
+
+def sweep_solve(ops, omega, rhs, _key=None):
+    """One direction's upwind solve by a single sweep (transport_sn.py:303-322)."""
+    g = ops.grid
+    omega = np.asarray(omega, dtype=float)
+    rhs = as_device(rhs).reshape(g.n_dofs, 1).contiguous()
+    plan = _SweepPlan(ops, omega[None, :], np.ones(1), dw=1)
+    vl = ops.vec_len
+    rhs_sk = empty(vl)
+    psi_sk = empty(vl)
+    zero_q = ops.buffer("zero_q", g.n_cells, zero=True)
+    _lib.call("dlrsn_rhs_build", ops.cellops_ptr, 1, _lib.ptr(plan.quads_dev), _lib.ptr(zero_q),
+              0.0, None, 1, _lib.ptr(rhs), 1, _lib.ptr(rhs_sk), stream())
+    _sweep(ops, plan, rhs_sk, psi_sk)
+    return _to_canonical(ops, plan, psi_sk)[:, 0].contiguous()
+
+
+def source_iteration(ops, omegas, closure, psi_time=None, *, use_dsa=True, tol=1e-8,
+                     max_iters=200, phi_start=None, extra_source=None, threads=0, dw=None,
+                     keep_sk=False):
+    """Lagged-scattering iteration over device sweeps (transport_sn.py:377-450).
+
+    ``threads`` is accepted for API compatibility and ignored (the sweeps of
+    all directions run in one launch).  ``psi_time`` / ``extra_source`` are
+    (n_dofs, n_angles) arrays; results are device tensors.
+    """
+    omegas = np.asarray(omegas.cpu() if isinstance(omegas, torch.Tensor) else omegas, dtype=float)
+    closure = np.asarray(closure.cpu() if isinstance(closure, torch.Tensor) else closure, dtype=float)
+    nd = omegas.shape[0]
+    if closure.shape != (nd,):
+        raise ContractViolation("closure vector must have one entry per swept angle")
+    if use_dsa:
+        raise ConfigurationError(
+            "use_dsa=True is not available on the B200 path yet; pass use_dsa=False "
+            "(SURVEY 4.3: DSA diverges for random angular bases)")
+    g = ops.grid
+    st = ops.step
+    plan = _SweepPlan(ops, omegas, closure, dw=dw)
+    vl = ops.vec_len
+    rhs_sk = ops.buffer("rhs_sk", nd * vl)
+    psi_sk = ops.buffer("psi_sk", nd * vl)
+    part = ops.buffer("phi_part", plan.G * vl)
+    scat = ops.buffer("scat_sk4", 4 * vl)
+    pt = None if psi_time is None else as_device(psi_time).reshape(g.n_dofs, nd).contiguous()
+    ex = None if extra_source is None else as_device(extra_source).reshape(g.n_dofs, nd).contiguous()
+    _lib.call("dlrsn_rhs_build", ops.cellops_ptr, nd, _lib.ptr(plan.quads_dev), _lib.ptr(st.q),
+              float(st.inv_cdt), _lib.ptr(pt), nd, _lib.ptr(ex), nd, _lib.ptr(rhs_sk), stream())
+    phi = zeros(g.n_dofs) if phi_start is None else as_device(phi_start).reshape(-1).clone()
+    phi_new = empty(g.n_dofs)
+    flags = zeros(1, dtype=torch.int32)
+    _lib.call("dlrsn_scatter_source", ops.cellops_ptr, _lib.ptr(phi), _lib.ptr(st.sigma_s),
+              _lib.ptr(scat), _lib.ptr(flags), stream())
+    nb = (g.n_cells + 255) // 256
+    red_ws = ops.buffer("red_ws", 256 // 8 + 2 * nb + 8, zero=True)
+    norms = zeros(2)
+    host = torch.empty(3, dtype=torch.float64, pin_memory=True)
+    change = math.inf
+    for it in range(1, max_iters + 1):
+        _sweep(ops, plan, rhs_sk, psi_sk, scat, part)
+        _lib.call("dlrsn_phi_combine", ops.cellops_ptr, plan.G, _lib.ptr(plan.groups_dev),
+                  _lib.ptr(part), _lib.ptr(phi), _lib.ptr(st.sigma_s), _lib.ptr(phi_new),
+                  _lib.ptr(scat), _lib.ptr(norms), _lib.ptr(red_ws), stream())
+        host[:2].copy_(norms, non_blocking=True)
+        if it == 1:
+            host[2:3].copy_(flags.to(torch.float64), non_blocking=True)
+        torch.cuda.current_stream(device()).synchronize()
+        phi, phi_new = phi_new, phi
+        if it == 1 and host[2].item() == 0.0:  # pure absorber (transport_sn.py:410,430-432)
+            return _finish(ops, plan, psi_sk, phi, 1, keep_sk)
+        d2, n2 = host[0].item(), host[1].item()
+        change = math.sqrt(d2) / max(math.sqrt(n2), 1e-300)
+        if change <= tol:
+            return _finish(ops, plan, psi_sk, phi, it, keep_sk)
+    raise IterationLimitError("source iteration did not converge", max_iters, change)
+
+
+def _finish(ops, plan, psi_sk, phi, it, keep_sk):
+    psi = _to_canonical(ops, plan, psi_sk)
+    res = SourceIterationResult(psi=psi, phi=phi, iterations=it)
+    if keep_sk:
+        res.psi_sk = psi_sk
+        res.plan = plan
+    return res
+
+
+def boundary_outflow(grid, psi, omegas, weights, ref_edge=None):
+    """Quadrature outflow through the boundary (transport_sn.py:479-492)."""
+    psi = as_device(psi)
+    cells, walls, normals, lengths = grid.boundary_faces
+    e0 = np.array([{"left": 0, "right": 1, "bottom": 0, "top": 2}[w] for w in walls])
+    e1 = np.array([{"left": 2, "right": 3, "bottom": 1, "top": 3}[w] for w in walls])
+    i0 = torch.from_numpy(4 * cells + e0).to(device())
+    i1 = torch.from_numpy(4 * cells + e1).to(device())
+    vals = 0.5 * (psi[i0] + psi[i1]) * as_device(lengths)[:, None]
+    on = as_device(normals) @ as_device(np.asarray(omegas)[:, :2]).T
+    return float((torch.clamp(on, min=0.0) * vals @ as_device(weights)).sum())
