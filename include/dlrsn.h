@@ -8,8 +8,8 @@
  * (paths relative to /root/reference/pkg/src/greytrt).
  *
  * Conventions
- *  - All pointers are caller-owned DEVICE pointers unless the comment says
- *    "host".  fp64 throughout ("f64"); ints are int32 unless noted.
+ *  - All pointers are caller-owned DEVICE pointers, except `ops`
+ *    (const dlrsn_cellops*), which points to HOST memory.  fp64 throughout ("f64"); ints are int32 unless noted.
  *  - `stream` is a cudaStream_t passed as void*.  No entry point allocates
  *    device memory or synchronises the host; workspaces are caller-owned.
  *  - Return: 0 = DLRSN_OK, negative = error (see codes).  The Python shim
@@ -80,8 +80,12 @@ int dlrsn_device_sm_count(int* out);
 
 int64_t dlrsn_sk_vec_len(int nx, int ny);
 int64_t dlrsn_sk_scalar_len(int nx, int ny);
-/* bytes of workspace dlrsn_sweep needs for G groups of width dw */
+/* bytes of workspace dlrsn_sweep needs for G groups of width dw; a new
+ * workspace must be initialised once with dlrsn_sweep_workspace_init (the
+ * sweep leaves it re-armed, so it can be reused across launches and plans).
+ * Word 1 of the workspace is a sticky status (2 = a handoff wait timed out). */
 int64_t dlrsn_sweep_workspace_bytes(int nx, int ny, int n_groups, int dw);
+int dlrsn_sweep_workspace_init(void* workspace, int64_t workspace_bytes, dlrsn_stream_t stream);
 
 /* ---- K4: per-cell physics (physics.py:63-132, driver.py:344-346,532-534) */
 
@@ -147,9 +151,9 @@ int dlrsn_sk_to_canonical(const dlrsn_cellops* ops, int D, const int* quad,
 /* ---- K1: the sweep (transport_sn.py:142-163,303-322 batched over
  * directions, sweep_all :419-427, phi_half :438).
  * One persistent launch sweeps every direction of every group: warp =
- * (group, 32-row strip), lanes = rows, marching the oriented x axis; the
- * strip above is fed through an L2 handoff with release/acquire progress
- * counters.  rhs_sk / psi_sk: D slabs; sigma_t_sk4 / scat_sk4: quadrant
+ * (group, 32-row strip), lanes = rows, marching the oriented x axis; inputs
+ * are staged to shared memory by TMA bulk copies; the strip above is fed
+ * through an L2 handoff of self-flagging slots.  rhs_sk / psi_sk: D slabs; sigma_t_sk4 / scat_sk4: quadrant
  * slabs (scat nullable => no scattering term); phi_part_sk: G slabs
  * (nullable).  dw = template width >= max group ndir (1,2,4,8). */
 int dlrsn_sweep(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int dw,

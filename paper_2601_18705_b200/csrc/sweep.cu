@@ -9,10 +9,10 @@
 //     __shfl_up_sync from the lane below one step earlier;
 //   * data are stored in the sweep-native SK layout, so each warp-wide access
 //     is one contiguous 512 B (double2 per lane) transaction;
-//   * the strip above is fed through an L2 "handoff" column with
-//     release/acquire progress counters; warps take work tickets in strip-major
-//     order, so every wait targets a smaller, already-running ticket
-//     (deadlock-free without co-residency assumptions);
+//   * the strip above is fed through an L2 "handoff" column of self-flagging
+//     slots (sNaN = empty); warps take work tickets in strip-major order, so
+//     every wait targets a smaller, already-running ticket (deadlock-free
+//     without co-residency assumptions);
 //   * the 4x4 local operator A = sigma_t M + |wx| Gx' + |wy| Gy' is formed and
 //     solved in registers per cell-angle (no stored inverses: the reference's
 //     128 B/cell-angle cache is not materialised);
@@ -33,8 +33,8 @@ struct SweepArgs {
   double* psi_sk;
   double* phi_sk;
   int* ticket;
-  int* progress;
   double* handoff;
+  int* status;
   double mass[16];
   double gxp[16];  // Gx + e2x embedded at the right edge (oriented +x outflow)
   double gyp[16];  // Gy + e2y embedded at the top edge
@@ -43,41 +43,100 @@ struct SweepArgs {
   int64_t vlen, slen;
 };
 
+// Empty handoff slot: a signalling NaN with a fixed payload.  Arithmetic only
+// produces quiet NaNs, so a swept value can never alias it.
+constexpr unsigned long long kEmpty = 0x7FF4DEADBEEFCAFEull;
+__device__ __forceinline__ bool is_empty(double v) {
+  return (unsigned long long)__double_as_longlong(v) == kEmpty;
+}
+
+// 1/x without the IEEE slow path: hardware approximation + two Newton steps
+// (relative error ~1 ulp; A's pivots are positive and normal).
+__device__ __forceinline__ double rcp64(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 __device__ __forceinline__ void solve4(double* a, double* b, double* x) {
   // Gaussian elimination without pivoting: A has a positive-definite
   // symmetric part (sigma_t M + upwind outflow terms), so the pivots are
   // positive.  The reference inverts with LAPACK (transport_sn.py:158); the
   // two differ only at round-off.
-  const double p0 = 1.0 / a[0];
+  const double p0 = rcp64(a[0]);
   double l = a[4] * p0;
   a[5] -= l * a[1]; a[6] -= l * a[2]; a[7] -= l * a[3]; b[1] -= l * b[0];
   l = a[8] * p0;
   a[9] -= l * a[1]; a[10] -= l * a[2]; a[11] -= l * a[3]; b[2] -= l * b[0];
   l = a[12] * p0;
   a[13] -= l * a[1]; a[14] -= l * a[2]; a[15] -= l * a[3]; b[3] -= l * b[0];
-  const double p1 = 1.0 / a[5];
+  const double p1 = rcp64(a[5]);
   l = a[9] * p1;
   a[10] -= l * a[6]; a[11] -= l * a[7]; b[2] -= l * b[1];
   l = a[13] * p1;
   a[14] -= l * a[6]; a[15] -= l * a[7]; b[3] -= l * b[1];
-  const double p2 = 1.0 / a[10];
+  const double p2 = rcp64(a[10]);
   l = a[14] * p2;
   a[15] -= l * a[11]; b[3] -= l * b[2];
-  x[3] = b[3] / a[15];
+  x[3] = b[3] * rcp64(a[15]);
   x[2] = (b[2] - a[11] * x[3]) * p2;
   x[1] = (b[1] - a[6] * x[2] - a[7] * x[3]) * p1;
   x[0] = (b[0] - a[1] * x[1] - a[2] * x[2] - a[3] * x[3]) * p0;
 }
 
+// Steps per TMA chunk, pipeline depth and warps per CTA for a group width.
+template <int DW> struct SweepCfg;
+template <> struct SweepCfg<1> { static constexpr int C = 4, P = 3, WPC = 4; };
+template <> struct SweepCfg<2> { static constexpr int C = 2, P = 3, WPC = 4; };
+template <> struct SweepCfg<4> { static constexpr int C = 2, P = 3, WPC = 2; };
+template <> struct SweepCfg<8> { static constexpr int C = 1, P = 3, WPC = 2; };
+
 template <int DW>
-__global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
-  __shared__ double s_S[4][DW][16];
+__host__ __device__ constexpr int stage_doubles() {
+  return SweepCfg<DW>::C * (32 + 128 + 128 * DW);  // sigma | scat | rhs[DW]
+}
+template <int DW>
+__host__ __device__ constexpr size_t sweep_smem_bytes() {
+  return (size_t)SweepCfg<DW>::WPC * SweepCfg<DW>::P * stage_doubles<DW>() * sizeof(double);
+}
+
+// One persistent launch; see the file header.  Per warp, a P-deep ring of
+// shared-memory stages is filled by TMA bulk copies (one elected lane, one
+// mbarrier per stage): each stage holds C consecutive skewed steps of sigma_t,
+// the scattering source and the DW direction rhs, all contiguous in the SK
+// layout.  The y-inflow of lane 0 comes from the strip below through an L2
+// handoff column whose slots start "empty" (sNaN sentinel): the producer
+// stores, the consumer spins on the slot itself (no fences, no counters) and
+// re-arms it after reading, so the buffer is clean for the next launch.
+template <int DW>
+__global__ void __launch_bounds__(SweepCfg<DW>::WPC * 32)
+sweep_kernel(const SweepArgs a) {
+  constexpr int C = SweepCfg<DW>::C, P = SweepCfg<DW>::P, WPC = SweepCfg<DW>::WPC;
+  constexpr int SD = stage_doubles<DW>();
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t bars[WPC][P];
+  __shared__ double s_S[WPC][DW][16];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
+  double* ring = smem + (size_t)wib * P * SD;
   const int nx = a.nx, ny = a.ny, G = a.G;
   const int T = nx + 31;
   const int ns = (ny + 31) >> 5;
   const int items = ns * G;
+  const int nchunks = (T + C - 1) / C;
+  const int hchunks = (nx + C - 1) / C;
+  const double empty = __longlong_as_double((long long)kEmpty);
+
+  if (lane == 0) {
+#pragma unroll
+    for (int st = 0; st < P; ++st) mbar_init(&bars[wib][st], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  uint32_t parity = 0;  // bit st: parity of the next completion of stage st
 
   for (;;) {
     int item = 0;
@@ -86,117 +145,183 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
     if (item >= items) break;
     const int s = item / G;
     const int g = item - s * G;
-    const dlrsn_group& grp = a.groups[g];
-    const int quad = grp.quad;
-    const int nd = grp.ndir;
+    const dlrsn_group* grp = a.groups + g;
+    const int quad = grp->quad;
+    const int nd = grp->ndir;
 
     __syncwarp();
     for (int e = lane; e < DW * 16; e += 32) {
       const int k = e >> 4, m = e & 15;
-      s_S[wib][k][m] = k < nd ? grp.ox[k] * a.gxp[m] + grp.oy[k] * a.gyp[m] : 0.0;
+      s_S[wib][k][m] = k < nd ? grp->ox[k] * a.gxp[m] + grp->oy[k] * a.gyp[m] : 0.0;
     }
-    __syncwarp();
-
+    const int64_t strip_vec = (int64_t)s * T * 128;  // SK offset of (s, t=0)
     double ox[DW], oy[DW], cw[DW];
-    const double* rhs_base[DW];
-    double* psi_base[DW];
+    int64_t slot_off[DW];
 #pragma unroll
     for (int k = 0; k < DW; ++k) {
       const bool on = k < nd;
-      ox[k] = on ? grp.ox[k] : 0.0;
-      oy[k] = on ? grp.oy[k] : 0.0;
-      cw[k] = on ? grp.cw[k] : 0.0;
-      const int slot = on ? grp.slot[k] : 0;
-      rhs_base[k] = a.rhs_sk + (int64_t)slot * a.vlen;
-      psi_base[k] = a.psi_sk + (int64_t)slot * a.vlen;
+      ox[k] = on ? grp->ox[k] : 0.0;
+      oy[k] = on ? grp->oy[k] : 0.0;
+      cw[k] = on ? grp->cw[k] : 0.0;
+      slot_off[k] = (on ? (int64_t)grp->slot[k] : 0) * a.vlen + strip_vec;
     }
-    const double* sig = a.sigma_sk4 + (int64_t)quad * a.slen;
-    const double* scat = a.scat_sk4 ? a.scat_sk4 + (int64_t)quad * a.vlen : nullptr;
-    double* phi = a.phi_sk ? a.phi_sk + (int64_t)g * a.vlen : nullptr;
+    const double* sig = a.sigma_sk4 + (int64_t)quad * a.slen + (int64_t)s * T * 32;
+    const double* scat = a.scat_sk4 ? a.scat_sk4 + (int64_t)quad * a.vlen + strip_vec : nullptr;
+    double* phi_p = a.phi_sk ? a.phi_sk + (int64_t)g * a.vlen + strip_vec + 2 * lane : nullptr;
+    __syncwarp();
 
-    const int jp = (s << 5) + lane;
-    const bool row_ok = jp < ny;
-    const double* hin = s > 0 ? a.handoff + ((int64_t)(s - 1) * G + g) * nx * DW * 2 : nullptr;
-    double* hout = (s + 1 < ns) ? a.handoff + ((int64_t)s * G + g) * nx * DW * 2 : nullptr;
-    const int* pin = s > 0 ? a.progress + (s - 1) * G + g : nullptr;
-    int* pout = a.progress + s * G + g;
-    int avail = 0;
+    // TMA producer (lane 0 only): chunk m -> stage m % P.  Prologue: P-1 chunks.
+    if (lane == 0) {
+      for (int m = 0; m < P - 1 && m < nchunks; ++m) {
+        const int st = m % P, t0 = m * C;
+        const uint32_t n = (uint32_t)min(C, T - t0);
+        double* buf = ring + st * SD;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bars[wib][st], n * (256u + (scat ? 1024u : 0u) + 1024u * (uint32_t)nd));
+        tma_load_1d(buf, sig + t0 * 32, n * 256u, &bars[wib][st]);
+        if (scat) tma_load_1d(buf + C * 32, scat + t0 * 128, n * 1024u, &bars[wib][st]);
+#pragma unroll
+        for (int k = 0; k < DW; ++k)
+          if (k < nd)
+            tma_load_1d(buf + C * 160 + k * C * 128, a.rhs_sk + slot_off[k] + t0 * 128, n * 1024u,
+                        &bars[wib][st]);
+      }
+    }
+
+    const bool row_ok = (s << 5) + lane < ny;
+    double2* hin = s > 0 ? reinterpret_cast<double2*>(a.handoff) + ((int64_t)(s - 1) * G + g) * nx * DW
+                         : nullptr;
+    double2* hout = (s + 1 < ns) ? reinterpret_cast<double2*>(a.handoff) + ((int64_t)s * G + g) * nx * DW
+                                 : nullptr;
+    // chunk h of the handoff: lane L < C*DW owns (column hC + L/DW, direction L%DW)
+    const bool hlane = hin != nullptr && lane < C * DW;
+    double2 h0 = make_double2(0.0, 0.0), h1 = h0, h2 = h0;
+    if (hlane && lane / DW < nx) h1 = __ldcg(hin + lane);
+    if (hlane && C + lane / DW < nx) h2 = __ldcg(hin + C * DW + lane);
 
     double xin[DW][2], yin[DW][2];
 #pragma unroll
     for (int k = 0; k < DW; ++k) xin[k][0] = xin[k][1] = yin[k][0] = yin[k][1] = 0.0;
 
-    for (int t = 0; t < T; ++t) {
-      const int ip = t - lane;
-      const bool act = row_ok && ip >= 0 && ip < nx;
-      if (lane == 0 && act && hin) {
-        if (ip >= avail) {
-          while ((avail = ld_acquire_gpu(pin)) <= ip) __nanosleep(32);
-        }
+    for (int m = 0; m < nchunks; ++m) {
+      if (lane == 0 && m + P - 1 < nchunks) {
+        const int mm = m + P - 1;
+        const int st = mm % P, t0 = mm * C;
+        const uint32_t n = (uint32_t)min(C, T - t0);
+        double* buf = ring + st * SD;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bars[wib][st], n * (256u + (scat ? 1024u : 0u) + 1024u * (uint32_t)nd));
+        tma_load_1d(buf, sig + t0 * 32, n * 256u, &bars[wib][st]);
+        if (scat) tma_load_1d(buf + C * 32, scat + t0 * 128, n * 1024u, &bars[wib][st]);
 #pragma unroll
-        for (int k = 0; k < DW; ++k) {
-          const double2 v = __ldcg(reinterpret_cast<const double2*>(hin) + (int64_t)ip * DW + k);
-          yin[k][0] = v.x;
-          yin[k][1] = v.y;
-        }
+        for (int k = 0; k < DW; ++k)
+          if (k < nd)
+            tma_load_1d(buf + C * 160 + k * C * 128, a.rhs_sk + slot_off[k] + t0 * 128, n * 1024u,
+                        &bars[wib][st]);
       }
-      double ytop[DW][2];
-#pragma unroll
-      for (int k = 0; k < DW; ++k) ytop[k][0] = ytop[k][1] = 0.0;
-      if (act) {
-        const double sigma = __ldg(sig + sk_sc_off(T, s, t, lane));
-        double sc[4] = {0.0, 0.0, 0.0, 0.0};
-        if (scat) {
-          const double2 u = __ldg(reinterpret_cast<const double2*>(scat + sk_vec_off(T, s, t, 0, lane)));
-          const double2 v = __ldg(reinterpret_cast<const double2*>(scat + sk_vec_off(T, s, t, 1, lane)));
-          sc[0] = u.x; sc[1] = u.y; sc[2] = v.x; sc[3] = v.y;
-        }
-        double ph[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int k = 0; k < DW; ++k) {
-          if (k < nd) {
-            const double2 u = __ldg(reinterpret_cast<const double2*>(rhs_base[k] + sk_vec_off(T, s, t, 0, lane)));
-            const double2 v = __ldg(reinterpret_cast<const double2*>(rhs_base[k] + sk_vec_off(T, s, t, 1, lane)));
-            double b[4] = {u.x + sc[0], u.y + sc[1], v.x + sc[2], v.y + sc[3]};
-            // upwind couplings (transport_sn.py:312-320): x first, then y
-            b[0] += ox[k] * (a.ex[0] * xin[k][0] + a.ex[1] * xin[k][1]);
-            b[2] += ox[k] * (a.ex[2] * xin[k][0] + a.ex[3] * xin[k][1]);
-            b[0] += oy[k] * (a.ey[0] * yin[k][0] + a.ey[1] * yin[k][1]);
-            b[1] += oy[k] * (a.ey[2] * yin[k][0] + a.ey[3] * yin[k][1]);
-            double A[16];
-#pragma unroll
-            for (int m = 0; m < 16; ++m) A[m] = fma(sigma, a.mass[m], s_S[wib][k][m]);
-            double x[4];
-            solve4(A, b, x);
-            double2* po = reinterpret_cast<double2*>(psi_base[k]);
-            po[sk_vec_off(T, s, t, 0, lane) >> 1] = make_double2(x[0], x[1]);
-            po[sk_vec_off(T, s, t, 1, lane) >> 1] = make_double2(x[2], x[3]);
-            xin[k][0] = x[1]; xin[k][1] = x[3];
-            ytop[k][0] = x[2]; ytop[k][1] = x[3];
-            ph[0] += cw[k] * x[0]; ph[1] += cw[k] * x[1];
-            ph[2] += cw[k] * x[2]; ph[3] += cw[k] * x[3];
+      // y-inflow of lane 0 for this chunk's columns (strip below, via L2)
+      h0 = h1;
+      h1 = h2;
+      if (hlane && m < hchunks && m * C + lane / DW < nx) {
+        double2* slot = hin + (int64_t)m * C * DW + lane;
+        int spins = 0;
+        while (is_empty(h0.x) || is_empty(h0.y)) {
+          ++spins;
+          __nanosleep(32);
+          h0 = __ldcv(slot);
+          if (spins > (1 << 26)) {  // report instead of hanging the GPU
+            atomicOr(a.status, 2);
+            h0 = make_double2(0.0, 0.0);
           }
         }
-        if (phi) {
-          double2* pp = reinterpret_cast<double2*>(phi);
-          pp[sk_vec_off(T, s, t, 0, lane) >> 1] = make_double2(ph[0], ph[1]);
-          pp[sk_vec_off(T, s, t, 1, lane) >> 1] = make_double2(ph[2], ph[3]);
+        __stcg(slot, make_double2(empty, empty));  // re-arm for the next launch
+      }
+      if (hlane && m + 2 < hchunks && (m + 2) * C + lane / DW < nx)
+        h2 = __ldcg(hin + (int64_t)(m + 2) * C * DW + lane);  // speculative prefetch
+      {
+        const int st = m % P;
+        mbar_wait(&bars[wib][st], (parity >> st) & 1u);
+        parity ^= 1u << st;
+      }
+      const double* buf = ring + (m % P) * SD;
+
+#pragma unroll
+      for (int tt = 0; tt < C; ++tt) {
+        const int t = m * C + tt;
+        const int ip = t - lane;
+        // t >= T implies ip >= nx, so inactive lanes cover the tail chunk
+        const bool act = row_ok && ip >= 0 && ip < nx;
+#pragma unroll
+        for (int k = 0; k < DW; ++k) {
+          const double y0 = __shfl_sync(kFull, h0.x, tt * DW + k);
+          const double y1 = __shfl_sync(kFull, h0.y, tt * DW + k);
+          if (lane == 0 && hin != nullptr) { yin[k][0] = y0; yin[k][1] = y1; }
+        }
+        double ytop[DW][2];
+#pragma unroll
+        for (int k = 0; k < DW; ++k) ytop[k][0] = ytop[k][1] = 0.0;
+        if (act) {
+          const double sigma = buf[tt * 32 + lane];
+          double sc[4] = {0.0, 0.0, 0.0, 0.0};
+          if (scat) {
+            const double2 u = reinterpret_cast<const double2*>(buf + C * 32 + tt * 128)[lane];
+            const double2 v = reinterpret_cast<const double2*>(buf + C * 32 + tt * 128 + 64)[lane];
+            sc[0] = u.x; sc[1] = u.y; sc[2] = v.x; sc[3] = v.y;
+          }
+          double ph[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int k = 0; k < DW; ++k) {
+            if (k < nd) {
+              const double* rb = buf + C * 160 + k * C * 128 + tt * 128;
+              const double2 u = reinterpret_cast<const double2*>(rb)[lane];
+              const double2 v = reinterpret_cast<const double2*>(rb + 64)[lane];
+              double b[4] = {u.x + sc[0], u.y + sc[1], v.x + sc[2], v.y + sc[3]};
+              // upwind couplings (transport_sn.py:312-320): x first, then y
+              b[0] += ox[k] * (a.ex[0] * xin[k][0] + a.ex[1] * xin[k][1]);
+              b[2] += ox[k] * (a.ex[2] * xin[k][0] + a.ex[3] * xin[k][1]);
+              b[0] += oy[k] * (a.ey[0] * yin[k][0] + a.ey[1] * yin[k][1]);
+              b[1] += oy[k] * (a.ey[2] * yin[k][0] + a.ey[3] * yin[k][1]);
+              double A[16];
+#pragma unroll
+              for (int q = 0; q < 16; ++q) A[q] = fma(sigma, a.mass[q], s_S[wib][k][q]);
+              double x[4];
+              solve4(A, b, x);
+              double2* po = reinterpret_cast<double2*>(a.psi_sk + slot_off[k] + (int64_t)t * 128 + 2 * lane);
+              po[0] = make_double2(x[0], x[1]);
+              po[32] = make_double2(x[2], x[3]);
+              xin[k][0] = x[1]; xin[k][1] = x[3];
+              ytop[k][0] = x[2]; ytop[k][1] = x[3];
+              ph[0] += cw[k] * x[0]; ph[1] += cw[k] * x[1];
+              ph[2] += cw[k] * x[2]; ph[3] += cw[k] * x[3];
+            }
+          }
+          if (phi_p) {
+            double2* pp = reinterpret_cast<double2*>(phi_p + (int64_t)t * 128);
+            pp[0] = make_double2(ph[0], ph[1]);
+            pp[32] = make_double2(ph[2], ph[3]);
+          }
+          if (lane == 31 && hout) {
+            double2* ho = hout + (int64_t)ip * DW;
+#pragma unroll
+            for (int k = 0; k < DW; ++k) __stcg(ho + k, make_double2(ytop[k][0], ytop[k][1]));
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < DW; ++k) {
+          const double y0 = __shfl_up_sync(kFull, ytop[k][0], 1);
+          const double y1 = __shfl_up_sync(kFull, ytop[k][1], 1);
+          if (lane > 0) { yin[k][0] = y0; yin[k][1] = y1; }
         }
       }
-#pragma unroll
-      for (int k = 0; k < DW; ++k) {
-        const double y0 = __shfl_up_sync(kFull, ytop[k][0], 1);
-        const double y1 = __shfl_up_sync(kFull, ytop[k][1], 1);
-        if (lane > 0) { yin[k][0] = y0; yin[k][1] = y1; }
-      }
-      if (lane == 31 && act && hout) {
-        double2* ho = reinterpret_cast<double2*>(hout) + (int64_t)ip * DW;
-#pragma unroll
-        for (int k = 0; k < DW; ++k) ho[k] = make_double2(ytop[k][0], ytop[k][1]);
-        if ((ip & 7) == 7 || ip == nx - 1) st_release_gpu(pout, ip + 1);
-      }
+      __syncwarp();  // every lane is done with stage m % P before it is refilled
     }
   }
+}
+
+
+__global__ void fill_empty_kernel(double* p, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = __longlong_as_double((long long)kEmpty);
 }
 
 // rhs_sk[d] = source_vector(q) + inv_cdt M psi_time[:, d] + extra[:, d]
@@ -370,24 +495,25 @@ __global__ void sk_to_canonical_kernel(int nx, int ny, int D, const int* __restr
   for (int l = 0; l < 4; ++l) psi[(int64_t)(4 * c + l) * ld + d] = o[l ^ f];
 }
 
-static int64_t handoff_offset_bytes(int nx, int ny, int G) {
-  const int64_t head = 256 + (int64_t)sk_strips(ny) * G * sizeof(int);
-  return (head + 255) / 256 * 256;
-}
+static int64_t handoff_offset_bytes(int, int, int) { return 256; }
 
 template <int DW>
 int launch_sweep(const SweepArgs& a, int max_ctas, cudaStream_t st) {
+  constexpr int WPC = SweepCfg<DW>::WPC;
+  constexpr size_t smem = sweep_smem_bytes<DW>();
   int dev = 0, sms = 0, occ = 0;
   DLRSN_TRY_CUDA(cudaGetDevice(&dev));
   DLRSN_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  DLRSN_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_kernel<DW>, 128, 0));
+  DLRSN_TRY_CUDA(cudaFuncSetAttribute(sweep_kernel<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+  DLRSN_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_kernel<DW>, WPC * 32, smem));
   const int items = sk_strips(a.ny) * a.G;
-  int ctas = (items + 3) / 4;
+  int ctas = (items + WPC - 1) / WPC;
   const int cap = sms * (occ > 0 ? occ : 1);
   if (ctas > cap) ctas = cap;
   if (max_ctas > 0 && ctas > max_ctas) ctas = max_ctas;
   if (ctas < 1) ctas = 1;
-  sweep_kernel<DW><<<ctas, 128, 0, st>>>(a);
+  sweep_kernel<DW><<<ctas, WPC * 32, smem, st>>>(a);
   DLRSN_CHECK_LAUNCH("sweep_kernel");
   return DLRSN_OK;
 }
@@ -460,6 +586,19 @@ int dlrsn_sk_to_canonical(const dlrsn_cellops* ops, int D, const int* quad, cons
   return DLRSN_OK;
 }
 
+int dlrsn_sweep_workspace_init(void* workspace, int64_t workspace_bytes, dlrsn_stream_t stream) {
+  DLRSN_REQUIRE(workspace && workspace_bytes >= 256, "sweep workspace too small");
+  cudaStream_t st = as_stream(stream);
+  DLRSN_TRY_CUDA(cudaMemsetAsync(workspace, 0, 256, st));
+  const int64_t n = (workspace_bytes - 256) / (int64_t)sizeof(double);
+  if (n > 0) {
+    fill_empty_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+        reinterpret_cast<double*>(reinterpret_cast<char*>(workspace) + 256), n);
+    DLRSN_CHECK_LAUNCH("fill_empty_kernel");
+  }
+  return DLRSN_OK;
+}
+
 int dlrsn_sweep(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int dw,
                 const double* sigma_t_sk4, const double* scat_sk4, const double* rhs_sk,
                 double* psi_sk, double* phi_part_sk, void* workspace, int64_t workspace_bytes,
@@ -473,7 +612,7 @@ int dlrsn_sweep(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int 
   if (G == 0) return DLRSN_OK;
   cudaStream_t st = as_stream(stream);
   const int64_t head = handoff_offset_bytes(ops->nx, ops->ny, G);
-  DLRSN_TRY_CUDA(cudaMemsetAsync(workspace, 0, head, st));
+  DLRSN_TRY_CUDA(cudaMemsetAsync(workspace, 0, sizeof(int), st));  // work ticket
   SweepArgs a;
   a.nx = ops->nx; a.ny = ops->ny; a.G = G;
   a.groups = groups;
@@ -483,7 +622,7 @@ int dlrsn_sweep(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int 
   a.psi_sk = psi_sk;
   a.phi_sk = phi_part_sk;
   a.ticket = reinterpret_cast<int*>(workspace);
-  a.progress = reinterpret_cast<int*>(reinterpret_cast<char*>(workspace) + 256);
+  a.status = reinterpret_cast<int*>(workspace) + 1;
   a.handoff = reinterpret_cast<double*>(reinterpret_cast<char*>(workspace) + head);
   for (int m = 0; m < 16; ++m) {
     a.mass[m] = ops->mass[m];

@@ -184,7 +184,7 @@ class _SweepPlan:
         self.groups_dev = _groups_to_device(self.groups)
         self.quads_dev = torch.from_numpy(quads).to(device())
         self.ws_bytes = int(_lib.load().dlrsn_sweep_workspace_bytes(g.nx, g.ny, self.G, self.dw))
-        self.workspace = ops.buffer("sweep_ws", self.ws_bytes, dtype=torch.uint8)
+        self.workspace = sweep_workspace(ops, self.ws_bytes)
 
 
 class ctypes_int:
@@ -199,10 +199,34 @@ class ctypes_int:
         return self._v.value
 
 
+def sweep_workspace(ops, nbytes):
+    """Sweep workspace (ticket, status, handoff slots), initialised once when
+    (re)allocated; the kernel leaves it re-armed after every launch."""
+    ws = ops._scratch.get("sweep_ws")
+    if ws is None or ws.numel() < nbytes:
+        ws = _shared_workspace(ops.grid, nbytes)
+        ops._scratch["sweep_ws"] = ws
+    return ws
+
+
+_WS_CACHE = {}
+
+
+def _shared_workspace(grid, nbytes):
+    key = torch.cuda.current_device()
+    ws = _WS_CACHE.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=device())
+        _lib.call("dlrsn_sweep_workspace_init", _lib.ptr(ws), ws.numel(), stream())
+        _WS_CACHE[key] = ws
+    return ws
+
+
 def _sweep(ops, plan, rhs_sk, psi_sk, scat_sk4=None, phi_part=None, max_ctas=0):
     _lib.call("dlrsn_sweep", ops.cellops_ptr, plan.G, _lib.ptr(plan.groups_dev), plan.dw,
               _lib.ptr(ops.sigma_t_sk4()), _lib.ptr(scat_sk4), _lib.ptr(rhs_sk), _lib.ptr(psi_sk),
-              _lib.ptr(phi_part), _lib.ptr(plan.workspace), plan.ws_bytes, int(max_ctas), stream())
+              _lib.ptr(phi_part), _lib.ptr(plan.workspace), plan.workspace.numel(), int(max_ctas),
+              stream())
 
 
 def _to_canonical(ops, plan, psi_sk, out=None):
