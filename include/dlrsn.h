@@ -161,6 +161,78 @@ int dlrsn_sweep(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int 
                 double* psi_sk, double* phi_part_sk, void* workspace, int64_t workspace_bytes,
                 int max_ctas, dlrsn_stream_t stream);
 
+/* ---- K2/K3/K5: the Galerkin side of step_collocation (dlr_sn.py:86-151) */
+
+/* Y = X K (+ beta Y): (n, kx) times small (kx, ky).  evaluate_rows
+ * (lowrank.py:220-227: X (S W_sel^T)), scalar_flux (:60-62), info.phi =
+ * X lbar (dlr_sn.py:147), l_full = W gamma (:136), X R^-1 (CholQR). */
+int dlrsn_rowmix(int64_t n, int kx, int ky, const double* X, int ldx, const double* K, int ldk,
+                 double beta, double* Y, int ldy, dlrsn_stream_t stream);
+
+/* doubles of `partial` scratch needed by dlrsn_mgram (kind 0: ra x rb) or
+ * dlrsn_project (kind 1: rank ra) */
+int64_t dlrsn_partials_len(int ncell, int ra, int rb, int kind);
+
+/* G (ra x rb) = sum_c coeff_c A_c^T M B_c (coeff nullable): mass_inner
+ * Grams for Gram-Schmidt and DlrState.check (lowrank.py:23-25,68-81).
+ * Deterministic fixed-order reduction. */
+int dlrsn_mgram(const dlrsn_cellops* ops, int ra, int rb, const double* A, int lda,
+                const double* B, int ldb, const double* coeff, double* G, double* partial,
+                dlrsn_stream_t stream);
+
+/* Fused reduced operators (project_row_operators, dlr_sn.py:61-71, plus
+ * X_old^T M X of project_initial, :50-58) in one pass over the cells:
+ * out = [px, py, jx, jy, mt, ms, mo] (7 r x r, row-major) then q-hat (r).
+ * Xold nullable (mo = 0). */
+int dlrsn_project(const dlrsn_cellops* ops, int r, const double* X, const double* Xold,
+                  const double* sigma_t, const double* sigma_s, const double* q, double* out,
+                  double* partial, dlrsn_stream_t stream);
+
+/* G = R^T R (R upper) and R^-1; diag_ratio[k] = R_kk / max(sqrt(G_kk), 1)
+ * (the CGS2 deficiency quantity of angular.py:137); *flag = 1 on a
+ * non-positive pivot.  r <= 128. */
+int dlrsn_chol_upper(int r, const double* G, double* R, double* Rinv, double* diag_ratio,
+                     int* flag, dlrsn_stream_t stream);
+
+/* C (m x n) = op(A) B, op = transpose if transA; small, one CTA. */
+int dlrsn_small_matmul(int m, int k, int n, const double* A, const double* B, double* C,
+                       int transA, dlrsn_stream_t stream);
+
+/* Node matrices and their inverses (row_matrices dlr_sn.py:74-83 +
+ * np.linalg.inv lowrank.py:245-252): B_d = wx px + wy py + |wx| jx + |wy| jy
+ * + mt from the dlrsn_project output and om_sel (n x 3); om_sel NULL: proj
+ * holds B (n x r x r).  status[d] = 1 if node d is singular. */
+int dlrsn_row_inverse(int n, int r, const double* proj, const double* om_sel, double* Binv,
+                      double* Bout, int* status, dlrsn_stream_t stream);
+
+/* solve_row_system tail (lowrank.py:253-259): cbar, zeta, lbar, L (n x r). */
+int dlrsn_row_combine(int n, int r, const double* Binv, const double* ms, const double* Q,
+                      const double* wts, double* L, double* lbar, int* status,
+                      dlrsn_stream_t stream);
+
+/* deim_select (lowrank.py:168-205) by Gaussian elimination with row
+ * pivoting on a work copy of W (n x r): idx (r picks), W[idx,:] = Lhat U.
+ * *err_col = -1 on success, else the column whose residual vanished. */
+int dlrsn_deim(int n, int r, double* Wwork, const double* W, int* idx, double* Lhat, double* U,
+               int* err_col, dlrsn_stream_t stream);
+
+/* W_hat solves: mode 0 X = W_hat^-1 V (interpolation_coefficients,
+ * lowrank.py:158-160), mode 1 x = W_hat^-T v (closure_weights, :162-165). */
+int dlrsn_what_solve(int r, int m, const double* Lhat, const double* U, const double* V,
+                     double* X, int mode, dlrsn_stream_t stream);
+
+/* Exact twice-projected classical Gram-Schmidt with the reference's
+ * deficiency test and deterministic completion (angular.py:104-160).
+ * metric 0: weighted (w, angular); 1: block mass (ops, spatial).
+ * comp_kind 0: ncomp angular monomials (exponent triples, coords = omegas
+ * n x 3) then unit vectors; 1: spatial monomials (exponent pairs, coords =
+ * extent x0,y0,lx,ly).  work: n doubles; coef: 2m doubles; *status = 1 if
+ * the candidates ran out (strict). */
+int dlrsn_cgs2(int n, int m, const double* cols, int ldc, double* Q, int ldq, double* R,
+               int* deficient, int metric, const double* w, const dlrsn_cellops* ops,
+               int comp_kind, int ncomp, const int* comp_exp, const double* coords, double* work,
+               double* coef, int* status, int strict, dlrsn_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

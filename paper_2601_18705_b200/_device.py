@@ -46,7 +46,7 @@ def as_device(x, n=None, dtype=torch.float64):
         a = np.asarray(x, dtype=np.float64 if dtype == torch.float64 else None)
         if a.ndim == 0 and n is not None:
             a = np.full(n, float(a))
-        t = torch.from_numpy(np.ascontiguousarray(a)).to(device=device(), dtype=dtype)
+        t = torch.from_numpy(np.array(a, copy=True, order="C")).to(device=device(), dtype=dtype)
     if t.ndim == 0 and n is not None:
         t = t.expand(n)
     return t.contiguous()

@@ -65,6 +65,19 @@ _SIGNATURES = {
     "dlrsn_sk_to_canonical": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp, c_int, c_vp]),
     "dlrsn_sweep": (c_int, [c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64,
                             c_int, c_vp]),
+    "dlrsn_rowmix": (c_int, [c_i64, c_int, c_int, c_vp, c_int, c_vp, c_int, c_dbl, c_vp, c_int,
+                             c_vp]),
+    "dlrsn_partials_len": (c_i64, [c_int, c_int, c_int, c_int]),
+    "dlrsn_mgram": (c_int, [c_vp, c_int, c_int, c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_vp]),
+    "dlrsn_project": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "dlrsn_chol_upper": (c_int, [c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "dlrsn_small_matmul": (c_int, [c_int, c_int, c_int, c_vp, c_vp, c_vp, c_int, c_vp]),
+    "dlrsn_row_inverse": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "dlrsn_row_combine": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "dlrsn_deim": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "dlrsn_what_solve": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp]),
+    "dlrsn_cgs2": (c_int, [c_int, c_int, c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_int, c_vp, c_vp,
+                           c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp]),
 }
 
 _lib = None

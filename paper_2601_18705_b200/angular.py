@@ -122,6 +122,42 @@ def constant_column(quad):
     return np.full(quad.n_angles, 1.0 / np.sqrt(FOUR_PI))
 
 
+def angular_monomial_exponents(count):
+    """(kx, ky, kz) of the first ``count`` candidates of angular_monomials."""
+    out = [(0, 0, 0)]
+    deg = 1
+    while len(out) < count:
+        for kx in range(deg, -1, -1):
+            for ky in range(deg - kx, -1, -1):
+                out.append((kx, ky, deg - kx - ky))
+        deg += 1
+    return out[:count]
+
+
+def orthonormalize(columns, quad, pin_constant=False):
+    """Weighted CGS2 with deterministic completion (angular.py:217-238), as
+    one CUDA kernel.  Returns (AngularBasis, R, deficient)."""
+    from .lowrank import _cgs2
+
+    cols = as_device(columns)
+    if cols.ndim != 2 or cols.shape[0] != quad.n_angles:
+        raise ContractViolation(
+            f"basis rows ({cols.shape[0]}) must match quadrature size ({quad.n_angles})")
+    if pin_constant:
+        const = torch.full((quad.n_angles, 1), 1.0 / np.sqrt(FOUR_PI), dtype=torch.float64,
+                           device=cols.device)
+        cols = torch.cat([const, cols], dim=1)
+    n, m = cols.shape
+    ncomp = (m - (1 if pin_constant else 0)) + 8
+    exps = np.asarray(angular_monomial_exponents(ncomp), dtype=np.int32)
+    Q, R, deficient = _cgs2(n, m, cols.contiguous(), metric=0, weights=quad.weights_device(),
+                            comp_kind=0, comp_exp=exps, coords=quad.omegas_device(), strict=True)
+    basis = AngularBasis(values=Q, pinned=pin_constant).bind(quad)
+    if pin_constant:
+        return basis, R[:, 1:], [d - 1 for d in deficient if d > 0]
+    return basis, R, deficient
+
+
 def angular_monomials(quad, count):
     """Completion candidates: monomials in omega by rising degree, then unit
     vectors (angular.py:198-214).  Returned as an (n_angles, k) host array."""

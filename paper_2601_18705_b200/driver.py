@@ -1,0 +1,136 @@
+"""Device-resident DLR-SN time loop for the BASELINE configurations.
+
+Restates the dlr-sn branch of the reference driver's loop
+(driver.py:485-539: linearize -> step_collocation -> dofs_to_cells ->
+update_temperature -> floor) with every per-cell array on the device, plus
+the SURVEY Appendix B adapters (physical scattering / external source added
+to the linearised step, T-dependent opacity, frozen coefficients for C5).
+Host I/O, CSV output and energy diagnostics of the reference driver are out
+of scope.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import as_device, device, empty, stream, zeros
+from .angular import AngularBasis, build_quadrature, orthonormalize
+from .errors import ContractViolation
+from .lowrank import DlrState, gram_schmidt_mass, mass_gram
+from .mesh import build_grid, cellops_struct
+from .physics import LinearizedStep, PhysicsConstants, linearize
+from .problems import ProblemSpec, draw_factors
+
+FOUR_PI = 4.0 * np.pi
+
+
+@dataclass(eq=False)
+class DeviceProblem:
+    spec: ProblemSpec
+    grid: object
+    quad: object
+    constants: PhysicsConstants
+    sigma_a0: torch.Tensor
+    rho_cv: torch.Tensor
+    ss_phys: torch.Tensor
+    q_ext: torch.Tensor
+
+    @classmethod
+    def from_spec(cls, spec):
+        grid = build_grid(spec.nx, spec.ny, spec.extent)
+        quad = build_quadrature(spec.n_polar, spec.n_azimuthal)
+        sa0 = spec.sigma_a if spec.opacity[0] == "constant" else np.full(spec.n_cells, spec.opacity[1])
+        return cls(spec, grid, quad, PhysicsConstants(c=spec.c, a_r=spec.a_r), as_device(sa0),
+                   as_device(spec.rho_cv), as_device(spec.sigma_s_phys), as_device(spec.q_ext))
+
+    @property
+    def opacity_power(self):
+        return 0.0 if self.spec.opacity[0] == "constant" else float(self.spec.opacity[2])
+
+    def linearized(self, T):
+        """Linearised step at temperature T (physics.py:94-120 + adapters)."""
+        T = as_device(T)
+        if self.spec.frozen:
+            st = linearize(T, as_device(self.spec.frozen_sigma_t) - 1.0 / (self.spec.c * self.spec.dt),
+                           self.rho_cv, self.spec.dt, self.constants, check=False)
+            st.sigma_t = as_device(self.spec.frozen_sigma_t)
+            st.sigma_s = zeros(self.spec.n_cells)
+            st.q = as_device(self.spec.frozen_q)
+            return st
+        sa = self.sigma_a0 if self.opacity_power == 0.0 else self.sigma_a0 * T ** self.opacity_power
+        return linearize(T, sa, self.rho_cv, self.spec.dt, self.constants,
+                         sigma_s_phys=self.ss_phys, q_ext=self.q_ext, check=False)
+
+    def advance(self, lin, phi_dofs, T):
+        """Finish a step (T update + floor, driver.py:532-534) and linearise
+        the next one in a single fused pass (K4).  Updates ``T`` in place and
+        returns the next LinearizedStep."""
+        n = self.spec.n_cells
+        if self.spec.frozen:
+            from .physics import update_temperature
+
+            T.copy_(update_temperature(phi_dofs, lin, self.spec.t_floor))
+            return lin
+        # the kernel reads this step's sigma_a / denom, then overwrites them
+        sa = lin.sigma_a.clone()
+        den = lin.denom.clone()
+        st, ss, q = (empty(n) for _ in range(3))
+        status = zeros(1, dtype=torch.int32)
+        k = self.constants
+        _lib.call("dlrsn_advance_relinearize", n, _lib.ptr(as_device(phi_dofs)), _lib.ptr(T),
+                  _lib.ptr(sa), _lib.ptr(self.sigma_a0), self.opacity_power,
+                  _lib.ptr(self.rho_cv), float(self.spec.dt), float(k.c), float(k.a_r),
+                  float(self.spec.t_floor), _lib.ptr(self.ss_phys), _lib.ptr(self.q_ext),
+                  _lib.ptr(st), _lib.ptr(ss), _lib.ptr(q), _lib.ptr(den), _lib.ptr(status),
+                  stream())
+        return LinearizedStep(sigma_t=st, sigma_s=ss, sigma_a=sa, q=q, T0=T.clone(), denom=den,
+                              rho_cv=self.rho_cv, dt=float(self.spec.dt),
+                              inv_cdt=1.0 / (k.c * self.spec.dt), constants=k)
+
+
+def initial_state(dp, X=None, W=None, seed=None, T=None):
+    """Seeded random-orthonormal X (M inner product, spatial-monomial
+    completion) and W (weighted), S = (X^T M b0) beta^T.
+    ``X`` / ``W`` may be given already orthonormal (e.g. by a test oracle)."""
+    spec = dp.spec
+    if X is None or W is None:
+        rng = np.random.default_rng(spec.seed if seed is None else seed)
+        Xr, Wr = draw_factors(spec, rng)
+        co = cellops_struct(dp.grid)
+        X, _, dx = gram_schmidt_mass(co, as_device(Xr), spec.rank + 8, method="cgs2")
+        basis, _, dw = orthonormalize(as_device(Wr), dp.quad)
+        if dx or dw:
+            raise ContractViolation("random initial factors are rank deficient")
+        W = basis
+    X = as_device(X)
+    W = W if isinstance(W, AngularBasis) else AngularBasis(values=W).bind(dp.quad)
+    T = as_device(spec.T0 if T is None else T)
+    k = dp.constants
+    b0 = (k.a_r * k.c / FOUR_PI) * (T * T) ** 2
+    b0 = b0.repeat_interleave(4).reshape(-1, 1)
+    xb = mass_gram(cellops_struct(dp.grid), X, b0)[:, 0]
+    S = torch.outer(xb, W.beta)
+    return DlrState(X=X, S=S, W=W)
+
+
+def run(dp, state, n_steps, *, si_tol=1e-8, si_max_iters=200, check_state=True, T=None,
+        record=None, gs_method="cholqr2"):
+    """n_steps of the dlr-sn loop; returns (state, T, infos)."""
+    from .dlr_sn import step_collocation
+
+    T = as_device(dp.spec.T0 if T is None else T).clone()
+    lin = dp.linearized(T)
+    infos = []
+    for _ in range(n_steps):
+        state, info = step_collocation(dp.grid, lin, dp.quad, state, si_tol=si_tol,
+                                       si_max_iters=si_max_iters, use_dsa=False,
+                                       check_state=check_state, gs_method=gs_method)
+        lin = dp.advance(lin, info.phi, T)
+        infos.append(info)
+        if record is not None:
+            record(state, info, T)
+    return state, T, infos
