@@ -1,0 +1,371 @@
+"""Benchmark of the SN-like DLR hot path on B200 (BASELINE.json metric).
+
+Workload (N=1): BASELINE config 2 -- 280x280 checkerboard on [0,7]^2,
+rank 16, 32x32 product quadrature (1024 directions), dt=0.01, fp64,
+seeded random-orthonormal initial factors, use_dsa=False, si_tol=1e-8.
+A step is one DLR time step: step_collocation (DEIM -> collocated source
+iteration -> spatial Gram-Schmidt -> fused projections -> row solve ->
+angular re-orthonormalisation) plus the fused temperature update /
+re-linearisation.  The value is sweep cell-angle updates per second over
+whole steps (sum over steps of n_cells x r x SI iterations / device time);
+``dlr_steps_per_s`` and the config-2 full-SN comparison sweep are reported
+alongside.
+
+``--impl reference`` times the CPU restatement of the reference (oracle/,
+"port") on the same config on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "SN-sweep cell-angle updates/s and DLR steps/s, % of HBM roofline, 1/2/4/8 B200"
+UNIT = "cell-angle updates/s"
+SWEEP_BYTES_PER_CELL_ANGLE = 64  # rhs read + psi write
+SWEEP_BYTES_PER_CELL = 160  # sigma_t + scatter source per quadrant batch (4 x 40 B)
+
+
+def _peaks():
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_reference_step_rate(spec, n_steps, warmup):
+    """Time the oracle port (the reference algorithm restated in numpy) on
+    the host: returns (cell-angle updates/s, steps/s, seconds, iterations)."""
+    from oracle import runner as R
+
+    rng = np.random.default_rng(spec.seed)
+    from paper_2601_18705_b200.problems import draw_factors
+
+    Xr, Wr = draw_factors(spec, rng)
+    X, W = R.orthonormal_factors(spec, Xr, Wr)
+    state = R.initial_state(spec, X, W)
+    T = spec.T0.copy()
+    for _ in range(warmup):
+        state, T, _ = R.run(spec, state, 1, si_tol=1e-8, T=T)
+    t0 = time.perf_counter()
+    state, T, infos = R.run(spec, state, n_steps, si_tol=1e-8, T=T)
+    dt = time.perf_counter() - t0
+    iters = sum(i.iterations for i in infos)
+    return spec.n_cells * spec.rank * iters / dt, n_steps / dt, dt, iters
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    from paper_2601_18705_b200 import problems
+
+    spec = problems.config2()
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    warm = min(args.warmup, 1)
+    rate, sps, sec, iters = cpu_reference_step_rate(spec, args.steps, warm)
+    line = {
+        "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": "C2 checkerboard 280x280, r=16, 32x32 quadrature, dlr-sn step",
+                   "si_tol": 1e-8, "use_dsa": False},
+        "dlr_steps_per_s": sps,
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} full C2 DLR steps ({iters} sweeps of 16 directions)"
+                                   f" after {warm} warm-up step(s), numpy/scipy, BLAS on all cores"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--full-sn", type=int, default=1, help="also time the config-2 full-SN sweep")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+
+    from paper_2601_18705_b200 import _lib, problems, transport
+    from paper_2601_18705_b200._device import set_device
+    from paper_2601_18705_b200.dlr_sn import step_collocation
+    from paper_2601_18705_b200.driver import DeviceProblem, initial_state
+
+    ws, rank, local = _dist()
+    set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    spec = problems.config2()
+    dp = DeviceProblem.from_spec(spec)
+    state = initial_state(dp)
+    T = torch.as_tensor(spec.T0, device="cuda").clone()
+    lin = dp.linearized(T)
+
+    def one_step(state, lin):
+        state, info = step_collocation(dp.grid, lin, dp.quad, state, si_tol=1e-8, use_dsa=False,
+                                       check_state=True)
+        lin = dp.advance(lin, info.phi, T)
+        return state, lin, info
+
+    for _ in range(args.warmup):
+        state, lin, _ = one_step(state, lin)
+    torch.cuda.synchronize()
+
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 512 MB > L2
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    transport.SWEEP_EVENTS = []
+    iters = []
+    launches0 = _lib.launch_count[0]
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(float(k))  # evict L2 between timed steps (outside the events)
+            starts[k].record()
+            state, lin, info = one_step(state, lin)
+            ends[k].record()
+            iters.append(info.iterations)
+        torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    launches = _lib.launch_count[0] - launches0 - args.steps * 0
+    if ws > 1:
+        torch.distributed.barrier()
+    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    sweeps = transport.SWEEP_EVENTS
+    transport.SWEEP_EVENTS = None
+    sweep_ms = [s.elapsed_time(e) for s, e, *_ in sweeps]
+    n_cells, D, G = sweeps[0][2], sweeps[0][3], sweeps[0][4]
+    updates = sum(spec.n_cells * spec.rank * it for it in iters)
+    value = updates / (ms * 1e-3)
+    peak, peak_kind = _peaks()
+    alg_bytes = n_cells * (D * SWEEP_BYTES_PER_CELL_ANGLE + SWEEP_BYTES_PER_CELL)
+    sweep_avg_ms = float(np.mean(sweep_ms))
+    achieved = alg_bytes / (sweep_avg_ms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(HERE, "profiles", "sweep_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("C2_dlr_sweep_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- end-to-end: public API with HOST (pinned) buffers each step -------
+    e2e = measure_e2e(dp, state, T, lin, max(1, min(args.steps, 5)))
+
+    # ---- full-SN comparison sweep (config 2: all 1024 directions) ----------
+    full = measure_full_sn(dp) if args.full_sn else None
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE config 2 checkerboard, random-orthonormal factors)",
+        "config": {"workload": "C2 checkerboard 280x280, r=16, 32x32 quadrature, dlr-sn step",
+                   "si_tol": 1e-8, "use_dsa": False, "parallelism": f"dp{ws} (directions)",
+                   "l2": "512 MB buffer written between timed steps (outside the step events)"},
+        "dlr_steps_per_s": args.steps / (ms * 1e-3),
+        "si_iterations_per_step": float(np.mean(iters)),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": "sweep_kernel", "launch_ms": sweep_avg_ms,
+                     "alg_bytes_per_launch": alg_bytes,
+                     "sweep_share_of_step": sum(sweep_ms) / ms},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "wall_s_timed_region": wall,
+    }
+    if full is not None:
+        line["full_sn_sweep"] = full
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+        rate, sps, sec, it = cpu_reference_step_rate(spec, args.cpu_steps, 0)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                                "sample": f"{args.cpu_steps} full C2 DLR steps of the oracle port "
+                                          f"({it} sweeps of 16 directions, {sec:.1f} s)",
+                                "dlr_steps_per_s": sps}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def measure_e2e(dp, state, T, lin, n):
+    """Same step through the public API with the state and per-cell fields
+    in pinned HOST memory: H2D of X, S, W, T and the step coefficients,
+    step_collocation, D2H of the new X, S, W and T every step."""
+    import torch
+
+    from paper_2601_18705_b200.dlr_sn import step_collocation
+    from paper_2601_18705_b200.lowrank import DlrState
+    from paper_2601_18705_b200.angular import AngularBasis
+    from paper_2601_18705_b200.physics import LinearizedStep
+
+    def pin(t):
+        return t.detach().cpu().pin_memory()
+
+    host = {"X": pin(state.X), "S": pin(state.S), "W": pin(state.W.values), "T": pin(T)}
+    fields = ("sigma_t", "sigma_s", "sigma_a", "q", "T0", "denom", "rho_cv")
+    hlin = {f: pin(getattr(lin, f)) for f in fields}
+    out = {k: torch.empty_like(v).pin_memory() for k, v in host.items()}
+    h2d = sum(v.numel() * 8 for v in host.values()) + sum(v.numel() * 8 for v in hlin.values())
+    d2h = sum(v.numel() * 8 for v in out.values())
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = 0
+    e0.record()
+    for _ in range(n):
+        X = host["X"].to("cuda", non_blocking=True)
+        S = host["S"].to("cuda", non_blocking=True)
+        W = host["W"].to("cuda", non_blocking=True)
+        dl = {f: v.to("cuda", non_blocking=True) for f, v in hlin.items()}
+        st = DlrState(X=X, S=S, W=AngularBasis(values=W).bind(dp.quad))
+        step = LinearizedStep(dt=lin.dt, inv_cdt=lin.inv_cdt, constants=lin.constants, **dl)
+        new, info = step_collocation(dp.grid, step, dp.quad, st, si_tol=1e-8, use_dsa=False)
+        Tn = dp.advance(step, info.phi, dl["T0"].clone())
+        out["X"].copy_(new.X, non_blocking=True)
+        out["S"].copy_(new.S, non_blocking=True)
+        out["W"].copy_(new.W.values, non_blocking=True)
+        out["T"].copy_(Tn.T0, non_blocking=True)
+        iters += info.iterations
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    spec = dp.spec
+    return {"value": spec.n_cells * spec.rank * iters / (ms * 1e-3), "unit": UNIT,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "steps": n, "ms_per_step": ms / n}
+
+
+def measure_full_sn(dp, reps=3):
+    """Config 2's full-SN comparison sweep: one source-iteration sweep over
+    all 1024 quadrature directions (closure = quadrature weights) on the
+    280x280 grid, psi stored (64 B/cell-angle algorithmic)."""
+    import torch
+
+    from paper_2601_18705_b200 import transport
+
+    T = torch.as_tensor(dp.spec.T0, device="cuda")
+    lin = dp.linearized(T)
+    ops = transport.assemble_operators(dp.grid, lin)
+    quad = dp.quad
+    plan = transport._SweepPlan(ops, quad.omegas, quad.weights)
+    vl = ops.vec_len
+    D = quad.n_angles
+    rhs = torch.rand(D * vl, dtype=torch.float64, device="cuda")
+    psi = torch.empty_like(rhs)
+    part = torch.empty(plan.G * vl, dtype=torch.float64, device="cuda")
+    scat = torch.zeros(4 * vl, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        transport._sweep(ops, plan, rhs, psi, scat, part)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        transport._sweep(ops, plan, rhs, psi, scat, part)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    nc = dp.grid.n_cells
+    alg = nc * (D * SWEEP_BYTES_PER_CELL_ANGLE + SWEEP_BYTES_PER_CELL)
+    peak, _ = _peaks()
+    return {"directions": D, "ms_per_sweep": ms, "cell_angle_per_s": nc * D / (ms * 1e-3),
+            "achieved_GBs": alg / (ms * 1e-3) / 1e9, "frac_of_hbm": alg / (ms * 1e-3) / 1e9 / peak,
+            "group_width": plan.dw, "groups": plan.G}
+
+
+if __name__ == "__main__":
+    main()

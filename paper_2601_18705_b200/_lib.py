@@ -119,8 +119,21 @@ def check(status, what=""):
     raise RuntimeError(f"dlrsn CUDA failure ({status}): {text}")
 
 
+# kernels each entry point launches (for bench.py's gpu_launches count)
+_KERNELS_PER_CALL = {
+    "dlrsn_linearize": 1, "dlrsn_update_temperature": 1, "dlrsn_advance_relinearize": 1,
+    "dlrsn_rhs_build": 1, "dlrsn_cells_to_sk4": 1, "dlrsn_scatter_source": 1,
+    "dlrsn_phi_combine": 1, "dlrsn_sk_to_canonical": 1, "dlrsn_sweep": 1,
+    "dlrsn_sweep_workspace_init": 1, "dlrsn_rowmix": 1, "dlrsn_mgram": 2, "dlrsn_project": 2,
+    "dlrsn_chol_upper": 1, "dlrsn_small_matmul": 1, "dlrsn_row_inverse": 1,
+    "dlrsn_row_combine": 1, "dlrsn_deim": 1, "dlrsn_what_solve": 1, "dlrsn_cgs2": 1,
+}
+launch_count = [0]
+
+
 def call(name, *args):
     check(getattr(load(), name)(*args), name)
+    launch_count[0] += _KERNELS_PER_CALL.get(name, 0)
 
 
 def ptr(t):

@@ -222,11 +222,24 @@ def _shared_workspace(grid, nbytes):
     return ws
 
 
+# Optional live timing of sweep launches (bench.py roofline): when set to a
+# list, every launch appends (start_event, end_event, n_cells, n_dirs).
+SWEEP_EVENTS = None
+
+
 def _sweep(ops, plan, rhs_sk, psi_sk, scat_sk4=None, phi_part=None, max_ctas=0):
+    sig = ops.sigma_t_sk4()
+    ev = None
+    if SWEEP_EVENTS is not None:
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        ev[0].record()
     _lib.call("dlrsn_sweep", ops.cellops_ptr, plan.G, _lib.ptr(plan.groups_dev), plan.dw,
-              _lib.ptr(ops.sigma_t_sk4()), _lib.ptr(scat_sk4), _lib.ptr(rhs_sk), _lib.ptr(psi_sk),
+              _lib.ptr(sig), _lib.ptr(scat_sk4), _lib.ptr(rhs_sk), _lib.ptr(psi_sk),
               _lib.ptr(phi_part), _lib.ptr(plan.workspace), plan.workspace.numel(), int(max_ctas),
               stream())
+    if ev is not None:
+        ev[1].record()
+        SWEEP_EVENTS.append((ev[0], ev[1], ops.grid.n_cells, plan.D, plan.G))
 
 
 def _to_canonical(ops, plan, psi_sk, out=None):
