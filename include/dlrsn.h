@@ -86,6 +86,10 @@ int64_t dlrsn_sk_scalar_len(int nx, int ny);
  * Word 1 of the workspace is a sticky status (2 = a handoff wait timed out). */
 int64_t dlrsn_sweep_workspace_bytes(int nx, int ny, int n_groups, int dw);
 int dlrsn_sweep_workspace_init(void* workspace, int64_t workspace_bytes, dlrsn_stream_t stream);
+/* debug: record globaltimer per (work item, chunk) before/after the strip
+ * handoff wait into buf[(item*chunks + m)*2 + {0,1}]; buf NULL disables. */
+int dlrsn_debug_trace(unsigned long long* buf, int chunks);
+int dlrsn_debug_flags(int flags); /* debug: bit0 = no speculative handoff prefetch */
 
 /* ---- K4: per-cell physics (physics.py:63-132, driver.py:344-346,532-534) */
 

@@ -49,6 +49,8 @@ _SIGNATURES = {
     "dlrsn_sk_scalar_len": (c_i64, [c_int, c_int]),
     "dlrsn_sweep_workspace_bytes": (c_i64, [c_int, c_int, c_int, c_int]),
     "dlrsn_sweep_workspace_init": (c_int, [c_vp, c_i64, c_vp]),
+    "dlrsn_debug_trace": (c_int, [c_vp, c_int]),
+    "dlrsn_debug_flags": (c_int, [c_int]),
     "dlrsn_linearize": (c_int, [c_int, c_vp, c_vp, c_vp, c_dbl, c_dbl, c_dbl, c_vp, c_vp,
                                 c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "dlrsn_update_temperature": (c_int, [c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_dbl, c_dbl,

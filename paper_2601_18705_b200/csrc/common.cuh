@@ -126,6 +126,11 @@ __device__ inline void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// warp-converged variant: every lane leaves the loop in the same iteration
+__device__ inline void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  while (!__all_sync(0xffffffffu, mbar_try_wait(bar, parity))) {
+  }
+}
 
 // deterministic block sum of NV doubles (fixed tree order); result in lane 0
 // of warp 0.  blockDim.x must be a multiple of 32 and <= 1024.

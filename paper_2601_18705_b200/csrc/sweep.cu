@@ -43,6 +43,23 @@ struct SweepArgs {
   int64_t vlen, slen;
 };
 
+// Debug timeline (dlrsn_debug_trace): per (item, chunk) globaltimer before
+// and after the handoff wait; null in production.
+__device__ unsigned long long* g_trace = nullptr;
+__device__ int g_trace_chunks = 0;
+__device__ int g_flags = 0;  // debug: bit0 = no speculative handoff prefetch
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // Empty handoff slot: a signalling NaN with a fixed payload.  Arithmetic only
 // produces quiet NaNs, so a swept value can never alias it.
 constexpr unsigned long long kEmpty = 0x7FF4DEADBEEFCAFEull;
@@ -196,14 +213,17 @@ sweep_kernel(const SweepArgs a) {
     // chunk h of the handoff: lane L < C*DW owns (column hC + L/DW, direction L%DW)
     const bool hlane = hin != nullptr && lane < C * DW;
     double2 h0 = make_double2(0.0, 0.0), h1 = h0, h2 = h0;
-    if (hlane && lane / DW < nx) h1 = __ldcg(hin + lane);
-    if (hlane && C + lane / DW < nx) h2 = __ldcg(hin + C * DW + lane);
+    const bool spec = (g_flags & 1) == 0;
+    if (!spec) h0 = h1 = h2 = make_double2(empty, empty);
+    if (spec && hlane && lane / DW < nx) h1 = __ldcg(hin + lane);
+    if (spec && hlane && C + lane / DW < nx) h2 = __ldcg(hin + C * DW + lane);
 
     double xin[DW][2], yin[DW][2];
 #pragma unroll
     for (int k = 0; k < DW; ++k) xin[k][0] = xin[k][1] = yin[k][0] = yin[k][1] = 0.0;
 
     for (int m = 0; m < nchunks; ++m) {
+      if (g_trace && lane == 0 && m < g_trace_chunks) g_trace[((int64_t)item * g_trace_chunks + m) * 4] = gtimer();
       if (lane == 0 && m + P - 1 < nchunks) {
         const int mm = m + P - 1;
         const int st = mm % P, t0 = mm * C;
@@ -219,30 +239,38 @@ sweep_kernel(const SweepArgs a) {
             tma_load_1d(buf + C * 160 + k * C * 128, a.rhs_sk + slot_off[k] + t0 * 128, n * 1024u,
                         &bars[wib][st]);
       }
+      unsigned long long* tr = g_trace;
+      if (tr && lane == 0 && m < g_trace_chunks) tr[((int64_t)item * g_trace_chunks + m) * 4 + 1] = gtimer();
       // y-inflow of lane 0 for this chunk's columns (strip below, via L2)
       h0 = h1;
       h1 = h2;
-      if (hlane && m < hchunks && m * C + lane / DW < nx) {
+      {
+        // Warp-uniform wait: every lane stays in the loop until all of this
+        // chunk's slots have arrived (a divergent per-lane spin measurably
+        // slowed the following compute 4x on sm_100a).
+        const bool need = hlane && m < hchunks && m * C + lane / DW < nx;
         double2* slot = hin + (int64_t)m * C * DW + lane;
         int spins = 0;
-        while (is_empty(h0.x) || is_empty(h0.y)) {
-          ++spins;
+        while (__any_sync(kFull, need && (is_empty(h0.x) || is_empty(h0.y)))) {
           __nanosleep(32);
-          h0 = __ldcv(slot);
-          if (spins > (1 << 26)) {  // report instead of hanging the GPU
-            atomicOr(a.status, 2);
+          if (need && (is_empty(h0.x) || is_empty(h0.y))) h0 = __ldcv(slot);
+          if (++spins > (1 << 26)) {  // report instead of hanging the GPU
+            if (need) atomicOr(a.status, 2);
             h0 = make_double2(0.0, 0.0);
           }
         }
-        __stcg(slot, make_double2(empty, empty));  // re-arm for the next launch
+        if (need) __stcg(slot, make_double2(empty, empty));  // re-arm for the next launch
       }
-      if (hlane && m + 2 < hchunks && (m + 2) * C + lane / DW < nx)
+      if (spec && hlane && m + 2 < hchunks && (m + 2) * C + lane / DW < nx)
         h2 = __ldcg(hin + (int64_t)(m + 2) * C * DW + lane);  // speculative prefetch
+      if (tr && lane == 0 && m < g_trace_chunks) tr[((int64_t)item * g_trace_chunks + m) * 4 + 2] = gtimer();
       {
         const int st = m % P;
-        mbar_wait(&bars[wib][st], (parity >> st) & 1u);
+        mbar_wait_warp(&bars[wib][st], (parity >> st) & 1u);
         parity ^= 1u << st;
       }
+      __syncwarp();
+      if (tr && lane == 0 && m < g_trace_chunks) tr[((int64_t)item * g_trace_chunks + m) * 4 + 3] = gtimer();
       const double* buf = ring + (m % P) * SD;
 
 #pragma unroll
@@ -255,7 +283,7 @@ sweep_kernel(const SweepArgs a) {
         for (int k = 0; k < DW; ++k) {
           const double y0 = __shfl_sync(kFull, h0.x, tt * DW + k);
           const double y1 = __shfl_sync(kFull, h0.y, tt * DW + k);
-          if (lane == 0 && hin != nullptr) { yin[k][0] = y0; yin[k][1] = y1; }
+          if (lane == 0 && hin != nullptr && (g_flags & 2) == 0) { yin[k][0] = y0; yin[k][1] = y1; }
         }
         double ytop[DW][2];
 #pragma unroll
@@ -583,6 +611,17 @@ int dlrsn_sk_to_canonical(const dlrsn_cellops* ops, int D, const int* quad, cons
   sk_to_canonical_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(
       ops->nx, ops->ny, D, quad, psi_sk, psi, ld, sk_vec_len(ops->nx, ops->ny));
   DLRSN_CHECK_LAUNCH("sk_to_canonical_kernel");
+  return DLRSN_OK;
+}
+
+int dlrsn_debug_flags(int flags) {
+  DLRSN_TRY_CUDA(cudaMemcpyToSymbol(g_flags, &flags, sizeof(int)));
+  return DLRSN_OK;
+}
+
+int dlrsn_debug_trace(unsigned long long* buf, int chunks) {
+  DLRSN_TRY_CUDA(cudaMemcpyToSymbol(g_trace, &buf, sizeof(buf)));
+  DLRSN_TRY_CUDA(cudaMemcpyToSymbol(g_trace_chunks, &chunks, sizeof(int)));
   return DLRSN_OK;
 }
 
