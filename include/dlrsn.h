@@ -192,7 +192,8 @@ int dlrsn_project(const dlrsn_cellops* ops, int r, const double* X, const double
                   const double* sigma_t, const double* sigma_s, const double* q, double* out,
                   double* partial, dlrsn_stream_t stream);
 
-/* G = R^T R (R upper) and R^-1; diag_ratio[k] = R_kk / max(sqrt(G_kk), 1)
+/* G = R^T R (R upper) and R^-1; diag_ratio (2r): [k] = R_kk / sqrt(G_kk)
+ * (relative norm left after projection), [r+k] = R_kk / max(sqrt(G_kk), 1)
  * (the CGS2 deficiency quantity of angular.py:137); *flag = 1 on a
  * non-positive pivot.  r <= 128. */
 int dlrsn_chol_upper(int r, const double* G, double* R, double* Rinv, double* diag_ratio,
@@ -226,16 +227,18 @@ int dlrsn_what_solve(int r, int m, const double* Lhat, const double* U, const do
                      double* X, int mode, dlrsn_stream_t stream);
 
 /* Exact twice-projected classical Gram-Schmidt with the reference's
- * deficiency test and deterministic completion (angular.py:104-160).
- * metric 0: weighted (w, angular); 1: block mass (ops, spatial).
- * comp_kind 0: ncomp angular monomials (exponent triples, coords = omegas
- * n x 3) then unit vectors; 1: spatial monomials (exponent pairs, coords =
- * extent x0,y0,lx,ly).  work: n doubles; coef: 2m doubles; *status = 1 if
- * the candidates ran out (strict). */
+ * deficiency test and deterministic completion (angular.py:104-160), one
+ * cooperative grid launch.  metric 0: weighted rows (w, angular); 1: block
+ * mass (ops, spatial, n = 4*cells).  comp_kind 0: ncomp angular monomials
+ * (exponent triples, coords = omegas n x 3) then unit vectors; 1: spatial
+ * monomials (exponent pairs, coords = extent x0,y0,lx,ly).  workspace:
+ * dlrsn_cgs2_workspace_len(n) doubles; *status = 1 if the candidates ran
+ * out (strict). */
+int64_t dlrsn_cgs2_workspace_len(int n);
 int dlrsn_cgs2(int n, int m, const double* cols, int ldc, double* Q, int ldq, double* R,
                int* deficient, int metric, const double* w, const dlrsn_cellops* ops,
-               int comp_kind, int ncomp, const int* comp_exp, const double* coords, double* work,
-               double* coef, int* status, int strict, dlrsn_stream_t stream);
+               int comp_kind, int ncomp, const int* comp_exp, const double* coords,
+               double* workspace, int* status, int strict, dlrsn_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -78,8 +78,9 @@ _SIGNATURES = {
     "dlrsn_row_combine": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "dlrsn_deim": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "dlrsn_what_solve": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp]),
+    "dlrsn_cgs2_workspace_len": (c_i64, [c_int]),
     "dlrsn_cgs2": (c_int, [c_int, c_int, c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_int, c_vp, c_vp,
-                           c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp]),
+                           c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp]),
 }
 
 _lib = None

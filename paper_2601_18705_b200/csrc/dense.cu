@@ -46,13 +46,24 @@ __global__ void rowmix_kernel(int n, int kx, int ky, const double* __restrict__ 
 // ---------------------------------------------------------------------------
 // Partial-sum plumbing: kernels that reduce over cells write one partial per
 // (chunk, output) and reduce_partials sums them in chunk order.
+// block = 32 consecutive outputs x 8 warps; warp w sums chunks w, w+8, ...
+// (coalesced), then the 8 warp sums are added in fixed order.
 __global__ void reduce_partials_kernel(int nchunks, int64_t len, const double* __restrict__ part,
                                        double* __restrict__ out, double alpha) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= len) return;
+  __shared__ double red[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t e = (int64_t)blockIdx.x * 32 + lane;
   double s = 0.0;
-  for (int c = 0; c < nchunks; ++c) s += part[(int64_t)c * len + e];
-  out[e] = alpha * s;
+  if (e < len)
+    for (int c = w; c < nchunks; c += 8) s += part[(int64_t)c * len + e];
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && e < len) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t += red[q][lane];
+    out[e] = alpha * t;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -257,32 +268,31 @@ __global__ void project_kernel(ProjArgs pa, dlrsn_cellops ops) {
     }
   }
   // right / top boundary faces of the cells in this block's range
-  // (a = this cell's right/top edge trace, b = 0)
-  for (int c = c_begin; c < c_end; ++c) {
-    const int ci = c % nx, cj = c / nx;
-    const bool right = ci == nx - 1, top = cj == pa.ny - 1;
-    if (!right && !top) continue;
+  // (a = this cell's right/top edge trace, b = 0); enumerate only those cells
+  {
     const int i = i0 + ti, j = j0 + tj;
-    if (i >= r || j >= r) continue;
-    if (right) {
-      double ai0, ai1, aj0, aj1;
-      edge_pair(pa.X, r, c, 1, 3, i, ai0, ai1);
-      edge_pair(pa.X, r, c, 1, 3, j, aj0, aj1);
-      const double f0 = 0.5 * (ops.e2x[0] * aj0 + ops.e2x[1] * aj1);
-      const double f1 = 0.5 * (ops.e2x[2] * aj0 + ops.e2x[3] * aj1);
-      const double val = ai0 * f0 + ai1 * f1;
-      acc[0] += val;
-      acc[2] += val;
-    }
-    if (top) {
-      double ai0, ai1, aj0, aj1;
-      edge_pair(pa.X, r, c, 2, 3, i, ai0, ai1);
-      edge_pair(pa.X, r, c, 2, 3, j, aj0, aj1);
-      const double f0 = 0.5 * (ops.e2y[0] * aj0 + ops.e2y[1] * aj1);
-      const double f1 = 0.5 * (ops.e2y[2] * aj0 + ops.e2y[3] * aj1);
-      const double val = ai0 * f0 + ai1 * f1;
-      acc[1] += val;
-      acc[3] += val;
+    if (i < r && j < r) {
+      const int first_right = c_begin + ((nx - 1 - c_begin % nx) % nx + nx) % nx;
+      for (int c = first_right; c < c_end; c += nx) {
+        double ai0, ai1, aj0, aj1;
+        edge_pair(pa.X, r, c, 1, 3, i, ai0, ai1);
+        edge_pair(pa.X, r, c, 1, 3, j, aj0, aj1);
+        const double f0 = 0.5 * (ops.e2x[0] * aj0 + ops.e2x[1] * aj1);
+        const double f1 = 0.5 * (ops.e2x[2] * aj0 + ops.e2x[3] * aj1);
+        const double val = ai0 * f0 + ai1 * f1;
+        acc[0] += val;
+        acc[2] += val;
+      }
+      for (int c = max(c_begin, (pa.ny - 1) * nx); c < c_end; ++c) {
+        double ai0, ai1, aj0, aj1;
+        edge_pair(pa.X, r, c, 2, 3, i, ai0, ai1);
+        edge_pair(pa.X, r, c, 2, 3, j, aj0, aj1);
+        const double f0 = 0.5 * (ops.e2y[0] * aj0 + ops.e2y[1] * aj1);
+        const double f1 = 0.5 * (ops.e2y[2] * aj0 + ops.e2y[3] * aj1);
+        const double val = ai0 * f0 + ai1 * f1;
+        acc[1] += val;
+        acc[3] += val;
+      }
     }
   }
   const int i = i0 + ti, j = j0 + tj;
@@ -323,9 +333,12 @@ __global__ void chol_upper_kernel(int r, const double* __restrict__ G, double* _
         bad = 1;
         a[k * r + k] = 0.0;
         diag_ratio[k] = 0.0;
+        diag_ratio[r + k] = 0.0;
       } else {
         a[k * r + k] = sqrt(d);
-        diag_ratio[k] = a[k * r + k] / fmax(sqrt(fmax(g, 0.0)), 1.0);
+        const double on = sqrt(fmax(g, 0.0));
+        diag_ratio[k] = on > 0.0 ? a[k * r + k] / on : 0.0;
+        diag_ratio[r + k] = a[k * r + k] / fmax(on, 1.0);
       }
     }
     __syncthreads();
@@ -570,7 +583,7 @@ __global__ void deim_kernel(int n, int r, double* __restrict__ Wk /* n x r work 
   double mx = 0.0;
   for (int64_t e = threadIdx.x; e < (int64_t)n * r; e += blockDim.x) {
     const double v = W[e];
-    Wk[e] = v;
+    Wk[(e % r) * n + e / r] = v;  // column-major work copy (coalesced column access)
     mx = fmax(mx, fabs(v));
   }
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_down_sync(kFull, mx, o));
@@ -589,7 +602,7 @@ __global__ void deim_kernel(int n, int r, double* __restrict__ Wk /* n x r work 
     double best = -1.0;
     int bidx = 0x7fffffff;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const double v = fabs(Wk[(int64_t)i * r + j]);
+      const double v = fabs(Wk[(int64_t)j * n + i]);
       if (v > best || (v == best && i < bidx)) { best = v; bidx = i; }
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -606,7 +619,7 @@ __global__ void deim_kernel(int n, int r, double* __restrict__ Wk /* n x r work 
       for (int q = 0; q < (int)(blockDim.x >> 5); ++q)
         if (bv[q] > b || (bv[q] == b && bi[q] < ii)) { b = bv[q]; ii = bi[q]; }
       pick = ii;
-      pval = Wk[(int64_t)ii * r + j];
+      pval = Wk[(int64_t)j * n + ii];
       if (!(fabs(pval) > floor_)) fail = j;
       for (int q = 0; q < j; ++q)
         if (idx[q] == ii) fail = j;
@@ -617,13 +630,13 @@ __global__ void deim_kernel(int n, int r, double* __restrict__ Wk /* n x r work 
     const int p = pick;
     const double pv = pval;
     // U row j = pivot row of the current (updated) matrix, columns j..r-1
-    for (int k = threadIdx.x; k < r; k += blockDim.x) U[j * r + k] = k >= j ? Wk[(int64_t)p * r + k] : 0.0;
+    for (int k = threadIdx.x; k < r; k += blockDim.x) U[j * r + k] = k >= j ? Wk[(int64_t)k * n + p] : 0.0;
     __syncthreads();
     // l = col / pivot; trailing update W[:, k] -= l * W[p, k] for k > j
     for (int64_t e = threadIdx.x; e < (int64_t)n; e += blockDim.x) {
-      const double l = Wk[e * r + j] / pv;
-      Wk[e * r + j] = l;  // keep the multiplier column
-      for (int k = j + 1; k < r; ++k) Wk[e * r + k] -= l * U[j * r + k];
+      const double l = Wk[(int64_t)j * n + e] / pv;
+      Wk[(int64_t)j * n + e] = l;  // keep the multiplier column
+      for (int k = j + 1; k < r; ++k) Wk[(int64_t)k * n + e] -= l * U[j * r + k];
     }
     __syncthreads();
   }
@@ -634,7 +647,7 @@ __global__ void deim_kernel(int n, int r, double* __restrict__ Wk /* n x r work 
   // Lhat[q, j] = multiplier of column j at the q-th picked row (unit lower)
   for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
     const int q = e / r, j = e % r;
-    Lhat[e] = j < q ? Wk[(int64_t)idx[q] * r + j] : (j == q ? 1.0 : 0.0);
+    Lhat[e] = j < q ? Wk[(int64_t)j * n + idx[q]] : (j == q ? 1.0 : 0.0);
   }
   if (threadIdx.x == 0) *err_col = -1;
 }
@@ -674,166 +687,6 @@ __global__ void what_solve_kernel(int r, int m, const double* __restrict__ Lhat,
   }
 }
 
-// ---------------------------------------------------------------------------
-// Exact twice-projected classical Gram-Schmidt (angular.py:104-160) in one
-// CTA.  metric 0: <u,v> = sum_d w_d u_d v_d (angular, n rows); metric 1:
-// <u,v> = sum_c u_c^T M v_c (spatial, n = 4*cells).  Completion candidates
-// (only when a column is deficient): comp_kind 0 = the first ncomp angular
-// monomials given by exponent triples (omega x,y,z) then unit vectors;
-// comp_kind 1 = spatial monomials xh^a yh^b with exponent pairs, no unit
-// vectors.  Q / R / deficient flags out; *status = 1 if candidates ran out.
-struct Cgs2Args {
-  int n, m;
-  const double* cols;
-  int ldc;
-  double* Q;
-  int ldq;
-  double* R;         // m x m
-  int* deficient;    // m flags
-  int metric;
-  const double* w;   // metric 0 weights (n)
-  dlrsn_cellops ops; // metric 1 mass
-  int comp_kind;
-  int ncomp;
-  const int* comp_exp;   // 3 per candidate (kind 0) or 2 (kind 1)
-  const double* coords;  // kind 0: omegas (n x 3); kind 1: extent (x0,y0,lx,ly)
-  double* work;          // n doubles (current vector)
-  double* coef;          // m doubles
-  int* status;
-  int strict;
-};
-
-__device__ double cta_sum(double v, double* red) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(kFull, v, o);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) red[w] = v;
-  __syncthreads();
-  double s = 0.0;
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) s += red[q];
-    red[32] = s;
-  }
-  __syncthreads();
-  return red[32];
-}
-
-// <a, b> with a = column of Q (or the work vector), b = work vector
-__device__ double cgs_dot(const Cgs2Args& g, const double* a, int lda, const double* b, int ldb,
-                          double* red) {
-  double s = 0.0;
-  if (g.metric == 0) {
-    for (int i = threadIdx.x; i < g.n; i += blockDim.x) s += g.w[i] * a[(int64_t)i * lda] * b[(int64_t)i * ldb];
-  } else {
-    for (int c = threadIdx.x; c < g.n / 4; c += blockDim.x) {
-      double mb[4];
-#pragma unroll
-      for (int l = 0; l < 4; ++l) {
-        mb[l] = 0.0;
-#pragma unroll
-        for (int p = 0; p < 4; ++p) mb[l] += g.ops.mass[4 * l + p] * b[(int64_t)(4 * c + p) * ldb];
-      }
-#pragma unroll
-      for (int l = 0; l < 4; ++l) s += a[(int64_t)(4 * c + l) * lda] * mb[l];
-    }
-  }
-  return cta_sum(s, red);
-}
-
-__device__ double cand_value(const Cgs2Args& g, int k, int i) {
-  if (g.comp_kind == 0) {
-    if (k < g.ncomp) {
-      const double* o = g.coords + 3 * (int64_t)i;
-      const int* e = g.comp_exp + 3 * k;
-      double v = 1.0;
-      for (int p = 0; p < e[0]; ++p) v *= o[0];
-      double vy = 1.0;
-      for (int p = 0; p < e[1]; ++p) vy *= o[1];
-      double vz = 1.0;
-      for (int p = 0; p < e[2]; ++p) vz *= o[2];
-      return v * vy * vz;
-    }
-    return (k - g.ncomp) == i ? 1.0 : 0.0;
-  }
-  // spatial monomials at dof i: corner coordinates of cell i/4
-  const int c = i >> 2, l = i & 3;
-  const int nx = g.ops.nx;
-  const double x = g.ops.x0 + (c % nx) * g.ops.dx + (l & 1) * g.ops.dx;
-  const double y = g.ops.y0 + (c / nx) * g.ops.dy + (l >> 1) * g.ops.dy;
-  const double xh = 2.0 * (x - g.coords[0]) / g.coords[2] - 1.0;
-  const double yh = 2.0 * (y - g.coords[1]) / g.coords[3] - 1.0;
-  const int* e = g.comp_exp + 2 * k;
-  double v = 1.0;
-  for (int p = 0; p < e[0]; ++p) v *= xh;
-  double vy = 1.0;
-  for (int p = 0; p < e[1]; ++p) vy *= yh;
-  return v * vy;
-}
-
-// two projection passes of work against Q[:, :k]; accumulates into coef
-__device__ void cgs_project_twice(const Cgs2Args& g, int k, double* red, bool keep) {
-  for (int pass = 0; pass < 2; ++pass) {
-    for (int i = 0; i < k; ++i) {
-      const double c = cgs_dot(g, g.Q + i, g.ldq, g.work, 1, red);
-      if (threadIdx.x == 0) g.coef[i] = (pass == 0 || !keep) ? c : g.coef[i] + c;
-      // keep a copy for this pass's update (classical: all coefficients
-      // from the same vector), stored after the first m entries
-      if (threadIdx.x == 0) g.coef[g.m + i] = c;
-    }
-    __syncthreads();
-    for (int64_t r = threadIdx.x; r < g.n; r += blockDim.x) {
-      double v = g.work[r];
-      for (int i = 0; i < k; ++i) v -= g.Q[r * g.ldq + i] * g.coef[g.m + i];
-      g.work[r] = v;
-    }
-    __syncthreads();
-  }
-}
-
-__global__ void cgs2_kernel(Cgs2Args g) {
-  __shared__ double red[33];
-  const double tol = 1e-12;  // DEFICIENCY_TOL, angular.py:24
-  int next_cand = 0;
-  const int max_cand = g.comp_kind == 0 ? g.ncomp + g.n : g.ncomp;
-  for (int k = 0; k < g.m; ++k) {
-    for (int64_t r = threadIdx.x; r < g.n; r += blockDim.x) g.work[r] = g.cols[r * g.ldc + k];
-    __syncthreads();
-    const double orig = sqrt(fmax(cgs_dot(g, g.work, 1, g.work, 1, red), 0.0));
-    cgs_project_twice(g, k, red, true);
-    const double nrm = sqrt(fmax(cgs_dot(g, g.work, 1, g.work, 1, red), 0.0));
-    for (int i = threadIdx.x; i < g.m; i += blockDim.x) g.R[i * g.m + k] = i < k ? g.coef[i] : 0.0;
-    __syncthreads();
-    if (nrm <= tol * fmax(orig, 1.0)) {
-      if (threadIdx.x == 0) g.deficient[k] = 1;
-      bool placed = false;
-      while (next_cand < max_cand) {
-        const int cand = next_cand++;
-        for (int64_t r = threadIdx.x; r < g.n; r += blockDim.x) g.work[r] = cand_value(g, cand, (int)r);
-        __syncthreads();
-        const double c0 = sqrt(fmax(cgs_dot(g, g.work, 1, g.work, 1, red), 0.0));
-        cgs_project_twice(g, k, red, false);
-        const double c1 = sqrt(fmax(cgs_dot(g, g.work, 1, g.work, 1, red), 0.0));
-        if (c1 > sqrt(tol) * fmax(c0, 1.0)) {
-          for (int64_t r = threadIdx.x; r < g.n; r += blockDim.x) g.Q[r * g.ldq + k] = g.work[r] / c1;
-          placed = true;
-          break;
-        }
-      }
-      if (!placed) {
-        if (threadIdx.x == 0 && g.strict) *g.status = 1;
-        for (int64_t r = threadIdx.x; r < g.n; r += blockDim.x) g.Q[r * g.ldq + k] = 0.0;
-      }
-    } else {
-      if (threadIdx.x == 0) {
-        g.deficient[k] = 0;
-        g.R[k * g.m + k] = nrm;
-      }
-      for (int64_t r = threadIdx.x; r < g.n; r += blockDim.x) g.Q[r * g.ldq + k] = g.work[r] / nrm;
-    }
-    __syncthreads();
-  }
-}
-
 }  // namespace dlrsn
 
 using namespace dlrsn;
@@ -859,10 +712,19 @@ int dlrsn_rowmix(int64_t n, int kx, int ky, const double* X, int ldx, const doub
   return DLRSN_OK;
 }
 
+// cells per block of the cell-reduction kernels: about 4 CTAs per SM in
+// total over all output tiles, in whole smem chunks
+static int cells_per_block(int ncell, int tiles) {
+  const int target = (4 * 148 + tiles - 1) / tiles;
+  int cpb = (ncell + target - 1) / target;
+  cpb = (cpb + kChunk - 1) / kChunk * kChunk;
+  return cpb < kChunk ? kChunk : cpb;
+}
+
 int64_t dlrsn_partials_len(int ncell, int ra, int rb, int kind) {
-  // upper bound on the partial buffer (doubles) for mgram (kind 0) /
-  // project (kind 1) with the default chunking
-  const int cpb = 1024;
+  // partial buffer (doubles) for mgram (kind 0) / project (kind 1)
+  const int tiles = ((ra + kTile - 1) / kTile) * ((rb + kTile - 1) / kTile);
+  const int cpb = cells_per_block(ncell, tiles);
   const int64_t nblk = (ncell + cpb - 1) / cpb;
   return kind == 0 ? nblk * ra * rb : nblk * (7 * (int64_t)ra * ra + ra);
 }
@@ -871,15 +733,15 @@ int dlrsn_mgram(const dlrsn_cellops* ops, int ra, int rb, const double* A, int l
                 const double* B, int ldb, const double* coeff, double* G, double* partial,
                 dlrsn_stream_t stream) {
   const int ncell = ops->nx * ops->ny;
-  const int cpb = 1024;
-  const int nblk = (ncell + cpb - 1) / cpb;
   const int tiles = ((ra + kTile - 1) / kTile) * ((rb + kTile - 1) / kTile);
+  const int cpb = cells_per_block(ncell, tiles);
+  const int nblk = (ncell + cpb - 1) / cpb;
   cudaStream_t st = as_stream(stream);
   mgram_kernel<<<dim3(nblk, tiles), kTile * kTile, 0, st>>>(ncell, ra, rb, A, lda, B, ldb, coeff,
                                                             *ops, cpb, partial);
   DLRSN_CHECK_LAUNCH("mgram_kernel");
   const int64_t len = (int64_t)ra * rb;
-  reduce_partials_kernel<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(nblk, len, partial, G, 1.0);
+  reduce_partials_kernel<<<(unsigned)((len + 31) / 32), 256, 0, st>>>(nblk, len, partial, G, 1.0);
   DLRSN_CHECK_LAUNCH("reduce_partials_kernel");
   return DLRSN_OK;
 }
@@ -888,9 +750,9 @@ int dlrsn_project(const dlrsn_cellops* ops, int r, const double* X, const double
                   const double* sigma_t, const double* sigma_s, const double* q, double* out,
                   double* partial, dlrsn_stream_t stream) {
   const int ncell = ops->nx * ops->ny;
-  const int cpb = 1024;
-  const int nblk = (ncell + cpb - 1) / cpb;
   const int tiles = ((r + kTile - 1) / kTile) * ((r + kTile - 1) / kTile);
+  const int cpb = cells_per_block(ncell, tiles);
+  const int nblk = (ncell + cpb - 1) / cpb;
   ProjArgs pa;
   pa.nx = ops->nx; pa.ny = ops->ny; pa.r = r;
   pa.X = X; pa.Xold = Xold; pa.sigma_t = sigma_t; pa.sigma_s = sigma_s; pa.q = q;
@@ -901,7 +763,7 @@ int dlrsn_project(const dlrsn_cellops* ops, int r, const double* X, const double
   project_kernel<<<dim3(nblk, tiles), kTile * kTile, 0, st>>>(pa, *ops);
   DLRSN_CHECK_LAUNCH("project_kernel");
   const int64_t len = 7 * (int64_t)r * r + r;
-  reduce_partials_kernel<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(nblk, len, partial, out, 1.0);
+  reduce_partials_kernel<<<(unsigned)((len + 31) / 32), 256, 0, st>>>(nblk, len, partial, out, 1.0);
   DLRSN_CHECK_LAUNCH("reduce_partials_kernel");
   return DLRSN_OK;
 }
@@ -957,21 +819,6 @@ int dlrsn_what_solve(int r, int m, const double* Lhat, const double* U, const do
                      double* X, int mode, dlrsn_stream_t stream) {
   what_solve_kernel<<<1, 128, 0, as_stream(stream)>>>(r, m, Lhat, U, V, X, mode);
   DLRSN_CHECK_LAUNCH("what_solve_kernel");
-  return DLRSN_OK;
-}
-
-int dlrsn_cgs2(int n, int m, const double* cols, int ldc, double* Q, int ldq, double* R,
-               int* deficient, int metric, const double* w, const dlrsn_cellops* ops,
-               int comp_kind, int ncomp, const int* comp_exp, const double* coords, double* work,
-               double* coef, int* status, int strict, dlrsn_stream_t stream) {
-  Cgs2Args g;
-  g.n = n; g.m = m; g.cols = cols; g.ldc = ldc; g.Q = Q; g.ldq = ldq; g.R = R;
-  g.deficient = deficient; g.metric = metric; g.w = w;
-  if (ops) g.ops = *ops; else memset(&g.ops, 0, sizeof(g.ops));
-  g.comp_kind = comp_kind; g.ncomp = ncomp; g.comp_exp = comp_exp; g.coords = coords;
-  g.work = work; g.coef = coef; g.status = status; g.strict = strict;
-  cgs2_kernel<<<1, 1024, 0, as_stream(stream)>>>(g);
-  DLRSN_CHECK_LAUNCH("cgs2_kernel");
   return DLRSN_OK;
 }
 

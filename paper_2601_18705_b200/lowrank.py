@@ -23,10 +23,10 @@ from .errors import ContractViolation, InterpolationError, SolverError
 from .mesh import cellops_struct
 
 FOUR_PI = 4.0 * np.pi
-# CholQR2 is used when every column keeps at least this much of its M-norm
+# CholQR2 is used when every column keeps at least this fraction of its M-norm
 # after projection (first-pass Cholesky); otherwise the exact CGS2 path with
 # the reference's deficiency rule (1e-12, angular.py:137) decides.
-CHOLQR_GUARD = 1e-5
+CHOLQR_GUARD = 1e-6
 
 
 def _i32(n):
@@ -100,7 +100,7 @@ def spatial_monomial_exponents(count):
 
 def _chol(G):
     r = G.shape[0]
-    R, Rinv, ratio = empty(r, r), empty(r, r), empty(r)
+    R, Rinv, ratio = empty(r, r), empty(r, r), empty(2 * r)
     flag = _i32(1)
     _lib.call("dlrsn_chol_upper", r, _lib.ptr(G), _lib.ptr(R), _lib.ptr(Rinv), _lib.ptr(ratio),
               _lib.ptr(flag), stream())
@@ -127,7 +127,12 @@ def gram_schmidt_mass(ops, columns, completion_count=None, strict=True, method="
         G = mass_gram(co, cols)
         R1, R1inv, ratio, flag = _chol(G)
         host = torch.cat([ratio, flag.to(torch.float64)]).cpu().numpy()
-        if host[-1] == 0 and float(host[:-1].min(initial=np.inf)) >= CHOLQR_GUARD:
+        rel, dec = host[:m], host[m:2 * m]
+        # CholQR's R_kk is accurate to ~eps/rel^2: trust it when every column
+        # keeps rel >= CHOLQR_GUARD of its norm and sits far (100x) above the
+        # reference's deficiency threshold 1e-12 * max(orig, 1)
+        if (host[-1] == 0 and float(rel.min(initial=np.inf)) >= CHOLQR_GUARD
+                and float(dec.min(initial=np.inf)) >= 1e-10):
             X1 = rowmix(cols, R1inv)
             R2, R2inv, _, _ = _chol(mass_gram(co, X1))
             X = rowmix(X1, R2inv)
@@ -144,14 +149,13 @@ def _cgs2(n, m, cols, *, metric, ops=None, weights=None, comp_kind, comp_exp, co
     R = zeros(m, m)
     defi = _i32(max(m, 1))
     status = _i32(1)
-    work = empty(max(n, 1))
-    coef = empty(2 * max(m, 1))
+    work = empty(int(_lib.load().dlrsn_cgs2_workspace_len(n)))
     ncomp = comp_exp.shape[0]
     exp_dev = as_device(comp_exp.reshape(-1), dtype=torch.int32) if ncomp else _i32(1)
     _lib.call("dlrsn_cgs2", n, m, _lib.ptr(cols), cols.stride(0), _lib.ptr(Q), m, _lib.ptr(R),
               _lib.ptr(defi), metric, _lib.ptr(weights), None if ops is None else _addr(ops),
               comp_kind, ncomp, _lib.ptr(exp_dev), _lib.ptr(as_device(coords)), _lib.ptr(work),
-              _lib.ptr(coef), _lib.ptr(status), int(bool(strict)), stream())
+              _lib.ptr(status), int(bool(strict)), stream())
     flags = defi[:m].cpu().numpy()
     if int(status.item()) != 0:
         raise ContractViolation("ran out of completion vectors during orthonormalization")
