@@ -187,9 +187,13 @@ def main():
     T = torch.as_tensor(spec.T0, device="cuda").clone()
     lin = dp.linearized(T)
 
+    from paper_2601_18705_b200.sharding import DirectionComm
+
+    comm = DirectionComm.from_default_group()  # None at N=1; NCCL direction sharding at N>1
+
     def one_step(state, lin):
         state, info = step_collocation(dp.grid, lin, dp.quad, state, si_tol=1e-8, use_dsa=False,
-                                       check_state=True)
+                                       check_state=True, comm=comm)
         lin = dp.advance(lin, info.phi, T)
         return state, lin, info
 
@@ -243,10 +247,10 @@ def main():
             traffic = None
 
     # ---- end-to-end: public API with HOST (pinned) buffers each step -------
-    e2e = measure_e2e(dp, state, T, lin, max(1, min(args.steps, 5)))
+    e2e = measure_e2e(dp, state, T, lin, max(1, min(args.steps, 5)), comm)
 
     # ---- full-SN comparison sweep (config 2: all 1024 directions) ----------
-    full = measure_full_sn(dp) if args.full_sn else None
+    full = measure_full_sn(dp, comm) if args.full_sn else None
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -283,7 +287,7 @@ def main():
         torch.distributed.destroy_process_group()
 
 
-def measure_e2e(dp, state, T, lin, n):
+def measure_e2e(dp, state, T, lin, n, comm=None):
     """Same step through the public API with the state and per-cell fields
     in pinned HOST memory: H2D of X, S, W, T and the step coefficients,
     step_collocation, D2H of the new X, S, W and T every step."""
@@ -314,7 +318,8 @@ def measure_e2e(dp, state, T, lin, n):
         dl = {f: v.to("cuda", non_blocking=True) for f, v in hlin.items()}
         st = DlrState(X=X, S=S, W=AngularBasis(values=W).bind(dp.quad))
         step = LinearizedStep(dt=lin.dt, inv_cdt=lin.inv_cdt, constants=lin.constants, **dl)
-        new, info = step_collocation(dp.grid, step, dp.quad, st, si_tol=1e-8, use_dsa=False)
+        new, info = step_collocation(dp.grid, step, dp.quad, st, si_tol=1e-8, use_dsa=False,
+                                     comm=comm)
         Tn = dp.advance(step, info.phi, dl["T0"].clone())
         out["X"].copy_(new.X, non_blocking=True)
         out["S"].copy_(new.S, non_blocking=True)
@@ -330,7 +335,7 @@ def measure_e2e(dp, state, T, lin, n):
             "steps": n, "ms_per_step": ms / n}
 
 
-def measure_full_sn(dp, reps=3):
+def measure_full_sn(dp, comm=None, reps=3):
     """Config 2's full-SN comparison sweep: one source-iteration sweep over
     all 1024 quadrature directions (closure = quadrature weights) on the
     280x280 grid, psi stored (64 B/cell-angle algorithmic)."""
@@ -342,10 +347,16 @@ def measure_full_sn(dp, reps=3):
     lin = dp.linearized(T)
     ops = transport.assemble_operators(dp.grid, lin)
     quad = dp.quad
-    plan = transport._SweepPlan(ops, quad.omegas, quad.weights)
-    vl = ops.vec_len
     D = quad.n_angles
-    rhs = torch.rand(D * vl, dtype=torch.float64, device="cuda")
+    mine = np.arange(D)
+    if comm is not None:
+        from paper_2601_18705_b200.sharding import partition_directions
+
+        mine = partition_directions(quad.omegas, comm.world_size)[comm.rank]
+    plan = transport._SweepPlan(ops, quad.omegas[mine], quad.weights[mine])
+    vl = ops.vec_len
+    Dl = len(mine)
+    rhs = torch.rand(Dl * vl, dtype=torch.float64, device="cuda")
     psi = torch.empty_like(rhs)
     part = torch.empty(plan.G * vl, dtype=torch.float64, device="cuda")
     scat = torch.zeros(4 * vl, dtype=torch.float64, device="cuda")
@@ -359,6 +370,8 @@ def measure_full_sn(dp, reps=3):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
+    if comm is not None:
+        ms = comm.max_scalar(ms)
     nc = dp.grid.n_cells
     alg = nc * (D * SWEEP_BYTES_PER_CELL_ANGLE + SWEEP_BYTES_PER_CELL)
     peak, _ = _peaks()

@@ -148,6 +148,13 @@ int dlrsn_phi_combine(const dlrsn_cellops* ops, int G, const dlrsn_group* groups
                       double* phi_new, double* scat_sk4, double* norms, void* partial_ws,
                       dlrsn_stream_t stream);
 
+/* Direction-sharded iteration (multi-GPU): phi_new is the rank-summed
+ * closure flux (canonical); norms against phi_old and the next scattering
+ * source, as dlrsn_phi_combine does for the unsharded case. */
+int dlrsn_phi_finish(const dlrsn_cellops* ops, const double* phi_new, const double* phi_old,
+                     const double* sigma_s, double* scat_sk4, double* norms, void* partial_ws,
+                     dlrsn_stream_t stream);
+
 /* psi (n_dofs, ld) canonical <- psi_sk[d] for d < D */
 int dlrsn_sk_to_canonical(const dlrsn_cellops* ops, int D, const int* quad,
                           const double* psi_sk, double* psi, int ld, dlrsn_stream_t stream);

@@ -64,6 +64,7 @@ _SIGNATURES = {
     "dlrsn_scatter_source": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "dlrsn_phi_combine": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                   c_vp]),
+    "dlrsn_phi_finish": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "dlrsn_sk_to_canonical": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp, c_int, c_vp]),
     "dlrsn_sweep": (c_int, [c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64,
                             c_int, c_vp]),
@@ -126,7 +127,7 @@ def check(status, what=""):
 _KERNELS_PER_CALL = {
     "dlrsn_linearize": 1, "dlrsn_update_temperature": 1, "dlrsn_advance_relinearize": 1,
     "dlrsn_rhs_build": 1, "dlrsn_cells_to_sk4": 1, "dlrsn_scatter_source": 1,
-    "dlrsn_phi_combine": 1, "dlrsn_sk_to_canonical": 1, "dlrsn_sweep": 1,
+    "dlrsn_phi_combine": 1, "dlrsn_phi_finish": 1, "dlrsn_sk_to_canonical": 1, "dlrsn_sweep": 1,
     "dlrsn_sweep_workspace_init": 1, "dlrsn_rowmix": 1, "dlrsn_mgram": 2, "dlrsn_project": 2,
     "dlrsn_chol_upper": 1, "dlrsn_small_matmul": 1, "dlrsn_row_inverse": 1,
     "dlrsn_row_combine": 1, "dlrsn_deim": 1, "dlrsn_what_solve": 1, "dlrsn_cgs2": 1,

@@ -503,6 +503,52 @@ __global__ void phi_combine_kernel(dlrsn_cellops ops, int G, const dlrsn_group* 
   }
 }
 
+// Sharded iteration: phi (canonical) already summed over ranks; compute the
+// convergence norms against phi_old and the next scattering source.
+__global__ void phi_finish_kernel(dlrsn_cellops ops, const double* __restrict__ phi_new,
+                                  const double* __restrict__ phi_old,
+                                  const double* __restrict__ ss, double* __restrict__ scat,
+                                  int64_t vlen, double* norms, double* partials,
+                                  unsigned* counter) {
+  __shared__ double red[64];
+  __shared__ bool last;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  double v[2] = {0.0, 0.0};
+  if (c < ops.nx * ops.ny) {
+    double p[4], po[4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      p[l] = phi_new[4 * c + l];
+      po[l] = phi_old[4 * c + l];
+      const double d = p[l] - po[l];
+      v[0] += d * d;
+      v[1] += p[l] * p[l];
+    }
+    if (scat) write_scat4(ops, c, p, ss[c], scat, vlen);
+  }
+  block_sum<2>(v, red);
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = v[0];
+    partials[2 * blockIdx.x + 1] = v[1];
+    __threadfence();
+    last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    double w[2] = {0.0, 0.0};
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+      w[0] += __ldcg(partials + 2 * b);
+      w[1] += __ldcg(partials + 2 * b + 1);
+    }
+    block_sum<2>(w, red);
+    if (threadIdx.x == 0) {
+      norms[0] = w[0];
+      norms[1] = w[1];
+      *counter = 0u;
+    }
+  }
+}
+
 __global__ void sk_to_canonical_kernel(int nx, int ny, int D, const int* __restrict__ quad,
                                        const double* __restrict__ sk, double* __restrict__ psi,
                                        int ld, int64_t vlen) {
@@ -601,6 +647,20 @@ int dlrsn_phi_combine(const dlrsn_cellops* ops, int G, const dlrsn_group* groups
                                                         sk_vec_len(ops->nx, ops->ny), norms,
                                                         partials, counter);
   DLRSN_CHECK_LAUNCH("phi_combine_kernel");
+  return DLRSN_OK;
+}
+
+int dlrsn_phi_finish(const dlrsn_cellops* ops, const double* phi_new, const double* phi_old,
+                     const double* sigma_s, double* scat_sk4, double* norms, void* partial_ws,
+                     dlrsn_stream_t stream) {
+  const int n = ops->nx * ops->ny;
+  const int nb = (n + 255) / 256;
+  unsigned* counter = reinterpret_cast<unsigned*>(partial_ws);
+  double* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(partial_ws) + 256);
+  phi_finish_kernel<<<nb, 256, 0, as_stream(stream)>>>(*ops, phi_new, phi_old, sigma_s, scat_sk4,
+                                                       sk_vec_len(ops->nx, ops->ny), norms,
+                                                       partials, counter);
+  DLRSN_CHECK_LAUNCH("phi_finish_kernel");
   return DLRSN_OK;
 }
 

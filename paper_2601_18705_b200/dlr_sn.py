@@ -104,7 +104,7 @@ def project_initial(state, x_new, ops):
 
 def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, use_dsa=True,
                      dsa_penalty="simplified", threads=0, check_state=True, gs_method="cholqr2",
-                     sweep_dw=None):
+                     sweep_dw=None, comm=None):
     """Advance one linearised step; returns (new DlrState, CollocationStepInfo)."""
     selection = deim_select(state.W.values)
     closure = selection.closure_weights(state.W.beta)
@@ -119,7 +119,8 @@ def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, 
     flux0 = evaluate_rows(state, selection)
     result = source_iteration(
         ops, omegas_sel, closure_host, psi_time=flux0.values, use_dsa=use_dsa, tol=si_tol,
-        max_iters=si_max_iters, phi_start=state.scalar_flux(), threads=threads, dw=sweep_dw)
+        max_iters=si_max_iters, phi_start=state.scalar_flux(), threads=threads, dw=sweep_dw,
+        comm=comm)
 
     # new spatial basis from the converged swept columns (dlr_sn.py:123-125)
     x_new, _, deficient_x = gram_schmidt_mass(ops, result.psi, state.rank + 8, method=gs_method)

@@ -268,12 +268,14 @@ def sweep_solve(ops, omega, rhs, _key=None):
 
 def source_iteration(ops, omegas, closure, psi_time=None, *, use_dsa=True, tol=1e-8,
                      max_iters=200, phi_start=None, extra_source=None, threads=0, dw=None,
-                     keep_sk=False):
+                     keep_sk=False, comm=None):
     """Lagged-scattering iteration over device sweeps (transport_sn.py:377-450).
 
     ``threads`` is accepted for API compatibility and ignored (the sweeps of
     all directions run in one launch).  ``psi_time`` / ``extra_source`` are
-    (n_dofs, n_angles) arrays; results are device tensors.
+    (n_dofs, n_angles) arrays; results are device tensors.  With ``comm`` (a
+    sharding.DirectionComm over > 1 rank) the directions are split across
+    ranks and the closure flux is all-reduced every iteration.
     """
     omegas = np.asarray(omegas.cpu() if isinstance(omegas, torch.Tensor) else omegas, dtype=float)
     closure = np.asarray(closure.cpu() if isinstance(closure, torch.Tensor) else closure, dtype=float)
@@ -286,16 +288,34 @@ def source_iteration(ops, omegas, closure, psi_time=None, *, use_dsa=True, tol=1
             "(SURVEY 4.3: DSA diverges for random angular bases)")
     g = ops.grid
     st = ops.step
-    plan = _SweepPlan(ops, omegas, closure, dw=dw)
+    # direction sharding across ranks (sharding.py): this rank sweeps `mine`
+    owners = None
+    mine = np.arange(nd)
+    if comm is not None and comm.world_size > 1:
+        from .sharding import partition_directions
+
+        owners = partition_directions(omegas, comm.world_size)
+        mine = owners[comm.rank]
+    nl = len(mine)
+    plan = _SweepPlan(ops, omegas[mine], closure[mine], dw=dw) if nl else None
     vl = ops.vec_len
-    rhs_sk = ops.buffer("rhs_sk", nd * vl)
-    psi_sk = ops.buffer("psi_sk", nd * vl)
-    part = ops.buffer("phi_part", plan.G * vl)
+    rhs_sk = ops.buffer("rhs_sk", max(nl, 1) * vl)
+    psi_sk = ops.buffer("psi_sk", max(nl, 1) * vl)
+    part = ops.buffer("phi_part", (plan.G if plan else 1) * vl)
     scat = ops.buffer("scat_sk4", 4 * vl)
-    pt = None if psi_time is None else as_device(psi_time).reshape(g.n_dofs, nd).contiguous()
-    ex = None if extra_source is None else as_device(extra_source).reshape(g.n_dofs, nd).contiguous()
-    _lib.call("dlrsn_rhs_build", ops.cellops_ptr, nd, _lib.ptr(plan.quads_dev), _lib.ptr(st.q),
-              float(st.inv_cdt), _lib.ptr(pt), nd, _lib.ptr(ex), nd, _lib.ptr(rhs_sk), stream())
+
+    def local_cols(a):
+        if a is None:
+            return None
+        a = as_device(a).reshape(g.n_dofs, nd)
+        if owners is not None:
+            a = a[:, torch.as_tensor(mine, device=a.device)]
+        return a.contiguous()
+
+    pt, ex = local_cols(psi_time), local_cols(extra_source)
+    if plan:
+        _lib.call("dlrsn_rhs_build", ops.cellops_ptr, nl, _lib.ptr(plan.quads_dev), _lib.ptr(st.q),
+                  float(st.inv_cdt), _lib.ptr(pt), nl, _lib.ptr(ex), nl, _lib.ptr(rhs_sk), stream())
     phi = zeros(g.n_dofs) if phi_start is None else as_device(phi_start).reshape(-1).clone()
     phi_new = empty(g.n_dofs)
     flags = zeros(1, dtype=torch.int32)
@@ -307,26 +327,45 @@ def source_iteration(ops, omegas, closure, psi_time=None, *, use_dsa=True, tol=1
     host = torch.empty(3, dtype=torch.float64, pin_memory=True)
     change = math.inf
     for it in range(1, max_iters + 1):
-        _sweep(ops, plan, rhs_sk, psi_sk, scat, part)
-        _lib.call("dlrsn_phi_combine", ops.cellops_ptr, plan.G, _lib.ptr(plan.groups_dev),
-                  _lib.ptr(part), _lib.ptr(phi), _lib.ptr(st.sigma_s), _lib.ptr(phi_new),
-                  _lib.ptr(scat), _lib.ptr(norms), _lib.ptr(red_ws), stream())
+        if owners is None:
+            _sweep(ops, plan, rhs_sk, psi_sk, scat, part)
+            _lib.call("dlrsn_phi_combine", ops.cellops_ptr, plan.G, _lib.ptr(plan.groups_dev),
+                      _lib.ptr(part), _lib.ptr(phi), _lib.ptr(st.sigma_s), _lib.ptr(phi_new),
+                      _lib.ptr(scat), _lib.ptr(norms), _lib.ptr(red_ws), stream())
+        else:
+            # local partial closure flux -> allreduce over NVLink -> norms and
+            # scattering source from the summed flux (identical on all ranks)
+            if plan:
+                _sweep(ops, plan, rhs_sk, psi_sk, scat, part)
+                _lib.call("dlrsn_phi_combine", ops.cellops_ptr, plan.G, _lib.ptr(plan.groups_dev),
+                          _lib.ptr(part), _lib.ptr(phi), _lib.ptr(st.sigma_s), _lib.ptr(phi_new),
+                          None, _lib.ptr(norms), _lib.ptr(red_ws), stream())
+            else:
+                phi_new.zero_()
+            comm.allreduce_sum_(phi_new)
+            _lib.call("dlrsn_phi_finish", ops.cellops_ptr, _lib.ptr(phi_new), _lib.ptr(phi),
+                      _lib.ptr(st.sigma_s), _lib.ptr(scat), _lib.ptr(norms), _lib.ptr(red_ws),
+                      stream())
         host[:2].copy_(norms, non_blocking=True)
         if it == 1:
             host[2:3].copy_(flags.to(torch.float64), non_blocking=True)
         torch.cuda.current_stream(device()).synchronize()
         phi, phi_new = phi_new, phi
         if it == 1 and host[2].item() == 0.0:  # pure absorber (transport_sn.py:410,430-432)
-            return _finish(ops, plan, psi_sk, phi, 1, keep_sk)
+            return _finish(ops, plan, psi_sk, phi, 1, keep_sk, comm, owners, nd)
         d2, n2 = host[0].item(), host[1].item()
         change = math.sqrt(d2) / max(math.sqrt(n2), 1e-300)
         if change <= tol:
-            return _finish(ops, plan, psi_sk, phi, it, keep_sk)
+            return _finish(ops, plan, psi_sk, phi, it, keep_sk, comm, owners, nd)
     raise IterationLimitError("source iteration did not converge", max_iters, change)
 
 
-def _finish(ops, plan, psi_sk, phi, it, keep_sk):
-    psi = _to_canonical(ops, plan, psi_sk)
+def _finish(ops, plan, psi_sk, phi, it, keep_sk, comm=None, owners=None, nd=0):
+    if owners is None:
+        psi = _to_canonical(ops, plan, psi_sk)
+    else:
+        local = _to_canonical(ops, plan, psi_sk) if plan else empty(ops.grid.n_dofs, 0)
+        psi = comm.allgather_columns(local, owners, nd)
     res = SourceIterationResult(psi=psi, phi=phi, iterations=it)
     if keep_sk:
         res.psi_sk = psi_sk
