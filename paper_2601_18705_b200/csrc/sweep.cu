@@ -19,90 +19,18 @@
 //   * the closure phi_g = sum_d cw_d psi_d of the warp's directions is
 //     accumulated in registers (deterministic, no atomics).
 #include <cmath>
+#include <cstdlib>
 
-#include "common.cuh"
+#include "sweep_common.cuh"
 
 namespace dlrsn {
-
-struct SweepArgs {
-  int nx, ny, G;
-  const dlrsn_group* groups;
-  const double* sigma_sk4;
-  const double* scat_sk4;
-  const double* rhs_sk;
-  double* psi_sk;
-  double* phi_sk;
-  int* ticket;
-  double* handoff;
-  int* status;
-  double mass[16];
-  double gxp[16];  // Gx + e2x embedded at the right edge (oriented +x outflow)
-  double gyp[16];  // Gy + e2y embedded at the top edge
-  double ex[4];    // e2x (left inflow coupling)
-  double ey[4];    // e2y (bottom inflow coupling)
-  int64_t vlen, slen;
-};
 
 // Debug timeline (dlrsn_debug_trace): per (item, chunk) globaltimer before
 // and after the handoff wait; null in production.
 __device__ unsigned long long* g_trace = nullptr;
 __device__ int g_trace_chunks = 0;
 __device__ int g_flags = 0;  // debug: bit0 = no speculative handoff prefetch
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 
-__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
-  double v;
-  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Empty handoff slot: a signalling NaN with a fixed payload.  Arithmetic only
-// produces quiet NaNs, so a swept value can never alias it.
-constexpr unsigned long long kEmpty = 0x7FF4DEADBEEFCAFEull;
-__device__ __forceinline__ bool is_empty(double v) {
-  return (unsigned long long)__double_as_longlong(v) == kEmpty;
-}
-
-// 1/x without the IEEE slow path: hardware approximation + two Newton steps
-// (relative error ~1 ulp; A's pivots are positive and normal).
-__device__ __forceinline__ double rcp64(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
-
-__device__ __forceinline__ void solve4(double* a, double* b, double* x) {
-  // Gaussian elimination without pivoting: A has a positive-definite
-  // symmetric part (sigma_t M + upwind outflow terms), so the pivots are
-  // positive.  The reference inverts with LAPACK (transport_sn.py:158); the
-  // two differ only at round-off.
-  const double p0 = rcp64(a[0]);
-  double l = a[4] * p0;
-  a[5] -= l * a[1]; a[6] -= l * a[2]; a[7] -= l * a[3]; b[1] -= l * b[0];
-  l = a[8] * p0;
-  a[9] -= l * a[1]; a[10] -= l * a[2]; a[11] -= l * a[3]; b[2] -= l * b[0];
-  l = a[12] * p0;
-  a[13] -= l * a[1]; a[14] -= l * a[2]; a[15] -= l * a[3]; b[3] -= l * b[0];
-  const double p1 = rcp64(a[5]);
-  l = a[9] * p1;
-  a[10] -= l * a[6]; a[11] -= l * a[7]; b[2] -= l * b[1];
-  l = a[13] * p1;
-  a[14] -= l * a[6]; a[15] -= l * a[7]; b[3] -= l * b[1];
-  const double p2 = rcp64(a[10]);
-  l = a[14] * p2;
-  a[15] -= l * a[11]; b[3] -= l * b[2];
-  x[3] = b[3] * rcp64(a[15]);
-  x[2] = (b[2] - a[11] * x[3]) * p2;
-  x[1] = (b[1] - a[6] * x[2] - a[7] * x[3]) * p1;
-  x[0] = (b[0] - a[1] * x[1] - a[2] * x[2] - a[3] * x[3]) * p0;
-}
 
 // Steps per TMA chunk, pipeline depth and warps per CTA for a group width.
 template <int DW> struct SweepCfg;
@@ -679,7 +607,12 @@ int dlrsn_debug_flags(int flags) {
   return DLRSN_OK;
 }
 
+static unsigned long long* h_trace = nullptr;
+static int h_trace_chunks = 0;
+
 int dlrsn_debug_trace(unsigned long long* buf, int chunks) {
+  h_trace = buf;
+  h_trace_chunks = chunks;
   DLRSN_TRY_CUDA(cudaMemcpyToSymbol(g_trace, &buf, sizeof(buf)));
   DLRSN_TRY_CUDA(cudaMemcpyToSymbol(g_trace_chunks, &chunks, sizeof(int)));
   return DLRSN_OK;
@@ -741,8 +674,23 @@ int dlrsn_sweep(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int 
   }
   a.vlen = sk_vec_len(ops->nx, ops->ny);
   a.slen = sk_scalar_len(ops->nx, ops->ny);
+  a.trace = h_trace;
+  a.trace_chunks = h_trace_chunks;
+  // single-direction groups: the warp-specialised kernel when the work items
+  // barely fill the GPU (latency-bound regime), the multi-warp kernel when
+  // there are enough items to hide the per-step latency by occupancy
+  static const char* ws_env = getenv("DLRSN_SWEEP_WS");
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int items = sk_strips(ops->ny) * G;
+  bool use_ws = items <= 2 * sms;
+  if (ws_env) use_ws = ws_env[0] == '1';
   switch (dw) {
-    case 1: return launch_sweep<1>(a, max_ctas, st);
+    case 1: return use_ws ? launch_sweep_ws(a, max_ctas, st) : launch_sweep<1>(a, max_ctas, st);
     case 2: return launch_sweep<2>(a, max_ctas, st);
     case 4: return launch_sweep<4>(a, max_ctas, st);
     default: return launch_sweep<8>(a, max_ctas, st);

@@ -1,0 +1,89 @@
+// Shared pieces of the two sweep kernels (sweep.cu: general group width;
+// sweep_ws.cu: warp-specialised single-direction groups).
+#pragma once
+
+#include "common.cuh"
+
+namespace dlrsn {
+
+struct SweepArgs {
+  int nx, ny, G;
+  const dlrsn_group* groups;
+  const double* sigma_sk4;
+  const double* scat_sk4;
+  const double* rhs_sk;
+  double* psi_sk;
+  double* phi_sk;
+  int* ticket;
+  double* handoff;
+  int* status;
+  double mass[16];
+  double gxp[16];  // Gx + e2x embedded at the right edge (oriented +x outflow)
+  double gyp[16];  // Gy + e2y embedded at the top edge
+  double ex[4];    // e2x (left inflow coupling)
+  double ey[4];    // e2y (bottom inflow coupling)
+  int64_t vlen, slen;
+  unsigned long long* trace;  // debug timeline (dlrsn_debug_trace), null in production
+  int trace_chunks;
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Empty handoff slot: a signalling NaN with a fixed payload.  Arithmetic only
+// produces quiet NaNs, so a swept value can never alias it.
+constexpr unsigned long long kEmpty = 0x7FF4DEADBEEFCAFEull;
+__device__ __forceinline__ bool is_empty(double v) {
+  return (unsigned long long)__double_as_longlong(v) == kEmpty;
+}
+
+// 1/x without the IEEE slow path: hardware approximation + two Newton steps
+// (relative error ~1 ulp; A's pivots are positive and normal).
+__device__ __forceinline__ double rcp64(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+__device__ __forceinline__ void solve4(double* a, double* b, double* x) {
+  // Gaussian elimination without pivoting: A has a positive-definite
+  // symmetric part (sigma_t M + upwind outflow terms), so the pivots are
+  // positive.  The reference inverts with LAPACK (transport_sn.py:158); the
+  // two differ only at round-off.
+  const double p0 = rcp64(a[0]);
+  double l = a[4] * p0;
+  a[5] -= l * a[1]; a[6] -= l * a[2]; a[7] -= l * a[3]; b[1] -= l * b[0];
+  l = a[8] * p0;
+  a[9] -= l * a[1]; a[10] -= l * a[2]; a[11] -= l * a[3]; b[2] -= l * b[0];
+  l = a[12] * p0;
+  a[13] -= l * a[1]; a[14] -= l * a[2]; a[15] -= l * a[3]; b[3] -= l * b[0];
+  const double p1 = rcp64(a[5]);
+  l = a[9] * p1;
+  a[10] -= l * a[6]; a[11] -= l * a[7]; b[2] -= l * b[1];
+  l = a[13] * p1;
+  a[14] -= l * a[6]; a[15] -= l * a[7]; b[3] -= l * b[1];
+  const double p2 = rcp64(a[10]);
+  l = a[14] * p2;
+  a[15] -= l * a[11]; b[3] -= l * b[2];
+  x[3] = b[3] * rcp64(a[15]);
+  x[2] = (b[2] - a[11] * x[3]) * p2;
+  x[1] = (b[1] - a[6] * x[2] - a[7] * x[3]) * p1;
+  x[0] = (b[0] - a[1] * x[1] - a[2] * x[2] - a[3] * x[3]) * p0;
+}
+
+
+int launch_sweep_ws(const SweepArgs& a, int max_ctas, cudaStream_t st);
+
+}  // namespace dlrsn

@@ -1,0 +1,316 @@
+// K1 (latency-optimised): warp-specialised sweep for single-direction groups.
+//
+// Same math and data layout as sweep.cu (transport_sn.py:142-163,303-322),
+// split so that only the upwind-dependent part sits on the critical path:
+//
+//   psi = A^-1 (rhs + scat + Cx x_in + Cy y_in) = z + Kx x_in + Ky y_in,
+//   z = A^-1 (rhs + scat),  Kx = A^-1 Cx (4x2),  Ky = A^-1 Cy (4x2).
+//
+// A CTA owns one (group, 32-row strip) work item at a time:
+//   * warps 1..3 ("producers") take the TMA-staged sigma_t / scattering
+//     source / rhs of each chunk of C skewed steps, form and LU-factor the
+//     4x4 local operator of every lane and write (z, Kx, Ky) -- 20 doubles per
+//     lane-step -- into a double-buffered shared-memory ring;
+//   * warp 0 ("consumer") walks the strip: per step 16 FMAs, the closure
+//     accumulation, two stores and one shuffle, so the dependent chain is
+//     ~3 FMAs + a shuffle instead of a full 4x4 factorisation.
+// mbarriers (one arrive per chunk) order producers and consumer; the strip
+// handoff is the self-flagging L2 column of sweep.cu.
+#include <cmath>
+
+#include "sweep_common.cuh"
+
+namespace dlrsn {
+
+__device__ __forceinline__ unsigned long long ws_timer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define WS_TRACE(k)                                                                   \
+  do {                                                                                \
+    if (a.trace && (threadIdx.x & 31) == 0 && m < a.trace_chunks)                     \
+      a.trace[((int64_t)item * a.trace_chunks + m) * 8 + (k)] = ws_timer();           \
+  } while (0)
+
+constexpr int kWsC = 6;      // skewed steps per chunk (= 2 x producers)
+constexpr int kWsProd = 3;   // producer warps
+constexpr int kWsPairs = 10; // z (2 pairs), Kx (4 pairs), Ky (4 pairs)
+constexpr int kWsInD = kWsC * (32 + 128 + 128);  // sigma | scat | rhs doubles per stage
+constexpr int kWsFacD = kWsC * kWsPairs * 64;    // factor doubles per stage
+constexpr size_t kWsSmem = (2 * (size_t)kWsInD + 2 * (size_t)kWsFacD) * sizeof(double);
+
+__device__ __forceinline__ void named_bar_producers() {
+  asm volatile("bar.sync 1, %0;" ::"r"(kWsProd * 32) : "memory");
+}
+
+// Factor one lane-step: (z, Kx, Ky) of the local operator at skewed step tt
+// of the staged chunk.  Straight-line code (no early exit) so that two calls
+// in a row are interleaved by the scheduler (two independent FP64 chains).
+__device__ __forceinline__ void ws_factor_step(const SweepArgs& a, const double* s_S,
+                                               const double* buf, double* fac, int tt, int lane,
+                                               bool scat, double ox, double oy) {
+  const double sigma = buf[tt * 32 + lane];
+  const double2 r0 = reinterpret_cast<const double2*>(buf + kWsC * 160 + tt * 128)[lane];
+  const double2 r1 = reinterpret_cast<const double2*>(buf + kWsC * 160 + tt * 128 + 64)[lane];
+  double b[4] = {r0.x, r0.y, r1.x, r1.y};
+  if (scat) {
+    const double2 u0 = reinterpret_cast<const double2*>(buf + kWsC * 32 + tt * 128)[lane];
+    const double2 u1 = reinterpret_cast<const double2*>(buf + kWsC * 32 + tt * 128 + 64)[lane];
+    b[0] += u0.x; b[1] += u0.y; b[2] += u1.x; b[3] += u1.y;
+  }
+  double A[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) A[q] = fma(sigma, a.mass[q], s_S[q]);
+  // LU without pivoting (positive-definite symmetric part, see solve4)
+  const double p0 = rcp64(A[0]);
+  const double l1 = A[4] * p0, l2 = A[8] * p0, l3 = A[12] * p0;
+  A[5] -= l1 * A[1]; A[6] -= l1 * A[2]; A[7] -= l1 * A[3];
+  A[9] -= l2 * A[1]; A[10] -= l2 * A[2]; A[11] -= l2 * A[3];
+  A[13] -= l3 * A[1]; A[14] -= l3 * A[2]; A[15] -= l3 * A[3];
+  const double p1 = rcp64(A[5]);
+  const double m2 = A[9] * p1, m3 = A[13] * p1;
+  A[10] -= m2 * A[6]; A[11] -= m2 * A[7];
+  A[14] -= m3 * A[6]; A[15] -= m3 * A[7];
+  const double p2 = rcp64(A[10]);
+  const double n3 = A[14] * p2;
+  A[15] -= n3 * A[11];
+  const double p3 = rcp64(A[15]);
+  auto solve = [&](double v0, double v1, double v2, double v3, double* x) {
+    const double y1 = v1 - l1 * v0;
+    const double y2 = v2 - l2 * v0 - m2 * y1;
+    const double y3 = v3 - l3 * v0 - m3 * y1 - n3 * y2;
+    x[3] = y3 * p3;
+    x[2] = (y2 - A[11] * x[3]) * p2;
+    x[1] = (y1 - A[6] * x[2] - A[7] * x[3]) * p1;
+    x[0] = (v0 - A[1] * x[1] - A[2] * x[2] - A[3] * x[3]) * p0;
+  };
+  double z[4], c0[4], c1[4], c2[4];
+  solve(b[0], b[1], b[2], b[3], z);
+  solve(1.0, 0.0, 0.0, 0.0, c0);
+  solve(0.0, 1.0, 0.0, 0.0, c1);
+  solve(0.0, 0.0, 1.0, 0.0, c2);
+  double2* out = reinterpret_cast<double2*>(fac + (int64_t)tt * kWsPairs * 64) + lane;
+  out[0] = make_double2(z[0], z[1]);
+  out[32] = make_double2(z[2], z[3]);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    // pair 2+i: row i of Kx = ox A^-1[:, {0,2}] e2x ; pair 6+i: Ky = oy A^-1[:, {0,1}] e2y
+    out[32 * (2 + i)] = make_double2(ox * (c0[i] * a.ex[0] + c2[i] * a.ex[2]),
+                                     ox * (c0[i] * a.ex[1] + c2[i] * a.ex[3]));
+    out[32 * (6 + i)] = make_double2(oy * (c0[i] * a.ey[0] + c1[i] * a.ey[2]),
+                                     oy * (c0[i] * a.ey[1] + c1[i] * a.ey[3]));
+  }
+}
+
+__global__ void __launch_bounds__(128) sweep_ws_kernel(const SweepArgs a) {
+  extern __shared__ __align__(128) double sm[];
+  double* in_ring = sm;                 // 2 x kWsInD
+  double* fac_ring = sm + 2 * kWsInD;   // 2 x kWsFacD
+  __shared__ __align__(8) uint64_t in_full[2], fac_full[2], fac_empty[2];
+  __shared__ double s_S[16];
+  __shared__ int s_item;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nx = a.nx, ny = a.ny, G = a.G;
+  const int T = nx + 31;
+  const int ns = (ny + 31) >> 5;
+  const int items = ns * G;
+  const int nchunks = (T + kWsC - 1) / kWsC;
+  const int hchunks = (nx + kWsC - 1) / kWsC;
+  const double empty = __longlong_as_double((long long)kEmpty);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&in_full[i], 1);
+      mbar_init(&fac_full[i], 1);
+      mbar_init(&fac_empty[i], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // per-stage use counters (identical in every thread that tracks them)
+  uint32_t uses[2] = {0, 0};
+
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(a.ticket, 1);
+    __syncthreads();
+    const int item = s_item;
+    __syncthreads();
+    if (item >= items) break;
+    const int s = item / G;
+    const int g = item - s * G;
+    const dlrsn_group* grp = a.groups + g;
+    const int quad = grp->quad;
+    const int slot = grp->slot[0];
+    const double ox = grp->ox[0], oy = grp->oy[0], cw = grp->cw[0];
+    if (threadIdx.x < 16) s_S[threadIdx.x] = ox * a.gxp[threadIdx.x] + oy * a.gyp[threadIdx.x];
+    __syncthreads();
+    const int64_t strip_vec = (int64_t)s * T * 128;
+    const double* sig = a.sigma_sk4 + (int64_t)quad * a.slen + (int64_t)s * T * 32;
+    const double* scat = a.scat_sk4 ? a.scat_sk4 + (int64_t)quad * a.vlen + strip_vec : nullptr;
+    const double* rhs = a.rhs_sk + (int64_t)slot * a.vlen + strip_vec;
+    const bool row_ok = (s << 5) + lane < ny;
+
+    auto issue = [&](int m) {  // thread 32 only
+      const int st = m & 1, t0 = m * kWsC;
+      const uint32_t n = (uint32_t)min(kWsC, T - t0);
+      double* buf = in_ring + st * kWsInD;
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&in_full[st], n * (256u + (scat ? 1024u : 0u) + 1024u));
+      tma_load_1d(buf, sig + t0 * 32, n * 256u, &in_full[st]);
+      if (scat) tma_load_1d(buf + kWsC * 32, scat + t0 * 128, n * 1024u, &in_full[st]);
+      tma_load_1d(buf + kWsC * 160, rhs + t0 * 128, n * 1024u, &in_full[st]);
+    };
+
+    if (warp > 0) {
+      // ------------------------------ producers ----------------------------
+      const int pw = warp - 1;
+      if (threadIdx.x == 32) {
+        issue(0);
+        if (nchunks > 1) issue(1);
+      }
+      for (int m = 0; m < nchunks; ++m) {
+        const int st = m & 1;
+        const uint32_t u = uses[st];
+        if (warp == 1) WS_TRACE(3);
+        mbar_wait_warp(&in_full[st], u & 1u);
+        if (u > 0) mbar_wait_warp(&fac_empty[st], (u - 1) & 1u);
+        if (warp == 1) WS_TRACE(4);
+        const double* buf = in_ring + st * kWsInD;
+        double* fac = fac_ring + st * kWsFacD;
+        // kWsC = 2 kWsProd: each producer warp factors steps pw and pw + kWsProd
+        // together (inactive lanes compute harmless garbage the consumer skips)
+        const double* bufc = buf;
+        ws_factor_step(a, s_S, bufc, fac, pw, lane, scat != nullptr, ox, oy);
+        ws_factor_step(a, s_S, bufc, fac, pw + kWsProd, lane, scat != nullptr, ox, oy);
+        if (warp == 1) WS_TRACE(5);
+        named_bar_producers();  // stage st fully read (inputs) and written (factors)
+        if (warp == 1) WS_TRACE(6);
+        if (threadIdx.x == 32) {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&fac_full[st])) : "memory");
+          if (m + 2 < nchunks) issue(m + 2);
+        }
+        uses[st] = u + 1;
+      }
+    } else {
+      // ------------------------------ consumer ------------------------------
+      double* psi_p = a.psi_sk + (int64_t)slot * a.vlen + strip_vec + 2 * lane;
+      double* phi_p = a.phi_sk ? a.phi_sk + (int64_t)g * a.vlen + strip_vec + 2 * lane : nullptr;
+      double2* hin = s > 0 ? reinterpret_cast<double2*>(a.handoff) + ((int64_t)(s - 1) * G + g) * nx
+                           : nullptr;
+      double2* hout = (s + 1 < ns) ? reinterpret_cast<double2*>(a.handoff) + ((int64_t)s * G + g) * nx
+                                   : nullptr;
+      const bool hlane = hin != nullptr && lane < kWsC;
+      double2 h0 = make_double2(0.0, 0.0), h1 = h0, h2 = h0;
+      if (hlane && lane < nx) h1 = __ldcg(hin + lane);
+      if (hlane && kWsC + lane < nx) h2 = __ldcg(hin + kWsC + lane);
+      double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
+      for (int m = 0; m < nchunks; ++m) {
+        const int st = m & 1;
+        const uint32_t u = uses[st];
+        h0 = h1;
+        h1 = h2;
+        {
+          const bool need = hlane && m < hchunks && m * kWsC + lane < nx;
+          double2* hs = hin + (int64_t)m * kWsC + lane;
+          int spins = 0;
+          while (__any_sync(kFull, need && (is_empty(h0.x) || is_empty(h0.y)))) {
+            __nanosleep(32);
+            if (need && (is_empty(h0.x) || is_empty(h0.y))) h0 = __ldcv(hs);
+            if (++spins > (1 << 26)) {
+              if (need) atomicOr(a.status, 2);
+              h0 = make_double2(0.0, 0.0);
+            }
+          }
+          if (need) __stcg(hs, make_double2(empty, empty));
+        }
+        if (hlane && m + 2 < hchunks && (m + 2) * kWsC + lane < nx)
+          h2 = __ldcg(hin + (int64_t)(m + 2) * kWsC + lane);
+        WS_TRACE(0);
+        mbar_wait_warp(&fac_full[st], u & 1u);
+        WS_TRACE(1);
+        const double2* fac = reinterpret_cast<const double2*>(fac_ring + st * kWsFacD) + lane;
+        // Branch-free steps with the factors of step tt+1 loaded while step tt
+        // computes.  Inactive lanes (skew padding / rows beyond ny) compute on
+        // padding and store into the SK padding slots; their values never reach
+        // an active lane (an inactive (lane, step) only feeds inactive ones)
+        // and the x carry only advances on active steps.
+        double2 fz[2], fk[8];
+        auto load = [&](int tt, double2* z, double2* k) {
+          const double2* f = fac + tt * kWsPairs * 32;  // double2 units
+          z[0] = f[0]; z[1] = f[32];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) k[i] = f[64 + 32 * i];
+        };
+        load(0, fz, fk);
+#pragma unroll
+        for (int tt = 0; tt < kWsC; ++tt) {
+          const int t = m * kWsC + tt;
+          const int ip = t - lane;
+          const bool act = row_ok && ip >= 0 && ip < nx;
+          double2 nz[2], nk[8];
+          if (tt + 1 < kWsC) load(tt + 1, nz, nk);
+          const double hy0 = __shfl_sync(kFull, h0.x, tt);
+          const double hy1 = __shfl_sync(kFull, h0.y, tt);
+          if (lane == 0) {
+            y0 = hin != nullptr ? hy0 : 0.0;
+            y1 = hin != nullptr ? hy1 : 0.0;
+          }
+          const double q0 = fma(fk[4].y, y1, fma(fk[4].x, y0, fma(fk[0].y, x1, fma(fk[0].x, x0, fz[0].x))));
+          const double q1 = fma(fk[5].y, y1, fma(fk[5].x, y0, fma(fk[1].y, x1, fma(fk[1].x, x0, fz[0].y))));
+          const double q2 = fma(fk[6].y, y1, fma(fk[6].x, y0, fma(fk[2].y, x1, fma(fk[2].x, x0, fz[1].x))));
+          const double q3 = fma(fk[7].y, y1, fma(fk[7].x, y0, fma(fk[3].y, x1, fma(fk[3].x, x0, fz[1].y))));
+          const double u0 = __shfl_up_sync(kFull, q2, 1);
+          const double u1 = __shfl_up_sync(kFull, q3, 1);
+          if (t < T) {  // steps past the slab's end would land in the next strip / slot
+            double2* po = reinterpret_cast<double2*>(psi_p + (int64_t)t * 128);
+            po[0] = make_double2(q0, q1);
+            po[32] = make_double2(q2, q3);
+            if (phi_p) {
+              double2* pp = reinterpret_cast<double2*>(phi_p + (int64_t)t * 128);
+              pp[0] = make_double2(cw * q0, cw * q1);
+              pp[32] = make_double2(cw * q2, cw * q3);
+            }
+          }
+          if (lane == 31 && act && hout) __stcg(hout + ip, make_double2(q2, q3));
+          x0 = act ? q1 : x0;
+          x1 = act ? q3 : x1;
+          if (lane > 0) { y0 = u0; y1 = u1; }
+          if (tt + 1 < kWsC) {
+            fz[0] = nz[0]; fz[1] = nz[1];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) fk[i] = nk[i];
+          }
+        }
+        __syncwarp();
+        WS_TRACE(2);
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&fac_empty[st])) : "memory");
+        uses[st] = u + 1;
+      }
+    }
+    __syncthreads();  // item done: every warp leaves the stage counters in step
+    // producers and consumer advanced uses[] by the same amounts; nothing else
+  }
+}
+
+int launch_sweep_ws(const SweepArgs& a, int max_ctas, cudaStream_t st) {
+  int dev = 0, sms = 0, occ = 0;
+  DLRSN_TRY_CUDA(cudaGetDevice(&dev));
+  DLRSN_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  DLRSN_TRY_CUDA(cudaFuncSetAttribute(sweep_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kWsSmem));
+  DLRSN_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_ws_kernel, 128, kWsSmem));
+  const int items = ((a.ny + 31) >> 5) * a.G;
+  int ctas = items;
+  const int cap = sms * (occ > 0 ? occ : 1);
+  if (ctas > cap) ctas = cap;
+  if (max_ctas > 0 && ctas > max_ctas) ctas = max_ctas;
+  if (ctas < 1) ctas = 1;
+  sweep_ws_kernel<<<ctas, 128, kWsSmem, st>>>(a);
+  DLRSN_CHECK_LAUNCH("sweep_ws_kernel");
+  return DLRSN_OK;
+}
+
+}  // namespace dlrsn
