@@ -139,12 +139,15 @@ int dlrsn_cells_to_sk4(const dlrsn_cellops* ops, const double* cell_values, doub
 int dlrsn_scatter_source(const dlrsn_cellops* ops, const double* phi, const double* sigma_s,
                          double* scat_sk4, int* any_scatter, dlrsn_stream_t stream);
 
-/* phi_new = sum_g phi_part[g] (fixed order), scat for the next iteration,
- * and norms[0] = ||phi_new - phi_old||^2, norms[1] = ||phi_new||^2
- * (deterministic reduction; transport_sn.py:438,442-446).  groups: device
- * table; partial_ws >= 2*ceil(n_cells/256) doubles + 1 int counter. */
+/* phi_new = sum_g phi_part[g] (fixed order) -- or, with phi_part_sk NULL,
+ * sum_g sum_k cw[g][k] psi[slot[g][k]] read from the swept psi_sk -- plus
+ * the scattering source for the next iteration and norms[0] =
+ * ||phi_new - phi_old||^2, norms[1] = ||phi_new||^2 (deterministic
+ * reduction; transport_sn.py:438,442-446).  scat_sk4 nullable.  partial_ws
+ * >= 256 bytes + 2*ceil(n_cells/256) doubles (its first word must start 0). */
 int dlrsn_phi_combine(const dlrsn_cellops* ops, int G, const dlrsn_group* groups,
-                      const double* phi_part_sk, const double* phi_old, const double* sigma_s,
+                      const double* phi_part_sk, const double* psi_sk, const double* phi_old,
+                      const double* sigma_s,
                       double* phi_new, double* scat_sk4, double* norms, void* partial_ws,
                       dlrsn_stream_t stream);
 

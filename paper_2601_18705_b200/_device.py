@@ -52,6 +52,29 @@ def as_device(x, n=None, dtype=torch.float64):
     return t.contiguous()
 
 
+def upload(a, dtype=None):
+    """Host array -> device without a stream sync: stage through pinned
+    memory and copy asynchronously (torch keeps the pinned block alive until
+    the copy has executed).  A pageable H2D copy would wait for the stream."""
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.pin_memory().to(device(), non_blocking=True)
+
+
+_CONST = {}
+
+
+def cached_upload(key, make):
+    """Device copy of a constant host array, uploaded once per device."""
+    k = (torch.cuda.current_device(), key)
+    t = _CONST.get(k)
+    if t is None:
+        t = upload(make())
+        _CONST[k] = t
+    return t
+
+
 def zeros(*shape, dtype=torch.float64):
     return torch.zeros(*shape, dtype=dtype, device=device())
 

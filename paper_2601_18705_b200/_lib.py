@@ -63,7 +63,7 @@ _SIGNATURES = {
     "dlrsn_cells_to_sk4": (c_int, [c_vp, c_vp, c_vp, c_vp]),
     "dlrsn_scatter_source": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "dlrsn_phi_combine": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
-                                  c_vp]),
+                                  c_vp, c_vp]),
     "dlrsn_phi_finish": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "dlrsn_sk_to_canonical": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp, c_int, c_vp]),
     "dlrsn_sweep": (c_int, [c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64,

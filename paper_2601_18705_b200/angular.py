@@ -137,7 +137,19 @@ def angular_monomial_exponents(count):
 def orthonormalize(columns, quad, pin_constant=False):
     """Weighted CGS2 with deterministic completion (angular.py:217-238), as
     one CUDA kernel.  Returns (AngularBasis, R, deficient)."""
-    from .lowrank import _cgs2
+    from .lowrank import _cgs2_flags
+
+    basis, R, defi, status = orthonormalize_async(columns, quad, pin_constant)
+    deficient = _cgs2_flags(defi.cpu().numpy(), status.cpu().numpy(), R.shape[0])
+    if pin_constant:
+        return basis, R, [d - 1 for d in deficient if d > 0]
+    return basis, R, deficient
+
+
+def orthonormalize_async(columns, quad, pin_constant=False):
+    """orthonormalize without a host sync: (basis, R, deficient flags,
+    status); R excludes the pinned constant's row... column (see above)."""
+    from .lowrank import _cgs2_async
 
     cols = as_device(columns)
     if cols.ndim != 2 or cols.shape[0] != quad.n_angles:
@@ -150,12 +162,11 @@ def orthonormalize(columns, quad, pin_constant=False):
     n, m = cols.shape
     ncomp = (m - (1 if pin_constant else 0)) + 8
     exps = np.asarray(angular_monomial_exponents(ncomp), dtype=np.int32)
-    Q, R, deficient = _cgs2(n, m, cols.contiguous(), metric=0, weights=quad.weights_device(),
-                            comp_kind=0, comp_exp=exps, coords=quad.omegas_device(), strict=True)
+    Q, R, defi, status = _cgs2_async(n, m, cols.contiguous(), metric=0,
+                                     weights=quad.weights_device(), comp_kind=0, comp_exp=exps,
+                                     coords=quad.omegas_device(), strict=True)
     basis = AngularBasis(values=Q, pinned=pin_constant).bind(quad)
-    if pin_constant:
-        return basis, R[:, 1:], [d - 1 for d in deficient if d > 0]
-    return basis, R, deficient
+    return basis, (R[:, 1:] if pin_constant else R), defi, status
 
 
 def angular_monomials(quad, count):

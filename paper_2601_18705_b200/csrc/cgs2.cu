@@ -101,6 +101,15 @@ __device__ void grid_sum(cg::grid_group& grid, const Cgs2Args& g, Cgs2State& s, 
     }
   }
   __syncthreads();
+  if (gridDim.x == 1) {  // single block: no global round trip
+    if (threadIdx.x < nv) {
+      double x = 0.0;
+      for (int q = 0; q < nw; ++q) x += red[q * kCgCh + threadIdx.x];
+      out[threadIdx.x] = x;
+    }
+    __syncthreads();
+    return;
+  }
   double* mine = g.part + ((int64_t)s.buf * gridDim.x + blockIdx.x) * kCgCh;
   if (threadIdx.x < nv) {
     double x = 0.0;

@@ -371,7 +371,8 @@ __global__ void scatter_source_kernel(dlrsn_cellops ops, const double* __restric
 }
 
 __global__ void phi_combine_kernel(dlrsn_cellops ops, int G, const dlrsn_group* __restrict__ groups,
-                                   const double* __restrict__ part, const double* __restrict__ phi_old,
+                                   const double* __restrict__ part, const double* __restrict__ psi,
+                                   const double* __restrict__ phi_old,
                                    const double* __restrict__ ss, double* __restrict__ phi_new,
                                    double* __restrict__ scat, int64_t vlen, double* norms,
                                    double* partials, unsigned* counter) {
@@ -386,13 +387,27 @@ __global__ void phi_combine_kernel(dlrsn_cellops ops, int G, const dlrsn_group* 
       const int qd = groups[g].quad;
       int s, t, lane;
       sk_locate(c % nx, c / nx, qd, nx, ny, s, t, lane);
-      const double* src = part + (int64_t)g * vlen;
-      const double2 a = *reinterpret_cast<const double2*>(src + sk_vec_off(T, s, t, 0, lane));
-      const double2 b = *reinterpret_cast<const double2*>(src + sk_vec_off(T, s, t, 1, lane));
-      const double o[4] = {a.x, a.y, b.x, b.y};
       const int f = sk_flip(qd);
+      if (part) {
+        const double* src = part + (int64_t)g * vlen;
+        const double2 a = *reinterpret_cast<const double2*>(src + sk_vec_off(T, s, t, 0, lane));
+        const double2 b = *reinterpret_cast<const double2*>(src + sk_vec_off(T, s, t, 1, lane));
+        const double o[4] = {a.x, a.y, b.x, b.y};
 #pragma unroll
-      for (int l = 0; l < 4; ++l) p[l] += o[l ^ f];
+        for (int l = 0; l < 4; ++l) p[l] += o[l ^ f];
+      } else {
+        // no per-group partials: closure straight from the swept psi
+        const int nd = groups[g].ndir;
+        for (int k = 0; k < nd; ++k) {
+          const double* src = psi + (int64_t)groups[g].slot[k] * vlen;
+          const double w = groups[g].cw[k];
+          const double2 a = *reinterpret_cast<const double2*>(src + sk_vec_off(T, s, t, 0, lane));
+          const double2 b = *reinterpret_cast<const double2*>(src + sk_vec_off(T, s, t, 1, lane));
+          const double o[4] = {w * a.x, w * a.y, w * b.x, w * b.y};
+#pragma unroll
+          for (int l = 0; l < 4; ++l) p[l] += o[l ^ f];
+        }
+      }
     }
     const double2 oa = reinterpret_cast<const double2*>(phi_old)[2 * c];
     const double2 ob = reinterpret_cast<const double2*>(phi_old)[2 * c + 1];
@@ -563,14 +578,16 @@ int dlrsn_scatter_source(const dlrsn_cellops* ops, const double* phi, const doub
 }
 
 int dlrsn_phi_combine(const dlrsn_cellops* ops, int G, const dlrsn_group* groups,
-                      const double* phi_part_sk, const double* phi_old, const double* sigma_s,
+                      const double* phi_part_sk, const double* psi_sk, const double* phi_old,
+                      const double* sigma_s,
                       double* phi_new, double* scat_sk4, double* norms, void* partial_ws,
                       dlrsn_stream_t stream) {
   const int n = ops->nx * ops->ny;
   const int nb = (n + 255) / 256;
   unsigned* counter = reinterpret_cast<unsigned*>(partial_ws);
   double* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(partial_ws) + 256);
-  phi_combine_kernel<<<nb, 256, 0, as_stream(stream)>>>(*ops, G, groups, phi_part_sk, phi_old,
+  DLRSN_REQUIRE(phi_part_sk || psi_sk, "phi_combine needs partials or psi");
+  phi_combine_kernel<<<nb, 256, 0, as_stream(stream)>>>(*ops, G, groups, phi_part_sk, psi_sk, phi_old,
                                                         sigma_s, phi_new, scat_sk4,
                                                         sk_vec_len(ops->nx, ops->ny), norms,
                                                         partials, counter);

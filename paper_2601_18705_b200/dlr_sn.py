@@ -24,15 +24,21 @@ import torch
 
 from . import _lib
 from ._device import as_device, empty, stream
-from .angular import orthonormalize
+from .angular import orthonormalize_async
+from .errors import ContractViolation
 from .lowrank import (
     DlrState,
     _addr,
     _cellops_of,
-    _row_solve,
-    deim_select,
+    _cgs2_flags,
+    _row_solve_async,
+    cgs2_spatial_async,
+    cholqr2_speculative,
+    cholqr_guard_ok,
+    deim_finish,
+    deim_launch,
     evaluate_rows,
-    gram_schmidt_mass,
+    raise_row_status,
     rowmix,
 )
 from .transport import assemble_operators, source_iteration
@@ -105,50 +111,110 @@ def project_initial(state, x_new, ops):
 def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, use_dsa=True,
                      dsa_penalty="simplified", threads=0, check_state=True, gs_method="cholqr2",
                      sweep_dw=None, comm=None):
-    """Advance one linearised step; returns (new DlrState, CollocationStepInfo)."""
-    selection = deim_select(state.W.values)
+    """Advance one linearised step; returns (new DlrState, CollocationStepInfo).
+
+    Host synchronisations: one before the source iteration (DEIM picks,
+    closure weights and the input checks come back together), one per source
+    iteration (convergence test) and one at the end (Gram-Schmidt guard,
+    row-system status, angular deficiencies, output check).  Errors are raised
+    in the reference's order (dlr_sn.py:99-141).
+    """
+    r = state.rank
+    # ---- DEIM + closure + input checks: one readback ------------------------
+    selection, err_idx = deim_launch(state.W.values)
     closure = selection.closure_weights(state.W.beta)
-    closure_host = closure.cpu().numpy()
-    omegas_sel = quad.omegas[selection.indices]
-
-    penalty_closure = (omegas_sel, closure_host) if dsa_penalty == "collocation" else None
-    ops = assemble_operators(grid, step, dsa_penalty=dsa_penalty, penalty_closure=penalty_closure)
+    ops = assemble_operators(grid, step, dsa_penalty=dsa_penalty, validate=False)
+    bad_sigma = (step.sigma_t - step.sigma_s <= 0).any().to(torch.float64).reshape(1)
+    parts = [err_idx.to(torch.float64), closure, bad_sigma]
     if check_state:
-        state.check(ops, quad)
+        parts.append(state.check_values(ops, quad))
+    host = torch.cat(parts).cpu().numpy()
+    deim_finish(selection, host[:r + 1])                       # InterpolationError
+    closure_host = host[r + 1:2 * r + 1].copy()
+    if host[2 * r + 1]:                                        # transport_sn.py:208-209
+        raise ContractViolation("pseudo absorption sigma_t - sigma_s must stay positive")
+    if check_state:
+        state.raise_check(host[2 * r + 2:])                    # lowrank.py:68-81
+    omegas_sel = quad.omegas[selection.indices]
+    if dsa_penalty == "collocation":
+        ops.penalty_closure = (omegas_sel, closure_host)
 
+    # ---- collocated source iteration (dlr_sn.py:110-121) ---------------------
     flux0 = evaluate_rows(state, selection)
     result = source_iteration(
         ops, omegas_sel, closure_host, psi_time=flux0.values, use_dsa=use_dsa, tol=si_tol,
         max_iters=si_max_iters, phi_start=state.scalar_flux(), threads=threads, dw=sweep_dw,
         comm=comm)
 
-    # new spatial basis from the converged swept columns (dlr_sn.py:123-125)
-    x_new, _, deficient_x = gram_schmidt_mass(ops, result.psi, state.rank + 8, method=gs_method)
-
-    # reduced row solve against the new basis (dlr_sn.py:127-132)
-    r = state.rank
-    proj, packed = project_operators(ops, x_new, x_old=state.X)
-    w_sel = state.W.values[selection.indices_dev]
-    l_time = w_sel @ (state.S.T @ proj["mo"])
-    q_all = (proj["q"][None, :] + step.inv_cdt * l_time).contiguous()
-    om_sel = as_device(omegas_sel).contiguous()
-    l_nodes, l_bar = _row_solve(r, r, packed, om_sel, proj["ms"].contiguous(), q_all, closure)
-
-    # nodal rows -> angular functions through the old basis (dlr_sn.py:134-137)
-    gamma = selection.interpolation_coefficients(l_nodes)
-    l_full = rowmix(state.W.values, gamma)
-    basis_new, r_ang, deficient_w = orthonormalize(l_full, quad)
-
-    new_state = DlrState(X=x_new, S=r_ang.T.contiguous(), W=basis_new)
-    if check_state:
-        new_state.check(ops, quad)
+    # ---- Galerkin side, speculative CholQR2 (dlr_sn.py:123-141) --------------
+    tail = _galerkin_tail(ops, step, quad, state, selection, closure, omegas_sel, result,
+                          gs_method, check_state)
+    if gs_method == "cholqr2" and not tail["gs_ok"]:
+        tail = _galerkin_tail(ops, step, quad, state, selection, closure, omegas_sel, result,
+                              "cgs2", check_state)
+    new_state = tail["state"]
     info = CollocationStepInfo(
         iterations=result.iterations,
         selection=selection,
         angle_indices=selection.indices.copy(),
-        phi=rowmix(x_new, l_bar.reshape(-1, 1))[:, 0],
-        spatial_deficiency=len(deficient_x),
-        angular_deficiency=len(deficient_w),
+        phi=tail["phi"],
+        spatial_deficiency=tail["sdef"],
+        angular_deficiency=tail["adef"],
         si_phi=result.phi,
     )
     return new_state, info
+
+
+def _galerkin_tail(ops, step, quad, state, selection, closure, omegas_sel, result, gs_method,
+                   check_state):
+    r = state.rank
+    co = _cellops_of(ops)
+    if gs_method == "cholqr2":
+        x_new, _, guard = cholqr2_speculative(co, result.psi)
+        defi_x = status_x = None
+    else:
+        x_new, _, defi_x, status_x = cgs2_spatial_async(co, result.psi, r + 8, True)
+        guard = None
+
+    proj, packed = project_operators(ops, x_new, x_old=state.X)
+    w_sel = state.W.values[selection.indices_dev]
+    l_time = w_sel @ (state.S.T @ proj["mo"])
+    q_all = (proj["q"][None, :] + step.inv_cdt * l_time).contiguous()
+    om_sel = quad.omegas_device()[selection.indices_dev].contiguous()
+    l_nodes, l_bar, row_status = _row_solve_async(r, r, packed, om_sel, proj["ms"].contiguous(),
+                                                  q_all, closure)
+    gamma = selection.interpolation_coefficients(l_nodes)
+    l_full = rowmix(state.W.values, gamma)
+    basis_new, r_ang, defi_w, status_w = orthonormalize_async(l_full, quad)
+    new_state = DlrState(X=x_new, S=r_ang.T.contiguous(), W=basis_new)
+
+    parts = [row_status.to(torch.float64), defi_w[:r].to(torch.float64),
+             status_w.to(torch.float64)]
+    if guard is not None:
+        parts.append(guard)
+    else:
+        parts += [defi_x[:r].to(torch.float64), status_x.to(torch.float64)]
+    if check_state:
+        parts.append(new_state.check_values(ops, quad))
+    host = torch.cat(parts).cpu().numpy()
+    o = r + 1
+    row_flags = host[:o]
+    adef = host[o:o + r]
+    st_w = host[o + r]
+    o += r + 1
+    if guard is not None:
+        gs_ok = cholqr_guard_ok(host[o:o + 2 * r + 1], r)
+        o += 2 * r + 1
+        if not gs_ok:
+            return {"gs_ok": False}
+        sdef = 0
+    else:
+        sdef = len(_cgs2_flags(host[o:o + r], host[o + r:o + r + 1], r))
+        o += r + 1
+    raise_row_status(row_flags, r)                             # SolverError
+    _cgs2_flags(adef, [st_w], r)                               # ContractViolation
+    if check_state:
+        new_state.raise_check(host[o:])
+    return {"gs_ok": True, "state": new_state, "sdef": sdef,
+            "adef": int(np.count_nonzero(adef)),
+            "phi": rowmix(x_new, l_bar.reshape(-1, 1))[:, 0]}

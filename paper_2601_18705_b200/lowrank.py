@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import as_device, device, empty, stream, to_numpy, zeros
+from ._device import as_device, cached_upload, device, empty, stream, to_numpy, zeros
 from .angular import AngularBasis
 from .errors import ContractViolation, InterpolationError, SolverError
 from .mesh import cellops_struct
@@ -124,42 +124,74 @@ def gram_schmidt_mass(ops, columns, completion_count=None, strict=True, method="
     if completion_count is None:
         completion_count = m + 8
     if method == "cholqr2":
-        G = mass_gram(co, cols)
-        R1, R1inv, ratio, flag = _chol(G)
-        host = torch.cat([ratio, flag.to(torch.float64)]).cpu().numpy()
-        rel, dec = host[:m], host[m:2 * m]
-        # CholQR's R_kk is accurate to ~eps/rel^2: trust it when every column
-        # keeps rel >= CHOLQR_GUARD of its norm and sits far (100x) above the
-        # reference's deficiency threshold 1e-12 * max(orig, 1)
-        if (host[-1] == 0 and float(rel.min(initial=np.inf)) >= CHOLQR_GUARD
-                and float(dec.min(initial=np.inf)) >= 1e-10):
-            X1 = rowmix(cols, R1inv)
-            R2, R2inv, _, _ = _chol(mass_gram(co, X1))
-            X = rowmix(X1, R2inv)
-            return X, R2 @ R1, []
+        X, R, guard = cholqr2_speculative(co, cols)
+        if cholqr_guard_ok(guard.cpu().numpy(), m):
+            return X, R, []
     elif method != "cgs2":
         raise ContractViolation(f"unknown Gram-Schmidt method {method!r}")
-    return _cgs2(n, m, cols, metric=1, ops=co, comp_kind=1,
-                 comp_exp=np.asarray(spatial_monomial_exponents(completion_count), np.int32),
-                 coords=np.asarray([co.x0, co.y0, co.nx * co.dx, co.ny * co.dy]), strict=strict)
+    Q, R, defi, status = cgs2_spatial_async(co, cols, completion_count, strict)
+    return Q, R, _cgs2_flags(defi.cpu().numpy(), status.cpu().numpy(), m)
 
 
-def _cgs2(n, m, cols, *, metric, ops=None, weights=None, comp_kind, comp_exp, coords, strict=True):
+def cholqr2_speculative(co, cols):
+    """Two Cholesky-QR passes in the M inner product without a host sync;
+    returns (X, R, guard) with guard = first-pass diag ratios (2m) + the
+    non-positive-pivot flag, to be checked with cholqr_guard_ok."""
+    G = mass_gram(co, cols)
+    R1, R1inv, ratio, flag = _chol(G)
+    X1 = rowmix(cols, R1inv)
+    R2, R2inv, _, _ = _chol(mass_gram(co, X1))
+    X = rowmix(X1, R2inv)
+    return X, R2 @ R1, torch.cat([ratio, flag.to(torch.float64)])
+
+
+def cholqr_guard_ok(host_guard, m):
+    """CholQR's R_kk is accurate to ~eps/rel^2: trust it when every column
+    keeps rel >= CHOLQR_GUARD of its norm and sits far (100x) above the
+    reference's deficiency threshold 1e-12 * max(orig, 1) (angular.py:137)."""
+    rel, dec = host_guard[:m], host_guard[m:2 * m]
+    return (host_guard[-1] == 0 and float(rel.min(initial=np.inf)) >= CHOLQR_GUARD
+            and float(dec.min(initial=np.inf)) >= 1e-10)
+
+
+def cgs2_spatial_async(co, cols, completion_count, strict=True):
+    n, m = cols.shape
+    return _cgs2_async(n, m, cols, metric=1, ops=co, comp_kind=1,
+                       comp_exp=np.asarray(spatial_monomial_exponents(completion_count), np.int32),
+                       coords=np.asarray([co.x0, co.y0, co.nx * co.dx, co.ny * co.dy]),
+                       strict=strict)
+
+
+def _cgs2_flags(defi, status, m):
+    if int(status[0]) != 0:
+        raise ContractViolation("ran out of completion vectors during orthonormalization")
+    return [int(k) for k in np.flatnonzero(defi[:m])]
+
+
+def _cgs2_async(n, m, cols, *, metric, ops=None, weights=None, comp_kind, comp_exp, coords,
+                strict=True):
+    """Exact CGS2 kernel without a host sync: (Q, R, deficient flags, status)."""
     Q = zeros(n, m)
     R = zeros(m, m)
     defi = _i32(max(m, 1))
     status = _i32(1)
     work = empty(int(_lib.load().dlrsn_cgs2_workspace_len(n)))
     ncomp = comp_exp.shape[0]
-    exp_dev = as_device(comp_exp.reshape(-1), dtype=torch.int32) if ncomp else _i32(1)
+    exp_dev = (cached_upload(("exp", comp_exp.shape, comp_exp.tobytes()),
+                             lambda: comp_exp.reshape(-1).astype(np.int32)) if ncomp else _i32(1))
+    if not isinstance(coords, torch.Tensor):
+        c = np.asarray(coords, dtype=np.float64)
+        coords = cached_upload(("coords", c.shape, c.tobytes()), lambda: c)
     _lib.call("dlrsn_cgs2", n, m, _lib.ptr(cols), cols.stride(0), _lib.ptr(Q), m, _lib.ptr(R),
               _lib.ptr(defi), metric, _lib.ptr(weights), None if ops is None else _addr(ops),
-              comp_kind, ncomp, _lib.ptr(exp_dev), _lib.ptr(as_device(coords)), _lib.ptr(work),
+              comp_kind, ncomp, _lib.ptr(exp_dev), _lib.ptr(coords), _lib.ptr(work),
               _lib.ptr(status), int(bool(strict)), stream())
-    flags = defi[:m].cpu().numpy()
-    if int(status.item()) != 0:
-        raise ContractViolation("ran out of completion vectors during orthonormalization")
-    return Q, R, [int(k) for k in np.flatnonzero(flags)]
+    return Q, R, defi, status
+
+
+def _cgs2(n, m, cols, **kw):
+    Q, R, defi, status = _cgs2_async(n, m, cols, **kw)
+    return Q, R, _cgs2_flags(defi.cpu().numpy(), status.cpu().numpy(), m)
 
 
 @dataclass(eq=False)
@@ -190,23 +222,28 @@ class DlrState:
     def angular_coefficients(self):
         return self.W.values @ self.S.T
 
-    def check(self, ops, quad, tol=1e-10):
-        """Both factors orthonormal in their inner products (lowrank.py:68-81)."""
+    def check_values(self, ops, quad):
+        """Device tensor [max|X^T M X - I|, max|W^T D W - I|(, pin drift)]."""
         gx = mass_gram(ops, self.X)
         eye = torch.eye(self.rank, dtype=torch.float64, device=device())
         w = quad.weights_device()
         gw = (self.W.values * w[:, None]).T @ self.W.values
-        vals = torch.stack([(gx - eye).abs().max(), (gw - eye).abs().max()])
+        vals = [(gx - eye).abs().max(), (gw - eye).abs().max()]
         if self.W.pinned:
-            pin = (self.W.values[:, 0] - 1.0 / np.sqrt(FOUR_PI)).abs().max()
-            vals = torch.cat([vals, pin.reshape(1)])
-        host = vals.cpu().numpy()
-        rx, rw = float(host[0]), float(host[1])
+            vals.append((self.W.values[:, 0] - 1.0 / np.sqrt(FOUR_PI)).abs().max())
+        return torch.stack(vals)
+
+    def raise_check(self, host_vals, tol=1e-10):
+        rx, rw = float(host_vals[0]), float(host_vals[1])
         if rx > tol or rw > tol:
             raise ContractViolation(f"factor orthonormality violated: spatial {rx:.2e}, angular {rw:.2e}")
-        if self.W.pinned and float(host[2]) > tol:
-            raise ContractViolation(f"constant column drifted by {float(host[2]):.2e}")
+        if self.W.pinned and float(host_vals[2]) > tol:
+            raise ContractViolation(f"constant column drifted by {float(host_vals[2]):.2e}")
         return rx, rw
+
+    def check(self, ops, quad, tol=1e-10):
+        """Both factors orthonormal in their inner products (lowrank.py:68-81)."""
+        return self.raise_check(self.check_values(ops, quad).cpu().numpy(), tol)
 
     def to_numpy(self):
         return to_numpy(self.X), to_numpy(self.S), to_numpy(self.W.values)
@@ -225,7 +262,7 @@ class DeimSelection:
 
     @property
     def rank(self):
-        return self.indices.size
+        return self.indices_dev.numel()
 
     @cached_property
     def cond(self):
@@ -258,21 +295,33 @@ def deim_select(basis_values):
     n, r = W.shape
     if r > n:
         raise ContractViolation(f"rank {r} exceeds the {n} available nodes")
-    W = W.contiguous()
+    sel, err_idx = deim_launch(W)
+    return deim_finish(sel, err_idx.cpu().numpy())
+
+
+def deim_launch(W):
+    """Launch DEIM without a host sync: (selection with device-side factors,
+    int32 [err_col, idx...]) -- see deim_finish."""
+    W = as_device(W).contiguous()
+    n, r = W.shape
     work = empty(n, r)
-    idx = _i32(r)
+    err_idx = _i32(r + 1)
     lhat, u = empty(r, r), empty(r, r)
-    err = _i32(1)
-    _lib.call("dlrsn_deim", n, r, _lib.ptr(work), _lib.ptr(W), _lib.ptr(idx), _lib.ptr(lhat),
-              _lib.ptr(u), _lib.ptr(err), stream())
-    host = torch.cat([err, idx]).cpu().numpy()
-    if host[0] >= 0:
+    _lib.call("dlrsn_deim", n, r, _lib.ptr(work), _lib.ptr(W), _lib.ptr(err_idx[1:]),
+              _lib.ptr(lhat), _lib.ptr(u), _lib.ptr(err_idx[:1]), stream())
+    idx_dev = err_idx[1:].to(torch.int64)
+    sel = DeimSelection(indices=None, indices_dev=idx_dev, w_hat=W[idx_dev].contiguous(),
+                        lhat=lhat, u=u)
+    return sel, err_idx
+
+
+def deim_finish(sel, host_err_idx):
+    """Raise InterpolationError (lowrank.py:192-199) or attach host indices."""
+    if host_err_idx[0] >= 0:
         raise InterpolationError("interpolation residual vanished; basis is rank deficient",
-                                 column=int(host[0]))
-    indices = host[1:].astype(np.int64)
-    idx_dev = idx.to(torch.int64)
-    return DeimSelection(indices=indices, indices_dev=idx_dev, w_hat=W[idx_dev].contiguous(),
-                         lhat=lhat, u=u)
+                                 column=int(host_err_idx[0]))
+    sel.indices = np.asarray(host_err_idx[1:], dtype=np.int64)
+    return sel
 
 
 @dataclass(eq=False)
@@ -296,22 +345,32 @@ def reconstruct_scalar_flux(flux):
     return flux.scalar_flux()
 
 
-def _row_solve(n, r, proj_or_B, om_sel, ms, Q, weights):
+def _row_solve_async(n, r, proj_or_B, om_sel, ms, Q, weights):
+    """Row solve without host sync: returns (L, lbar, status) with status
+    (n + 1 ints) = per-node singular flags, then the coupled-system flag."""
     Binv = empty(n, r, r)
-    st = _i32(max(n, 1))
+    status = _i32(n + 1)
     _lib.call("dlrsn_row_inverse", n, r, _lib.ptr(proj_or_B), _lib.ptr(om_sel), _lib.ptr(Binv),
-              None, _lib.ptr(st), stream())
+              None, _lib.ptr(status), stream())
     L = empty(n, r)
     lbar = empty(r)
-    st2 = _i32(1)
     _lib.call("dlrsn_row_combine", n, r, _lib.ptr(Binv), _lib.ptr(ms), _lib.ptr(Q),
-              _lib.ptr(weights), _lib.ptr(L), _lib.ptr(lbar), _lib.ptr(st2), stream())
-    flags = torch.cat([st[:n], st2]).cpu().numpy()
-    bad = np.flatnonzero(flags[:n])
+              _lib.ptr(weights), _lib.ptr(L), _lib.ptr(lbar), _lib.ptr(status[n:]), stream())
+    return L, lbar, status
+
+
+def raise_row_status(flags, n):
+    """SolverError naming the first singular node (lowrank.py:246-252)."""
+    bad = np.flatnonzero(np.asarray(flags)[:n])
     if bad.size:
         raise SolverError(f"singular reduced transport operator at node {int(bad[0])}")
-    if flags[n]:
+    if np.asarray(flags)[n]:
         raise SolverError("singular closure-coupled reduced system")
+
+
+def _row_solve(n, r, proj_or_B, om_sel, ms, Q, weights):
+    L, lbar, status = _row_solve_async(n, r, proj_or_B, om_sel, ms, Q, weights)
+    raise_row_status(status.cpu().numpy(), n)
     return L, lbar
 
 

@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import as_device, device, empty, stream, zeros
+from ._device import as_device, device, empty, stream, upload, zeros
 from .errors import ConfigurationError, ContractViolation, IterationLimitError
 from .mesh import DISCONTINUOUS, cellops_struct
 
@@ -75,8 +75,7 @@ def plan_groups(omegas, closure, n_strips, dw=None, sm_count=148):
 
 
 def _groups_to_device(groups):
-    raw = np.frombuffer(groups.tobytes(), dtype=np.uint8)
-    return torch.from_numpy(raw.copy()).to(device())
+    return upload(np.frombuffer(groups.tobytes(), dtype=np.uint8).copy())
 
 
 @dataclass(eq=False)
@@ -148,14 +147,15 @@ class DiscreteOperators:
         return (as_device(cell_values)[:, None] * row[None, :]).reshape(-1)
 
 
-def assemble_operators(grid, step, dsa_penalty="simplified", penalty_closure=None):
-    """Per-step operator data (transport_sn.py:201-300); same checks."""
+def assemble_operators(grid, step, dsa_penalty="simplified", penalty_closure=None, validate=True):
+    """Per-step operator data (transport_sn.py:201-300); same checks
+    (``validate=False`` defers the device-side sigma check to the caller)."""
     if grid.flavor != DISCONTINUOUS:
         raise ContractViolation("sweep transport needs the discontinuous dof layout")
     for name in ("sigma_t", "sigma_s", "q"):
         if tuple(getattr(step, name).shape) != (grid.n_cells,):
             raise ContractViolation(f"step field {name} must be per-cell")
-    if bool((step.sigma_t - step.sigma_s <= 0).any()):
+    if validate and bool((step.sigma_t - step.sigma_s <= 0).any()):
         raise ContractViolation("pseudo absorption sigma_t - sigma_s must stay positive")
     if dsa_penalty not in ("simplified", "collocation"):
         raise ContractViolation(f"unknown dsa penalty variant {dsa_penalty!r}")
@@ -182,7 +182,7 @@ class _SweepPlan:
         self.G = len(self.groups)
         self.D = len(quads)
         self.groups_dev = _groups_to_device(self.groups)
-        self.quads_dev = torch.from_numpy(quads).to(device())
+        self.quads_dev = upload(quads)
         self.ws_bytes = int(_lib.load().dlrsn_sweep_workspace_bytes(g.nx, g.ny, self.G, self.dw))
         self.workspace = sweep_workspace(ops, self.ws_bytes)
 
@@ -301,7 +301,10 @@ def source_iteration(ops, omegas, closure, psi_time=None, *, use_dsa=True, tol=1
     vl = ops.vec_len
     rhs_sk = ops.buffer("rhs_sk", max(nl, 1) * vl)
     psi_sk = ops.buffer("psi_sk", max(nl, 1) * vl)
-    part = ops.buffer("phi_part", (plan.G if plan else 1) * vl)
+    # single-direction groups: the closure is read from psi itself (no partials)
+    use_part = plan is not None and plan.dw > 1
+    part = ops.buffer("phi_part", (plan.G if use_part else 1) * vl)
+    part_arg = part if use_part else None
     scat = ops.buffer("scat_sk4", 4 * vl)
 
     def local_cols(a):
@@ -328,18 +331,18 @@ def source_iteration(ops, omegas, closure, psi_time=None, *, use_dsa=True, tol=1
     change = math.inf
     for it in range(1, max_iters + 1):
         if owners is None:
-            _sweep(ops, plan, rhs_sk, psi_sk, scat, part)
+            _sweep(ops, plan, rhs_sk, psi_sk, scat, part_arg)
             _lib.call("dlrsn_phi_combine", ops.cellops_ptr, plan.G, _lib.ptr(plan.groups_dev),
-                      _lib.ptr(part), _lib.ptr(phi), _lib.ptr(st.sigma_s), _lib.ptr(phi_new),
-                      _lib.ptr(scat), _lib.ptr(norms), _lib.ptr(red_ws), stream())
+                      _lib.ptr(part_arg), _lib.ptr(psi_sk), _lib.ptr(phi), _lib.ptr(st.sigma_s),
+                      _lib.ptr(phi_new), _lib.ptr(scat), _lib.ptr(norms), _lib.ptr(red_ws), stream())
         else:
             # local partial closure flux -> allreduce over NVLink -> norms and
             # scattering source from the summed flux (identical on all ranks)
             if plan:
-                _sweep(ops, plan, rhs_sk, psi_sk, scat, part)
+                _sweep(ops, plan, rhs_sk, psi_sk, scat, part_arg)
                 _lib.call("dlrsn_phi_combine", ops.cellops_ptr, plan.G, _lib.ptr(plan.groups_dev),
-                          _lib.ptr(part), _lib.ptr(phi), _lib.ptr(st.sigma_s), _lib.ptr(phi_new),
-                          None, _lib.ptr(norms), _lib.ptr(red_ws), stream())
+                          _lib.ptr(part_arg), _lib.ptr(psi_sk), _lib.ptr(phi), _lib.ptr(st.sigma_s),
+                          _lib.ptr(phi_new), None, _lib.ptr(norms), _lib.ptr(red_ws), stream())
             else:
                 phi_new.zero_()
             comm.allreduce_sum_(phi_new)
