@@ -253,6 +253,122 @@ __global__ void __launch_bounds__(kCgT) cgs2_grid_kernel(Cgs2Args g) {
   }
 }
 
+// Single-CTA variant with Q, the work vector and the weights resident in
+// shared memory (used when n (m + 2) doubles fit): every inner product is a
+// block reduction, no global round trips.  Same operation order and
+// decisions as cgs2_grid_kernel.
+constexpr int kSmT = 1024;
+
+__device__ double block_dot(double v, double* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(kFull, v, o);
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int q = 0; q < nw; ++q) s += red[q];
+  return s;
+}
+
+__global__ void __launch_bounds__(kSmT) cgs2_smem_kernel(Cgs2Args g) {
+  extern __shared__ double sm[];
+  const int n = g.n, m = g.m;
+  const int lq = m | 1;                  // odd row stride: conflict-free column walks
+  double* Qs = sm;                       // n x lq
+  double* work = Qs + (size_t)n * lq;    // n
+  double* wts = work + n;                // n (metric 0 weights)
+  double* coef = wts + n;                // m
+  double* total = coef + m;              // m
+  __shared__ double red[32];
+  const double tol = 1e-12;
+  const int rpu = g.metric == 0 ? 1 : 4;
+  const int units = n / rpu;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) wts[i] = g.metric == 0 ? g.w[i] : 0.0;
+  __syncthreads();
+
+  auto mw_of = [&](int u, int l) -> double {  // (metric applied to work)[u*rpu + l]
+    if (rpu == 1) return wts[u] * work[u];
+    const double* x = work + 4 * u;
+    return g.ops.mass[4 * l] * x[0] + g.ops.mass[4 * l + 1] * x[1] + g.ops.mass[4 * l + 2] * x[2] +
+           g.ops.mass[4 * l + 3] * x[3];
+  };
+  auto norm2 = [&]() -> double {
+    double acc = 0.0;
+    for (int u = threadIdx.x; u < units; u += blockDim.x)
+      for (int l = 0; l < rpu; ++l) acc += work[u * rpu + l] * mw_of(u, l);
+    return block_dot(acc, red);
+  };
+  // mw = metric applied to work, materialised once per pass; then warp w
+  // computes the coefficients i = w, w + 32, ... over all rows (lane-strided,
+  // shuffle-reduced: fixed order), one block barrier per pass
+  double* mw = total + m;                // n
+  auto project_twice = [&](int k, bool keep) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int u = threadIdx.x; u < units; u += blockDim.x)
+        for (int l = 0; l < rpu; ++l) mw[u * rpu + l] = mw_of(u, l);
+      __syncthreads();
+      for (int i = wid; i < k; i += nw) {
+        double acc = 0.0;
+        for (int r = lane; r < n; r += 32) acc += Qs[(size_t)r * lq + i] * mw[r];
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(kFull, acc, o);
+        if (lane == 0) {
+          coef[i] = acc;
+          if (keep) total[i] = pass == 0 ? acc : total[i] + acc;
+        }
+      }
+      __syncthreads();
+      for (int r = threadIdx.x; r < n; r += blockDim.x) {
+        double x = work[r];
+        for (int i = 0; i < k; ++i) x -= Qs[(size_t)r * lq + i] * coef[i];
+        work[r] = x;
+      }
+      __syncthreads();
+    }
+  };
+
+  int next_cand = 0;
+  const int max_cand = g.comp_kind == 0 ? g.ncomp + n : g.ncomp;
+  for (int k = 0; k < m; ++k) {
+    for (int r = threadIdx.x; r < n; r += blockDim.x) work[r] = g.cols[(int64_t)r * g.ldc + k];
+    __syncthreads();
+    const double orig = sqrt(fmax(norm2(), 0.0));
+    project_twice(k, true);
+    const double nrm = sqrt(fmax(norm2(), 0.0));
+    for (int i = threadIdx.x; i < m; i += blockDim.x) g.R[(int64_t)i * m + k] = i < k ? total[i] : 0.0;
+    if (nrm <= tol * fmax(orig, 1.0)) {
+      if (threadIdx.x == 0) g.deficient[k] = 1;
+      bool placed = false;
+      while (next_cand < max_cand) {
+        const int cand = next_cand++;
+        for (int r = threadIdx.x; r < n; r += blockDim.x) work[r] = cand_value(g, cand, r);
+        __syncthreads();
+        const double c0 = sqrt(fmax(norm2(), 0.0));
+        project_twice(k, false);
+        const double c1 = sqrt(fmax(norm2(), 0.0));
+        if (c1 > sqrt(tol) * fmax(c0, 1.0)) {
+          for (int r = threadIdx.x; r < n; r += blockDim.x) Qs[(size_t)r * lq + k] = work[r] / c1;
+          placed = true;
+          break;
+        }
+      }
+      if (!placed) {
+        if (threadIdx.x == 0 && g.strict) *g.status = 1;
+        for (int r = threadIdx.x; r < n; r += blockDim.x) Qs[(size_t)r * lq + k] = 0.0;
+      }
+    } else {
+      if (threadIdx.x == 0) {
+        g.deficient[k] = 0;
+        g.R[(int64_t)k * m + k] = nrm;
+      }
+      for (int r = threadIdx.x; r < n; r += blockDim.x) Qs[(size_t)r * lq + k] = work[r] / nrm;
+    }
+    __syncthreads();
+  }
+  for (int64_t e = threadIdx.x; e < (int64_t)n * m; e += blockDim.x)
+    g.Q[(e / m) * g.ldq + e % m] = Qs[(size_t)(e / m) * lq + e % m];
+}
+
 }  // namespace dlrsn
 
 using namespace dlrsn;
@@ -275,6 +391,15 @@ int dlrsn_cgs2(int n, int m, const double* cols, int ldc, double* Q, int ldq, do
   g.comp_kind = comp_kind; g.ncomp = ncomp; g.comp_exp = comp_exp; g.coords = coords;
   g.work = workspace;
   g.status = status; g.strict = strict;
+  const size_t lq = (size_t)(m | 1);
+  const size_t smem_res = ((size_t)n * lq + 3 * (size_t)n + 2 * (size_t)m) * sizeof(double);
+  if (smem_res <= 200 * 1024 && (metric == 0 || n <= 16384)) {
+    DLRSN_TRY_CUDA(cudaFuncSetAttribute(cgs2_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem_res));
+    cgs2_smem_kernel<<<1, kSmT, smem_res, as_stream(stream)>>>(g);
+    DLRSN_CHECK_LAUNCH("cgs2_smem_kernel");
+    return DLRSN_OK;
+  }
   int dev = 0, sms = 0, occ = 0;
   DLRSN_TRY_CUDA(cudaGetDevice(&dev));
   DLRSN_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

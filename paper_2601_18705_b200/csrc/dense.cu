@@ -570,9 +570,12 @@ __global__ void row_combine_kernel(int n, int r, const double* __restrict__ Binv
 // the interpolation residual W[:,j] - W[:,:j] W[p,:j]^-1 W[p,j]; the pivot is
 // its first maximal |entry| (np.argmax).  Produces the picks, the unit lower
 // factor rows L[p,:] and U (so W[p,:] = Lhat U), all in pick order.
-__global__ void deim_kernel(int n, int r, double* __restrict__ Wk /* n x r work copy */,
+__global__ void deim_kernel(int n, int r, double* __restrict__ Wk_global /* n x r work copy */,
                             const double* __restrict__ W, int* __restrict__ idx,
-                            double* __restrict__ Lhat, double* __restrict__ U, int* err_col) {
+                            double* __restrict__ Lhat, double* __restrict__ U, int* err_col,
+                            int in_smem) {
+  extern __shared__ double dsm[];
+  double* Wk = in_smem ? dsm : Wk_global;  // work copy resident in smem when it fits
   __shared__ double bv[33];
   __shared__ int bi[32];
   __shared__ int pick;
@@ -658,33 +661,54 @@ __global__ void deim_kernel(int n, int r, double* __restrict__ Wk /* n x r work 
 __global__ void what_solve_kernel(int r, int m, const double* __restrict__ Lhat,
                                   const double* __restrict__ U, const double* __restrict__ V,
                                   double* __restrict__ X, int mode) {
-  for (int c = threadIdx.x; c < m; c += blockDim.x) {
+  extern __shared__ double sw[];
+  double* sL = sw;               // r x r
+  double* sU = sL + r * r;       // r x r
+  double* sX = sU + r * r;       // r x m
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+    sL[e] = Lhat[e];
+    sU[e] = U[e];
+  }
+  for (int e = threadIdx.x; e < r * m; e += blockDim.x) sX[e] = V[e];
+  __syncthreads();
+  // one warp per right-hand side: the row recurrences are sequential, the
+  // inner products over the solved entries are split across the lanes
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int c = warp; c < m; c += nw) {
     if (mode == 0) {
-      // L y = v (forward), U x = y (backward)
-      for (int i = 0; i < r; ++i) {
-        double s = V[i * m + c];
-        for (int p = 0; p < i; ++p) s -= Lhat[i * r + p] * X[p * m + c];
-        X[i * m + c] = s;
+      for (int i = 0; i < r; ++i) {  // L y = v
+        double s = 0.0;
+        for (int p = lane; p < i; p += 32) s += sL[i * r + p] * sX[p * m + c];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(kFull, s, o);
+        if (lane == 0) sX[i * m + c] -= s;
+        __syncwarp();
       }
-      for (int i = r - 1; i >= 0; --i) {
-        double s = X[i * m + c];
-        for (int p = i + 1; p < r; ++p) s -= U[i * r + p] * X[p * m + c];
-        X[i * m + c] = s / U[i * r + i];
+      for (int i = r - 1; i >= 0; --i) {  // U x = y
+        double s = 0.0;
+        for (int p = i + 1 + lane; p < r; p += 32) s += sU[i * r + p] * sX[p * m + c];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(kFull, s, o);
+        if (lane == 0) sX[i * m + c] = (sX[i * m + c] - s) / sU[i * r + i];
+        __syncwarp();
       }
     } else {
-      // U^T y = v (forward), L^T x = y (backward)
-      for (int i = 0; i < r; ++i) {
-        double s = V[i * m + c];
-        for (int p = 0; p < i; ++p) s -= U[p * r + i] * X[p * m + c];
-        X[i * m + c] = s / U[i * r + i];
+      for (int i = 0; i < r; ++i) {  // U^T y = v
+        double s = 0.0;
+        for (int p = lane; p < i; p += 32) s += sU[p * r + i] * sX[p * m + c];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(kFull, s, o);
+        if (lane == 0) sX[i * m + c] = (sX[i * m + c] - s) / sU[i * r + i];
+        __syncwarp();
       }
-      for (int i = r - 1; i >= 0; --i) {
-        double s = X[i * m + c];
-        for (int p = i + 1; p < r; ++p) s -= Lhat[p * r + i] * X[p * m + c];
-        X[i * m + c] = s;
+      for (int i = r - 1; i >= 0; --i) {  // L^T x = y
+        double s = 0.0;
+        for (int p = i + 1 + lane; p < r; p += 32) s += sL[p * r + i] * sX[p * m + c];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(kFull, s, o);
+        if (lane == 0) sX[i * m + c] -= s;
+        __syncwarp();
       }
     }
   }
+  __syncthreads();
+  for (int e = threadIdx.x; e < r * m; e += blockDim.x) X[e] = sX[e];
 }
 
 }  // namespace dlrsn
@@ -810,14 +834,24 @@ int dlrsn_row_combine(int n, int r, const double* Binv, const double* ms, const 
 int dlrsn_deim(int n, int r, double* Wwork, const double* W, int* idx, double* Lhat, double* U,
                int* err_col, dlrsn_stream_t stream) {
   DLRSN_REQUIRE(r <= n, "rank %d exceeds the %d available nodes", r, n);
-  deim_kernel<<<1, 1024, 0, as_stream(stream)>>>(n, r, Wwork, W, idx, Lhat, U, err_col);
+  const size_t smem = (size_t)n * r * sizeof(double);
+  const int in_smem = smem <= 200 * 1024;
+  if (in_smem)
+    DLRSN_TRY_CUDA(cudaFuncSetAttribute(deim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+  deim_kernel<<<1, 1024, in_smem ? smem : 0, as_stream(stream)>>>(n, r, Wwork, W, idx, Lhat, U,
+                                                                  err_col, in_smem);
   DLRSN_CHECK_LAUNCH("deim_kernel");
   return DLRSN_OK;
 }
 
 int dlrsn_what_solve(int r, int m, const double* Lhat, const double* U, const double* V,
                      double* X, int mode, dlrsn_stream_t stream) {
-  what_solve_kernel<<<1, 128, 0, as_stream(stream)>>>(r, m, Lhat, U, V, X, mode);
+  const size_t smem = (2 * (size_t)r * r + (size_t)r * m) * sizeof(double);
+  DLRSN_REQUIRE(smem <= 200 * 1024, "W_hat solve too large for shared memory");
+  DLRSN_TRY_CUDA(cudaFuncSetAttribute(what_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+  what_solve_kernel<<<1, 512, smem, as_stream(stream)>>>(r, m, Lhat, U, V, X, mode);
   DLRSN_CHECK_LAUNCH("what_solve_kernel");
   return DLRSN_OK;
 }
