@@ -204,9 +204,9 @@ def main():
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 512 MB > L2
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    transport.SWEEP_EVENTS = []
+    _lib.call("dlrsn_sweep_timing", 1)  # CUDA events around every sweep launch
     iters = []
-    launches0 = _lib.launch_count[0]
+    launches0 = _lib.launch_count()
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -220,7 +220,7 @@ def main():
             iters.append(info.iterations)
         torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
-    launches = _lib.launch_count[0] - launches0 - args.steps * 0
+    launches = _lib.launch_count() - launches0
     if ws > 1:
         torch.distributed.barrier()
     ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
@@ -228,10 +228,8 @@ def main():
         t = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    sweeps = transport.SWEEP_EVENTS
-    transport.SWEEP_EVENTS = None
-    sweep_ms = [s.elapsed_time(e) for s, e, *_ in sweeps]
-    n_cells, D, G = sweeps[0][2], sweeps[0][3], sweeps[0][4]
+    sweep_ms, sweep_groups = _sweep_timings(_lib)
+    n_cells, D = spec.n_cells, int(sweep_groups[0])  # single-direction groups: D = G
     updates = sum(spec.n_cells * spec.rank * it for it in iters)
     value = updates / (ms * 1e-3)
     peak, peak_kind = _peaks()
@@ -333,6 +331,23 @@ def measure_e2e(dp, state, T, lin, n, comm=None):
     return {"value": spec.n_cells * spec.rank * iters / (ms * 1e-3), "unit": UNIT,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "steps": n, "ms_per_step": ms / n}
+
+
+def _sweep_timings(_lib):
+    """Per-launch sweep times recorded by the library (dlrsn_sweep_timing)."""
+    import ctypes
+
+    cap = 4096
+    ms = (ctypes.c_float * cap)()
+    groups = (ctypes.c_int * cap)()
+    dw = (ctypes.c_int * cap)()
+    cnt = ctypes.c_int()
+    _lib.call("dlrsn_sweep_timing_read", cap, ms, groups, dw, ctypes.byref(cnt))
+    _lib.call("dlrsn_sweep_timing", 0)
+    n = min(cnt.value, cap)
+    if n == 0 or any(dw[k] != 1 for k in range(n)):
+        raise RuntimeError("sweep timing: expected single-direction groups")
+    return [ms[k] for k in range(n)], [groups[k] for k in range(n)]
 
 
 def measure_full_sn(dp, comm=None, reps=3):

@@ -45,8 +45,11 @@ enum {
   DLRSN_ENONFINITE = -3,  /* SolverError (non-finite values) */
   DLRSN_ECUDA = -4,       /* CUDA runtime failure */
   DLRSN_EINTERP = -5,     /* InterpolationError */
-  DLRSN_ECOMPLETION = -6  /* ContractViolation: ran out of completion vectors */
+  DLRSN_ECOMPLETION = -6, /* ContractViolation: ran out of completion vectors */
+  DLRSN_EITER = -7        /* IterationLimitError (info->iterations, info->residual) */
 };
+
+#define DLRSN_MAX_RANK 128 /* largest rank r of the step-level entry point */
 
 #define DLRSN_MAX_DW 8 /* directions per sweep group (one warp) */
 
@@ -76,6 +79,8 @@ typedef struct dlrsn_group {
 
 int dlrsn_version(void);
 const char* dlrsn_last_error(void);
+/* number of kernels this library has launched since it was loaded */
+int64_t dlrsn_launch_count(void);
 int dlrsn_device_sm_count(int* out);
 
 int64_t dlrsn_sk_vec_len(int nx, int ny);
@@ -84,6 +89,12 @@ int64_t dlrsn_sk_scalar_len(int nx, int ny);
  * workspace must be initialised once with dlrsn_sweep_workspace_init (the
  * sweep leaves it re-armed, so it can be reused across launches and plans).
  * Word 1 of the workspace is a sticky status (2 = a handoff wait timed out). */
+/* Measurement hook: while enabled, every dlrsn_sweep records a CUDA event
+ * pair around its launch on the caller's stream; _read synchronises on them
+ * and returns per-launch ms, group count and width (cap entries at most;
+ * *count = launches recorded).  Enabling resets the list. */
+int dlrsn_sweep_timing(int enable);
+int dlrsn_sweep_timing_read(int cap, float* ms, int* groups, int* dw, int* count);
 int64_t dlrsn_sweep_workspace_bytes(int nx, int ny, int n_groups, int dw);
 int dlrsn_sweep_workspace_init(void* workspace, int64_t workspace_bytes, dlrsn_stream_t stream);
 /* debug: record globaltimer per (work item, chunk) before/after the strip
@@ -249,6 +260,68 @@ int dlrsn_cgs2(int n, int m, const double* cols, int ldc, double* Q, int ldq, do
                int* deficient, int metric, const double* w, const dlrsn_cellops* ops,
                int comp_kind, int ncomp, const int* comp_exp, const double* coords,
                double* workspace, int* status, int strict, dlrsn_stream_t stream);
+
+/* ---- One whole step (dlr_sn.py:86-151) ----------------------------------- */
+
+typedef struct dlrsn_step_params {
+  int rank;                  /* r <= DLRSN_MAX_RANK */
+  int n_omega;               /* quadrature size */
+  const double* omegas_host; /* (n_omega, 3), HOST */
+  const double* omegas_dev;  /* (n_omega, 3), device */
+  const double* weights_dev; /* (n_omega), device */
+  double inv_cdt;            /* LinearizedStep.inv_cdt */
+  double si_tol;             /* source iteration tolerance */
+  int si_max_iters;
+  int check_state;           /* DlrState.check on input and output */
+  int gs_method;             /* 0: CholQR2 guarded by exact CGS2, 1: exact CGS2 */
+  int sweep_dw;              /* sweep group width (0 = 1) */
+} dlrsn_step_params;
+
+typedef struct dlrsn_step_info { /* HOST, filled by the call */
+  int iterations;
+  int spatial_deficiency;
+  int angular_deficiency;
+  int error_index;           /* InterpolationError column / singular node, else -1 */
+  int gs_fallback;           /* 1 if the exact CGS2 pass replaced CholQR2 */
+  double residual;           /* last source-iteration change */
+  double check_in[2];        /* input orthonormality residuals (spatial, angular) */
+  double check_out[2];
+  int64_t angle_indices[DLRSN_MAX_RANK];
+  double closure[DLRSN_MAX_RANK];
+} dlrsn_step_info;
+
+/* Multi-GPU hooks (NULL = one GPU): the step calls allreduce_sum(user) to
+ * sum reduce_buf (n_dofs doubles, device) over ranks once per source
+ * iteration, and allgather(user) to gather gather_send (n_dofs x
+ * gather_width) of every rank into gather_recv (world_size blocks). */
+typedef struct dlrsn_comm {
+  int rank, world_size;
+  void* user;
+  int (*allreduce_sum)(void* user);
+  int (*allgather)(void* user);
+  double* reduce_buf;
+  double* gather_send;
+  double* gather_recv;
+  int gather_width;
+} dlrsn_comm;
+
+int64_t dlrsn_step_workspace_bytes(int nx, int ny, int r, int n_omega, int world_size);
+
+/* step_collocation (dlr_sn.py:86-151) in one call: DEIM, closure, collocated
+ * source iteration, M-orthonormal spatial basis (CholQR2 / CGS2), fused
+ * projections, row solve, angular re-orthonormalisation, checks.  Inputs
+ * X (n_dofs, r), S (r, r), W (n_omega, r), beta (r), per-cell sigma_t,
+ * sigma_s, q; outputs X_new, S_new, W_new, beta_new, phi = X_new lbar (the
+ * flux of the temperature update) and si_phi (source-iteration flux).
+ * Returns DLRSN_EINTERP / DLRSN_EINVAL / DLRSN_EITER / DLRSN_ESINGULAR /
+ * DLRSN_ECOMPLETION like the reference raises (errors in its order). */
+int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p, const double* X,
+                           const double* S, const double* W, const double* beta,
+                           const double* sigma_t, const double* sigma_s, const double* q,
+                           double* X_new, double* S_new, double* W_new, double* beta_new,
+                           double* phi, double* si_phi, void* workspace, int64_t workspace_bytes,
+                           void* sweep_ws, int64_t sweep_ws_bytes, const dlrsn_comm* comm,
+                           dlrsn_step_info* info, dlrsn_stream_t stream);
 
 #ifdef __cplusplus
 }

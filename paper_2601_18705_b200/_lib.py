@@ -34,6 +34,32 @@ class CellOps(ctypes.Structure):
     ]
 
 
+MAX_RANK = 128
+
+
+class StepParams(ctypes.Structure):
+    _fields_ = [("rank", c_int), ("n_omega", c_int), ("omegas_host", c_vp), ("omegas_dev", c_vp),
+                ("weights_dev", c_vp), ("inv_cdt", c_dbl), ("si_tol", c_dbl),
+                ("si_max_iters", c_int), ("check_state", c_int), ("gs_method", c_int),
+                ("sweep_dw", c_int)]
+
+
+class StepInfo(ctypes.Structure):
+    _fields_ = [("iterations", c_int), ("spatial_deficiency", c_int),
+                ("angular_deficiency", c_int), ("error_index", c_int), ("gs_fallback", c_int),
+                ("residual", c_dbl), ("check_in", c_dbl * 2), ("check_out", c_dbl * 2),
+                ("angle_indices", c_i64 * MAX_RANK), ("closure", c_dbl * MAX_RANK)]
+
+
+COMM_FN = ctypes.CFUNCTYPE(c_int, c_vp)
+
+
+class Comm(ctypes.Structure):
+    _fields_ = [("rank", c_int), ("world_size", c_int), ("user", c_vp),
+                ("allreduce_sum", COMM_FN), ("allgather", COMM_FN), ("reduce_buf", c_vp),
+                ("gather_send", c_vp), ("gather_recv", c_vp), ("gather_width", c_int)]
+
+
 # numpy mirror of struct dlrsn_group (include/dlrsn.h)
 GROUP_DTYPE = np.dtype([
     ("quad", np.int32), ("ndir", np.int32), ("slot", np.int32, (MAX_DW,)),
@@ -43,6 +69,7 @@ GROUP_DTYPE = np.dtype([
 # name -> (restype, argtypes); keep in sync with include/dlrsn.h
 _SIGNATURES = {
     "dlrsn_version": (c_int, []),
+    "dlrsn_launch_count": (c_i64, []),
     "dlrsn_last_error": (ctypes.c_char_p, []),
     "dlrsn_device_sm_count": (c_int, [c_vp]),
     "dlrsn_sk_vec_len": (c_i64, [c_int, c_int]),
@@ -80,6 +107,10 @@ _SIGNATURES = {
     "dlrsn_deim": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "dlrsn_what_solve": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp]),
     "dlrsn_cgs2_workspace_len": (c_i64, [c_int]),
+    "dlrsn_sweep_timing": (c_int, [c_int]),
+    "dlrsn_sweep_timing_read": (c_int, [c_int, c_vp, c_vp, c_vp, c_vp]),
+    "dlrsn_step_workspace_bytes": (c_i64, [c_int, c_int, c_int, c_int, c_int]),
+    "dlrsn_step_collocation": (c_int, [c_vp] * 16 + [c_i64, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "dlrsn_cgs2": (c_int, [c_int, c_int, c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_int, c_vp, c_vp,
                            c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp]),
 }
@@ -118,26 +149,17 @@ def check(status, what=""):
         raise ContractViolation(text)
     if status == -5:
         raise InterpolationError(text, column=-1)
+    if status == -7:
+        raise SolverError(text)
     if status in (-2, -3):
         raise SolverError(text)
     raise RuntimeError(f"dlrsn CUDA failure ({status}): {text}")
 
 
-# kernels each entry point launches (for bench.py's gpu_launches count)
-_KERNELS_PER_CALL = {
-    "dlrsn_linearize": 1, "dlrsn_update_temperature": 1, "dlrsn_advance_relinearize": 1,
-    "dlrsn_rhs_build": 1, "dlrsn_cells_to_sk4": 1, "dlrsn_scatter_source": 1,
-    "dlrsn_phi_combine": 1, "dlrsn_phi_finish": 1, "dlrsn_sk_to_canonical": 1, "dlrsn_sweep": 1,
-    "dlrsn_sweep_workspace_init": 1, "dlrsn_rowmix": 1, "dlrsn_mgram": 2, "dlrsn_project": 2,
-    "dlrsn_chol_upper": 1, "dlrsn_small_matmul": 1, "dlrsn_row_inverse": 1,
-    "dlrsn_row_combine": 1, "dlrsn_deim": 1, "dlrsn_what_solve": 1, "dlrsn_cgs2": 1,
-}
-launch_count = [0]
 
 
 def call(name, *args):
     check(getattr(load(), name)(*args), name)
-    launch_count[0] += _KERNELS_PER_CALL.get(name, 0)
 
 
 def ptr(t):
@@ -149,3 +171,9 @@ def stream_handle(device=None):
     import torch
 
     return c_vp(torch.cuda.current_stream(device).cuda_stream)
+
+
+def launch_count():
+    """Kernels the library has launched since it was loaded (counted in C++
+    at every launch site, csrc/common.cuh DLRSN_CHECK_LAUNCH)."""
+    return int(load().dlrsn_launch_count())

@@ -413,6 +413,7 @@ int dlrsn_cgs2(int n, int m, const double* cols, int ldc, double* Q, int ldq, do
   if (blocks < 1) blocks = 1;
   g.part = workspace + ((n + 7) / 8) * 8;
   void* params[] = {&g};
+  launch_counter().fetch_add(1, std::memory_order_relaxed);
   DLRSN_TRY_CUDA(cudaLaunchCooperativeKernel((const void*)cgs2_grid_kernel, dim3(blocks), dim3(kCgT),
                                              params, smem, as_stream(stream)));
   return DLRSN_OK;

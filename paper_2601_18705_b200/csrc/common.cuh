@@ -5,11 +5,19 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/dlrsn.h"
 
 namespace dlrsn {
 
 void set_error(const char* fmt, ...);
+
+// kernels launched by this library since load (dlrsn_launch_count)
+inline std::atomic<int64_t>& launch_counter() {
+  static std::atomic<int64_t> c{0};
+  return c;
+}
 
 #define DLRSN_TRY_CUDA(expr)                                                        \
   do {                                                                              \
@@ -22,6 +30,7 @@ void set_error(const char* fmt, ...);
 
 #define DLRSN_CHECK_LAUNCH(name)                                                    \
   do {                                                                              \
+    ::dlrsn::launch_counter().fetch_add(1, std::memory_order_relaxed);              \
     cudaError_t e_ = cudaGetLastError();                                            \
     if (e_ != cudaSuccess) {                                                        \
       ::dlrsn::set_error("launch of %s failed: %s", name, cudaGetErrorString(e_));  \

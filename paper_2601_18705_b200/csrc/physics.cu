@@ -109,6 +109,8 @@ int dlrsn_version(void) { return 1; }
 
 const char* dlrsn_last_error(void) { return g_err; }
 
+int64_t dlrsn_launch_count(void) { return dlrsn::launch_counter().load(); }
+
 int dlrsn_device_sm_count(int* out) {
   int dev = 0;
   DLRSN_TRY_CUDA(cudaGetDevice(&dev));

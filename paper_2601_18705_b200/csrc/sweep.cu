@@ -20,6 +20,7 @@
 //     accumulated in registers (deterministic, no atomics).
 #include <cmath>
 #include <cstdlib>
+#include <vector>
 
 #include "sweep_common.cuh"
 
@@ -624,6 +625,27 @@ int dlrsn_debug_flags(int flags) {
   return DLRSN_OK;
 }
 
+// optional CUDA-event timing of every sweep launch (bench.py roofline)
+struct SweepTimer {
+  cudaEvent_t start, stop;
+  int G, dw;
+};
+static bool g_timing = false;
+static std::vector<SweepTimer> g_timers;
+static size_t g_timers_used = 0;
+static SweepTimer* timer_slot(int G, int dw) {
+  if (g_timers_used == g_timers.size()) {
+    SweepTimer t;
+    if (cudaEventCreate(&t.start) != cudaSuccess || cudaEventCreate(&t.stop) != cudaSuccess)
+      return nullptr;
+    g_timers.push_back(t);
+  }
+  SweepTimer* t = &g_timers[g_timers_used++];
+  t->G = G;
+  t->dw = dw;
+  return t;
+}
+
 static unsigned long long* h_trace = nullptr;
 static int h_trace_chunks = 0;
 
@@ -706,12 +728,39 @@ int dlrsn_sweep(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int 
   const int items = sk_strips(ops->ny) * G;
   bool use_ws = items <= 2 * sms;
   if (ws_env) use_ws = ws_env[0] == '1';
+  SweepTimer* tm = g_timing ? timer_slot(G, dw) : nullptr;
+  if (tm) DLRSN_TRY_CUDA(cudaEventRecord(tm->start, st));
+  int rc;
   switch (dw) {
-    case 1: return use_ws ? launch_sweep_ws(a, max_ctas, st) : launch_sweep<1>(a, max_ctas, st);
-    case 2: return launch_sweep<2>(a, max_ctas, st);
-    case 4: return launch_sweep<4>(a, max_ctas, st);
-    default: return launch_sweep<8>(a, max_ctas, st);
+    case 1: rc = use_ws ? launch_sweep_ws(a, max_ctas, st) : launch_sweep<1>(a, max_ctas, st); break;
+    case 2: rc = launch_sweep<2>(a, max_ctas, st); break;
+    case 4: rc = launch_sweep<4>(a, max_ctas, st); break;
+    default: rc = launch_sweep<8>(a, max_ctas, st); break;
   }
+  if (tm && rc == DLRSN_OK) DLRSN_TRY_CUDA(cudaEventRecord(tm->stop, st));
+  return rc;
+}
+
+int dlrsn_sweep_timing(int enable) {
+  g_timing = enable != 0;
+  g_timers_used = 0;
+  return DLRSN_OK;
+}
+
+int dlrsn_sweep_timing_read(int cap, float* ms, int* groups, int* dw, int* count) {
+  int n = 0;
+  for (size_t k = 0; k < g_timers_used; ++k) {
+    SweepTimer& t = g_timers[k];
+    if (n < cap) {
+      DLRSN_TRY_CUDA(cudaEventSynchronize(t.stop));
+      DLRSN_TRY_CUDA(cudaEventElapsedTime(&ms[n], t.start, t.stop));
+      groups[n] = t.G;
+      dw[n] = t.dw;
+    }
+    ++n;
+  }
+  *count = n;
+  return DLRSN_OK;
 }
 
 }  // extern "C"

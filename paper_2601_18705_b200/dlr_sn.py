@@ -16,6 +16,7 @@ scalars of the source iteration.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 from functools import cached_property
 
@@ -23,9 +24,15 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import as_device, empty, stream
-from .angular import orthonormalize_async
-from .errors import ContractViolation
+from ._device import as_device, device, empty, stream
+from .angular import AngularBasis, orthonormalize_async
+from .errors import (
+    ConfigurationError,
+    ContractViolation,
+    InterpolationError,
+    IterationLimitError,
+    SolverError,
+)
 from .lowrank import (
     DlrState,
     _addr,
@@ -110,8 +117,13 @@ def project_initial(state, x_new, ops):
 
 def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, use_dsa=True,
                      dsa_penalty="simplified", threads=0, check_state=True, gs_method="cholqr2",
-                     sweep_dw=None, comm=None):
+                     sweep_dw=None, comm=None, engine="native"):
     """Advance one linearised step; returns (new DlrState, CollocationStepInfo).
+
+    ``engine="native"`` issues the whole step from C++ through the single
+    C-ABI call ``dlrsn_step_collocation`` (include/dlrsn.h); ``"python"``
+    orchestrates the same kernels from Python (kept as a cross-check and for
+    the cases the native call does not take: DSA, a pinned constant column).
 
     Host synchronisations: one before the source iteration (DEIM picks,
     closure weights and the input checks come back together), one per source
@@ -119,6 +131,16 @@ def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, 
     row-system status, angular deficiencies, output check).  Errors are raised
     in the reference's order (dlr_sn.py:99-141).
     """
+    if gs_method not in ("cholqr2", "cgs2"):
+        raise ConfigurationError(f"unknown gs_method {gs_method!r}")
+    if engine not in ("native", "python"):
+        raise ConfigurationError(f"unknown engine {engine!r}")
+    if (engine == "native" and not use_dsa and not state.W.pinned
+            and state.rank <= _lib.MAX_RANK):
+        if dsa_penalty not in ("simplified", "collocation"):
+            raise ContractViolation(f"unknown dsa penalty variant {dsa_penalty!r}")
+        return _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state,
+                            gs_method, sweep_dw, comm)
     r = state.rank
     # ---- DEIM + closure + input checks: one readback ------------------------
     selection, err_idx = deim_launch(state.W.values)
@@ -218,3 +240,189 @@ def _galerkin_tail(ops, step, quad, state, selection, closure, omegas_sel, resul
     return {"gs_ok": True, "state": new_state, "sdef": sdef,
             "adef": int(np.count_nonzero(adef)),
             "phi": rowmix(x_new, l_bar.reshape(-1, 1))[:, 0]}
+
+
+# ---- native engine: the whole step in one C-ABI call ------------------------
+
+class _NativeSelection:
+    """DEIM picks of a native step (indices on the host; W_hat = W[idx] for
+    the condition number, lowrank.py:204)."""
+
+    def __init__(self, indices, w_values):
+        self.indices = indices
+        self._w = w_values
+
+    @property
+    def rank(self):
+        return len(self.indices)
+
+    @cached_property
+    def indices_dev(self):
+        return torch.as_tensor(self.indices, device=device())
+
+    @cached_property
+    def w_hat(self):
+        return self._w[self.indices_dev]
+
+    @cached_property
+    def cond(self):
+        return float(torch.linalg.cond(self.w_hat))
+
+
+_STEP_WS = {}
+
+
+def _grid_cellops(grid):
+    co = grid.__dict__.get("_cellops")
+    if co is None:
+        from .mesh import cellops_struct
+
+        co = cellops_struct(grid)
+        object.__setattr__(grid, "_cellops", co)
+    return co
+
+
+def _step_workspace(grid, r, no, world, rank):
+    key = (torch.cuda.current_device(), grid.nx, grid.ny, r, no, world, rank)
+    ws = _STEP_WS.get(key)
+    if ws is None:
+        nbytes = int(_lib.load().dlrsn_step_workspace_bytes(grid.nx, grid.ny, r, no, world))
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=device())
+        _STEP_WS[key] = ws
+    return ws
+
+
+class _CommHooks:
+    """C callbacks of dlrsn_comm over a DirectionComm-like object (anything
+    with ``allreduce_sum_``; ``allgather_into_`` when it has one, else the
+    gather is an allreduce of zero-padded blocks, which is exact)."""
+
+    def __init__(self, comm, n, width):
+        self.comm = comm
+        self.n, self.width = n, width
+        self.reduce_buf = empty(n)
+        self.send = empty(n, width)
+        self.recv = empty(comm.world_size, n, width)
+        self.error = None
+        self._ar = _lib.COMM_FN(self._allreduce)
+        self._ag = _lib.COMM_FN(self._allgather)
+        s = _lib.Comm()
+        s.rank, s.world_size = comm.rank, comm.world_size
+        s.user = None
+        s.allreduce_sum, s.allgather = self._ar, self._ag
+        s.reduce_buf = self.reduce_buf.data_ptr()
+        s.gather_send = self.send.data_ptr()
+        s.gather_recv = self.recv.data_ptr()
+        s.gather_width = width
+        self.struct = s
+
+    def _allreduce(self, _user):
+        try:
+            self.comm.allreduce_sum_(self.reduce_buf)
+            return 0
+        except Exception as e:  # surfaced after the C call returns
+            self.error = e
+            return 1
+
+    def _allgather(self, _user):
+        try:
+            if hasattr(self.comm, "allgather_into_"):
+                self.comm.allgather_into_(self.recv, self.send)
+            else:
+                self.recv.zero_()
+                self.recv[self.comm.rank].copy_(self.send)
+                self.comm.allreduce_sum_(self.recv)
+            return 0
+        except Exception as e:
+            self.error = e
+            return 1
+
+
+_HOOKS = {}
+
+
+def _comm_hooks(comm, n, r):
+    width = -(-r // comm.world_size) + 1
+    key = (id(comm), comm.rank, n, width)
+    h = _HOOKS.get(key)
+    if h is None or h.comm is not comm:
+        h = _CommHooks(comm, n, width)
+        _HOOKS[key] = h
+    return h
+
+
+def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_method, sweep_dw,
+                 comm):
+    from .transport import _shared_workspace
+
+    lib = _lib.load()
+    r = state.rank
+    no = quad.n_angles
+    n = grid.n_dofs
+    for name in ("sigma_t", "sigma_s", "q"):
+        if tuple(getattr(step, name).shape) != (grid.n_cells,):
+            raise ContractViolation(f"step field {name} must be per-cell")
+    if state.W.values.shape != (no, r) or tuple(state.X.shape) != (n, r):
+        raise ContractViolation("factor shapes do not match the grid / quadrature")
+    world = comm.world_size if comm is not None else 1
+    rank = comm.rank if comm is not None else 0
+    co = _grid_cellops(grid)
+    X = state.X.contiguous()
+    S = state.S.contiguous()
+    W = state.W.values.contiguous()
+    beta = state.W.beta if state.W.beta is not None else state.W.bind(quad).beta
+    beta = beta.contiguous()
+    X_new, S_new, W_new = empty(n, r), empty(r, r), empty(no, r)
+    beta_new, phi, si_phi = empty(r), empty(n), empty(n)
+    ws = _step_workspace(grid, r, no, world, rank)
+    dw = int(sweep_dw) if sweep_dw else 1
+    sw_bytes = int(lib.dlrsn_sweep_workspace_bytes(grid.nx, grid.ny, r, dw))
+    sws = _shared_workspace(grid, sw_bytes)
+    om_host = quad.omegas if quad.omegas.flags.c_contiguous else np.ascontiguousarray(quad.omegas)
+    p = _lib.StepParams()
+    p.rank, p.n_omega = r, no
+    p.omegas_host = om_host.ctypes.data
+    p.omegas_dev = quad.omegas_device().data_ptr()
+    p.weights_dev = quad.weights_device().data_ptr()
+    p.inv_cdt = float(step.inv_cdt)
+    p.si_tol, p.si_max_iters = float(si_tol), int(si_max_iters)
+    p.check_state = 1 if check_state else 0
+    p.gs_method = 0 if gs_method == "cholqr2" else 1
+    p.sweep_dw = dw
+    info = _lib.StepInfo()
+    hooks = _comm_hooks(comm, n, r) if world > 1 else None
+    P = _lib.ptr
+    rc = lib.dlrsn_step_collocation(
+        _addr(co), ctypes.byref(p), P(X), P(S), P(W), P(beta), P(step.sigma_t), P(step.sigma_s),
+        P(step.q), P(X_new), P(S_new), P(W_new), P(beta_new), P(phi), P(si_phi), P(ws), ws.numel(),
+        P(sws), sws.numel(), ctypes.byref(hooks.struct) if hooks else None, ctypes.byref(info),
+        stream())
+    if hooks is not None and hooks.error is not None:
+        raise hooks.error
+    if rc != 0:
+        msg = lib.dlrsn_last_error().decode(errors="replace")
+        if rc == -5:
+            raise InterpolationError("interpolation residual vanished; basis is rank deficient",
+                                     column=int(info.error_index))
+        if rc == -7:
+            raise IterationLimitError("source iteration did not converge", int(info.iterations),
+                                      float(info.residual))
+        if rc in (-2, -3):
+            raise SolverError(msg)
+        if rc in (-1, -6):
+            raise ContractViolation(msg)
+        raise RuntimeError(f"dlrsn CUDA failure ({rc}): {msg}")
+    indices = np.frombuffer(info.angle_indices, dtype=np.int64, count=r).copy()
+    basis = AngularBasis(values=W_new, beta=beta_new)
+    new_state = DlrState(X=X_new, S=S_new, W=basis)
+    out = CollocationStepInfo(
+        iterations=int(info.iterations),
+        selection=_NativeSelection(indices, W),
+        angle_indices=indices.copy(),
+        phi=phi,
+        spatial_deficiency=int(info.spatial_deficiency),
+        angular_deficiency=int(info.angular_deficiency),
+        si_phi=si_phi,
+    )
+    out.gs_fallback = bool(info.gs_fallback)
+    return new_state, out

@@ -118,7 +118,7 @@ def initial_state(dp, X=None, W=None, seed=None, T=None):
 
 
 def run(dp, state, n_steps, *, si_tol=1e-8, si_max_iters=200, check_state=True, T=None,
-        record=None, gs_method="cholqr2"):
+        record=None, gs_method="cholqr2", engine="native", comm=None):
     """n_steps of the dlr-sn loop; returns (state, T, infos)."""
     from .dlr_sn import step_collocation
 
@@ -128,7 +128,8 @@ def run(dp, state, n_steps, *, si_tol=1e-8, si_max_iters=200, check_state=True, 
     for _ in range(n_steps):
         state, info = step_collocation(dp.grid, lin, dp.quad, state, si_tol=si_tol,
                                        si_max_iters=si_max_iters, use_dsa=False,
-                                       check_state=check_state, gs_method=gs_method)
+                                       check_state=check_state, gs_method=gs_method,
+                                       engine=engine, comm=comm)
         lin = dp.advance(lin, info.phi, T)
         infos.append(info)
         if record is not None:

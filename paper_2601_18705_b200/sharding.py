@@ -94,6 +94,18 @@ class DirectionComm:
                 full[:, idx] = recv[p][:len(slots)].T
         return full
 
+    def allgather_into_(self, recv, send):
+        """recv[p] = send of rank p (recv: (world_size, *send.shape)); the
+        native step's gather of the swept columns (include/dlrsn.h dlrsn_comm)."""
+        import torch.distributed as dist
+
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_gather_into_tensor(recv.reshape(-1), send.contiguous().reshape(-1),
+                                        group=self.group)
+        else:
+            dist.all_gather(list(recv.unbind(0)), send.contiguous(), group=self.group)
+        return recv
+
     def max_scalar(self, x):
         import torch.distributed as dist
 

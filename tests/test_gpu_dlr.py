@@ -245,3 +245,68 @@ def test_config1_twenty_steps_match_oracle():
         assert rel_l2(gt, rt) <= 1e-11, k
         X2, S2, W2 = gs.to_numpy()
         assert P.lowrank_rel_diff(X2, S2, W2, rs.X, rs.S, rs.W) <= 1e-11, k
+
+
+@pytest.mark.parametrize("gs_method", ["cholqr2", "cgs2"])
+def test_native_step_matches_python_orchestration(gs_method):
+    """The one-call C++ step (dlrsn_step_collocation) issues the same kernels
+    as the Python orchestration: identical picks and iteration counts, and
+    states equal to round-off."""
+    from oracle.port import lowrank_rel_diff
+    from paper_2601_18705_b200 import problems
+    from paper_2601_18705_b200.driver import DeviceProblem, initial_state, run
+
+    spec = problems.checkerboard(4, rank=8, n_polar=6, n_azimuthal=8, seed=11)
+    out = {}
+    for engine in ("native", "python"):
+        dp = DeviceProblem.from_spec(spec)
+        recs = []
+        run(dp, initial_state(dp), 4, si_tol=1e-12, si_max_iters=400, gs_method=gs_method,
+            engine=engine, record=lambda s, i, t: recs.append((s.to_numpy(), i, _np(t).copy())))
+        out[engine] = recs
+    for (a, ia, ta), (b, ib, tb) in zip(out["native"], out["python"]):
+        assert list(ia.angle_indices) == list(ib.angle_indices)
+        assert ia.iterations == ib.iterations
+        assert ia.spatial_deficiency == ib.spatial_deficiency
+        assert ia.angular_deficiency == ib.angular_deficiency
+        assert lowrank_rel_diff(*a, *b) <= 1e-13
+        assert rel_l2(_np(ia.phi), _np(ib.phi)) <= 1e-13
+        assert rel_l2(_np(ia.si_phi), _np(ib.si_phi)) <= 1e-13
+        assert rel_l2(ta, tb) <= 1e-13
+        assert abs(ia.interpolation_condition - ib.interpolation_condition) <= 1e-9 * ib.interpolation_condition
+
+
+def test_native_step_raises_like_the_reference():
+    from paper_2601_18705_b200.angular import build_quadrature
+    from paper_2601_18705_b200.dlr_sn import step_collocation
+    from paper_2601_18705_b200.errors import ContractViolation, InterpolationError, IterationLimitError
+    from paper_2601_18705_b200.lowrank import DlrState
+    from paper_2601_18705_b200.mesh import build_grid
+    from paper_2601_18705_b200.physics import linearize
+
+    from paper_2601_18705_b200.angular import orthonormalize
+    from paper_2601_18705_b200.lowrank import gram_schmidt_mass
+
+    grid = build_grid(4, 4)
+    quad = build_quadrature(2, 4)
+    rng = np.random.default_rng(3)
+    Wq = _np(orthonormalize(rng.standard_normal((quad.n_angles, 3)), quad)[0].values)
+    Xq = _np(gram_schmidt_mass(grid, rng.standard_normal((grid.n_dofs, 3)))[0])
+    n = grid.n_cells
+    step = linearize(np.full(n, 0.5), np.full(n, 2.0), np.ones(n), 0.1)
+    st = DlrState(X=Xq, S=np.diag([1.0, 0.5, 0.25]), W=Wq)
+    st.W.bind(quad)
+    with pytest.raises(IterationLimitError) as e:
+        step_collocation(grid, step, quad, st, use_dsa=False, si_tol=1e-300, si_max_iters=2)
+    assert e.value.iterations == 2
+    bad = DlrState(X=Xq, S=np.eye(3), W=np.column_stack([Wq[:, 0], Wq[:, 0], Wq[:, 1]]))
+    bad.W.bind(quad)
+    with pytest.raises(InterpolationError) as e:
+        step_collocation(grid, step, quad, bad, use_dsa=False, check_state=False)
+    assert e.value.column == 1
+    with pytest.raises(ContractViolation, match="orthonormality"):
+        step_collocation(grid, step, quad, DlrState(X=2 * Xq, S=np.eye(3), W=Wq), use_dsa=False)
+    step2 = linearize(np.full(n, 0.5), np.full(n, 2.0), np.ones(n), 0.1)
+    step2.sigma_s.copy_(step2.sigma_t)
+    with pytest.raises(ContractViolation, match="pseudo absorption"):
+        step_collocation(grid, step2, quad, st, use_dsa=False)

@@ -108,7 +108,8 @@ def test_sharded_source_iteration_matches_unsharded():
     assert np.array_equal(out[0][1], out[1][1])  # ranks hold identical results
 
 
-def test_sharded_dlr_steps_match_unsharded():
+@pytest.mark.parametrize("engine", ["native", "python"])
+def test_sharded_dlr_steps_match_unsharded(engine):
     from paper_2601_18705_b200 import problems
     from paper_2601_18705_b200.dlr_sn import step_collocation
     from paper_2601_18705_b200.driver import DeviceProblem, initial_state
@@ -122,7 +123,7 @@ def test_sharded_dlr_steps_match_unsharded():
         lin = dp.linearized(T)
         for _ in range(3):
             state, info = step_collocation(dp.grid, lin, dp.quad, state, si_tol=1e-12, use_dsa=False,
-                                           comm=comm)
+                                           comm=comm, engine=engine)
             lin = dp.advance(lin, info.phi, T)
         X, S, W = state.to_numpy()
         return X, S, W, T.cpu().numpy()
