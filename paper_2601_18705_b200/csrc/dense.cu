@@ -43,6 +43,36 @@ __global__ void rowmix_kernel(int n, int kx, int ky, const double* __restrict__ 
   }
 }
 
+// Fixed-width variant: thread (i, j) keeps column j of K in registers and
+// reads row i of X with 16-byte loads (shared by the ky threads of the row).
+template <int KX>
+__global__ void __launch_bounds__(256) rowmix_reg_kernel(int n, int ky, const double* __restrict__ X,
+                                                        int ldx, const double* __restrict__ K,
+                                                        int ldk, double beta,
+                                                        double* __restrict__ Y, int ldy) {
+  const int64_t total = (int64_t)n * ky;
+  // blockDim % ky == 0 (checked by the launcher): column j is fixed per thread
+  const int j = threadIdx.x % ky;
+  double k[KX];
+#pragma unroll
+  for (int p = 0; p < KX; ++p) k[p] = __ldg(K + p * ldk + j);
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / ky;
+    const double2* x = reinterpret_cast<const double2*>(X + i * ldx);
+    double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+    for (int p = 0; p < KX / 2; ++p) {
+      const double2 v = __ldg(x + p);
+      acc0 = fma(v.x, k[2 * p], acc0);
+      acc1 = fma(v.y, k[2 * p + 1], acc1);
+    }
+    const double acc = acc0 + acc1;
+    double* y = Y + i * ldy + j;
+    *y = beta == 0.0 ? acc : fma(beta, *y, acc);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Partial-sum plumbing: kernels that reduce over cells write one partial per
 // (chunk, output) and reduce_partials sums them in chunk order.
@@ -74,25 +104,33 @@ constexpr int kTile = 16;
 constexpr int kChunk = 32;   // cells per smem pass (mgram)
 constexpr int kChunkP = 8;  // cells per smem pass (project)
 
-__global__ void mgram_kernel(int ncell, int ra, int rb, const double* __restrict__ A, int lda,
-                             const double* __restrict__ B, int ldb,
-                             const double* __restrict__ coeff, dlrsn_cellops ops, int cells_per_block,
-                             double* __restrict__ part) {
-  __shared__ double sA[kChunk * 4][kTile + 1];
-  __shared__ double sB[kChunk * 4][kTile + 1];
-  const int ti = threadIdx.x / kTile, tj = threadIdx.x % kTile;
+__global__ void __launch_bounds__(256) mgram_kernel(int ncell, int ra, int rb,
+                                                    const double* __restrict__ A, int lda,
+                                                    const double* __restrict__ B, int ldb,
+                                                    const double* __restrict__ coeff,
+                                                    dlrsn_cellops ops, int cells_per_block,
+                                                    double* __restrict__ part) {
+  // 4 row groups x 64 threads; thread (ti, tj) owns the 2x2 micro-tile
+  // (2ti.., 2tj..) of the block's 16x16 output tile, so each pair of 16-byte
+  // shared loads feeds 4 FMAs.  Groups take interleaved rows and are summed
+  // in fixed order at the end (deterministic).
+  __shared__ __align__(16) double sA[kChunk * 4][kTile];
+  __shared__ __align__(16) double sB[kChunk * 4][kTile];
+  __shared__ double red[3][64][4];
+  const int g = threadIdx.x >> 6, t = threadIdx.x & 63;
+  const int ti = t >> 3, tj = t & 7;
   const int tiles_j = (rb + kTile - 1) / kTile;
   const int i0 = (blockIdx.y / tiles_j) * kTile, j0 = (blockIdx.y % tiles_j) * kTile;
   const int c_begin = blockIdx.x * cells_per_block;
   const int c_end = min(ncell, c_begin + cells_per_block);
-  double acc = 0.0;
+  double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;
   for (int c0 = c_begin; c0 < c_end; c0 += kChunk) {
     const int nc = min(kChunk, c_end - c0);
     __syncthreads();
     for (int e = threadIdx.x; e < nc * 4 * kTile; e += blockDim.x) {
       const int row = e / kTile, col = e % kTile;
       const int64_t grow = (int64_t)c0 * 4 + row;
-      sA[row][col] = (i0 + col < ra) ? A[grow * lda + i0 + col] : 0.0;
+      sA[row][col] = (i0 + col < ra) ? __ldg(A + grow * lda + i0 + col) : 0.0;
     }
     // B rows pre-multiplied by coeff_c * M
     for (int e = threadIdx.x; e < nc * kTile; e += blockDim.x) {
@@ -101,7 +139,7 @@ __global__ void mgram_kernel(int ncell, int ra, int rb, const double* __restrict
       double b[4];
 #pragma unroll
       for (int l = 0; l < 4; ++l)
-        b[l] = (j0 + col < rb) ? B[((int64_t)c * 4 + l) * ldb + j0 + col] : 0.0;
+        b[l] = (j0 + col < rb) ? __ldg(B + ((int64_t)c * 4 + l) * ldb + j0 + col) : 0.0;
       const double w = coeff ? coeff[c] : 1.0;
 #pragma unroll
       for (int l = 0; l < 4; ++l) {
@@ -111,10 +149,40 @@ __global__ void mgram_kernel(int ncell, int ra, int rb, const double* __restrict
       }
     }
     __syncthreads();
-    for (int row = 0; row < nc * 4; ++row) acc = fma(sA[row][ti], sB[row][tj], acc);
+#pragma unroll 4
+    for (int row = g; row < nc * 4; row += 4) {
+      const double2 a = *reinterpret_cast<const double2*>(&sA[row][2 * ti]);
+      const double2 b = *reinterpret_cast<const double2*>(&sB[row][2 * tj]);
+      a00 = fma(a.x, b.x, a00);
+      a01 = fma(a.x, b.y, a01);
+      a10 = fma(a.y, b.x, a10);
+      a11 = fma(a.y, b.y, a11);
+    }
   }
-  const int i = i0 + ti, j = j0 + tj;
-  if (i < ra && j < rb) part[(int64_t)blockIdx.x * ra * rb + (int64_t)i * rb + j] = acc;
+  __syncthreads();
+  if (g > 0) {
+    red[g - 1][t][0] = a00;
+    red[g - 1][t][1] = a01;
+    red[g - 1][t][2] = a10;
+    red[g - 1][t][3] = a11;
+  }
+  __syncthreads();
+  if (g == 0) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      a00 += red[q][t][0];
+      a01 += red[q][t][1];
+      a10 += red[q][t][2];
+      a11 += red[q][t][3];
+    }
+    const double v[4] = {a00, a01, a10, a11};
+    double* out = part + (int64_t)blockIdx.x * ra * rb;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + 2 * ti + (q >> 1), j = j0 + 2 * tj + (q & 1);
+      if (i < ra && j < rb) out[(int64_t)i * rb + j] = v[q];
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -141,37 +209,68 @@ struct ProjArgs {
   int cells_per_block;
 };
 
-__device__ inline void edge_pair(const double* X, int r, int cell, int l0, int l1, int col,
-                                 double& v0, double& v1) {
-  if (cell < 0) {
-    v0 = v1 = 0.0;
-    return;
-  }
-  v0 = __ldg(X + ((int64_t)cell * 4 + l0) * r + col);
-  v1 = __ldg(X + ((int64_t)cell * 4 + l1) * r + col);
+__device__ inline double ldx(const double* X, int r, int64_t row, int col) {
+  return col < r ? __ldg(X + row * r + col) : 0.0;
 }
 
-__global__ void project_kernel(ProjArgs pa, dlrsn_cellops ops) {
-  // staged per chunk: X_c (4 rows), transformed rows for j
-  __shared__ double sX[kChunkP][4][kTile + 1];    // X rows, tile-i columns
-  __shared__ double sXo[kChunkP][4][kTile + 1];   // Xold rows, tile-i columns
-  __shared__ double sMX[kChunkP][4][kTile + 1];   // M X, tile-j columns
-  __shared__ double sGX[kChunkP][4][kTile + 1];   // Gx X
-  __shared__ double sGY[kChunkP][4][kTile + 1];   // Gy X
-  __shared__ double sUi[kChunkP][4][kTile + 1];   // x-face u (2), y-face u (2), tile-i
-  __shared__ double sFj[kChunkP][8][kTile + 1];   // 1/2 e2 v (x,y) and 1/2 e2 u (x,y), tile-j
-  __shared__ double sC[kChunkP][3];               // sigma_t, sigma_s, q
-  const int r = pa.r, nx = pa.nx;
-  const int ncell = pa.nx * pa.ny;
-  const int ti = threadIdx.x / kTile, tj = threadIdx.x % kTile;
+__device__ inline double2 ld2s(const double* p) { return *reinterpret_cast<const double2*>(p); }
+
+// acc (2x2, row-major) += a (2) outer b (2)
+__device__ inline void outer2(double* acc, double2 a, double2 b) {
+  acc[0] = fma(a.x, b.x, acc[0]);
+  acc[1] = fma(a.x, b.y, acc[1]);
+  acc[2] = fma(a.y, b.x, acc[2]);
+  acc[3] = fma(a.y, b.y, acc[3]);
+}
+
+__global__ void __launch_bounds__(256, 2) project_kernel(ProjArgs pa, dlrsn_cellops ops) {
+  // Per chunk of kChunkP cells the block stages, for its 16x16 output tile,
+  // the i-side rows (X, Xold, face jumps u) and the j-side rows (M X, Gx X,
+  // Gy X, 1/2 e2 v, 1/2 e2 u, q_c src.X).  4 cell groups x 64 threads; each
+  // thread owns a 2x2 micro-tile of all 7 outputs (28 accumulators), so each
+  // 16-byte shared load feeds several FMAs.  Groups are summed in fixed order.
+  constexpr int C = kChunkP;
+  constexpr int kPer = C * 16;  // doubles per [C][16] plane
+  __shared__ __align__(16) double sm[kPer * 33 + 2 * C];
+  double* sX = sm;               // [C][4][16]
+  double* sXo = sX + 4 * kPer;   // [C][4][16]
+  double* sU = sXo + 4 * kPer;   // [C][4][16]: ux0 ux1 uy0 uy1
+  double* sMX = sU + 4 * kPer;   // [C][4][16]
+  double* sGX = sMX + 4 * kPer;  // [C][4][16]
+  double* sGY = sGX + 4 * kPer;  // [C][4][16]
+  double* sF = sGY + 4 * kPer;   // [C][8][16]
+  double* sQ = sF + 8 * kPer;    // [C][16]
+  double* sC = sQ + kPer;        // [C][2]
+  // cell operator constants in shared memory (keeps them out of registers)
+  __shared__ double so[64];  // mass 0-15, gx 16-31, gy 32-47, e2x 48-51, e2y 52-55, src 56-59
+  if (threadIdx.x < 16) {
+    so[threadIdx.x] = ops.mass[threadIdx.x];
+    so[16 + threadIdx.x] = ops.gx[threadIdx.x];
+    so[32 + threadIdx.x] = ops.gy[threadIdx.x];
+  } else if (threadIdx.x < 20) {
+    so[48 + threadIdx.x - 16] = ops.e2x[threadIdx.x - 16];
+    so[52 + threadIdx.x - 16] = ops.e2y[threadIdx.x - 16];
+    so[56 + threadIdx.x - 16] = ops.src_row[threadIdx.x - 16];
+  }
+  const double* e2x = so + 48;
+  const double* e2y = so + 52;
+  const int r = pa.r, nx = pa.nx, ny = pa.ny;
+  const int ncell = nx * ny;
+  const int g = threadIdx.x >> 6, t = threadIdx.x & 63;
+  const int ti = t >> 3, tj = t & 7;
   const int tiles_j = (r + kTile - 1) / kTile;
   const int i0 = (blockIdx.y / tiles_j) * kTile, j0 = (blockIdx.y % tiles_j) * kTile;
   const int c_begin = blockIdx.x * pa.cells_per_block;
   const int c_end = min(ncell, c_begin + pa.cells_per_block);
-  double acc[7] = {0, 0, 0, 0, 0, 0, 0};
-  double qacc = 0.0;
-  for (int c0 = c_begin; c0 < c_end; c0 += kChunkP) {
-    const int nc = min(kChunkP, c_end - c0);
+  double acc[7][4];
+#pragma unroll
+  for (int o = 0; o < 7; ++o)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[o][q] = 0.0;
+  double qacc[2] = {0.0, 0.0};
+  const double* X = pa.X;
+  for (int c0 = c_begin; c0 < c_end; c0 += C) {
+    const int nc = min(C, c_end - c0);
     __syncthreads();
     for (int e = threadIdx.x; e < nc * kTile * 2; e += blockDim.x) {
       const int side = e / (nc * kTile);  // 0: tile-i columns, 1: tile-j columns
@@ -179,130 +278,200 @@ __global__ void project_kernel(ProjArgs pa, dlrsn_cellops ops) {
       const int cl = rem / kTile, col = rem % kTile;
       const int c = c0 + cl;
       const int gcol = (side == 0 ? i0 : j0) + col;
-      const bool ok = gcol < r;
       const int ci = c % nx, cj = c / nx;
       double x[4];
 #pragma unroll
-      for (int l = 0; l < 4; ++l) x[l] = ok ? __ldg(pa.X + ((int64_t)c * 4 + l) * r + gcol) : 0.0;
-      // face traces: left face (minus = left neighbour right edge (1,3), plus
-      // = this cell's left edge (0,2)); bottom face (minus = lower neighbour
-      // top edge (2,3), plus = this cell's bottom edge (0,1))
-      double ax0 = 0, ax1 = 0, ay0 = 0, ay1 = 0;
-      if (ok) {
-        edge_pair(pa.X, r, ci > 0 ? c - 1 : -1, 1, 3, gcol, ax0, ax1);
-        edge_pair(pa.X, r, cj > 0 ? c - nx : -1, 2, 3, gcol, ay0, ay1);
+      for (int l = 0; l < 4; ++l) x[l] = ldx(X, r, (int64_t)c * 4 + l, gcol);
+      // face traces: left face (minus = left neighbour's right edge (1,3),
+      // plus = this cell's left edge (0,2)); bottom face (minus = lower
+      // neighbour's top edge (2,3), plus = this cell's bottom edge (0,1))
+      double ax0 = 0.0, ax1 = 0.0, ay0 = 0.0, ay1 = 0.0;
+      if (ci > 0) {
+        ax0 = ldx(X, r, (int64_t)(c - 1) * 4 + 1, gcol);
+        ax1 = ldx(X, r, (int64_t)(c - 1) * 4 + 3, gcol);
+      }
+      if (cj > 0) {
+        ay0 = ldx(X, r, (int64_t)(c - nx) * 4 + 2, gcol);
+        ay1 = ldx(X, r, (int64_t)(c - nx) * 4 + 3, gcol);
       }
       const double ux0 = ax0 - x[0], ux1 = ax1 - x[2], vx0 = ax0 + x[0], vx1 = ax1 + x[2];
       const double uy0 = ay0 - x[0], uy1 = ay1 - x[1], vy0 = ay0 + x[0], vy1 = ay1 + x[1];
+      const int base = cl * 64 + col;  // [cl][l][col] in a 4-row plane
       if (side == 0) {
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
-          sX[cl][l][col] = x[l];
-          sXo[cl][l][col] = (ok && pa.Xold) ? __ldg(pa.Xold + ((int64_t)c * 4 + l) * r + gcol) : 0.0;
+          sX[base + 16 * l] = x[l];
+          sXo[base + 16 * l] = pa.Xold ? ldx(pa.Xold, r, (int64_t)c * 4 + l, gcol) : 0.0;
         }
-        sUi[cl][0][col] = ux0; sUi[cl][1][col] = ux1;
-        sUi[cl][2][col] = uy0; sUi[cl][3][col] = uy1;
+        sU[base] = ux0;
+        sU[base + 16] = ux1;
+        sU[base + 32] = uy0;
+        sU[base + 48] = uy1;
       } else {
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
-          double m = 0, gx = 0, gy = 0;
+          double m = 0.0, gx = 0.0, gy = 0.0;
 #pragma unroll
           for (int p = 0; p < 4; ++p) {
-            m += ops.mass[4 * l + p] * x[p];
-            gx += ops.gx[4 * l + p] * x[p];
-            gy += ops.gy[4 * l + p] * x[p];
+            m = fma(so[4 * l + p], x[p], m);
+            gx = fma(so[16 + 4 * l + p], x[p], gx);
+            gy = fma(so[32 + 4 * l + p], x[p], gy);
           }
-          sMX[cl][l][col] = m;
-          sGX[cl][l][col] = gx;
-          sGY[cl][l][col] = gy;
+          sMX[base + 16 * l] = m;
+          sGX[base + 16 * l] = gx;
+          sGY[base + 16 * l] = gy;
         }
-        // 1/2 e2 v and 1/2 e2 u for both faces
-        sFj[cl][0][col] = 0.5 * (ops.e2x[0] * vx0 + ops.e2x[1] * vx1);
-        sFj[cl][1][col] = 0.5 * (ops.e2x[2] * vx0 + ops.e2x[3] * vx1);
-        sFj[cl][2][col] = 0.5 * (ops.e2y[0] * vy0 + ops.e2y[1] * vy1);
-        sFj[cl][3][col] = 0.5 * (ops.e2y[2] * vy0 + ops.e2y[3] * vy1);
-        sFj[cl][4][col] = 0.5 * (ops.e2x[0] * ux0 + ops.e2x[1] * ux1);
-        sFj[cl][5][col] = 0.5 * (ops.e2x[2] * ux0 + ops.e2x[3] * ux1);
-        sFj[cl][6][col] = 0.5 * (ops.e2y[0] * uy0 + ops.e2y[1] * uy1);
-        sFj[cl][7][col] = 0.5 * (ops.e2y[2] * uy0 + ops.e2y[3] * uy1);
+        double* f = sF + cl * 128 + col;
+        f[0] = 0.5 * (e2x[0] * vx0 + e2x[1] * vx1);
+        f[16] = 0.5 * (e2x[2] * vx0 + e2x[3] * vx1);
+        f[32] = 0.5 * (e2y[0] * vy0 + e2y[1] * vy1);
+        f[48] = 0.5 * (e2y[2] * vy0 + e2y[3] * vy1);
+        f[64] = 0.5 * (e2x[0] * ux0 + e2x[1] * ux1);
+        f[80] = 0.5 * (e2x[2] * ux0 + e2x[3] * ux1);
+        f[96] = 0.5 * (e2y[0] * uy0 + e2y[1] * uy1);
+        f[112] = 0.5 * (e2y[2] * uy0 + e2y[3] * uy1);
+        double s = 0.0;
+#pragma unroll
+        for (int l = 0; l < 4; ++l) s = fma(so[56 + l], x[l], s);
+        sQ[cl * 16 + col] = __ldg(pa.q + c) * s;  // q-hat (dlr_sn.py:70)
       }
     }
     for (int e = threadIdx.x; e < nc; e += blockDim.x) {
-      sC[e][0] = pa.sigma_t[c0 + e];
-      sC[e][1] = pa.sigma_s[c0 + e];
-      sC[e][2] = pa.q[c0 + e];
+      sC[2 * e] = __ldg(pa.sigma_t + c0 + e);
+      sC[2 * e + 1] = __ldg(pa.sigma_s + c0 + e);
     }
     __syncthreads();
-    for (int cl = 0; cl < nc; ++cl) {
-      double xm = 0, gx = 0, gy = 0, om = 0;
+    for (int cl = g; cl < nc; cl += 4) {
+      double xm[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int l = 0; l < 4; ++l) {
-        const double xi = sX[cl][l][ti];
-        xm = fma(xi, sMX[cl][l][tj], xm);
-        gx = fma(xi, sGX[cl][l][tj], gx);
-        gy = fma(xi, sGY[cl][l][tj], gy);
-        om = fma(sXo[cl][l][ti], sMX[cl][l][tj], om);
+        const int o = cl * 64 + 16 * l;
+        const double2 xi = ld2s(sX + o + 2 * ti), xo = ld2s(sXo + o + 2 * ti);
+        const double2 mj = ld2s(sMX + o + 2 * tj);
+        outer2(xm, xi, mj);
+        outer2(acc[0], xi, ld2s(sGX + o + 2 * tj));
+        outer2(acc[1], xi, ld2s(sGY + o + 2 * tj));
+        outer2(acc[6], xo, mj);
       }
-      const double uxi0 = sUi[cl][0][ti], uxi1 = sUi[cl][1][ti];
-      const double uyi0 = sUi[cl][2][ti], uyi1 = sUi[cl][3][ti];
-      acc[0] += gx + (uxi0 * sFj[cl][0][tj] + uxi1 * sFj[cl][1][tj]);
-      acc[1] += gy + (uyi0 * sFj[cl][2][tj] + uyi1 * sFj[cl][3][tj]);
-      acc[2] += uxi0 * sFj[cl][4][tj] + uxi1 * sFj[cl][5][tj];
-      acc[3] += uyi0 * sFj[cl][6][tj] + uyi1 * sFj[cl][7][tj];
-      acc[4] = fma(sC[cl][0], xm, acc[4]);
-      acc[5] = fma(sC[cl][1], xm, acc[5]);
-      acc[6] += om;
-    }
-    // q-hat (dlr_sn.py:70): the (i0 == 0) tiles own columns j0..j0+15
-    if (i0 == 0 && ti == 0) {
-      for (int cl = 0; cl < nc; ++cl) {
-        const int c = c0 + cl;
-        const int col = j0 + tj;
-        if (col < r) {
-          double s = 0;
+      const double2 ux0 = ld2s(sU + cl * 64 + 2 * ti), ux1 = ld2s(sU + cl * 64 + 16 + 2 * ti);
+      const double2 uy0 = ld2s(sU + cl * 64 + 32 + 2 * ti), uy1 = ld2s(sU + cl * 64 + 48 + 2 * ti);
+      const double* f = sF + cl * 128 + 2 * tj;
+      outer2(acc[0], ux0, ld2s(f));
+      outer2(acc[0], ux1, ld2s(f + 16));
+      outer2(acc[1], uy0, ld2s(f + 32));
+      outer2(acc[1], uy1, ld2s(f + 48));
+      outer2(acc[2], ux0, ld2s(f + 64));
+      outer2(acc[2], ux1, ld2s(f + 80));
+      outer2(acc[3], uy0, ld2s(f + 96));
+      outer2(acc[3], uy1, ld2s(f + 112));
+      const double st = sC[2 * cl], ss = sC[2 * cl + 1];
 #pragma unroll
-          for (int l = 0; l < 4; ++l) s = fma(ops.src_row[l], __ldg(pa.X + ((int64_t)c * 4 + l) * r + col), s);
-          qacc = fma(sC[cl][2], s, qacc);
-        }
+      for (int q = 0; q < 4; ++q) {
+        acc[4][q] = fma(st, xm[q], acc[4][q]);
+        acc[5][q] = fma(ss, xm[q], acc[5][q]);
+      }
+      if (ti == 0) {
+        qacc[0] += sQ[cl * 16 + 2 * tj];
+        qacc[1] += sQ[cl * 16 + 2 * tj + 1];
       }
     }
   }
   // right / top boundary faces of the cells in this block's range
-  // (a = this cell's right/top edge trace, b = 0); enumerate only those cells
+  // (a = this cell's right/top edge trace, b = 0)
   {
-    const int i = i0 + ti, j = j0 + tj;
-    if (i < r && j < r) {
-      const int first_right = c_begin + ((nx - 1 - c_begin % nx) % nx + nx) % nx;
-      for (int c = first_right; c < c_end; c += nx) {
-        double ai0, ai1, aj0, aj1;
-        edge_pair(pa.X, r, c, 1, 3, i, ai0, ai1);
-        edge_pair(pa.X, r, c, 1, 3, j, aj0, aj1);
-        const double f0 = 0.5 * (ops.e2x[0] * aj0 + ops.e2x[1] * aj1);
-        const double f1 = 0.5 * (ops.e2x[2] * aj0 + ops.e2x[3] * aj1);
-        const double val = ai0 * f0 + ai1 * f1;
-        acc[0] += val;
-        acc[2] += val;
+    const int ia = i0 + 2 * ti, ja = j0 + 2 * tj;
+    const int first_right = c_begin + ((nx - 1 - c_begin % nx) % nx + nx) % nx;
+    for (int c = first_right + g * nx; c < c_end; c += 4 * nx) {
+      const int64_t r1 = (int64_t)c * 4 + 1, r3 = (int64_t)c * 4 + 3;
+      const double2 a0 = make_double2(ldx(X, r, r1, ia), ldx(X, r, r1, ia + 1));
+      const double2 a1 = make_double2(ldx(X, r, r3, ia), ldx(X, r, r3, ia + 1));
+      const double bj0[2] = {ldx(X, r, r1, ja), ldx(X, r, r1, ja + 1)};
+      const double bj1[2] = {ldx(X, r, r3, ja), ldx(X, r, r3, ja + 1)};
+      const double2 f0 = make_double2(0.5 * (e2x[0] * bj0[0] + e2x[1] * bj1[0]),
+                                      0.5 * (e2x[0] * bj0[1] + e2x[1] * bj1[1]));
+      const double2 f1 = make_double2(0.5 * (e2x[2] * bj0[0] + e2x[3] * bj1[0]),
+                                      0.5 * (e2x[2] * bj0[1] + e2x[3] * bj1[1]));
+      double v[4] = {0.0, 0.0, 0.0, 0.0};
+      outer2(v, a0, f0);
+      outer2(v, a1, f1);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        acc[0][q] += v[q];
+        acc[2][q] += v[q];
       }
-      for (int c = max(c_begin, (pa.ny - 1) * nx); c < c_end; ++c) {
-        double ai0, ai1, aj0, aj1;
-        edge_pair(pa.X, r, c, 2, 3, i, ai0, ai1);
-        edge_pair(pa.X, r, c, 2, 3, j, aj0, aj1);
-        const double f0 = 0.5 * (ops.e2y[0] * aj0 + ops.e2y[1] * aj1);
-        const double f1 = 0.5 * (ops.e2y[2] * aj0 + ops.e2y[3] * aj1);
-        const double val = ai0 * f0 + ai1 * f1;
-        acc[1] += val;
-        acc[3] += val;
+    }
+    for (int c = max(c_begin, (ny - 1) * nx) + g; c < c_end; c += 4) {
+      const int64_t r2 = (int64_t)c * 4 + 2, r3 = (int64_t)c * 4 + 3;
+      const double2 a0 = make_double2(ldx(X, r, r2, ia), ldx(X, r, r2, ia + 1));
+      const double2 a1 = make_double2(ldx(X, r, r3, ia), ldx(X, r, r3, ia + 1));
+      const double bj0[2] = {ldx(X, r, r2, ja), ldx(X, r, r2, ja + 1)};
+      const double bj1[2] = {ldx(X, r, r3, ja), ldx(X, r, r3, ja + 1)};
+      const double2 f0 = make_double2(0.5 * (e2y[0] * bj0[0] + e2y[1] * bj1[0]),
+                                      0.5 * (e2y[0] * bj0[1] + e2y[1] * bj1[1]));
+      const double2 f1 = make_double2(0.5 * (e2y[2] * bj0[0] + e2y[3] * bj1[0]),
+                                      0.5 * (e2y[2] * bj0[1] + e2y[3] * bj1[1]));
+      double v[4] = {0.0, 0.0, 0.0, 0.0};
+      outer2(v, a0, f0);
+      outer2(v, a1, f1);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        acc[1][q] += v[q];
+        acc[3][q] += v[q];
       }
     }
   }
-  const int i = i0 + ti, j = j0 + tj;
-  const int64_t stride = 7 * (int64_t)r * r + r;
-  double* out = pa.part + (int64_t)blockIdx.x * stride;
-  if (i < r && j < r) {
+  // fixed-order group reduction through the staging buffer:
+  // (g0 + g2) + (g1 + g3)
+  constexpr int kV = 30;
+  __syncthreads();
+  if (g >= 2) {
+    double* dst = sm + ((g - 2) * 64 + t) * kV;
 #pragma unroll
-    for (int o = 0; o < 7; ++o) out[(int64_t)o * r * r + (int64_t)i * r + j] = acc[o];
+    for (int o = 0; o < 7; ++o)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dst[4 * o + q] = acc[o][q];
+    dst[28] = qacc[0];
+    dst[29] = qacc[1];
   }
-  if (i0 == 0 && ti == 0 && j < r) out[7 * (int64_t)r * r + j] = qacc;
+  __syncthreads();
+  if (g < 2) {
+    const double* src = sm + (g * 64 + t) * kV;
+#pragma unroll
+    for (int o = 0; o < 7; ++o)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[o][q] += src[4 * o + q];
+    qacc[0] += src[28];
+    qacc[1] += src[29];
+  }
+  __syncthreads();
+  if (g == 1) {
+    double* dst = sm + t * kV;
+#pragma unroll
+    for (int o = 0; o < 7; ++o)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dst[4 * o + q] = acc[o][q];
+    dst[28] = qacc[0];
+    dst[29] = qacc[1];
+  }
+  __syncthreads();
+  if (g == 0) {
+    const double* src = sm + t * kV;
+    const int64_t stride = 7 * (int64_t)r * r + r;
+    double* out = pa.part + (int64_t)blockIdx.x * stride;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + 2 * ti + (q >> 1), j = j0 + 2 * tj + (q & 1);
+      if (i < r && j < r) {
+#pragma unroll
+        for (int o = 0; o < 7; ++o) out[(int64_t)o * r * r + (int64_t)i * r + j] = acc[o][q] + src[4 * o + q];
+      }
+    }
+    if (i0 == 0 && ti == 0) {
+      const int j = j0 + 2 * tj;
+      if (j < r) out[7 * (int64_t)r * r + j] = qacc[0] + src[28];
+      if (j + 1 < r) out[7 * (int64_t)r * r + j + 1] = qacc[1] + src[29];
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -727,6 +896,19 @@ int dlrsn_rowmix(int64_t n, int kx, int ky, const double* X, int ldx, const doub
                  double beta, double* Y, int ldy, dlrsn_stream_t stream) {
   DLRSN_REQUIRE(kx >= 0 && ky >= 0 && kx * ky <= 48 * 1024 / 8 * 4, "rowmix operand too large");
   if (n == 0 || ky == 0) return DLRSN_OK;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(X) | (uintptr_t)ldx * 8) & 15) == 0;
+  if (aligned && (kx == 8 || kx == 16 || kx == 32) && kRB % ky == 0) {
+    const int grid = grid_for(n * ky);
+    cudaStream_t st = as_stream(stream);
+    if (kx == 8)
+      rowmix_reg_kernel<8><<<grid, kRB, 0, st>>>((int)n, ky, X, ldx, K, ldk, beta, Y, ldy);
+    else if (kx == 16)
+      rowmix_reg_kernel<16><<<grid, kRB, 0, st>>>((int)n, ky, X, ldx, K, ldk, beta, Y, ldy);
+    else
+      rowmix_reg_kernel<32><<<grid, kRB, 0, st>>>((int)n, ky, X, ldx, K, ldk, beta, Y, ldy);
+    DLRSN_CHECK_LAUNCH("rowmix_reg_kernel");
+    return DLRSN_OK;
+  }
   const size_t smem = (size_t)kx * ky * sizeof(double);
   if (smem > 48 * 1024)
     DLRSN_TRY_CUDA(cudaFuncSetAttribute(rowmix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -60,6 +60,7 @@ __host__ __device__ constexpr size_t sweep_smem_bytes() {
 template <int DW>
 __global__ void __launch_bounds__(SweepCfg<DW>::WPC * 32)
 sweep_kernel(const SweepArgs a) {
+  if (a.skip && *a.skip) return;  // iteration past convergence
   constexpr int C = SweepCfg<DW>::C, P = SweepCfg<DW>::P, WPC = SweepCfg<DW>::WPC;
   constexpr int SD = stage_doubles<DW>();
   extern __shared__ __align__(128) double smem[];
@@ -371,14 +372,28 @@ __global__ void scatter_source_kernel(dlrsn_cellops ops, const double* __restric
   write_scat4(ops, c, p, s, scat, vlen);
 }
 
+// convergence test of transport_sn.py:430-447 on the device
+__device__ void si_decide(SiCtl* ctl, const double* w, int it, double tol, const int* any_scat) {
+  const double change = sqrt(w[0]) / fmax(sqrt(w[1]), 1e-300);
+  ctl->change = change;
+  ctl->last = it;
+  if (change <= tol || (it == 1 && any_scat && *any_scat == 0)) {
+    ctl->iters = it;
+    __threadfence();
+    ctl->done = 1;
+  }
+}
+
 __global__ void phi_combine_kernel(dlrsn_cellops ops, int G, const dlrsn_group* __restrict__ groups,
                                    const double* __restrict__ part, const double* __restrict__ psi,
                                    const double* __restrict__ phi_old,
                                    const double* __restrict__ ss, double* __restrict__ phi_new,
                                    double* __restrict__ scat, int64_t vlen, double* norms,
-                                   double* partials, unsigned* counter) {
+                                   double* partials, unsigned* counter, SiCtl* ctl, int it,
+                                   double tol, const int* any_scat) {
   __shared__ double red[64];
   __shared__ bool last;
+  if (ctl && ctl->done) return;
   const int nx = ops.nx, ny = ops.ny, T = nx + 31;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   double v[2] = {0.0, 0.0};
@@ -443,26 +458,31 @@ __global__ void phi_combine_kernel(dlrsn_cellops ops, int G, const dlrsn_group* 
       norms[0] = w[0];
       norms[1] = w[1];
       *counter = 0u;
+      if (ctl && it > 0) si_decide(ctl, w, it, tol, any_scat);
     }
   }
 }
 
 // Sharded iteration: phi (canonical) already summed over ranks; compute the
 // convergence norms against phi_old and the next scattering source.
-__global__ void phi_finish_kernel(dlrsn_cellops ops, const double* __restrict__ phi_new,
+__global__ void phi_finish_kernel(dlrsn_cellops ops, const double* __restrict__ phi_src,
+                                  double* __restrict__ phi_dst,
                                   const double* __restrict__ phi_old,
                                   const double* __restrict__ ss, double* __restrict__ scat,
                                   int64_t vlen, double* norms, double* partials,
-                                  unsigned* counter) {
+                                  unsigned* counter, SiCtl* ctl, int it, double tol,
+                                  const int* any_scat) {
   __shared__ double red[64];
   __shared__ bool last;
+  if (ctl && ctl->done) return;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   double v[2] = {0.0, 0.0};
   if (c < ops.nx * ops.ny) {
     double p[4], po[4];
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
-      p[l] = phi_new[4 * c + l];
+      p[l] = phi_src[4 * c + l];
+      if (phi_dst != phi_src) phi_dst[4 * c + l] = p[l];
       po[l] = phi_old[4 * c + l];
       const double d = p[l] - po[l];
       v[0] += d * d;
@@ -489,6 +509,7 @@ __global__ void phi_finish_kernel(dlrsn_cellops ops, const double* __restrict__ 
       norms[0] = w[0];
       norms[1] = w[1];
       *counter = 0u;
+      if (ctl && it > 0) si_decide(ctl, w, it, tol, any_scat);
     }
   }
 }
@@ -540,6 +561,42 @@ int launch_sweep(const SweepArgs& a, int max_ctas, cudaStream_t st) {
 
 using namespace dlrsn;
 
+namespace dlrsn {
+
+int phi_combine_launch(const dlrsn_cellops* ops, int G, const dlrsn_group* groups,
+                       const double* phi_part_sk, const double* psi_sk, const double* phi_old,
+                       const double* sigma_s, double* phi_new, double* scat_sk4, double* norms,
+                       void* partial_ws, SiCtl* ctl, int it, double tol, const int* any_scat,
+                       cudaStream_t st) {
+  const int n = ops->nx * ops->ny;
+  const int nb = (n + 255) / 256;
+  unsigned* counter = reinterpret_cast<unsigned*>(partial_ws);
+  double* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(partial_ws) + 256);
+  DLRSN_REQUIRE(phi_part_sk || psi_sk, "phi_combine needs partials or psi");
+  phi_combine_kernel<<<nb, 256, 0, st>>>(*ops, G, groups, phi_part_sk, psi_sk, phi_old, sigma_s,
+                                         phi_new, scat_sk4, sk_vec_len(ops->nx, ops->ny), norms,
+                                         partials, counter, ctl, it, tol, any_scat);
+  DLRSN_CHECK_LAUNCH("phi_combine_kernel");
+  return DLRSN_OK;
+}
+
+int phi_finish_launch(const dlrsn_cellops* ops, const double* phi_src, double* phi_dst,
+                      const double* phi_old, const double* sigma_s, double* scat_sk4,
+                      double* norms, void* partial_ws, SiCtl* ctl, int it, double tol,
+                      const int* any_scat, cudaStream_t st) {
+  const int n = ops->nx * ops->ny;
+  const int nb = (n + 255) / 256;
+  unsigned* counter = reinterpret_cast<unsigned*>(partial_ws);
+  double* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(partial_ws) + 256);
+  phi_finish_kernel<<<nb, 256, 0, st>>>(*ops, phi_src, phi_dst, phi_old, sigma_s, scat_sk4,
+                                        sk_vec_len(ops->nx, ops->ny), norms, partials, counter,
+                                        ctl, it, tol, any_scat);
+  DLRSN_CHECK_LAUNCH("phi_finish_kernel");
+  return DLRSN_OK;
+}
+
+}  // namespace dlrsn
+
 extern "C" {
 
 int64_t dlrsn_sweep_workspace_bytes(int nx, int ny, int n_groups, int dw) {
@@ -583,31 +640,16 @@ int dlrsn_phi_combine(const dlrsn_cellops* ops, int G, const dlrsn_group* groups
                       const double* sigma_s,
                       double* phi_new, double* scat_sk4, double* norms, void* partial_ws,
                       dlrsn_stream_t stream) {
-  const int n = ops->nx * ops->ny;
-  const int nb = (n + 255) / 256;
-  unsigned* counter = reinterpret_cast<unsigned*>(partial_ws);
-  double* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(partial_ws) + 256);
-  DLRSN_REQUIRE(phi_part_sk || psi_sk, "phi_combine needs partials or psi");
-  phi_combine_kernel<<<nb, 256, 0, as_stream(stream)>>>(*ops, G, groups, phi_part_sk, psi_sk, phi_old,
-                                                        sigma_s, phi_new, scat_sk4,
-                                                        sk_vec_len(ops->nx, ops->ny), norms,
-                                                        partials, counter);
-  DLRSN_CHECK_LAUNCH("phi_combine_kernel");
-  return DLRSN_OK;
+  return phi_combine_launch(ops, G, groups, phi_part_sk, psi_sk, phi_old, sigma_s, phi_new,
+                            scat_sk4, norms, partial_ws, nullptr, 0, 0.0, nullptr,
+                            as_stream(stream));
 }
 
 int dlrsn_phi_finish(const dlrsn_cellops* ops, const double* phi_new, const double* phi_old,
                      const double* sigma_s, double* scat_sk4, double* norms, void* partial_ws,
                      dlrsn_stream_t stream) {
-  const int n = ops->nx * ops->ny;
-  const int nb = (n + 255) / 256;
-  unsigned* counter = reinterpret_cast<unsigned*>(partial_ws);
-  double* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(partial_ws) + 256);
-  phi_finish_kernel<<<nb, 256, 0, as_stream(stream)>>>(*ops, phi_new, phi_old, sigma_s, scat_sk4,
-                                                       sk_vec_len(ops->nx, ops->ny), norms,
-                                                       partials, counter);
-  DLRSN_CHECK_LAUNCH("phi_finish_kernel");
-  return DLRSN_OK;
+  return phi_finish_launch(ops, phi_new, const_cast<double*>(phi_new), phi_old, sigma_s, scat_sk4,
+                           norms, partial_ws, nullptr, 0, 0.0, nullptr, as_stream(stream));
 }
 
 int dlrsn_sk_to_canonical(const dlrsn_cellops* ops, int D, const int* quad, const double* psi_sk,
@@ -670,10 +712,14 @@ int dlrsn_sweep_workspace_init(void* workspace, int64_t workspace_bytes, dlrsn_s
   return DLRSN_OK;
 }
 
-int dlrsn_sweep(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int dw,
-                const double* sigma_t_sk4, const double* scat_sk4, const double* rhs_sk,
-                double* psi_sk, double* phi_part_sk, void* workspace, int64_t workspace_bytes,
-                int max_ctas, dlrsn_stream_t stream) {
+}  // extern "C"
+
+namespace dlrsn {
+
+int sweep_launch(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int dw,
+                 const double* sigma_t_sk4, const double* scat_sk4, const double* rhs_sk,
+                 double* psi_sk, double* phi_part_sk, void* workspace, int64_t workspace_bytes,
+                 int max_ctas, const int* skip, cudaStream_t st) {
   DLRSN_REQUIRE(ops && groups && sigma_t_sk4 && rhs_sk && psi_sk && workspace,
                 "null argument to dlrsn_sweep");
   DLRSN_REQUIRE(dw == 1 || dw == 2 || dw == 4 || dw == 8, "sweep width must be 1, 2, 4 or 8");
@@ -681,7 +727,6 @@ int dlrsn_sweep(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int 
   DLRSN_REQUIRE(workspace_bytes >= need, "sweep workspace too small (%lld < %lld)",
                 (long long)workspace_bytes, (long long)need);
   if (G == 0) return DLRSN_OK;
-  cudaStream_t st = as_stream(stream);
   const int64_t head = handoff_offset_bytes(ops->nx, ops->ny, G);
   DLRSN_TRY_CUDA(cudaMemsetAsync(workspace, 0, sizeof(int), st));  // work ticket
   SweepArgs a;
@@ -715,6 +760,7 @@ int dlrsn_sweep(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int 
   a.slen = sk_scalar_len(ops->nx, ops->ny);
   a.trace = h_trace;
   a.trace_chunks = h_trace_chunks;
+  a.skip = skip;
   // single-direction groups: the warp-specialised kernel when the work items
   // barely fill the GPU (latency-bound regime), the multi-warp kernel when
   // there are enough items to hide the per-step latency by occupancy
@@ -739,6 +785,18 @@ int dlrsn_sweep(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int 
   }
   if (tm && rc == DLRSN_OK) DLRSN_TRY_CUDA(cudaEventRecord(tm->stop, st));
   return rc;
+}
+
+}  // namespace dlrsn
+
+extern "C" {
+
+int dlrsn_sweep(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int dw,
+                const double* sigma_t_sk4, const double* scat_sk4, const double* rhs_sk,
+                double* psi_sk, double* phi_part_sk, void* workspace, int64_t workspace_bytes,
+                int max_ctas, dlrsn_stream_t stream) {
+  return sweep_launch(ops, G, groups, dw, sigma_t_sk4, scat_sk4, rhs_sk, psi_sk, phi_part_sk,
+                      workspace, workspace_bytes, max_ctas, nullptr, as_stream(stream));
 }
 
 int dlrsn_sweep_timing(int enable) {

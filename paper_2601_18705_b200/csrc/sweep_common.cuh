@@ -25,6 +25,17 @@ struct SweepArgs {
   int64_t vlen, slen;
   unsigned long long* trace;  // debug timeline (dlrsn_debug_trace), null in production
   int trace_chunks;
+  const int* skip;  // device flag: return at once when set (speculative iterations)
+};
+
+// Device-side control of a batched source iteration (step.cu): iterations
+// enqueued past convergence see done = 1 and return immediately.
+struct SiCtl {
+  int done;    // converged (or pure absorber after one sweep)
+  int iters;   // iteration that converged
+  int last;    // last iteration that ran
+  int pad;
+  double change;  // last relative change
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -85,5 +96,21 @@ __device__ __forceinline__ void solve4(double* a, double* b, double* x) {
 
 
 int launch_sweep_ws(const SweepArgs& a, int max_ctas, cudaStream_t st);
+
+// internal entry points of the step (step.cu); the public C-ABI calls pass
+// skip / ctl = nullptr
+int sweep_launch(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int dw,
+                 const double* sigma_t_sk4, const double* scat_sk4, const double* rhs_sk,
+                 double* psi_sk, double* phi_part_sk, void* workspace, int64_t workspace_bytes,
+                 int max_ctas, const int* skip, cudaStream_t st);
+int phi_combine_launch(const dlrsn_cellops* ops, int G, const dlrsn_group* groups,
+                       const double* phi_part_sk, const double* psi_sk, const double* phi_old,
+                       const double* sigma_s, double* phi_new, double* scat_sk4, double* norms,
+                       void* partial_ws, SiCtl* ctl, int it, double tol, const int* any_scat,
+                       cudaStream_t st);
+int phi_finish_launch(const dlrsn_cellops* ops, const double* phi_src, double* phi_dst,
+                      const double* phi_old, const double* sigma_s, double* scat_sk4,
+                      double* norms, void* partial_ws, SiCtl* ctl, int it, double tol,
+                      const int* any_scat, cudaStream_t st);
 
 }  // namespace dlrsn

@@ -104,6 +104,7 @@ __device__ __forceinline__ void ws_factor_step(const SweepArgs& a, const double*
 }
 
 __global__ void __launch_bounds__(128) sweep_ws_kernel(const SweepArgs a) {
+  if (a.skip && *a.skip) return;  // iteration past convergence
   extern __shared__ __align__(128) double sm[];
   double* in_ring = sm;                 // 2 x kWsInD
   double* fac_ring = sm + 2 * kWsInD;   // 2 x kWsFacD

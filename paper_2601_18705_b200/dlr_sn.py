@@ -136,7 +136,8 @@ def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, 
     if engine not in ("native", "python"):
         raise ConfigurationError(f"unknown engine {engine!r}")
     if (engine == "native" and not use_dsa and not state.W.pinned
-            and state.rank <= _lib.MAX_RANK):
+            and state.rank <= _lib.MAX_RANK and (sweep_dw or 1) == 1
+            and (comm is None or comm.world_size <= 8)):
         if dsa_penalty not in ("simplified", "collocation"):
             raise ContractViolation(f"unknown dsa penalty variant {dsa_penalty!r}")
         return _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state,
