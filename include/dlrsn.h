@@ -123,12 +123,16 @@ int dlrsn_update_temperature(int n, const double* phi, int phi_per_dof, const do
  * linearisation of the next one (driver.py:486-487,532-534 +
  * physics.py:94-120).  sigma_a(T) = sigma_a0 * T^opacity_power when
  * opacity_power != 0 (Marshak), else sigma_a0. */
-int dlrsn_advance_relinearize(int n, const double* phi_dofs, double* T, double* sigma_a,
+/* sigma_a_in / denom_in are the finished step's coefficients (they may alias
+ * the outputs sigma_a / denom); T0_out (optional) receives a copy of the new
+ * T (the next step's linearisation point). */
+int dlrsn_advance_relinearize(int n, const double* phi_dofs, double* T,
+                              const double* sigma_a_in, const double* denom_in, double* sigma_a,
                               const double* sigma_a0, double opacity_power,
                               const double* rho_cv, double dt, double c, double a_r,
                               double t_floor, const double* ss_phys, const double* q_ext,
                               double* sigma_t, double* sigma_s, double* q, double* denom,
-                              int* status, dlrsn_stream_t stream);
+                              double* T0_out, int* status, dlrsn_stream_t stream);
 
 /* ---- K1: sweep data movement (transport_sn.py:377-450) */
 
@@ -255,6 +259,14 @@ int dlrsn_what_solve(int r, int m, const double* Lhat, const double* U, const do
  * monomials (exponent pairs, coords = extent x0,y0,lx,ly).  workspace:
  * dlrsn_cgs2_workspace_len(n) doubles; *status = 1 if the candidates ran
  * out (strict). */
+/* Weighted CholQR2 of a small tall n x m matrix (m <= 32, fits one CTA):
+ * Q R = W with Q^T diag(w) Q = I; ratio (2m) and flag (2) feed the
+ * speculative-CholQR guard (see dlrsn_chol_upper); deficient[k] = 0.  The
+ * full-rank fast path of the angular re-orthonormalisation. */
+int64_t dlrsn_cholqr2_small_smem(int n, int m);
+int dlrsn_cholqr2_small(int n, int m, const double* W, int ldw, const double* w, double* Q,
+                        int ldq, double* R, double* ratio, int* flag, int* deficient,
+                        dlrsn_stream_t stream);
 int64_t dlrsn_cgs2_workspace_len(int n);
 int dlrsn_cgs2(int n, int m, const double* cols, int ldc, double* Q, int ldq, double* R,
                int* deficient, int metric, const double* w, const dlrsn_cellops* ops,
@@ -282,7 +294,8 @@ typedef struct dlrsn_step_info { /* HOST, filled by the call */
   int spatial_deficiency;
   int angular_deficiency;
   int error_index;           /* InterpolationError column / singular node, else -1 */
-  int gs_fallback;           /* 1 if the exact CGS2 pass replaced CholQR2 */
+  int gs_fallback;           /* bit 0: exact CGS2 replaced the spatial CholQR2,
+                                bit 1: ... the angular one */
   double residual;           /* last source-iteration change */
   double check_in[2];        /* input orthonormality residuals (spatial, angular) */
   double check_out[2];

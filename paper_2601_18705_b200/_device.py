@@ -34,13 +34,16 @@ def set_device(index):
 
 
 def stream():
-    return ctypes.c_void_p(torch.cuda.current_stream(device()).cuda_stream)
+    """Raw handle of the current CUDA stream (the C-ABI's dlrsn_stream_t)."""
+    return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(device().index))
 
 
 def as_device(x, n=None, dtype=torch.float64):
     """fp64 contiguous CUDA tensor from numpy / torch / scalar (scalars
     broadcast to length ``n``)."""
     if isinstance(x, torch.Tensor):
+        if x.dtype == dtype and x.is_cuda and x.ndim > 0 and x.is_contiguous():
+            return x  # fast path: already a device tensor of the right kind
         t = x.to(device=device(), dtype=dtype)
     else:
         a = np.asarray(x, dtype=np.float64 if dtype == torch.float64 else None)

@@ -82,9 +82,9 @@ _SIGNATURES = {
                                 c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "dlrsn_update_temperature": (c_int, [c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_dbl, c_dbl,
                                          c_dbl, c_dbl, c_vp, c_vp]),
-    "dlrsn_advance_relinearize": (c_int, [c_int, c_vp, c_vp, c_vp, c_vp, c_dbl, c_vp, c_dbl,
-                                          c_dbl, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp,
-                                          c_vp, c_vp, c_vp]),
+    "dlrsn_advance_relinearize": (c_int, [c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_dbl,
+                                          c_vp, c_dbl, c_dbl, c_dbl, c_dbl, c_vp, c_vp, c_vp,
+                                          c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "dlrsn_rhs_build": (c_int, [c_vp, c_int, c_vp, c_vp, c_dbl, c_vp, c_int, c_vp, c_int, c_vp,
                                 c_vp]),
     "dlrsn_cells_to_sk4": (c_int, [c_vp, c_vp, c_vp, c_vp]),
@@ -107,6 +107,9 @@ _SIGNATURES = {
     "dlrsn_deim": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "dlrsn_what_solve": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp]),
     "dlrsn_cgs2_workspace_len": (c_i64, [c_int]),
+    "dlrsn_cholqr2_small_smem": (c_i64, [c_int, c_int]),
+    "dlrsn_cholqr2_small": (c_int, [c_int, c_int, c_vp, c_int, c_vp, c_vp, c_int, c_vp, c_vp, c_vp,
+                                    c_vp, c_vp]),
     "dlrsn_sweep_timing": (c_int, [c_int]),
     "dlrsn_sweep_timing_read": (c_int, [c_int, c_vp, c_vp, c_vp, c_vp]),
     "dlrsn_step_workspace_bytes": (c_i64, [c_int, c_int, c_int, c_int, c_int]),

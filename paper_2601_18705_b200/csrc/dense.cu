@@ -80,19 +80,83 @@ __global__ void __launch_bounds__(256) rowmix_reg_kernel(int n, int ky, const do
 // (coalesced), then the 8 warp sums are added in fixed order.
 __global__ void reduce_partials_kernel(int nchunks, int64_t len, const double* __restrict__ part,
                                        double* __restrict__ out, double alpha) {
-  __shared__ double red[8][33];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // block = 32 consecutive outputs x nw warps; warp w sums chunks w, w+nw, ...
+  // (coalesced, two independent chains), then the warp sums are added in
+  // warp order (deterministic for a given launch shape)
+  __shared__ double red[32][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int64_t e = (int64_t)blockIdx.x * 32 + lane;
-  double s = 0.0;
-  if (e < len)
-    for (int c = w; c < nchunks; c += 8) s += part[(int64_t)c * len + e];
-  red[w][lane] = s;
+  double s0 = 0.0, s1 = 0.0;
+  if (e < len) {
+    int c = w;
+    for (; c + nw < nchunks; c += 2 * nw) {
+      s0 += __ldg(part + (int64_t)c * len + e);
+      s1 += __ldg(part + (int64_t)(c + nw) * len + e);
+    }
+    if (c < nchunks) s0 += __ldg(part + (int64_t)c * len + e);
+  }
+  red[w][lane] = s0 + s1;
   __syncthreads();
   if (w == 0 && e < len) {
     double t = 0.0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) t += red[q][lane];
+    for (int q = 0; q < nw; ++q) t += red[q][lane];
     out[e] = alpha * t;
+  }
+}
+
+// FP64 tensor-core MMA (DMMA), D(8x8) += A(8x4) B(4x8); fragments per lane
+// (g = lane / 4, q = lane % 4): A[g][q], B[q][g], D[g][2q], D[g][2q+1].
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// rowmix on the FP64 tensor cores: each warp multiplies 8-row tiles of X by
+// K (KS k-steps of 4, NT n-tiles of 8), K's fragments held in registers for
+// the whole launch and X's fragments loaded straight from global memory.
+template <int KS, int NT>
+__global__ void __launch_bounds__(256) rowmix_mma_kernel(int n, int kx, int ky,
+                                                         const double* __restrict__ X, int ldx,
+                                                         const double* __restrict__ K, int ldk,
+                                                         double beta, double* __restrict__ Y,
+                                                         int ldy) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  double bf[KS][NT];
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int k = 4 * ks + q, c = 8 * nt + g;
+      bf[ks][nt] = (k < kx && c < ky) ? __ldg(K + (int64_t)k * ldk + c) : 0.0;
+    }
+  const int64_t tiles = ((int64_t)n + 7) / 8;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < tiles; t += nwarps) {
+    const int64_t row = t * 8 + g;
+    double af[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int c = 4 * ks + q;
+      af[ks] = (row < n && c < kx) ? __ldg(X + row * ldx + c) : 0.0;
+    }
+    double d[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) d[nt][0] = d[nt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) dmma(d[nt][0], d[nt][1], af[ks], bf[ks][nt]);
+    if (row < n) {
+      double* y = Y + row * ldy;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int c = 8 * nt + 2 * q + i;
+          if (c < ky) y[c] = beta == 0.0 ? d[nt][i] : fma(beta, y[c], d[nt][i]);
+        }
+    }
   }
 }
 
@@ -183,6 +247,70 @@ __global__ void __launch_bounds__(256) mgram_kernel(int ncell, int ra, int rb,
       if (i < ra && j < rb) out[(int64_t)i * rb + j] = v[q];
     }
   }
+}
+
+// mgram on the FP64 tensor cores: warp w of the block takes cells
+// c_begin + w, + 8, ...; per cell the k dimension of the MMA is the cell's 4
+// dofs, A = X_c^T (m = column of A), B = M X_c (the 4x4 mass block applied
+// across each lane quad by shuffles).  Warp partials are summed in warp order.
+__global__ void __launch_bounds__(256) mgram_mma_kernel(int ncell, int ra, int rb,
+                                                        const double* __restrict__ A, int lda,
+                                                        const double* __restrict__ B, int ldb,
+                                                        const double* __restrict__ coeff,
+                                                        dlrsn_cellops ops, int cells_per_block,
+                                                        double* __restrict__ part) {
+  __shared__ double red[8][kTile * kTile];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, q = lane & 3;
+  const int tiles_j = (rb + kTile - 1) / kTile;
+  const int i0 = (blockIdx.y / tiles_j) * kTile, j0 = (blockIdx.y % tiles_j) * kTile;
+  const int c_begin = blockIdx.x * cells_per_block;
+  const int c_end = min(ncell, c_begin + cells_per_block);
+  double m[4];
+#pragma unroll
+  for (int b = 0; b < 4; ++b) m[b] = ops.mass[4 * q + b];
+  const bool same = (A == B) && (lda == ldb) && (i0 == j0);
+  const bool ia0 = i0 + g < ra, ia1 = i0 + 8 + g < ra, jb0 = j0 + g < rb, jb1 = j0 + 8 + g < rb;
+  const int base = lane & ~3;
+  double d[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
+#pragma unroll 4
+  for (int c = c_begin + warp; c < c_end; c += 8) {
+    const int64_t row = (int64_t)c * 4 + q;
+    const double a0 = ia0 ? __ldg(A + row * lda + i0 + g) : 0.0;
+    const double a1 = ia1 ? __ldg(A + row * lda + i0 + 8 + g) : 0.0;
+    double v0 = a0, v1 = a1;
+    if (!same) {
+      v0 = jb0 ? __ldg(B + row * ldb + j0 + g) : 0.0;
+      v1 = jb1 ? __ldg(B + row * ldb + j0 + 8 + g) : 0.0;
+    }
+    double b0 = 0.0, b1 = 0.0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      b0 = fma(m[b], __shfl_sync(kFull, v0, base | b), b0);
+      b1 = fma(m[b], __shfl_sync(kFull, v1, base | b), b1);
+    }
+    if (coeff) {
+      const double w = __ldg(coeff + c);
+      b0 *= w;
+      b1 *= w;
+    }
+    dmma(d[0][0][0], d[0][0][1], a0, b0);
+    dmma(d[0][1][0], d[0][1][1], a0, b1);
+    dmma(d[1][0][0], d[1][0][1], a1, b0);
+    dmma(d[1][1][0], d[1][1][1], a1, b1);
+  }
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) red[warp][(8 * mt + g) * kTile + 8 * nt + 2 * q + i] = d[mt][nt][i];
+  __syncthreads();
+  const int e = threadIdx.x;  // 256 = kTile * kTile entries
+  double s = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) s += red[w][e];
+  const int i = i0 + e / kTile, j = j0 + e % kTile;
+  if (i < ra && j < rb) part[(int64_t)blockIdx.x * ra * rb + (int64_t)i * rb + j] = s;
 }
 
 // ---------------------------------------------------------------------------
@@ -542,6 +670,235 @@ __global__ void chol_upper_kernel(int r, const double* __restrict__ G, double* _
   if (threadIdx.x == 0 && flag) *flag = bad;
 }
 
+// Asynchronous global -> shared copies (LDGSTS): a single-CTA kernel issues
+// all its loads at once and pays the memory latency one time.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// Register-resident single-warp Cholesky G = R^T R (R upper), r <= RT <= 32:
+// lane j holds column j (c[i] = G[i][j] on entry, R[i][j] on exit); row k
+// entries of other columns arrive by shuffles.  Same operation order as the
+// shared-memory version.  inv returns column j of R^-1.
+template <int RT>
+__device__ int warp_chol_reg(int r, double (&c)[RT], double (&inv)[RT]) {
+  const int lane = threadIdx.x & 31;
+  int bad = 0;
+#pragma unroll
+  for (int k = 0; k < RT; ++k) {
+    if (k < r) {
+      const double d = __shfl_sync(kFull, c[k], k);
+      const bool ok = d > 0.0;
+      bad |= !ok;
+      const double rkk = ok ? sqrt(d) : 0.0;
+      if (lane == k) c[k] = rkk;
+      else if (lane > k) c[k] = rkk > 0.0 ? c[k] / rkk : 0.0;
+#pragma unroll
+      for (int i = k + 1; i < RT; ++i) {
+        const double aki = __shfl_sync(kFull, c[k], i);
+        if (i < r && i <= lane) c[i] -= aki * c[k];
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < RT; ++i)
+    if (i > lane) c[i] = 0.0;  // strict lower part of R
+  // R^-1 column j = lane by back substitution; R[i][p] = lane p's c[i]
+#pragma unroll
+  for (int i = RT - 1; i >= 0; --i) {
+    double s = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int p = i + 1; p < RT; ++p) {
+      const double rip = __shfl_sync(kFull, c[i], p);
+      if (p <= lane && p < r) s -= rip * inv[p];
+    }
+    const double dd = __shfl_sync(kFull, c[i], i);
+    inv[i] = (i <= lane && i < r && dd > 0.0) ? s / dd : 0.0;
+  }
+  return bad;
+}
+
+// Single-warp Cholesky G = R^T R (R upper, r <= 32) on a shared copy `a`
+// (row-major, becomes R) and R^-1 into `inv`; lane j owns column j, so only
+// __syncwarp is needed.  Same operation order as chol_upper_kernel.
+// ratio (optional, 2r): R_kk / sqrt(G_kk) and R_kk / max(sqrt(G_kk), 1).
+__device__ int warp_chol_inv(int r, double* a, double* inv, double* ratio) {
+  const int lane = threadIdx.x & 31;
+  int bad = 0;
+  for (int k = 0; k < r; ++k) {
+    const double g = a[k * r + k];
+    const double d = g;  // a[k][k] already holds the updated pivot
+    const bool ok = d > 0.0;
+    bad |= !ok;
+    const double rkk = ok ? sqrt(d) : 0.0;
+    __syncwarp();
+    if (lane == k) a[k * r + k] = rkk;
+    if (lane > k && lane < r) a[k * r + lane] = rkk > 0.0 ? a[k * r + lane] / rkk : 0.0;
+    __syncwarp();
+    if (lane > k && lane < r) {
+      const double akj = a[k * r + lane];
+      for (int i = k + 1; i <= lane; ++i) a[i * r + lane] -= a[k * r + i] * akj;
+    }
+    __syncwarp();
+  }
+  // inverse by columns: back substitution R x = e_j
+  if (lane < r) {
+    const int j = lane;
+    for (int i = r - 1; i > j; --i) inv[i * r + j] = 0.0;
+    for (int i = j; i >= 0; --i) {
+      double s = (i == j) ? 1.0 : 0.0;
+      for (int p = i + 1; p <= j; ++p) s -= a[i * r + p] * inv[p * r + j];
+      const double dd = a[i * r + i];
+      inv[i * r + j] = dd > 0.0 ? s / dd : 0.0;
+    }
+    for (int i = j + 1; i < r; ++i) a[i * r + j] = 0.0;  // R: zero the strict lower part
+  }
+  __syncwarp();
+  return bad;
+}
+
+// chol_upper for r <= 32: one warp, registers only
+template <int RT>
+__global__ void chol_upper_warp_kernel(int r, const double* __restrict__ G, double* __restrict__ R,
+                                       double* __restrict__ Rinv, double* __restrict__ diag_ratio,
+                                       int* flag) {
+  const int lane = threadIdx.x;
+  double c[RT], inv[RT];
+#pragma unroll
+  for (int i = 0; i < RT; ++i) c[i] = (i < r && lane < r) ? __ldg(G + i * r + lane) : 0.0;
+  const double gkk = lane < r ? __ldg(G + lane * r + lane) : 0.0;
+  const int bad = warp_chol_reg<RT>(r, c, inv);
+  if (lane < r) {
+#pragma unroll
+    for (int i = 0; i < RT; ++i)
+      if (i < r) {
+        R[i * r + lane] = c[i];
+        Rinv[i * r + lane] = inv[i];
+      }
+    if (diag_ratio) {
+      double rkk = 0.0;
+#pragma unroll
+      for (int i = 0; i < RT; ++i)
+        if (i == lane) rkk = c[i];
+      const double on = sqrt(fmax(gkk, 0.0));
+      diag_ratio[lane] = (rkk > 0.0 && on > 0.0) ? rkk / on : 0.0;
+      diag_ratio[r + lane] = rkk > 0.0 ? rkk / fmax(on, 1.0) : 0.0;
+    }
+  }
+  if (lane == 0 && flag) *flag = bad;
+}
+
+// Weighted CholQR2 of a small tall matrix held in shared memory (the angular
+// basis update, angular.py:217-238, full-rank case): Q = W R^-1 with
+// W^T diag(w) W = R^T R, applied twice; R = R2 R1.  ratio/flag feed the same
+// guard as the spatial CholQR2 (a failed guard reruns the exact CGS2).
+template <int MT>
+__global__ void __launch_bounds__(256) cholqr2_small_kernel(int n, int m,
+                                                            const double* __restrict__ Win,
+                                                            int ldw, const double* __restrict__ w,
+                                                            double* __restrict__ Q, int ldq,
+                                                            double* __restrict__ R,
+                                                            double* __restrict__ ratio,
+                                                            int* flag, int* deficient) {
+  extern __shared__ double sm[];
+  const int lq = m | 1;
+  double* A = sm;                       // n x lq
+  double* G = A + (size_t)n * lq;       // m x m (becomes R of the pass)
+  double* inv = G + m * m;              // m x m
+  double* R1 = inv + m * m;             // m x m
+  double* g0 = R1 + m * m;              // m (diag of the first Gram)
+  __shared__ int bad_s[2];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t e = threadIdx.x; e < (int64_t)n * m; e += blockDim.x)
+    cp_async8(A + (e / m) * lq + e % m, Win + (e / m) * ldw + e % m);
+  double* ws = g0 + m;  // n weights
+  for (int e = threadIdx.x; e < n; e += blockDim.x) cp_async8(ws + e, w + e);
+  cp_async_wait_all();
+  __syncthreads();
+  const int ntri = m * (m + 1) / 2;
+  for (int pass = 0; pass < 2; ++pass) {
+    // Gram (upper triangle): warp per entry, lanes over rows, shuffle sums
+    for (int t = wid; t < ntri; t += nw) {
+      int i = 0, rem = t;
+      while (rem >= m - i) { rem -= m - i; ++i; }
+      const int j = i + rem;
+      double acc = 0.0;
+      for (int row = lane; row < n; row += 32) acc += ws[row] * A[row * lq + i] * A[row * lq + j];
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+      if (lane == 0) {
+        G[i * m + j] = acc;
+        G[j * m + i] = acc;
+      }
+    }
+    __syncthreads();
+    if (wid == 0) {
+      double c[MT], iv[MT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) c[i] = (i < m && lane < m) ? G[i * m + lane] : 0.0;
+      const double gkk = lane < m ? G[lane * m + lane] : 0.0;
+      const int bad = warp_chol_reg<MT>(m, c, iv);
+      __syncwarp();
+      if (lane < m) {
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+          if (i < m) {
+            G[i * m + lane] = c[i];
+            inv[i * m + lane] = iv[i];
+          }
+      }
+      if (lane == 0) bad_s[pass] = bad;
+      if (pass == 0 && lane < m) {
+        double rkk = 0.0;
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+          if (i == lane) rkk = c[i];
+        const double on = sqrt(fmax(gkk, 0.0));
+        ratio[lane] = (rkk > 0.0 && on > 0.0) ? rkk / on : 0.0;
+        ratio[m + lane] = rkk > 0.0 ? rkk / fmax(on, 1.0) : 0.0;
+      }
+    }
+    __syncthreads();
+    // A = A R^-1, row by row
+    for (int row = threadIdx.x; row < n; row += blockDim.x) {
+      double x[MT], y[MT];
+#pragma unroll
+      for (int p = 0; p < MT; ++p) x[p] = p < m ? A[row * lq + p] : 0.0;
+#pragma unroll
+      for (int j = 0; j < MT; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int p = 0; p <= j; ++p)
+          if (j < m) acc = fma(x[p], inv[p * m + j], acc);
+        y[j] = acc;
+      }
+#pragma unroll
+      for (int j = 0; j < MT; ++j)
+        if (j < m) A[row * lq + j] = y[j];
+    }
+    if (pass == 0)
+      for (int e = threadIdx.x; e < m * m; e += blockDim.x) R1[e] = G[e];
+    __syncthreads();
+  }
+  // R = R2 R1 (both upper)
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const int i = e / m, j = e % m;
+    double acc = 0.0;
+    for (int p = i; p <= j; ++p) acc = fma(G[i * m + p], R1[p * m + j], acc);
+    R[e] = j >= i ? acc : 0.0;
+  }
+  for (int64_t e = threadIdx.x; e < (int64_t)n * m; e += blockDim.x)
+    Q[(e / m) * ldq + e % m] = A[(e / m) * lq + e % m];
+  for (int k = threadIdx.x; k < m; k += blockDim.x) deficient[k] = 0;
+  if (threadIdx.x == 0) {
+    flag[0] = bad_s[0];
+    flag[1] = bad_s[1];
+  }
+}
+
 // C = A B for small square r x r (one CTA); used for R = R2 R1 etc.
 __global__ void small_matmul_kernel(int m, int k, int n, const double* __restrict__ A,
                                     const double* __restrict__ B, double* __restrict__ C,
@@ -699,16 +1056,21 @@ __global__ void row_combine_kernel(int n, int r, const double* __restrict__ Binv
     for (int d = 0; d < n; ++d) s += wts[d] * Binv[d * rr + e];
     cbar[e] = s;
   }
-  for (int i = threadIdx.x; i < r; i += blockDim.x) {
-    double s = 0.0;
-    for (int d = 0; d < n; ++d) {
-      double bq = 0.0;
-      for (int j = 0; j < r; ++j) bq += Binv[d * rr + i * r + j] * Q[d * r + j];
-      s += wts[d] * bq;
-    }
-    zeta[i] = s;
+  // zeta = sum_d w_d Binv_d q_d: the per-node products in parallel (stored
+  // in lhs as scratch), then the node sum in fixed order
+  for (int e = threadIdx.x; e < n * r; e += blockDim.x) {
+    const int d = e / r, i = e % r;
+    double bq = 0.0;
+    for (int j = 0; j < r; ++j) bq += Binv[d * rr + i * r + j] * Q[d * r + j];
+    L[e] = bq;  // L is overwritten below
   }
   if (threadIdx.x == 0) sing = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < r; i += blockDim.x) {
+    double s = 0.0;
+    for (int d = 0; d < n; ++d) s += wts[d] * L[d * r + i];
+    zeta[i] = s;
+  }
   __syncthreads();
   for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
     const int i = e / r, j = e % r;
@@ -739,76 +1101,89 @@ __global__ void row_combine_kernel(int n, int r, const double* __restrict__ Binv
 // the interpolation residual W[:,j] - W[:,:j] W[p,:j]^-1 W[p,j]; the pivot is
 // its first maximal |entry| (np.argmax).  Produces the picks, the unit lower
 // factor rows L[p,:] and U (so W[p,:] = Lhat U), all in pick order.
-__global__ void deim_kernel(int n, int r, double* __restrict__ Wk_global /* n x r work copy */,
-                            const double* __restrict__ W, int* __restrict__ idx,
-                            double* __restrict__ Lhat, double* __restrict__ U, int* err_col,
-                            int in_smem) {
+__global__ void __launch_bounds__(256) deim_kernel(int n, int r,
+                                                   double* __restrict__ Wk_global /* n x r work */,
+                                                   const double* __restrict__ W,
+                                                   int* __restrict__ idx, double* __restrict__ Lhat,
+                                                   double* __restrict__ U, int* err_col,
+                                                   int in_smem) {
+  // Column-major work copy (smem when it fits).  Per column: block argmax
+  // of |residual| (first index on ties) with two barriers; the picked row is
+  // read-only during the elimination (its own update would zero it exactly,
+  // so it is skipped and excluded from later argmaxes instead).
   extern __shared__ double dsm[];
-  double* Wk = in_smem ? dsm : Wk_global;  // work copy resident in smem when it fits
-  __shared__ double bv[33];
-  __shared__ int bi[32];
-  __shared__ int pick;
-  __shared__ double pval;
-  __shared__ int fail;
-  if (threadIdx.x == 0) fail = -1;
-  // working copy and floor = 1e-14 * max(1, max|W|) (lowrank.py:185)
+  double* Wk = in_smem ? dsm : Wk_global;
+  unsigned char* picked = reinterpret_cast<unsigned char*>(in_smem ? dsm + (size_t)n * r : nullptr);
+  __shared__ double bv[2][8];
+  __shared__ int bi[2][8];
+  __shared__ double s_floor[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double mx = 0.0;
-  for (int64_t e = threadIdx.x; e < (int64_t)n * r; e += blockDim.x) {
-    const double v = W[e];
-    Wk[(e % r) * n + e / r] = v;  // column-major work copy (coalesced column access)
-    mx = fmax(mx, fabs(v));
+  if (in_smem) {
+    for (int64_t e = threadIdx.x; e < (int64_t)n * r; e += blockDim.x)
+      cp_async8(Wk + (e % r) * n + e / r, W + e);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) picked[i] = 0;
+    cp_async_wait_all();
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < (int64_t)n * r; e += blockDim.x) mx = fmax(mx, fabs(Wk[e]));
+  } else {
+    for (int64_t e = threadIdx.x; e < (int64_t)n * r; e += blockDim.x) {
+      const int i = (int)(e / r), k = (int)(e % r);
+      const double v = W[e];
+      Wk[(int64_t)k * n + i] = v;
+      mx = fmax(mx, fabs(v));
+    }
   }
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_down_sync(kFull, mx, o));
-  if ((threadIdx.x & 31) == 0) bv[threadIdx.x >> 5] = mx;
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
+  if (lane == 0) s_floor[w] = mx;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double m = 0.0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) m = fmax(m, bv[q]);
-    bv[32] = 1e-14 * fmax(1.0, m);
-  }
-  __syncthreads();
-  const double floor_ = bv[32];
-  __syncthreads();
+  double m0 = 0.0;
+  for (int q = 0; q < nw; ++q) m0 = fmax(m0, s_floor[q]);
+  const double floor_ = 1e-14 * fmax(1.0, m0);  // lowrank.py:185
+  int fail = -1;
   for (int j = 0; j < r; ++j) {
-    // argmax |Wk[:, j]|, lowest index on ties
+    const int buf = j & 1;
     double best = -1.0;
     int bidx = 0x7fffffff;
+    const double* col = Wk + (int64_t)j * n;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const double v = fabs(Wk[(int64_t)j * n + i]);
-      if (v > best || (v == best && i < bidx)) { best = v; bidx = i; }
+      if (picked && picked[i]) continue;
+      const double v = fabs(col[i]);
+      if (v > best) { best = v; bidx = i; }  // rows ascend per thread: first max kept
     }
     for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_down_sync(kFull, best, o);
-      const int oi = __shfl_down_sync(kFull, bidx, o);
+      const double ov = __shfl_xor_sync(kFull, best, o);
+      const int oi = __shfl_xor_sync(kFull, bidx, o);
       if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
     }
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (lane == 0) { bv[w] = best; bi[w] = bidx; }
+    if (lane == 0) { bv[buf][w] = best; bi[buf][w] = bidx; }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      double b = -1.0;
-      int ii = 0x7fffffff;
-      for (int q = 0; q < (int)(blockDim.x >> 5); ++q)
-        if (bv[q] > b || (bv[q] == b && bi[q] < ii)) { b = bv[q]; ii = bi[q]; }
-      pick = ii;
-      pval = Wk[(int64_t)j * n + ii];
-      if (!(fabs(pval) > floor_)) fail = j;
-      for (int q = 0; q < j; ++q)
-        if (idx[q] == ii) fail = j;
-      idx[j] = ii;
+    double b = -1.0;
+    int p = 0x7fffffff;
+    for (int q = 0; q < nw; ++q)
+      if (bv[buf][q] > b || (bv[buf][q] == b && bi[buf][q] < p)) { b = bv[buf][q]; p = bi[buf][q]; }
+    if (p < 0 || p >= n) p = 0;  // all-NaN column: still a valid row
+    const double pv = col[p];
+    bool bad = !(fabs(pv) > floor_);
+    if (!picked)
+      for (int q = 0; q < j; ++q) bad |= idx[q] == p;  // (global-memory variant)
+    if (threadIdx.x == 0) idx[j] = p;
+    if (bad) { fail = j; break; }
+    // U row j = pivot row, columns j..r-1; eliminate below (rows != p)
+    for (int k = threadIdx.x; k < r; k += blockDim.x) U[j * r + k] = k >= j ? Wk[(int64_t)k * n + p] : 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      if (i == p || (picked && picked[i])) continue;
+      const double l = col[i] / pv;
+      Wk[(int64_t)j * n + i] = l;  // the multiplier column (Lhat entries)
+      for (int k = j + 1; k < r; ++k) Wk[(int64_t)k * n + i] -= l * Wk[(int64_t)k * n + p];
     }
     __syncthreads();
-    if (fail >= 0) break;
-    const int p = pick;
-    const double pv = pval;
-    // U row j = pivot row of the current (updated) matrix, columns j..r-1
-    for (int k = threadIdx.x; k < r; k += blockDim.x) U[j * r + k] = k >= j ? Wk[(int64_t)k * n + p] : 0.0;
-    __syncthreads();
-    // l = col / pivot; trailing update W[:, k] -= l * W[p, k] for k > j
-    for (int64_t e = threadIdx.x; e < (int64_t)n; e += blockDim.x) {
-      const double l = Wk[(int64_t)j * n + e] / pv;
-      Wk[(int64_t)j * n + e] = l;  // keep the multiplier column
-      for (int k = j + 1; k < r; ++k) Wk[(int64_t)k * n + e] -= l * U[j * r + k];
+    if (picked && threadIdx.x == 0) picked[p] = 1;
+    if (!picked) {
+      // global variant: the picked row is excluded by the duplicate test
+      // above; zero it as the elimination would
+      for (int k = j + 1 + threadIdx.x; k < r; k += blockDim.x) Wk[(int64_t)k * n + p] = 0.0;
+      if (threadIdx.x == 0) Wk[(int64_t)j * n + p] = 1.0;
     }
     __syncthreads();
   }
@@ -835,44 +1210,58 @@ __global__ void what_solve_kernel(int r, int m, const double* __restrict__ Lhat,
   double* sU = sL + r * r;       // r x r
   double* sX = sU + r * r;       // r x m
   for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
-    sL[e] = Lhat[e];
-    sU[e] = U[e];
+    cp_async8(sL + e, Lhat + e);
+    cp_async8(sU + e, U + e);
   }
-  for (int e = threadIdx.x; e < r * m; e += blockDim.x) sX[e] = V[e];
+  for (int e = threadIdx.x; e < r * m; e += blockDim.x) cp_async8(sX + e, V + e);
+  cp_async_wait_all();
   __syncthreads();
-  // one warp per right-hand side: the row recurrences are sequential, the
-  // inner products over the solved entries are split across the lanes
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int c = warp; c < m; c += nw) {
+  // one thread per right-hand side: sequential substitutions, the factor
+  // entries are warp-broadcast reads, the solution column is thread-private
+  // (two partial sums per row for a shorter dependency chain)
+  for (int c = threadIdx.x; c < m; c += blockDim.x) {
+    double* x = sX + c;
     if (mode == 0) {
       for (int i = 0; i < r; ++i) {  // L y = v
-        double s = 0.0;
-        for (int p = lane; p < i; p += 32) s += sL[i * r + p] * sX[p * m + c];
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(kFull, s, o);
-        if (lane == 0) sX[i * m + c] -= s;
-        __syncwarp();
+        double s0 = 0.0, s1 = 0.0;
+        int p = 0;
+        for (; p + 1 < i; p += 2) {
+          s0 = fma(sL[i * r + p], x[p * m], s0);
+          s1 = fma(sL[i * r + p + 1], x[(p + 1) * m], s1);
+        }
+        if (p < i) s0 = fma(sL[i * r + p], x[p * m], s0);
+        x[i * m] -= s0 + s1;
       }
       for (int i = r - 1; i >= 0; --i) {  // U x = y
-        double s = 0.0;
-        for (int p = i + 1 + lane; p < r; p += 32) s += sU[i * r + p] * sX[p * m + c];
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(kFull, s, o);
-        if (lane == 0) sX[i * m + c] = (sX[i * m + c] - s) / sU[i * r + i];
-        __syncwarp();
+        double s0 = 0.0, s1 = 0.0;
+        int p = i + 1;
+        for (; p + 1 < r; p += 2) {
+          s0 = fma(sU[i * r + p], x[p * m], s0);
+          s1 = fma(sU[i * r + p + 1], x[(p + 1) * m], s1);
+        }
+        if (p < r) s0 = fma(sU[i * r + p], x[p * m], s0);
+        x[i * m] = (x[i * m] - (s0 + s1)) / sU[i * r + i];
       }
     } else {
       for (int i = 0; i < r; ++i) {  // U^T y = v
-        double s = 0.0;
-        for (int p = lane; p < i; p += 32) s += sU[p * r + i] * sX[p * m + c];
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(kFull, s, o);
-        if (lane == 0) sX[i * m + c] = (sX[i * m + c] - s) / sU[i * r + i];
-        __syncwarp();
+        double s0 = 0.0, s1 = 0.0;
+        int p = 0;
+        for (; p + 1 < i; p += 2) {
+          s0 = fma(sU[p * r + i], x[p * m], s0);
+          s1 = fma(sU[(p + 1) * r + i], x[(p + 1) * m], s1);
+        }
+        if (p < i) s0 = fma(sU[p * r + i], x[p * m], s0);
+        x[i * m] = (x[i * m] - (s0 + s1)) / sU[i * r + i];
       }
       for (int i = r - 1; i >= 0; --i) {  // L^T x = y
-        double s = 0.0;
-        for (int p = i + 1 + lane; p < r; p += 32) s += sL[p * r + i] * sX[p * m + c];
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(kFull, s, o);
-        if (lane == 0) sX[i * m + c] -= s;
-        __syncwarp();
+        double s0 = 0.0, s1 = 0.0;
+        int p = i + 1;
+        for (; p + 1 < r; p += 2) {
+          s0 = fma(sL[p * r + i], x[p * m], s0);
+          s1 = fma(sL[(p + 1) * r + i], x[(p + 1) * m], s1);
+        }
+        if (p < r) s0 = fma(sL[p * r + i], x[p * m], s0);
+        x[i * m] -= s0 + s1;
       }
     }
   }
@@ -896,6 +1285,30 @@ int dlrsn_rowmix(int64_t n, int kx, int ky, const double* X, int ldx, const doub
                  double beta, double* Y, int ldy, dlrsn_stream_t stream) {
   DLRSN_REQUIRE(kx >= 0 && ky >= 0 && kx * ky <= 48 * 1024 / 8 * 4, "rowmix operand too large");
   if (n == 0 || ky == 0) return DLRSN_OK;
+  if (kx <= 32 && ky <= 16 && n >= 64) {
+    const int64_t tiles = (n + 7) / 8;
+    int64_t blocks = (tiles + 7) / 8;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    const int grid = (int)(blocks < 1 ? 1 : blocks);
+    cudaStream_t st = as_stream(stream);
+    const int ks = (kx + 3) / 4;
+#define DLRSN_ROWMIX_MMA(KS, NT) \
+  rowmix_mma_kernel<KS, NT><<<grid, 256, 0, st>>>((int)n, kx, ky, X, ldx, K, ldk, beta, Y, ldy)
+    if (ky <= 8) {
+      if (ks <= 1) DLRSN_ROWMIX_MMA(1, 1);
+      else if (ks <= 2) DLRSN_ROWMIX_MMA(2, 1);
+      else if (ks <= 4) DLRSN_ROWMIX_MMA(4, 1);
+      else DLRSN_ROWMIX_MMA(8, 1);
+    } else {
+      if (ks <= 1) DLRSN_ROWMIX_MMA(1, 2);
+      else if (ks <= 2) DLRSN_ROWMIX_MMA(2, 2);
+      else if (ks <= 4) DLRSN_ROWMIX_MMA(4, 2);
+      else DLRSN_ROWMIX_MMA(8, 2);
+    }
+#undef DLRSN_ROWMIX_MMA
+    DLRSN_CHECK_LAUNCH("rowmix_mma_kernel");
+    return DLRSN_OK;
+  }
   const bool aligned = ((reinterpret_cast<uintptr_t>(X) | (uintptr_t)ldx * 8) & 15) == 0;
   if (aligned && (kx == 8 || kx == 16 || kx == 32) && kRB % ky == 0) {
     const int grid = grid_for(n * ky);
@@ -943,11 +1356,11 @@ int dlrsn_mgram(const dlrsn_cellops* ops, int ra, int rb, const double* A, int l
   const int cpb = cells_per_block(ncell, tiles);
   const int nblk = (ncell + cpb - 1) / cpb;
   cudaStream_t st = as_stream(stream);
-  mgram_kernel<<<dim3(nblk, tiles), kTile * kTile, 0, st>>>(ncell, ra, rb, A, lda, B, ldb, coeff,
+  mgram_mma_kernel<<<dim3(nblk, tiles), kTile * kTile, 0, st>>>(ncell, ra, rb, A, lda, B, ldb, coeff,
                                                             *ops, cpb, partial);
-  DLRSN_CHECK_LAUNCH("mgram_kernel");
+  DLRSN_CHECK_LAUNCH("mgram_mma_kernel");
   const int64_t len = (int64_t)ra * rb;
-  reduce_partials_kernel<<<(unsigned)((len + 31) / 32), 256, 0, st>>>(nblk, len, partial, G, 1.0);
+  reduce_partials_kernel<<<(unsigned)((len + 31) / 32), 1024, 0, st>>>(nblk, len, partial, G, 1.0);
   DLRSN_CHECK_LAUNCH("reduce_partials_kernel");
   return DLRSN_OK;
 }
@@ -969,7 +1382,7 @@ int dlrsn_project(const dlrsn_cellops* ops, int r, const double* X, const double
   project_kernel<<<dim3(nblk, tiles), kTile * kTile, 0, st>>>(pa, *ops);
   DLRSN_CHECK_LAUNCH("project_kernel");
   const int64_t len = 7 * (int64_t)r * r + r;
-  reduce_partials_kernel<<<(unsigned)((len + 31) / 32), 256, 0, st>>>(nblk, len, partial, out, 1.0);
+  reduce_partials_kernel<<<(unsigned)((len + 31) / 32), 1024, 0, st>>>(nblk, len, partial, out, 1.0);
   DLRSN_CHECK_LAUNCH("reduce_partials_kernel");
   return DLRSN_OK;
 }
@@ -978,9 +1391,41 @@ int dlrsn_chol_upper(int r, const double* G, double* R, double* Rinv, double* di
                      int* flag, dlrsn_stream_t stream) {
   const size_t smem = 2 * (size_t)r * r * sizeof(double);
   DLRSN_REQUIRE(smem <= 200 * 1024, "rank %d too large for chol_upper", r);
+  if (r <= 32) {
+    if (r <= 16)
+      chol_upper_warp_kernel<16><<<1, 32, 0, as_stream(stream)>>>(r, G, R, Rinv, diag_ratio, flag);
+    else
+      chol_upper_warp_kernel<32><<<1, 32, 0, as_stream(stream)>>>(r, G, R, Rinv, diag_ratio, flag);
+    DLRSN_CHECK_LAUNCH("chol_upper_warp_kernel");
+    return DLRSN_OK;
+  }
   DLRSN_TRY_CUDA(cudaFuncSetAttribute(chol_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   chol_upper_kernel<<<1, 256, smem, as_stream(stream)>>>(r, G, R, Rinv, diag_ratio, flag);
   DLRSN_CHECK_LAUNCH("chol_upper_kernel");
+  return DLRSN_OK;
+}
+
+int64_t dlrsn_cholqr2_small_smem(int n, int m) {
+  return ((int64_t)n * (m | 1) + 3 * (int64_t)m * m + m + n) * (int64_t)sizeof(double);
+}
+
+int dlrsn_cholqr2_small(int n, int m, const double* W, int ldw, const double* w, double* Q,
+                        int ldq, double* R, double* ratio, int* flag, int* deficient,
+                        dlrsn_stream_t stream) {
+  const int64_t smem = dlrsn_cholqr2_small_smem(n, m);
+  DLRSN_REQUIRE(m >= 1 && m <= 32 && smem <= 200 * 1024,
+                "cholqr2_small: %d x %d does not fit one CTA", n, m);
+  cudaStream_t st = as_stream(stream);
+  if (m <= 16) {
+    DLRSN_TRY_CUDA(cudaFuncSetAttribute(cholqr2_small_kernel<16>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cholqr2_small_kernel<16><<<1, 256, smem, st>>>(n, m, W, ldw, w, Q, ldq, R, ratio, flag, deficient);
+  } else {
+    DLRSN_TRY_CUDA(cudaFuncSetAttribute(cholqr2_small_kernel<32>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cholqr2_small_kernel<32><<<1, 256, smem, st>>>(n, m, W, ldw, w, Q, ldq, R, ratio, flag, deficient);
+  }
+  DLRSN_CHECK_LAUNCH("cholqr2_small_kernel");
   return DLRSN_OK;
 }
 
@@ -1016,13 +1461,13 @@ int dlrsn_row_combine(int n, int r, const double* Binv, const double* ms, const 
 int dlrsn_deim(int n, int r, double* Wwork, const double* W, int* idx, double* Lhat, double* U,
                int* err_col, dlrsn_stream_t stream) {
   DLRSN_REQUIRE(r <= n, "rank %d exceeds the %d available nodes", r, n);
-  const size_t smem = (size_t)n * r * sizeof(double);
+  const size_t smem = (size_t)n * r * sizeof(double) + (size_t)n;
   const int in_smem = smem <= 200 * 1024;
   if (in_smem)
     DLRSN_TRY_CUDA(cudaFuncSetAttribute(deim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
-  deim_kernel<<<1, 1024, in_smem ? smem : 0, as_stream(stream)>>>(n, r, Wwork, W, idx, Lhat, U,
-                                                                  err_col, in_smem);
+  deim_kernel<<<1, 256, in_smem ? smem : 0, as_stream(stream)>>>(n, r, Wwork, W, idx, Lhat, U,
+                                                                 err_col, in_smem);
   DLRSN_CHECK_LAUNCH("deim_kernel");
   return DLRSN_OK;
 }
@@ -1033,7 +1478,7 @@ int dlrsn_what_solve(int r, int m, const double* Lhat, const double* U, const do
   DLRSN_REQUIRE(smem <= 200 * 1024, "W_hat solve too large for shared memory");
   DLRSN_TRY_CUDA(cudaFuncSetAttribute(what_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
-  what_solve_kernel<<<1, 512, smem, as_stream(stream)>>>(r, m, Lhat, U, V, X, mode);
+  what_solve_kernel<<<1, 128, smem, as_stream(stream)>>>(r, m, Lhat, U, V, X, mode);
   DLRSN_CHECK_LAUNCH("what_solve_kernel");
   return DLRSN_OK;
 }

@@ -79,17 +79,19 @@ __global__ void update_temperature_kernel(int n, const double* __restrict__ phi,
 }
 
 __global__ void advance_kernel(int n, const double* __restrict__ phi, double* __restrict__ T,
-                               double* __restrict__ sa, const double* __restrict__ sa0,
+                               const double* sa_in, const double* den_in, double* sa,
+                               const double* __restrict__ sa0,
                                double power, const double* __restrict__ rc, double dt, double c,
                                double a_r, double t_floor, const double* __restrict__ ssp,
                                const double* __restrict__ qe, double* __restrict__ st,
                                double* __restrict__ ss, double* __restrict__ q,
-                               double* __restrict__ den, int* status) {
+                               double* den, double* __restrict__ T0_out, int* status) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   // finish the step that produced phi (uses that step's sigma_a / denom)
-  const double Tn = new_temperature(cell_mean4(phi, i), T[i], sa[i], den[i], dt, c, a_r, t_floor);
+  const double Tn = new_temperature(cell_mean4(phi, i), T[i], sa_in[i], den_in[i], dt, c, a_r, t_floor);
   T[i] = Tn;
+  if (T0_out) T0_out[i] = Tn;
   // linearise the next step about the new temperature
   const double s_a = power != 0.0 ? sa0[i] * pow(Tn, power) : sa0[i];
   sa[i] = s_a;
@@ -144,17 +146,18 @@ int dlrsn_update_temperature(int n, const double* phi, int phi_per_dof, const do
   return DLRSN_OK;
 }
 
-int dlrsn_advance_relinearize(int n, const double* phi_dofs, double* T, double* sigma_a,
+int dlrsn_advance_relinearize(int n, const double* phi_dofs, double* T,
+                              const double* sigma_a_in, const double* denom_in, double* sigma_a,
                               const double* sigma_a0, double opacity_power, const double* rho_cv,
                               double dt, double c, double a_r, double t_floor,
                               const double* ss_phys, const double* q_ext, double* sigma_t,
-                              double* sigma_s, double* q, double* denom, int* status,
-                              dlrsn_stream_t stream) {
+                              double* sigma_s, double* q, double* denom, double* T0_out,
+                              int* status, dlrsn_stream_t stream) {
   DLRSN_REQUIRE(dt > 0.0, "time step must be positive, got %g", dt);
   if (n == 0) return DLRSN_OK;
   advance_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(
-      n, phi_dofs, T, sigma_a, sigma_a0, opacity_power, rho_cv, dt, c, a_r, t_floor, ss_phys,
-      q_ext, sigma_t, sigma_s, q, denom, status);
+      n, phi_dofs, T, sigma_a_in, denom_in, sigma_a, sigma_a0, opacity_power, rho_cv, dt, c, a_r,
+      t_floor, ss_phys, q_ext, sigma_t, sigma_s, q, denom, T0_out, status);
   DLRSN_CHECK_LAUNCH("advance_kernel");
   return DLRSN_OK;
 }

@@ -141,6 +141,69 @@ __global__ void finish_kernel(int r, const double* __restrict__ R, const double*
   for (int j = threadIdx.x; j < r; j += blockDim.x) beta_new[j] = wg[r * r + j];
 }
 
+// Step start in one launch: zero the control words (flags, statuses, the
+// combine's block counter, the iteration control) and write the completion
+// exponents (spatial_monomials / angular_monomials, angular.py:198-214) and
+// the domain extent used by the CGS2 completion candidates.
+struct InitArgs {
+  int* flags;
+  int* statw;
+  int* statx;
+  void* red_ws;
+  SiCtl* ctl;
+  int* sexp;
+  int* aexp;
+  double* extent;
+  int count;  // r + 8 candidates
+  double x0, y0, lx, ly;
+};
+
+__global__ void init_kernel(InitArgs a) {
+  const int t = threadIdx.x;
+  if (t < 8) a.flags[t] = 0;
+  if (t < 64) reinterpret_cast<unsigned*>(a.red_ws)[t] = 0u;
+  if (t == 0) {
+    *a.statw = 0;
+    *a.statx = 0;
+    memset(a.ctl, 0, sizeof(SiCtl));
+    a.extent[0] = a.x0;
+    a.extent[1] = a.y0;
+    a.extent[2] = a.lx;
+    a.extent[3] = a.ly;
+  } else if (t == 32) {
+    int cnt = 0;
+    for (int deg = 0; cnt < a.count; ++deg)
+      for (int x = deg; x >= 0 && cnt < a.count; --x, ++cnt) {
+        a.sexp[2 * cnt] = x;
+        a.sexp[2 * cnt + 1] = deg - x;
+      }
+  } else if (t == 64) {
+    int cnt = 1;
+    a.aexp[0] = a.aexp[1] = a.aexp[2] = 0;
+    for (int deg = 1; cnt < a.count; ++deg)
+      for (int kx = deg; kx >= 0 && cnt < a.count; --kx)
+        for (int ky = deg - kx; ky >= 0 && cnt < a.count; --ky, ++cnt) {
+          a.aexp[3 * cnt] = kx;
+          a.aexp[3 * cnt + 1] = ky;
+          a.aexp[3 * cnt + 2] = deg - kx - ky;
+        }
+  }
+}
+
+// Readback packing: copy scattered device words into one staging block so
+// that a single device-to-host copy carries every status of the step.
+struct PackList {
+  const unsigned* src[24];
+  int words[24];
+  int off[24];
+  int n;
+};
+
+__global__ void pack_kernel(PackList l, unsigned* __restrict__ dst) {
+  for (int k = 0; k < l.n; ++k)
+    for (int w = threadIdx.x; w < l.words[k]; w += blockDim.x) dst[l.off[k] + w] = l.src[k][w];
+}
+
 // ---- workspace arena ---------------------------------------------------------
 struct Arena {
   char* base;
@@ -175,6 +238,9 @@ struct StepBufs {
   int64_t* place;
   dlrsn_group* groups;
   SiCtl* ctl;
+  unsigned* rbdev;
+  double* ratiow;
+  int* cholw;
   Upload* up;
 };
 
@@ -240,6 +306,9 @@ static size_t carve(Arena& ar, StepBufs& b, int nx, int ny, int r, int no, int w
   b.place = ar.take<int64_t>(r);
   b.groups = ar.take<dlrsn_group>(r);
   b.ctl = ar.take<SiCtl>(1);
+  b.rbdev = ar.take<unsigned>(8192);
+  b.ratiow = ar.take<double>(2 * r);
+  b.cholw = ar.take<int>(2);
   b.up = ar.take<Upload>(1);
   return ar.off;
 }
@@ -270,23 +339,33 @@ struct Readback {
   struct Item { const void* dev; size_t bytes; void* host; };
   std::vector<Item> items;
   void add(const void* dev, size_t bytes, void* host) { items.push_back({dev, bytes, host}); }
-  int run(cudaStream_t st) {
-    size_t total = 0;
-    for (auto& it : items) total += (it.bytes + 15) & ~size_t(15);
+  // one pack kernel + one device-to-host copy + one synchronisation
+  int run(cudaStream_t st, unsigned* staging) {
+    PackList l;
+    l.n = 0;
+    int off = 0;
+    for (auto& it : items) {
+      if (l.n == 24) {
+        set_error("internal: too many readback items");
+        return DLRSN_ECUDA;
+      }
+      l.src[l.n] = static_cast<const unsigned*>(it.dev);
+      l.words[l.n] = (int)((it.bytes + 3) / 4);
+      l.off[l.n] = off;
+      off += (l.words[l.n] + 1) & ~1;  // keep doubles 8-byte aligned
+      ++l.n;
+    }
+    if (off > 8192) {
+      set_error("internal: readback larger than its staging block");
+      return DLRSN_ECUDA;
+    }
     char* h = nullptr;
-    DLRSN_RET(pinned(total + sizeof(Upload) + 64, &h));
-    h += ((sizeof(Upload) + 63) / 64) * 64;  // keep clear of the upload region
-    size_t off = 0;
-    for (auto& it : items) {
-      DLRSN_TRY_CUDA(cudaMemcpyAsync(h + off, it.dev, it.bytes, cudaMemcpyDeviceToHost, st));
-      off += (it.bytes + 15) & ~size_t(15);
-    }
+    DLRSN_RET(pinned((size_t)off * 4 + 64, &h));
+    pack_kernel<<<1, 256, 0, st>>>(l, staging);
+    DLRSN_CHECK_LAUNCH("pack_kernel");
+    DLRSN_TRY_CUDA(cudaMemcpyAsync(h, staging, (size_t)off * 4, cudaMemcpyDeviceToHost, st));
     DLRSN_TRY_CUDA(cudaStreamSynchronize(st));
-    off = 0;
-    for (auto& it : items) {
-      memcpy(it.host, h + off, it.bytes);
-      off += (it.bytes + 15) & ~size_t(15);
-    }
+    for (int k = 0; k < l.n; ++k) memcpy(items[k].host, h + (size_t)l.off[k] * 4, items[k].bytes);
     items.clear();
     return DLRSN_OK;
   }
@@ -309,44 +388,49 @@ __global__ void plan_kernel(int r, int no, int world, int rank, const int* __res
                             dlrsn_group* __restrict__ groups, int* __restrict__ quads,
                             int* __restrict__ mine, int64_t* __restrict__ place, int64_t n_dofs,
                             int width) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  // thread d = selected direction d (r <= 128); every rank / position is a
+  // count over the r directions (O(r) per thread)
+  __shared__ int sq[DLRSN_MAX_RANK], sown[DLRSN_MAX_RANK];
+  const int d = threadIdx.x;
   const bool bad = err[0] >= 0;
-  int owner[DLRSN_MAX_RANK], pos[DLRSN_MAX_RANK], q[DLRSN_MAX_RANK];
-  for (int d = 0; d < r; ++d) {
-    int v = bad ? d : idx_raw[d];
+  int v = d;
+  if (d < r) {
+    v = bad ? d : idx_raw[d];
     if (v < 0 || v >= no) v = d;
     idx[d] = v;
-    q[d] = quad_code(omegas + 3 * (int64_t)v);
+    sq[d] = quad_code(omegas + 3 * (int64_t)v);
   }
-  int nxt = 0;
-  for (int qd = 0; qd < 4; ++qd)
-    for (int d = 0; d < r; ++d)
-      if (q[d] == qd) owner[d] = (nxt++) % world;
-  int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  int nl = 0;
-  for (int d = 0; d < r; ++d) {
-    const int o = owner[d];
-    pos[d] = o < 8 ? cnt[o]++ : 0;
-    place[d] = (int64_t)o * n_dofs * width + pos[d];
-    if (o == rank) mine[nl++] = d;
+  __syncthreads();
+  int owner = 0;
+  if (d < r) {
+    int before = 0;  // position in quadrant-major order (partition_directions)
+    for (int e = 0; e < r; ++e) before += (sq[e] < sq[d]) || (sq[e] == sq[d] && e < d);
+    owner = before % world;
+    sown[d] = owner;
   }
-  int G = 0;
-  for (int qd = 0; qd < 4; ++qd)
-    for (int k = 0; k < nl; ++k) {
-      const int d = mine[k];
-      if (q[d] != qd) continue;
-      const double* om = omegas + 3 * (int64_t)idx[d];
+  __syncthreads();
+  if (d < r) {
+    int pos = 0;
+    for (int e = 0; e < d; ++e) pos += sown[e] == owner;
+    place[d] = (int64_t)owner * n_dofs * width + pos;
+    if (owner == rank) {
+      mine[pos] = d;
+      quads[pos] = sq[d];
+      int gi = 0;  // this rank's groups in quadrant order (transport.plan_groups)
+      for (int e = 0; e < r; ++e)
+        gi += sown[e] == rank && ((sq[e] < sq[d]) || (sq[e] == sq[d] && e < d));
+      const double* om = omegas + 3 * (int64_t)v;
       dlrsn_group g;
       memset(&g, 0, sizeof(g));
-      g.quad = qd;
+      g.quad = sq[d];
       g.ndir = 1;
-      g.slot[0] = k;
+      g.slot[0] = pos;
       g.ox[0] = fabs(om[0]);
       g.oy[0] = fabs(om[1]);
       g.cw[0] = closure[d];
-      groups[G++] = g;
+      groups[gi] = g;
     }
-  for (int k = 0; k < nl; ++k) quads[k] = q[mine[k]];
+  }
 }
 
 // dst (n x nl) = src[:, mine] (src n x r): this rank's psi_time columns
@@ -436,38 +520,28 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
   Readback rb;
   const int nl = (r - rank_id + world - 1) / world;  // this rank's directions
   const int G = nl;                                  // single-direction groups
+  // full-rank fast path of the angular update: one-CTA weighted CholQR2
+  const bool ang_fast = r <= 32 && dlrsn_cholqr2_small_smem(no, r) <= 200 * 1024;
 
-  // ---- 0. constants (completion exponents, extent) ---------------------------
-  char* hpin = nullptr;
-  DLRSN_RET(pinned(sizeof(Upload) + 4096, &hpin));
-  Upload* hu = reinterpret_cast<Upload*>(hpin);
+  // ---- 0. control words and constants: one launch ------------------------------
   {
-    int cnt = 0;
-    for (int deg = 0; cnt < r + 8; ++deg)
-      for (int a = deg; a >= 0 && cnt < r + 8; --a, ++cnt) {
-        hu->sexp[2 * cnt] = a;
-        hu->sexp[2 * cnt + 1] = deg - a;
-      }
-    cnt = 1;  // angular_monomials (angular.py:198-214): 1, then rising degree
-    hu->aexp[0] = hu->aexp[1] = hu->aexp[2] = 0;
-    for (int deg = 1; cnt < r + 8; ++deg)
-      for (int kx = deg; kx >= 0 && cnt < r + 8; --kx)
-        for (int ky = deg - kx; ky >= 0 && cnt < r + 8; --ky, ++cnt) {
-          hu->aexp[3 * cnt] = kx;
-          hu->aexp[3 * cnt + 1] = ky;
-          hu->aexp[3 * cnt + 2] = deg - kx - ky;
-        }
-    hu->extent[0] = ops->x0;
-    hu->extent[1] = ops->y0;
-    hu->extent[2] = ops->nx * ops->dx;
-    hu->extent[3] = ops->ny * ops->dy;
+    InitArgs ia;
+    ia.flags = b.flags;
+    ia.statw = b.statw;
+    ia.statx = b.statx;
+    ia.red_ws = b.red_ws;
+    ia.ctl = b.ctl;
+    ia.sexp = b.up->sexp;
+    ia.aexp = b.up->aexp;
+    ia.extent = b.up->extent;
+    ia.count = r + 8;
+    ia.x0 = ops->x0;
+    ia.y0 = ops->y0;
+    ia.lx = ops->nx * ops->dx;
+    ia.ly = ops->ny * ops->dy;
+    init_kernel<<<1, 96, 0, st>>>(ia);
+    DLRSN_CHECK_LAUNCH("init_kernel");
   }
-  DLRSN_TRY_CUDA(cudaMemcpyAsync(b.up, hu, sizeof(Upload), cudaMemcpyHostToDevice, st));
-  DLRSN_TRY_CUDA(cudaMemsetAsync(b.flags, 0, 8 * sizeof(int), st));
-  DLRSN_TRY_CUDA(cudaMemsetAsync(b.red_ws, 0, 256, st));  // combine's block counter
-  DLRSN_TRY_CUDA(cudaMemsetAsync(b.statw, 0, sizeof(int), st));
-  DLRSN_TRY_CUDA(cudaMemsetAsync(b.statx, 0, sizeof(int), st));
-  DLRSN_TRY_CUDA(cudaMemsetAsync(b.ctl, 0, sizeof(SiCtl), st));
 
   // ---- 1. DEIM, closure weights, input checks (reported at the readback) ----
   DLRSN_RET(dlrsn_deim(no, r, b.Wk, W, b.err_idx + 1, b.Lhat, b.U, b.err_idx, s));
@@ -481,7 +555,7 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     DLRSN_CHECK_LAUNCH("ortho_residual_kernel");
   }
   const int width = world > 1 ? comm->gather_width : 1;
-  plan_kernel<<<1, 32, 0, st>>>(r, no, world, rank_id, b.err_idx, b.err_idx + 1, p->omegas_dev,
+  plan_kernel<<<1, DLRSN_MAX_RANK, 0, st>>>(r, no, world, rank_id, b.err_idx, b.err_idx + 1, p->omegas_dev,
                                 b.closure, b.idx, b.groups, b.quads, b.mine, b.place, N, width);
   DLRSN_CHECK_LAUNCH("plan_kernel");
 
@@ -562,7 +636,13 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     }
 
     // ---- 4. Galerkin side (dlr_sn.py:123-150): speculative CholQR2 ----------
-    for (int exact = p->gs_method == 1 ? 1 : 0; exact <= 1; ++exact) {
+    int exact = p->gs_method == 1 ? 1 : 0;
+    int exact_w = ang_fast ? 0 : 1;
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      if (attempt > 0) {
+        DLRSN_TRY_CUDA(cudaMemsetAsync(b.statw, 0, sizeof(int), st));
+        DLRSN_TRY_CUDA(cudaMemsetAsync(b.statx, 0, sizeof(int), st));
+      }
       if (!exact) {
         DLRSN_RET(dlrsn_mgram(ops, r, r, b.psi, r, b.psi, r, nullptr, b.G, b.part, s));
         DLRSN_RET(dlrsn_chol_upper(r, b.G, b.R1, b.R1inv, b.ratio, b.cholflag, s));
@@ -584,8 +664,13 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
                                   b.lbar, b.rowstat + r, s));
       DLRSN_RET(dlrsn_what_solve(r, r, b.Lhat, b.U, b.L, b.gamma, 0, s));
       DLRSN_RET(dlrsn_rowmix(no, r, r, W, r, b.gamma, r, 0.0, b.lfull, r, s));
-      DLRSN_RET(dlrsn_cgs2(no, r, b.lfull, r, W_new, r, b.Rang, b.defw, 0, p->weights_dev,
-                           nullptr, 0, r + 8, b.up->aexp, p->omegas_dev, b.cgsws, b.statw, 1, s));
+      if (!exact_w)
+        DLRSN_RET(dlrsn_cholqr2_small(no, r, b.lfull, r, p->weights_dev, W_new, r, b.Rang,
+                                      b.ratiow, b.cholw, b.defw, s));
+      else
+        DLRSN_RET(dlrsn_cgs2(no, r, b.lfull, r, W_new, r, b.Rang, b.defw, 0, p->weights_dev,
+                             nullptr, 0, r + 8, b.up->aexp, p->omegas_dev, b.cgsws, b.statw, 1,
+                             s));
       DLRSN_RET(wgram(no, r, W_new, p->weights_dev, b.wpart, b.wg, st));
       finish_kernel<<<1, 256, 0, st>>>(r, b.Rang, b.wg, S_new, beta_new);
       DLRSN_CHECK_LAUNCH("finish_kernel");
@@ -624,8 +709,14 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
         rb.add(b.defx, r * sizeof(int), defx.data());
         rb.add(b.statx, sizeof(int), &statx);
       }
+      std::vector<double> ratiow(2 * r);
+      int cholw[2] = {0, 0};
+      if (!exact_w) {
+        rb.add(b.ratiow, 2 * r * sizeof(double), ratiow.data());
+        rb.add(b.cholw, sizeof(cholw), cholw);
+      }
       if (p->check_state) rb.add(b.chk_out, sizeof(chko), chko);
-      DLRSN_RET(rb.run(st));
+      DLRSN_RET(rb.run(st, b.rbdev));
 
       if (!pre_checked) {  // errors of the reference's order (dlr_sn.py:99-109)
         pre_checked = true;
@@ -667,7 +758,8 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
         bool ok = cholflag[0] == 0;
         for (int k = 0; k < r && ok; ++k) ok = ratio[k] >= 1e-6 && ratio[r + k] >= 1e-10;
         if (!ok) {
-          info->gs_fallback = 1;
+          info->gs_fallback |= 1;
+          exact = 1;
           continue;
         }
         info->spatial_deficiency = 0;
@@ -679,6 +771,15 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
         int nd = 0;
         for (int k = 0; k < r; ++k) nd += defx[k] != 0;
         info->spatial_deficiency = nd;
+      }
+      if (!exact_w) {  // same guard for the angular CholQR2 (angular.py:137 threshold)
+        bool ok = cholw[0] == 0 && cholw[1] == 0;
+        for (int k = 0; k < r && ok; ++k) ok = ratiow[k] >= 1e-6 && ratiow[r + k] >= 1e-10;
+        if (!ok) {
+          info->gs_fallback |= 2;
+          exact_w = 1;
+          continue;
+        }
       }
       for (int d = 0; d < r; ++d)
         if (rowstat[d]) {

@@ -22,6 +22,10 @@
 
 namespace dlrsn {
 
+__device__ __forceinline__ double ld_volatile_shared_f64(const double* p) {
+  return *reinterpret_cast<const volatile double*>(p);
+}
+
 __device__ __forceinline__ unsigned long long ws_timer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -34,11 +38,16 @@ __device__ __forceinline__ unsigned long long ws_timer() {
   } while (0)
 
 constexpr int kWsC = 6;      // skewed steps per chunk (= 2 x producers)
-constexpr int kWsProd = 3;   // producer warps
+constexpr int kWsProd = 3;   // producer warps 1-3; warp 7 polls the strip handoff;
+                             // warps 4-6 stay idle so that the consumer (warp 0)
+                             // has its SM sub-partition to itself
+constexpr int kWsThreads = 256;
+constexpr int kWsStages = 3;  // ring depth (also keeps the CTA alone on its SM)
+constexpr int kWsHRing = 8;   // chunks of strip-handoff values staged in shared memory
 constexpr int kWsPairs = 10; // z (2 pairs), Kx (4 pairs), Ky (4 pairs)
 constexpr int kWsInD = kWsC * (32 + 128 + 128);  // sigma | scat | rhs doubles per stage
 constexpr int kWsFacD = kWsC * kWsPairs * 64;    // factor doubles per stage
-constexpr size_t kWsSmem = (2 * (size_t)kWsInD + 2 * (size_t)kWsFacD) * sizeof(double);
+constexpr size_t kWsSmem = (kWsStages * (size_t)kWsInD + kWsStages * (size_t)kWsFacD) * sizeof(double);
 
 __device__ __forceinline__ void named_bar_producers() {
   asm volatile("bar.sync 1, %0;" ::"r"(kWsProd * 32) : "memory");
@@ -103,14 +112,17 @@ __device__ __forceinline__ void ws_factor_step(const SweepArgs& a, const double*
   }
 }
 
-__global__ void __launch_bounds__(128) sweep_ws_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__(kWsThreads) sweep_ws_kernel(const SweepArgs a) {
   if (a.skip && *a.skip) return;  // iteration past convergence
   extern __shared__ __align__(128) double sm[];
   double* in_ring = sm;                 // 2 x kWsInD
-  double* fac_ring = sm + 2 * kWsInD;   // 2 x kWsFacD
-  __shared__ __align__(8) uint64_t in_full[2], fac_full[2], fac_empty[2];
+  double* fac_ring = sm + kWsStages * kWsInD;   // kWsStages x kWsFacD
+  __shared__ __align__(8) uint64_t in_full[kWsStages], fac_full[kWsStages], fac_empty[kWsStages];
   __shared__ double s_S[16];
   __shared__ int s_item;
+  // inflow from the strip below, staged by the poller warp (warp 7):
+  // slot (m % kWsHRing) holds chunk m's kWsC values; kEmpty marks a free slot
+  __shared__ __align__(16) double2 s_hin[kWsHRing * kWsC];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nx = a.nx, ny = a.ny, G = a.G;
@@ -122,7 +134,7 @@ __global__ void __launch_bounds__(128) sweep_ws_kernel(const SweepArgs a) {
   const double empty = __longlong_as_double((long long)kEmpty);
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kWsStages; ++i) {
       mbar_init(&in_full[i], 1);
       mbar_init(&fac_full[i], 1);
       mbar_init(&fac_empty[i], 1);
@@ -131,7 +143,7 @@ __global__ void __launch_bounds__(128) sweep_ws_kernel(const SweepArgs a) {
   }
   __syncthreads();
   // per-stage use counters (identical in every thread that tracks them)
-  uint32_t uses[2] = {0, 0};
+  uint32_t uses[kWsStages] = {};
 
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(a.ticket, 1);
@@ -147,6 +159,9 @@ __global__ void __launch_bounds__(128) sweep_ws_kernel(const SweepArgs a) {
     const double ox = grp->ox[0], oy = grp->oy[0], cw = grp->cw[0];
     if (threadIdx.x < 16) s_S[threadIdx.x] = ox * a.gxp[threadIdx.x] + oy * a.gyp[threadIdx.x];
     __syncthreads();
+    for (int e = threadIdx.x; e < kWsHRing * kWsC; e += blockDim.x)
+      s_hin[e] = make_double2(empty, empty);
+    __syncthreads();
     const int64_t strip_vec = (int64_t)s * T * 128;
     const double* sig = a.sigma_sk4 + (int64_t)quad * a.slen + (int64_t)s * T * 32;
     const double* scat = a.scat_sk4 ? a.scat_sk4 + (int64_t)quad * a.vlen + strip_vec : nullptr;
@@ -154,7 +169,7 @@ __global__ void __launch_bounds__(128) sweep_ws_kernel(const SweepArgs a) {
     const bool row_ok = (s << 5) + lane < ny;
 
     auto issue = [&](int m) {  // thread 32 only
-      const int st = m & 1, t0 = m * kWsC;
+      const int st = m % kWsStages, t0 = m * kWsC;
       const uint32_t n = (uint32_t)min(kWsC, T - t0);
       double* buf = in_ring + st * kWsInD;
       fence_proxy_async_smem();
@@ -164,15 +179,69 @@ __global__ void __launch_bounds__(128) sweep_ws_kernel(const SweepArgs a) {
       tma_load_1d(buf + kWsC * 160, rhs + t0 * 128, n * 1024u, &in_full[st]);
     };
 
-    if (warp > 0) {
+    if (warp == 7) {
+      // ------------------------------ handoff poller -----------------------
+      // Polls the L2 handoff column of the strip below for the next chunks
+      // (kWsHRing - 1 chunks of lookahead, one L2 round trip per sweep of
+      // polls) and stages arrived values in s_hin, so the consumer never
+      // waits on an L2 round trip itself.  It re-arms the L2 slots it read.
+      if (s > 0) {
+        double2* hin = reinterpret_cast<double2*>(a.handoff) + ((int64_t)(s - 1) * G + g) * nx;
+        // lane -> (chunk offset, position): kWsC positions x 5 chunks in flight
+        const int off = lane / kWsC, pos = lane - off * kWsC;
+        const bool poll_lane = off < 5;
+        int base = 0;  // oldest chunk not yet staged
+        double2 v = make_double2(empty, empty);
+        int vm = -1;  // chunk the pending value belongs to
+        long long spins = 0;
+        while (base < hchunks) {
+          const int m = base + off;
+          const int col = m * kWsC + pos;
+          const bool want = poll_lane && m < hchunks && col < nx;
+          if (want && m != vm) {
+            v = make_double2(empty, empty);
+            vm = m;
+          }
+          if (want && (is_empty(v.x) || is_empty(v.y))) v = __ldcv(hin + col);
+          // stage chunk `base` once all its values arrived and its slot is free
+          const bool mine = want && off == 0;
+          const bool ready = !mine || (!is_empty(v.x) && !is_empty(v.y));
+          double2* slot = s_hin + (base % kWsHRing) * kWsC + pos;
+          const bool slot_free = !mine || is_empty(ld_volatile_shared_f64(&slot->x));
+          if (__all_sync(kFull, ready && slot_free)) {
+            if (mine) {
+              *reinterpret_cast<volatile double*>(&slot->y) = v.y;
+              __threadfence_block();
+              *reinterpret_cast<volatile double*>(&slot->x) = v.x;
+              __stcg(hin + col, make_double2(empty, empty));  // re-arm for the next sweep
+            }
+            // shift the in-flight values down one chunk
+            const double vx = __shfl_down_sync(kFull, v.x, kWsC);
+            const double vy = __shfl_down_sync(kFull, v.y, kWsC);
+            const int vmn = __shfl_down_sync(kFull, vm, kWsC);
+            v = off < 4 ? make_double2(vx, vy) : make_double2(empty, empty);
+            vm = off < 4 ? vmn : -1;
+            ++base;
+            spins = 0;
+          } else {
+            __nanosleep(20);
+            if (++spins > (1ll << 28)) {  // upstream never arrived: flag and unblock
+              if (lane == 0) atomicOr(a.status, 2);
+              break;
+            }
+          }
+        }
+      }
+    } else if (warp >= 4) {
+      // idle
+    } else if (warp > 0) {
       // ------------------------------ producers ----------------------------
       const int pw = warp - 1;
       if (threadIdx.x == 32) {
-        issue(0);
-        if (nchunks > 1) issue(1);
+        for (int m0 = 0; m0 < kWsStages && m0 < nchunks; ++m0) issue(m0);
       }
       for (int m = 0; m < nchunks; ++m) {
-        const int st = m & 1;
+        const int st = m % kWsStages;
         const uint32_t u = uses[st];
         if (warp == 1) WS_TRACE(3);
         mbar_wait_warp(&in_full[st], u & 1u);
@@ -182,15 +251,14 @@ __global__ void __launch_bounds__(128) sweep_ws_kernel(const SweepArgs a) {
         double* fac = fac_ring + st * kWsFacD;
         // kWsC = 2 kWsProd: each producer warp factors steps pw and pw + kWsProd
         // together (inactive lanes compute harmless garbage the consumer skips)
-        const double* bufc = buf;
-        ws_factor_step(a, s_S, bufc, fac, pw, lane, scat != nullptr, ox, oy);
-        ws_factor_step(a, s_S, bufc, fac, pw + kWsProd, lane, scat != nullptr, ox, oy);
+        ws_factor_step(a, s_S, buf, fac, pw, lane, scat != nullptr, ox, oy);
+        ws_factor_step(a, s_S, buf, fac, pw + kWsProd, lane, scat != nullptr, ox, oy);
         if (warp == 1) WS_TRACE(5);
         named_bar_producers();  // stage st fully read (inputs) and written (factors)
         if (warp == 1) WS_TRACE(6);
         if (threadIdx.x == 32) {
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&fac_full[st])) : "memory");
-          if (m + 2 < nchunks) issue(m + 2);
+          if (m + kWsStages < nchunks) issue(m + kWsStages);
         }
         uses[st] = u + 1;
       }
@@ -203,31 +271,37 @@ __global__ void __launch_bounds__(128) sweep_ws_kernel(const SweepArgs a) {
       double2* hout = (s + 1 < ns) ? reinterpret_cast<double2*>(a.handoff) + ((int64_t)s * G + g) * nx
                                    : nullptr;
       const bool hlane = hin != nullptr && lane < kWsC;
-      double2 h0 = make_double2(0.0, 0.0), h1 = h0, h2 = h0;
-      if (hlane && lane < nx) h1 = __ldcg(hin + lane);
-      if (hlane && kWsC + lane < nx) h2 = __ldcg(hin + kWsC + lane);
+      double2 h0 = make_double2(0.0, 0.0);
       double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
       for (int m = 0; m < nchunks; ++m) {
-        const int st = m & 1;
+        const int st = m % kWsStages;
         const uint32_t u = uses[st];
-        h0 = h1;
-        h1 = h2;
         {
           const bool need = hlane && m < hchunks && m * kWsC + lane < nx;
-          double2* hs = hin + (int64_t)m * kWsC + lane;
-          int spins = 0;
-          while (__any_sync(kFull, need && (is_empty(h0.x) || is_empty(h0.y)))) {
-            __nanosleep(32);
-            if (need && (is_empty(h0.x) || is_empty(h0.y))) h0 = __ldcv(hs);
-            if (++spins > (1 << 26)) {
-              if (need) atomicOr(a.status, 2);
-              h0 = make_double2(0.0, 0.0);
+          double2* hs = s_hin + (m % kWsHRing) * kWsC + lane;
+          h0 = make_double2(0.0, 0.0);
+          long long spins = 0;
+          bool got = !need;
+          while (!__all_sync(kFull, got)) {
+            if (!got) {
+              const double hx = ld_volatile_shared_f64(&hs->x);
+              const double hy = ld_volatile_shared_f64(&hs->y);
+              if (!is_empty(hx) && !is_empty(hy)) {
+                h0 = make_double2(hx, hy);
+                got = true;
+              }
+            }
+            if (++spins > (1ll << 30)) {
+              if (need && !got) atomicOr(a.status, 2);
+              got = true;
             }
           }
-          if (need) __stcg(hs, make_double2(empty, empty));
+          if (need) {  // free the slot: y first, x last (the poller tests x)
+            *reinterpret_cast<volatile double*>(&hs->y) = empty;
+            __threadfence_block();
+            *reinterpret_cast<volatile double*>(&hs->x) = empty;
+          }
         }
-        if (hlane && m + 2 < hchunks && (m + 2) * kWsC + lane < nx)
-          h2 = __ldcg(hin + (int64_t)(m + 2) * kWsC + lane);
         WS_TRACE(0);
         mbar_wait_warp(&fac_full[st], u & 1u);
         WS_TRACE(1);
@@ -302,14 +376,15 @@ int launch_sweep_ws(const SweepArgs& a, int max_ctas, cudaStream_t st) {
   DLRSN_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   DLRSN_TRY_CUDA(cudaFuncSetAttribute(sweep_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)kWsSmem));
-  DLRSN_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_ws_kernel, 128, kWsSmem));
+  DLRSN_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_ws_kernel, kWsThreads,
+                                                               kWsSmem));
   const int items = ((a.ny + 31) >> 5) * a.G;
   int ctas = items;
   const int cap = sms * (occ > 0 ? occ : 1);
   if (ctas > cap) ctas = cap;
   if (max_ctas > 0 && ctas > max_ctas) ctas = max_ctas;
   if (ctas < 1) ctas = 1;
-  sweep_ws_kernel<<<ctas, 128, kWsSmem, st>>>(a);
+  sweep_ws_kernel<<<ctas, kWsThreads, kWsSmem, st>>>(a);
   DLRSN_CHECK_LAUNCH("sweep_ws_kernel");
   return DLRSN_OK;
 }

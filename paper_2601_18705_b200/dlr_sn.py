@@ -352,55 +352,101 @@ def _comm_hooks(comm, n, r):
     return h
 
 
+class _NativeCtx:
+    """Per-(grid, quadrature, rank, sharding) state of the native step: the
+    cellops struct, the parameter block, the step and sweep workspaces and
+    the collective hooks, built once and reused by every step."""
+
+    def __init__(self, grid, quad, r, comm):
+        from .transport import _shared_workspace
+
+        lib = _lib.load()
+        self.grid, self.quad, self.comm = grid, quad, comm
+        world = comm.world_size if comm is not None else 1
+        rank = comm.rank if comm is not None else 0
+        self.co = _grid_cellops(grid)
+        self.co_ptr = _addr(self.co)
+        self.ws = _step_workspace(grid, r, quad.n_angles, world, rank)
+        sw_bytes = int(lib.dlrsn_sweep_workspace_bytes(grid.nx, grid.ny, r, 1))
+        self.sws = _shared_workspace(grid, sw_bytes)
+        self.om_host = np.ascontiguousarray(quad.omegas, dtype=np.float64)
+        p = _lib.StepParams()
+        p.rank, p.n_omega = r, quad.n_angles
+        p.omegas_host = self.om_host.ctypes.data
+        p.omegas_dev = quad.omegas_device().data_ptr()
+        p.weights_dev = quad.weights_device().data_ptr()
+        p.sweep_dw = 1
+        self.params = p
+        self.params_ref = ctypes.byref(p)
+        self.hooks = _comm_hooks(comm, grid.n_dofs, r) if world > 1 else None
+        self.comm_ref = ctypes.byref(self.hooks.struct) if self.hooks else None
+        n, no = grid.n_dofs, quad.n_angles
+        # output block: X_new | S_new | W_new | beta_new | phi | si_phi, each
+        # segment padded to an even length (16-byte aligned rows for X)
+        sizes = [n * r, r * r, no * r, r, n, n]
+        offs, o = [], 0
+        for z in sizes:
+            offs.append(o)
+            o += z + (z & 1)
+        self.out_len, self.offs = o, offs
+        self.shapes = [(n, r), (r, r), (no, r), (r,), (n,), (n,)]
+        self.strides = [(r, 1), (r, 1), (r, 1), (1,), (1,), (1,)]
+        self.fn = lib.dlrsn_step_collocation
+
+
+_CTX = {}
+
+
+def _native_ctx(grid, quad, r, comm):
+    key = (id(grid), id(quad), r, id(comm), torch.cuda.current_device())
+    ctx = _CTX.get(key)
+    if ctx is None or ctx.grid is not grid or ctx.quad is not quad or ctx.comm is not comm:
+        if len(_CTX) > 64:
+            _CTX.clear()
+        ctx = _NativeCtx(grid, quad, r, comm)
+        _CTX[key] = ctx
+    return ctx
+
+
 def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_method, sweep_dw,
                  comm):
-    from .transport import _shared_workspace
-
-    lib = _lib.load()
     r = state.rank
     no = quad.n_angles
     n = grid.n_dofs
     for name in ("sigma_t", "sigma_s", "q"):
-        if tuple(getattr(step, name).shape) != (grid.n_cells,):
+        if getattr(step, name).shape[0] != grid.n_cells:
             raise ContractViolation(f"step field {name} must be per-cell")
-    if state.W.values.shape != (no, r) or tuple(state.X.shape) != (n, r):
+    if tuple(state.W.values.shape) != (no, r) or tuple(state.X.shape) != (n, r):
         raise ContractViolation("factor shapes do not match the grid / quadrature")
-    world = comm.world_size if comm is not None else 1
-    rank = comm.rank if comm is not None else 0
-    co = _grid_cellops(grid)
+    ctx = _native_ctx(grid, quad, r, comm if comm is not None and comm.world_size > 1 else None)
     X = state.X.contiguous()
     S = state.S.contiguous()
     W = state.W.values.contiguous()
     beta = state.W.beta if state.W.beta is not None else state.W.bind(quad).beta
     beta = beta.contiguous()
-    X_new, S_new, W_new = empty(n, r), empty(r, r), empty(no, r)
-    beta_new, phi, si_phi = empty(r), empty(n), empty(n)
-    ws = _step_workspace(grid, r, no, world, rank)
-    dw = int(sweep_dw) if sweep_dw else 1
-    sw_bytes = int(lib.dlrsn_sweep_workspace_bytes(grid.nx, grid.ny, r, dw))
-    sws = _shared_workspace(grid, sw_bytes)
-    om_host = quad.omegas if quad.omegas.flags.c_contiguous else np.ascontiguousarray(quad.omegas)
-    p = _lib.StepParams()
-    p.rank, p.n_omega = r, no
-    p.omegas_host = om_host.ctypes.data
-    p.omegas_dev = quad.omegas_device().data_ptr()
-    p.weights_dev = quad.weights_device().data_ptr()
+    out = torch.empty(ctx.out_len, dtype=torch.float64, device=X.device)
+    X_new, S_new, W_new, beta_new, phi, si_phi = (
+        out.as_strided(sh, st, o) for sh, st, o in zip(ctx.shapes, ctx.strides, ctx.offs))
+    p = ctx.params
     p.inv_cdt = float(step.inv_cdt)
     p.si_tol, p.si_max_iters = float(si_tol), int(si_max_iters)
     p.check_state = 1 if check_state else 0
     p.gs_method = 0 if gs_method == "cholqr2" else 1
-    p.sweep_dw = dw
     info = _lib.StepInfo()
-    hooks = _comm_hooks(comm, n, r) if world > 1 else None
-    P = _lib.ptr
-    rc = lib.dlrsn_step_collocation(
-        _addr(co), ctypes.byref(p), P(X), P(S), P(W), P(beta), P(step.sigma_t), P(step.sigma_s),
-        P(step.q), P(X_new), P(S_new), P(W_new), P(beta_new), P(phi), P(si_phi), P(ws), ws.numel(),
-        P(sws), sws.numel(), ctypes.byref(hooks.struct) if hooks else None, ctypes.byref(info),
-        stream())
+    hooks = ctx.hooks
+    if hooks is not None:
+        hooks.error = None
+    ob = out.data_ptr()
+    rc = ctx.fn(
+        ctx.co_ptr, ctx.params_ref, X.data_ptr(), S.data_ptr(), W.data_ptr(), beta.data_ptr(),
+        step.sigma_t.data_ptr(), step.sigma_s.data_ptr(), step.q.data_ptr(),
+        ob + 8 * ctx.offs[0], ob + 8 * ctx.offs[1], ob + 8 * ctx.offs[2], ob + 8 * ctx.offs[3],
+        ob + 8 * ctx.offs[4], ob + 8 * ctx.offs[5], ctx.ws.data_ptr(), ctx.ws.numel(),
+        ctx.sws.data_ptr(), ctx.sws.numel(), ctx.comm_ref, ctypes.byref(info), stream())
     if hooks is not None and hooks.error is not None:
         raise hooks.error
     if rc != 0:
+        lib = _lib.load()
         msg = lib.dlrsn_last_error().decode(errors="replace")
         if rc == -5:
             raise InterpolationError("interpolation residual vanished; basis is rank deficient",
@@ -416,7 +462,7 @@ def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_
     indices = np.frombuffer(info.angle_indices, dtype=np.int64, count=r).copy()
     basis = AngularBasis(values=W_new, beta=beta_new)
     new_state = DlrState(X=X_new, S=S_new, W=basis)
-    out = CollocationStepInfo(
+    res = CollocationStepInfo(
         iterations=int(info.iterations),
         selection=_NativeSelection(indices, W),
         angle_indices=indices.copy(),
@@ -425,5 +471,5 @@ def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_
         angular_deficiency=int(info.angular_deficiency),
         si_phi=si_phi,
     )
-    out.gs_fallback = bool(info.gs_fallback)
-    return new_state, out
+    res.gs_fallback = int(info.gs_fallback)
+    return new_state, res

@@ -75,19 +75,18 @@ class DeviceProblem:
 
             T.copy_(update_temperature(phi_dofs, lin, self.spec.t_floor))
             return lin
-        # the kernel reads this step's sigma_a / denom, then overwrites them
-        sa = lin.sigma_a.clone()
-        den = lin.denom.clone()
-        st, ss, q = (empty(n) for _ in range(3))
-        status = zeros(1, dtype=torch.int32)
+        # one allocation for the next step's coefficients; the kernel reads
+        # this step's sigma_a / denom and writes the new ones out of place
+        buf = empty(6, n)
+        sa, den, st, ss, q, T0 = buf.unbind(0)
         k = self.constants
         _lib.call("dlrsn_advance_relinearize", n, _lib.ptr(as_device(phi_dofs)), _lib.ptr(T),
-                  _lib.ptr(sa), _lib.ptr(self.sigma_a0), self.opacity_power,
-                  _lib.ptr(self.rho_cv), float(self.spec.dt), float(k.c), float(k.a_r),
-                  float(self.spec.t_floor), _lib.ptr(self.ss_phys), _lib.ptr(self.q_ext),
-                  _lib.ptr(st), _lib.ptr(ss), _lib.ptr(q), _lib.ptr(den), _lib.ptr(status),
-                  stream())
-        return LinearizedStep(sigma_t=st, sigma_s=ss, sigma_a=sa, q=q, T0=T.clone(), denom=den,
+                  _lib.ptr(lin.sigma_a), _lib.ptr(lin.denom), _lib.ptr(sa), _lib.ptr(self.sigma_a0),
+                  self.opacity_power, _lib.ptr(self.rho_cv), float(self.spec.dt), float(k.c),
+                  float(k.a_r), float(self.spec.t_floor), _lib.ptr(self.ss_phys),
+                  _lib.ptr(self.q_ext), _lib.ptr(st), _lib.ptr(ss), _lib.ptr(q), _lib.ptr(den),
+                  _lib.ptr(T0), None, stream())
+        return LinearizedStep(sigma_t=st, sigma_s=ss, sigma_a=sa, q=q, T0=T0, denom=den,
                               rho_cv=self.rho_cv, dt=float(self.spec.dt),
                               inv_cdt=1.0 / (k.c * self.spec.dt), constants=k)
 

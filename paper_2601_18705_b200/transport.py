@@ -12,6 +12,7 @@ return types and exceptions.
 from __future__ import annotations
 
 import math
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -213,7 +214,9 @@ _WS_CACHE = {}
 
 
 def _shared_workspace(grid, nbytes):
-    key = torch.cuda.current_device()
+    # one per (device, host thread): sweeps issued from different threads
+    # (thread-ranks in the tests) must not share the ticket / handoff words
+    key = (torch.cuda.current_device(), threading.get_ident())
     ws = _WS_CACHE.get(key)
     if ws is None or ws.numel() < nbytes:
         ws = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=device())

@@ -36,3 +36,25 @@ cw = x[:, 1] - x[:, 0]; cc = x[:, 2] - x[:, 1]
 pw = x[:, 4] - x[:, 3]; pc = x[:, 5] - x[:, 4]; pb = x[:, 6] - x[:, 5]
 print(f"consumer: wait {np.median(cw):.3f} compute {np.median(cc):.3f} us/chunk (sum wait {cw.sum():.0f}, compute {cc.sum():.0f})")
 print(f"producer: wait {np.median(pw):.3f} compute {np.median(pc):.3f} namedbar {np.median(pb):.3f} us/chunk (sums {pw.sum():.0f} {pc.sum():.0f} {pb.sum():.0f})")
+# per-strip timeline of group 0 (items are strip-major: item = s * G + g)
+G = plan.G
+for s in range(ns):
+    x = t[s * G]
+    ok = x[:, 2] > 0
+    if not ok.any():
+        continue
+    cw = x[ok, 1] - x[ok, 0]
+    print(f"strip {s}: start {x[ok, 0].min():7.2f} end {x[ok, 2].max():7.2f} us, consumer wait sum {cw.sum():6.2f}"
+          f" first-chunk wait {cw[0]:6.2f}")
+for s in (0, 1, 4):
+    x = t[s * G]
+    cw = x[:, 1] - x[:, 0]; cc = x[:, 2] - x[:, 1]; gap = x[1:, 0] - x[:-1, 2]
+    print(f"strip {s} per-chunk wait:", np.round(cw[:20], 2))
+    print(f"strip {s} per-chunk comp:", np.round(cc[:20], 2))
+    print(f"strip {s} gap to next   :", np.round(gap[:20], 2))
+for s in (0, 4):
+    x = t[s * G]
+    pw = x[:, 4] - x[:, 3]; pc = x[:, 5] - x[:, 4]
+    print(f"strip {s} producer wait:", np.round(pw[:16], 2))
+    print(f"strip {s} producer comp:", np.round(pc[:16], 2))
+    print(f"strip {s} prod ready(5) - cons wantstart(0):", np.round((x[:, 6] - x[:, 0])[:16], 2))
