@@ -794,8 +794,10 @@ __global__ void chol_upper_warp_kernel(int r, const double* __restrict__ G, doub
 
 // Weighted CholQR2 of a small tall matrix held in shared memory (the angular
 // basis update, angular.py:217-238, full-rank case): Q = W R^-1 with
-// W^T diag(w) W = R^T R, applied twice; R = R2 R1.  ratio/flag feed the same
-// guard as the spatial CholQR2 (a failed guard reruns the exact CGS2).
+// W^T diag(w) W = R^T R, applied twice; R = R2 R1.  The Gram and the row
+// update run on the FP64 tensor cores (DMMA m8n8k4) over MT-padded tiles;
+// the Cholesky is one warp, in registers.  ratio/flag feed the same guard as
+// the spatial CholQR2 (a failed guard reruns the exact CGS2).
 template <int MT>
 __global__ void __launch_bounds__(256) cholqr2_small_kernel(int n, int m,
                                                             const double* __restrict__ Win,
@@ -804,51 +806,78 @@ __global__ void __launch_bounds__(256) cholqr2_small_kernel(int n, int m,
                                                             double* __restrict__ R,
                                                             double* __restrict__ ratio,
                                                             int* flag, int* deficient) {
+  constexpr int NT = MT / 8, KS = MT / 4, LQ = MT + 1;  // odd stride: conflict-free fragments
   extern __shared__ double sm[];
-  const int lq = m | 1;
-  double* A = sm;                       // n x lq
-  double* G = A + (size_t)n * lq;       // m x m (becomes R of the pass)
-  double* inv = G + m * m;              // m x m
-  double* R1 = inv + m * m;             // m x m
-  double* g0 = R1 + m * m;              // m (diag of the first Gram)
+  const int np = (n + 7) & ~7;               // rows padded to whole 8-row tiles
+  double* A = sm;                            // np x LQ (zero padded)
+  double* ws = A + (size_t)np * LQ;          // np weights (zero padded)
+  double* G = ws + np;                       // MT x MT (becomes R of the pass)
+  double* inv = G + MT * MT;                 // MT x MT
+  double* R1 = inv + MT * MT;                // MT x MT
+  double* red = R1 + MT * MT;                // 8 warps x MT x MT
   __shared__ int bad_s[2];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int64_t e = threadIdx.x; e < (int64_t)n * m; e += blockDim.x)
-    cp_async8(A + (e / m) * lq + e % m, Win + (e / m) * ldw + e % m);
-  double* ws = g0 + m;  // n weights
-  for (int e = threadIdx.x; e < n; e += blockDim.x) cp_async8(ws + e, w + e);
+  const int g = lane >> 2, q = lane & 3;
+  for (int e = threadIdx.x; e < np * LQ; e += blockDim.x) {
+    const int row = e / LQ, col = e - row * LQ;
+    if (row < n && col < m) cp_async8(A + e, Win + (int64_t)row * ldw + col);
+    else A[e] = 0.0;
+  }
+  for (int e = threadIdx.x; e < np; e += blockDim.x) {
+    if (e < n) cp_async8(ws + e, w + e);
+    else ws[e] = 0.0;
+  }
   cp_async_wait_all();
   __syncthreads();
-  const int ntri = m * (m + 1) / 2;
   for (int pass = 0; pass < 2; ++pass) {
-    // Gram (upper triangle): warp per entry, lanes over rows, shuffle sums
-    for (int t = wid; t < ntri; t += nw) {
-      int i = 0, rem = t;
-      while (rem >= m - i) { rem -= m - i; ++i; }
-      const int j = i + rem;
-      double acc = 0.0;
-      for (int row = lane; row < n; row += 32) acc += ws[row] * A[row * lq + i] * A[row * lq + j];
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-      if (lane == 0) {
-        G[i * m + j] = acc;
-        G[j * m + i] = acc;
+    // ---- Gram G = A^T diag(w) A: warp `wid` takes row quads wid, wid + nw, ...
+    double d[NT][NT][2];
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) d[i][j][0] = d[i][j][1] = 0.0;
+    for (int k0 = 4 * wid; k0 < np; k0 += 4 * nw) {
+      const double* arow = A + (k0 + q) * LQ;
+      const double wk = ws[k0 + q];
+      double af[NT], bf[NT];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        af[t] = arow[8 * t + g];
+        bf[t] = wk * af[t];
       }
+#pragma unroll
+      for (int i = 0; i < NT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(d[i][j][0], d[i][j][1], af[i], bf[j]);
+    }
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        red[(wid * MT + 8 * i + g) * MT + 8 * j + 2 * q] = d[i][j][0];
+        red[(wid * MT + 8 * i + g) * MT + 8 * j + 2 * q + 1] = d[i][j][1];
+      }
+    __syncthreads();
+    for (int e = threadIdx.x; e < MT * MT; e += blockDim.x) {
+      double acc = 0.0;
+      for (int ww = 0; ww < nw; ++ww) acc += red[ww * MT * MT + e];
+      G[e] = acc;
     }
     __syncthreads();
+    // ---- Cholesky + inverse (one warp, registers)
     if (wid == 0) {
       double c[MT], iv[MT];
 #pragma unroll
-      for (int i = 0; i < MT; ++i) c[i] = (i < m && lane < m) ? G[i * m + lane] : 0.0;
-      const double gkk = lane < m ? G[lane * m + lane] : 0.0;
+      for (int i = 0; i < MT; ++i) c[i] = (i < m && lane < m) ? G[i * MT + lane] : 0.0;
+      const double gkk = lane < m ? G[lane * MT + lane] : 0.0;
       const int bad = warp_chol_reg<MT>(m, c, iv);
       __syncwarp();
-      if (lane < m) {
+      if (lane < MT) {
 #pragma unroll
-        for (int i = 0; i < MT; ++i)
-          if (i < m) {
-            G[i * m + lane] = c[i];
-            inv[i * m + lane] = iv[i];
-          }
+        for (int i = 0; i < MT; ++i) {
+          G[i * MT + lane] = lane < m ? c[i] : 0.0;
+          inv[i * MT + lane] = lane < m ? iv[i] : 0.0;
+        }
       }
       if (lane == 0) bad_s[pass] = bad;
       if (pass == 0 && lane < m) {
@@ -862,36 +891,45 @@ __global__ void __launch_bounds__(256) cholqr2_small_kernel(int n, int m,
       }
     }
     __syncthreads();
-    // A = A R^-1, row by row
-    for (int row = threadIdx.x; row < n; row += blockDim.x) {
-      double x[MT], y[MT];
+    // ---- A = A R^-1 by 8-row tiles (DMMA), in place
+    {
+      double bf[KS][NT];
 #pragma unroll
-      for (int p = 0; p < MT; ++p) x[p] = p < m ? A[row * lq + p] : 0.0;
+      for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-      for (int j = 0; j < MT; ++j) {
-        double acc = 0.0;
+        for (int t = 0; t < NT; ++t) bf[ks][t] = inv[(4 * ks + q) * MT + 8 * t + g];
+      for (int r0 = 8 * wid; r0 < np; r0 += 8 * nw) {
+        double af[KS];
 #pragma unroll
-        for (int p = 0; p <= j; ++p)
-          if (j < m) acc = fma(x[p], inv[p * m + j], acc);
-        y[j] = acc;
+        for (int ks = 0; ks < KS; ++ks) af[ks] = A[(r0 + g) * LQ + 4 * ks + q];
+        double dd[NT][2];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) dd[t][0] = dd[t][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+          for (int t = 0; t < NT; ++t) dmma(dd[t][0], dd[t][1], af[ks], bf[ks][t]);
+        __syncwarp();  // every lane has read the tile before it is overwritten
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          A[(r0 + g) * LQ + 8 * t + 2 * q] = dd[t][0];
+          A[(r0 + g) * LQ + 8 * t + 2 * q + 1] = dd[t][1];
+        }
       }
-#pragma unroll
-      for (int j = 0; j < MT; ++j)
-        if (j < m) A[row * lq + j] = y[j];
     }
     if (pass == 0)
-      for (int e = threadIdx.x; e < m * m; e += blockDim.x) R1[e] = G[e];
+      for (int e = threadIdx.x; e < MT * MT; e += blockDim.x) R1[e] = G[e];
     __syncthreads();
   }
   // R = R2 R1 (both upper)
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
     const int i = e / m, j = e % m;
     double acc = 0.0;
-    for (int p = i; p <= j; ++p) acc = fma(G[i * m + p], R1[p * m + j], acc);
+    for (int p = i; p <= j; ++p) acc = fma(G[i * MT + p], R1[p * MT + j], acc);
     R[e] = j >= i ? acc : 0.0;
   }
   for (int64_t e = threadIdx.x; e < (int64_t)n * m; e += blockDim.x)
-    Q[(e / m) * ldq + e % m] = A[(e / m) * lq + e % m];
+    Q[(e / m) * ldq + e % m] = A[(e / m) * LQ + e % m];
   for (int k = threadIdx.x; k < m; k += blockDim.x) deficient[k] = 0;
   if (threadIdx.x == 0) {
     flag[0] = bad_s[0];
@@ -1406,7 +1444,8 @@ int dlrsn_chol_upper(int r, const double* G, double* R, double* Rinv, double* di
 }
 
 int64_t dlrsn_cholqr2_small_smem(int n, int m) {
-  return ((int64_t)n * (m | 1) + 3 * (int64_t)m * m + m + n) * (int64_t)sizeof(double);
+  const int64_t mt = m <= 16 ? 16 : 32, np = (n + 7) / 8 * 8;
+  return (np * (mt + 1) + np + 3 * mt * mt + 8 * mt * mt) * (int64_t)sizeof(double);
 }
 
 int dlrsn_cholqr2_small(int n, int m, const double* W, int ldw, const double* w, double* Q,

@@ -236,6 +236,7 @@ struct StepBufs {
   double *wpart, *wg;
   int *idx, *quads, *mine;
   int64_t* place;
+  double* cw_local;
   dlrsn_group* groups;
   SiCtl* ctl;
   unsigned* rbdev;
@@ -304,6 +305,7 @@ static size_t carve(Arena& ar, StepBufs& b, int nx, int ny, int r, int no, int w
   b.quads = ar.take<int>(r);
   b.mine = ar.take<int>(r);
   b.place = ar.take<int64_t>(r);
+  b.cw_local = ar.take<double>(r);
   b.groups = ar.take<dlrsn_group>(r);
   b.ctl = ar.take<SiCtl>(1);
   b.rbdev = ar.take<unsigned>(8192);
@@ -387,7 +389,7 @@ __global__ void plan_kernel(int r, int no, int world, int rank, const int* __res
                             const double* __restrict__ closure, int* __restrict__ idx,
                             dlrsn_group* __restrict__ groups, int* __restrict__ quads,
                             int* __restrict__ mine, int64_t* __restrict__ place, int64_t n_dofs,
-                            int width) {
+                            int width, double* __restrict__ cw_local) {
   // thread d = selected direction d (r <= 128); every rank / position is a
   // count over the r directions (O(r) per thread)
   __shared__ int sq[DLRSN_MAX_RANK], sown[DLRSN_MAX_RANK];
@@ -416,6 +418,7 @@ __global__ void plan_kernel(int r, int no, int world, int rank, const int* __res
     if (owner == rank) {
       mine[pos] = d;
       quads[pos] = sq[d];
+      cw_local[pos] = closure[d];
       int gi = 0;  // this rank's groups in quadrant order (transport.plan_groups)
       for (int e = 0; e < r; ++e)
         gi += sown[e] == rank && ((sq[e] < sq[d]) || (sq[e] == sq[d] && e < d));
@@ -556,7 +559,8 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
   }
   const int width = world > 1 ? comm->gather_width : 1;
   plan_kernel<<<1, DLRSN_MAX_RANK, 0, st>>>(r, no, world, rank_id, b.err_idx, b.err_idx + 1, p->omegas_dev,
-                                b.closure, b.idx, b.groups, b.quads, b.mine, b.place, N, width);
+                                b.closure, b.idx, b.groups, b.quads, b.mine, b.place, N, width,
+                                b.cw_local);
   DLRSN_CHECK_LAUNCH("plan_kernel");
 
   // ---- 2. evaluate_rows, scalar_flux, rhs (dlr_sn.py:110-121) ---------------
@@ -603,8 +607,8 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
         if (nl > 0)
           DLRSN_RET(phi_combine_launch(ops, G, b.groups, nullptr, b.psi_sk, phi, sigma_s,
                                        comm->reduce_buf, nullptr, b.norms, b.red_ws, b.ctl,
-                                       -1 /* skip test only: partial norms */, p->si_tol,
-                                       nullptr, st));
+                                       -1 /* skip test only: partial norms */, p->si_tol, nullptr,
+                                       st));
         else
           DLRSN_TRY_CUDA(cudaMemsetAsync(comm->reduce_buf, 0, N * sizeof(double), st));
         if (comm->allreduce_sum(comm->user) != 0) {

@@ -60,7 +60,9 @@ __host__ __device__ constexpr size_t sweep_smem_bytes() {
 template <int DW>
 __global__ void __launch_bounds__(SweepCfg<DW>::WPC * 32)
 sweep_kernel(const SweepArgs a) {
-  if (a.skip && *a.skip) return;  // iteration past convergence
+  // iterations past convergence take no work item (no early return: that
+  // would cost the compiler its proof that the warps stay converged)
+  const bool skip = a.skip != nullptr && *a.skip != 0;
   constexpr int C = SweepCfg<DW>::C, P = SweepCfg<DW>::P, WPC = SweepCfg<DW>::WPC;
   constexpr int SD = stage_doubles<DW>();
   extern __shared__ __align__(128) double smem[];
@@ -87,7 +89,7 @@ sweep_kernel(const SweepArgs a) {
 
   for (;;) {
     int item = 0;
-    if (lane == 0) item = atomicAdd(a.ticket, 1);
+    if (lane == 0) item = skip ? items : atomicAdd(a.ticket, 1);
     item = __shfl_sync(kFull, item, 0);
     if (item >= items) break;
     const int s = item / G;
@@ -417,8 +419,8 @@ __global__ void phi_combine_kernel(dlrsn_cellops ops, int G, const dlrsn_group* 
         for (int k = 0; k < nd; ++k) {
           const double* src = psi + (int64_t)groups[g].slot[k] * vlen;
           const double w = groups[g].cw[k];
-          const double2 a = *reinterpret_cast<const double2*>(src + sk_vec_off(T, s, t, 0, lane));
-          const double2 b = *reinterpret_cast<const double2*>(src + sk_vec_off(T, s, t, 1, lane));
+          const double2 a = __ldcg(reinterpret_cast<const double2*>(src + sk_vec_off(T, s, t, 0, lane)));
+          const double2 b = __ldcg(reinterpret_cast<const double2*>(src + sk_vec_off(T, s, t, 1, lane)));
           const double o[4] = {w * a.x, w * a.y, w * b.x, w * b.y};
 #pragma unroll
           for (int l = 0; l < 4; ++l) p[l] += o[l ^ f];

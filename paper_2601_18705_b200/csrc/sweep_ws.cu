@@ -113,7 +113,9 @@ __device__ __forceinline__ void ws_factor_step(const SweepArgs& a, const double*
 }
 
 __global__ void __launch_bounds__(kWsThreads) sweep_ws_kernel(const SweepArgs a) {
-  if (a.skip && *a.skip) return;  // iteration past convergence
+  // iterations past convergence take no work item (an early return would
+  // cost the compiler its proof that warps stay converged at the shuffles)
+  const bool skip = a.skip != nullptr && *a.skip != 0;
   extern __shared__ __align__(128) double sm[];
   double* in_ring = sm;                 // 2 x kWsInD
   double* fac_ring = sm + kWsStages * kWsInD;   // kWsStages x kWsFacD
@@ -146,7 +148,7 @@ __global__ void __launch_bounds__(kWsThreads) sweep_ws_kernel(const SweepArgs a)
   uint32_t uses[kWsStages] = {};
 
   for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(a.ticket, 1);
+    if (threadIdx.x == 0) s_item = skip ? items : atomicAdd(a.ticket, 1);
     __syncthreads();
     const int item = s_item;
     __syncthreads();
@@ -302,6 +304,9 @@ __global__ void __launch_bounds__(kWsThreads) sweep_ws_kernel(const SweepArgs a)
             *reinterpret_cast<volatile double*>(&hs->x) = empty;
           }
         }
+        // full-warp vote: lets the compiler prove convergence for the step
+        // loop's shuffles (without it every shuffle gets a collective path)
+        (void)__any_sync(kFull, true);
         WS_TRACE(0);
         mbar_wait_warp(&fac_full[st], u & 1u);
         WS_TRACE(1);
