@@ -15,6 +15,8 @@
 #include <cmath>
 #include <cstring>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace dlrsn {
