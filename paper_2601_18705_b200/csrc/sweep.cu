@@ -34,10 +34,14 @@ __device__ int g_flags = 0;  // debug: bit0 = no speculative handoff prefetch
 
 
 // Steps per TMA chunk, pipeline depth and warps per CTA for a group width.
+// (C steps per stage, P stages, WPC warps per CTA): measured on the config-2
+// full-SN sweep (1024 directions, 280x280): double buffering with 4-warp CTAs
+// keeps enough warps resident per SM; wider chunks or deeper rings lose
+// occupancy to shared memory (scripts/full_sn.py).
 template <int DW> struct SweepCfg;
-template <> struct SweepCfg<1> { static constexpr int C = 4, P = 3, WPC = 4; };
-template <> struct SweepCfg<2> { static constexpr int C = 2, P = 3, WPC = 4; };
-template <> struct SweepCfg<4> { static constexpr int C = 2, P = 3, WPC = 2; };
+template <> struct SweepCfg<1> { static constexpr int C = 4, P = 2, WPC = 4; };
+template <> struct SweepCfg<2> { static constexpr int C = 4, P = 2, WPC = 4; };
+template <> struct SweepCfg<4> { static constexpr int C = 2, P = 2, WPC = 4; };
 template <> struct SweepCfg<8> { static constexpr int C = 1, P = 3, WPC = 2; };
 
 template <int DW>

@@ -37,9 +37,8 @@ def plan_groups(omegas, closure, n_strips, dw=None, sm_count=148):
     """Partition the swept directions into warp groups (host logic).
 
     Directions of one quadrant share the traversal order, so a group holds
-    up to ``dw`` directions of a single quadrant; the width is the largest
-    power of two that still yields enough warps (groups x strips) to fill the
-    GPU, else 1.  Returns (groups structured array, dw, quad codes per slot).
+    up to ``dw`` directions of a single quadrant; the default width is 2 when
+    that still yields enough warps (groups x strips) to fill the GPU, else 1.  Returns (groups structured array, dw, quad codes per slot).
     """
     om = np.asarray(omegas, dtype=float)
     clo = np.asarray(closure, dtype=float)
@@ -47,13 +46,12 @@ def plan_groups(omegas, closure, n_strips, dw=None, sm_count=148):
     quads = np.array([quadrant_code(om[d]) for d in range(D)], dtype=np.int32)
     members = [np.flatnonzero(quads == q) for q in range(4)]
     if dw is None:
+        # pairs of directions per warp when that still fills the GPU with
+        # (group, strip) items (fastest on the config-2 full-SN sweep:
+        # dw 2 > 4 > 1 > 8, scripts/full_sn.py), else one direction per warp
         target = _WARPS_PER_SM_TARGET * sm_count
-        dw = 1
-        for cand in (8, 4, 2):
-            g = sum(math.ceil(len(m) / cand) for m in members)
-            if g * n_strips >= target:
-                dw = cand
-                break
+        g2 = sum(math.ceil(len(m) / 2) for m in members)
+        dw = 2 if g2 * n_strips >= target else 1
     biggest = max((len(m) for m in members), default=1)
     while dw > 1 and dw // 2 >= biggest:
         dw //= 2
