@@ -132,32 +132,52 @@ __global__ void __launch_bounds__(256) rowmix_mma_kernel(int n, int kx, int ky,
       const int k = 4 * ks + q, c = 8 * nt + g;
       bf[ks][nt] = (k < kx && c < ky) ? __ldg(K + (int64_t)k * ldk + c) : 0.0;
     }
+  // U tiles per warp and iteration: their loads are in flight together and
+  // their MMA chains interleave (one tile at a time is latency-bound)
+  constexpr int U = 4;
   const int64_t tiles = ((int64_t)n + 7) / 8;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < tiles; t += nwarps) {
-    const int64_t row = t * 8 + g;
-    double af[KS];
+  for (int64_t t0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t0 < tiles;
+       t0 += U * nwarps) {
+    double af[U][KS];
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const int c = 4 * ks + q;
-      af[ks] = (row < n && c < kx) ? __ldg(X + row * ldx + c) : 0.0;
+    for (int u = 0; u < U; ++u) {
+      const int64_t row = (t0 + u * nwarps) * 8 + g;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int c = 4 * ks + q;
+        af[u][ks] = (row < n && c < kx) ? __ldg(X + row * ldx + c) : 0.0;
+      }
     }
-    double d[NT][2];
+    double d[U][NT][2];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) d[nt][0] = d[nt][1] = 0.0;
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) d[u][nt][0] = d[u][nt][1] = 0.0;
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) dmma(d[nt][0], d[nt][1], af[ks], bf[ks][nt]);
-    if (row < n) {
-      double* y = Y + row * ldy;
+      for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
+        for (int nt = 0; nt < NT; ++nt) dmma(d[u][nt][0], d[u][nt][1], af[u][ks], bf[ks][nt]);
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int c = 8 * nt + 2 * q + i;
-          if (c < ky) y[c] = beta == 0.0 ? d[nt][i] : fma(beta, y[c], d[nt][i]);
+    for (int u = 0; u < U; ++u) {
+      const int64_t row = (t0 + u * nwarps) * 8 + g;
+      if (row < n) {
+        double* y = Y + row * ldy;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int c = 8 * nt + 2 * q;
+          if (beta == 0.0 && c + 1 < ky && ((ldy & 1) == 0) &&
+              ((reinterpret_cast<uintptr_t>(Y) & 15) == 0)) {
+            *reinterpret_cast<double2*>(y + c) = make_double2(d[u][nt][0], d[u][nt][1]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+              if (c + i < ky) y[c + i] = beta == 0.0 ? d[u][nt][i] : fma(beta, y[c + i], d[u][nt][i]);
+          }
         }
+      }
     }
   }
 }
@@ -255,7 +275,7 @@ __global__ void __launch_bounds__(256) mgram_kernel(int ncell, int ra, int rb,
 // c_begin + w, + 8, ...; per cell the k dimension of the MMA is the cell's 4
 // dofs, A = X_c^T (m = column of A), B = M X_c (the 4x4 mass block applied
 // across each lane quad by shuffles).  Warp partials are summed in warp order.
-__global__ void __launch_bounds__(256) mgram_mma_kernel(int ncell, int ra, int rb,
+__global__ void __launch_bounds__(256, 4) mgram_mma_kernel(int ncell, int ra, int rb,
                                                         const double* __restrict__ A, int lda,
                                                         const double* __restrict__ B, int ldb,
                                                         const double* __restrict__ coeff,
@@ -274,31 +294,41 @@ __global__ void __launch_bounds__(256) mgram_mma_kernel(int ncell, int ra, int r
   const bool ia0 = i0 + g < ra, ia1 = i0 + 8 + g < ra, jb0 = j0 + g < rb, jb1 = j0 + 8 + g < rb;
   const int base = lane & ~3;
   double d[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
-#pragma unroll 4
-  for (int c = c_begin + warp; c < c_end; c += 8) {
-    const int64_t row = (int64_t)c * 4 + q;
-    const double a0 = ia0 ? __ldg(A + row * lda + i0 + g) : 0.0;
-    const double a1 = ia1 ? __ldg(A + row * lda + i0 + 8 + g) : 0.0;
-    double v0 = a0, v1 = a1;
-    if (!same) {
-      v0 = jb0 ? __ldg(B + row * ldb + j0 + g) : 0.0;
-      v1 = jb1 ? __ldg(B + row * ldb + j0 + 8 + g) : 0.0;
-    }
-    double b0 = 0.0, b1 = 0.0;
+  constexpr int U = 2;  // cells per warp and iteration: loads in flight together
+  for (int c0 = c_begin + warp; c0 < c_end; c0 += 8 * U) {
+    double a0[U], a1[U], v0[U], v1[U], wc[U];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      b0 = fma(m[b], __shfl_sync(kFull, v0, base | b), b0);
-      b1 = fma(m[b], __shfl_sync(kFull, v1, base | b), b1);
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + 8 * u;
+      const bool in = c < c_end;
+      const int64_t row = (int64_t)c * 4 + q;
+      a0[u] = (in && ia0) ? __ldg(A + row * lda + i0 + g) : 0.0;
+      a1[u] = (in && ia1) ? __ldg(A + row * lda + i0 + 8 + g) : 0.0;
+      v0[u] = a0[u];
+      v1[u] = a1[u];
+      if (!same) {
+        v0[u] = (in && jb0) ? __ldg(B + row * ldb + j0 + g) : 0.0;
+        v1[u] = (in && jb1) ? __ldg(B + row * ldb + j0 + 8 + g) : 0.0;
+      }
+      wc[u] = (coeff && in) ? __ldg(coeff + c) : 1.0;
     }
-    if (coeff) {
-      const double w = __ldg(coeff + c);
-      b0 *= w;
-      b1 *= w;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double b0 = 0.0, b1 = 0.0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        b0 = fma(m[b], __shfl_sync(kFull, v0[u], base | b), b0);
+        b1 = fma(m[b], __shfl_sync(kFull, v1[u], base | b), b1);
+      }
+      if (coeff) {
+        b0 *= wc[u];
+        b1 *= wc[u];
+      }
+      dmma(d[0][0][0], d[0][0][1], a0[u], b0);
+      dmma(d[0][1][0], d[0][1][1], a0[u], b1);
+      dmma(d[1][0][0], d[1][0][1], a1[u], b0);
+      dmma(d[1][1][0], d[1][1][1], a1[u], b1);
     }
-    dmma(d[0][0][0], d[0][0][1], a0, b0);
-    dmma(d[0][1][0], d[0][1][1], a0, b1);
-    dmma(d[1][0][0], d[1][0][1], a1, b0);
-    dmma(d[1][1][0], d[1][1][1], a1, b1);
   }
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)

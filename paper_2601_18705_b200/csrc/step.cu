@@ -237,6 +237,7 @@ struct StepBufs {
   int *idx, *quads, *mine;
   int64_t* place;
   double* cw_local;
+  double* phiq;
   dlrsn_group* groups;
   SiCtl* ctl;
   unsigned* rbdev;
@@ -306,6 +307,7 @@ static size_t carve(Arena& ar, StepBufs& b, int nx, int ny, int r, int no, int w
   b.mine = ar.take<int>(r);
   b.place = ar.take<int64_t>(r);
   b.cw_local = ar.take<double>(r);
+  b.phiq = ar.take<double>(4 * N);
   b.groups = ar.take<dlrsn_group>(r);
   b.ctl = ar.take<SiCtl>(1);
   b.rbdev = ar.take<unsigned>(8192);
@@ -600,15 +602,14 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
         DLRSN_RET(sweep_launch(ops, G, b.groups, 1, b.sig4, b.scat, b.rhs_sk, b.psi_sk, nullptr,
                                sweep_ws, sweep_ws_bytes, 0, &b.ctl->done, st));
       if (world == 1) {
-        DLRSN_RET(phi_combine_launch(ops, G, b.groups, nullptr, b.psi_sk, phi, sigma_s, phin,
-                                     b.scat, b.norms, b.red_ws, b.ctl, it, p->si_tol,
-                                     b.flags + 1, st));
+        DLRSN_RET(phi_closure_launch(ops, nl, b.quads, b.cw_local, b.psi_sk, b.phiq, phi, sigma_s,
+                                     phin, b.scat, b.norms, b.red_ws, b.ctl, it, p->si_tol,
+                                     b.flags + 1, nullptr, st));
       } else {
         if (nl > 0)
-          DLRSN_RET(phi_combine_launch(ops, G, b.groups, nullptr, b.psi_sk, phi, sigma_s,
-                                       comm->reduce_buf, nullptr, b.norms, b.red_ws, b.ctl,
-                                       -1 /* skip test only: partial norms */, p->si_tol, nullptr,
-                                       st));
+          DLRSN_RET(phi_closure_launch(ops, nl, b.quads, b.cw_local, b.psi_sk, b.phiq, phi,
+                                       sigma_s, nullptr, nullptr, b.norms, b.red_ws, b.ctl, -1,
+                                       p->si_tol, nullptr, comm->reduce_buf, st));
         else
           DLRSN_TRY_CUDA(cudaMemsetAsync(comm->reduce_buf, 0, N * sizeof(double), st));
         if (comm->allreduce_sum(comm->user) != 0) {

@@ -469,6 +469,138 @@ __global__ void phi_combine_kernel(dlrsn_cellops ops, int G, const dlrsn_group* 
   }
 }
 
+// Closure flux of the one-call step in two coalesced passes.  Pass 1: for
+// quadrant q (blockIdx.y), thread = one SK element (strip, step, lane) -- the
+// same cell for every direction of that quadrant -- sums cw_k psi_k over the
+// quadrant's slots in slot order (loads of 32 lanes contiguous) and writes
+// the quadrant partial of that cell, canonical dofs, one 32-byte sector.
+__global__ void __launch_bounds__(256) phi_quadrant_kernel(
+    int nx, int ny, int D, const int* __restrict__ quads, const double* __restrict__ cw,
+    const double* __restrict__ psi, int64_t vlen, double* __restrict__ phiq, int64_t nd,
+    const SiCtl* ctl) {
+  __shared__ int s_k[DLRSN_MAX_RANK];
+  __shared__ double s_w[DLRSN_MAX_RANK];
+  __shared__ int s_n;
+  if (ctl != nullptr && ctl->done != 0) return;
+  const int qd = blockIdx.y;
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int k = 0; k < D; ++k)
+      if (quads[k] == qd) {
+        s_k[n] = k;
+        s_w[n] = cw[k];
+        ++n;
+      }
+    s_n = n;
+  }
+  __syncthreads();
+  const int n = s_n;
+  const int T = nx + 31;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (s, t, lane)
+  const int lane = (int)(e & 31);
+  const int64_t st = e >> 5;
+  const int s = (int)(st / T), t = (int)(st - (int64_t)s * T);
+  const int ip = t - lane, jp = 32 * s + lane;
+  if (jp >= ny || ip < 0 || ip >= nx) return;
+  const int i = (qd & 1) ? nx - 1 - ip : ip;
+  const int j = (qd & 2) ? ny - 1 - jp : jp;
+  const int64_t off = sk_vec_off(T, s, t, 0, lane);
+  double p[4] = {0.0, 0.0, 0.0, 0.0};
+  if (n > 0) {
+#pragma unroll 4
+    for (int m = 0; m < n; ++m) {
+      const double* src = psi + (int64_t)s_k[m] * vlen + off;
+      const double2 a = __ldcg(reinterpret_cast<const double2*>(src));
+      const double2 b = __ldcg(reinterpret_cast<const double2*>(src + 64));
+      const double w = s_w[m];
+      p[0] += w * a.x;
+      p[1] += w * a.y;
+      p[2] += w * b.x;
+      p[3] += w * b.y;
+    }
+  }
+  // oriented dof l is canonical dof l ^ quad
+  const int f = sk_flip(qd);
+  double o[4];
+#pragma unroll
+  for (int l = 0; l < 4; ++l) o[l ^ f] = p[l];
+  double2* dst = reinterpret_cast<double2*>(phiq + (int64_t)qd * nd + 4 * ((int64_t)j * nx + i));
+  dst[0] = make_double2(o[0], o[1]);
+  dst[1] = make_double2(o[2], o[3]);
+}
+
+// Pass 2: phi = ((q0 + q1) + q2) + q3 per dof; then the norms / scattering
+// source / convergence decision of phi_combine_kernel (partial_out: write the
+// rank-partial phi for the allreduce instead and stop).
+__global__ void __launch_bounds__(256) phi_sum_kernel(
+    dlrsn_cellops ops, const double* __restrict__ phiq, int64_t nd,
+    const double* __restrict__ phi_old, const double* __restrict__ ss,
+    double* __restrict__ phi_new, double* __restrict__ scat, int64_t vlen, double* norms,
+    double* partials, unsigned* counter, SiCtl* ctl, int it, double tol, const int* any_scat,
+    double* __restrict__ partial_out) {
+  __shared__ double red[64];
+  __shared__ bool last;
+  if (ctl && ctl->done) return;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool in = c < ops.nx * ops.ny;
+  double p[4] = {0.0, 0.0, 0.0, 0.0};
+  if (in) {
+#pragma unroll
+    for (int qd = 0; qd < 4; ++qd) {
+      const double2 a = __ldcg(reinterpret_cast<const double2*>(phiq + qd * nd) + 2 * c);
+      const double2 b = __ldcg(reinterpret_cast<const double2*>(phiq + qd * nd) + 2 * c + 1);
+      p[0] += a.x;
+      p[1] += a.y;
+      p[2] += b.x;
+      p[3] += b.y;
+    }
+  }
+  if (partial_out) {
+    if (in) {
+      reinterpret_cast<double2*>(partial_out)[2 * c] = make_double2(p[0], p[1]);
+      reinterpret_cast<double2*>(partial_out)[2 * c + 1] = make_double2(p[2], p[3]);
+    }
+    return;
+  }
+  double v[2] = {0.0, 0.0};
+  if (in) {
+    const double2 oa = reinterpret_cast<const double2*>(phi_old)[2 * c];
+    const double2 ob = reinterpret_cast<const double2*>(phi_old)[2 * c + 1];
+    const double po[4] = {oa.x, oa.y, ob.x, ob.y};
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const double dlt = p[l] - po[l];
+      v[0] += dlt * dlt;
+      v[1] += p[l] * p[l];
+    }
+    reinterpret_cast<double2*>(phi_new)[2 * c] = make_double2(p[0], p[1]);
+    reinterpret_cast<double2*>(phi_new)[2 * c + 1] = make_double2(p[2], p[3]);
+    if (scat) write_scat4(ops, c, p, ss[c], scat, vlen);
+  }
+  block_sum<2>(v, red);
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = v[0];
+    partials[2 * blockIdx.x + 1] = v[1];
+    __threadfence();
+    last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    double w[2] = {0.0, 0.0};
+    for (int b2 = threadIdx.x; b2 < (int)gridDim.x; b2 += blockDim.x) {
+      w[0] += __ldcg(partials + 2 * b2);
+      w[1] += __ldcg(partials + 2 * b2 + 1);
+    }
+    block_sum<2>(w, red);
+    if (threadIdx.x == 0) {
+      norms[0] = w[0];
+      norms[1] = w[1];
+      *counter = 0u;
+      if (ctl && it > 0) si_decide(ctl, w, it, tol, any_scat);
+    }
+  }
+}
+
 // Sharded iteration: phi (canonical) already summed over ranks; compute the
 // convergence norms against phi_old and the next scattering source.
 __global__ void phi_finish_kernel(dlrsn_cellops ops, const double* __restrict__ phi_src,
@@ -583,6 +715,28 @@ int phi_combine_launch(const dlrsn_cellops* ops, int G, const dlrsn_group* group
                                          phi_new, scat_sk4, sk_vec_len(ops->nx, ops->ny), norms,
                                          partials, counter, ctl, it, tol, any_scat);
   DLRSN_CHECK_LAUNCH("phi_combine_kernel");
+  return DLRSN_OK;
+}
+
+int phi_closure_launch(const dlrsn_cellops* ops, int D, const int* quads, const double* cw,
+                       const double* psi_sk, double* phiq, const double* phi_old,
+                       const double* sigma_s, double* phi_new, double* scat_sk4, double* norms,
+                       void* partial_ws, SiCtl* ctl, int it, double tol, const int* any_scat,
+                       double* partial_out, cudaStream_t st) {
+  DLRSN_REQUIRE(D >= 1 && D <= DLRSN_MAX_RANK, "closure: 1..%d slots", DLRSN_MAX_RANK);
+  const int nx = ops->nx, ny = ops->ny, ns = (ny + 31) / 32;
+  const int64_t nd = 4 * (int64_t)nx * ny;
+  const int64_t elems = (int64_t)ns * (nx + 31) * 32;
+  phi_quadrant_kernel<<<dim3((unsigned)((elems + 255) / 256), 4), 256, 0, st>>>(
+      nx, ny, D, quads, cw, psi_sk, sk_vec_len(nx, ny), phiq, nd, ctl);
+  DLRSN_CHECK_LAUNCH("phi_quadrant_kernel");
+  const int nb = (nx * ny + 255) / 256;
+  unsigned* counter = reinterpret_cast<unsigned*>(partial_ws);
+  double* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(partial_ws) + 256);
+  phi_sum_kernel<<<nb, 256, 0, st>>>(*ops, phiq, nd, phi_old, sigma_s, phi_new, scat_sk4,
+                                     sk_vec_len(nx, ny), norms, partials, counter, ctl, it, tol,
+                                     any_scat, partial_out);
+  DLRSN_CHECK_LAUNCH("phi_sum_kernel");
   return DLRSN_OK;
 }
 

@@ -108,6 +108,14 @@ int phi_combine_launch(const dlrsn_cellops* ops, int G, const dlrsn_group* group
                        const double* sigma_s, double* phi_new, double* scat_sk4, double* norms,
                        void* partial_ws, SiCtl* ctl, int it, double tol, const int* any_scat,
                        cudaStream_t st);
+// closure flux in two coalesced passes over the SK slabs of D swept slots:
+// per-quadrant partials into phiq (4 x n_dofs), then the sum + norms +
+// scattering source (partial_out != nullptr: rank partial only, sharded)
+int phi_closure_launch(const dlrsn_cellops* ops, int D, const int* quads, const double* cw,
+                       const double* psi_sk, double* phiq, const double* phi_old,
+                       const double* sigma_s, double* phi_new, double* scat_sk4, double* norms,
+                       void* partial_ws, SiCtl* ctl, int it, double tol, const int* any_scat,
+                       double* partial_out, cudaStream_t st);
 int phi_finish_launch(const dlrsn_cellops* ops, const double* phi_src, double* phi_dst,
                       const double* phi_old, const double* sigma_s, double* scat_sk4,
                       double* norms, void* partial_ws, SiCtl* ctl, int it, double tol,
