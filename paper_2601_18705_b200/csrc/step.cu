@@ -317,63 +317,179 @@ static size_t carve(Arena& ar, StepBufs& b, int nx, int ny, int r, int no, int w
   return ar.off;
 }
 
-// pinned host staging (grown on demand, owned by the library)
-static thread_local char* g_pinned = nullptr;
-static thread_local size_t g_pinned_bytes = 0;
-static int pinned(size_t bytes, char** out) {
-  if (bytes > g_pinned_bytes) {
-    if (g_pinned) cudaFreeHost(g_pinned);
-    g_pinned = nullptr;
-    g_pinned_bytes = 0;
-    DLRSN_TRY_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&g_pinned), bytes, cudaHostAllocDefault));
-    g_pinned_bytes = bytes;
-  }
-  *out = g_pinned;
-  return DLRSN_OK;
-}
-
 #define DLRSN_RET(expr)              \
   do {                               \
     int rc_ = (expr);                \
     if (rc_ != DLRSN_OK) return rc_; \
   } while (0)
 
-// gather device regions into the pinned block, one sync
-struct Readback {
-  struct Item { const void* dev; size_t bytes; void* host; };
-  std::vector<Item> items;
-  void add(const void* dev, size_t bytes, void* host) { items.push_back({dev, bytes, host}); }
-  // one pack kernel + one device-to-host copy + one synchronisation
-  int run(cudaStream_t st, unsigned* staging) {
-    PackList l;
-    l.n = 0;
-    int off = 0;
-    for (auto& it : items) {
-      if (l.n == 24) {
-        set_error("internal: too many readback items");
-        return DLRSN_ECUDA;
-      }
-      l.src[l.n] = static_cast<const unsigned*>(it.dev);
-      l.words[l.n] = (int)((it.bytes + 3) / 4);
-      l.off[l.n] = off;
-      off += (l.words[l.n] + 1) & ~1;  // keep doubles 8-byte aligned
-      ++l.n;
-    }
-    if (off > 8192) {
-      set_error("internal: readback larger than its staging block");
-      return DLRSN_ECUDA;
-    }
-    char* h = nullptr;
-    DLRSN_RET(pinned((size_t)off * 4 + 64, &h));
-    pack_kernel<<<1, 256, 0, st>>>(l, staging);
-    DLRSN_CHECK_LAUNCH("pack_kernel");
-    DLRSN_TRY_CUDA(cudaMemcpyAsync(h, staging, (size_t)off * 4, cudaMemcpyDeviceToHost, st));
-    DLRSN_TRY_CUDA(cudaStreamSynchronize(st));
-    for (int k = 0; k < l.n; ++k) memcpy(items[k].host, h + (size_t)l.off[k] * 4, items[k].bytes);
-    items.clear();
-    return DLRSN_OK;
-  }
+// ---- the status block: every word the host needs after a segment, packed
+// on the device into a fixed layout and read back with one copy -----------
+struct StepStatus {
+  int err_idx[DLRSN_MAX_RANK + 1];  // [0] DEIM failure column (-1 ok), then the picks
+  int flags[8];                     // [0] sigma check, [1] any scattering
+  double chk_in[2], chk_out[2];     // orthonormality residuals (in / out)
+  SiCtl ctl;
+  double closure[DLRSN_MAX_RANK];
+  int rowstat[DLRSN_MAX_RANK + 1];
+  int defw[DLRSN_MAX_RANK], defx[DLRSN_MAX_RANK];
+  int statw, statx;
+  double ratio[2 * DLRSN_MAX_RANK], ratiow[2 * DLRSN_MAX_RANK];
+  int cholflag[2], cholw[2];
 };
+
+// pinned host copy of the status block (one per host thread; its address is
+// baked into captured graphs, so it is never reallocated)
+static int status_block(StepStatus** out) {
+  static thread_local StepStatus* hs = nullptr;
+  if (!hs) {
+    void* ptr = nullptr;
+    DLRSN_TRY_CUDA(cudaHostAlloc(&ptr, sizeof(StepStatus), cudaHostAllocDefault));
+    hs = static_cast<StepStatus*>(ptr);
+  }
+  *out = hs;
+  return DLRSN_OK;
+}
+
+// pack kernel + one device-to-host copy of the status block
+static int enqueue_status(cudaStream_t st, const StepBufs& b, int r, StepStatus* hs) {
+  PackList l;
+  l.n = 0;
+  StepStatus* dev = reinterpret_cast<StepStatus*>(b.rbdev);
+  auto add = [&](const void* src, size_t bytes, const void* dst_field) {
+    l.src[l.n] = static_cast<const unsigned*>(src);
+    l.words[l.n] = (int)((bytes + 3) / 4);
+    l.off[l.n] = (int)((reinterpret_cast<const char*>(dst_field) - reinterpret_cast<const char*>(dev)) / 4);
+    ++l.n;
+  };
+  add(b.err_idx, (r + 1) * sizeof(int), dev->err_idx);
+  add(b.flags, 8 * sizeof(int), dev->flags);
+  add(b.chk_in, 2 * sizeof(double), dev->chk_in);
+  add(b.chk_out, 2 * sizeof(double), dev->chk_out);
+  add(b.ctl, sizeof(SiCtl), &dev->ctl);
+  add(b.closure, r * sizeof(double), dev->closure);
+  add(b.rowstat, (r + 1) * sizeof(int), dev->rowstat);
+  add(b.defw, r * sizeof(int), dev->defw);
+  add(b.defx, r * sizeof(int), dev->defx);
+  add(b.statw, sizeof(int), &dev->statw);
+  add(b.statx, sizeof(int), &dev->statx);
+  add(b.ratio, 2 * r * sizeof(double), dev->ratio);
+  add(b.ratiow, 2 * r * sizeof(double), dev->ratiow);
+  add(b.cholflag, 2 * sizeof(int), dev->cholflag);
+  add(b.cholw, 2 * sizeof(int), dev->cholw);
+  pack_kernel<<<1, 256, 0, st>>>(l, b.rbdev);
+  DLRSN_CHECK_LAUNCH("pack_kernel");
+  DLRSN_TRY_CUDA(cudaMemcpyAsync(hs, dev, sizeof(StepStatus), cudaMemcpyDeviceToHost, st));
+  return DLRSN_OK;
+}
+
+// ---- CUDA-graph replay of the step's first segment --------------------------
+// The segment's ~50 launches depend only on the buffers, the parameters and
+// the iteration batch; a driver loop hands the same buffers back every other
+// step (the caching allocator), so the segment is captured once per buffer
+// set and replayed with one graph launch (no per-kernel host cost, no launch
+// gaps).  Everything baked into the graph is part of the key.
+struct GraphKey {
+  unsigned char bytes[sizeof(dlrsn_cellops) + sizeof(dlrsn_step_params) + 24 * sizeof(void*)];
+  void set(const dlrsn_cellops* ops, const dlrsn_step_params* p, const void* X, const void* S,
+           const void* W, const void* beta, const void* st, const void* ss, const void* q,
+           const void* Xn, const void* Sn, const void* Wn, const void* bn, const void* phi,
+           const void* siphi, const void* ws, const void* sws, int64_t sws_bytes, int batch,
+           int exact, int exact_w) {
+    memset(bytes, 0, sizeof(bytes));
+    size_t o = 0;
+    memcpy(bytes + o, ops, sizeof(*ops));
+    o += sizeof(*ops);
+    dlrsn_step_params pp = *p;
+    pp.omegas_host = nullptr;  // read on the host only
+    memcpy(bytes + o, &pp, sizeof(pp));
+    o += sizeof(pp);
+    const void* ptrs[] = {X, S, W, beta, st, ss, q, Xn, Sn, Wn, bn, phi, siphi, ws, sws};
+    memcpy(bytes + o, ptrs, sizeof(ptrs));
+    o += sizeof(ptrs);
+    const int64_t extra[4] = {sws_bytes, batch, exact, exact_w};
+    memcpy(bytes + o, extra, sizeof(extra));
+  }
+  bool operator==(const GraphKey& k) const { return memcmp(bytes, k.bytes, sizeof(bytes)) == 0; }
+};
+
+struct GraphEntry {
+  GraphKey key;
+  cudaGraphExec_t exec;
+  int device;
+  uint64_t used;
+  int64_t kernels;  // launches captured (added to the launch counter per replay)
+};
+
+static bool graphs_enabled() {
+  static const char* e = getenv("DLRSN_STEP_GRAPH");
+  return !(e && e[0] == '0');
+}
+
+template <class F>
+static int graph_run(const GraphKey& key, F&& enqueue, cudaStream_t st) {
+  static thread_local std::vector<GraphEntry> cache;
+  static thread_local uint64_t tick = 0;
+  static thread_local cudaStream_t cs = nullptr;
+  int dev = 0;
+  DLRSN_TRY_CUDA(cudaGetDevice(&dev));
+  ++tick;
+  GraphEntry* seen = nullptr;
+  for (auto& e : cache)
+    if (e.device == dev && e.key == key) {
+      e.used = tick;
+      if (e.exec) {
+        DLRSN_TRY_CUDA(cudaGraphLaunch(e.exec, st));
+        launch_counter().fetch_add(e.kernels, std::memory_order_relaxed);
+        return DLRSN_OK;
+      }
+      seen = &e;
+      break;
+    }
+  auto evict = [&]() {
+    if (cache.size() < 16) return;
+    size_t lru = 0;
+    for (size_t i = 1; i < cache.size(); ++i)
+      if (cache[i].used < cache[lru].used) lru = i;
+    if (cache[lru].exec) cudaGraphExecDestroy(cache[lru].exec);
+    cache.erase(cache.begin() + lru);
+  };
+  if (!seen) {
+    // first sighting: launch directly and remember the key; buffers that
+    // come back (a driver loop) are captured on their second use, one-off
+    // buffers (fresh allocations every step) never pay for a capture
+    evict();
+    GraphEntry e;
+    e.key = key;
+    e.exec = nullptr;
+    e.device = dev;
+    e.used = tick;
+    e.kernels = 0;
+    cache.push_back(e);
+    return enqueue(st);
+  }
+  if (!cs) DLRSN_TRY_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  // capture on a private stream (the caller's may be the legacy default stream)
+  DLRSN_TRY_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  const int64_t k0 = launch_counter().load();
+  const int rc = enqueue(cs);
+  const int64_t kernels = launch_counter().load() - k0;
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
+  if (rc != DLRSN_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  DLRSN_TRY_CUDA(ec);
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  DLRSN_TRY_CUDA(ei);
+  seen->exec = exec;
+  seen->kernels = kernels;
+  DLRSN_TRY_CUDA(cudaGraphLaunch(exec, st));
+  return DLRSN_OK;
+}
 
 // ---- device-side planning (no host round trip for the DEIM picks) ---------
 __device__ __host__ inline int quad_code(const double* om) {
@@ -499,8 +615,7 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
                            double* phi_out, double* si_phi, void* workspace,
                            int64_t workspace_bytes, void* sweep_ws, int64_t sweep_ws_bytes,
                            const dlrsn_comm* comm, dlrsn_step_info* info, dlrsn_stream_t stream) {
-  cudaStream_t st = as_stream(stream);
-  void* s = stream;
+  const cudaStream_t st0 = as_stream(stream);
   const int r = p->rank, no = p->n_omega, nx = ops->nx, ny = ops->ny;
   DLRSN_REQUIRE(r >= 1 && r <= DLRSN_MAX_RANK, "rank %d outside [1, %d]", r, DLRSN_MAX_RANK);
   DLRSN_REQUIRE(r <= no, "rank %d exceeds the %d available nodes", r, no);
@@ -522,14 +637,19 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
   const int64_t N = 4 * (int64_t)nc;
   memset(info, 0, sizeof(*info));
   info->error_index = -1;
-  Readback rb;
   const int nl = (r - rank_id + world - 1) / world;  // this rank's directions
   const int G = nl;                                  // single-direction groups
   // full-rank fast path of the angular update: one-CTA weighted CholQR2
   const bool ang_fast = r <= 32 && dlrsn_cholqr2_small_smem(no, r) <= 200 * 1024;
+  StepStatus* hs = nullptr;
+  DLRSN_RET(status_block(&hs));
+  double* P[2] = {b.phi0, b.phi1};
 
-  // ---- 0. control words and constants: one launch ------------------------------
-  {
+  // ---- the step as segments of device work, each closed by the packed
+  // status readback (so a segment is one host synchronisation) ------------
+  // head: constants, DEIM, closure weights, input checks, plan, rhs
+  auto enqueue_head = [&](cudaStream_t st) -> int {
+    void* s = st;
     InitArgs ia;
     ia.flags = b.flags;
     ia.statw = b.statw;
@@ -546,56 +666,49 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     ia.ly = ops->ny * ops->dy;
     init_kernel<<<1, 96, 0, st>>>(ia);
     DLRSN_CHECK_LAUNCH("init_kernel");
-  }
-
-  // ---- 1. DEIM, closure weights, input checks (reported at the readback) ----
-  DLRSN_RET(dlrsn_deim(no, r, b.Wk, W, b.err_idx + 1, b.Lhat, b.U, b.err_idx, s));
-  DLRSN_RET(dlrsn_what_solve(r, 1, b.Lhat, b.U, beta, b.closure, 1, s));
-  sigma_check_kernel<<<std::min(1024, (nc + 255) / 256), 256, 0, st>>>(nc, sigma_t, sigma_s, b.flags);
-  DLRSN_CHECK_LAUNCH("sigma_check_kernel");
-  if (p->check_state) {
-    DLRSN_RET(dlrsn_mgram(ops, r, r, X, r, X, r, nullptr, b.G, b.part, s));
-    DLRSN_RET(wgram(no, r, W, p->weights_dev, b.wpart, b.wg, st));
-    ortho_residual_kernel<<<1, 256, 0, st>>>(r, b.G, b.wg, b.chk_in);
-    DLRSN_CHECK_LAUNCH("ortho_residual_kernel");
-  }
-  const int width = world > 1 ? comm->gather_width : 1;
-  plan_kernel<<<1, DLRSN_MAX_RANK, 0, st>>>(r, no, world, rank_id, b.err_idx, b.err_idx + 1, p->omegas_dev,
-                                b.closure, b.idx, b.groups, b.quads, b.mine, b.place, N, width,
-                                b.cw_local);
-  DLRSN_CHECK_LAUNCH("plan_kernel");
-
-  // ---- 2. evaluate_rows, scalar_flux, rhs (dlr_sn.py:110-121) ---------------
-  ks_kernel<<<1, 256, 0, st>>>(r, S, W, b.idx, beta, b.K, b.Sb, p->omegas_dev, b.om_sel);
-  DLRSN_CHECK_LAUNCH("ks_kernel");
-  DLRSN_RET(dlrsn_rowmix(N, r, r, X, r, b.K, r, 0.0, b.psi_time, r, s));
-  DLRSN_RET(dlrsn_rowmix(N, r, 1, X, r, b.Sb, 1, 0.0, b.phi0, 1, s));
-  DLRSN_RET(dlrsn_cells_to_sk4(ops, sigma_t, b.sig4, s));
-  const double* pt_local = b.psi_time;
-  int ld_pt = r;
-  if (world > 1 && nl > 0) {
-    gather_cols_kernel<<<grid_n(N * nl), 256, 0, st>>>(N, r, nl, b.mine, b.psi_time, b.psi);
-    DLRSN_CHECK_LAUNCH("gather_cols_kernel");
-    pt_local = b.psi;
-    ld_pt = nl;
-  }
-  if (nl > 0)
-    DLRSN_RET(dlrsn_rhs_build(ops, nl, b.quads, q, p->inv_cdt, pt_local, ld_pt, nullptr, 1,
-                              b.rhs_sk, s));
-  DLRSN_RET(dlrsn_scatter_source(ops, b.phi0, sigma_s, b.scat, b.flags + 1, s));
-
-  // ---- 3. source iteration (transport_sn.py:408-447), batched ---------------
-  // Iterations are enqueued in batches without a host round trip; the
+    // 1. DEIM, closure weights, input checks (reported at the readback)
+    DLRSN_RET(dlrsn_deim(no, r, b.Wk, W, b.err_idx + 1, b.Lhat, b.U, b.err_idx, s));
+    DLRSN_RET(dlrsn_what_solve(r, 1, b.Lhat, b.U, beta, b.closure, 1, s));
+    sigma_check_kernel<<<std::min(1024, (nc + 255) / 256), 256, 0, st>>>(nc, sigma_t, sigma_s,
+                                                                         b.flags);
+    DLRSN_CHECK_LAUNCH("sigma_check_kernel");
+    if (p->check_state) {
+      DLRSN_RET(dlrsn_mgram(ops, r, r, X, r, X, r, nullptr, b.G, b.part, s));
+      DLRSN_RET(wgram(no, r, W, p->weights_dev, b.wpart, b.wg, st));
+      ortho_residual_kernel<<<1, 256, 0, st>>>(r, b.G, b.wg, b.chk_in);
+      DLRSN_CHECK_LAUNCH("ortho_residual_kernel");
+    }
+    const int width = world > 1 ? comm->gather_width : 1;
+    plan_kernel<<<1, DLRSN_MAX_RANK, 0, st>>>(r, no, world, rank_id, b.err_idx, b.err_idx + 1,
+                                              p->omegas_dev, b.closure, b.idx, b.groups, b.quads,
+                                              b.mine, b.place, N, width, b.cw_local);
+    DLRSN_CHECK_LAUNCH("plan_kernel");
+    // 2. evaluate_rows, scalar_flux, rhs (dlr_sn.py:110-121)
+    ks_kernel<<<1, 256, 0, st>>>(r, S, W, b.idx, beta, b.K, b.Sb, p->omegas_dev, b.om_sel);
+    DLRSN_CHECK_LAUNCH("ks_kernel");
+    DLRSN_RET(dlrsn_rowmix(N, r, r, X, r, b.K, r, 0.0, b.psi_time, r, s));
+    DLRSN_RET(dlrsn_rowmix(N, r, 1, X, r, b.Sb, 1, 0.0, b.phi0, 1, s));
+    DLRSN_RET(dlrsn_cells_to_sk4(ops, sigma_t, b.sig4, s));
+    const double* pt_local = b.psi_time;
+    int ld_pt = r;
+    if (world > 1 && nl > 0) {
+      gather_cols_kernel<<<grid_n(N * nl), 256, 0, st>>>(N, r, nl, b.mine, b.psi_time, b.psi);
+      DLRSN_CHECK_LAUNCH("gather_cols_kernel");
+      pt_local = b.psi;
+      ld_pt = nl;
+    }
+    if (nl > 0)
+      DLRSN_RET(dlrsn_rhs_build(ops, nl, b.quads, q, p->inv_cdt, pt_local, ld_pt, nullptr, 1,
+                                b.rhs_sk, s));
+    DLRSN_RET(dlrsn_scatter_source(ops, b.phi0, sigma_s, b.scat, b.flags + 1, s));
+    return DLRSN_OK;
+  };
+  // 3. source iterations it_from..it_to (transport_sn.py:408-447): the
   // convergence test runs on the device (si_decide) and iterations past it
-  // return at once.  The Galerkin side is enqueued speculatively behind each
-  // batch, so a step normally costs one host synchronisation.
-  double* P[2] = {b.phi0, b.phi1};
-  int it_next = 1;
-  int batch = g_si_hint > 0 ? g_si_hint + 1 : 8;
-  bool pre_checked = false;
-  for (;;) {
-    const int it_end = std::min(p->si_max_iters, it_next + batch - 1);
-    for (int it = it_next; it <= it_end; ++it) {
+  // return at once; then the converged flux / swept columns are selected
+  auto enqueue_si = [&](cudaStream_t st, int it_from, int it_to) -> int {
+    void* s = st;
+    for (int it = it_from; it <= it_to; ++it) {
       const double* phi = P[(it - 1) & 1];
       double* phin = P[it & 1];
       if (nl > 0)
@@ -620,12 +733,9 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
                                     b.red_ws, b.ctl, it, p->si_tol, b.flags + 1, st));
       }
     }
-    it_next = it_end + 1;
     si_select_kernel<<<grid_n(N), 256, 0, st>>>(N, b.ctl, b.phi0, b.phi1, si_phi);
     DLRSN_CHECK_LAUNCH("si_select_kernel");
-
-    // swept columns in the canonical layout (all ranks: allgather)
-    if (world > 1) {
+    if (world > 1) {  // swept columns of all ranks (allgather), canonical layout
       if (nl > 0)
         DLRSN_RET(dlrsn_sk_to_canonical(ops, nl, b.quads, b.psi_sk, comm->gather_send,
                                         comm->gather_width, s));
@@ -639,182 +749,182 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     } else {
       DLRSN_RET(dlrsn_sk_to_canonical(ops, r, b.quads, b.psi_sk, b.psi, r, s));
     }
+    return DLRSN_OK;
+  };
+  // 4. Galerkin side (dlr_sn.py:123-150) with the chosen Gram-Schmidt paths
+  auto enqueue_tail = [&](cudaStream_t st, int exact, int exact_w, bool reset) -> int {
+    void* s = st;
+    if (reset) {
+      DLRSN_TRY_CUDA(cudaMemsetAsync(b.statw, 0, sizeof(int), st));
+      DLRSN_TRY_CUDA(cudaMemsetAsync(b.statx, 0, sizeof(int), st));
+    }
+    if (!exact) {
+      DLRSN_RET(dlrsn_mgram(ops, r, r, b.psi, r, b.psi, r, nullptr, b.G, b.part, s));
+      DLRSN_RET(dlrsn_chol_upper(r, b.G, b.R1, b.R1inv, b.ratio, b.cholflag, s));
+      DLRSN_RET(dlrsn_rowmix(N, r, r, b.psi, r, b.R1inv, r, 0.0, b.X1, r, s));
+      DLRSN_RET(dlrsn_mgram(ops, r, r, b.X1, r, b.X1, r, nullptr, b.G, b.part, s));
+      DLRSN_RET(dlrsn_chol_upper(r, b.G, b.R2, b.R2inv, b.ratio2, b.cholflag + 1, s));
+      DLRSN_RET(dlrsn_rowmix(N, r, r, b.X1, r, b.R2inv, r, 0.0, X_new, r, s));
+    } else {
+      DLRSN_RET(dlrsn_cgs2((int)N, r, b.psi, r, X_new, r, b.Rtot, b.defx, 1, nullptr, ops, 1,
+                           r + 8, b.up->sexp, b.up->extent, b.cgsws, b.statx, 1, s));
+    }
+    DLRSN_RET(dlrsn_project(ops, r, X_new, X, sigma_t, sigma_s, q, b.proj, b.part, s));
+    qall_kernel<<<1, 256, 0, st>>>(r, S, b.proj + 6 * r * r, b.proj + 7 * r * r, W, b.idx,
+                                   p->inv_cdt, b.T, b.qall);
+    DLRSN_CHECK_LAUNCH("qall_kernel");
+    DLRSN_TRY_CUDA(cudaMemsetAsync(b.rowstat, 0, (r + 1) * sizeof(int), st));
+    DLRSN_RET(dlrsn_row_inverse(r, r, b.proj, b.om_sel, b.Binv, nullptr, b.rowstat, s));
+    DLRSN_RET(dlrsn_row_combine(r, r, b.Binv, b.proj + 5 * r * r, b.qall, b.closure, b.L,
+                                b.lbar, b.rowstat + r, s));
+    DLRSN_RET(dlrsn_what_solve(r, r, b.Lhat, b.U, b.L, b.gamma, 0, s));
+    DLRSN_RET(dlrsn_rowmix(no, r, r, W, r, b.gamma, r, 0.0, b.lfull, r, s));
+    if (!exact_w)
+      DLRSN_RET(dlrsn_cholqr2_small(no, r, b.lfull, r, p->weights_dev, W_new, r, b.Rang,
+                                    b.ratiow, b.cholw, b.defw, s));
+    else
+      DLRSN_RET(dlrsn_cgs2(no, r, b.lfull, r, W_new, r, b.Rang, b.defw, 0, p->weights_dev,
+                           nullptr, 0, r + 8, b.up->aexp, p->omegas_dev, b.cgsws, b.statw, 1, s));
+    DLRSN_RET(wgram(no, r, W_new, p->weights_dev, b.wpart, b.wg, st));
+    finish_kernel<<<1, 256, 0, st>>>(r, b.Rang, b.wg, S_new, beta_new);
+    DLRSN_CHECK_LAUNCH("finish_kernel");
+    if (p->check_state) {
+      DLRSN_RET(dlrsn_mgram(ops, r, r, X_new, r, X_new, r, nullptr, b.G, b.part, s));
+      ortho_residual_kernel<<<1, 256, 0, st>>>(r, b.G, b.wg, b.chk_out);
+      DLRSN_CHECK_LAUNCH("ortho_residual_kernel");
+    }
+    DLRSN_RET(dlrsn_rowmix(N, r, 1, X_new, r, b.lbar, 1, 0.0, phi_out, 1, s));
+    return enqueue_status(st, b, r, hs);
+  };
 
-    // ---- 4. Galerkin side (dlr_sn.py:123-150): speculative CholQR2 ----------
-    int exact = p->gs_method == 1 ? 1 : 0;
-    int exact_w = ang_fast ? 0 : 1;
-    for (int attempt = 0; attempt < 3; ++attempt) {
-      if (attempt > 0) {
-        DLRSN_TRY_CUDA(cudaMemsetAsync(b.statw, 0, sizeof(int), st));
-        DLRSN_TRY_CUDA(cudaMemsetAsync(b.statx, 0, sizeof(int), st));
+  int exact = p->gs_method == 1 ? 1 : 0;
+  int exact_w = ang_fast ? 0 : 1;
+  const int batch0 = g_si_hint > 0 ? g_si_hint + 1 : 8;
+  int it_next = std::min(p->si_max_iters, batch0) + 1;
+  // ---- segment 1 (the whole step in the common case): replayed as a CUDA
+  // graph when the same buffers come back (world 1; see graph_cache)
+  {
+    auto seg1 = [&](cudaStream_t st) -> int {
+      DLRSN_RET(enqueue_head(st));
+      DLRSN_RET(enqueue_si(st, 1, it_next - 1));
+      return enqueue_tail(st, exact, exact_w, false);
+    };
+    GraphKey key;
+    const bool graphed = world == 1 && graphs_enabled() && !sweep_timing_enabled();
+    if (graphed) {
+      key.set(ops, p, X, S, W, beta, sigma_t, sigma_s, q, X_new, S_new, W_new, beta_new, phi_out,
+              si_phi, workspace, sweep_ws, sweep_ws_bytes, batch0, exact, exact_w);
+      DLRSN_RET(graph_run(key, seg1, st0));
+    } else {
+      DLRSN_RET(seg1(st0));
+    }
+  }
+  DLRSN_TRY_CUDA(cudaStreamSynchronize(st0));
+  // errors of the reference's order (dlr_sn.py:99-109)
+  if (hs->err_idx[0] >= 0) {  // InterpolationError (lowrank.py:192-199)
+    info->error_index = hs->err_idx[0];
+    set_error("interpolation residual vanished; basis is rank deficient");
+    return DLRSN_EINTERP;
+  }
+  for (int d = 0; d < r; ++d) info->angle_indices[d] = hs->err_idx[d + 1];
+  if (hs->flags[0]) {
+    set_error("pseudo absorption sigma_t - sigma_s must stay positive");
+    return DLRSN_EINVAL;
+  }
+  info->check_in[0] = hs->chk_in[0];
+  info->check_in[1] = hs->chk_in[1];
+  if (p->check_state && (hs->chk_in[0] > 1e-10 || hs->chk_in[1] > 1e-10)) {
+    set_error("factor orthonormality violated: spatial %.2e, angular %.2e", hs->chk_in[0],
+              hs->chk_in[1]);
+    return DLRSN_EINVAL;
+  }
+  // ---- further segments: more iterations (the batch fell short) or an
+  // exact Gram-Schmidt pass (a CholQR2 guard failed) -- rare, not graphed
+  int batch = batch0;
+  for (int guard = 0; guard < 1 << 20; ++guard) {
+    for (int d = 0; d < r; ++d) info->closure[d] = hs->closure[d];
+    info->residual = hs->ctl.change;
+    if (!hs->ctl.done) {
+      if (it_next > p->si_max_iters) {
+        info->iterations = p->si_max_iters;
+        set_error("source iteration did not converge (iterations=%d, residual=%.3e)",
+                  p->si_max_iters, hs->ctl.change);
+        return DLRSN_EITER;
       }
-      if (!exact) {
-        DLRSN_RET(dlrsn_mgram(ops, r, r, b.psi, r, b.psi, r, nullptr, b.G, b.part, s));
-        DLRSN_RET(dlrsn_chol_upper(r, b.G, b.R1, b.R1inv, b.ratio, b.cholflag, s));
-        DLRSN_RET(dlrsn_rowmix(N, r, r, b.psi, r, b.R1inv, r, 0.0, b.X1, r, s));
-        DLRSN_RET(dlrsn_mgram(ops, r, r, b.X1, r, b.X1, r, nullptr, b.G, b.part, s));
-        DLRSN_RET(dlrsn_chol_upper(r, b.G, b.R2, b.R2inv, b.ratio2, b.cholflag + 1, s));
-        DLRSN_RET(dlrsn_rowmix(N, r, r, b.X1, r, b.R2inv, r, 0.0, X_new, r, s));
-      } else {
-        DLRSN_RET(dlrsn_cgs2((int)N, r, b.psi, r, X_new, r, b.Rtot, b.defx, 1, nullptr, ops, 1,
-                             r + 8, b.up->sexp, b.up->extent, b.cgsws, b.statx, 1, s));
+      batch = std::max(2, batch / 2);
+      const int it_end = std::min(p->si_max_iters, it_next + batch - 1);
+      DLRSN_RET(enqueue_si(st0, it_next, it_end));
+      it_next = it_end + 1;
+      DLRSN_RET(enqueue_tail(st0, exact, exact_w, true));
+      DLRSN_TRY_CUDA(cudaStreamSynchronize(st0));
+      continue;
+    }
+    info->iterations = hs->ctl.iters;
+    // batch hint: the iteration count, decaying by one per step (stable
+    // batches keep the graph keys stable; a shortfall costs one more segment)
+    g_si_hint = std::max(hs->ctl.iters, g_si_hint - 1);
+    if (!exact) {
+      // CholQR's R_kk is accurate to ~eps/rel^2: keep it only when every
+      // column retains >= 1e-6 of its M-norm and sits 100x above the
+      // reference's deficiency threshold 1e-12 max(|v|, 1) (angular.py:137)
+      bool ok = hs->cholflag[0] == 0;
+      for (int k = 0; k < r && ok; ++k) ok = hs->ratio[k] >= 1e-6 && hs->ratio[r + k] >= 1e-10;
+      if (!ok) {
+        info->gs_fallback |= 1;
+        exact = 1;
+        DLRSN_RET(enqueue_tail(st0, exact, exact_w, true));
+        DLRSN_TRY_CUDA(cudaStreamSynchronize(st0));
+        continue;
       }
-      DLRSN_RET(dlrsn_project(ops, r, X_new, X, sigma_t, sigma_s, q, b.proj, b.part, s));
-      qall_kernel<<<1, 256, 0, st>>>(r, S, b.proj + 6 * r * r, b.proj + 7 * r * r, W, b.idx,
-                                     p->inv_cdt, b.T, b.qall);
-      DLRSN_CHECK_LAUNCH("qall_kernel");
-      DLRSN_TRY_CUDA(cudaMemsetAsync(b.rowstat, 0, (r + 1) * sizeof(int), st));
-      DLRSN_RET(dlrsn_row_inverse(r, r, b.proj, b.om_sel, b.Binv, nullptr, b.rowstat, s));
-      DLRSN_RET(dlrsn_row_combine(r, r, b.Binv, b.proj + 5 * r * r, b.qall, b.closure, b.L,
-                                  b.lbar, b.rowstat + r, s));
-      DLRSN_RET(dlrsn_what_solve(r, r, b.Lhat, b.U, b.L, b.gamma, 0, s));
-      DLRSN_RET(dlrsn_rowmix(no, r, r, W, r, b.gamma, r, 0.0, b.lfull, r, s));
-      if (!exact_w)
-        DLRSN_RET(dlrsn_cholqr2_small(no, r, b.lfull, r, p->weights_dev, W_new, r, b.Rang,
-                                      b.ratiow, b.cholw, b.defw, s));
-      else
-        DLRSN_RET(dlrsn_cgs2(no, r, b.lfull, r, W_new, r, b.Rang, b.defw, 0, p->weights_dev,
-                             nullptr, 0, r + 8, b.up->aexp, p->omegas_dev, b.cgsws, b.statw, 1,
-                             s));
-      DLRSN_RET(wgram(no, r, W_new, p->weights_dev, b.wpart, b.wg, st));
-      finish_kernel<<<1, 256, 0, st>>>(r, b.Rang, b.wg, S_new, beta_new);
-      DLRSN_CHECK_LAUNCH("finish_kernel");
-      if (p->check_state) {
-        DLRSN_RET(dlrsn_mgram(ops, r, r, X_new, r, X_new, r, nullptr, b.G, b.part, s));
-        ortho_residual_kernel<<<1, 256, 0, st>>>(r, b.G, b.wg, b.chk_out);
-        DLRSN_CHECK_LAUNCH("ortho_residual_kernel");
-      }
-      DLRSN_RET(dlrsn_rowmix(N, r, 1, X_new, r, b.lbar, 1, 0.0, phi_out, 1, s));
-
-      // ---- the readback: pre-iteration checks, iteration state, tail status
-      std::vector<int> err_idx(r + 1);
-      std::vector<double> closure(r);
-      int flags[8] = {0};
-      double chk[2] = {0.0, 0.0};
-      SiCtl ctl;
-      std::vector<double> ratio(2 * r);
-      int cholflag[2] = {0, 0};
-      std::vector<int> rowstat(r + 1), defw(r), defx(r, 0);
-      int statw = 0, statx = 0;
-      double chko[2] = {0.0, 0.0};
-      if (!pre_checked) {
-        rb.add(b.err_idx, (r + 1) * sizeof(int), err_idx.data());
-        rb.add(b.flags, sizeof(flags), flags);
-        if (p->check_state) rb.add(b.chk_in, 2 * sizeof(double), chk);
-      }
-      rb.add(b.ctl, sizeof(SiCtl), &ctl);
-      rb.add(b.closure, r * sizeof(double), closure.data());
-      rb.add(b.rowstat, (r + 1) * sizeof(int), rowstat.data());
-      rb.add(b.defw, r * sizeof(int), defw.data());
-      rb.add(b.statw, sizeof(int), &statw);
-      if (!exact) {
-        rb.add(b.ratio, 2 * r * sizeof(double), ratio.data());
-        rb.add(b.cholflag, sizeof(cholflag), cholflag);
-      } else {
-        rb.add(b.defx, r * sizeof(int), defx.data());
-        rb.add(b.statx, sizeof(int), &statx);
-      }
-      std::vector<double> ratiow(2 * r);
-      int cholw[2] = {0, 0};
-      if (!exact_w) {
-        rb.add(b.ratiow, 2 * r * sizeof(double), ratiow.data());
-        rb.add(b.cholw, sizeof(cholw), cholw);
-      }
-      if (p->check_state) rb.add(b.chk_out, sizeof(chko), chko);
-      DLRSN_RET(rb.run(st, b.rbdev));
-
-      if (!pre_checked) {  // errors of the reference's order (dlr_sn.py:99-109)
-        pre_checked = true;
-        if (err_idx[0] >= 0) {  // InterpolationError (lowrank.py:192-199)
-          info->error_index = err_idx[0];
-          set_error("interpolation residual vanished; basis is rank deficient");
-          return DLRSN_EINTERP;
-        }
-        for (int d = 0; d < r; ++d) info->angle_indices[d] = err_idx[d + 1];
-        if (flags[0]) {
-          set_error("pseudo absorption sigma_t - sigma_s must stay positive");
-          return DLRSN_EINVAL;
-        }
-        info->check_in[0] = chk[0];
-        info->check_in[1] = chk[1];
-        if (p->check_state && (chk[0] > 1e-10 || chk[1] > 1e-10)) {
-          set_error("factor orthonormality violated: spatial %.2e, angular %.2e", chk[0], chk[1]);
-          return DLRSN_EINVAL;
-        }
-      }
-      for (int d = 0; d < r; ++d) info->closure[d] = closure[d];
-      info->residual = ctl.change;
-      if (!ctl.done) {
-        if (it_next > p->si_max_iters) {
-          info->iterations = p->si_max_iters;
-          set_error("source iteration did not converge (iterations=%d, residual=%.3e)",
-                    p->si_max_iters, ctl.change);
-          return DLRSN_EITER;
-        }
-        batch = std::max(2, batch / 2);
-        goto next_batch;  // the tail ran on an unconverged flux: iterate on
-      }
-      info->iterations = ctl.iters;
-      g_si_hint = ctl.iters;
-      if (!exact) {
-        // CholQR's R_kk is accurate to ~eps/rel^2: keep it only when every
-        // column retains >= 1e-6 of its M-norm and sits 100x above the
-        // reference's deficiency threshold 1e-12 max(|v|, 1) (angular.py:137)
-        bool ok = cholflag[0] == 0;
-        for (int k = 0; k < r && ok; ++k) ok = ratio[k] >= 1e-6 && ratio[r + k] >= 1e-10;
-        if (!ok) {
-          info->gs_fallback |= 1;
-          exact = 1;
-          continue;
-        }
-        info->spatial_deficiency = 0;
-      } else {
-        if (statx) {
-          set_error("ran out of completion vectors during orthonormalization");
-          return DLRSN_ECOMPLETION;
-        }
-        int nd = 0;
-        for (int k = 0; k < r; ++k) nd += defx[k] != 0;
-        info->spatial_deficiency = nd;
-      }
-      if (!exact_w) {  // same guard for the angular CholQR2 (angular.py:137 threshold)
-        bool ok = cholw[0] == 0 && cholw[1] == 0;
-        for (int k = 0; k < r && ok; ++k) ok = ratiow[k] >= 1e-6 && ratiow[r + k] >= 1e-10;
-        if (!ok) {
-          info->gs_fallback |= 2;
-          exact_w = 1;
-          continue;
-        }
-      }
-      for (int d = 0; d < r; ++d)
-        if (rowstat[d]) {
-          info->error_index = d;
-          set_error("singular reduced transport operator at node %d", d);
-          return DLRSN_ESINGULAR;
-        }
-      if (rowstat[r]) {
-        set_error("singular closure-coupled reduced system");
-        return DLRSN_ESINGULAR;
-      }
-      if (statw) {
+      info->spatial_deficiency = 0;
+    } else {
+      if (hs->statx) {
         set_error("ran out of completion vectors during orthonormalization");
         return DLRSN_ECOMPLETION;
       }
-      int na = 0;
-      for (int k = 0; k < r; ++k) na += defw[k] != 0;
-      info->angular_deficiency = na;
-      info->check_out[0] = chko[0];
-      info->check_out[1] = chko[1];
-      if (p->check_state && (chko[0] > 1e-10 || chko[1] > 1e-10)) {
-        set_error("factor orthonormality violated: spatial %.2e, angular %.2e", chko[0], chko[1]);
-        return DLRSN_EINVAL;
-      }
-      return DLRSN_OK;
+      int nd = 0;
+      for (int k = 0; k < r; ++k) nd += hs->defx[k] != 0;
+      info->spatial_deficiency = nd;
     }
-    set_error("internal: Gram-Schmidt fallback did not run");
-    return DLRSN_ECUDA;
-  next_batch:;
+    if (!exact_w) {  // same guard for the angular CholQR2 (angular.py:137 threshold)
+      bool ok = hs->cholw[0] == 0 && hs->cholw[1] == 0;
+      for (int k = 0; k < r && ok; ++k) ok = hs->ratiow[k] >= 1e-6 && hs->ratiow[r + k] >= 1e-10;
+      if (!ok) {
+        info->gs_fallback |= 2;
+        exact_w = 1;
+        DLRSN_RET(enqueue_tail(st0, exact, exact_w, true));
+        DLRSN_TRY_CUDA(cudaStreamSynchronize(st0));
+        continue;
+      }
+    }
+    for (int d = 0; d < r; ++d)
+      if (hs->rowstat[d]) {
+        info->error_index = d;
+        set_error("singular reduced transport operator at node %d", d);
+        return DLRSN_ESINGULAR;
+      }
+    if (hs->rowstat[r]) {
+      set_error("singular closure-coupled reduced system");
+      return DLRSN_ESINGULAR;
+    }
+    if (hs->statw) {
+      set_error("ran out of completion vectors during orthonormalization");
+      return DLRSN_ECOMPLETION;
+    }
+    int na = 0;
+    for (int k = 0; k < r; ++k) na += hs->defw[k] != 0;
+    info->angular_deficiency = na;
+    info->check_out[0] = hs->chk_out[0];
+    info->check_out[1] = hs->chk_out[1];
+    if (p->check_state && (hs->chk_out[0] > 1e-10 || hs->chk_out[1] > 1e-10)) {
+      set_error("factor orthonormality violated: spatial %.2e, angular %.2e", hs->chk_out[0],
+                hs->chk_out[1]);
+      return DLRSN_EINVAL;
+    }
+    return DLRSN_OK;
   }
+  set_error("internal: step did not settle");
+  return DLRSN_ECUDA;
 }
 
 }  // extern "C"

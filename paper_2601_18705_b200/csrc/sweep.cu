@@ -959,6 +959,14 @@ int dlrsn_sweep(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int 
                       workspace, workspace_bytes, max_ctas, nullptr, as_stream(stream));
 }
 
+}  // extern "C"
+
+namespace dlrsn {
+bool sweep_timing_enabled() { return g_timing; }
+}  // namespace dlrsn
+
+extern "C" {
+
 int dlrsn_sweep_timing(int enable) {
   g_timing = enable != 0;
   g_timers_used = 0;

@@ -97,6 +97,8 @@ __device__ __forceinline__ void solve4(double* a, double* b, double* x) {
 
 int launch_sweep_ws(const SweepArgs& a, int max_ctas, cudaStream_t st);
 
+bool sweep_timing_enabled();  // dlrsn_sweep_timing on (the step then skips graphs)
+
 // internal entry points of the step (step.cu); the public C-ABI calls pass
 // skip / ctl = nullptr
 int sweep_launch(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int dw,
