@@ -197,10 +197,13 @@ def main():
 
     comm = DirectionComm.from_default_group()  # None at N=1; NCCL direction sharding at N>1
 
+    Tbox = [T]
+
     def one_step(state, lin):
-        state, info = step_collocation(dp.grid, lin, dp.quad, state, si_tol=1e-8, use_dsa=False,
-                                       check_state=True, comm=comm)
-        lin = dp.advance(lin, info.phi, T)
+        # step_collocation + the step boundary (T update, re-linearisation)
+        # in one native call (DeviceProblem.step)
+        state, lin, Tbox[0], info = dp.step(state, lin, Tbox[0], si_tol=1e-8, check_state=True,
+                                            comm=comm)
         return state, lin, info
 
     for _ in range(args.warmup):
@@ -261,7 +264,7 @@ def main():
             traffic = None
 
     # ---- end-to-end: public API with HOST (pinned) buffers each step -------
-    e2e = measure_e2e(dp, state, T, lin, max(1, min(args.steps, 5)), comm)
+    e2e = measure_e2e(dp, state, Tbox[0], lin, max(1, min(args.steps, 5)), comm)
 
     # ---- full-SN comparison sweep (config 2: all 1024 directions) ----------
     full = measure_full_sn(dp, comm) if args.full_sn else None

@@ -275,6 +275,30 @@ int dlrsn_cgs2(int n, int m, const double* cols, int ldc, double* Q, int ldq, do
 
 /* ---- One whole step (dlr_sn.py:86-151) ----------------------------------- */
 
+/* Optional fused step boundary of a driver loop (driver.py:486-487,532-534):
+ * after the step, T_out = the updated temperature of the finished step and
+ * (sigma_a .. denom) = the next step's linearisation (dlrsn_advance_relinearize
+ * out of place: T_in and the *_in fields are not written, so a failing step
+ * leaves the caller's state untouched). */
+typedef struct dlrsn_advance {
+  int n;                     /* cells */
+  const double* T_in;
+  const double* sigma_a_in;
+  const double* denom_in;
+  const double* sigma_a0;
+  double opacity_power;
+  const double* rho_cv;
+  double dt, c, a_r, t_floor;
+  const double* ss_phys;     /* optional */
+  const double* q_ext;       /* optional */
+  double* T_out;
+  double* sigma_a;
+  double* sigma_t;
+  double* sigma_s;
+  double* q;
+  double* denom;
+} dlrsn_advance;
+
 typedef struct dlrsn_step_params {
   int rank;                  /* r <= DLRSN_MAX_RANK */
   int n_omega;               /* quadrature size */
@@ -287,6 +311,7 @@ typedef struct dlrsn_step_params {
   int check_state;           /* DlrState.check on input and output */
   int gs_method;             /* 0: CholQR2 guarded by exact CGS2, 1: exact CGS2 */
   int sweep_dw;              /* sweep group width (0 = 1) */
+  const dlrsn_advance* advance; /* optional fused T update + re-linearisation (NULL: none) */
 } dlrsn_step_params;
 
 typedef struct dlrsn_step_info { /* HOST, filled by the call */

@@ -37,11 +37,19 @@ class CellOps(ctypes.Structure):
 MAX_RANK = 128
 
 
+class Advance(ctypes.Structure):  # struct dlrsn_advance
+    _fields_ = [("n", c_int), ("T_in", c_vp), ("sigma_a_in", c_vp), ("denom_in", c_vp),
+                ("sigma_a0", c_vp), ("opacity_power", c_dbl), ("rho_cv", c_vp), ("dt", c_dbl),
+                ("c", c_dbl), ("a_r", c_dbl), ("t_floor", c_dbl), ("ss_phys", c_vp),
+                ("q_ext", c_vp), ("T_out", c_vp), ("sigma_a", c_vp), ("sigma_t", c_vp),
+                ("sigma_s", c_vp), ("q", c_vp), ("denom", c_vp)]
+
+
 class StepParams(ctypes.Structure):
     _fields_ = [("rank", c_int), ("n_omega", c_int), ("omegas_host", c_vp), ("omegas_dev", c_vp),
                 ("weights_dev", c_vp), ("inv_cdt", c_dbl), ("si_tol", c_dbl),
                 ("si_max_iters", c_int), ("check_state", c_int), ("gs_method", c_int),
-                ("sweep_dw", c_int)]
+                ("sweep_dw", c_int), ("advance", c_vp)]
 
 
 class StepInfo(ctypes.Structure):

@@ -78,8 +78,8 @@ __global__ void update_temperature_kernel(int n, const double* __restrict__ phi,
   T[i] = new_temperature(p, T0[i], sa[i], den[i], dt, c, a_r, t_floor);
 }
 
-__global__ void advance_kernel(int n, const double* __restrict__ phi, double* __restrict__ T,
-                               const double* sa_in, const double* den_in, double* sa,
+__global__ void advance_kernel(int n, const double* __restrict__ phi, const double* T_in,
+                               double* T, const double* sa_in, const double* den_in, double* sa,
                                const double* __restrict__ sa0,
                                double power, const double* __restrict__ rc, double dt, double c,
                                double a_r, double t_floor, const double* __restrict__ ssp,
@@ -89,8 +89,9 @@ __global__ void advance_kernel(int n, const double* __restrict__ phi, double* __
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   // finish the step that produced phi (uses that step's sigma_a / denom)
-  const double Tn = new_temperature(cell_mean4(phi, i), T[i], sa_in[i], den_in[i], dt, c, a_r, t_floor);
-  T[i] = Tn;
+  const double Tn = new_temperature(cell_mean4(phi, i), T_in[i], sa_in[i], den_in[i], dt, c, a_r,
+                                    t_floor);
+  if (T) T[i] = Tn;  // (T may alias T_in: each thread reads its cell first)
   if (T0_out) T0_out[i] = Tn;
   // linearise the next step about the new temperature
   const double s_a = power != 0.0 ? sa0[i] * pow(Tn, power) : sa0[i];
@@ -99,6 +100,17 @@ __global__ void advance_kernel(int n, const double* __restrict__ phi, double* __
   linearize_cell(Tn, s_a, rc[i], dt, c, a_r, ssp ? ssp[i] : 0.0, qe ? qe[i] : 0.0, st[i], ss[i],
                  q[i], den[i], bad);
   if (bad && status) atomicOr(status, 1);
+}
+
+int advance_launch(const dlrsn_advance* av, const double* phi, cudaStream_t st) {
+  const int n = av->n;
+  if (n == 0) return DLRSN_OK;
+  advance_kernel<<<(n + 255) / 256, 256, 0, st>>>(
+      n, phi, av->T_in, nullptr, av->sigma_a_in, av->denom_in, av->sigma_a, av->sigma_a0,
+      av->opacity_power, av->rho_cv, av->dt, av->c, av->a_r, av->t_floor, av->ss_phys, av->q_ext,
+      av->sigma_t, av->sigma_s, av->q, av->denom, av->T_out, nullptr);
+  DLRSN_CHECK_LAUNCH("advance_kernel");
+  return DLRSN_OK;
 }
 
 }  // namespace dlrsn
@@ -156,8 +168,8 @@ int dlrsn_advance_relinearize(int n, const double* phi_dofs, double* T,
   DLRSN_REQUIRE(dt > 0.0, "time step must be positive, got %g", dt);
   if (n == 0) return DLRSN_OK;
   advance_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(
-      n, phi_dofs, T, sigma_a_in, denom_in, sigma_a, sigma_a0, opacity_power, rho_cv, dt, c, a_r,
-      t_floor, ss_phys, q_ext, sigma_t, sigma_s, q, denom, T0_out, status);
+      n, phi_dofs, T, T, sigma_a_in, denom_in, sigma_a, sigma_a0, opacity_power, rho_cv, dt, c,
+      a_r, t_floor, ss_phys, q_ext, sigma_t, sigma_s, q, denom, T0_out, status);
   DLRSN_CHECK_LAUNCH("advance_kernel");
   return DLRSN_OK;
 }

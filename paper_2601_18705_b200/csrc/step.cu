@@ -390,7 +390,8 @@ static int enqueue_status(cudaStream_t st, const StepBufs& b, int r, StepStatus*
 // set and replayed with one graph launch (no per-kernel host cost, no launch
 // gaps).  Everything baked into the graph is part of the key.
 struct GraphKey {
-  unsigned char bytes[sizeof(dlrsn_cellops) + sizeof(dlrsn_step_params) + 24 * sizeof(void*)];
+  unsigned char bytes[sizeof(dlrsn_cellops) + sizeof(dlrsn_step_params) + sizeof(dlrsn_advance) +
+                      24 * sizeof(void*)];
   void set(const dlrsn_cellops* ops, const dlrsn_step_params* p, const void* X, const void* S,
            const void* W, const void* beta, const void* st, const void* ss, const void* q,
            const void* Xn, const void* Sn, const void* Wn, const void* bn, const void* phi,
@@ -402,8 +403,11 @@ struct GraphKey {
     o += sizeof(*ops);
     dlrsn_step_params pp = *p;
     pp.omegas_host = nullptr;  // read on the host only
+    pp.advance = nullptr;      // compared by content below
     memcpy(bytes + o, &pp, sizeof(pp));
     o += sizeof(pp);
+    if (p->advance) memcpy(bytes + o, p->advance, sizeof(dlrsn_advance));
+    o += sizeof(dlrsn_advance);
     const void* ptrs[] = {X, S, W, beta, st, ss, q, Xn, Sn, Wn, bn, phi, siphi, ws, sws};
     memcpy(bytes + o, ptrs, sizeof(ptrs));
     o += sizeof(ptrs);
@@ -794,6 +798,7 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
       DLRSN_CHECK_LAUNCH("ortho_residual_kernel");
     }
     DLRSN_RET(dlrsn_rowmix(N, r, 1, X_new, r, b.lbar, 1, 0.0, phi_out, 1, s));
+    if (p->advance) DLRSN_RET(advance_launch(p->advance, phi_out, st));
     return enqueue_status(st, b, r, hs);
   };
 

@@ -97,7 +97,8 @@ __device__ __forceinline__ void solve4(double* a, double* b, double* x) {
 
 int launch_sweep_ws(const SweepArgs& a, int max_ctas, cudaStream_t st);
 
-bool sweep_timing_enabled();  // dlrsn_sweep_timing on (the step then skips graphs)
+bool sweep_timing_enabled();
+int advance_launch(const dlrsn_advance* av, const double* phi, cudaStream_t st);  // physics.cu  // dlrsn_sweep_timing on (the step then skips graphs)
 
 // internal entry points of the step (step.cu); the public C-ABI calls pass
 // skip / ctl = nullptr

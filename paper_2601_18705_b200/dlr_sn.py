@@ -117,7 +117,7 @@ def project_initial(state, x_new, ops):
 
 def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, use_dsa=True,
                      dsa_penalty="simplified", threads=0, check_state=True, gs_method="cholqr2",
-                     sweep_dw=None, comm=None, engine="native"):
+                     sweep_dw=None, comm=None, engine="native", _advance=None):
     """Advance one linearised step; returns (new DlrState, CollocationStepInfo).
 
     ``engine="native"`` issues the whole step from C++ through the single
@@ -141,7 +141,9 @@ def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, 
         if dsa_penalty not in ("simplified", "collocation"):
             raise ContractViolation(f"unknown dsa penalty variant {dsa_penalty!r}")
         return _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state,
-                            gs_method, sweep_dw, comm)
+                            gs_method, sweep_dw, comm, _advance)
+    if _advance is not None:
+        raise ConfigurationError("the fused step boundary needs the native engine")
     r = state.rank
     # ---- DEIM + closure + input checks: one readback ------------------------
     selection, err_idx = deim_launch(state.W.values)
@@ -409,7 +411,7 @@ def _native_ctx(grid, quad, r, comm):
 
 
 def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_method, sweep_dw,
-                 comm):
+                 comm, advance=None):
     r = state.rank
     no = quad.n_angles
     n = grid.n_dofs
@@ -432,6 +434,7 @@ def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_
     p.si_tol, p.si_max_iters = float(si_tol), int(si_max_iters)
     p.check_state = 1 if check_state else 0
     p.gs_method = 0 if gs_method == "cholqr2" else 1
+    p.advance = ctypes.addressof(advance) if advance is not None else None
     info = _lib.StepInfo()
     hooks = ctx.hooks
     if hooks is not None:

@@ -91,6 +91,52 @@ class DeviceProblem:
                               inv_cdt=1.0 / (k.c * self.spec.dt), constants=k)
 
 
+    def step(self, state, lin, T, *, si_tol=1e-8, si_max_iters=200, check_state=True,
+             gs_method="cholqr2", comm=None):
+        """One DLR step and the step boundary (T update + re-linearisation)
+        in a single native call (the fused form of step_collocation +
+        advance, driver.py:486-487,532-534).  Returns (state, next
+        LinearizedStep, new T tensor, info); T itself is not modified, so a
+        step that raises leaves the caller's state as it was."""
+        from .dlr_sn import step_collocation
+
+        if self.spec.frozen:
+            state, info = step_collocation(self.grid, lin, self.quad, state, si_tol=si_tol,
+                                           si_max_iters=si_max_iters, use_dsa=False,
+                                           check_state=check_state, gs_method=gs_method,
+                                           comm=comm)
+            T = T.clone()
+            return state, self.advance(lin, info.phi, T), T, info
+        n = self.spec.n_cells
+        buf = empty(6, n)
+        sa, den, st, ss, q, T0 = buf.unbind(0)
+        av = self.__dict__.get("_adv")
+        if av is None:
+            k = self.constants
+            av = _lib.Advance()
+            av.n = n
+            av.sigma_a0 = self.sigma_a0.data_ptr()
+            av.opacity_power = float(self.opacity_power)
+            av.rho_cv = self.rho_cv.data_ptr()
+            av.dt, av.c, av.a_r = float(self.spec.dt), float(k.c), float(k.a_r)
+            av.t_floor = float(self.spec.t_floor)
+            av.ss_phys = None if self.ss_phys is None else self.ss_phys.data_ptr()
+            av.q_ext = None if self.q_ext is None else self.q_ext.data_ptr()
+            self._adv = av
+        av.T_in, av.sigma_a_in, av.denom_in = T.data_ptr(), lin.sigma_a.data_ptr(), lin.denom.data_ptr()
+        av.T_out, av.sigma_a, av.sigma_t = T0.data_ptr(), sa.data_ptr(), st.data_ptr()
+        av.sigma_s, av.q, av.denom = ss.data_ptr(), q.data_ptr(), den.data_ptr()
+        state, info = step_collocation(self.grid, lin, self.quad, state, si_tol=si_tol,
+                                       si_max_iters=si_max_iters, use_dsa=False,
+                                       check_state=check_state, gs_method=gs_method, comm=comm,
+                                       _advance=av)
+        k = self.constants
+        nxt = LinearizedStep(sigma_t=st, sigma_s=ss, sigma_a=sa, q=q, T0=T0, denom=den,
+                             rho_cv=self.rho_cv, dt=float(self.spec.dt),
+                             inv_cdt=1.0 / (k.c * self.spec.dt), constants=k)
+        return state, nxt, T0, info
+
+
 def initial_state(dp, X=None, W=None, seed=None, T=None):
     """Seeded random-orthonormal X (M inner product, spatial-monomial
     completion) and W (weighted), S = (X^T M b0) beta^T.
@@ -125,11 +171,15 @@ def run(dp, state, n_steps, *, si_tol=1e-8, si_max_iters=200, check_state=True, 
     lin = dp.linearized(T)
     infos = []
     for _ in range(n_steps):
-        state, info = step_collocation(dp.grid, lin, dp.quad, state, si_tol=si_tol,
-                                       si_max_iters=si_max_iters, use_dsa=False,
-                                       check_state=check_state, gs_method=gs_method,
-                                       engine=engine, comm=comm)
-        lin = dp.advance(lin, info.phi, T)
+        if engine == "native":  # step + boundary in one native call
+            state, lin, T, info = dp.step(state, lin, T, si_tol=si_tol, si_max_iters=si_max_iters,
+                                          check_state=check_state, gs_method=gs_method, comm=comm)
+        else:
+            state, info = step_collocation(dp.grid, lin, dp.quad, state, si_tol=si_tol,
+                                           si_max_iters=si_max_iters, use_dsa=False,
+                                           check_state=check_state, gs_method=gs_method,
+                                           engine=engine, comm=comm)
+            lin = dp.advance(lin, info.phi, T)
         infos.append(info)
         if record is not None:
             record(state, info, T)

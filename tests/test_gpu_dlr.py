@@ -310,3 +310,32 @@ def test_native_step_raises_like_the_reference():
     step2.sigma_s.copy_(step2.sigma_t)
     with pytest.raises(ContractViolation, match="pseudo absorption"):
         step_collocation(grid, step2, quad, st, use_dsa=False)
+
+
+def test_fused_step_boundary_matches_separate_advance():
+    """DeviceProblem.step (step + T update + re-linearisation in one native
+    call, T not modified in place) equals step_collocation followed by
+    DeviceProblem.advance."""
+    from paper_2601_18705_b200 import problems
+    from paper_2601_18705_b200.dlr_sn import step_collocation
+    from paper_2601_18705_b200.driver import DeviceProblem, initial_state
+
+    spec = problems.checkerboard(4, rank=6, n_polar=4, n_azimuthal=8, seed=5)
+    dp = DeviceProblem.from_spec(spec)
+    s1 = s2 = initial_state(dp)
+    T1 = torch.as_tensor(spec.T0, device="cuda").clone()
+    T2 = T1.clone()
+    l1 = dp.linearized(T1)
+    l2 = dp.linearized(T2)
+    for _ in range(3):
+        T_before = T2.clone()
+        s2, l2, T2n, i2 = dp.step(s2, l2, T2, si_tol=1e-12)
+        assert torch.equal(T2, T_before)  # the caller's T is untouched
+        T2 = T2n
+        s1, i1 = step_collocation(dp.grid, l1, dp.quad, s1, si_tol=1e-12, use_dsa=False)
+        l1 = dp.advance(l1, i1.phi, T1)
+        assert i1.iterations == i2.iterations
+        assert torch.equal(T1, T2)
+        for f in ("sigma_t", "sigma_s", "sigma_a", "q", "denom"):
+            assert torch.equal(getattr(l1, f), getattr(l2, f)), f
+        assert torch.equal(s1.X, s2.X) and torch.equal(s1.S, s2.S)
