@@ -635,6 +635,225 @@ __global__ void __launch_bounds__(256, 2) project_kernel(ProjArgs pa, dlrsn_cell
 }
 
 // ---------------------------------------------------------------------------
+// project on the FP64 tensor cores (DMMA m8n8k4) over shared-memory staged
+// cell chunks.  The staging is project_kernel's (i-side rows X, Xold, face
+// jumps u; j-side rows M X, Gx X, Gy X, 1/2 e2 v, 1/2 e2 u, q src.X), with a
+// 20-double row stride so that the fragment loads of a lane quad hit distinct
+// banks.  Warp w owns the 8x8 sub-tile (mt, nt) = (w & 1, (w >> 1) & 1) of
+// all 7 outputs for half hf = w >> 2 of every chunk.  Per cell the MMA k
+// dimension is its 4 dofs (volume terms: px, py, mt, ms, mo); the face terms
+// of a cell pair share one MMA (k = the 2 face dofs of each cell: px, py, jx,
+// jy).  Domain-boundary faces, q-hat and the fixed-order reductions are SIMT.
+constexpr int kPC = 8;    // cells per chunk
+constexpr int kLS = 20;   // row stride (doubles) of the staged planes
+__global__ void __launch_bounds__(256, 2) project_mma_kernel(ProjArgs pa, dlrsn_cellops ops) {
+  constexpr int C = kPC;
+  constexpr int kRow = 4 * kLS;  // one cell's 4 rows
+  __shared__ __align__(16) double sm[C * (6 * kRow + 2 * kRow) + C * 16 + 2 * C];
+  double* sX = sm;               // [C][4][kLS] i-side
+  double* sXo = sX + C * kRow;   // [C][4][kLS] i-side
+  double* sU = sXo + C * kRow;   // [C][4][kLS] i-side: ux0 ux1 uy0 uy1
+  double* sMX = sU + C * kRow;   // [C][4][kLS] j-side
+  double* sGX = sMX + C * kRow;  // [C][4][kLS]
+  double* sGY = sGX + C * kRow;  // [C][4][kLS]
+  double* sF = sGY + C * kRow;   // [C][8][kLS]: (e2x v)x2 (e2y v)x2 (e2x u)x2 (e2y u)x2, halved
+  double* sQ = sF + 2 * C * kRow;  // [C][16]
+  double* sC = sQ + C * 16;        // [C][2]
+  __shared__ double so[64];  // mass 0-15, gx 16-31, gy 32-47, e2x 48-51, e2y 52-55, src 56-59
+  __shared__ double bnd[2][16][17];  // boundary-face parts of px (= jx) and py (= jy)
+  if (threadIdx.x < 16) {
+    so[threadIdx.x] = ops.mass[threadIdx.x];
+    so[16 + threadIdx.x] = ops.gx[threadIdx.x];
+    so[32 + threadIdx.x] = ops.gy[threadIdx.x];
+  } else if (threadIdx.x < 20) {
+    so[48 + threadIdx.x - 16] = ops.e2x[threadIdx.x - 16];
+    so[52 + threadIdx.x - 16] = ops.e2y[threadIdx.x - 16];
+    so[56 + threadIdx.x - 16] = ops.src_row[threadIdx.x - 16];
+  }
+  const double* e2x = so + 48;
+  const double* e2y = so + 52;
+  const int r = pa.r, nx = pa.nx, ny = pa.ny;
+  const int ncell = nx * ny;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3, kk = q & 1, second = q >> 1;
+  const int mt = warp & 1, nt = (warp >> 1) & 1, hf = warp >> 2;
+  const int tiles_j = (r + kTile - 1) / kTile;
+  const int i0 = (blockIdx.y / tiles_j) * kTile, j0 = (blockIdx.y % tiles_j) * kTile;
+  const int c_begin = blockIdx.x * pa.cells_per_block;
+  const int c_end = min(ncell, c_begin + pa.cells_per_block);
+  double acc[7][2];
+#pragma unroll
+  for (int o = 0; o < 7; ++o) acc[o][0] = acc[o][1] = 0.0;
+  double qacc = 0.0;
+  const double* X = pa.X;
+  const int ca = 8 * mt + g, cb = 8 * nt + g;  // fragment columns within the tile
+  // staging item of this thread (C x 16 columns x 2 sides = blockDim): the
+  // global loads of chunk k+1 are issued before chunk k is computed
+  const int side = threadIdx.x / (C * kTile);  // 0: tile-i columns, 1: tile-j columns
+  const int scl = (threadIdx.x % (C * kTile)) / kTile, scol = threadIdx.x % kTile;
+  const int sgcol = (side == 0 ? i0 : j0) + scol;
+  struct Raw {
+    double x[4], xo[4], ax0, ax1, ay0, ay1, qc, st, ss;
+  };
+  auto fetch = [&](int cc0, Raw& w) {
+    const int c = cc0 + scl;
+    const bool live = cc0 < c_end && c < c_end;
+    const int ci = c % nx, cj = c / nx;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      w.x[l] = live ? ldx(X, r, (int64_t)c * 4 + l, sgcol) : 0.0;
+      w.xo[l] = (live && side == 0 && pa.Xold) ? ldx(pa.Xold, r, (int64_t)c * 4 + l, sgcol) : 0.0;
+    }
+    const bool lx = live && ci > 0, ly = live && cj > 0;
+    w.ax0 = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 1, sgcol) : 0.0;
+    w.ax1 = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 3, sgcol) : 0.0;
+    w.ay0 = ly ? ldx(X, r, (int64_t)(c - nx) * 4 + 2, sgcol) : 0.0;
+    w.ay1 = ly ? ldx(X, r, (int64_t)(c - nx) * 4 + 3, sgcol) : 0.0;
+    w.qc = (live && side == 1) ? __ldg(pa.q + c) : 0.0;
+    const bool cst = live && threadIdx.x < C;  // sigma of cell cc0 + threadIdx.x
+    const int cs = cc0 + (int)threadIdx.x;
+    w.st = (cc0 < c_end && threadIdx.x < C && cs < c_end) ? __ldg(pa.sigma_t + cs) : 0.0;
+    w.ss = (cc0 < c_end && threadIdx.x < C && cs < c_end) ? __ldg(pa.sigma_s + cs) : 0.0;
+    (void)cst;
+  };
+  Raw cur;
+  fetch(c_begin, cur);
+  for (int c0 = c_begin; c0 < c_end; c0 += C) {
+    const int nc = min(C, c_end - c0);
+    __syncthreads();  // the previous chunk's fragments are consumed
+    {
+      const double* x = cur.x;
+      const double ux0 = cur.ax0 - x[0], ux1 = cur.ax1 - x[2];
+      const double vx0 = cur.ax0 + x[0], vx1 = cur.ax1 + x[2];
+      const double uy0 = cur.ay0 - x[0], uy1 = cur.ay1 - x[1];
+      const double vy0 = cur.ay0 + x[0], vy1 = cur.ay1 + x[1];
+      const int base = scl * kRow + scol;
+      if (side == 0) {
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+          sX[base + kLS * l] = x[l];
+          sXo[base + kLS * l] = cur.xo[l];
+        }
+        sU[base] = ux0;
+        sU[base + kLS] = ux1;
+        sU[base + 2 * kLS] = uy0;
+        sU[base + 3 * kLS] = uy1;
+      } else {
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+          double m = 0.0, gx = 0.0, gy = 0.0;
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            m = fma(so[4 * l + p], x[p], m);
+            gx = fma(so[16 + 4 * l + p], x[p], gx);
+            gy = fma(so[32 + 4 * l + p], x[p], gy);
+          }
+          sMX[base + kLS * l] = m;
+          sGX[base + kLS * l] = gx;
+          sGY[base + kLS * l] = gy;
+        }
+        double* f = sF + 2 * scl * kRow + scol;
+        f[0] = 0.5 * (e2x[0] * vx0 + e2x[1] * vx1);
+        f[kLS] = 0.5 * (e2x[2] * vx0 + e2x[3] * vx1);
+        f[2 * kLS] = 0.5 * (e2y[0] * vy0 + e2y[1] * vy1);
+        f[3 * kLS] = 0.5 * (e2y[2] * vy0 + e2y[3] * vy1);
+        f[4 * kLS] = 0.5 * (e2x[0] * ux0 + e2x[1] * ux1);
+        f[5 * kLS] = 0.5 * (e2x[2] * ux0 + e2x[3] * ux1);
+        f[6 * kLS] = 0.5 * (e2y[0] * uy0 + e2y[1] * uy1);
+        f[7 * kLS] = 0.5 * (e2y[2] * uy0 + e2y[3] * uy1);
+        double sq = 0.0;
+#pragma unroll
+        for (int l = 0; l < 4; ++l) sq = fma(so[56 + l], x[l], sq);
+        sQ[scl * 16 + scol] = cur.qc * sq;  // q-hat (dlr_sn.py:70)
+      }
+      if (threadIdx.x < C) {
+        sC[2 * threadIdx.x] = cur.st;
+        sC[2 * threadIdx.x + 1] = cur.ss;
+      }
+    }
+    __syncthreads();
+    fetch(c0 + C, cur);  // next chunk's loads in flight during the MMAs
+    // ---- volume terms: the 4 cells of this warp's half
+#pragma unroll
+    for (int k = 0; k < C / 2; ++k) {
+      const int cl = hf * (C / 2) + k;
+      const double xa = sX[cl * kRow + q * kLS + ca];
+      const double xo = sXo[cl * kRow + q * kLS + ca];
+      const double mx = sMX[cl * kRow + q * kLS + cb];
+      const double gx = sGX[cl * kRow + q * kLS + cb];
+      const double gy = sGY[cl * kRow + q * kLS + cb];
+      const double stc = sC[2 * cl], ssc = sC[2 * cl + 1];
+      dmma(acc[0][0], acc[0][1], xa, gx);        // px (volume)
+      dmma(acc[1][0], acc[1][1], xa, gy);        // py (volume)
+      dmma(acc[4][0], acc[4][1], stc * xa, mx);  // mt
+      dmma(acc[5][0], acc[5][1], ssc * xa, mx);  // ms
+      dmma(acc[6][0], acc[6][1], xo, mx);        // mo
+    }
+    // ---- face terms: pairs (cl, cl + 1) of this half; k slot q -> cell
+    // cl + q / 2, face dof q % 2
+#pragma unroll
+    for (int k = 0; k < C / 4; ++k) {
+      const int cl = hf * (C / 2) + 2 * k + second;
+      const double uxa = sU[cl * kRow + kk * kLS + ca];
+      const double uya = sU[cl * kRow + (2 + kk) * kLS + ca];
+      const double* f = sF + 2 * cl * kRow + cb;
+      dmma(acc[0][0], acc[0][1], uxa, f[kk * kLS]);        // px (faces)
+      dmma(acc[1][0], acc[1][1], uya, f[(2 + kk) * kLS]);  // py (faces)
+      dmma(acc[2][0], acc[2][1], uxa, f[(4 + kk) * kLS]);  // jx
+      dmma(acc[3][0], acc[3][1], uya, f[(6 + kk) * kLS]);  // jy
+    }
+    if (i0 == 0 && threadIdx.x < 16)
+      for (int cl = 0; cl < nc; ++cl) qacc += sQ[cl * 16 + threadIdx.x];
+  }
+  // ---- right / top domain-boundary faces (a = own right/top edge, b = 0)
+  {
+    const int ti = threadIdx.x >> 4, tj = threadIdx.x & 15;
+    const int i = i0 + ti, j = j0 + tj;
+    double bx = 0.0, by = 0.0;
+    if (i < r && j < r) {
+      const int first_right = c_begin + ((nx - 1 - c_begin % nx) % nx + nx) % nx;
+      for (int c = first_right; c < c_end; c += nx) {
+        const int64_t r1 = (int64_t)c * 4 + 1, r3 = (int64_t)c * 4 + 3;
+        const double ai0 = ldx(X, r, r1, i), ai1 = ldx(X, r, r3, i);
+        const double aj0 = ldx(X, r, r1, j), aj1 = ldx(X, r, r3, j);
+        bx += ai0 * (0.5 * (e2x[0] * aj0 + e2x[1] * aj1)) + ai1 * (0.5 * (e2x[2] * aj0 + e2x[3] * aj1));
+      }
+      for (int c = max(c_begin, (ny - 1) * nx); c < c_end; ++c) {
+        const int64_t r2 = (int64_t)c * 4 + 2, r3 = (int64_t)c * 4 + 3;
+        const double ai0 = ldx(X, r, r2, i), ai1 = ldx(X, r, r3, i);
+        const double aj0 = ldx(X, r, r2, j), aj1 = ldx(X, r, r3, j);
+        by += ai0 * (0.5 * (e2y[0] * aj0 + e2y[1] * aj1)) + ai1 * (0.5 * (e2y[2] * aj0 + e2y[3] * aj1));
+      }
+    }
+    bnd[0][ti][tj] = bx;
+    bnd[1][ti][tj] = by;
+  }
+  // ---- fixed-order reduction: (half 0 + half 1) + boundary
+  __syncthreads();
+  double* red = sm;  // [2 halves][7][16][17], reusing the staging planes
+#pragma unroll
+  for (int o = 0; o < 7; ++o) {
+    red[((hf * 7 + o) * 16 + 8 * mt + g) * 17 + 8 * nt + 2 * q] = acc[o][0];
+    red[((hf * 7 + o) * 16 + 8 * mt + g) * 17 + 8 * nt + 2 * q + 1] = acc[o][1];
+  }
+  if (i0 == 0 && threadIdx.x < 16) sQ[threadIdx.x] = qacc;  // (staging planes are dead)
+  __syncthreads();
+  const int64_t stride = 7 * (int64_t)r * r + r;
+  double* out = pa.part + (int64_t)blockIdx.x * stride;
+  for (int e = threadIdx.x; e < 7 * 256; e += blockDim.x) {
+    const int o = e >> 8, rem = e & 255, row = rem >> 4, col = rem & 15;
+    const int i = i0 + row, j = j0 + col;
+    if (i >= r || j >= r) continue;
+    double v = red[((0 * 7 + o) * 16 + row) * 17 + col] + red[((1 * 7 + o) * 16 + row) * 17 + col];
+    if (o == 0 || o == 2) v += bnd[0][row][col];  // px, jx
+    if (o == 1 || o == 3) v += bnd[1][row][col];  // py, jy
+    out[(int64_t)o * r * r + (int64_t)i * r + j] = v;
+  }
+  if (i0 == 0 && threadIdx.x < 16 && j0 + (int)threadIdx.x < r)
+    out[7 * (int64_t)r * r + j0 + threadIdx.x] = sQ[threadIdx.x];
+}
+
+// ---------------------------------------------------------------------------
 // Small dense kernels: one CTA, matrices in global memory (L2 resident).
 
 // Cholesky G = R^T R (R upper) and Rinv = R^-1 (upper).  flag[0] = 1 if a
@@ -1449,8 +1668,14 @@ int dlrsn_project(const dlrsn_cellops* ops, int r, const double* X, const double
   cudaStream_t st = as_stream(stream);
   // partial slots not written by some tiles must be zero
   DLRSN_TRY_CUDA(cudaMemsetAsync(partial, 0, sizeof(double) * (size_t)nblk * (7 * (size_t)r * r + r), st));
-  project_kernel<<<dim3(nblk, tiles), kTile * kTile, 0, st>>>(pa, *ops);
-  DLRSN_CHECK_LAUNCH("project_kernel");
+  static const char* simt = getenv("DLRSN_PROJECT_SIMT");
+  if (simt && simt[0] == '1') {
+    project_kernel<<<dim3(nblk, tiles), kTile * kTile, 0, st>>>(pa, *ops);
+    DLRSN_CHECK_LAUNCH("project_kernel");
+  } else {
+    project_mma_kernel<<<dim3(nblk, tiles), 256, 0, st>>>(pa, *ops);
+    DLRSN_CHECK_LAUNCH("project_mma_kernel");
+  }
   const int64_t len = 7 * (int64_t)r * r + r;
   reduce_partials_kernel<<<(unsigned)((len + 31) / 32), 1024, 0, st>>>(nblk, len, partial, out, 1.0);
   DLRSN_CHECK_LAUNCH("reduce_partials_kernel");
