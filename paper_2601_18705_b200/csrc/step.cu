@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -23,19 +24,23 @@ __global__ void ks_kernel(int r, const double* __restrict__ S, const double* __r
                           const int* __restrict__ idx, const double* __restrict__ beta,
                           double* __restrict__ K, double* __restrict__ Sb,
                           const double* __restrict__ omegas, double* __restrict__ om_sel) {
-  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
-    const int i = e / r, d = e % r;
-    const double* w = W + (int64_t)idx[d] * r;
-    double s = 0.0;
-    for (int j = 0; j < r; ++j) s = fma(S[i * r + j], w[j], s);
-    K[e] = s;
-  }
-  for (int i = threadIdx.x; i < r; i += blockDim.x) {
-    double s = 0.0;
-    for (int j = 0; j < r; ++j) s = fma(S[i * r + j], beta[j], s);
-    Sb[i] = s;
-  }
-  for (int e = threadIdx.x; e < 3 * r; e += blockDim.x) om_sel[e] = omegas[(int64_t)idx[e / 3] * 3 + e % 3];
+  if (K)
+    for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+      const int i = e / r, d = e % r;
+      const double* w = W + (int64_t)idx[d] * r;
+      double s = 0.0;
+      for (int j = 0; j < r; ++j) s = fma(S[i * r + j], w[j], s);
+      K[e] = s;
+    }
+  if (Sb)
+    for (int i = threadIdx.x; i < r; i += blockDim.x) {
+      double s = 0.0;
+      for (int j = 0; j < r; ++j) s = fma(S[i * r + j], beta[j], s);
+      Sb[i] = s;
+    }
+  if (om_sel)
+    for (int e = threadIdx.x; e < 3 * r; e += blockDim.x)
+      om_sel[e] = omegas[(int64_t)idx[e / 3] * 3 + e % 3];
 }
 
 // *out |= any(sigma_t - sigma_s <= 0)  (transport_sn.py:208-209)
@@ -383,6 +388,53 @@ static int enqueue_status(cudaStream_t st, const StepBufs& b, int r, StepStatus*
   return DLRSN_OK;
 }
 
+// ---- a second stream for the step's parallel branches (fork / join by
+// events; captured into a graph they become parallel branches) -------------
+struct Fork {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+// Off by default: measured on C2 the forked graph was slower (1.49 vs 1.35 ms
+// per step; the side branch's grid-wide kernels stretch the critical path
+// more than the overlap with the single-CTA kernels gains).  DLRSN_STEP_FORK=1
+// enables it.
+static bool fork_enabled() {
+  static const char* e = getenv("DLRSN_STEP_FORK");
+  return e && e[0] == '1';
+}
+static int fork_streams(Fork** out) {
+  static thread_local Fork f;
+  if (!fork_enabled()) {  // serial variant: the "side" work stays on the caller's stream
+    static thread_local Fork none;
+    *out = &none;
+    return DLRSN_OK;
+  }
+  if (!f.side) {
+    DLRSN_TRY_CUDA(cudaStreamCreateWithFlags(&f.side, cudaStreamNonBlocking));
+    DLRSN_TRY_CUDA(cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming));
+    DLRSN_TRY_CUDA(cudaEventCreateWithFlags(&f.join, cudaEventDisableTiming));
+  }
+  *out = &f;
+  return DLRSN_OK;
+}
+// side stream starts after everything enqueued on `st` so far
+static int fork_to(Fork* f, cudaStream_t st) {
+  if (!f->fork) {
+    f->side = st;
+    return DLRSN_OK;
+  }
+  DLRSN_TRY_CUDA(cudaEventRecord(f->fork, st));
+  DLRSN_TRY_CUDA(cudaStreamWaitEvent(f->side, f->fork, 0));
+  return DLRSN_OK;
+}
+// `st` continues after everything enqueued on the side stream
+static int join_from(const Fork* f, cudaStream_t st) {
+  if (!f->join) return DLRSN_OK;
+  DLRSN_TRY_CUDA(cudaEventRecord(f->join, f->side));
+  DLRSN_TRY_CUDA(cudaStreamWaitEvent(st, f->join, 0));
+  return DLRSN_OK;
+}
+
 // ---- CUDA-graph replay of the step's first segment --------------------------
 // The segment's ~50 launches depend only on the buffers, the parameters and
 // the iteration batch; a driver loop hands the same buffers back every other
@@ -670,29 +722,43 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     ia.ly = ops->ny * ops->dy;
     init_kernel<<<1, 96, 0, st>>>(ia);
     DLRSN_CHECK_LAUNCH("init_kernel");
-    // 1. DEIM, closure weights, input checks (reported at the readback)
+    // Two branches: the DEIM chain (one CTA for most of it) on `st`, the
+    // checks / scalar flux / scattering source / sigma layout on the side
+    // stream, so the single-CTA kernels overlap GPU-wide work.
+    Fork* fk = nullptr;
+    DLRSN_RET(fork_streams(&fk));
+    DLRSN_RET(fork_to(fk, st));
+    {
+      cudaStream_t sd = fk->side;
+      void* ss2 = sd;
+      sigma_check_kernel<<<std::min(1024, (nc + 255) / 256), 256, 0, sd>>>(nc, sigma_t, sigma_s,
+                                                                           b.flags);
+      DLRSN_CHECK_LAUNCH("sigma_check_kernel");
+      if (p->check_state) {
+        DLRSN_RET(dlrsn_mgram(ops, r, r, X, r, X, r, nullptr, b.G, b.part, ss2));
+        DLRSN_RET(wgram(no, r, W, p->weights_dev, b.wpart, b.wg, sd));
+        ortho_residual_kernel<<<1, 256, 0, sd>>>(r, b.G, b.wg, b.chk_in);
+        DLRSN_CHECK_LAUNCH("ortho_residual_kernel");
+      }
+      // scalar_flux (lowrank.py:60-62) -> the first scattering source
+      ks_kernel<<<1, 256, 0, sd>>>(r, S, W, nullptr, beta, nullptr, b.Sb, p->omegas_dev, nullptr);
+      DLRSN_CHECK_LAUNCH("ks_kernel");
+      DLRSN_RET(dlrsn_rowmix(N, r, 1, X, r, b.Sb, 1, 0.0, b.phi0, 1, ss2));
+      DLRSN_RET(dlrsn_scatter_source(ops, b.phi0, sigma_s, b.scat, b.flags + 1, ss2));
+      DLRSN_RET(dlrsn_cells_to_sk4(ops, sigma_t, b.sig4, ss2));
+    }
+    // 1. DEIM, closure weights (errors reported at the readback)
     DLRSN_RET(dlrsn_deim(no, r, b.Wk, W, b.err_idx + 1, b.Lhat, b.U, b.err_idx, s));
     DLRSN_RET(dlrsn_what_solve(r, 1, b.Lhat, b.U, beta, b.closure, 1, s));
-    sigma_check_kernel<<<std::min(1024, (nc + 255) / 256), 256, 0, st>>>(nc, sigma_t, sigma_s,
-                                                                         b.flags);
-    DLRSN_CHECK_LAUNCH("sigma_check_kernel");
-    if (p->check_state) {
-      DLRSN_RET(dlrsn_mgram(ops, r, r, X, r, X, r, nullptr, b.G, b.part, s));
-      DLRSN_RET(wgram(no, r, W, p->weights_dev, b.wpart, b.wg, st));
-      ortho_residual_kernel<<<1, 256, 0, st>>>(r, b.G, b.wg, b.chk_in);
-      DLRSN_CHECK_LAUNCH("ortho_residual_kernel");
-    }
     const int width = world > 1 ? comm->gather_width : 1;
     plan_kernel<<<1, DLRSN_MAX_RANK, 0, st>>>(r, no, world, rank_id, b.err_idx, b.err_idx + 1,
                                               p->omegas_dev, b.closure, b.idx, b.groups, b.quads,
                                               b.mine, b.place, N, width, b.cw_local);
     DLRSN_CHECK_LAUNCH("plan_kernel");
-    // 2. evaluate_rows, scalar_flux, rhs (dlr_sn.py:110-121)
-    ks_kernel<<<1, 256, 0, st>>>(r, S, W, b.idx, beta, b.K, b.Sb, p->omegas_dev, b.om_sel);
+    // 2. evaluate_rows (dlr_sn.py:110-121) and the sweep rhs
+    ks_kernel<<<1, 256, 0, st>>>(r, S, W, b.idx, beta, b.K, nullptr, p->omegas_dev, b.om_sel);
     DLRSN_CHECK_LAUNCH("ks_kernel");
     DLRSN_RET(dlrsn_rowmix(N, r, r, X, r, b.K, r, 0.0, b.psi_time, r, s));
-    DLRSN_RET(dlrsn_rowmix(N, r, 1, X, r, b.Sb, 1, 0.0, b.phi0, 1, s));
-    DLRSN_RET(dlrsn_cells_to_sk4(ops, sigma_t, b.sig4, s));
     const double* pt_local = b.psi_time;
     int ld_pt = r;
     if (world > 1 && nl > 0) {
@@ -704,7 +770,7 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     if (nl > 0)
       DLRSN_RET(dlrsn_rhs_build(ops, nl, b.quads, q, p->inv_cdt, pt_local, ld_pt, nullptr, 1,
                                 b.rhs_sk, s));
-    DLRSN_RET(dlrsn_scatter_source(ops, b.phi0, sigma_s, b.scat, b.flags + 1, s));
+    DLRSN_RET(join_from(fk, st));
     return DLRSN_OK;
   };
   // 3. source iterations it_from..it_to (transport_sn.py:408-447): the
@@ -782,6 +848,18 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     DLRSN_RET(dlrsn_row_combine(r, r, b.Binv, b.proj + 5 * r * r, b.qall, b.closure, b.L,
                                 b.lbar, b.rowstat + r, s));
     DLRSN_RET(dlrsn_what_solve(r, r, b.Lhat, b.U, b.L, b.gamma, 0, s));
+    // two branches: the angular update (one CTA) on `st`; the flux of the
+    // new state, the step boundary and the spatial check on the side stream
+    Fork* fk = nullptr;
+    DLRSN_RET(fork_streams(&fk));
+    DLRSN_RET(fork_to(fk, st));
+    {
+      cudaStream_t sd = fk->side;
+      void* ss2 = sd;
+      DLRSN_RET(dlrsn_rowmix(N, r, 1, X_new, r, b.lbar, 1, 0.0, phi_out, 1, ss2));
+      if (p->advance) DLRSN_RET(advance_launch(p->advance, phi_out, sd));
+      if (p->check_state) DLRSN_RET(dlrsn_mgram(ops, r, r, X_new, r, X_new, r, nullptr, b.G, b.part, ss2));
+    }
     DLRSN_RET(dlrsn_rowmix(no, r, r, W, r, b.gamma, r, 0.0, b.lfull, r, s));
     if (!exact_w)
       DLRSN_RET(dlrsn_cholqr2_small(no, r, b.lfull, r, p->weights_dev, W_new, r, b.Rang,
@@ -792,13 +870,11 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     DLRSN_RET(wgram(no, r, W_new, p->weights_dev, b.wpart, b.wg, st));
     finish_kernel<<<1, 256, 0, st>>>(r, b.Rang, b.wg, S_new, beta_new);
     DLRSN_CHECK_LAUNCH("finish_kernel");
+    DLRSN_RET(join_from(fk, st));
     if (p->check_state) {
-      DLRSN_RET(dlrsn_mgram(ops, r, r, X_new, r, X_new, r, nullptr, b.G, b.part, s));
       ortho_residual_kernel<<<1, 256, 0, st>>>(r, b.G, b.wg, b.chk_out);
       DLRSN_CHECK_LAUNCH("ortho_residual_kernel");
     }
-    DLRSN_RET(dlrsn_rowmix(N, r, 1, X_new, r, b.lbar, 1, 0.0, phi_out, 1, s));
-    if (p->advance) DLRSN_RET(advance_launch(p->advance, phi_out, st));
     return enqueue_status(st, b, r, hs);
   };
 
