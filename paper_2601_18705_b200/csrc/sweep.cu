@@ -934,6 +934,7 @@ int sweep_launch(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int
   const int items = sk_strips(ops->ny) * G;
   bool use_ws = items <= 2 * sms;
   if (ws_env) use_ws = ws_env[0] == '1';
+  if (phi_part_sk) use_ws = false;  // the warp-specialised kernel writes no closure partials
   SweepTimer* tm = g_timing ? timer_slot(G, dw) : nullptr;
   if (tm) DLRSN_TRY_CUDA(cudaEventRecord(tm->start, st));
   int rc;

@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kWsThreads) sweep_ws_kernel(const SweepArgs a)
     const dlrsn_group* grp = a.groups + g;
     const int quad = grp->quad;
     const int slot = grp->slot[0];
-    const double ox = grp->ox[0], oy = grp->oy[0], cw = grp->cw[0];
+    const double ox = grp->ox[0], oy = grp->oy[0];
     if (threadIdx.x < 16) s_S[threadIdx.x] = ox * a.gxp[threadIdx.x] + oy * a.gyp[threadIdx.x];
     __syncthreads();
     for (int e = threadIdx.x; e < kWsHRing * kWsC; e += blockDim.x)
@@ -267,37 +267,51 @@ __global__ void __launch_bounds__(kWsThreads) sweep_ws_kernel(const SweepArgs a)
     } else {
       // ------------------------------ consumer ------------------------------
       double* psi_p = a.psi_sk + (int64_t)slot * a.vlen + strip_vec + 2 * lane;
-      double* phi_p = a.phi_sk ? a.phi_sk + (int64_t)g * a.vlen + strip_vec + 2 * lane : nullptr;
       double2* hin = s > 0 ? reinterpret_cast<double2*>(a.handoff) + ((int64_t)(s - 1) * G + g) * nx
                            : nullptr;
       double2* hout = (s + 1 < ns) ? reinterpret_cast<double2*>(a.handoff) + ((int64_t)s * G + g) * nx
                                    : nullptr;
       const bool hlane = hin != nullptr && lane < kWsC;
-      double2 h0 = make_double2(0.0, 0.0);
-      double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
+      double x0 = 0.0, x1 = 0.0;
+      double u0 = 0.0, u1 = 0.0;  // the lane below's top edge, one step back
       for (int m = 0; m < nchunks; ++m) {
         const int st = m % kWsStages;
         const uint32_t u = uses[st];
-        {
+        // inflow of lane 0 for this chunk's columns (staged by the poller);
+        // lane 0 keeps all kWsC values in registers
+        double2 hv[kWsC];
+#pragma unroll
+        for (int tt = 0; tt < kWsC; ++tt) hv[tt] = make_double2(0.0, 0.0);
+        if (hin != nullptr) {
           const bool need = hlane && m < hchunks && m * kWsC + lane < nx;
           double2* hs = s_hin + (m % kWsHRing) * kWsC + lane;
-          h0 = make_double2(0.0, 0.0);
           long long spins = 0;
           bool got = !need;
           while (!__all_sync(kFull, got)) {
             if (!got) {
               const double hx = ld_volatile_shared_f64(&hs->x);
               const double hy = ld_volatile_shared_f64(&hs->y);
-              if (!is_empty(hx) && !is_empty(hy)) {
-                h0 = make_double2(hx, hy);
-                got = true;
-              }
+              got = !is_empty(hx) && !is_empty(hy);
             }
             if (++spins > (1ll << 30)) {
-              if (need && !got) atomicOr(a.status, 2);
+              if (need && !got) {
+                atomicOr(a.status, 2);
+                hs->x = 0.0;
+                hs->y = 0.0;
+              }
               got = true;
             }
           }
+          if (lane == 0) {
+            const double2* h = s_hin + (m % kWsHRing) * kWsC;
+#pragma unroll
+            for (int tt = 0; tt < kWsC; ++tt)
+              if (m < hchunks && m * kWsC + tt < nx) {
+                hv[tt].x = ld_volatile_shared_f64(&h[tt].x);
+                hv[tt].y = ld_volatile_shared_f64(&h[tt].y);
+              }
+          }
+          __syncwarp();
           if (need) {  // free the slot: y first, x last (the poller tests x)
             *reinterpret_cast<volatile double*>(&hs->y) = empty;
             __threadfence_block();
@@ -331,32 +345,23 @@ __global__ void __launch_bounds__(kWsThreads) sweep_ws_kernel(const SweepArgs a)
           const bool act = row_ok && ip >= 0 && ip < nx;
           double2 nz[2], nk[8];
           if (tt + 1 < kWsC) load(tt + 1, nz, nk);
-          const double hy0 = __shfl_sync(kFull, h0.x, tt);
-          const double hy1 = __shfl_sync(kFull, h0.y, tt);
-          if (lane == 0) {
-            y0 = hin != nullptr ? hy0 : 0.0;
-            y1 = hin != nullptr ? hy1 : 0.0;
-          }
+          // y-inflow: the strip below for lane 0, the lane below otherwise
+          const double y0 = lane == 0 ? hv[tt].x : u0;
+          const double y1 = lane == 0 ? hv[tt].y : u1;
           const double q0 = fma(fk[4].y, y1, fma(fk[4].x, y0, fma(fk[0].y, x1, fma(fk[0].x, x0, fz[0].x))));
           const double q1 = fma(fk[5].y, y1, fma(fk[5].x, y0, fma(fk[1].y, x1, fma(fk[1].x, x0, fz[0].y))));
           const double q2 = fma(fk[6].y, y1, fma(fk[6].x, y0, fma(fk[2].y, x1, fma(fk[2].x, x0, fz[1].x))));
           const double q3 = fma(fk[7].y, y1, fma(fk[7].x, y0, fma(fk[3].y, x1, fma(fk[3].x, x0, fz[1].y))));
-          const double u0 = __shfl_up_sync(kFull, q2, 1);
-          const double u1 = __shfl_up_sync(kFull, q3, 1);
+          u0 = __shfl_up_sync(kFull, q2, 1);
+          u1 = __shfl_up_sync(kFull, q3, 1);
           if (t < T) {  // steps past the slab's end would land in the next strip / slot
             double2* po = reinterpret_cast<double2*>(psi_p + (int64_t)t * 128);
             po[0] = make_double2(q0, q1);
             po[32] = make_double2(q2, q3);
-            if (phi_p) {
-              double2* pp = reinterpret_cast<double2*>(phi_p + (int64_t)t * 128);
-              pp[0] = make_double2(cw * q0, cw * q1);
-              pp[32] = make_double2(cw * q2, cw * q3);
-            }
           }
           if (lane == 31 && act && hout) __stcg(hout + ip, make_double2(q2, q3));
           x0 = act ? q1 : x0;
           x1 = act ? q3 : x1;
-          if (lane > 0) { y0 = u0; y1 = u1; }
           if (tt + 1 < kWsC) {
             fz[0] = nz[0]; fz[1] = nz[1];
 #pragma unroll

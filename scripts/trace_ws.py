@@ -20,13 +20,13 @@ plan = Tr._SweepPlan(ops, quad.omegas[:D], quad.weights[:D], dw=1)
 vl = ops.vec_len
 rhs = torch.rand(D * vl, dtype=torch.float64, device='cuda'); psi = torch.empty_like(rhs)
 part = torch.empty(plan.G * vl, dtype=torch.float64, device='cuda'); scat = torch.rand(4 * vl, dtype=torch.float64, device='cuda')
-Tr._sweep(ops, plan, rhs, psi, scat, part); torch.cuda.synchronize()
+Tr._sweep(ops, plan, rhs, psi, scat, None); torch.cuda.synchronize()
 chunks = (n + 31 + C - 1) // C
 ns = (ny + 31) // 32
 buf = torch.zeros(ns * plan.G * chunks * 8, dtype=torch.int64, device='cuda')
 _lib.call("dlrsn_debug_trace", ctypes.c_void_p(buf.data_ptr()), chunks)
 e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-e0.record(); Tr._sweep(ops, plan, rhs, psi, scat, part); e1.record(); torch.cuda.synchronize()
+e0.record(); Tr._sweep(ops, plan, rhs, psi, scat, None); e1.record(); torch.cuda.synchronize()
 _lib.call("dlrsn_debug_trace", None, 0)
 print("launch ms", e0.elapsed_time(e1))
 t = buf.cpu().numpy().reshape(ns * plan.G, chunks, 8).astype(np.float64)
