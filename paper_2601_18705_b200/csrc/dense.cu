@@ -1390,7 +1390,7 @@ __global__ void row_combine_kernel(int n, int r, const double* __restrict__ Binv
 // the interpolation residual W[:,j] - W[:,:j] W[p,:j]^-1 W[p,j]; the pivot is
 // its first maximal |entry| (np.argmax).  Produces the picks, the unit lower
 // factor rows L[p,:] and U (so W[p,:] = Lhat U), all in pick order.
-__global__ void __launch_bounds__(256) deim_kernel(int n, int r,
+__global__ void __launch_bounds__(1024) deim_kernel(int n, int r,
                                                    double* __restrict__ Wk_global /* n x r work */,
                                                    const double* __restrict__ W,
                                                    int* __restrict__ idx, double* __restrict__ Lhat,
@@ -1403,9 +1403,9 @@ __global__ void __launch_bounds__(256) deim_kernel(int n, int r,
   extern __shared__ double dsm[];
   double* Wk = in_smem ? dsm : Wk_global;
   unsigned char* picked = reinterpret_cast<unsigned char*>(in_smem ? dsm + (size_t)n * r : nullptr);
-  __shared__ double bv[2][8];
-  __shared__ int bi[2][8];
-  __shared__ double s_floor[8];
+  __shared__ double bv[2][32];
+  __shared__ int bi[2][32];
+  __shared__ double s_floor[32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double mx = 0.0;
   if (in_smem) {
@@ -1762,7 +1762,9 @@ int dlrsn_deim(int n, int r, double* Wwork, const double* W, int* idx, double* L
   if (in_smem)
     DLRSN_TRY_CUDA(cudaFuncSetAttribute(deim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
-  deim_kernel<<<1, 256, in_smem ? smem : 0, as_stream(stream)>>>(n, r, Wwork, W, idx, Lhat, U,
+  static const char* dt = getenv("DLRSN_DEIM_THREADS");
+  const int threads = dt ? atoi(dt) : 256;  // 256 / 512 equal, 1024 slower (C2)
+  deim_kernel<<<1, threads, in_smem ? smem : 0, as_stream(stream)>>>(n, r, Wwork, W, idx, Lhat, U,
                                                                  err_col, in_smem);
   DLRSN_CHECK_LAUNCH("deim_kernel");
   return DLRSN_OK;
