@@ -483,7 +483,7 @@ static bool graphs_enabled() {
 }
 
 template <class F>
-static int graph_run(const GraphKey& key, F&& enqueue, cudaStream_t st) {
+static int graph_run(const GraphKey& key, F&& enqueue, cudaStream_t st, bool chained) {
   static thread_local std::vector<GraphEntry> cache;
   static thread_local uint64_t tick = 0;
   static thread_local cudaStream_t cs = nullptr;
@@ -510,7 +510,7 @@ static int graph_run(const GraphKey& key, F&& enqueue, cudaStream_t st) {
     if (cache[lru].exec) cudaGraphExecDestroy(cache[lru].exec);
     cache.erase(cache.begin() + lru);
   };
-  if (!seen) {
+  if (!seen && !chained) {
     // first sighting: launch directly and remember the key; buffers that
     // come back (a driver loop) are captured on their second use, one-off
     // buffers (fresh allocations every step) never pay for a capture
@@ -523,6 +523,17 @@ static int graph_run(const GraphKey& key, F&& enqueue, cudaStream_t st) {
     e.kernels = 0;
     cache.push_back(e);
     return enqueue(st);
+  }
+  if (!seen) {  // a chained step (its input is a previous step's output): capture now
+    evict();
+    GraphEntry e;
+    e.key = key;
+    e.exec = nullptr;
+    e.device = dev;
+    e.used = tick;
+    e.kernels = 0;
+    cache.push_back(e);
+    seen = &cache.back();
   }
   if (!cs) DLRSN_TRY_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   // capture on a private stream (the caller's may be the legacy default stream)
@@ -649,8 +660,11 @@ static int grid_n(int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
 }
 
-// source-iteration batch size hint: the previous step's count + 1
+// source-iteration batch size hint: the largest count seen (+1)
 static thread_local int g_si_hint = 0;
+// X_new of the previous successful step: a step whose X is it is part of a
+// driver loop, whose buffers come back, so its graph is captured at once
+static thread_local const void* g_last_xnew = nullptr;
 
 }  // namespace dlrsn
 
@@ -880,7 +894,8 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
 
   int exact = p->gs_method == 1 ? 1 : 0;
   int exact_w = ang_fast ? 0 : 1;
-  const int batch0 = g_si_hint > 0 ? g_si_hint + 1 : 8;
+  // iteration batch: sticky (only grows), so the graph keys stay stable
+  const int batch0 = std::min(std::max(g_si_hint + 1, 6), 24);
   int it_next = std::min(p->si_max_iters, batch0) + 1;
   // ---- segment 1 (the whole step in the common case): replayed as a CUDA
   // graph when the same buffers come back (world 1; see graph_cache)
@@ -895,7 +910,7 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     if (graphed) {
       key.set(ops, p, X, S, W, beta, sigma_t, sigma_s, q, X_new, S_new, W_new, beta_new, phi_out,
               si_phi, workspace, sweep_ws, sweep_ws_bytes, batch0, exact, exact_w);
-      DLRSN_RET(graph_run(key, seg1, st0));
+      DLRSN_RET(graph_run(key, seg1, st0, X == g_last_xnew));
     } else {
       DLRSN_RET(seg1(st0));
     }
@@ -943,7 +958,7 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     info->iterations = hs->ctl.iters;
     // batch hint: the iteration count, decaying by one per step (stable
     // batches keep the graph keys stable; a shortfall costs one more segment)
-    g_si_hint = std::max(hs->ctl.iters, g_si_hint - 1);
+    g_si_hint = std::max(hs->ctl.iters, g_si_hint);
     if (!exact) {
       // CholQR's R_kk is accurate to ~eps/rel^2: keep it only when every
       // column retains >= 1e-6 of its M-norm and sits 100x above the
@@ -1002,6 +1017,7 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
                 hs->chk_out[1]);
       return DLRSN_EINVAL;
     }
+    g_last_xnew = X_new;
     return DLRSN_OK;
   }
   set_error("internal: step did not settle");

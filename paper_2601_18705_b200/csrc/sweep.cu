@@ -921,6 +921,10 @@ int sweep_launch(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int
   a.trace = h_trace;
   a.trace_chunks = h_trace_chunks;
   a.skip = skip;
+  {
+    static const char* dbg = getenv("DLRSN_SWEEP_DEBUG");
+    a.debug = dbg ? atoi(dbg) : 0;
+  }
   // single-direction groups: the warp-specialised kernel when the work items
   // barely fill the GPU (latency-bound regime), the multi-warp kernel when
   // there are enough items to hide the per-step latency by occupancy

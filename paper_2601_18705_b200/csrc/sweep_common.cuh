@@ -26,6 +26,7 @@ struct SweepArgs {
   unsigned long long* trace;  // debug timeline (dlrsn_debug_trace), null in production
   int trace_chunks;
   const int* skip;  // device flag: return at once when set (speculative iterations)
+  int debug;        // bit 0: ignore the strip inflow (timing experiments only)
 };
 
 // Device-side control of a batched source iteration (step.cu): iterations
