@@ -17,9 +17,13 @@
 
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace dlrsn {
+
+namespace cg = cooperative_groups;
 
 constexpr int kRB = 256;  // threads per block for the row kernels
 
@@ -170,6 +174,86 @@ __global__ void __launch_bounds__(256) rowmix_mma_kernel(int n, int kx, int ky,
           const int c = 8 * nt + 2 * q;
           if (beta == 0.0 && c + 1 < ky && ((ldy & 1) == 0) &&
               ((reinterpret_cast<uintptr_t>(Y) & 15) == 0)) {
+            *reinterpret_cast<double2*>(y + c) = make_double2(d[u][nt][0], d[u][nt][1]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+              if (c + i < ky) y[c + i] = beta == 0.0 ? d[u][nt][i] : fma(beta, y[c + i], d[u][nt][i]);
+          }
+        }
+      }
+    }
+  }
+}
+
+// rowmix for wide operands (kx <= 4 KS <= 128, any ky): the MMA k index is
+// permuted so that lane quad q owns the contiguous X columns q KS .. q KS +
+// KS - 1 (16-byte loads); K sits in shared memory in fragment order (row
+// 4 ks + q holds K row q KS + ks; row stride = 4 mod 16 doubles, so a
+// fragment load is conflict-free).  Each warp takes pairs of 8-row tiles, so
+// every K fragment feeds two DMMAs; column groups of 8 NT.
+template <int KS, int NT>
+__global__ void __launch_bounds__(256, (4 * KS + 8 * NT <= 96) ? 2 : 1) rowmix_wide_kernel(int n, int kx, int ky,
+                                                          const double* __restrict__ X, int ldx,
+                                                          const double* __restrict__ K, int ldk,
+                                                          double beta, double* __restrict__ Y,
+                                                          int ldy, int kyp, int ldks, int vec) {
+  extern __shared__ double sK[];  // (4 KS) x ldks
+  for (int e = threadIdx.x; e < 4 * KS * kyp; e += blockDim.x) {
+    const int pr = e / kyp, col = e - pr * kyp;
+    const int k = (pr & 3) * KS + (pr >> 2);
+    sK[pr * ldks + col] = (k < kx && col < ky) ? __ldg(K + (int64_t)k * ldk + col) : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int64_t tiles = ((int64_t)n + 7) / 8;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool vstore = beta == 0.0 && ((ldy & 1) == 0) && ((reinterpret_cast<uintptr_t>(Y) & 15) == 0);
+  for (int64_t t0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 2; t0 < tiles;
+       t0 += 2 * nwarps) {
+    double af[2][KS];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t row = (t0 + u) * 8 + g;
+      const double* xr = X + row * ldx + q * KS;
+      if (row < n && vec) {
+#pragma unroll
+        for (int ks = 0; ks < KS; ks += 2) {
+          const double2 v = __ldg(reinterpret_cast<const double2*>(xr + ks));
+          af[u][ks] = v.x;
+          af[u][ks + 1] = v.y;
+        }
+      } else {
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks)
+          af[u][ks] = (row < n && q * KS + ks < kx) ? __ldg(xr + ks) : 0.0;
+      }
+    }
+    for (int c0 = 0; c0 < ky; c0 += 8 * NT) {
+      double d[2][NT][2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) d[u][nt][0] = d[u][nt][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const double* kr = sK + (4 * ks + q) * ldks + c0 + g;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const double b = kr[8 * nt];
+          dmma(d[0][nt][0], d[0][nt][1], af[0][ks], b);
+          dmma(d[1][nt][0], d[1][nt][1], af[1][ks], b);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t row = (t0 + u) * 8 + g;
+        if (row >= n) continue;
+        double* y = Y + row * ldy;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int c = c0 + 8 * nt + 2 * q;
+          if (vstore && c + 1 < ky) {
             *reinterpret_cast<double2*>(y + c) = make_double2(d[u][nt][0], d[u][nt][1]);
           } else {
 #pragma unroll
@@ -344,6 +428,161 @@ __global__ void __launch_bounds__(256, 4) mgram_mma_kernel(int ncell, int ra, in
   const int i = i0 + e / kTile, j = j0 + e % kTile;
   if (i < ra && j < rb) part[(int64_t)blockIdx.x * ra * rb + (int64_t)i * rb + j] = s;
 }
+
+// mgram for wide bases (ra or rb > 32): a CTA owns a TB x TB output block
+// over a range of cells.  Chunks of 16 cells stream into shared memory with
+// cp.async (double-buffered: the next chunk is in flight while this one is
+// multiplied); B rows are then premultiplied by coeff_c M into a third
+// plane.  Row stride TB + 4 makes every fragment load conflict-free.  Each
+// warp owns a 32 x 32 sub-block (4 x 4 DMMA tiles) for 1 / KP of every
+// chunk's cells (k step = one cell's 4 dofs); the KP parts are summed in
+// fixed order at the end.
+constexpr int kMgC = 16;  // cells per chunk
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int TB>
+struct MgramWide {
+  static constexpr int LD = TB + 4, CR = 4 * kMgC, PL = CR * LD;  // plane = one chunk
+  static constexpr int KP = 8 / ((TB / 32) * (TB / 32));
+  // planes: A x2, B' x1, raw B x2 (separate operands only)
+  static constexpr size_t smem(bool same) {
+    const size_t st = (size_t)PL * (same ? 3 : 5);
+    const size_t red = (size_t)KP * TB * (TB + 1);
+    return sizeof(double) * (st > red ? st : red);
+  }
+};
+
+template <int TB>
+__global__ void __launch_bounds__(256, 1) mgram_wide_kernel(int ncell, int ra, int rb,
+                                                         const double* __restrict__ A, int lda,
+                                                         const double* __restrict__ B, int ldb,
+                                                         const double* __restrict__ coeff,
+                                                         dlrsn_cellops ops, int cells_per_block,
+                                                         double* __restrict__ part, int vec) {
+  using P = MgramWide<TB>;
+  constexpr int LD = P::LD, PL = P::PL, KP = P::KP, NWT = 8 / KP, CPK = kMgC / KP;
+  constexpr int NCP = TB / 2;  // column pairs
+  extern __shared__ __align__(16) double smw[];
+  __shared__ double m[16];
+  if (threadIdx.x < 16) m[threadIdx.x] = ops.mass[threadIdx.x];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, q = lane & 3;
+  const int wt = warp % NWT, kp = warp / NWT;
+  const int wi = wt / (TB / 32), wj = wt % (TB / 32);
+  const int tiles_j = (rb + TB - 1) / TB;
+  const int i0 = (blockIdx.y / tiles_j) * TB, j0 = (blockIdx.y % tiles_j) * TB;
+  const int c_begin = blockIdx.x * cells_per_block;
+  const int c_end = min(ncell, c_begin + cells_per_block);
+  const bool same = (A == B) && (lda == ldb) && (i0 == j0);
+  double* sA0 = smw;
+  double* sBm = smw + 2 * PL;   // B' (premultiplied)
+  double* sBr0 = smw + 3 * PL;  // raw B x2 (separate operands)
+  const int64_t row_end = 4 * (int64_t)c_end;
+  auto stage = [&](const double* __restrict__ src, int ld, int cols, int col0, double* dst,
+                   int64_t row0) {
+    for (int e = threadIdx.x; e < P::CR * NCP; e += 256) {
+      const int row = e / NCP, cp = e - row * NCP;
+      const int64_t grow = row0 + row;
+      const int col = col0 + 2 * cp;
+      double* d = dst + row * LD + 2 * cp;
+      if (grow < row_end && vec && col + 1 < cols) {
+        cp_async16(d, src + grow * ld + col);
+      } else {
+        d[0] = (grow < row_end && col < cols) ? __ldg(src + grow * ld + col) : 0.0;
+        d[1] = (grow < row_end && col + 1 < cols) ? __ldg(src + grow * ld + col + 1) : 0.0;
+      }
+    }
+  };
+  auto issue = [&](int c0, int buf) {
+    stage(A, lda, ra, i0, sA0 + buf * PL, 4 * (int64_t)c0);
+    if (!same) stage(B, ldb, rb, j0, sBr0 + buf * PL, 4 * (int64_t)c0);
+    cp_async_commit();
+  };
+  double d[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) d[a][b][0] = d[a][b][1] = 0.0;
+  if (c_begin < c_end) issue(c_begin, 0);
+  int buf = 0;
+  for (int c0 = c_begin; c0 < c_end; c0 += kMgC, buf ^= 1) {
+    if (c0 + kMgC < c_end) {
+      issue(c0 + kMgC, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();  // chunk landed (cp.async and plain fills of all threads)
+    const double* sA = sA0 + buf * PL;
+    const double* sBsrc = same ? sA : sBr0 + buf * PL;
+    for (int e = threadIdx.x; e < kMgC * NCP; e += 256) {
+      const int cl = e / NCP, cp = e - cl * NCP;
+      double2 v[4];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) v[l] = *reinterpret_cast<const double2*>(sBsrc + (4 * cl + l) * LD + 2 * cp);
+      const double w = (coeff && c0 + cl < c_end) ? __ldg(coeff + c0 + cl) : 1.0;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        double2 mb = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          mb.x = fma(m[4 * l + b], v[b].x, mb.x);
+          mb.y = fma(m[4 * l + b], v[b].y, mb.y);
+        }
+        if (coeff) {
+          mb.x *= w;
+          mb.y *= w;
+        }
+        *reinterpret_cast<double2*>(sBm + (4 * cl + l) * LD + 2 * cp) = mb;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < CPK; ++k) {
+      const int cl = kp * CPK + k;
+      const double* ar = sA + (4 * cl + q) * LD + 32 * wi + g;
+      const double* br = sBm + (4 * cl + q) * LD + 32 * wj + g;
+      double af[4], bf[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        af[t] = ar[8 * t];
+        bf[t] = br[8 * t];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma(d[a][b][0], d[a][b][1], af[a], bf[b]);
+    }
+    __syncthreads();  // this chunk's planes are free for the next issue
+  }
+  double* red = smw;  // [KP][TB][TB + 1]
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        red[(kp * TB + 32 * wi + 8 * a + g) * (TB + 1) + 32 * wj + 8 * b + 2 * q + i] = d[a][b][i];
+  __syncthreads();
+  double* out = part + (int64_t)blockIdx.x * ra * rb;
+  for (int e = threadIdx.x; e < TB * TB; e += 256) {
+    const int ii = e / TB, jj = e % TB;
+    const int i = i0 + ii, j = j0 + jj;
+    if (i >= ra || j >= rb) continue;
+    double v = 0.0;
+#pragma unroll
+    for (int p = 0; p < KP; ++p) v += red[(p * TB + ii) * (TB + 1) + jj];
+    out[(int64_t)i * rb + j] = v;
+  }
+}
+
 
 // ---------------------------------------------------------------------------
 // project: per output tile (i0.., j0..) and chunk of cells, accumulate
@@ -1488,6 +1727,149 @@ __global__ void __launch_bounds__(1024) deim_kernel(int n, int r,
   if (threadIdx.x == 0) *err_col = -1;
 }
 
+// DEIM over a thread-block cluster (the same left-to-right GEPP as
+// deim_kernel, lowrank.py:168-205): CTA `rank` keeps rows [rank*nl, +nl) of
+// W in shared memory (column-major).  Per pick one cluster barrier: every
+// CTA publishes its best non-picked row (|residual|, row, the row's trailing
+// entries) in a double-buffered slot; after the barrier all CTAs read the
+// slots over DSMEM, take the same winner (largest |residual|, lowest row on
+// ties) and eliminate their own rows, computing the next column's local
+// argmax in the same pass.  Per element the arithmetic is deim_kernel's.
+constexpr int kDeimCT = 512;
+__global__ void __launch_bounds__(kDeimCT) deim_cluster_kernel(int n, int r, int nl,
+                                                              const double* __restrict__ W,
+                                                              int* __restrict__ idx,
+                                                              double* __restrict__ Lhat,
+                                                              double* __restrict__ U, int* err_col) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int crank = (int)cl.block_rank(), cs = (int)cl.num_blocks();
+  extern __shared__ double dsm[];
+  const int i0 = crank * nl;
+  const int nloc = max(0, min(nl, n - i0));
+  const int ls = r + 2;                    // slot stride: value, row, entries
+  double* Wk = dsm;                        // r x nl, Wk[k * nl + i]
+  double* slot = Wk + (size_t)r * nl;      // 2 x ls
+  double* prow = slot + 2 * ls;            // r: the pivot row
+  unsigned char* picked = reinterpret_cast<unsigned char*>(prow + r);
+  __shared__ double wv[kDeimCT / 32];
+  __shared__ int wi[kDeimCT / 32];
+  __shared__ int s_idx[DLRSN_MAX_RANK];
+  __shared__ int s_p, s_fail;
+  __shared__ double s_floor;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = kDeimCT / 32;
+  for (int e = tid; e < nloc * r; e += kDeimCT) cp_async8(Wk + (e % r) * nl + e / r, W + (int64_t)i0 * r + e);
+  for (int i = tid; i < nl; i += kDeimCT) picked[i] = 0;
+  cp_async_wait_all();
+  __syncthreads();
+  // floor = 1e-14 max(1, max |W|) (lowrank.py:182), via slot 0
+  double mx = 0.0;
+  for (int e = tid; e < nloc * r; e += kDeimCT) mx = fmax(mx, fabs(Wk[(e % r) * nl + e / r]));
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
+  if (lane == 0) wv[w] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int q = 0; q < nw; ++q) m = fmax(m, wv[q]);
+    slot[0] = m;
+  }
+  cl.sync();
+  if (w == 0) {
+    double m = lane < cs ? cl.map_shared_rank(slot, lane)[0] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(kFull, m, o));
+    if (lane == 0) s_floor = 1e-14 * fmax(1.0, m);
+  }
+  // local argmax of column 0
+  double best = -1.0;
+  int bidx = 0x7fffffff;
+  for (int i = tid; i < nloc; i += kDeimCT) {
+    const double v = fabs(Wk[i]);
+    if (v > best) { best = v; bidx = i0 + i; }
+  }
+  int fail = -1;
+  for (int j = 0; j < r; ++j) {
+    double* my = slot + ((j + 1) & 1) * ls;  // step 0 uses slot 1 (slot 0 held the max)
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(kFull, best, o);
+      const int oi = __shfl_xor_sync(kFull, bidx, o);
+      if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
+    }
+    if (lane == 0) { wv[w] = best; wi[w] = bidx; }
+    __syncthreads();
+    if (w == 0) {
+      double b = lane < nw ? wv[lane] : -1.0;
+      int bi = lane < nw ? wi[lane] : 0x7fffffff;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(kFull, b, o);
+        const int oi = __shfl_xor_sync(kFull, bi, o);
+        if (ov > b || (ov == b && oi < bi)) { b = ov; bi = oi; }
+      }
+      if (lane == 0) { my[0] = b; my[1] = (double)bi; }
+      const bool have = bi >= i0 && bi < i0 + nloc;
+      for (int k = j + lane; k < r; k += 32) my[2 + k] = have ? Wk[k * nl + (bi - i0)] : 0.0;
+    }
+    cl.sync();
+    if (w == 0) {
+      const double* rs = lane < cs ? cl.map_shared_rank(my, lane) : nullptr;
+      double b = rs ? rs[0] : -1.0;
+      int bi = rs ? (int)rs[1] : 0x7fffffff;
+      int src = lane;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(kFull, b, o);
+        const int oi = __shfl_xor_sync(kFull, bi, o);
+        const int os = __shfl_xor_sync(kFull, src, o);
+        if (ov > b || (ov == b && oi < bi)) { b = ov; bi = oi; src = os; }
+      }
+      const bool valid = bi >= 0 && bi < n;
+      if (valid) {
+        const double* win = cl.map_shared_rank(my, src);
+        for (int k = j + lane; k < r; k += 32) prow[k] = win[2 + k];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const double pv = valid ? prow[j] : 0.0;
+        s_p = valid ? bi : 0;
+        s_fail = !(valid && fabs(pv) > s_floor);
+      }
+    }
+    __syncthreads();
+    const int p = s_p;
+    if (crank == 0 && tid == 0) idx[j] = p;
+    if (tid == 0) s_idx[j] = p;
+    if (s_fail) { fail = j; break; }
+    if (crank == 0)
+      for (int k = tid; k < r; k += kDeimCT) U[j * r + k] = k >= j ? prow[k] : 0.0;
+    const double pv = prow[j];
+    const int pl = p - i0;
+    if (tid == 0 && pl >= 0 && pl < nloc) picked[pl] = 1;
+    best = -1.0;
+    bidx = 0x7fffffff;
+    for (int i = tid; i < nloc; i += kDeimCT) {
+      if (i == pl || picked[i]) continue;
+      const double l = Wk[j * nl + i] / pv;
+      Wk[j * nl + i] = l;  // the multiplier column (Lhat entries)
+      for (int k = j + 1; k < r; ++k) Wk[k * nl + i] -= l * prow[k];
+      if (j + 1 < r) {
+        const double v = fabs(Wk[(j + 1) * nl + i]);
+        if (v > best) { best = v; bidx = i0 + i; }
+      }
+    }
+    // the next step's slot write happens after the __syncthreads of its
+    // block argmax: no thread still reads prow / picked of this step then
+  }
+  if (fail < 0) {
+    __syncthreads();
+    // Lhat[q, j] = multiplier of column j at the q-th picked row (unit lower)
+    for (int e = tid; e < r * r; e += kDeimCT) {
+      const int q = e / r, j = e % r;
+      const int pl = s_idx[q] - i0;
+      if (pl < 0 || pl >= nloc) continue;
+      Lhat[e] = j < q ? Wk[j * nl + pl] : (j == q ? 1.0 : 0.0);
+    }
+  }
+  if (crank == 0 && tid == 0) *err_col = fail;
+  cl.sync();  // no CTA leaves while its slots may still be read
+}
+
 // Solves with W_hat = Lhat U (pick order):
 //   mode 0 (interpolation_coefficients): X = W_hat^-1 V   (V r x m)
 //   mode 1 (closure_weights):            x = W_hat^-T v   (v r)
@@ -1599,6 +1981,41 @@ int dlrsn_rowmix(int64_t n, int kx, int ky, const double* X, int ldx, const doub
     return DLRSN_OK;
   }
   const bool aligned = ((reinterpret_cast<uintptr_t>(X) | (uintptr_t)ldx * 8) & 15) == 0;
+  if ((kx > 32 || ky > 16) && kx <= 128 && n >= 64) {
+    const int ks = kx <= 16 ? 4 : (kx <= 32 ? 8 : (kx <= 64 ? 16 : 32));
+    const int nt = ky > 32 ? 8 : (ky > 16 ? 4 : (ky > 8 ? 2 : 1));
+    const int kyp = (ky + 8 * nt - 1) / (8 * nt) * (8 * nt);
+    const int ldks = kyp + ((4 - kyp % 16) + 16) % 16;
+    const size_t smem = (size_t)4 * ks * ldks * sizeof(double);
+    const int vec = aligned && kx == 4 * ks;
+    const int64_t tiles = (n + 7) / 8;
+    int64_t blocks = (tiles + 15) / 16;
+    if (blocks > 148 * 4) blocks = 148 * 4;
+    cudaStream_t st = as_stream(stream);
+#define DLRSN_ROWMIX_WIDE(KS, NT)                                                                do {                                                                                             if (smem > 48 * 1024)                                                                            DLRSN_TRY_CUDA(cudaFuncSetAttribute(rowmix_wide_kernel<KS, NT>,                                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));     rowmix_wide_kernel<KS, NT><<<(int)blocks, 256, smem, st>>>((int)n, kx, ky, X, ldx, K, ldk, beta,                                                                Y, ldy, kyp, ldks, vec);          } while (0)
+    if (ks == 4) {
+      if (nt == 8) DLRSN_ROWMIX_WIDE(4, 8);
+      else if (nt == 4) DLRSN_ROWMIX_WIDE(4, 4);
+      else DLRSN_ROWMIX_WIDE(4, 2);
+    } else if (ks == 8) {
+      if (nt == 8) DLRSN_ROWMIX_WIDE(8, 8);
+      else if (nt == 4) DLRSN_ROWMIX_WIDE(8, 4);
+      else DLRSN_ROWMIX_WIDE(8, 2);
+    } else if (ks == 16) {
+      if (nt == 8) DLRSN_ROWMIX_WIDE(16, 8);
+      else if (nt == 4) DLRSN_ROWMIX_WIDE(16, 4);
+      else if (nt == 2) DLRSN_ROWMIX_WIDE(16, 2);
+      else DLRSN_ROWMIX_WIDE(16, 1);
+    } else {
+      if (nt == 8) DLRSN_ROWMIX_WIDE(32, 8);
+      else if (nt == 4) DLRSN_ROWMIX_WIDE(32, 4);
+      else if (nt == 2) DLRSN_ROWMIX_WIDE(32, 2);
+      else DLRSN_ROWMIX_WIDE(32, 1);
+    }
+#undef DLRSN_ROWMIX_WIDE
+    DLRSN_CHECK_LAUNCH("rowmix_wide_kernel");
+    return DLRSN_OK;
+  }
   if (aligned && (kx == 8 || kx == 16 || kx == 32) && kRB % ky == 0) {
     const int grid = grid_for(n * ky);
     cudaStream_t st = as_stream(stream);
@@ -1629,25 +2046,68 @@ static int cells_per_block(int ncell, int tiles) {
   return cpb < kChunk ? kChunk : cpb;
 }
 
+// mgram launch plan: the wide kernel (TB = 32 / 64 blocks, about 2 CTAs per
+// SM over all output blocks, whole 16-cell chunks) when ra or rb > 32
+struct MgramPlan {
+  int tb, tiles, cpb, nblk;
+};
+static MgramPlan mgram_plan(int ncell, int ra, int rb) {
+  MgramPlan pl;
+  const int mx = ra > rb ? ra : rb;
+  pl.tb = mx > 32 ? (mx > 48 ? 64 : 32) : 0;
+  if (pl.tb == 0) {
+    pl.tiles = ((ra + kTile - 1) / kTile) * ((rb + kTile - 1) / kTile);
+    pl.cpb = cells_per_block(ncell, pl.tiles);
+  } else {
+    pl.tiles = ((ra + pl.tb - 1) / pl.tb) * ((rb + pl.tb - 1) / pl.tb);
+    const int target = (2 * 148 + pl.tiles - 1) / pl.tiles;
+    int cpb = (ncell + target - 1) / target;
+    cpb = (cpb + kMgC - 1) / kMgC * kMgC;
+    pl.cpb = cpb < kMgC ? kMgC : cpb;
+  }
+  pl.nblk = (ncell + pl.cpb - 1) / pl.cpb;
+  return pl;
+}
+
 int64_t dlrsn_partials_len(int ncell, int ra, int rb, int kind) {
   // partial buffer (doubles) for mgram (kind 0) / project (kind 1)
+  if (kind == 0) return (int64_t)mgram_plan(ncell, ra, rb).nblk * ra * rb;
   const int tiles = ((ra + kTile - 1) / kTile) * ((rb + kTile - 1) / kTile);
   const int cpb = cells_per_block(ncell, tiles);
   const int64_t nblk = (ncell + cpb - 1) / cpb;
-  return kind == 0 ? nblk * ra * rb : nblk * (7 * (int64_t)ra * ra + ra);
+  return nblk * (7 * (int64_t)ra * ra + ra);
 }
 
 int dlrsn_mgram(const dlrsn_cellops* ops, int ra, int rb, const double* A, int lda,
                 const double* B, int ldb, const double* coeff, double* G, double* partial,
                 dlrsn_stream_t stream) {
   const int ncell = ops->nx * ops->ny;
-  const int tiles = ((ra + kTile - 1) / kTile) * ((rb + kTile - 1) / kTile);
-  const int cpb = cells_per_block(ncell, tiles);
-  const int nblk = (ncell + cpb - 1) / cpb;
+  const MgramPlan pl = mgram_plan(ncell, ra, rb);
+  const int nblk = pl.nblk;
   cudaStream_t st = as_stream(stream);
-  mgram_mma_kernel<<<dim3(nblk, tiles), kTile * kTile, 0, st>>>(ncell, ra, rb, A, lda, B, ldb, coeff,
-                                                            *ops, cpb, partial);
-  DLRSN_CHECK_LAUNCH("mgram_mma_kernel");
+  if (pl.tb == 0) {
+    mgram_mma_kernel<<<dim3(nblk, pl.tiles), kTile * kTile, 0, st>>>(ncell, ra, rb, A, lda, B, ldb,
+                                                                     coeff, *ops, pl.cpb, partial);
+    DLRSN_CHECK_LAUNCH("mgram_mma_kernel");
+  } else {
+    const int vec = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) |
+                      (uintptr_t)lda * 8 | (uintptr_t)ldb * 8) & 15) == 0;
+    const bool same = A == B && lda == ldb && pl.tiles == 1;  // every block then takes the same path
+    if (pl.tb == 64) {
+      const size_t smem = MgramWide<64>::smem(same);
+      DLRSN_TRY_CUDA(cudaFuncSetAttribute(mgram_wide_kernel<64>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      mgram_wide_kernel<64><<<dim3(nblk, pl.tiles), 256, smem, st>>>(ncell, ra, rb, A, lda, B, ldb,
+                                                                     coeff, *ops, pl.cpb, partial, vec);
+    } else {
+      const size_t smem = MgramWide<32>::smem(same);
+      DLRSN_TRY_CUDA(cudaFuncSetAttribute(mgram_wide_kernel<32>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      mgram_wide_kernel<32><<<dim3(nblk, pl.tiles), 256, smem, st>>>(ncell, ra, rb, A, lda, B, ldb,
+                                                                     coeff, *ops, pl.cpb, partial, vec);
+    }
+    DLRSN_CHECK_LAUNCH("mgram_wide_kernel");
+  }
   const int64_t len = (int64_t)ra * rb;
   reduce_partials_kernel<<<(unsigned)((len + 31) / 32), 1024, 0, st>>>(nblk, len, partial, G, 1.0);
   DLRSN_CHECK_LAUNCH("reduce_partials_kernel");
@@ -1757,6 +2217,57 @@ int dlrsn_row_combine(int n, int r, const double* Binv, const double* ms, const 
 int dlrsn_deim(int n, int r, double* Wwork, const double* W, int* idx, double* Lhat, double* U,
                int* err_col, dlrsn_stream_t stream) {
   DLRSN_REQUIRE(r <= n, "rank %d exceeds the %d available nodes", r, n);
+  DLRSN_REQUIRE(r <= DLRSN_MAX_RANK, "rank %d exceeds DLRSN_MAX_RANK", r);
+  // cluster variant: about 256 rows per CTA, up to 16 CTAs (non-portable
+  // cluster size, checked against the occupancy calculator once)
+  static const char* ecs = getenv("DLRSN_DEIM_CS");
+  int cs = 1;
+  if (ecs) cs = atoi(ecs);
+  else while (cs < 16 && cs * 256 < n) cs *= 2;
+  auto csmem = [&](int c) {
+    const int64_t nl = (n + c - 1) / c;
+    return (nl * r + 2 * (r + 2) + r) * (int64_t)sizeof(double) + nl;
+  };
+  while (cs < 16 && csmem(cs) > 200 * 1024) cs *= 2;
+  static int max_cs = 0;
+  if (max_cs == 0) {
+    max_cs = 8;
+    DLRSN_TRY_CUDA(cudaFuncSetAttribute(deim_cluster_kernel,
+                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    DLRSN_TRY_CUDA(cudaFuncSetAttribute(deim_cluster_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    cudaLaunchConfig_t qc = {};
+    qc.gridDim = dim3(16);
+    qc.blockDim = dim3(kDeimCT);
+    qc.dynamicSmemBytes = 200 * 1024;
+    cudaLaunchAttribute qa;
+    qa.id = cudaLaunchAttributeClusterDimension;
+    qa.val.clusterDim.x = 16;
+    qa.val.clusterDim.y = qa.val.clusterDim.z = 1;
+    qc.attrs = &qa;
+    qc.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, deim_cluster_kernel, &qc) == cudaSuccess && ncl > 0)
+      max_cs = 16;
+    cudaGetLastError();
+  }
+  if (cs >= 1 && cs <= max_cs && csmem(cs) <= 200 * 1024) {
+    const int nl = (n + cs - 1) / cs;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(cs);
+    lc.blockDim = dim3(kDeimCT);
+    lc.dynamicSmemBytes = (size_t)csmem(cs);
+    lc.stream = as_stream(stream);
+    cudaLaunchAttribute la;
+    la.id = cudaLaunchAttributeClusterDimension;
+    la.val.clusterDim.x = cs;
+    la.val.clusterDim.y = la.val.clusterDim.z = 1;
+    lc.attrs = &la;
+    lc.numAttrs = 1;
+    DLRSN_TRY_CUDA(cudaLaunchKernelEx(&lc, deim_cluster_kernel, n, r, nl, W, idx, Lhat, U, err_col));
+    DLRSN_CHECK_LAUNCH("deim_cluster_kernel");
+    return DLRSN_OK;
+  }
   const size_t smem = (size_t)n * r * sizeof(double) + (size_t)n;
   const int in_smem = smem <= 200 * 1024;
   if (in_smem)

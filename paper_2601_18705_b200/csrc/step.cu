@@ -248,6 +248,7 @@ struct StepBufs {
   unsigned* rbdev;
   double* ratiow;
   int* cholw;
+  double *Rw1, *Rw1inv, *Rw2, *Rw2inv, *ratiow2, *lq1;  // angular CholQR2, r > 32
   Upload* up;
 };
 
@@ -318,8 +319,28 @@ static size_t carve(Arena& ar, StepBufs& b, int nx, int ny, int r, int no, int w
   b.rbdev = ar.take<unsigned>(8192);
   b.ratiow = ar.take<double>(2 * r);
   b.cholw = ar.take<int>(2);
+  b.Rw1 = ar.take<double>((size_t)r * r);
+  b.Rw1inv = ar.take<double>((size_t)r * r);
+  b.Rw2 = ar.take<double>((size_t)r * r);
+  b.Rw2inv = ar.take<double>((size_t)r * r);
+  b.ratiow2 = ar.take<double>(2 * r);
+  b.lq1 = ar.take<double>((size_t)no * r);
   b.up = ar.take<Upload>(1);
   return ar.off;
+}
+
+// CholQR2 guard threshold (min R_kk / |a_k| over the columns) and a debug
+// print of the observed minimum (DLRSN_GUARD_RATIO / DLRSN_GUARD_DEBUG)
+static double guard_ratio() {
+  static const double v = [] {
+    const char* e = getenv("DLRSN_GUARD_RATIO");
+    return e ? atof(e) : 1e-6;
+  }();
+  return v;
+}
+static bool guard_debug() {
+  static const bool v = getenv("DLRSN_GUARD_DEBUG") != nullptr;
+  return v;
 }
 
 #define DLRSN_RET(expr)              \
@@ -875,10 +896,21 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
       if (p->check_state) DLRSN_RET(dlrsn_mgram(ops, r, r, X_new, r, X_new, r, nullptr, b.G, b.part, ss2));
     }
     DLRSN_RET(dlrsn_rowmix(no, r, r, W, r, b.gamma, r, 0.0, b.lfull, r, s));
-    if (!exact_w)
+    if (!exact_w && ang_fast) {
       DLRSN_RET(dlrsn_cholqr2_small(no, r, b.lfull, r, p->weights_dev, W_new, r, b.Rang,
                                     b.ratiow, b.cholw, b.defw, s));
-    else
+    } else if (!exact_w) {
+      // the same weighted CholQR2 over row blocks (r > 32): Gram, Cholesky,
+      // Q = W R^-1, twice; R = R2 R1
+      DLRSN_RET(wgram(no, r, b.lfull, p->weights_dev, b.wpart, b.wg, st));
+      DLRSN_RET(dlrsn_chol_upper(r, b.wg, b.Rw1, b.Rw1inv, b.ratiow, b.cholw, s));
+      DLRSN_RET(dlrsn_rowmix(no, r, r, b.lfull, r, b.Rw1inv, r, 0.0, b.lq1, r, s));
+      DLRSN_RET(wgram(no, r, b.lq1, p->weights_dev, b.wpart, b.wg, st));
+      DLRSN_RET(dlrsn_chol_upper(r, b.wg, b.Rw2, b.Rw2inv, b.ratiow2, b.cholw + 1, s));
+      DLRSN_RET(dlrsn_rowmix(no, r, r, b.lq1, r, b.Rw2inv, r, 0.0, W_new, r, s));
+      DLRSN_RET(dlrsn_small_matmul(r, r, r, b.Rw2, b.Rw1, b.Rang, 0, s));
+      DLRSN_TRY_CUDA(cudaMemsetAsync(b.defw, 0, r * sizeof(int), st));
+    } else
       DLRSN_RET(dlrsn_cgs2(no, r, b.lfull, r, W_new, r, b.Rang, b.defw, 0, p->weights_dev,
                            nullptr, 0, r + 8, b.up->aexp, p->omegas_dev, b.cgsws, b.statw, 1, s));
     DLRSN_RET(wgram(no, r, W_new, p->weights_dev, b.wpart, b.wg, st));
@@ -893,7 +925,7 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
   };
 
   int exact = p->gs_method == 1 ? 1 : 0;
-  int exact_w = ang_fast ? 0 : 1;
+  int exact_w = 0;
   // iteration batch: sticky (only grows), so the graph keys stay stable
   const int batch0 = std::min(std::max(g_si_hint + 1, 6), 24);
   int it_next = std::min(p->si_max_iters, batch0) + 1;
@@ -964,7 +996,12 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
       // column retains >= 1e-6 of its M-norm and sits 100x above the
       // reference's deficiency threshold 1e-12 max(|v|, 1) (angular.py:137)
       bool ok = hs->cholflag[0] == 0;
-      for (int k = 0; k < r && ok; ++k) ok = hs->ratio[k] >= 1e-6 && hs->ratio[r + k] >= 1e-10;
+      if (guard_debug()) {
+        double mn = 1e300;
+        for (int k = 0; k < r; ++k) mn = std::min(mn, hs->ratio[k]);
+        fprintf(stderr, "dlrsn guard: spatial min ratio %.3e\n", mn);
+      }
+      for (int k = 0; k < r && ok; ++k) ok = hs->ratio[k] >= guard_ratio() && hs->ratio[r + k] >= 1e-10;
       if (!ok) {
         info->gs_fallback |= 1;
         exact = 1;
@@ -984,7 +1021,12 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     }
     if (!exact_w) {  // same guard for the angular CholQR2 (angular.py:137 threshold)
       bool ok = hs->cholw[0] == 0 && hs->cholw[1] == 0;
-      for (int k = 0; k < r && ok; ++k) ok = hs->ratiow[k] >= 1e-6 && hs->ratiow[r + k] >= 1e-10;
+      if (guard_debug()) {
+        double mn = 1e300;
+        for (int k = 0; k < r; ++k) mn = std::min(mn, hs->ratiow[k]);
+        fprintf(stderr, "dlrsn guard: angular min ratio %.3e\n", mn);
+      }
+      for (int k = 0; k < r && ok; ++k) ok = hs->ratiow[k] >= guard_ratio() && hs->ratiow[r + k] >= 1e-10;
       if (!ok) {
         info->gs_fallback |= 2;
         exact_w = 1;

@@ -26,7 +26,11 @@ def _rel(a, b):
 @pytest.mark.parametrize("n,kx,ky,ldx,beta", [
     (1000, 16, 16, 16, 0.0), (1000, 16, 1, 16, 0.0), (997, 13, 11, 13, 0.0),
     (50, 5, 3, 5, 0.0), (5000, 32, 16, 32, 0.0), (333, 40, 20, 40, 0.0),
-    (4096, 8, 8, 24, 0.5), (1003, 16, 16, 16, -1.25), (70, 3, 9, 7, 0.0)])
+    (4096, 8, 8, 24, 0.5), (1003, 16, 16, 16, -1.25), (70, 3, 9, 7, 0.0),
+    # wide operands (rowmix_wide_kernel): r = 32 .. 128, ragged and strided
+    (100000, 64, 64, 64, 0.0), (4099, 64, 1, 64, 0.0), (3001, 128, 128, 128, 0.5),
+    (2000, 96, 70, 100, -1.0), (1000, 32, 32, 32, 0.0), (777, 12, 40, 12, 0.0),
+    (5003, 64, 33, 66, 0.0), (640, 17, 24, 17, 0.0)])
 def test_rowmix_matches_numpy(n, kx, ky, ldx, beta):
     from paper_2601_18705_b200.lowrank import rowmix
 
@@ -43,7 +47,11 @@ def test_rowmix_matches_numpy(n, kx, ky, ldx, beta):
 
 @pytest.mark.parametrize("nx,ny,ra,rb,same,with_coeff", [
     (12, 9, 16, 16, True, False), (12, 9, 16, 16, False, True), (7, 5, 5, 19, False, False),
-    (20, 17, 20, 20, True, True), (33, 4, 1, 1, True, False), (9, 9, 8, 3, False, True)])
+    (20, 17, 20, 20, True, True), (33, 4, 1, 1, True, False), (9, 9, 8, 3, False, True),
+    # wide bases (mgram_wide_kernel, 32- and 64-wide output blocks)
+    (40, 30, 64, 64, True, False), (33, 20, 64, 64, False, True), (25, 25, 40, 40, True, True),
+    (20, 20, 128, 128, True, False), (17, 9, 64, 37, False, False), (31, 31, 100, 20, False, True),
+    (128, 96, 64, 64, True, True)])
 def test_mass_gram_matches_numpy(nx, ny, ra, rb, same, with_coeff):
     from paper_2601_18705_b200.lowrank import mass_gram
     from paper_2601_18705_b200.mesh import build_grid, cell_blocks
