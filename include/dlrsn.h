@@ -144,6 +144,40 @@ int dlrsn_rhs_build(const dlrsn_cellops* ops, int D, const int* quad, const doub
                     double inv_cdt, const double* psi_time, int ld_psi_time,
                     const double* extra, int ld_extra, double* rhs_sk, dlrsn_stream_t stream);
 
+/* Isotropic inflow boundary (BASELINE config 3; the reference is vacuum-only,
+ * transport_sn.py:11-13).  inflow = HOST double[4]: psi_b on the left,
+ * right, bottom, top walls (0 = vacuum).  Adds |omega.n| psi_b (e2 row sums)
+ * to the wall edge dofs of each direction's SK rhs -- the reference's
+ * `extra_source` slot of source_iteration (transport_sn.py:387,406-407).
+ * omegas: device (rows, 3); slot d uses row map[d] (map NULL: row d). */
+int dlrsn_inflow_add(const dlrsn_cellops* ops, int D, const int* quad, const double* omegas,
+                     const int* map, const double* inflow, double* rhs_sk,
+                     dlrsn_stream_t stream);
+/* h (4 x r, device) = X^T g_w for the unit inflow load g_w of each wall w
+ * with inflow[w] != 0 (0 elsewhere): the inflow part of the projected row
+ * source, q_all[d] += sum_w max(-omega_d.n_w, 0) psi_b,w h[w]. */
+int dlrsn_inflow_project(const dlrsn_cellops* ops, int r, const double* X, int ldx,
+                         const double* inflow, double* h, dlrsn_stream_t stream);
+
+/* ---- K6: diffusion synthetic acceleration (transport_sn.py:166-198,
+ * 325-367, applied at :439-441) */
+
+/* doubles of workspace dlrsn_dsa_correct needs */
+int64_t dlrsn_dsa_workspace_len(int nx, int ny);
+/* phi_out = phi_half + delta, delta the Jacobi-PCG solution (x0 = 0, stop at
+ * ||r|| <= tol ||b||, at most max_iters) of the consistent diffusion system
+ * ((Px^T Mt^-1 Px + Py^T Mt^-1 Py)/3 + 2 kx Jx + 2 ky Jy + M_(sigma_t-sigma_s))
+ * delta = M (sigma_s (phi_half - phi_old)), matrix-free on the structured
+ * grid, in one cooperative launch.  kx = ky = 1/4 is the reference's
+ * "simplified" penalty, the "collocation" one is 1/2 cw.|omega_x| / (4 pi).
+ * info (device int[2]) = {CG iterations, 1 if max_iters was reached};
+ * history (device, nullable) gets ||r_k|| for k < hist_cap. */
+int dlrsn_dsa_correct(const dlrsn_cellops* ops, const double* sigma_t, const double* sigma_s,
+                      double kx, double ky, const double* phi_half, const double* phi_old,
+                      double* phi_out, double tol, int max_iters, double* workspace,
+                      int64_t workspace_len, int* info, double* history, int hist_cap,
+                      dlrsn_stream_t stream);
+
 /* scalar per cell -> 4 quadrant SK slabs (out + k*sk_scalar_len) */
 int dlrsn_cells_to_sk4(const dlrsn_cellops* ops, const double* cell_values, double* out_sk4,
                        dlrsn_stream_t stream);
@@ -312,6 +346,7 @@ typedef struct dlrsn_step_params {
   int gs_method;             /* 0: CholQR2 guarded by exact CGS2, 1: exact CGS2 */
   int sweep_dw;              /* sweep group width (0 = 1) */
   const dlrsn_advance* advance; /* optional fused T update + re-linearisation (NULL: none) */
+  double inflow[4];          /* isotropic inflow psi_b: left, right, bottom, top (0: vacuum) */
 } dlrsn_step_params;
 
 typedef struct dlrsn_step_info { /* HOST, filled by the call */

@@ -650,6 +650,64 @@ def source_iteration(ops, omegas, closure, psi_time=None, *, use_dsa=True, tol=1
     raise IterationLimitError("source iteration did not converge", max_iters, change)
 
 
+# --------------------------------------------------------------------------
+# isotropic inflow boundary (BASELINE config 3) -- NOT in the reference, which
+# is vacuum-only (transport_sn.py:11-13: "on the boundary the exterior state is
+# zero").  Restatement: with a constant exterior state psi_b on an inflow wall
+# the upwind face flux contributes the same coupling the interior faces use
+# (|omega.n| * e2, the ``couple`` blocks of transport_sn.py:219-224) applied to
+# psi_b [1, 1]: |omega.n| * psi_b * (e2 @ [1, 1]) on the wall's edge dofs.  It
+# enters the sweep through the reference's ``extra_source`` slot
+# (transport_sn.py:387,406-407) and the reduced rows through X^T of the same
+# load.  With psi_b = 0 everything reduces to the reference.
+
+WALLS = ("left", "right", "bottom", "top")
+WALL_NORMALS = {"left": (-1.0, 0.0), "right": (1.0, 0.0), "bottom": (0.0, -1.0),
+                "top": (0.0, 1.0)}
+
+
+def inflow_tuple(inflow):
+    """None | {wall: psi_b} | 4 values (left, right, bottom, top) -> 4-tuple or None."""
+    if inflow is None:
+        return None
+    if isinstance(inflow, dict):
+        bad = set(inflow) - set(WALLS)
+        if bad:
+            raise ContractViolation(f"unknown inflow walls {sorted(bad)}")
+        vals = tuple(float(inflow.get(w, 0.0)) for w in WALLS)
+    else:
+        vals = tuple(float(v) for v in inflow)
+        if len(vals) != 4:
+            raise ContractViolation("inflow needs 4 values (left, right, bottom, top)")
+    if any(not np.isfinite(v) or v < 0 for v in vals):
+        raise ContractViolation("inflow intensities must be finite and non-negative")
+    return vals if any(vals) else None
+
+
+def inflow_load(grid, omegas, inflow):
+    """(n_dofs, D) load of an isotropic inflow: column d gets
+    max(-omega_d.n_w, 0) * psi_b,w * (e2 @ [1, 1]) on the edge dofs of every
+    cell of each wall w."""
+    vals = inflow_tuple(inflow)
+    om = np.atleast_2d(np.asarray(omegas, dtype=float))
+    out = np.zeros((grid.n_dofs, om.shape[0]))
+    if vals is None:
+        return out
+    edge = q1_blocks()[3]
+    cid = np.arange(grid.n_cells).reshape(grid.ny, grid.nx)
+    cells = {"left": cid[:, 0], "right": cid[:, -1], "bottom": cid[0, :], "top": cid[-1, :]}
+    for w, psi_b in zip(WALLS, vals):
+        if psi_b == 0.0:
+            continue
+        e2 = (grid.dy if w in ("left", "right") else grid.dx) * edge
+        g = e2 @ np.ones(2)
+        n = WALL_NORMALS[w]
+        coef = np.maximum(-(om[:, 0] * n[0] + om[:, 1] * n[1]), 0.0) * psi_b
+        for k, l in enumerate(EDGE[w]):
+            out[4 * cells[w] + l, :] += g[k] * coef[None, :]
+    return out
+
+
 def boundary_outflow(grid, psi, omegas, weights):
     """transport_sn.py:479-492 (trapezoid rule on the boundary traces)."""
     psi = np.asarray(psi)
@@ -810,8 +868,9 @@ class StepInfo:
 
 
 def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, use_dsa=True,
-                     dsa_penalty="simplified", threads=0, check_state=True):
-    """One implicit DLR-SN step, Algorithm 1 (dlr_sn.py:86-151)."""
+                     dsa_penalty="simplified", threads=0, check_state=True, inflow=None):
+    """One implicit DLR-SN step, Algorithm 1 (dlr_sn.py:86-151).  ``inflow``
+    (not in the reference): isotropic inflow walls, see ``inflow_load``."""
     sel = deim_select(state.W)
     closure = sel.closure_weights(state.beta)
     om_sel = quad.omegas[sel.indices]
@@ -820,14 +879,18 @@ def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, 
     if check_state:
         state_check(state, ops, quad)
     psi_time = state.X @ (state.S @ state.W[sel.indices].T)  # evaluate_rows, lowrank.py:220-227
+    extra = inflow_load(grid, om_sel, inflow) if inflow_tuple(inflow) else None
     res = source_iteration(ops, om_sel, closure, psi_time=psi_time, use_dsa=use_dsa, tol=si_tol,
-                           max_iters=si_max_iters, phi_start=state.scalar_flux())
+                           max_iters=si_max_iters, phi_start=state.scalar_flux(),
+                           extra_source=extra)
     comp = spatial_monomials(dof_coordinates(grid), grid.extent, state.rank + 8)
     x_new, _, dx_ = gram_schmidt(res.psi, mass_dot(ops), comp)
     proj = project_row_operators(ops, x_new)
     B = row_matrices(proj, om_sel)
     l_time = project_initial(state, x_new, ops)[sel.indices]
     q_all = proj["q"][None, :] + step.inv_cdt * l_time
+    if extra is not None:  # Galerkin rows of the inflow load
+        q_all = q_all + (x_new.T @ extra).T
     l_nodes, l_bar = solve_row_system(B, proj["ms"], q_all, closure)
     gamma = sel.interpolation_coefficients(l_nodes)
     l_full = state.W @ gamma

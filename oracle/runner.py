@@ -83,7 +83,8 @@ def run(spec, state, n_steps, *, si_tol=1e-12, si_max_iters=400, use_dsa=False,
         lin = linearized(spec, T)
         state, info = P.step_collocation(grid, lin, quad, state, si_tol=si_tol,
                                          si_max_iters=si_max_iters, use_dsa=use_dsa,
-                                         check_state=check_state)
+                                         check_state=check_state,
+                                         inflow=getattr(spec, "inflow", None))
         T = advance_temperature(spec, lin, info.phi)
         infos.append(info)
         if record is not None:

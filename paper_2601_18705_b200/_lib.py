@@ -49,7 +49,7 @@ class StepParams(ctypes.Structure):
     _fields_ = [("rank", c_int), ("n_omega", c_int), ("omegas_host", c_vp), ("omegas_dev", c_vp),
                 ("weights_dev", c_vp), ("inv_cdt", c_dbl), ("si_tol", c_dbl),
                 ("si_max_iters", c_int), ("check_state", c_int), ("gs_method", c_int),
-                ("sweep_dw", c_int), ("advance", c_vp)]
+                ("sweep_dw", c_int), ("advance", c_vp), ("inflow", c_dbl * 4)]
 
 
 class StepInfo(ctypes.Structure):
@@ -95,6 +95,11 @@ _SIGNATURES = {
                                           c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "dlrsn_rhs_build": (c_int, [c_vp, c_int, c_vp, c_vp, c_dbl, c_vp, c_int, c_vp, c_int, c_vp,
                                 c_vp]),
+    "dlrsn_inflow_add": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "dlrsn_inflow_project": (c_int, [c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_vp]),
+    "dlrsn_dsa_workspace_len": (c_i64, [c_int, c_int]),
+    "dlrsn_dsa_correct": (c_int, [c_vp, c_vp, c_vp, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_dbl, c_int,
+                                  c_vp, c_i64, c_vp, c_vp, c_int, c_vp]),
     "dlrsn_cells_to_sk4": (c_int, [c_vp, c_vp, c_vp, c_vp]),
     "dlrsn_scatter_source": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "dlrsn_phi_combine": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
@@ -170,6 +175,9 @@ def check(status, what=""):
 
 
 def call(name, *args):
+    nargs = len(_SIGNATURES[name][1])
+    if len(args) != nargs:  # ctypes would pass surplus arguments through
+        raise TypeError(f"{name} takes {nargs} arguments ({len(args)} given)")
     check(getattr(load(), name)(*args), name)
 
 

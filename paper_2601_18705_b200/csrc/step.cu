@@ -119,10 +119,14 @@ __global__ void ortho_residual_kernel(int r, const double* __restrict__ Gx,
 }
 
 // q_all[d][j] = qhat[j] + inv_cdt * (W_sel (S^T mo))[d][j]  (dlr_sn.py:130-131)
+// + sum_w max(-omega_d.n_w, 0) psi_b,w h[w][j]: the projected inflow load of
+// the selected direction d (isotropic inflow walls, h = X_new^T g_w; hin null
+// for vacuum walls, the reference's case)
 __global__ void qall_kernel(int r, const double* __restrict__ S, const double* __restrict__ mo,
                             const double* __restrict__ qhat, const double* __restrict__ W,
                             const int* __restrict__ idx, double inv_cdt, double* __restrict__ T,
-                            double* __restrict__ qall) {
+                            double* __restrict__ qall, const double* __restrict__ hin,
+                            Inflow4 inflow, const double* __restrict__ om_sel) {
   for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
     const int i = e / r, j = e % r;
     double s = 0.0;
@@ -135,7 +139,17 @@ __global__ void qall_kernel(int r, const double* __restrict__ S, const double* _
     const double* w = W + (int64_t)idx[d] * r;
     double s = 0.0;
     for (int i = 0; i < r; ++i) s = fma(w[i], T[i * r + j], s);
-    qall[e] = qhat[j] + inv_cdt * s;
+    double v = qhat[j] + inv_cdt * s;
+    if (hin) {
+      const double ox = om_sel[3 * d], oy = om_sel[3 * d + 1];
+      const double c[4] = {inflow.v[0] * fmax(ox, 0.0), inflow.v[1] * fmax(-ox, 0.0),
+                           inflow.v[2] * fmax(oy, 0.0), inflow.v[3] * fmax(-oy, 0.0)};
+      double a = 0.0;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) a = fma(c[w], hin[w * r + j], a);
+      v += a;
+    }
+    qall[e] = v;
   }
 }
 
@@ -249,6 +263,7 @@ struct StepBufs {
   double* ratiow;
   int* cholw;
   double *Rw1, *Rw1inv, *Rw2, *Rw2inv, *ratiow2, *lq1;  // angular CholQR2, r > 32
+  double* hin;  // X_new^T of the unit inflow load per wall (4 x r)
   Upload* up;
 };
 
@@ -325,6 +340,7 @@ static size_t carve(Arena& ar, StepBufs& b, int nx, int ny, int r, int no, int w
   b.Rw2inv = ar.take<double>((size_t)r * r);
   b.ratiow2 = ar.take<double>(2 * r);
   b.lq1 = ar.take<double>((size_t)no * r);
+  b.hin = ar.take<double>(4 * (size_t)r);
   b.up = ar.take<Upload>(1);
   return ar.off;
 }
@@ -735,6 +751,12 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
   StepStatus* hs = nullptr;
   DLRSN_RET(status_block(&hs));
   double* P[2] = {b.phi0, b.phi1};
+  Inflow4 infl;
+  bool has_inflow = false;
+  for (int w = 0; w < 4; ++w) {
+    infl.v[w] = p->inflow[w];
+    has_inflow |= p->inflow[w] != 0.0;
+  }
 
   // ---- the step as segments of device work, each closed by the packed
   // status readback (so a segment is one host synchronisation) ------------
@@ -802,9 +824,12 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
       pt_local = b.psi;
       ld_pt = nl;
     }
-    if (nl > 0)
+    if (nl > 0) {
       DLRSN_RET(dlrsn_rhs_build(ops, nl, b.quads, q, p->inv_cdt, pt_local, ld_pt, nullptr, 1,
                                 b.rhs_sk, s));
+      if (has_inflow)
+        DLRSN_RET(dlrsn_inflow_add(ops, nl, b.quads, b.om_sel, b.mine, p->inflow, b.rhs_sk, s));
+    }
     DLRSN_RET(join_from(fk, st));
     return DLRSN_OK;
   };
@@ -875,8 +900,10 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
                            r + 8, b.up->sexp, b.up->extent, b.cgsws, b.statx, 1, s));
     }
     DLRSN_RET(dlrsn_project(ops, r, X_new, X, sigma_t, sigma_s, q, b.proj, b.part, s));
+    if (has_inflow) DLRSN_RET(dlrsn_inflow_project(ops, r, X_new, r, p->inflow, b.hin, s));
     qall_kernel<<<1, 256, 0, st>>>(r, S, b.proj + 6 * r * r, b.proj + 7 * r * r, W, b.idx,
-                                   p->inv_cdt, b.T, b.qall);
+                                   p->inv_cdt, b.T, b.qall, has_inflow ? b.hin : nullptr, infl,
+                                   b.om_sel);
     DLRSN_CHECK_LAUNCH("qall_kernel");
     DLRSN_TRY_CUDA(cudaMemsetAsync(b.rowstat, 0, (r + 1) * sizeof(int), st));
     DLRSN_RET(dlrsn_row_inverse(r, r, b.proj, b.om_sel, b.Binv, nullptr, b.rowstat, s));

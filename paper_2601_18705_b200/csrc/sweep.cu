@@ -328,6 +328,93 @@ __global__ void rhs_build_kernel(int nx, int ny, int D, const int* __restrict__ 
   o[sk_vec_off(T, s, t, 1, lane) >> 1] = make_double2(v[2 ^ f], v[3 ^ f]);
 }
 
+// ---- isotropic inflow boundary (BASELINE config 3) -------------------------
+// The reference is vacuum-only (transport_sn.py:11-13: exterior state 0).  An
+// isotropic inflow psi_b on a wall is the upwind face flux of a constant
+// exterior state: the inflow coupling |omega.n| * e2 (transport_sn.py:219-224)
+// applied to psi_b [1, 1], i.e. |omega.n| psi_b (e2 row sums) on the wall's
+// two edge dofs of every wall cell.  Added to the sweep rhs of each direction
+// (the reference's `extra_source` slot, transport_sn.py:406-407).  In the
+// oriented SK frame the x-inflow wall is i' = 0 (oriented dofs 0', 2') and the
+// y-inflow wall j' = 0 (dofs 0', 1').  Thread (d, k): k < ny is the x-wall cell
+// of oriented row k (it also adds the y term of the corner cell), k >= ny the
+// y-wall cell of oriented column k - ny > 0, so no two threads touch a cell.
+__global__ void inflow_add_kernel(int nx, int ny, int D, const int* __restrict__ quad,
+                                  const double* __restrict__ om, const int* __restrict__ map,
+                                  Inflow4 inflow, double exs, double eys,
+                                  double* __restrict__ rhs, int64_t vlen) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int K = nx + ny;
+  if (idx >= (int64_t)K * D) return;
+  const int d = (int)(idx / K);
+  const int k = (int)(idx - (int64_t)d * K);
+  const int qd = quad[d];
+  const int row = map ? map[d] : d;
+  const double bx = inflow.v[(qd & 1) ? 1 : 0];
+  const double by = inflow.v[(qd & 2) ? 3 : 2];
+  const double ax = fabs(om[3 * (int64_t)row]) * bx * exs;
+  const double ay = fabs(om[3 * (int64_t)row + 1]) * by * eys;
+  const int T = nx + 31;
+  double2* o = reinterpret_cast<double2*>(rhs + (int64_t)d * vlen);
+  if (k < ny) {  // oriented (i' = 0, j' = k)
+    const int s = k >> 5, lane = k & 31, t = lane;
+    double2 p0 = o[sk_vec_off(T, s, t, 0, lane) >> 1];
+    double2 p1 = o[sk_vec_off(T, s, t, 1, lane) >> 1];
+    p0.x += ax;
+    p1.x += ax;
+    if (k == 0) {
+      p0.x += ay;
+      p0.y += ay;
+    }
+    o[sk_vec_off(T, s, t, 0, lane) >> 1] = p0;
+    o[sk_vec_off(T, s, t, 1, lane) >> 1] = p1;
+  } else {  // oriented (i' = k - ny, j' = 0), i' > 0
+    const int ip = k - ny;
+    if (ip == 0) return;
+    double2 p0 = o[sk_vec_off(T, 0, ip, 0, 0) >> 1];
+    p0.x += ay;
+    p0.y += ay;
+    o[sk_vec_off(T, 0, ip, 0, 0) >> 1] = p0;
+  }
+}
+
+// h[w][k] = sum over the cells of wall w of (e2 row sums) . X[edge dofs][k]:
+// X^T of the unit inflow load of wall w (block (k, w)); walls without inflow
+// get 0.  Fixed-order block reduction (deterministic).
+__global__ void __launch_bounds__(256) inflow_project_kernel(int nx, int ny, int r,
+                                                             const double* __restrict__ X,
+                                                             int ldx, Inflow4 inflow,
+                                                             dlrsn_cellops ops,
+                                                             double* __restrict__ h) {
+  const int k = blockIdx.x, w = blockIdx.y;
+  __shared__ double red[8];
+  double acc = 0.0;
+  if (inflow.v[w] != 0.0) {
+    const bool vert = w < 2;
+    const int ncell = vert ? ny : nx;
+    const double* e2 = vert ? ops.e2x : ops.e2y;
+    const double g0 = e2[0] + e2[1], g1 = e2[2] + e2[3];
+    // edge dofs (mesh.py:34-39): left (0,2) right (1,3) bottom (0,1) top (2,3)
+    const int l0 = w == 0 ? 0 : w == 1 ? 1 : w == 2 ? 0 : 2;
+    const int l1 = w == 0 ? 2 : w == 1 ? 3 : w == 2 ? 1 : 3;
+    for (int m = threadIdx.x; m < ncell; m += blockDim.x) {
+      const int i = vert ? (w == 0 ? 0 : nx - 1) : m;
+      const int j = vert ? m : (w == 2 ? 0 : ny - 1);
+      const int64_t c = (int64_t)j * nx + i;
+      acc = fma(g0, X[(4 * c + l0) * ldx + k], acc);
+      acc = fma(g1, X[(4 * c + l1) * ldx + k], acc);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) s += red[q];
+    h[w * r + k] = s;
+  }
+}
+
 __global__ void cells_to_sk4_kernel(int nx, int ny, const double* __restrict__ v,
                                     double* __restrict__ out, int64_t slen) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -774,6 +861,36 @@ int dlrsn_rhs_build(const dlrsn_cellops* ops, int D, const int* quad, const doub
       ops->nx, ops->ny, D, quad, q, inv_cdt, psi_time, ld_psi_time, extra, ld_extra, rhs_sk,
       sk_vec_len(ops->nx, ops->ny), *ops);
   DLRSN_CHECK_LAUNCH("rhs_build_kernel");
+  return DLRSN_OK;
+}
+
+int dlrsn_inflow_add(const dlrsn_cellops* ops, int D, const int* quad, const double* omegas,
+                     const int* map, const double* inflow, double* rhs_sk,
+                     dlrsn_stream_t stream) {
+  DLRSN_REQUIRE(ops && D >= 0 && inflow, "bad arguments to dlrsn_inflow_add");
+  Inflow4 f;
+  bool any = false;
+  for (int w = 0; w < 4; ++w) {
+    f.v[w] = inflow[w];
+    any |= inflow[w] != 0.0;
+  }
+  const int64_t n = (int64_t)(ops->nx + ops->ny) * D;
+  if (!any || n == 0) return DLRSN_OK;
+  inflow_add_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(
+      ops->nx, ops->ny, D, quad, omegas, map, f, ops->e2x[0] + ops->e2x[1],
+      ops->e2y[0] + ops->e2y[1], rhs_sk, sk_vec_len(ops->nx, ops->ny));
+  DLRSN_CHECK_LAUNCH("inflow_add_kernel");
+  return DLRSN_OK;
+}
+
+int dlrsn_inflow_project(const dlrsn_cellops* ops, int r, const double* X, int ldx,
+                         const double* inflow, double* h, dlrsn_stream_t stream) {
+  DLRSN_REQUIRE(ops && r > 0 && inflow, "bad arguments to dlrsn_inflow_project");
+  Inflow4 f;
+  for (int w = 0; w < 4; ++w) f.v[w] = inflow[w];
+  inflow_project_kernel<<<dim3(r, 4), 256, 0, as_stream(stream)>>>(ops->nx, ops->ny, r, X, ldx,
+                                                                    f, *ops, h);
+  DLRSN_CHECK_LAUNCH("inflow_project_kernel");
   return DLRSN_OK;
 }
 

@@ -29,6 +29,11 @@ struct SweepArgs {
   int debug;        // bit 0: ignore the strip inflow (timing experiments only)
 };
 
+// isotropic inflow psi_b on the left, right, bottom, top walls (0: vacuum)
+struct Inflow4 {
+  double v[4];
+};
+
 // Device-side control of a batched source iteration (step.cu): iterations
 // enqueued past convergence see done = 1 and return immediately.
 struct SiCtl {

@@ -48,7 +48,7 @@ from .lowrank import (
     raise_row_status,
     rowmix,
 )
-from .transport import assemble_operators, source_iteration
+from .transport import assemble_operators, inflow_values, source_iteration
 
 FOUR_PI = 4.0 * np.pi
 
@@ -117,7 +117,7 @@ def project_initial(state, x_new, ops):
 
 def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, use_dsa=True,
                      dsa_penalty="simplified", threads=0, check_state=True, gs_method="cholqr2",
-                     sweep_dw=None, comm=None, engine="native", _advance=None):
+                     sweep_dw=None, comm=None, engine="native", inflow=None, _advance=None):
     """Advance one linearised step; returns (new DlrState, CollocationStepInfo).
 
     ``engine="native"`` issues the whole step from C++ through the single
@@ -130,6 +130,13 @@ def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, 
     iteration (convergence test) and one at the end (Gram-Schmidt guard,
     row-system status, angular deficiencies, output check).  Errors are raised
     in the reference's order (dlr_sn.py:99-141).
+
+    ``inflow`` (an extension; the reference is vacuum-only,
+    transport_sn.py:11-13): isotropic inflow intensities psi_b per wall, as
+    ``{wall: psi_b}`` or (left, right, bottom, top).  The load
+    |omega.n| psi_b (e2 row sums) on the wall edge dofs joins each selected
+    direction's sweep rhs and, projected on X_new, its reduced row source
+    (BASELINE config 3; restated in oracle/port.py ``inflow_load``).
     """
     if gs_method not in ("cholqr2", "cgs2"):
         raise ConfigurationError(f"unknown gs_method {gs_method!r}")
@@ -141,7 +148,9 @@ def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, 
         if dsa_penalty not in ("simplified", "collocation"):
             raise ContractViolation(f"unknown dsa penalty variant {dsa_penalty!r}")
         return _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state,
-                            gs_method, sweep_dw, comm, _advance)
+                            gs_method, sweep_dw, comm, _advance, inflow_values(inflow))
+    if inflow_values(inflow) is not None:
+        raise ConfigurationError("inflow boundaries need the native engine")
     if _advance is not None:
         raise ConfigurationError("the fused step boundary needs the native engine")
     r = state.rank
@@ -411,7 +420,7 @@ def _native_ctx(grid, quad, r, comm):
 
 
 def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_method, sweep_dw,
-                 comm, advance=None):
+                 comm, advance=None, inflow=None):
     r = state.rank
     no = quad.n_angles
     n = grid.n_dofs
@@ -435,6 +444,7 @@ def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_
     p.check_state = 1 if check_state else 0
     p.gs_method = 0 if gs_method == "cholqr2" else 1
     p.advance = ctypes.addressof(advance) if advance is not None else None
+    p.inflow[:] = inflow if inflow is not None else (0.0, 0.0, 0.0, 0.0)
     info = _lib.StepInfo()
     hooks = ctx.hooks
     if hooks is not None:

@@ -104,7 +104,7 @@ class DeviceProblem:
             state, info = step_collocation(self.grid, lin, self.quad, state, si_tol=si_tol,
                                            si_max_iters=si_max_iters, use_dsa=False,
                                            check_state=check_state, gs_method=gs_method,
-                                           comm=comm)
+                                           comm=comm, inflow=self.spec.inflow)
             T = T.clone()
             return state, self.advance(lin, info.phi, T), T, info
         n = self.spec.n_cells
@@ -129,7 +129,7 @@ class DeviceProblem:
         state, info = step_collocation(self.grid, lin, self.quad, state, si_tol=si_tol,
                                        si_max_iters=si_max_iters, use_dsa=False,
                                        check_state=check_state, gs_method=gs_method, comm=comm,
-                                       _advance=av)
+                                       inflow=self.spec.inflow, _advance=av)
         k = self.constants
         nxt = LinearizedStep(sigma_t=st, sigma_s=ss, sigma_a=sa, q=q, T0=T0, denom=den,
                              rho_cv=self.rho_cv, dt=float(self.spec.dt),
@@ -178,7 +178,7 @@ def run(dp, state, n_steps, *, si_tol=1e-8, si_max_iters=200, check_state=True, 
             state, info = step_collocation(dp.grid, lin, dp.quad, state, si_tol=si_tol,
                                            si_max_iters=si_max_iters, use_dsa=False,
                                            check_state=check_state, gs_method=gs_method,
-                                           engine=engine, comm=comm)
+                                           engine=engine, comm=comm, inflow=dp.spec.inflow)
             lin = dp.advance(lin, info.phi, T)
         infos.append(info)
         if record is not None:

@@ -50,6 +50,7 @@ class ProblemSpec:
     frozen_sigma_t: np.ndarray | None = None
     frozen_q: np.ndarray | None = None
     t_floor: float = 1e-6
+    inflow: tuple | None = None  # isotropic inflow psi_b (left, right, bottom, top); None: vacuum
     notes: dict = field(default_factory=dict)
 
     @property
@@ -117,6 +118,26 @@ def config1():
 def config2():
     return checkerboard(40, rank=16, n_polar=32, n_azimuthal=32, dt=0.01, n_steps=50, seed=2,
                         name="C2")
+
+
+def marshak(n=512, rank=32, n_polar=64, n_azimuthal=64, dt=1e-3, n_steps=100, seed=3,
+            sigma0=300.0, T_b=1.0, T_init=1e-4, name="C3"):
+    """C3: Marshak wave in [0,1]^2: sigma_a = sigma0 T^-3 (explicit in T, the
+    linearisation point of each step), isotropic inflow at
+    T_b on the left wall, psi_b = a c T_b^4 / (4 pi), vacuum
+    elsewhere, T0 = 1e-4, c = a = rho c_v = 1, no physical scattering or
+    external source."""
+    spec = _empty(name, n, n, (0.0, 0.0, 1.0, 1.0), n_polar, n_azimuthal, rank, dt, n_steps,
+                  seed)
+    spec.T0 = np.full(spec.n_cells, float(T_init))
+    spec.opacity = ("power", float(sigma0), -3.0)
+    spec.sigma_a = spec.opacity_at(spec.T0)
+    spec.inflow = (spec.a_r * spec.c * T_b ** 4 / FOUR_PI, 0.0, 0.0, 0.0)
+    return spec
+
+
+def config3():
+    return marshak()
 
 
 def random_medium(n=1024, rank=64, n_polar=64, n_azimuthal=64, dt=1e-2, n_steps=50, seed=4,

@@ -11,6 +11,7 @@ return types and exceptions.
 
 from __future__ import annotations
 
+import ctypes
 import math
 import threading
 from dataclasses import dataclass, field
@@ -20,7 +21,7 @@ import torch
 
 from . import _lib
 from ._device import as_device, device, empty, stream, upload, zeros
-from .errors import ConfigurationError, ContractViolation, IterationLimitError
+from .errors import CgError, ConfigurationError, ContractViolation, IterationLimitError
 from .mesh import DISCONTINUOUS, cellops_struct
 
 FOUR_PI = 4.0 * np.pi
@@ -269,24 +270,22 @@ def sweep_solve(ops, omega, rhs, _key=None):
 
 def source_iteration(ops, omegas, closure, psi_time=None, *, use_dsa=True, tol=1e-8,
                      max_iters=200, phi_start=None, extra_source=None, threads=0, dw=None,
-                     keep_sk=False, comm=None):
+                     keep_sk=False, comm=None, inflow=None):
     """Lagged-scattering iteration over device sweeps (transport_sn.py:377-450).
 
     ``threads`` is accepted for API compatibility and ignored (the sweeps of
     all directions run in one launch).  ``psi_time`` / ``extra_source`` are
     (n_dofs, n_angles) arrays; results are device tensors.  With ``comm`` (a
     sharding.DirectionComm over > 1 rank) the directions are split across
-    ranks and the closure flux is all-reduced every iteration.
+    ranks and the closure flux is all-reduced every iteration.  ``inflow``
+    (extension, see ``inflow_source``): isotropic inflow walls, added to the
+    sweep rhs on the device (dlrsn_inflow_add) next to ``extra_source``.
     """
     omegas = np.asarray(omegas.cpu() if isinstance(omegas, torch.Tensor) else omegas, dtype=float)
     closure = np.asarray(closure.cpu() if isinstance(closure, torch.Tensor) else closure, dtype=float)
     nd = omegas.shape[0]
     if closure.shape != (nd,):
         raise ContractViolation("closure vector must have one entry per swept angle")
-    if use_dsa:
-        raise ConfigurationError(
-            "use_dsa=True is not available on the B200 path yet; pass use_dsa=False "
-            "(SURVEY 4.3: DSA diverges for random angular bases)")
     g = ops.grid
     st = ops.step
     # direction sharding across ranks (sharding.py): this rank sweeps `mine`
@@ -320,6 +319,12 @@ def source_iteration(ops, omegas, closure, psi_time=None, *, use_dsa=True, tol=1
     if plan:
         _lib.call("dlrsn_rhs_build", ops.cellops_ptr, nl, _lib.ptr(plan.quads_dev), _lib.ptr(st.q),
                   float(st.inv_cdt), _lib.ptr(pt), nl, _lib.ptr(ex), nl, _lib.ptr(rhs_sk), stream())
+        inflow4 = inflow_values(inflow)
+        if inflow4 is not None:
+            om_dev = upload(np.ascontiguousarray(omegas[mine], dtype=np.float64))
+            vals = (ctypes.c_double * 4)(*inflow4)
+            _lib.call("dlrsn_inflow_add", ops.cellops_ptr, nl, _lib.ptr(plan.quads_dev),
+                      _lib.ptr(om_dev), None, vals, _lib.ptr(rhs_sk), stream())
     phi = zeros(g.n_dofs) if phi_start is None else as_device(phi_start).reshape(-1).clone()
     phi_new = empty(g.n_dofs)
     flags = zeros(1, dtype=torch.int32)
@@ -329,13 +334,25 @@ def source_iteration(ops, omegas, closure, psi_time=None, *, use_dsa=True, tol=1
     red_ws = ops.buffer("red_ws", 256 // 8 + 2 * nb + 8, zero=True)
     norms = zeros(2)
     host = torch.empty(3, dtype=torch.float64, pin_memory=True)
+    dsa = _DsaState(ops) if use_dsa else None
     change = math.inf
     for it in range(1, max_iters + 1):
-        if owners is None:
+        if owners is None and dsa is None:
             _sweep(ops, plan, rhs_sk, psi_sk, scat, part_arg)
             _lib.call("dlrsn_phi_combine", ops.cellops_ptr, plan.G, _lib.ptr(plan.groups_dev),
                       _lib.ptr(part_arg), _lib.ptr(psi_sk), _lib.ptr(phi), _lib.ptr(st.sigma_s),
                       _lib.ptr(phi_new), _lib.ptr(scat), _lib.ptr(norms), _lib.ptr(red_ws), stream())
+        elif owners is None:
+            # DSA: phi_half from the sweep, the diffusion correction, then the
+            # norms and the next scattering source from phi_half + delta
+            _sweep(ops, plan, rhs_sk, psi_sk, scat, part_arg)
+            _lib.call("dlrsn_phi_combine", ops.cellops_ptr, plan.G, _lib.ptr(plan.groups_dev),
+                      _lib.ptr(part_arg), _lib.ptr(psi_sk), _lib.ptr(phi), _lib.ptr(st.sigma_s),
+                      _lib.ptr(phi_new), None, _lib.ptr(norms), _lib.ptr(red_ws), stream())
+            dsa.correct(phi_new, phi)
+            _lib.call("dlrsn_phi_finish", ops.cellops_ptr, _lib.ptr(phi_new), _lib.ptr(phi),
+                      _lib.ptr(st.sigma_s), _lib.ptr(scat), _lib.ptr(norms), _lib.ptr(red_ws),
+                      stream())
         else:
             # local partial closure flux -> allreduce over NVLink -> norms and
             # scattering source from the summed flux (identical on all ranks)
@@ -347,13 +364,19 @@ def source_iteration(ops, omegas, closure, psi_time=None, *, use_dsa=True, tol=1
             else:
                 phi_new.zero_()
             comm.allreduce_sum_(phi_new)
+            if dsa is not None:  # replicated on every rank from the summed flux
+                dsa.correct(phi_new, phi)
             _lib.call("dlrsn_phi_finish", ops.cellops_ptr, _lib.ptr(phi_new), _lib.ptr(phi),
                       _lib.ptr(st.sigma_s), _lib.ptr(scat), _lib.ptr(norms), _lib.ptr(red_ws),
                       stream())
         host[:2].copy_(norms, non_blocking=True)
         if it == 1:
             host[2:3].copy_(flags.to(torch.float64), non_blocking=True)
+        if dsa is not None:
+            dsa.stage_info()
         torch.cuda.current_stream(device()).synchronize()
+        if dsa is not None:
+            dsa.raise_on_failure()
         phi, phi_new = phi_new, phi
         if it == 1 and host[2].item() == 0.0:  # pure absorber (transport_sn.py:410,430-432)
             return _finish(ops, plan, psi_sk, phi, 1, keep_sk, comm, owners, nd)
@@ -362,6 +385,53 @@ def source_iteration(ops, omegas, closure, psi_time=None, *, use_dsa=True, tol=1
         if change <= tol:
             return _finish(ops, plan, psi_sk, phi, it, keep_sk, comm, owners, nd)
     raise IterationLimitError("source iteration did not converge", max_iters, change)
+
+
+class _DsaState:
+    """Device state of the diffusion correction (transport_sn.py:353-367):
+    dlrsn_dsa_correct solves the Jacobi-PCG system in one cooperative launch
+    (tol 1e-10, at most 10 n_dofs iterations, the reference's pcg defaults)
+    and writes phi_half + delta in place."""
+
+    TOL = 1e-10
+    HIST = 4096
+
+    def __init__(self, ops):
+        g = ops.grid
+        st = ops.step
+        if ops.dsa_penalty == "simplified":
+            self.kx = self.ky = 0.25  # (1/2) <|omega.n|>, transport_sn.py:183-184
+        else:
+            om, cw = ops.penalty_closure
+            om = np.asarray(om.cpu() if isinstance(om, torch.Tensor) else om, dtype=float)
+            cw = np.asarray(cw.cpu() if isinstance(cw, torch.Tensor) else cw, dtype=float)
+            self.kx = 0.5 * float(cw @ np.abs(om[:, 0])) / FOUR_PI  # :186-188
+            self.ky = 0.5 * float(cw @ np.abs(om[:, 1])) / FOUR_PI
+        self.ops = ops
+        self.max_iters = 10 * g.n_dofs
+        ln = int(_lib.load().dlrsn_dsa_workspace_len(g.nx, g.ny))
+        self.ws = ops.buffer("dsa_ws", ln)
+        self.ws_len = ln
+        self.info = ops.buffer("dsa_info", 2, dtype=torch.int32)
+        self.hist = ops.buffer("dsa_hist", self.HIST)
+        self.host = torch.empty(2, dtype=torch.int32, pin_memory=True)
+        self.sigma_t, self.sigma_s = st.sigma_t, st.sigma_s
+
+    def correct(self, phi_half, phi_old):
+        _lib.call("dlrsn_dsa_correct", self.ops.cellops_ptr, _lib.ptr(self.sigma_t),
+                  _lib.ptr(self.sigma_s), self.kx, self.ky, _lib.ptr(phi_half),
+                  _lib.ptr(phi_old), _lib.ptr(phi_half), self.TOL, self.max_iters,
+                  _lib.ptr(self.ws), self.ws_len, _lib.ptr(self.info), _lib.ptr(self.hist),
+                  self.HIST, stream())
+
+    def stage_info(self):
+        self.host.copy_(self.info[:2], non_blocking=True)
+
+    def raise_on_failure(self):
+        if int(self.host[1]):
+            n = min(self.max_iters + 1, self.HIST)
+            hist = self.hist[:n].cpu().numpy().tolist()
+            raise CgError(f"dsa failed to reach tol {self.TOL:g}", self.max_iters, hist)
 
 
 def _finish(ops, plan, psi_sk, phi, it, keep_sk, comm=None, owners=None, nd=0):
@@ -388,3 +458,51 @@ def boundary_outflow(grid, psi, omegas, weights, ref_edge=None):
     vals = 0.5 * (psi[i0] + psi[i1]) * as_device(lengths)[:, None]
     on = as_device(normals) @ as_device(np.asarray(omegas)[:, :2]).T
     return float((torch.clamp(on, min=0.0) * vals @ as_device(weights)).sum())
+
+
+def inflow_values(inflow):
+    """None | {wall: psi_b} | (left, right, bottom, top) -> 4-tuple, or None
+    when every wall is vacuum (ContractViolation for unknown walls or
+    negative / non-finite intensities)."""
+    if inflow is None:
+        return None
+    walls = ("left", "right", "bottom", "top")
+    if isinstance(inflow, dict):
+        bad = set(inflow) - set(walls)
+        if bad:
+            raise ContractViolation(f"unknown inflow walls {sorted(bad)}")
+        vals = tuple(float(inflow.get(w, 0.0)) for w in walls)
+    else:
+        vals = tuple(float(v) for v in inflow)
+        if len(vals) != 4:
+            raise ContractViolation("inflow needs 4 values (left, right, bottom, top)")
+    if any(not np.isfinite(v) or v < 0 for v in vals):
+        raise ContractViolation("inflow intensities must be finite and non-negative")
+    return vals if any(vals) else None
+
+def inflow_source(grid, omegas, inflow):
+    """(n_dofs, D) device load of isotropic inflow walls for the
+    ``extra_source`` argument of ``source_iteration`` (transport_sn.py:387,
+    406-407): column d gets max(-omega_d.n_w, 0) psi_b,w (e2 @ [1, 1]) on the
+    edge dofs of the cells of wall w (mesh.py:34-39).  An extension: the
+    reference is vacuum-only (transport_sn.py:11-13); restated in
+    oracle/port.py ``inflow_load``."""
+    vals = inflow_values(inflow)
+    om = torch.as_tensor(np.array(np.atleast_2d(omegas), dtype=float), device=device())
+    out = zeros(grid.n_dofs, om.shape[0])
+    if vals is None:
+        return out
+    co = cellops_struct(grid)
+    cid = torch.arange(grid.n_cells, device=out.device).reshape(grid.ny, grid.nx)
+    walls = (("left", cid[:, 0], (-1.0, 0.0), (0, 2), co.e2x),
+             ("right", cid[:, -1], (1.0, 0.0), (1, 3), co.e2x),
+             ("bottom", cid[0, :], (0.0, -1.0), (0, 1), co.e2y),
+             ("top", cid[-1, :], (0.0, 1.0), (2, 3), co.e2y))
+    for (_, cells, n, locs, e2), psi_b in zip(walls, vals):
+        if psi_b == 0.0:
+            continue
+        g = (e2[0] + e2[1], e2[2] + e2[3])
+        coef = torch.clamp(-(om[:, 0] * n[0] + om[:, 1] * n[1]), min=0.0) * psi_b
+        for k, l in enumerate(locs):
+            out[4 * cells + l, :] += g[k] * coef[None, :]
+    return out

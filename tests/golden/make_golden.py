@@ -238,6 +238,103 @@ def run_checker(tag, per, r, nq, nsteps, seed):
     save(tag, nsteps=nsteps, per=per, rank=r, nq=nq, seed=seed, **out)
 
 
+def ref_step_inflow(g, og, step, quad, state, inflow, si_tol):
+    """step_collocation (dlr_sn.py:99-151) composed from the reference's own
+    functions, plus the two inflow terms of the restatement (the reference
+    is vacuum-only and does not forward extra_source): the load joins the
+    sweep rhs via source_iteration(extra_source=...) and the rows via
+    X_new^T load."""
+    from oracle import port as OP
+
+    sel = lowrank.deim_select(state.W.values)
+    closure = sel.closure_weights(state.W.beta)
+    om = quad.omegas[sel.indices]
+    ops = transport_sn.assemble_operators(g, step)
+    mass = ops.mass_matrix()
+    state.check(mass, quad)
+    flux0 = lowrank.evaluate_rows(state, sel)
+    extra = OP.inflow_load(og, om, inflow)
+    res = transport_sn.source_iteration(ops, om, closure, psi_time=flux0.values, use_dsa=False,
+                                        tol=si_tol, max_iters=800, phi_start=state.scalar_flux(),
+                                        extra_source=extra)
+    comp = lowrank.spatial_monomials(mesh.dof_coordinates(g), g.extent, state.rank + 8)
+    x_new, _, dx = angular.gram_schmidt(res.psi, lowrank.mass_inner(mass), comp)
+    proj = dlr_sn.project_row_operators(ops, x_new)
+    B = dlr_sn.row_matrices(proj, om)
+    l_time = dlr_sn.project_initial(state, x_new, mass)[sel.indices]
+    q_all = proj["q"][None, :] + step.inv_cdt * l_time + (x_new.T @ extra).T
+    l_nodes, l_bar = lowrank.solve_row_system(B, proj["ms"], q_all, closure)
+    gamma = sel.interpolation_coefficients(l_nodes)
+    basis, r_ang, dw = angular.orthonormalize(state.W.values @ gamma, quad)
+    new = lowrank.DlrState(X=x_new, S=r_ang.T.copy(), W=basis)
+    new.check(mass, quad)
+    return new, res.iterations, sel.indices.copy(), x_new @ l_bar
+
+
+def gen_inflow():
+    """Inflow boundary restatement pinned on the reference's operators:
+    (1) known answer -- isotropic inflow psi_b on every wall with
+    q = (sigma_t - sigma_s) psi_b reproduces psi = psi_b exactly (the DG
+    upwind scheme is exact for constants); (2) a left-wall inflow source
+    iteration with scattering; (3) 3 DLR steps of a small Marshak problem
+    (sigma_a = 300 T^-3, left inflow at T_b = 1) composed from the
+    reference's step functions."""
+    from oracle import port as OP
+
+    out = {}
+    rng = np.random.default_rng(71)
+    g = mesh.build_grid(6, 5, extent=(0.0, 0.0, 1.2, 1.0))
+    og = OP.Grid(6, 5, 0.0, 0.0, 1.2, 1.0)
+    n = g.n_cells
+    sig = np.exp(rng.uniform(np.log(0.5), np.log(50.0), n))
+    ss = sig * rng.uniform(0.2, 0.9, n)
+    quad = angular.build_quadrature(2, 6)
+    psib = 0.37
+    ops = transport_sn.assemble_operators(g, manual_step(n, sig, ss, (sig - ss) * psib, 0.0))
+    ext = OP.inflow_load(og, quad.omegas, (psib,) * 4)
+    res = transport_sn.source_iteration(ops, quad.omegas, quad.weights, use_dsa=False, tol=1e-14,
+                                        max_iters=800, extra_source=ext)
+    out.update(const_psi=res.psi, const_phi=res.phi, const_iters=res.iterations,
+               const_sigma_t=sig, const_sigma_s=ss, const_psib=psib)
+    q = rng.uniform(0, 1, n)
+    om = quad.omegas
+    pt = rng.standard_normal((g.n_dofs, om.shape[0]))
+    ops = transport_sn.assemble_operators(g, manual_step(n, sig, ss, q, 0.4))
+    ext = OP.inflow_load(og, om, {"left": 0.8, "top": 0.3})
+    res = transport_sn.source_iteration(ops, om, quad.weights, psi_time=pt, use_dsa=False,
+                                        tol=1e-13, max_iters=800, extra_source=ext)
+    out.update(si_q=q, si_psi_time=pt, si_load=ext, si_psi=res.psi, si_phi=res.phi,
+               si_iters=res.iterations)
+    # 3 Marshak steps (8x8, r=4, 4x4 quadrature), reference-orthonormalised draws
+    spec = problems.marshak(n=8, rank=4, n_polar=4, n_azimuthal=4, dt=1e-3, n_steps=3, seed=3,
+                            T_init=0.05)
+    r = spec.rank
+    rng = np.random.default_rng(spec.seed)
+    Xr, Wr = problems.draw_factors(spec, rng)
+    gm = mesh.build_grid(spec.nx, spec.ny, spec.extent)
+    ogm = OP.Grid(spec.nx, spec.ny, *spec.extent)
+    qm = angular.build_quadrature(spec.n_polar, spec.n_azimuthal)
+    mass = driver.assemble_mass(gm)
+    comp = lowrank.spatial_monomials(mesh.dof_coordinates(gm), gm.extent, r + 8)
+    X, _, _ = angular.gram_schmidt(Xr, lowrank.mass_inner(mass), comp)
+    Wb, _, _ = angular.orthonormalize(Wr, qm)
+    k = physics.PhysicsConstants(c=spec.c, a_r=spec.a_r)
+    b0, _ = physics.planck(driver.cells_to_dofs(gm, spec.T0), k)
+    S = np.outer(X.T @ (mass @ b0), Wb.beta)
+    state = lowrank.DlrState(X=X, S=S, W=Wb)
+    out.update(m_X0=X, m_S0=S, m_W0=Wb.values, m_inflow=np.array(spec.inflow))
+    T = spec.T0.copy()
+    for s in range(spec.n_steps):
+        lin = physics.linearize(T, spec.opacity_at(T), spec.rho_cv, spec.dt, k)
+        state, it, idx, phi = ref_step_inflow(gm, ogm, lin, qm, state, spec.inflow, 1e-12)
+        T = np.maximum(physics.update_temperature(driver.dofs_to_cells(gm, phi), lin, -np.inf),
+                       spec.t_floor)
+        out.update({f"m{s}_X": state.X, f"m{s}_S": state.S, f"m{s}_W": state.W.values,
+                    f"m{s}_T": T, f"m{s}_iters": it, f"m{s}_idx": idx, f"m{s}_phi": phi})
+        print("marshak step", s, it, idx, T.max())
+    save("inflow", **out)
+
+
 def gen_edge_cases():
     """Cold-empty problem (tests/test_dlr_sn.py:127-136) and the full-rank
     step (tests/test_dlr_sn.py:91-109), outputs of the reference."""
@@ -279,5 +376,6 @@ if __name__ == "__main__":
     gen_deim()
     gen_projections()
     gen_edge_cases()
+    gen_inflow()
     run_checker("dlr_small", per=2, r=4, nq=4, nsteps=4, seed=11)
     run_checker("dlr_c1", per=10, r=8, nq=16, nsteps=3, seed=1)

@@ -400,3 +400,57 @@ def test_wide_rank_steps_match_oracle(per_block, r, n_polar, n_azimuthal):
         # their norm): the reference and the oracle, both CPU, already differ
         # by up to 4.6e-10 after one step (scripts/ref_sensitivity.py)
         assert P.lowrank_rel_diff(X2, S2, W2, rs.X, rs.S, rs.W) <= (1e-11 if k == 0 else 1e-9), k
+
+
+@pytest.mark.parametrize("gs_method", ["cholqr2", "cgs2"])
+def test_marshak_steps_match_reference_composition(golden, gs_method):
+    """3 native DLR steps of a small Marshak problem (sigma_a = 300 T^-3,
+    left-wall inflow at T_b = 1; spatial and angular deficiencies fire every
+    step) against the step composed from the reference's functions plus the
+    inflow terms (tests/golden/make_golden.py ref_step_inflow)."""
+    from test_oracle_golden import marshak_small, marshak_state_close
+    from paper_2601_18705_b200.driver import DeviceProblem, initial_state, run
+
+    g = golden("inflow")
+    spec = marshak_small()
+    dp = DeviceProblem.from_spec(spec)
+    state = initial_state(dp, X=g["m_X0"], W=g["m_W0"])
+    assert rel_l2(_np(state.S), g["m_S0"]) <= 1e-13
+    recs = []
+    run(dp, state, spec.n_steps, si_tol=1e-12, si_max_iters=800, gs_method=gs_method,
+        record=lambda s, i, t: recs.append((s, i, _np(t).copy())))
+    for k, (s, info, T) in enumerate(recs):
+        assert list(info.angle_indices) == list(g[f"m{k}_idx"]), k
+        assert info.iterations == int(g[f"m{k}_iters"]), k
+        assert rel_l2(_np(info.phi), g[f"m{k}_phi"]) <= 1e-11
+        assert rel_l2(T, g[f"m{k}_T"]) <= 1e-11
+        X, S, W = s.to_numpy()
+        assert marshak_state_close(X, S, W, g, k)
+
+
+def test_marshak_multistrip_matches_oracle():
+    """Marshak on a 40x40 grid (two 32-row strips, so the strip handoff
+    carries inflow-driven values), r=6, 6x6 quadrature, 4 steps."""
+    from oracle import port as P
+    from oracle import runner as R
+    from paper_2601_18705_b200 import problems
+    from paper_2601_18705_b200.driver import DeviceProblem, initial_state, run
+
+    spec = problems.marshak(n=40, rank=6, n_polar=6, n_azimuthal=6, dt=1e-3, n_steps=4, seed=3,
+                            T_init=0.05)
+    rng = np.random.default_rng(spec.seed)
+    Xr, Wr = problems.draw_factors(spec, rng)
+    X, W = R.orthonormal_factors(spec, Xr, Wr)
+    ref = []
+    R.run(spec, R.initial_state(spec, X, W), spec.n_steps, record=lambda s, i, t: ref.append((s, i, t)))
+    dp = DeviceProblem.from_spec(spec)
+    got = []
+    run(dp, initial_state(dp, X=X, W=W), spec.n_steps, si_tol=1e-12, si_max_iters=400,
+        record=lambda s, i, t: got.append((s, i, _np(t).copy())))
+    for k, ((rs, ri, rt), (gs, gi, gt)) in enumerate(zip(ref, got)):
+        assert list(gi.angle_indices) == list(ri.angle_indices), k
+        assert gi.iterations == ri.iterations, k
+        assert rel_l2(_np(gi.phi), ri.phi) <= 1e-11, k
+        assert rel_l2(gt, rt) <= 1e-11, k
+        X2, S2, W2 = gs.to_numpy()
+        assert P.lowrank_rel_diff(X2, S2, W2, rs.X, rs.S, rs.W) <= 1e-11, k

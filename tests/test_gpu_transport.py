@@ -163,3 +163,124 @@ def test_sweep_is_deterministic():
     b = Tr.source_iteration(ops, om, np.full(D, 0.3), use_dsa=False, tol=1e-10)
     assert a.iterations == b.iterations
     assert torch.equal(a.psi, b.psi) and torch.equal(a.phi, b.phi)
+
+
+# ---- isotropic inflow boundary (config 3), device kernel dlrsn_inflow_add
+
+
+def test_inflow_constant_state_is_exact(golden):
+    """psi_b on every wall, q = (sigma_t - sigma_s) psi_b: psi = psi_b."""
+    from paper_2601_18705_b200 import transport as Tr
+    from paper_2601_18705_b200.angular import build_quadrature
+
+    g = golden("inflow")
+    grid = _grid(np.array([6, 5, 0.0, 0.0, 1.2, 1.0]))
+    n = grid.n_cells
+    psib = float(g["const_psib"])
+    sig, ss = g["const_sigma_t"], g["const_sigma_s"]
+    quad = build_quadrature(2, 6)
+    ops = Tr.assemble_operators(grid, _manual_step(n, sig, ss, (sig - ss) * psib, 0.0))
+    for dw in (1, 2):
+        res = Tr.source_iteration(ops, quad.omegas, quad.weights, use_dsa=False, tol=1e-14,
+                                  max_iters=800, inflow=(psib,) * 4, dw=dw)
+        assert res.iterations == int(g["const_iters"])
+        assert np.abs(_np(res.psi) - psib).max() <= 1e-13
+        assert rel_l2(_np(res.psi), g["const_psi"]) <= 1e-13
+
+
+def test_inflow_source_iteration_matches_reference(golden):
+    from paper_2601_18705_b200 import transport as Tr
+    from paper_2601_18705_b200.angular import build_quadrature
+
+    g = golden("inflow")
+    grid = _grid(np.array([6, 5, 0.0, 0.0, 1.2, 1.0]))
+    n = grid.n_cells
+    quad = build_quadrature(2, 6)
+    inflow = {"left": 0.8, "top": 0.3}
+    assert rel_l2(_np(Tr.inflow_source(grid, quad.omegas, inflow)), g["si_load"]) == 0.0
+    ops = Tr.assemble_operators(grid, _manual_step(n, g["const_sigma_t"], g["const_sigma_s"],
+                                                   g["si_q"], 0.4))
+    for dw in (1, 4):
+        res = Tr.source_iteration(ops, quad.omegas, quad.weights, psi_time=g["si_psi_time"],
+                                  use_dsa=False, tol=1e-13, max_iters=800, inflow=inflow, dw=dw)
+        assert res.iterations == int(g["si_iters"])
+        assert rel_l2(_np(res.psi), g["si_psi"]) <= 1e-12
+        assert rel_l2(_np(res.phi), g["si_phi"]) <= 1e-12
+
+
+# ---- K6: diffusion synthetic acceleration (transport_sn.py:166-198, 325-367)
+
+
+def test_dsa_source_iteration_matches_reference(golden):
+    """use_dsa=True (the reference default) against the reference's own run."""
+    from paper_2601_18705_b200 import transport as Tr
+
+    g = golden("source_iteration")
+    grid = _grid(g["grid"])
+    n = grid.n_cells
+    ops = Tr.assemble_operators(grid, _manual_step(n, g["sigma_t"], g["sigma_s"], g["q"],
+                                                   float(g["inv_cdt"])))
+    for dw in (1, 4):
+        res = Tr.source_iteration(ops, g["omegas"], g["closure"], psi_time=g["psi_time"],
+                                  use_dsa=True, tol=1e-12, max_iters=400,
+                                  phi_start=g["phi_start"], extra_source=g["extra"], dw=dw)
+        assert res.iterations == int(g["dsa_iters"]), dw
+        assert rel_l2(_np(res.psi), g["dsa_psi"]) <= 1e-11
+        assert rel_l2(_np(res.phi), g["dsa_phi"]) <= 1e-11
+
+
+@pytest.mark.parametrize("nx,ny,penalty", [(40, 45, "simplified"), (7, 70, "collocation")])
+def test_dsa_matches_oracle(nx, ny, penalty):
+    """Full quadrature closure on multi-strip grids with thick scattering
+    cells (where DSA matters): GPU vs oracle with the same DSA, both penalty
+    variants; DSA must cut the iteration count."""
+    from oracle import port as P
+    from paper_2601_18705_b200 import transport as Tr
+    from paper_2601_18705_b200.angular import build_quadrature
+    from paper_2601_18705_b200.mesh import build_grid
+
+    rng = np.random.default_rng(nx * 7 + ny)
+    n = nx * ny
+    sig = np.exp(rng.uniform(np.log(1.0), np.log(200.0), n))
+    ss = sig * rng.uniform(0.8, 0.99, n)
+    q = rng.uniform(0, 1, n)
+    quad = build_quadrature(2, 8)
+    om, w = quad.omegas, quad.weights
+    grid = build_grid(nx, ny, (0.0, 0.0, 1.0, 1.1))
+    pc = (om, w) if penalty == "collocation" else None
+    ops = Tr.assemble_operators(grid, _manual_step(n, sig, ss, q, 0.0), dsa_penalty=penalty,
+                                penalty_closure=pc)
+    res = Tr.source_iteration(ops, om, w, use_dsa=True, tol=1e-10, max_iters=500)
+    plain = Tr.source_iteration(ops, om, w, use_dsa=False, tol=1e-10, max_iters=2000)
+    pg = P.Grid(nx, ny, 0.0, 0.0, 1.0, 1.1)
+    pst = P.Step(sig, ss, sig, q, np.zeros(n), np.ones(n), np.ones(n), 1.0, 0.0)
+    pops = P.assemble_operators(pg, pst, dsa_penalty=penalty, penalty_closure=pc)
+    ref = P.source_iteration(pops, om, w, use_dsa=True, tol=1e-10, max_iters=500)
+    assert res.iterations == ref.iterations
+    assert res.iterations < plain.iterations
+    assert rel_l2(_np(res.phi), ref.phi) <= 1e-10
+    assert rel_l2(_np(res.psi), ref.psi) <= 1e-10
+    assert rel_l2(_np(res.phi), _np(plain.phi)) <= 1e-8  # same fixed point
+
+
+def test_dsa_step_collocation_matches_reference(golden):
+    """The cold-empty edge case ran through the reference with its default
+    use_dsa=True (tests/test_dlr_sn.py:127-136)."""
+    from paper_2601_18705_b200.angular import build_quadrature
+    from paper_2601_18705_b200.dlr_sn import step_collocation
+    from paper_2601_18705_b200.lowrank import DlrState
+    from paper_2601_18705_b200.mesh import build_grid
+    from paper_2601_18705_b200.physics import linearize
+
+    g = golden("edge_cases")
+    grid = build_grid(4, 4)
+    quad = build_quadrature(2, 4)
+    st = DlrState(X=g["cold_X"], S=g["cold_S"], W=g["cold_W"])
+    st.W.bind(quad)
+    n = grid.n_cells
+    step = linearize(np.zeros(n), np.full(n, 2.0), np.ones(n), 0.2)
+    new, info = step_collocation(grid, step, quad, st)  # use_dsa=True by default
+    assert info.spatial_deficiency == int(g["cold_sdef"])
+    assert list(info.angle_indices) == list(g["cold_idx"])
+    assert info.iterations == int(g["cold_iters"])
+    assert np.abs(_np(new.X) - g["cold_newX"]).max() <= 1e-12
