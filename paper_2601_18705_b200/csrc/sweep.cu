@@ -38,19 +38,28 @@ __device__ int g_flags = 0;  // debug: bit0 = no speculative handoff prefetch
 // full-SN sweep (1024 directions, 280x280): double buffering with 4-warp CTAs
 // keeps enough warps resident per SM; wider chunks or deeper rings lose
 // occupancy to shared memory (scripts/full_sn.py).
-template <int DW> struct SweepCfg;
-template <> struct SweepCfg<1> { static constexpr int C = 4, P = 2, WPC = 4; };
-template <> struct SweepCfg<2> { static constexpr int C = 4, P = 2, WPC = 4; };
-template <> struct SweepCfg<4> { static constexpr int C = 2, P = 2, WPC = 4; };
-template <> struct SweepCfg<8> { static constexpr int C = 1, P = 3, WPC = 2; };
+// V selects a variant of the single-direction kernel (DLRSN_SWEEP1_CFG, tuning).
+template <int DW, int V = 0> struct SweepCfg;
+// DW = 1 (DLR steps, many strips): a 3-deep ring in 2-warp CTAs measured
+// best on 1024^2 / 64 directions (1.48 vs 1.58 ms for 4-warp CTAs with a
+// 2-deep ring; scripts/sweep_bench.py); variant 1 is the previous default
+template <> struct SweepCfg<1, 0> { static constexpr int C = 4, P = 3, WPC = 2; };
+template <> struct SweepCfg<1, 1> { static constexpr int C = 4, P = 2, WPC = 4; };
+template <> struct SweepCfg<1, 2> { static constexpr int C = 8, P = 2, WPC = 2; };
+template <> struct SweepCfg<1, 3> { static constexpr int C = 4, P = 4, WPC = 2; };
+template <> struct SweepCfg<1, 4> { static constexpr int C = 4, P = 2, WPC = 2; };
+template <> struct SweepCfg<1, 5> { static constexpr int C = 2, P = 6, WPC = 2; };
+template <> struct SweepCfg<2, 0> { static constexpr int C = 4, P = 2, WPC = 4; };
+template <> struct SweepCfg<4, 0> { static constexpr int C = 2, P = 2, WPC = 4; };
+template <> struct SweepCfg<8, 0> { static constexpr int C = 1, P = 3, WPC = 2; };
 
-template <int DW>
+template <int DW, int V = 0>
 __host__ __device__ constexpr int stage_doubles() {
-  return SweepCfg<DW>::C * (32 + 128 + 128 * DW);  // sigma | scat | rhs[DW]
+  return SweepCfg<DW, V>::C * (32 + 128 + 128 * DW);  // sigma | scat | rhs[DW]
 }
-template <int DW>
+template <int DW, int V = 0>
 __host__ __device__ constexpr size_t sweep_smem_bytes() {
-  return (size_t)SweepCfg<DW>::WPC * SweepCfg<DW>::P * stage_doubles<DW>() * sizeof(double);
+  return (size_t)SweepCfg<DW, V>::WPC * SweepCfg<DW, V>::P * stage_doubles<DW, V>() * sizeof(double);
 }
 
 // One persistent launch; see the file header.  Per warp, a P-deep ring of
@@ -61,14 +70,14 @@ __host__ __device__ constexpr size_t sweep_smem_bytes() {
 // handoff column whose slots start "empty" (sNaN sentinel): the producer
 // stores, the consumer spins on the slot itself (no fences, no counters) and
 // re-arms it after reading, so the buffer is clean for the next launch.
-template <int DW>
-__global__ void __launch_bounds__(SweepCfg<DW>::WPC * 32)
+template <int DW, int V = 0>
+__global__ void __launch_bounds__(SweepCfg<DW, V>::WPC * 32)
 sweep_kernel(const SweepArgs a) {
   // iterations past convergence take no work item (no early return: that
   // would cost the compiler its proof that the warps stay converged)
   const bool skip = a.skip != nullptr && *a.skip != 0;
-  constexpr int C = SweepCfg<DW>::C, P = SweepCfg<DW>::P, WPC = SweepCfg<DW>::WPC;
-  constexpr int SD = stage_doubles<DW>();
+  constexpr int C = SweepCfg<DW, V>::C, P = SweepCfg<DW, V>::P, WPC = SweepCfg<DW, V>::WPC;
+  constexpr int SD = stage_doubles<DW, V>();
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t bars[WPC][P];
   __shared__ double s_S[WPC][DW][16];
@@ -761,23 +770,32 @@ __global__ void sk_to_canonical_kernel(int nx, int ny, int D, const int* __restr
 
 static int64_t handoff_offset_bytes(int, int, int) { return 256; }
 
-template <int DW>
+// configuration variant of the single-direction throughput kernel
+static int sweep1_variant() {
+  static const int v = [] {
+    const char* e = getenv("DLRSN_SWEEP1_CFG");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <int DW, int V = 0>
 int launch_sweep(const SweepArgs& a, int max_ctas, cudaStream_t st) {
-  constexpr int WPC = SweepCfg<DW>::WPC;
-  constexpr size_t smem = sweep_smem_bytes<DW>();
+  constexpr int WPC = SweepCfg<DW, V>::WPC;
+  constexpr size_t smem = sweep_smem_bytes<DW, V>();
   int dev = 0, sms = 0, occ = 0;
   DLRSN_TRY_CUDA(cudaGetDevice(&dev));
   DLRSN_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  DLRSN_TRY_CUDA(cudaFuncSetAttribute(sweep_kernel<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-  DLRSN_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_kernel<DW>, WPC * 32, smem));
+  DLRSN_TRY_CUDA(cudaFuncSetAttribute(sweep_kernel<DW, V>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  DLRSN_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_kernel<DW, V>, WPC * 32, smem));
   const int items = sk_strips(a.ny) * a.G;
   int ctas = (items + WPC - 1) / WPC;
   const int cap = sms * (occ > 0 ? occ : 1);
   if (ctas > cap) ctas = cap;
   if (max_ctas > 0 && ctas > max_ctas) ctas = max_ctas;
   if (ctas < 1) ctas = 1;
-  sweep_kernel<DW><<<ctas, WPC * 32, smem, st>>>(a);
+  sweep_kernel<DW, V><<<ctas, WPC * 32, smem, st>>>(a);
   DLRSN_CHECK_LAUNCH("sweep_kernel");
   return DLRSN_OK;
 }
@@ -1060,7 +1078,20 @@ int sweep_launch(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int
   if (tm) DLRSN_TRY_CUDA(cudaEventRecord(tm->start, st));
   int rc;
   switch (dw) {
-    case 1: rc = use_ws ? launch_sweep_ws(a, max_ctas, st) : launch_sweep<1>(a, max_ctas, st); break;
+    case 1:
+      if (use_ws) {
+        rc = launch_sweep_ws(a, max_ctas, st);
+        break;
+      }
+      switch (sweep1_variant()) {
+        case 1: rc = launch_sweep<1, 1>(a, max_ctas, st); break;
+        case 2: rc = launch_sweep<1, 2>(a, max_ctas, st); break;
+        case 3: rc = launch_sweep<1, 3>(a, max_ctas, st); break;
+        case 4: rc = launch_sweep<1, 4>(a, max_ctas, st); break;
+        case 5: rc = launch_sweep<1, 5>(a, max_ctas, st); break;
+        default: rc = launch_sweep<1, 0>(a, max_ctas, st); break;
+      }
+      break;
     case 2: rc = launch_sweep<2>(a, max_ctas, st); break;
     case 4: rc = launch_sweep<4>(a, max_ctas, st); break;
     default: rc = launch_sweep<8>(a, max_ctas, st); break;

@@ -1,7 +1,6 @@
 """Run a few native DLR steps of the BASELINE configurations that fit one
-B200 (C1, C2, C4; C3 needs the inflow boundary the reference lacks, C5's
-68.7 GB factors need space sharding) and print per-step device time,
-source iterations and the sweep launch time."""
+B200 (C1, C2, C3, C4; C5's 68.7 GB factors need space sharding) and print
+per-step device time, source iterations and the sweep launch time."""
 import os
 import sys
 import time
@@ -19,6 +18,9 @@ def spec_of(name):
         return problems.config1()
     if name == "C2":
         return problems.config2()
+    if name.startswith("C3"):
+        n = int(name.split(":")[1]) if ":" in name else 512
+        return problems.marshak(n=n)
     if name.startswith("C4"):
         n = int(name.split(":")[1]) if ":" in name else 1024
         spec, fields = problems.random_medium(n=n)
