@@ -144,7 +144,10 @@ def run_reference(args):
     spec = problems.config2()
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     warm = min(args.warmup, 1)
-    rate, sps, sec, iters = cpu_reference_step_rate(spec, args.steps, warm)
+    # bounded sample: at most 12 oracle steps (~40 s on 16 cores), rate per step
+    n_run = max(1, min(args.steps, 12))
+    rate, sps, sec, iters = cpu_reference_step_rate(spec, n_run, warm)
+    sec = sec * args.steps / n_run
     line = {
         "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps, "higher_is_better": True,
@@ -154,8 +157,9 @@ def run_reference(args):
                    "si_tol": 1e-8, "use_dsa": False},
         "dlr_steps_per_s": sps,
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} full C2 DLR steps ({iters} sweeps of 16 directions)"
-                                   f" after {warm} warm-up step(s), numpy/scipy, BLAS on all cores"},
+                         "sample": f"{n_run} of the {args.steps} C2 DLR steps run ({iters} sweeps of "
+                                   f"16 directions) after {warm} warm-up step(s), numpy/scipy, BLAS "
+                                   f"on all cores; ms_per_step is the per-step mean"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -170,6 +174,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--full-sn", type=int, default=1, help="also time the config-2 full-SN sweep")
+    ap.add_argument("--more-configs", default="C4,C3",
+                    help="also time a few steps of these BASELINE configs at N=1 ('' = none)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -270,6 +276,15 @@ def main():
     # ---- full-SN comparison sweep (config 2: all 1024 directions) ----------
     full = measure_full_sn(dp, comm) if args.full_sn else None
 
+    # ---- larger BASELINE configs at N=1 (not the headline: step time and
+    # the DLR sweep's HBM fraction where the sweep is bandwidth-bound) -------
+    more = []
+    if ws == 1 and args.more_configs:
+        del state, lin, Tbox, dp
+        torch.cuda.empty_cache()
+        for name in args.more_configs.split(","):
+            more.append(measure_config(name.strip()))
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -293,6 +308,8 @@ def main():
     }
     if full is not None:
         line["full_sn_sweep"] = full
+    if more:
+        line["more_configs"] = more
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
         rate, sps, sec, it = cpu_reference_step_rate(spec, args.cpu_steps, 0)
@@ -400,6 +417,62 @@ def measure_e2e(dp, state, T, lin, n, comm=None, warmup=3):
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "steps": n, "warmup": warmup, "ms_per_step": ms / n,
             "pipelined": "H2D of step k+1 and D2H of step k-1 overlap step k (2 copy streams)"}
+
+
+def measure_config(name, steps=5, warmup=3):
+    """A few DLR steps of a larger BASELINE config (C3 Marshak 512^2 r=32
+    from its initial state, C4 random medium 1024^2 r=64): device time per
+    step (inputs resident, L2 flushed between steps) and the DLR sweep's
+    algorithmic HBM fraction from per-launch CUDA events."""
+    import torch
+
+    from paper_2601_18705_b200 import _lib, problems
+    from paper_2601_18705_b200.driver import DeviceProblem, initial_state
+
+    if name == "C3":
+        spec = problems.marshak()
+        label = "C3 Marshak 512x512, r=32, 64x64 quadrature, inflow T_b=1, dlr-sn step"
+    elif name == "C4":
+        spec, fields = problems.random_medium()
+        rng = np.random.default_rng(spec.seed)
+        problems.draw_factors(spec, rng)  # X, W first (SURVEY 8d draw order)
+        fields(rng)
+        label = "C4 random medium 1024x1024, r=64, 64x64 quadrature, dlr-sn step"
+    else:
+        raise SystemExit(f"unknown config {name}")
+    dp = DeviceProblem.from_spec(spec)
+    state = initial_state(dp)
+    T = torch.as_tensor(spec.T0, device="cuda").clone()
+    lin = dp.linearized(T)
+    for _ in range(warmup):
+        state, lin, T, _ = dp.step(state, lin, T, si_tol=1e-8)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
+    ms, iters = 0.0, []
+    for k in range(steps):
+        flush.fill_(float(k))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        state, lin, T, info = dp.step(state, lin, T, si_tol=1e-8)
+        e1.record()
+        torch.cuda.synchronize()
+        ms += e0.elapsed_time(e1)
+        iters.append(info.iterations)
+    _lib.call("dlrsn_sweep_timing", 1)
+    state, lin, T, info = dp.step(state, lin, T, si_tol=1e-8)
+    torch.cuda.synchronize()
+    sw, _ = _sweep_timings(_lib)
+    sweep_ms = float(np.sum(sw)) / max(1, info.iterations)
+    alg = spec.n_cells * (spec.rank * SWEEP_BYTES_PER_CELL_ANGLE + SWEEP_BYTES_PER_CELL)
+    peak, _ = _peaks()
+    out = {"workload": label, "steps": steps, "ms_per_step": ms / steps,
+           "dlr_steps_per_s": steps / (ms * 1e-3), "si_iterations": iters,
+           "cell_angle_per_s": spec.n_cells * spec.rank * sum(iters) / (ms * 1e-3),
+           "sweep": {"kernel": "sweep_kernel<1>", "launch_ms": sweep_ms,
+                     "alg_bytes_per_launch": alg, "achieved_GBs": alg / (sweep_ms * 1e-3) / 1e9,
+                     "frac_of_hbm": alg / (sweep_ms * 1e-3) / 1e9 / peak}}
+    del state, lin, T, dp, flush
+    torch.cuda.empty_cache()
+    return out
 
 
 def _sweep_timings(_lib):
