@@ -96,3 +96,38 @@ def _dummy_step(spec):
     n = spec.n_cells
     one = np.ones(n)
     return P.Step(one * 2.0, one, one, one, one, one, one, 1.0, 1.0)
+
+
+def run_sn(spec, n_steps, *, si_tol=1e-12, si_max_iters=400, use_dsa=False):
+    """The reference driver's full-SN method (driver.py:463-466, 492-504)
+    with its energy rows (driver.py:521-553): returns (psi, records) with
+    records[k] = (T, phi, iterations, (e_mat, e_rad, outflow, residual,
+    floor_source))."""
+    grid, quad = grid_of(spec), quad_of(spec)
+    k = constants_of(spec)
+    T = np.asarray(spec.T0, dtype=float).copy()
+    b0, _ = P.planck(P.cells_to_dofs(T), k)
+    psi = np.tile(b0[:, None], (1, quad.n_angles))
+    phi = psi @ quad.weights
+    area = grid.cell_area
+    e_mat = float(np.sum(spec.rho_cv * T) * area)
+    e_rad = float(P.dofs_to_cells(phi).sum() * area) / k.c
+    recs = []
+    for _ in range(n_steps):
+        lin = linearized(spec, T)
+        ops = P.assemble_operators(grid, lin)
+        res = P.source_iteration(ops, quad.omegas, quad.weights, psi_time=psi, use_dsa=use_dsa,
+                                 tol=si_tol, max_iters=si_max_iters, phi_start=phi)
+        psi, phi = res.psi, res.phi
+        raw = P.update_temperature(P.dofs_to_cells(phi), lin, -np.inf)
+        Tn = np.maximum(raw, spec.t_floor)
+        floor_source = float(np.sum(spec.rho_cv * (Tn - raw)) * area)
+        outflow = P.boundary_outflow(grid, psi, quad.omegas, quad.weights)
+        e_mat_n = float(np.sum(spec.rho_cv * Tn) * area)
+        e_rad_n = float(P.dofs_to_cells(psi @ quad.weights).sum() * area) / k.c
+        total = e_mat_n + e_rad_n
+        resid = (total - e_mat - e_rad + spec.dt * outflow - floor_source) / max(abs(total), 1e-300)
+        e_mat, e_rad = e_mat_n, e_rad_n
+        T = Tn
+        recs.append((T, phi, res.iterations, np.array([e_mat, e_rad, outflow, resid, floor_source])))
+    return psi, recs

@@ -163,14 +163,25 @@ def initial_state(dp, X=None, W=None, seed=None, T=None):
 
 
 def run(dp, state, n_steps, *, si_tol=1e-8, si_max_iters=200, check_state=True, T=None,
-        record=None, gs_method="cholqr2", engine="native", comm=None):
-    """n_steps of the dlr-sn loop; returns (state, T, infos)."""
+        record=None, gs_method="cholqr2", engine="native", comm=None, diagnostics=None):
+    """n_steps of the dlr-sn loop; returns (state, T, infos).  With a list
+    as ``diagnostics``, the reference driver's energy rows (driver.py:
+    521-553, DIAGNOSTIC_COLUMNS order) are appended to it, evaluated on the
+    factors (diagnostics.py)."""
     from .dlr_sn import step_collocation
+    from .physics import update_temperature
 
     T = as_device(dp.spec.T0 if T is None else T).clone()
     lin = dp.linearized(T)
     infos = []
-    for _ in range(n_steps):
+    ledger = None
+    if diagnostics is not None:
+        from .diagnostics import EnergyLedger
+
+        ledger = EnergyLedger.start(dp.grid, dp.quad, dp.rho_cv, T, state.scalar_flux(),
+                                    dp.constants.c, dp.spec.dt)
+    for step_no in range(1, n_steps + 1):
+        lin_used = lin
         if engine == "native":  # step + boundary in one native call
             state, lin, T, info = dp.step(state, lin, T, si_tol=si_tol, si_max_iters=si_max_iters,
                                           check_state=check_state, gs_method=gs_method, comm=comm)
@@ -181,6 +192,56 @@ def run(dp, state, n_steps, *, si_tol=1e-8, si_max_iters=200, check_state=True, 
                                            engine=engine, comm=comm, inflow=dp.spec.inflow)
             lin = dp.advance(lin, info.phi, T)
         infos.append(info)
+        if ledger is not None:
+            from .diagnostics import outflow_lowrank
+
+            raw = update_temperature(info.phi, lin_used, -np.inf)
+            diagnostics.append(ledger.row(step_no, info.iterations, info.interpolation_condition,
+                                          T, raw, state.scalar_flux(),
+                                          outflow_lowrank(dp.grid, state, dp.quad)))
         if record is not None:
             record(state, info, T)
     return state, T, infos
+
+
+def run_sn(dp, n_steps, *, si_tol=1e-8, si_max_iters=200, use_dsa=True, dsa_penalty="simplified",
+           T=None, record=None, diagnostics=None, comm=None):
+    """The reference driver's full discrete-ordinates method ("sn",
+    driver.py:463-466, 492-504): psi0 = B(T0) on every quadrature node, then
+    per step the source iteration over ALL directions with the previous
+    intensity as psi_time (sweeps grouped DW directions per warp), the
+    temperature update and the floor.  psi (n_dofs x N_Omega) stays on the
+    device.  Returns (psi, phi, T, iterations per step); ``diagnostics``
+    as in ``run``."""
+    from . import transport
+    from .physics import planck, update_temperature
+
+    spec = dp.spec
+    quad = dp.quad
+    T = as_device(spec.T0 if T is None else T).clone()
+    b0, _ = planck(T.repeat_interleave(4), dp.constants)
+    psi = b0[:, None].repeat(1, quad.n_angles).contiguous()
+    w = torch.as_tensor(np.array(quad.weights, dtype=float), device=device())
+    phi = psi @ w
+    ledger = None
+    if diagnostics is not None:
+        from .diagnostics import EnergyLedger, outflow_dense
+
+        ledger = EnergyLedger.start(dp.grid, quad, dp.rho_cv, T, phi, dp.constants.c, spec.dt)
+    iters = []
+    for step_no in range(1, n_steps + 1):
+        lin = dp.linearized(T)
+        ops = transport.assemble_operators(dp.grid, lin, dsa_penalty=dsa_penalty)
+        res = transport.source_iteration(ops, quad.omegas, quad.weights, psi_time=psi,
+                                         use_dsa=use_dsa, tol=si_tol, max_iters=si_max_iters,
+                                         phi_start=phi, inflow=spec.inflow, comm=comm)
+        psi, phi = res.psi, res.phi
+        raw = update_temperature(phi, lin, -np.inf)
+        T = torch.clamp(raw, min=spec.t_floor)
+        iters.append(res.iterations)
+        if ledger is not None:
+            diagnostics.append(ledger.row(step_no, res.iterations, 0.0, T, raw, psi @ w,
+                                          outflow_dense(dp.grid, psi, quad)))
+        if record is not None:
+            record(psi, phi, T, res.iterations)
+    return psi, phi, T, iters

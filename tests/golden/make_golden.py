@@ -200,6 +200,64 @@ def sketch(X, S, W, seed=9):
     return (phi.T @ X) @ S @ (W.T @ om)
 
 
+def diag_row(g, quad, spec, T_prev, T, raw_T, psi_full, e_prev):
+    """driver.run_problem's per-step energy diagnostics (driver.py:532-553):
+    (e_mat, e_rad, outflow, residual, floor_source) via the reference's own
+    boundary_outflow / integrate_dofs on the dense intensity."""
+    k = physics.PhysicsConstants(c=spec.c, a_r=spec.a_r)
+    floor_source = float(np.sum(spec.rho_cv * (T - raw_T)) * g.cell_area)
+    outflow = transport_sn.boundary_outflow(g, psi_full, quad.omegas, quad.weights)
+    e_mat = float(np.sum(spec.rho_cv * T) * g.cell_area)
+    e_rad = driver.integrate_dofs(g, psi_full @ quad.weights) / k.c
+    total = e_mat + e_rad
+    residual = (total - e_prev[0] - e_prev[1] + spec.dt * outflow - floor_source) / max(abs(total), 1e-300)
+    return np.array([e_mat, e_rad, outflow, residual, floor_source])
+
+
+def initial_energies(g, quad, spec, phi_dofs):
+    k = physics.PhysicsConstants(c=spec.c, a_r=spec.a_r)
+    return (float(np.sum(spec.rho_cv * spec.T0) * g.cell_area),
+            driver.integrate_dofs(g, phi_dofs) / k.c)
+
+
+def gen_sn():
+    """The reference driver's full-SN method (driver.py:463-466, 492-504:
+    psi0 = B(T0) on every direction, source_iteration over all quadrature
+    nodes with psi_time = psi) plus its energy diagnostics, on a small
+    checkerboard (SURVEY App. B adapters), with and without DSA."""
+    spec = problems.checkerboard(2, rank=4, n_polar=4, n_azimuthal=4, seed=21, n_steps=3)
+    g = mesh.build_grid(spec.nx, spec.ny, spec.extent)
+    quad = angular.build_quadrature(spec.n_polar, spec.n_azimuthal)
+    k = physics.PhysicsConstants(c=spec.c, a_r=spec.a_r)
+    out = {}
+    for tag, dsa in (("plain", False), ("dsa", True)):
+        T = spec.T0.copy()
+        b0, _ = physics.planck(driver.cells_to_dofs(g, T), k)
+        psi = np.tile(b0[:, None], (1, quad.n_angles))
+        phi = psi @ quad.weights
+        e_prev = initial_energies(g, quad, spec, phi)
+        for s in range(spec.n_steps):
+            lin = physics.linearize(T, spec.sigma_a, spec.rho_cv, spec.dt, k)
+            lin.sigma_t = lin.sigma_t + spec.sigma_s_phys
+            lin.sigma_s = lin.sigma_s + spec.sigma_s_phys
+            lin.q = lin.q + spec.q_ext
+            ops = transport_sn.assemble_operators(g, lin)
+            res = transport_sn.source_iteration(ops, quad.omegas, quad.weights, psi_time=psi,
+                                                use_dsa=dsa, tol=1e-12, max_iters=400,
+                                                phi_start=phi)
+            psi, phi = res.psi, res.phi
+            raw = physics.update_temperature(driver.dofs_to_cells(g, phi), lin, -np.inf)
+            Tn = np.maximum(raw, spec.t_floor)
+            row = diag_row(g, quad, spec, T, Tn, raw, psi, e_prev)
+            e_prev = (row[0], row[1])
+            T = Tn
+            out.update({f"{tag}{s}_T": T, f"{tag}{s}_phi": phi, f"{tag}{s}_iters": res.iterations,
+                        f"{tag}{s}_diag": row})
+            print("sn", tag, s, res.iterations, row)
+        out[f"{tag}_psi"] = psi
+    save("sn", **out)
+
+
 def run_checker(tag, per, r, nq, nsteps, seed):
     """Reference dlr-sn loop on a checkerboard (SURVEY App. B adapters)."""
     spec = problems.checkerboard(per, rank=r, n_polar=nq, n_azimuthal=nq, seed=seed)
@@ -218,6 +276,7 @@ def run_checker(tag, per, r, nq, nsteps, seed):
     state = lowrank.DlrState(X=X, S=S, W=Wb)
     out = {"X0_mb0": X.T @ (mass @ b0), "X0_colsum": X.sum(axis=0), "W0": Wb.values, "S0": S}
     T = spec.T0.copy()
+    e_prev = initial_energies(g, quad, spec, state.scalar_flux())
     for s in range(nsteps):
         lin = physics.linearize(T, spec.sigma_a, spec.rho_cv, spec.dt, k)
         lin.sigma_t = lin.sigma_t + spec.sigma_s_phys
@@ -225,9 +284,13 @@ def run_checker(tag, per, r, nq, nsteps, seed):
         lin.q = lin.q + spec.q_ext
         state, info = dlr_sn.step_collocation(g, lin, quad, state, si_tol=1e-12, si_max_iters=400,
                                               use_dsa=False)
-        T = np.maximum(physics.update_temperature(driver.dofs_to_cells(g, info.phi), lin, -np.inf),
-                       1e-6)
+        raw = physics.update_temperature(driver.dofs_to_cells(g, info.phi), lin, -np.inf)
+        Tn = np.maximum(raw, 1e-6)
+        row = diag_row(g, quad, spec, T, Tn, raw, state.reconstruct(), e_prev)
+        e_prev = (row[0], row[1])
+        T = Tn
         out.update({f"s{s}_idx": info.angle_indices, f"s{s}_iters": info.iterations,
+                    f"s{s}_diag": row,
                     f"s{s}_cond": info.interpolation_condition, f"s{s}_phi": info.phi,
                     f"s{s}_T": T, f"s{s}_phiq": state.scalar_flux(),
                     f"s{s}_sketch": sketch(state.X, state.S, state.W.values),
@@ -377,5 +440,6 @@ if __name__ == "__main__":
     gen_projections()
     gen_edge_cases()
     gen_inflow()
+    gen_sn()
     run_checker("dlr_small", per=2, r=4, nq=4, nsteps=4, seed=11)
     run_checker("dlr_c1", per=10, r=8, nq=16, nsteps=3, seed=1)

@@ -454,3 +454,33 @@ def test_marshak_multistrip_matches_oracle():
         assert rel_l2(gt, rt) <= 1e-11, k
         X2, S2, W2 = gs.to_numpy()
         assert P.lowrank_rel_diff(X2, S2, W2, rs.X, rs.S, rs.W) <= 1e-11, k
+
+
+@pytest.mark.parametrize("nx,ny,r", [(37, 29, 24), (31, 33, 48), (20, 17, 64), (9, 40, 128),
+                                     (33, 35, 16)])
+def test_projections_match_oracle_wide(nx, ny, r):
+    """K3 at every tile width: r <= 16 (16x16 tiles), r > 16 (32x32 tiles,
+    partial edge tiles at 24 and 48): px, py, jx, jy, mt, ms, q-hat and
+    mo = X_old^T M X against the oracle's assembled sparse operators."""
+    from oracle import port as P
+    from paper_2601_18705_b200 import transport as Tr
+    from paper_2601_18705_b200.dlr_sn import project_operators
+    from paper_2601_18705_b200.mesh import build_grid
+
+    rng = np.random.default_rng(nx * 100 + r)
+    n = nx * ny
+    sig = np.exp(rng.uniform(-1, 3, n))
+    ss = sig * rng.uniform(0, 0.9, n)
+    q = rng.uniform(0, 1, n)
+    X = rng.standard_normal((4 * n, r))
+    Xo = rng.standard_normal((4 * n, r))
+    grid = build_grid(nx, ny, (0.0, 0.0, 1.3, 0.7))
+    ops = Tr.assemble_operators(grid, _manual_step(n, sig, ss, q, 0.3))
+    proj, _ = project_operators(ops, X, x_old=Xo)
+    pops = P.assemble_operators(P.Grid(nx, ny, 0.0, 0.0, 1.3, 0.7),
+                                P.Step(sig, ss, sig - 0.3, q, np.zeros(n), np.ones(n), np.ones(n),
+                                       1.0, 0.3))
+    ref = P.project_row_operators(pops, X)
+    ref["mo"] = Xo.T @ pops.mass_apply(X)
+    for k in ("px", "py", "jx", "jy", "mt", "ms", "mo", "q"):
+        assert rel_l2(_np(proj[k]), ref[k]) <= 1e-13, k

@@ -307,3 +307,21 @@ def marshak_state_close(X, S, W, g, k, tol=1e-11):
         return True
     scale = np.linalg.norm(g[f"m{k}_X"] @ g[f"m{k}_S"]) * np.linalg.norm(g[f"m{k}_W"])
     return err * scale <= tol * float(np.max(g["m_inflow"]))
+
+
+# ---- full-SN method + energy diagnostics of the reference driver
+
+
+@pytest.mark.parametrize("tag,dsa", [("plain", False), ("dsa", True)])
+def test_sn_method_matches_reference(golden, tag, dsa):
+    g = golden("sn")
+    spec = problems.checkerboard(2, rank=4, n_polar=4, n_azimuthal=4, seed=21, n_steps=3)
+    psi, recs = R.run_sn(spec, 3, use_dsa=dsa)
+    for k, (T, phi, it, diag) in enumerate(recs):
+        assert it == int(g[f"{tag}{k}_iters"]), k
+        assert rel_l2(T, g[f"{tag}{k}_T"]) <= 1e-12
+        assert rel_l2(phi, g[f"{tag}{k}_phi"]) <= 1e-11
+        ref = g[f"{tag}{k}_diag"]
+        assert np.allclose(diag[:3], ref[:3], rtol=1e-11, atol=0), (diag, ref)
+        assert abs(diag[3] - ref[3]) <= 1e-10
+    assert rel_l2(psi, g[f"{tag}_psi"]) <= 1e-11
