@@ -174,7 +174,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--full-sn", type=int, default=1, help="also time the config-2 full-SN sweep")
-    ap.add_argument("--more-configs", default="C4,C3",
+    ap.add_argument("--more-configs", default="C4,C3,C5",
                     help="also time a few steps of these BASELINE configs at N=1 ('' = none)")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -429,6 +429,8 @@ def measure_config(name, steps=5, warmup=3):
     from paper_2601_18705_b200 import _lib, problems
     from paper_2601_18705_b200.driver import DeviceProblem, initial_state
 
+    if name == "C5":
+        return measure_c5_sweep()
     if name == "C3":
         spec = problems.marshak()
         label = "C3 Marshak 512x512, r=32, 64x64 quadrature, inflow T_b=1, dlr-sn step"
@@ -471,6 +473,47 @@ def measure_config(name, steps=5, warmup=3):
                      "alg_bytes_per_launch": alg, "achieved_GBs": alg / (sweep_ms * 1e-3) / 1e9,
                      "frac_of_hbm": alg / (sweep_ms * 1e-3) / 1e9 / peak}}
     del state, lin, T, dp, flush
+    torch.cuda.empty_cache()
+    return out
+
+
+def measure_c5_sweep(reps=1):
+    """Config 5's full-SN stress sweep on one GPU: 16384 directions on the
+    4096^2 tile medium (sigma_a log-uniform [0.1, 100] per 64x64 tile, q ~
+    U[0,1], dt = dx = 1, pure absorber => one sweep per step), closure only:
+    psi (8.8 TB) is never stored, so there are no per-cell-angle HBM bytes
+    and the sweep is FP64-issue bound (report cell-angle/s).  The fields
+    are drawn from seed 5 directly (the 68.7 GB X draw of the DLR factors
+    is skipped: config 5's DLR step needs the space-sharded layout)."""
+    import torch
+
+    from paper_2601_18705_b200 import problems, transport
+    from paper_2601_18705_b200.driver import DeviceProblem
+
+    spec, fields = problems.stress()
+    fields(np.random.default_rng(spec.seed))
+    dp = DeviceProblem.from_spec(spec)
+    T = torch.as_tensor(spec.T0, device="cuda")
+    lin = dp.linearized(T)
+    ops = transport.assemble_operators(dp.grid, lin)
+    b0 = (spec.a_r * spec.c / (4 * np.pi)) * (T * T) ** 2  # isotropic psi_old = B(T0)
+    rhs = ops.source_vector(lin.q) + lin.inv_cdt * ops.mass_apply(b0.repeat_interleave(4))
+    quad = dp.quad
+    phi = transport.closure_sweep(ops, quad.omegas, quad.weights, rhs)  # warm-up
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        phi = transport.closure_sweep(ops, quad.omegas, quad.weights, rhs)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    ca = spec.n_cells * quad.n_angles
+    out = {"workload": "C5 stress 4096x4096, 128x128 = 16384 directions, full-SN closure-only sweep",
+           "ms_per_sweep": ms, "cell_angle_per_s": ca / (ms * 1e-3), "cell_angles": ca,
+           "bound": "fp64 issue (no per-cell-angle HBM traffic: psi not stored)",
+           "phi_checksum": float(phi.sum())}
+    del ops, lin, T, rhs, phi, dp
     torch.cuda.empty_cache()
     return out
 

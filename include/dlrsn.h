@@ -159,6 +159,19 @@ int dlrsn_inflow_add(const dlrsn_cellops* ops, int D, const int* quad, const dou
 int dlrsn_inflow_project(const dlrsn_cellops* ops, int r, const double* X, int ldx,
                          const double* inflow, double* h, dlrsn_stream_t stream);
 
+/* Closure-only sweep (full-SN stress sweeps whose psi cannot be stored, e.g.
+ * config 5's 16384 directions on 4096^2 = 8.8 TB): every direction sees the
+ * same rhs (rhs_sk4 = 4 quadrant SK slabs of one rhs, e.g. an isotropic
+ * source), psi is not written, and each group adds its closure sum
+ * sum_d cw_d psi_d into the canonical phi (n_dofs, caller-initialised) with
+ * fp64 atomics -- the summation order over groups is not fixed, so phi is
+ * reproducible to round-off only.  transport_sn.py:303-322 + the closure
+ * psi @ closure of :438. */
+int dlrsn_sweep_closure(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int dw,
+                        const double* sigma_t_sk4, const double* scat_sk4, const double* rhs_sk4,
+                        double* phi, void* workspace, int64_t workspace_bytes, int max_ctas,
+                        dlrsn_stream_t stream);
+
 /* ---- K6: diffusion synthetic acceleration (transport_sn.py:166-198,
  * 325-367, applied at :439-441) */
 

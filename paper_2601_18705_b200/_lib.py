@@ -108,6 +108,8 @@ _SIGNATURES = {
     "dlrsn_sk_to_canonical": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp, c_int, c_vp]),
     "dlrsn_sweep": (c_int, [c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64,
                             c_int, c_vp]),
+    "dlrsn_sweep_closure": (c_int, [c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64,
+                                    c_int, c_vp]),
     "dlrsn_rowmix": (c_int, [c_i64, c_int, c_int, c_vp, c_int, c_vp, c_int, c_dbl, c_vp, c_int,
                              c_vp]),
     "dlrsn_partials_len": (c_i64, [c_int, c_int, c_int, c_int]),

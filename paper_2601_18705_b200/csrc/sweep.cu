@@ -118,7 +118,8 @@ sweep_kernel(const SweepArgs a) {
     }
     const int64_t strip_vec = (int64_t)s * T * 128;  // SK offset of (s, t=0)
     double ox[DW], oy[DW], cw[DW];
-    int64_t slot_off[DW];
+    int64_t slot_off[DW], rhs_off[DW];
+    const bool shared = a.rhs_shared != 0;
 #pragma unroll
     for (int k = 0; k < DW; ++k) {
       const bool on = k < nd;
@@ -126,7 +127,9 @@ sweep_kernel(const SweepArgs a) {
       oy[k] = on ? grp->oy[k] : 0.0;
       cw[k] = on ? grp->cw[k] : 0.0;
       slot_off[k] = (on ? (int64_t)grp->slot[k] : 0) * a.vlen + strip_vec;
+      rhs_off[k] = shared ? (int64_t)quad * a.vlen + strip_vec : slot_off[k];
     }
+    const uint32_t nrhs = shared ? 1u : (uint32_t)nd;  // rhs slabs staged per chunk
     const double* sig = a.sigma_sk4 + (int64_t)quad * a.slen + (int64_t)s * T * 32;
     const double* scat = a.scat_sk4 ? a.scat_sk4 + (int64_t)quad * a.vlen + strip_vec : nullptr;
     double* phi_p = a.phi_sk ? a.phi_sk + (int64_t)g * a.vlen + strip_vec + 2 * lane : nullptr;
@@ -139,13 +142,13 @@ sweep_kernel(const SweepArgs a) {
         const uint32_t n = (uint32_t)min(C, T - t0);
         double* buf = ring + st * SD;
         fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&bars[wib][st], n * (256u + (scat ? 1024u : 0u) + 1024u * (uint32_t)nd));
+        mbar_arrive_expect_tx(&bars[wib][st], n * (256u + (scat ? 1024u : 0u) + 1024u * nrhs));
         tma_load_1d(buf, sig + t0 * 32, n * 256u, &bars[wib][st]);
         if (scat) tma_load_1d(buf + C * 32, scat + t0 * 128, n * 1024u, &bars[wib][st]);
 #pragma unroll
         for (int k = 0; k < DW; ++k)
-          if (k < nd)
-            tma_load_1d(buf + C * 160 + k * C * 128, a.rhs_sk + slot_off[k] + t0 * 128, n * 1024u,
+          if (k < (int)nrhs)
+            tma_load_1d(buf + C * 160 + k * C * 128, a.rhs_sk + rhs_off[k] + t0 * 128, n * 1024u,
                         &bars[wib][st]);
       }
     }
@@ -175,13 +178,13 @@ sweep_kernel(const SweepArgs a) {
         const uint32_t n = (uint32_t)min(C, T - t0);
         double* buf = ring + st * SD;
         fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&bars[wib][st], n * (256u + (scat ? 1024u : 0u) + 1024u * (uint32_t)nd));
+        mbar_arrive_expect_tx(&bars[wib][st], n * (256u + (scat ? 1024u : 0u) + 1024u * nrhs));
         tma_load_1d(buf, sig + t0 * 32, n * 256u, &bars[wib][st]);
         if (scat) tma_load_1d(buf + C * 32, scat + t0 * 128, n * 1024u, &bars[wib][st]);
 #pragma unroll
         for (int k = 0; k < DW; ++k)
-          if (k < nd)
-            tma_load_1d(buf + C * 160 + k * C * 128, a.rhs_sk + slot_off[k] + t0 * 128, n * 1024u,
+          if (k < (int)nrhs)
+            tma_load_1d(buf + C * 160 + k * C * 128, a.rhs_sk + rhs_off[k] + t0 * 128, n * 1024u,
                         &bars[wib][st]);
       }
       unsigned long long* tr = g_trace;
@@ -245,7 +248,7 @@ sweep_kernel(const SweepArgs a) {
 #pragma unroll
           for (int k = 0; k < DW; ++k) {
             if (k < nd) {
-              const double* rb = buf + C * 160 + k * C * 128 + tt * 128;
+              const double* rb = buf + C * 160 + (shared ? 0 : k) * C * 128 + tt * 128;
               const double2 u = reinterpret_cast<const double2*>(rb)[lane];
               const double2 v = reinterpret_cast<const double2*>(rb + 64)[lane];
               double b[4] = {u.x + sc[0], u.y + sc[1], v.x + sc[2], v.y + sc[3]};
@@ -259,9 +262,11 @@ sweep_kernel(const SweepArgs a) {
               for (int q = 0; q < 16; ++q) A[q] = fma(sigma, a.mass[q], s_S[wib][k][q]);
               double x[4];
               solve4(A, b, x);
-              double2* po = reinterpret_cast<double2*>(a.psi_sk + slot_off[k] + (int64_t)t * 128 + 2 * lane);
-              po[0] = make_double2(x[0], x[1]);
-              po[32] = make_double2(x[2], x[3]);
+              if (a.psi_sk) {
+                double2* po = reinterpret_cast<double2*>(a.psi_sk + slot_off[k] + (int64_t)t * 128 + 2 * lane);
+                po[0] = make_double2(x[0], x[1]);
+                po[32] = make_double2(x[2], x[3]);
+              }
               xin[k][0] = x[1]; xin[k][1] = x[3];
               ytop[k][0] = x[2]; ytop[k][1] = x[3];
               ph[0] += cw[k] * x[0]; ph[1] += cw[k] * x[1];
@@ -272,6 +277,15 @@ sweep_kernel(const SweepArgs a) {
             double2* pp = reinterpret_cast<double2*>(phi_p + (int64_t)t * 128);
             pp[0] = make_double2(ph[0], ph[1]);
             pp[32] = make_double2(ph[2], ph[3]);
+          }
+          if (a.phi_atomic) {  // canonical cell and dof order of this lane-step
+            const int ic = (quad & 1) ? nx - 1 - ip : ip;
+            const int jo = (s << 5) + lane;
+            const int jc = (quad & 2) ? ny - 1 - jo : jo;
+            double* pa = a.phi_atomic + 4 * ((int64_t)jc * nx + ic);
+            const int f = sk_flip(quad);
+#pragma unroll
+            for (int l = 0; l < 4; ++l) atomicAdd(pa + (l ^ f), ph[l]);
           }
           if (lane == 31 && hout) {
             double2* ho = hout + (int64_t)ip * DW;
@@ -1011,11 +1025,27 @@ int dlrsn_sweep_workspace_init(void* workspace, int64_t workspace_bytes, dlrsn_s
 
 namespace dlrsn {
 
+static int sweep_launch_ex(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int dw,
+                           const double* sigma_t_sk4, const double* scat_sk4,
+                           const double* rhs_sk, double* psi_sk, double* phi_part_sk,
+                           void* workspace, int64_t workspace_bytes, int max_ctas,
+                           const int* skip, int rhs_shared, double* phi_atomic, cudaStream_t st);
+
 int sweep_launch(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int dw,
                  const double* sigma_t_sk4, const double* scat_sk4, const double* rhs_sk,
                  double* psi_sk, double* phi_part_sk, void* workspace, int64_t workspace_bytes,
                  int max_ctas, const int* skip, cudaStream_t st) {
-  DLRSN_REQUIRE(ops && groups && sigma_t_sk4 && rhs_sk && psi_sk && workspace,
+  DLRSN_REQUIRE(psi_sk, "null argument to dlrsn_sweep");
+  return sweep_launch_ex(ops, G, groups, dw, sigma_t_sk4, scat_sk4, rhs_sk, psi_sk, phi_part_sk,
+                         workspace, workspace_bytes, max_ctas, skip, 0, nullptr, st);
+}
+
+static int sweep_launch_ex(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int dw,
+                           const double* sigma_t_sk4, const double* scat_sk4,
+                           const double* rhs_sk, double* psi_sk, double* phi_part_sk,
+                           void* workspace, int64_t workspace_bytes, int max_ctas,
+                           const int* skip, int rhs_shared, double* phi_atomic, cudaStream_t st) {
+  DLRSN_REQUIRE(ops && groups && sigma_t_sk4 && rhs_sk && workspace && (psi_sk || phi_atomic),
                 "null argument to dlrsn_sweep");
   DLRSN_REQUIRE(dw == 1 || dw == 2 || dw == 4 || dw == 8, "sweep width must be 1, 2, 4 or 8");
   const int64_t need = dlrsn_sweep_workspace_bytes(ops->nx, ops->ny, G, dw);
@@ -1056,6 +1086,8 @@ int sweep_launch(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int
   a.trace = h_trace;
   a.trace_chunks = h_trace_chunks;
   a.skip = skip;
+  a.rhs_shared = rhs_shared;
+  a.phi_atomic = phi_atomic;
   {
     static const char* dbg = getenv("DLRSN_SWEEP_DEBUG");
     a.debug = dbg ? atoi(dbg) : 0;
@@ -1074,6 +1106,7 @@ int sweep_launch(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int
   bool use_ws = items <= 2 * sms;
   if (ws_env) use_ws = ws_env[0] == '1';
   if (phi_part_sk) use_ws = false;  // the warp-specialised kernel writes no closure partials
+  if (rhs_shared || phi_atomic) use_ws = false;
   SweepTimer* tm = g_timing ? timer_slot(G, dw) : nullptr;
   if (tm) DLRSN_TRY_CUDA(cudaEventRecord(tm->start, st));
   int rc;
@@ -1103,6 +1136,15 @@ int sweep_launch(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int
 }  // namespace dlrsn
 
 extern "C" {
+
+int dlrsn_sweep_closure(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int dw,
+                        const double* sigma_t_sk4, const double* scat_sk4, const double* rhs_sk4,
+                        double* phi, void* workspace, int64_t workspace_bytes, int max_ctas,
+                        dlrsn_stream_t stream) {
+  DLRSN_REQUIRE(phi, "dlrsn_sweep_closure needs phi");
+  return sweep_launch_ex(ops, G, groups, dw, sigma_t_sk4, scat_sk4, rhs_sk4, nullptr, nullptr,
+                         workspace, workspace_bytes, max_ctas, nullptr, 1, phi, as_stream(stream));
+}
 
 int dlrsn_sweep(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int dw,
                 const double* sigma_t_sk4, const double* scat_sk4, const double* rhs_sk,

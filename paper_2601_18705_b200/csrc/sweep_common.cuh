@@ -27,6 +27,11 @@ struct SweepArgs {
   int trace_chunks;
   const int* skip;  // device flag: return at once when set (speculative iterations)
   int debug;        // bit 0: ignore the strip inflow (timing experiments only)
+  // closure-only sweeps (full-SN stress, no psi storage): rhs_sk holds 4
+  // quadrant slabs of one rhs shared by every direction, psi_sk is null and
+  // the group's closure sum is added into the canonical phi_atomic
+  int rhs_shared;
+  double* phi_atomic;
 };
 
 // isotropic inflow psi_b on the left, right, bottom, top walls (0: vacuum)

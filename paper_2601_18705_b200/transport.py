@@ -244,6 +244,60 @@ def _sweep(ops, plan, rhs_sk, psi_sk, scat_sk4=None, phi_part=None, max_ctas=0):
         SWEEP_EVENTS.append((ev[0], ev[1], ops.grid.n_cells, plan.D, plan.G))
 
 
+def closure_sweep(ops, omegas, closure, rhs, *, scat_phi=None, dw=8, ws_limit=8 << 30):
+    """One sweep of many directions that all see the same rhs, returning only
+    the closure phi = sum_d closure_d psi_d (transport_sn.py:303-322 per
+    direction, psi @ closure of :438) -- psi is never stored.  This is the
+    full-SN stress sweep of config 5 (16384 directions on 4096^2: psi would
+    be 8.8 TB).  ``rhs`` (n_dofs) is the shared right-hand side, e.g.
+    source_vector(q) + inv_cdt M psi_old for an isotropic psi_old;
+    ``scat_phi`` (n_dofs, optional) adds the scattering source
+    M (sigma_s phi) / 4 pi.  Groups of ``dw`` directions add their closure
+    sums with fp64 atomics (dlrsn_sweep_closure), so phi is reproducible to
+    round-off only; the groups are launched in batches whose strip-handoff
+    workspace stays under ``ws_limit`` bytes."""
+    g = ops.grid
+    st = ops.step
+    om = np.asarray(omegas.cpu() if isinstance(omegas, torch.Tensor) else omegas, dtype=float)
+    clo = np.asarray(closure.cpu() if isinstance(closure, torch.Tensor) else closure, dtype=float)
+    if clo.shape != (om.shape[0],):
+        raise ContractViolation("closure vector must have one entry per swept angle")
+    vl = ops.vec_len
+    rhs = as_device(rhs).reshape(g.n_dofs, 1)
+    cols = rhs.expand(-1, 4).contiguous()  # the same rhs in the 4 quadrant orientations
+    rhs4 = ops.buffer("rhs4", 4 * vl)
+    quads4 = upload(np.arange(4, dtype=np.int32))
+    zero_q = ops.buffer("zero_q", g.n_cells, zero=True)
+    _lib.call("dlrsn_rhs_build", ops.cellops_ptr, 4, _lib.ptr(quads4), _lib.ptr(zero_q), 0.0,
+              None, 1, _lib.ptr(cols), 4, _lib.ptr(rhs4), stream())
+    del cols
+    scat = None
+    if scat_phi is not None:
+        scat = ops.buffer("scat_sk4", 4 * vl)
+        flags = zeros(1, dtype=torch.int32)
+        _lib.call("dlrsn_scatter_source", ops.cellops_ptr, _lib.ptr(as_device(scat_phi)),
+                  _lib.ptr(st.sigma_s), _lib.ptr(scat), _lib.ptr(flags), stream())
+    ns = (g.ny + 31) // 32
+    groups, dw, _ = plan_groups(om, clo, ns, dw=dw)
+    G = len(groups)
+    lib = _lib.load()
+    per_group = int(lib.dlrsn_sweep_workspace_bytes(g.nx, g.ny, 1, dw))
+    batch = max(1, min(G, ws_limit // max(per_group, 1)))
+    ws_bytes = int(lib.dlrsn_sweep_workspace_bytes(g.nx, g.ny, batch, dw))
+    ws = sweep_workspace(ops, ws_bytes)
+    gdev = _groups_to_device(groups)
+    gsize = _lib.GROUP_DTYPE.itemsize
+    phi = zeros(g.n_dofs)
+    sig = ops.sigma_t_sk4()
+    for g0 in range(0, G, batch):
+        nb = min(batch, G - g0)
+        _lib.call("dlrsn_sweep_closure", ops.cellops_ptr, nb,
+                  ctypes.c_void_p(gdev.data_ptr() + g0 * gsize), dw, _lib.ptr(sig),
+                  _lib.ptr(scat), _lib.ptr(rhs4), _lib.ptr(phi), _lib.ptr(ws), ws.numel(), 0,
+                  stream())
+    return phi
+
+
 def _to_canonical(ops, plan, psi_sk, out=None):
     g = ops.grid
     psi = out if out is not None else empty(g.n_dofs, plan.D)

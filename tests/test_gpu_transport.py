@@ -286,3 +286,31 @@ def test_dsa_step_collocation_matches_reference(golden):
     assert list(info.angle_indices) == list(g["cold_idx"])
     assert info.iterations == int(g["cold_iters"])
     assert np.abs(_np(new.X) - g["cold_newX"]).max() <= 1e-12
+
+
+@pytest.mark.parametrize("nx,ny,npol,naz,dw", [(40, 70, 4, 8, 8), (33, 29, 2, 6, 2), (70, 40, 4, 8, 1)])
+def test_closure_sweep_matches_oracle(nx, ny, npol, naz, dw):
+    """Config 5's closure-only full-SN sweep (psi never stored, closure sums
+    added with fp64 atomics): phi against the oracle's sweeps of every
+    direction with the shared rhs, to round-off (the atomic order varies)."""
+    from oracle import port as P
+    from paper_2601_18705_b200 import transport as Tr
+    from paper_2601_18705_b200.angular import build_quadrature
+    from paper_2601_18705_b200.mesh import build_grid
+
+    rng = np.random.default_rng(nx + ny)
+    n = nx * ny
+    sig = np.exp(rng.uniform(np.log(0.1), np.log(100.0), n))
+    q = rng.uniform(0, 1, n)
+    grid = build_grid(nx, ny, (0.0, 0.0, float(nx), float(ny)))
+    quad = build_quadrature(npol, naz)
+    ops = Tr.assemble_operators(grid, _manual_step(n, sig, 0 * sig, q, 1.0))
+    psi_old = rng.uniform(0, 1, 4 * n)  # isotropic previous intensity
+    rhs = ops.source_vector(q) + 1.0 * ops.mass_apply(psi_old)
+    phi = Tr.closure_sweep(ops, quad.omegas, quad.weights, rhs, dw=dw, ws_limit=1 << 13)
+    pg = P.Grid(nx, ny, 0.0, 0.0, float(nx), float(ny))
+    pops = P.assemble_operators(pg, P.Step(sig, 0 * sig, sig - 1.0, q, np.zeros(n), np.ones(n),
+                                           np.ones(n), 1.0, 1.0))
+    rhs_np = pops.source_vector(q) + pops.mass_apply(psi_old)
+    ref = P.sweep_many(pops, quad.omegas, np.tile(rhs_np[:, None], (1, quad.n_angles))) @ quad.weights
+    assert rel_l2(_np(phi), ref) <= 1e-13
