@@ -244,7 +244,7 @@ def _sweep(ops, plan, rhs_sk, psi_sk, scat_sk4=None, phi_part=None, max_ctas=0):
         SWEEP_EVENTS.append((ev[0], ev[1], ops.grid.n_cells, plan.D, plan.G))
 
 
-def closure_sweep(ops, omegas, closure, rhs, *, scat_phi=None, dw=8, ws_limit=8 << 30):
+def closure_sweep(ops, omegas, closure, rhs, *, scat_phi=None, dw=4, ws_limit=8 << 30):
     """One sweep of many directions that all see the same rhs, returning only
     the closure phi = sum_d closure_d psi_d (transport_sn.py:303-322 per
     direction, psi @ closure of :438) -- psi is never stored.  This is the

@@ -32,7 +32,7 @@ def main():
     for rep in range(2):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        phi = transport.closure_sweep(ops, quad.omegas, quad.weights, rhs)
+        phi = transport.closure_sweep(ops, quad.omegas, quad.weights, rhs, dw=int(os.environ.get("DW", "4")))
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
