@@ -311,6 +311,145 @@ __global__ void fill_empty_kernel(double* p, int64_t n) {
   if (i < n) p[i] = __longlong_as_double((long long)kEmpty);
 }
 
+// ---- tiled canonical <-> SK transposes ----------------------------------------
+// A block owns a canonical tile of 8 x 32 cells and walks the directions in
+// chunks of 8.  The canonical side moves whole 64-byte runs (8 directions of
+// one dof row); the SK side is written / read along the skewed diagonals of
+// the tile in the direction's own orientation, so 8 consecutive threads touch
+// 8 consecutive SK lanes of one step (128-byte runs) instead of 32 scattered
+// 16-byte pieces.  The chunk is staged in shared memory as [dof][dir][cell].
+constexpr int kTrI = 8, kTrJ = 32, kTrD = 8, kTrCells = kTrI * kTrJ;
+constexpr int kTrS = kTrCells + 1;  // cell stride (conflict-free staging writes)
+constexpr size_t kTrSmem = (size_t)4 * kTrD * kTrS * sizeof(double);
+
+// e-th cell of the tile in diagonal order of the oriented local frame:
+// diagonal t' = il + jl, lanes jl rising along a diagonal
+__device__ __forceinline__ void tr_diag_cell(int e, int& il, int& jl) {
+  // diagonals t' = 0..38 hold min(t'+1, 8, 39-t') cells; walk the counts
+  int t = 0, base = 0;
+  for (;; ++t) {
+    const int lo = t - (kTrI - 1) > 0 ? t - (kTrI - 1) : 0;
+    const int hi = t < kTrJ - 1 ? t : kTrJ - 1;
+    const int cnt = hi - lo + 1;
+    if (e < base + cnt) {
+      jl = lo + (e - base);
+      il = t - jl;
+      return;
+    }
+    base += cnt;
+  }
+}
+
+__global__ void __launch_bounds__(256) rhs_build_tiled_kernel(
+    int nx, int ny, int D, const int* __restrict__ quad, const double* __restrict__ q,
+    double inv_cdt, const double* __restrict__ pt, int ldp, const double* __restrict__ ex, int lde,
+    double* __restrict__ out, int64_t vlen, dlrsn_cellops ops) {
+  extern __shared__ double tr_sm[];  // [4][kTrD][kTrS]
+  const int i0 = blockIdx.x * kTrI, j0 = blockIdx.y * kTrJ;
+  const int ti = min(kTrI, nx - i0), tj = min(kTrJ, ny - j0);
+  const int T = nx + 31;
+  int il, jl;
+  tr_diag_cell(threadIdx.x, il, jl);
+  for (int d0 = 0; d0 < D; d0 += kTrD) {
+    const int dn = min(kTrD, D - d0);
+    if (pt) {
+      // canonical rows: e -> (cell, dof, dir) with dir fastest (64-byte runs);
+      // unrolled so that each thread has 8 loads in flight
+#pragma unroll 8
+      for (int e = threadIdx.x; e < kTrCells * 4 * kTrD; e += blockDim.x) {
+        const int dd = e & (kTrD - 1), l = (e >> 3) & 3, cl = e >> 5;
+        const int ci = cl & (kTrI - 1), cj = cl >> 3;
+        double v = 0.0;
+        if (ci < ti && cj < tj && dd < dn) {
+          const int64_t c = (int64_t)(j0 + cj) * nx + i0 + ci;
+          v = pt[(4 * c + l) * ldp + d0 + dd];
+        }
+        tr_sm[(l * kTrD + dd) * kTrS + cl] = v;
+      }
+    }
+    __syncthreads();
+    for (int dd = 0; dd < dn; ++dd) {
+      const int d = d0 + dd;
+      const int qd = quad[d];
+      // oriented local (il, jl) -> canonical local cell of this direction
+      const int ci = (qd & 1) ? ti - 1 - il : il;
+      const int cj = (qd & 2) ? tj - 1 - jl : jl;
+      if (il < ti && jl < tj) {
+        const int cl = cj * kTrI + ci;
+        const int64_t c = (int64_t)(j0 + cj) * nx + i0 + ci;
+        const double qc = q[c];
+        double v[4];
+#pragma unroll
+        for (int l = 0; l < 4; ++l) v[l] = qc * ops.src_row[l];
+        if (pt) {
+          double u[4];
+#pragma unroll
+          for (int l = 0; l < 4; ++l) u[l] = tr_sm[(l * kTrD + dd) * kTrS + cl];
+#pragma unroll
+          for (int l = 0; l < 4; ++l) {
+            const double mu = ops.mass[4 * l] * u[0] + ops.mass[4 * l + 1] * u[1] +
+                              ops.mass[4 * l + 2] * u[2] + ops.mass[4 * l + 3] * u[3];
+            v[l] += inv_cdt * mu;
+          }
+        }
+        if (ex) {
+#pragma unroll
+          for (int l = 0; l < 4; ++l) v[l] += ex[(4 * c + l) * lde + d];
+        }
+        const int f = sk_flip(qd);
+        int s, t, lane;
+        sk_locate(i0 + ci, j0 + cj, qd, nx, ny, s, t, lane);
+        double2* o = reinterpret_cast<double2*>(out + (int64_t)d * vlen);
+        o[sk_vec_off(T, s, t, 0, lane) >> 1] = make_double2(v[0 ^ f], v[1 ^ f]);
+        o[sk_vec_off(T, s, t, 1, lane) >> 1] = make_double2(v[2 ^ f], v[3 ^ f]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) sk_to_canonical_tiled_kernel(
+    int nx, int ny, int D, const int* __restrict__ quad, const double* __restrict__ sk,
+    double* __restrict__ psi, int ld, int64_t vlen) {
+  extern __shared__ double tr_sm[];  // [4][kTrD][kTrS]
+  const int i0 = blockIdx.x * kTrI, j0 = blockIdx.y * kTrJ;
+  const int ti = min(kTrI, nx - i0), tj = min(kTrJ, ny - j0);
+  const int T = nx + 31;
+  int il, jl;
+  tr_diag_cell(threadIdx.x, il, jl);
+  for (int d0 = 0; d0 < D; d0 += kTrD) {
+    const int dn = min(kTrD, D - d0);
+    for (int dd = 0; dd < dn; ++dd) {
+      const int d = d0 + dd;
+      const int qd = quad[d];
+      const int ci = (qd & 1) ? ti - 1 - il : il;
+      const int cj = (qd & 2) ? tj - 1 - jl : jl;
+      if (il < ti && jl < tj) {
+        const int cl = cj * kTrI + ci;
+        const int f = sk_flip(qd);
+        int s, t, lane;
+        sk_locate(i0 + ci, j0 + cj, qd, nx, ny, s, t, lane);
+        const double* src = sk + (int64_t)d * vlen;
+        const double2 a = *reinterpret_cast<const double2*>(src + sk_vec_off(T, s, t, 0, lane));
+        const double2 b = *reinterpret_cast<const double2*>(src + sk_vec_off(T, s, t, 1, lane));
+        const double o[4] = {a.x, a.y, b.x, b.y};
+#pragma unroll
+        for (int l = 0; l < 4; ++l) tr_sm[(l * kTrD + dd) * kTrS + cl] = o[l ^ f];
+      }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kTrCells * 4 * kTrD; e += blockDim.x) {
+      const int dd = e & (kTrD - 1), l = (e >> 3) & 3, cl = e >> 5;
+      const int ci = cl & (kTrI - 1), cj = cl >> 3;
+      if (ci < ti && cj < tj && dd < dn) {
+        const int64_t c = (int64_t)(j0 + cj) * nx + i0 + ci;
+        psi[(4 * c + l) * ld + d0 + dd] = tr_sm[(l * kTrD + dd) * kTrS + cl];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // rhs_sk[d] = source_vector(q) + inv_cdt M psi_time[:, d] + extra[:, d]
 __global__ void rhs_build_kernel(int nx, int ny, int D, const int* __restrict__ quad,
                                  const double* __restrict__ q, double inv_cdt,
@@ -784,6 +923,16 @@ __global__ void sk_to_canonical_kernel(int nx, int ny, int D, const int* __restr
 
 static int64_t handoff_offset_bytes(int, int, int) { return 256; }
 
+// tiled canonical <-> SK transposes (DLRSN_TILED_TRANSPOSE=0: the
+// thread-per-(cell, direction) kernels)
+static bool tiled_transposes() {
+  static const bool on = [] {
+    const char* e = getenv("DLRSN_TILED_TRANSPOSE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // configuration variant of the single-direction throughput kernel
 static int sweep1_variant() {
   static const int v = [] {
@@ -889,6 +1038,16 @@ int dlrsn_rhs_build(const dlrsn_cellops* ops, int D, const int* quad, const doub
   DLRSN_REQUIRE(ops && D >= 0, "bad arguments to dlrsn_rhs_build");
   const int64_t n = (int64_t)ops->nx * ops->ny * D;
   if (n == 0) return DLRSN_OK;
+  if (tiled_transposes()) {
+    DLRSN_TRY_CUDA(cudaFuncSetAttribute(rhs_build_tiled_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrSmem));
+    const dim3 grid((ops->nx + kTrI - 1) / kTrI, (ops->ny + kTrJ - 1) / kTrJ);
+    rhs_build_tiled_kernel<<<grid, 256, kTrSmem, as_stream(stream)>>>(
+        ops->nx, ops->ny, D, quad, q, inv_cdt, psi_time, ld_psi_time, extra, ld_extra, rhs_sk,
+        sk_vec_len(ops->nx, ops->ny), *ops);
+    DLRSN_CHECK_LAUNCH("rhs_build_tiled_kernel");
+    return DLRSN_OK;
+  }
   rhs_build_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(
       ops->nx, ops->ny, D, quad, q, inv_cdt, psi_time, ld_psi_time, extra, ld_extra, rhs_sk,
       sk_vec_len(ops->nx, ops->ny), *ops);
@@ -965,6 +1124,15 @@ int dlrsn_sk_to_canonical(const dlrsn_cellops* ops, int D, const int* quad, cons
                           double* psi, int ld, dlrsn_stream_t stream) {
   const int64_t n = (int64_t)ops->nx * ops->ny * D;
   if (n == 0) return DLRSN_OK;
+  if (tiled_transposes()) {
+    DLRSN_TRY_CUDA(cudaFuncSetAttribute(sk_to_canonical_tiled_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrSmem));
+    const dim3 grid((ops->nx + kTrI - 1) / kTrI, (ops->ny + kTrJ - 1) / kTrJ);
+    sk_to_canonical_tiled_kernel<<<grid, 256, kTrSmem, as_stream(stream)>>>(
+        ops->nx, ops->ny, D, quad, psi_sk, psi, ld, sk_vec_len(ops->nx, ops->ny));
+    DLRSN_CHECK_LAUNCH("sk_to_canonical_tiled_kernel");
+    return DLRSN_OK;
+  }
   sk_to_canonical_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(
       ops->nx, ops->ny, D, quad, psi_sk, psi, ld, sk_vec_len(ops->nx, ops->ny));
   DLRSN_CHECK_LAUNCH("sk_to_canonical_kernel");
