@@ -174,7 +174,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--full-sn", type=int, default=1, help="also time the config-2 full-SN sweep")
-    ap.add_argument("--more-configs", default="C4,C3,C5",
+    ap.add_argument("--more-configs", default="C4,C3,C5dlr,C5",
                     help="also time a few steps of these BASELINE configs at N=1 ('' = none)")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -431,6 +431,8 @@ def measure_config(name, steps=5, warmup=3):
 
     if name == "C5":
         return measure_c5_sweep()
+    if name == "C5dlr":
+        return measure_c5_dlr_sweep()
     if name == "C3":
         spec = problems.marshak()
         label = "C3 Marshak 512x512, r=32, 64x64 quadrature, inflow T_b=1, dlr-sn step"
@@ -473,6 +475,85 @@ def measure_config(name, steps=5, warmup=3):
                      "alg_bytes_per_launch": alg, "achieved_GBs": alg / (sweep_ms * 1e-3) / 1e9,
                      "frac_of_hbm": alg / (sweep_ms * 1e-3) / 1e9 / peak}}
     del state, lin, T, dp, flush
+    torch.cuda.empty_cache()
+    return out
+
+
+def measure_c5_dlr_sweep(reps=3):
+    """Config 5's DLR sweep on one GPU: the r = 128 directions DEIM selects
+    from a seeded random orthonormal W (16384 x 128, lowrank.py:168-205),
+    swept over the 4096^2 tile medium with psi STORED for every direction
+    (rhs and psi are 69 GB each in the SK layout, both in HBM), i.e. the
+    per-iteration sweep of the C5 DLR step (sigma_s = 0: one sweep per step,
+    no scattering source).  The rhs of every direction is the step's
+    source_vector(q) + inv_cdt M psi_old for the isotropic psi_old = B(T0)
+    (forming X S W_sel^T needs the 68.7 GB X, which with rhs and psi does
+    not fit one GPU; the sweep's traffic and arithmetic do not depend on
+    the rhs values).  Algorithmic bytes: 64 per cell-angle + 32 per cell
+    (sigma_t in 4 quadrant orientations)."""
+    import torch
+
+    from paper_2601_18705_b200 import _lib, problems, transport
+    from paper_2601_18705_b200.driver import DeviceProblem
+    from paper_2601_18705_b200.lowrank import deim_select
+
+    spec, fields = problems.stress()
+    rng = np.random.default_rng(spec.seed)
+    fields(rng)
+    dp = DeviceProblem.from_spec(spec)
+    T = torch.as_tensor(spec.T0, device="cuda")
+    lin = dp.linearized(T)
+    ops = transport.assemble_operators(dp.grid, lin)
+    quad = dp.quad
+    W0 = torch.randn(quad.n_angles, spec.rank, dtype=torch.float64, device="cuda",
+                     generator=torch.Generator(device="cuda").manual_seed(spec.seed))
+    W = torch.linalg.qr(W0 * torch.sqrt(quad.weights_device())[:, None])[0] / \
+        torch.sqrt(quad.weights_device())[:, None]
+    sel = deim_select(W)
+    idx = sel.indices
+    om = quad.omegas[idx]
+    cw = np.ones(len(idx))
+    plan = transport._SweepPlan(ops, om, cw)
+    b0 = (spec.a_r * spec.c / (4 * np.pi)) * (T * T) ** 2
+    rhs = ops.source_vector(lin.q) + lin.inv_cdt * ops.mass_apply(b0.repeat_interleave(4))
+    vl = ops.vec_len
+    rhs4 = torch.empty(4 * vl, dtype=torch.float64, device="cuda")
+    cols = rhs.reshape(-1, 1).expand(-1, 4).contiguous()
+    quads4 = torch.arange(4, dtype=torch.int32, device="cuda")
+    zero_q = torch.zeros(spec.n_cells, dtype=torch.float64, device="cuda")
+    _lib.call("dlrsn_rhs_build", ops.cellops_ptr, 4, _lib.ptr(quads4), _lib.ptr(zero_q), 0.0,
+              None, 1, _lib.ptr(cols), 4, _lib.ptr(rhs4), transport.stream())
+    del cols, W0, W
+    D = len(idx)
+    quads = plan.quads_dev.cpu().numpy()
+    rhs_sk = torch.empty(D * vl, dtype=torch.float64, device="cuda")
+    for d in range(D):
+        rhs_sk[d * vl:(d + 1) * vl].copy_(rhs4[int(quads[d]) * vl:(int(quads[d]) + 1) * vl])
+    del rhs4
+    psi_sk = torch.empty_like(rhs_sk)
+    transport._sweep(ops, plan, rhs_sk, psi_sk)  # warm-up
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(reps)]
+    for e0, e1 in evs:  # 138 GB touched per sweep: inputs far larger than L2
+        e0.record()
+        transport._sweep(ops, plan, rhs_sk, psi_sk)
+        e1.record()
+    torch.cuda.synchronize()
+    ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    n_sel_quads = np.bincount(quads, minlength=4).tolist()
+    chk = float(psi_sk[:vl].sum())
+    alg = spec.n_cells * (D * SWEEP_BYTES_PER_CELL_ANGLE + 32)
+    peak, _ = _peaks()
+    out = {"workload": "C5 stress 4096x4096, r=128 DEIM-selected of 128x128 directions, "
+                       "DLR sweep with psi stored (sigma_s = 0: one sweep per step)",
+           "kernel": f"sweep_kernel<{plan.dw}>", "groups": plan.G, "directions_per_quadrant":
+           n_sel_quads, "ms_per_sweep": ms, "cell_angle_per_s": spec.n_cells * D / (ms * 1e-3),
+           "alg_bytes_per_launch": alg, "achieved_GBs": alg / (ms * 1e-3) / 1e9,
+           "frac_of_hbm": alg / (ms * 1e-3) / 1e9 / peak, "psi_checksum": chk,
+           "note": "rhs = source + inv_cdt M B(T0) per direction (X S W_sel^T needs the "
+                   "68.7 GB X); l2: inputs 138 GB >> L2"}
+    del rhs_sk, psi_sk, ops, lin, T, rhs, dp, plan
     torch.cuda.empty_cache()
     return out
 
