@@ -270,8 +270,10 @@ def main():
             traffic = None
 
     # ---- end-to-end: public API with HOST (pinned) buffers each step -------
+    # (untimed warm-up long enough for both buffer sets' step graphs to be
+    # captured: output buffers cycle through the caching allocator)
     e2e = measure_e2e(dp, state, Tbox[0], lin, max(1, min(args.steps, 20)), comm,
-                      warmup=args.warmup)
+                      warmup=max(args.warmup, 8))
 
     # ---- full-SN comparison sweep (config 2: all 1024 directions) ----------
     full = measure_full_sn(dp, comm) if args.full_sn else None
@@ -376,7 +378,8 @@ def measure_e2e(dp, state, T, lin, n, comm=None, warmup=3):
                               **{f: d[f] for f in fields})
         new, info = step_collocation(dp.grid, step, dp.quad, st, si_tol=1e-8, use_dsa=False,
                                      comm=comm)
-        Tn = dp.advance(step, info.phi, d["T0"].clone())
+        # T update in place on this step's input slot (re-filled by the upload of step k+2)
+        Tn = dp.advance(step, info.phi, d["T0"])
         freed[b].record(comp)  # the input set may be overwritten from here on
         res = {"X": new.X, "S": new.S, "W": new.W.values, "T": Tn.T0}
         done[b].record(comp)

@@ -360,6 +360,11 @@ typedef struct dlrsn_step_params {
   int sweep_dw;              /* sweep group width (0 = 1) */
   const dlrsn_advance* advance; /* optional fused T update + re-linearisation (NULL: none) */
   double inflow[4];          /* isotropic inflow psi_b: left, right, bottom, top (0: vacuum) */
+  const double* x_check_in;  /* device, optional: max|X^T M X - I| of the input X, already
+                                computed by the step that produced it (the input Gram is then
+                                skipped; M depends on the grid only, so the value is the one
+                                the Gram would give).  NULL: compute it */
+  double* x_check_out;       /* device, optional: receives max|X_new^T M X_new - I| */
 } dlrsn_step_params;
 
 typedef struct dlrsn_step_info { /* HOST, filled by the call */

@@ -49,7 +49,8 @@ class StepParams(ctypes.Structure):
     _fields_ = [("rank", c_int), ("n_omega", c_int), ("omegas_host", c_vp), ("omegas_dev", c_vp),
                 ("weights_dev", c_vp), ("inv_cdt", c_dbl), ("si_tol", c_dbl),
                 ("si_max_iters", c_int), ("check_state", c_int), ("gs_method", c_int),
-                ("sweep_dw", c_int), ("advance", c_vp), ("inflow", c_dbl * 4)]
+                ("sweep_dw", c_int), ("advance", c_vp), ("inflow", c_dbl * 4),
+                ("x_check_in", c_vp), ("x_check_out", c_vp)]
 
 
 class StepInfo(ctypes.Structure):

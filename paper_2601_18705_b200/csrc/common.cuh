@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <atomic>
 
 #include "../../include/dlrsn.h"
@@ -47,6 +48,24 @@ inline std::atomic<int64_t>& launch_counter() {
   } while (0)
 
 inline cudaStream_t as_stream(dlrsn_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Zero fill as a kernel, not cudaMemsetAsync: a memset can be queued on a
+// copy engine behind unrelated bulk host<->device copies of other streams
+// (measured: 256-byte memsets stretched to 75-135 us while bench.py's e2e
+// copies ran), while a kernel stays on the compute pipe.
+static __global__ void zero_words_kernel(uint32_t* p, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 0u;
+}
+static inline cudaError_t zero_async(void* p, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return cudaSuccess;
+  const int64_t n = (int64_t)((bytes + 3) / 4);  // callers pass 4-byte multiples
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 1184);
+  zero_words_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<uint32_t*>(p), n);
+  launch_counter().fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
 
 constexpr double kFourPi = 12.566370614359172;  // 4*np.pi
 constexpr double kPi = 3.141592653589793;

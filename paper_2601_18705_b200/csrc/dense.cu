@@ -2406,7 +2406,7 @@ int dlrsn_project(const dlrsn_cellops* ops, int r, const double* X, const double
   pa.part = partial; pa.cells_per_block = cpb;
   cudaStream_t st = as_stream(stream);
   // partial slots not written by some tiles must be zero
-  DLRSN_TRY_CUDA(cudaMemsetAsync(partial, 0, sizeof(double) * (size_t)nblk * (7 * (size_t)r * r + r), st));
+  DLRSN_TRY_CUDA(zero_async(partial, sizeof(double) * (size_t)nblk * (7 * (size_t)r * r + r), st));
   static const char* simt = getenv("DLRSN_PROJECT_SIMT");
   static const char* wide = getenv("DLRSN_PROJECT_WIDE");
   if (r > kTile && !(wide && wide[0] == '0') && !(simt && simt[0] == '1')) {
@@ -2415,7 +2415,7 @@ int dlrsn_project(const dlrsn_cellops* ops, int r, const double* X, const double
     const int cpb32 = project32_cells_per_block(ncell, r);
     const int nblk32 = (ncell + cpb32 - 1) / cpb32;
     pa.cells_per_block = cpb32;
-    DLRSN_TRY_CUDA(cudaMemsetAsync(partial, 0, sizeof(double) * (size_t)nblk32 * (7 * (size_t)r * r + r), st));
+    DLRSN_TRY_CUDA(zero_async(partial, sizeof(double) * (size_t)nblk32 * (7 * (size_t)r * r + r), st));
     DLRSN_TRY_CUDA(cudaFuncSetAttribute(project_mma32_kernel,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)kProj32Smem));

@@ -96,15 +96,19 @@ static int wgram(int n, int r, const double* W, const double* w, double* part, d
 }
 
 // out[0] = max |Gx - I|, out[1] = max |Gw - I| (DlrState.check, lowrank.py:68-81)
+// Gx == nullptr: the spatial residual is already known (*x_known, written
+// by the step that produced X); x_copy (optional) receives out[0].
 __global__ void ortho_residual_kernel(int r, const double* __restrict__ Gx,
-                                      const double* __restrict__ Gw, double* out) {
+                                      const double* __restrict__ Gw, double* out,
+                                      const double* x_known = nullptr, double* x_copy = nullptr) {
   __shared__ double red[2][32];
   double m[2] = {0.0, 0.0};
   for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
     const double d = (e / r == e % r) ? 1.0 : 0.0;
-    m[0] = fmax(m[0], fabs(Gx[e] - d));
+    if (Gx) m[0] = fmax(m[0], fabs(Gx[e] - d));
     m[1] = fmax(m[1], fabs(Gw[e] - d));
   }
+  if (!Gx && threadIdx.x == 0) m[0] = *x_known;
   for (int q = 0; q < 2; ++q) {
     double v = m[q];
     for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(kFull, v, o));
@@ -115,6 +119,7 @@ __global__ void ortho_residual_kernel(int r, const double* __restrict__ Gx,
     double v = 0.0;
     for (int k = 0; k < (int)(blockDim.x >> 5); ++k) v = fmax(v, red[threadIdx.x][k]);
     out[threadIdx.x] = v;
+    if (threadIdx.x == 0 && x_copy) *x_copy = v;
   }
 }
 
@@ -380,14 +385,20 @@ struct StepStatus {
   int cholflag[2], cholw[2];
 };
 
-// pinned host copy of the status block (one per host thread; its address is
-// baked into captured graphs, so it is never reallocated)
+// pinned, device-mapped host copy of the status block (one per host thread;
+// its address is baked into captured graphs, so it is never reallocated).
+// The pack kernel stores into it directly: no copy-engine transfer, so the
+// step's readback never queues behind bulk copies of other streams.
+static thread_local StepStatus* g_status_dev = nullptr;
 static int status_block(StepStatus** out) {
   static thread_local StepStatus* hs = nullptr;
   if (!hs) {
     void* ptr = nullptr;
-    DLRSN_TRY_CUDA(cudaHostAlloc(&ptr, sizeof(StepStatus), cudaHostAllocDefault));
+    DLRSN_TRY_CUDA(cudaHostAlloc(&ptr, sizeof(StepStatus), cudaHostAllocMapped));
+    void* dptr = nullptr;
+    DLRSN_TRY_CUDA(cudaHostGetDevicePointer(&dptr, ptr, 0));
     hs = static_cast<StepStatus*>(ptr);
+    g_status_dev = static_cast<StepStatus*>(dptr);
   }
   *out = hs;
   return DLRSN_OK;
@@ -419,9 +430,9 @@ static int enqueue_status(cudaStream_t st, const StepBufs& b, int r, StepStatus*
   add(b.ratiow, 2 * r * sizeof(double), dev->ratiow);
   add(b.cholflag, 2 * sizeof(int), dev->cholflag);
   add(b.cholw, 2 * sizeof(int), dev->cholw);
-  pack_kernel<<<1, 256, 0, st>>>(l, b.rbdev);
+  (void)hs;
+  pack_kernel<<<1, 256, 0, st>>>(l, reinterpret_cast<unsigned*>(g_status_dev));
   DLRSN_CHECK_LAUNCH("pack_kernel");
-  DLRSN_TRY_CUDA(cudaMemcpyAsync(hs, dev, sizeof(StepStatus), cudaMemcpyDeviceToHost, st));
   return DLRSN_OK;
 }
 
@@ -792,9 +803,11 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
                                                                            b.flags);
       DLRSN_CHECK_LAUNCH("sigma_check_kernel");
       if (p->check_state) {
-        DLRSN_RET(dlrsn_mgram(ops, r, r, X, r, X, r, nullptr, b.G, b.part, ss2));
+        // the input Gram is skipped when the producing step already checked X
+        if (!p->x_check_in) DLRSN_RET(dlrsn_mgram(ops, r, r, X, r, X, r, nullptr, b.G, b.part, ss2));
         DLRSN_RET(wgram(no, r, W, p->weights_dev, b.wpart, b.wg, sd));
-        ortho_residual_kernel<<<1, 256, 0, sd>>>(r, b.G, b.wg, b.chk_in);
+        ortho_residual_kernel<<<1, 256, 0, sd>>>(r, p->x_check_in ? nullptr : b.G, b.wg,
+                                                 b.chk_in, p->x_check_in);
         DLRSN_CHECK_LAUNCH("ortho_residual_kernel");
       }
       // scalar_flux (lowrank.py:60-62) -> the first scattering source
@@ -854,7 +867,7 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
                                        sigma_s, nullptr, nullptr, b.norms, b.red_ws, b.ctl, -1,
                                        p->si_tol, nullptr, comm->reduce_buf, st));
         else
-          DLRSN_TRY_CUDA(cudaMemsetAsync(comm->reduce_buf, 0, N * sizeof(double), st));
+          DLRSN_TRY_CUDA(zero_async(comm->reduce_buf, N * sizeof(double), st));
         if (comm->allreduce_sum(comm->user) != 0) {
           set_error("allreduce of the closure flux failed");
           return DLRSN_ECUDA;
@@ -885,8 +898,8 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
   auto enqueue_tail = [&](cudaStream_t st, int exact, int exact_w, bool reset) -> int {
     void* s = st;
     if (reset) {
-      DLRSN_TRY_CUDA(cudaMemsetAsync(b.statw, 0, sizeof(int), st));
-      DLRSN_TRY_CUDA(cudaMemsetAsync(b.statx, 0, sizeof(int), st));
+      DLRSN_TRY_CUDA(zero_async(b.statw, sizeof(int), st));
+      DLRSN_TRY_CUDA(zero_async(b.statx, sizeof(int), st));
     }
     if (!exact) {
       DLRSN_RET(dlrsn_mgram(ops, r, r, b.psi, r, b.psi, r, nullptr, b.G, b.part, s));
@@ -905,7 +918,7 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
                                    p->inv_cdt, b.T, b.qall, has_inflow ? b.hin : nullptr, infl,
                                    b.om_sel);
     DLRSN_CHECK_LAUNCH("qall_kernel");
-    DLRSN_TRY_CUDA(cudaMemsetAsync(b.rowstat, 0, (r + 1) * sizeof(int), st));
+    DLRSN_TRY_CUDA(zero_async(b.rowstat, (r + 1) * sizeof(int), st));
     DLRSN_RET(dlrsn_row_inverse(r, r, b.proj, b.om_sel, b.Binv, nullptr, b.rowstat, s));
     DLRSN_RET(dlrsn_row_combine(r, r, b.Binv, b.proj + 5 * r * r, b.qall, b.closure, b.L,
                                 b.lbar, b.rowstat + r, s));
@@ -936,7 +949,7 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
       DLRSN_RET(dlrsn_chol_upper(r, b.wg, b.Rw2, b.Rw2inv, b.ratiow2, b.cholw + 1, s));
       DLRSN_RET(dlrsn_rowmix(no, r, r, b.lq1, r, b.Rw2inv, r, 0.0, W_new, r, s));
       DLRSN_RET(dlrsn_small_matmul(r, r, r, b.Rw2, b.Rw1, b.Rang, 0, s));
-      DLRSN_TRY_CUDA(cudaMemsetAsync(b.defw, 0, r * sizeof(int), st));
+      DLRSN_TRY_CUDA(zero_async(b.defw, r * sizeof(int), st));
     } else
       DLRSN_RET(dlrsn_cgs2(no, r, b.lfull, r, W_new, r, b.Rang, b.defw, 0, p->weights_dev,
                            nullptr, 0, r + 8, b.up->aexp, p->omegas_dev, b.cgsws, b.statw, 1, s));
@@ -945,7 +958,7 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     DLRSN_CHECK_LAUNCH("finish_kernel");
     DLRSN_RET(join_from(fk, st));
     if (p->check_state) {
-      ortho_residual_kernel<<<1, 256, 0, st>>>(r, b.G, b.wg, b.chk_out);
+      ortho_residual_kernel<<<1, 256, 0, st>>>(r, b.G, b.wg, b.chk_out, nullptr, p->x_check_out);
       DLRSN_CHECK_LAUNCH("ortho_residual_kernel");
     }
     return enqueue_status(st, b, r, hs);

@@ -1179,7 +1179,7 @@ int dlrsn_debug_trace(unsigned long long* buf, int chunks) {
 int dlrsn_sweep_workspace_init(void* workspace, int64_t workspace_bytes, dlrsn_stream_t stream) {
   DLRSN_REQUIRE(workspace && workspace_bytes >= 256, "sweep workspace too small");
   cudaStream_t st = as_stream(stream);
-  DLRSN_TRY_CUDA(cudaMemsetAsync(workspace, 0, 256, st));
+  DLRSN_TRY_CUDA(zero_async(workspace, 256, st));
   const int64_t n = (workspace_bytes - 256) / (int64_t)sizeof(double);
   if (n > 0) {
     fill_empty_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
@@ -1221,7 +1221,7 @@ static int sweep_launch_ex(const dlrsn_cellops* ops, int G, const dlrsn_group* g
                 (long long)workspace_bytes, (long long)need);
   if (G == 0) return DLRSN_OK;
   const int64_t head = handoff_offset_bytes(ops->nx, ops->ny, G);
-  DLRSN_TRY_CUDA(cudaMemsetAsync(workspace, 0, sizeof(int), st));  // work ticket
+  DLRSN_TRY_CUDA(zero_async(workspace, sizeof(int), st));  // work ticket
   SweepArgs a;
   a.nx = ops->nx; a.ny = ops->ny; a.G = G;
   a.groups = groups;

@@ -399,7 +399,8 @@ class _NativeCtx:
         for z in sizes:
             offs.append(o)
             o += z + (z & 1)
-        self.out_len, self.offs = o, offs
+        self.x_slot = o  # spatial check of X_new (dlrsn_step_params.x_check_out)
+        self.out_len, self.offs = o + 2, offs
         self.shapes = [(n, r), (r, r), (no, r), (r,), (n,), (n,)]
         self.strides = [(r, 1), (r, 1), (r, 1), (1,), (1,), (1,)]
         self.fn = lib.dlrsn_step_collocation
@@ -445,6 +446,14 @@ def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_
     p.gs_method = 0 if gs_method == "cholqr2" else 1
     p.advance = ctypes.addressof(advance) if advance is not None else None
     p.inflow[:] = inflow if inflow is not None else (0.0, 0.0, 0.0, 0.0)
+    # DlrState.check of an X this library produced and already checked (same
+    # tensor, not modified since): the input Gram is not recomputed
+    xc = getattr(state, "_xcheck", None)
+    known = (check_state and xc is not None and xc[1] is state.X
+             and xc[2] == state.X._version and X is state.X)
+    p.x_check_in = xc[0].data_ptr() if known else None
+    slot = out[ctx.x_slot:ctx.x_slot + 1]
+    p.x_check_out = slot.data_ptr() if check_state else None
     info = _lib.StepInfo()
     hooks = ctx.hooks
     if hooks is not None:
@@ -475,6 +484,8 @@ def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_
     indices = np.frombuffer(info.angle_indices, dtype=np.int64, count=r).copy()
     basis = AngularBasis(values=W_new, beta=beta_new)
     new_state = DlrState(X=X_new, S=S_new, W=basis)
+    if check_state:
+        new_state._xcheck = (slot, X_new, X_new._version)
     res = CollocationStepInfo(
         iterations=int(info.iterations),
         selection=_NativeSelection(indices, W),

@@ -310,6 +310,15 @@ def test_native_step_raises_like_the_reference():
     step2.sigma_s.copy_(step2.sigma_t)
     with pytest.raises(ContractViolation, match="pseudo absorption"):
         step_collocation(grid, step2, quad, st, use_dsa=False)
+    # a state produced (and checked) by a step carries its spatial check, so
+    # the next step skips the input Gram; a modified X is checked again
+    s1, i1 = step_collocation(grid, step, quad, st, use_dsa=False)
+    assert getattr(s1, "_xcheck", None) is not None
+    s2, i2 = step_collocation(grid, step, quad, s1, use_dsa=False)
+    assert i2.iterations >= 1
+    s1.X.mul_(2.0)
+    with pytest.raises(ContractViolation, match="orthonormality"):
+        step_collocation(grid, step, quad, s1, use_dsa=False)
 
 
 def test_fused_step_boundary_matches_separate_advance():
