@@ -15,7 +15,7 @@ import numpy as np
 from .errors import ContractViolation, InterpolationError, SolverError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdlrsn.so")
+LIB_PATH = os.environ.get("DLRSN_LIB") or os.path.join(HERE, "libdlrsn.so")  # DLRSN_LIB: A/B builds
 
 MAX_DW = 8
 

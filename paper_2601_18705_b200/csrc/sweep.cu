@@ -102,7 +102,12 @@ sweep_kernel(const SweepArgs a) {
 
   for (;;) {
     int item = 0;
-    if (lane == 0) item = skip ? items : atomicAdd(a.ticket, 1);
+    if (lane == 0) {
+      item = skip ? items : atomicAdd(a.ticket, 1);
+      // every warp draws exactly one ticket past the end; the last of those
+      // draws re-arms the counter for the next launch (no memset per launch)
+      if (!skip && item == items + (int)(gridDim.x * blockDim.x / 32) - 1) atomicExch(a.ticket, 0);
+    }
     item = __shfl_sync(kFull, item, 0);
     if (item >= items) break;
     const int s = item / G;
@@ -1221,7 +1226,8 @@ static int sweep_launch_ex(const dlrsn_cellops* ops, int G, const dlrsn_group* g
                 (long long)workspace_bytes, (long long)need);
   if (G == 0) return DLRSN_OK;
   const int64_t head = handoff_offset_bytes(ops->nx, ops->ny, G);
-  DLRSN_TRY_CUDA(zero_async(workspace, sizeof(int), st));  // work ticket
+  // the work ticket is re-armed by the last draw of every launch (the
+  // workspace starts zeroed: dlrsn_sweep_workspace_init)
   SweepArgs a;
   a.nx = ops->nx; a.ny = ops->ny; a.G = G;
   a.groups = groups;

@@ -148,7 +148,11 @@ __global__ void __launch_bounds__(kWsThreads) sweep_ws_kernel(const SweepArgs a)
   uint32_t uses[kWsStages] = {};
 
   for (;;) {
-    if (threadIdx.x == 0) s_item = skip ? items : atomicAdd(a.ticket, 1);
+    if (threadIdx.x == 0) {
+      s_item = skip ? items : atomicAdd(a.ticket, 1);
+      // one draw past the end per CTA; the last one re-arms the counter
+      if (!skip && s_item == items + (int)gridDim.x - 1) atomicExch(a.ticket, 0);
+    }
     __syncthreads();
     const int item = s_item;
     __syncthreads();
