@@ -1277,7 +1277,10 @@ static int sweep_launch_ex(const dlrsn_cellops* ops, int G, const dlrsn_group* g
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int items = sk_strips(ops->ny) * G;
-  bool use_ws = items <= 2 * sms;
+  // crossover measured on B200 (scripts/sweep_bench.py, configs.py): WS wins
+  // at 512 items (C3: 0.41 vs 0.63 ms) and 1024 items (1.31 vs 1.39 ms), the
+  // multi-warp kernel at 1152 items (1.05 vs 1.13 ms) and 2048 (C4: 1.59 vs 2.57)
+  bool use_ws = items <= 7 * sms;
   if (ws_env) use_ws = ws_env[0] == '1';
   if (phi_part_sk) use_ws = false;  // the warp-specialised kernel writes no closure partials
   if (rhs_shared || phi_atomic) use_ws = false;
