@@ -543,6 +543,33 @@ def sweep_solve(ops, omega, rhs):
     return sweep_many(ops, np.asarray(omega, float)[None, :], np.asarray(rhs, float)[:, None])[:, 0]
 
 
+
+def sweep_balance(grid, omega, sigma_t, rhs, psi):
+    """Global particle balance of one direction's upwind DG(Q1) solve, a
+    size-independent property of the reference discretisation
+    (transport_sn.py:142-163 local operator, :213-227 face couplings,
+    :303-322 sweep; vacuum inflow).  Testing every cell equation with the
+    constant 1 (the sum of its 4 rows): the volume streaming term vanishes
+    (the columns of the reference gradient blocks sum to zero: sum_i dN_i = 0),
+    each interior face's outflow term cancels the downwind cell's inflow
+    coupling (upwind flux), and 1^T M_hat = 1/4.  What is left is
+        sum_c sigma_t,c dx dy / 4 sum_l psi_{c,l}
+      + sum_{outflow walls} |omega.n| len (psi_a + psi_b) / 2  =  sum(rhs)
+    exactly, for any grid size.  Returns (left side, right side)."""
+    nx, ny = grid.nx, grid.ny
+    ox, oy = float(omega[0]), float(omega[1])
+    p = np.asarray(psi, dtype=float).reshape(ny, nx, 4)
+    st = np.asarray(sigma_t, dtype=float).reshape(ny, nx)
+    absorbed = float(np.sum(st * p.sum(axis=2))) * grid.dx * grid.dy / 4.0
+    out = 0.0
+    if ox != 0.0:  # right wall (dofs 1, 3) for ox > 0, left wall (0, 2) otherwise
+        col, e = (p[:, -1, :], EDGE["right"]) if ox > 0 else (p[:, 0, :], EDGE["left"])
+        out += abs(ox) * grid.dy * 0.5 * float(np.sum(col[:, e[0]] + col[:, e[1]]))
+    if oy != 0.0:
+        row, e = (p[-1, :, :], EDGE["top"]) if oy > 0 else (p[0, :, :], EDGE["bottom"])
+        out += abs(oy) * grid.dx * 0.5 * float(np.sum(row[:, e[0]] + row[:, e[1]]))
+    return absorbed + out, float(np.sum(np.asarray(rhs, dtype=float)))
+
 # --------------------------------------------------------------------------
 # synthetic diffusion (transport_sn.py:166-198, 325-367)
 

@@ -70,6 +70,19 @@ def test_sweep_matches_reference(golden, tag):
         assert rel_l2(psi[:, d], ref[:, d]) <= 1e-13, d
 
 
+@pytest.mark.parametrize("tag", ["a", "b"])
+def test_sweep_balance_holds_on_reference_sweeps(golden, tag):
+    """Pin of the size-independent balance check (oracle sweep_balance) on
+    the reference's own swept psi: every quadrant and the grazing angles."""
+    g = golden("sweep")
+    grid = _grid(g[f"{tag}_grid"])
+    sig = g[f"{tag}_sigma_t"]
+    for d, om in enumerate(g[f"{tag}_omegas"]):
+        lhs, rhs = P.sweep_balance(grid, om, sig, g[f"{tag}_rhs"][:, d], g[f"{tag}_psi"][:, d])
+        scale = np.abs(g[f"{tag}_rhs"][:, d]).sum()
+        assert abs(lhs - rhs) <= 1e-13 * scale, (d, lhs, rhs)
+
+
 def test_sweep_quadrant_reflection_identity():
     """A_c(omega) = P A_c(|omega|) P per quadrant: the basis
     of the single-code-path GPU sweep."""
