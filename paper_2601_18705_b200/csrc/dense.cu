@@ -2405,8 +2405,6 @@ int dlrsn_project(const dlrsn_cellops* ops, int r, const double* X, const double
   pa.X = X; pa.Xold = Xold; pa.sigma_t = sigma_t; pa.sigma_s = sigma_s; pa.q = q;
   pa.part = partial; pa.cells_per_block = cpb;
   cudaStream_t st = as_stream(stream);
-  // partial slots not written by some tiles must be zero
-  DLRSN_TRY_CUDA(zero_async(partial, sizeof(double) * (size_t)nblk * (7 * (size_t)r * r + r), st));
   static const char* simt = getenv("DLRSN_PROJECT_SIMT");
   static const char* wide = getenv("DLRSN_PROJECT_WIDE");
   if (r > kTile && !(wide && wide[0] == '0') && !(simt && simt[0] == '1')) {
@@ -2427,6 +2425,8 @@ int dlrsn_project(const dlrsn_cellops* ops, int r, const double* X, const double
     DLRSN_CHECK_LAUNCH("reduce_partials_kernel");
     return DLRSN_OK;
   }
+  // partial slots not written by some tiles must be zero
+  DLRSN_TRY_CUDA(zero_async(partial, sizeof(double) * (size_t)nblk * (7 * (size_t)r * r + r), st));
   if (simt && simt[0] == '1') {
     project_kernel<<<dim3(nblk, tiles), kTile * kTile, 0, st>>>(pa, *ops);
     DLRSN_CHECK_LAUNCH("project_kernel");
