@@ -275,10 +275,11 @@ def main():
             traffic = None
 
     # ---- end-to-end: public API with HOST (pinned) buffers each step -------
-    # (untimed warm-up long enough for both buffer sets' step graphs to be
-    # captured: output buffers cycle through the caching allocator)
+    # (untimed warm-up long enough for every step graph of the rotation to be
+    # captured: 2 input sets x 3 output blocks cycling through the caching
+    # allocator = 6 buffer keys, each captured on its second sighting)
     e2e = measure_e2e(dp, state, Tbox[0], lin, max(1, min(args.steps, 20)), comm,
-                      warmup=max(args.warmup, 8))
+                      warmup=max(args.warmup, 14))
 
     # ---- full-SN comparison sweep (config 2: all 1024 directions) ----------
     full = measure_full_sn(dp, comm) if args.full_sn else None
