@@ -1463,7 +1463,14 @@ __device__ int warp_chol_reg(int r, double (&c)[RT], double (&inv)[RT]) {
 #pragma unroll
   for (int i = 0; i < RT; ++i)
     if (i > lane) c[i] = 0.0;  // strict lower part of R
-  // R^-1 column j = lane by back substitution; R[i][p] = lane p's c[i]
+  // R^-1 column j = lane by back substitution; R[i][p] = lane p's c[i].
+  // The reciprocals of the diagonal are formed up front, in parallel (lane i
+  // owns 1 / R_ii), so the substitution chain carries no division.
+  double rd = 0.0;
+#pragma unroll
+  for (int i = 0; i < RT; ++i)
+    if (i == lane) rd = c[i];
+  const double rinv_own = (lane < r && rd > 0.0) ? 1.0 / rd : 0.0;
 #pragma unroll
   for (int i = RT - 1; i >= 0; --i) {
     double s = (i == lane) ? 1.0 : 0.0;
@@ -1472,8 +1479,8 @@ __device__ int warp_chol_reg(int r, double (&c)[RT], double (&inv)[RT]) {
       const double rip = __shfl_sync(kFull, c[i], p);
       if (p <= lane && p < r) s -= rip * inv[p];
     }
-    const double dd = __shfl_sync(kFull, c[i], i);
-    inv[i] = (i <= lane && i < r && dd > 0.0) ? s / dd : 0.0;
+    const double ri = __shfl_sync(kFull, rinv_own, i);
+    inv[i] = (i <= lane && i < r) ? s * ri : 0.0;
   }
   return bad;
 }
@@ -1684,8 +1691,12 @@ __global__ void __launch_bounds__(256) cholqr2_small_kernel(int n, int m,
     for (int p = i; p <= j; ++p) acc = fma(G[i * MT + p], R1[p * MT + j], acc);
     R[e] = j >= i ? acc : 0.0;
   }
-  for (int64_t e = threadIdx.x; e < (int64_t)n * m; e += blockDim.x)
-    Q[(e / m) * ldq + e % m] = A[(e / m) * LQ + e % m];
+  // (compile-time column count: no 64-bit division by the runtime m, which
+  // compiles to a slow-path subroutine call per element)
+  for (int e = threadIdx.x; e < n * MT; e += blockDim.x) {
+    const int row = e / MT, col = e % MT;
+    if (col < m) Q[(int64_t)row * ldq + col] = A[row * LQ + col];
+  }
   for (int k = threadIdx.x; k < m; k += blockDim.x) deficient[k] = 0;
   if (threadIdx.x == 0) {
     flag[0] = bad_s[0];
