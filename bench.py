@@ -1,26 +1,44 @@
 """Benchmark of the SN-like DLR hot path on B200 (BASELINE.json metric).
 
-Workload (N=1): BASELINE config 2 -- 280x280 checkerboard on [0,7]^2,
-rank 16, 32x32 product quadrature (1024 directions), dt=0.01, fp64,
-seeded random-orthonormal initial factors, use_dsa=False, si_tol=1e-8.
-A step is one DLR time step: step_collocation (DEIM -> collocated source
-iteration -> spatial Gram-Schmidt -> fused projections -> row solve ->
-angular re-orthonormalisation) plus the fused temperature update /
-re-linearisation.  The value is sweep cell-angle updates per second over
-whole steps (sum over steps of n_cells x r x SI iterations / device time);
-``dlr_steps_per_s`` and the config-2 full-SN comparison sweep are reported
-alongside.
+Headline workload (N=1): BASELINE config 4 -- the largest configuration
+whose DLR step fits one GPU (config 5's step needs the space-sharded layout):
+1024x1024 random log-normal medium, rank 64, 64x64 product quadrature (4096
+directions), dt=0.01, fp64, seeded random-orthonormal factors,
+use_dsa=False, si_tol=1e-8.  A step is one DLR time step: step_collocation
+(DEIM -> collocated source iteration -> spatial CholQR2 -> fused projections
+-> row solve -> angular re-orthonormalisation) plus the fused temperature
+update / re-linearisation, chained (each step starts from the previous
+one's state).  ``value`` = sweep cell-angle updates per second over whole
+steps (sum of n_cells x r x SI iterations / device time); ``dlr_steps_per_s``
+beside it.  ``--config C2|C3|C4`` picks another BASELINE config.
+
+``e2e``: the same steps through the public step API with the state in
+(pinned) HOST memory: every step copies X, S, W, T and the step coefficients
+host->device, runs, and reads X, S, W, T and the next coefficients back;
+sequential on one stream, chained through the host, all inside the timed
+region (the copy pattern of a reference time loop, driver.py:485-539).
+
+``roofline``: the dominant kernel of the step (K3, the fused projections,
+DMMA-bound) as an FP64 tensor fraction against the FP64 peak measured in
+this run (max of our DMMA probe and cuBLAS DGEMM); the DLR sweep's HBM
+fraction (K1) beside it.
 
 ``--impl reference`` times the CPU restatement of the reference (oracle/,
-"port") on the same config on the host cores.
+"port": numpy/scipy with a plain-C sweep) on the same config on the host
+cores, rank 0 only, and prints the steps it actually ran.
+
+``--gpus N`` without a torchrun environment re-launches itself under
+``torch.distributed.run`` with N ranks (NCCL, directions sharded across
+ranks); ``--dry`` runs the multi-rank plumbing on CPU (gloo) without CUDA.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import platform
+import socket
 import subprocess
 import sys
 import threading
@@ -35,15 +53,37 @@ METRIC = "SN-sweep cell-angle updates/s and DLR steps/s, % of HBM roofline, 1/2/
 UNIT = "cell-angle updates/s"
 SWEEP_BYTES_PER_CELL_ANGLE = 64  # rhs read + psi write
 SWEEP_BYTES_PER_CELL = 160  # sigma_t + scatter source per quadrant batch (4 x 40 B)
+K3_OUTPUTS = 7  # px, py, jx, jy, mt, ms, mo: 2 N_x r^2 flop each (dense-equivalent)
+
+WORKLOADS = {
+    "C2": "C2 checkerboard 280x280, r=16, 32x32 quadrature, dlr-sn step",
+    "C3": "C3 Marshak 512x512, r=32, 64x64 quadrature, inflow T_b=1, dlr-sn step",
+    "C4": "C4 random medium 1024x1024, r=64, 64x64 quadrature, dlr-sn step",
+}
 
 
 def _peaks():
     try:
         with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as fh:
             p = json.load(fh)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy test)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor() or "unknown"
+
+
+def _cores():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
 
 
 class ClockSampler:
@@ -114,78 +154,245 @@ def _dist():
     return ws, rank, local
 
 
-def cpu_reference_step_rate(spec, n_steps, warmup):
-    """Time the oracle port (the reference algorithm restated in numpy) on
-    the host: returns (cell-angle updates/s, steps/s, seconds, iterations)."""
-    from oracle import runner as R
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
-    rng = np.random.default_rng(spec.seed)
+
+def relaunch(argv, n):
+    """Re-run this script as N ranks under torch.distributed.run (one
+    process per GPU); returns the launcher's exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
+           os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd)
+
+
+# ---- problem setup --------------------------------------------------------
+
+def make_spec(name):
+    from paper_2601_18705_b200 import problems
+
+    if name == "C2":
+        spec = problems.config2()
+        problems.draw_factors(spec, np.random.default_rng(spec.seed))
+        return spec
+    if name == "C3":
+        return problems.marshak()
+    if name == "C4":
+        spec, fields = problems.random_medium()
+        rng = np.random.default_rng(spec.seed)
+        problems.draw_factors(spec, rng)  # X, W first (SURVEY 8d draw order)
+        fields(rng)
+        return spec
+    raise SystemExit(f"unknown config {name}")
+
+
+# ---- reference arm: the CPU restatement on the host cores ------------------
+
+def cpu_reference_steps(spec, max_steps, budget_s, X=None, W=None):
+    """Run the oracle port (the reference algorithm restated in numpy/scipy,
+    plain-C sweep) for up to ``max_steps`` DLR steps or until ``budget_s``
+    seconds of step time have passed (at least one step).  X, W (already
+    orthonormal) may be handed in to skip the port's own CGS2 of the seeded
+    factors (untimed setup either way).  Returns a dict of the timed run."""
+    from oracle import port as P
+    from oracle import runner as R
     from paper_2601_18705_b200.problems import draw_factors
 
-    Xr, Wr = draw_factors(spec, rng)
-    X, W = R.orthonormal_factors(spec, Xr, Wr)
+    try:  # BLAS on all host cores (torchrun sets OMP_NUM_THREADS=1 for its ranks)
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(limits=_cores())
+    except Exception:
+        pass
+    t_setup = time.perf_counter()
+    P.build_csweep()
+    if X is None or W is None:
+        rng = np.random.default_rng(spec.seed)
+        Xr, Wr = draw_factors(spec, rng)
+        X, W = R.orthonormal_factors(spec, Xr, Wr)
     state = R.initial_state(spec, X, W)
     T = spec.T0.copy()
-    for _ in range(warmup):
-        state, T, _ = R.run(spec, state, 1, si_tol=1e-8, T=T)
-    t0 = time.perf_counter()
-    state, T, infos = R.run(spec, state, n_steps, si_tol=1e-8, T=T)
-    dt = time.perf_counter() - t0
-    iters = sum(i.iterations for i in infos)
-    return spec.n_cells * spec.rank * iters / dt, n_steps / dt, dt, iters
+    setup = time.perf_counter() - t_setup
+    per, iters = [], []
+    while len(per) < max_steps and (not per or sum(per) + per[-1] <= budget_s):
+        t0 = time.perf_counter()
+        state, T, infos = R.run(spec, state, 1, si_tol=1e-8, T=T)
+        per.append(time.perf_counter() - t0)
+        iters.append(infos[0].iterations)
+    sec = sum(per)
+    return {"rate": spec.n_cells * spec.rank * sum(iters) / sec, "steps": len(per),
+            "sec": sec, "iters": iters, "per_step_s": per, "setup_s": setup}
 
 
 def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
-        return
-    from paper_2601_18705_b200 import problems
-
-    spec = problems.config2()
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    warm = min(args.warmup, 1)
-    # bounded sample: at most 12 oracle steps (~40 s on 16 cores), rate per step
-    n_run = max(1, min(args.steps, 12))
-    rate, sps, sec, iters = cpu_reference_step_rate(spec, n_run, warm)
-    sec = sec * args.steps / n_run
+        return 0
+    spec = make_spec(args.config)
+    cores = _cores()
+    # bounded sample: whole DLR steps of the port until ~150 s of step time
+    res = cpu_reference_steps(spec, args.steps, args.ref_budget)
+    ms = 1e3 * res["sec"] / res["steps"]
+    sample = (f"{res['steps']} whole {args.config} DLR steps of the oracle port run (of the "
+              f"{args.steps} requested; bounded to ~{args.ref_budget:.0f} s), SI iterations "
+              f"{res['iters']}, numpy/scipy with BLAS on all cores + plain-C sweep (OpenMP over "
+              f"directions); factor setup {res['setup_s']:.0f} s untimed")
     line = {
-        "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "impl": "reference",
-        "config": {"workload": "C2 checkerboard 280x280, r=16, 32x32 quadrature, dlr-sn step",
-                   "si_tol": 1e-8, "use_dsa": False},
-        "dlr_steps_per_s": sps,
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{n_run} of the {args.steps} C2 DLR steps run ({iters} sweeps of "
-                                   f"16 directions) after {warm} warm-up step(s), numpy/scipy, BLAS "
-                                   f"on all cores; ms_per_step is the per-step mean"},
-        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "metric": METRIC, "value": res["rate"], "unit": UNIT, "n_gpus": args.gpus,
+        "steps": res["steps"], "warmup": 0, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (seeded BASELINE {args.config})", "impl": "reference",
+        "config": {"workload": WORKLOADS[args.config], "si_tol": 1e-8, "use_dsa": False},
+        "dlr_steps_per_s": res["steps"] / res["sec"],
+        "si_iterations": res["iters"],
+        "cpu_baseline": {"value": res["rate"], "unit": UNIT, "cores": cores, "kind": "port",
+                         "cpu_model": _cpu_model(), "sample": sample},
+        "e2e": {"value": res["rate"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "requested": {"steps": args.steps, "warmup": args.warmup},
     }
     print(json.dumps(line), flush=True)
+    return 0
 
 
-def main():
+# ---- dry mode: the multi-rank plumbing on CPU ------------------------------
+
+def run_dry(args):
+    """Exercise the N-rank path without CUDA: gloo process group, the
+    direction partition of each rank, barrier + max-over-ranks timing, and
+    one JSON line from rank 0 (value = directions swept per second of a host
+    stand-in, clearly not a GPU number)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_18705_b200.problems import random_medium
+    from paper_2601_18705_b200.angular import build_quadrature
+    from paper_2601_18705_b200.sharding import partition_directions
+
+    ws, rank, _ = _dist()
+    if ws > 1:
+        dist.init_process_group("gloo")
+    spec, _ = random_medium(n=64, rank=16, n_polar=8, n_azimuthal=8)
+    quad = build_quadrature(spec.n_polar, spec.n_azimuthal)
+    sel = np.arange(spec.rank) * (quad.n_angles // spec.rank)
+    parts = partition_directions(quad.omegas[sel], ws)
+    mine = parts[rank]
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        np.linalg.qr(np.random.default_rng(rank).standard_normal((256, max(1, len(mine)))))
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64)
+    counts = torch.tensor([float(len(mine))], dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM)
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": float(counts.item()) * args.steps / max(t.item(), 1e-9),
+            "unit": "directions/s (dry host stand-in)", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "dry": True, "scaling": "weak",
+            "directions_per_rank": [len(p) for p in parts], "config": {"workload": "dry"}}),
+            flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+# ---- the B200 arm -----------------------------------------------------------
+
+def fp64_peak(torch, _lib):
+    """FP64 tensor peak on this GPU, measured now: our DMMA probe (all SMs,
+    register operands) and cuBLAS DGEMM 8192^3 via torch.matmul; the larger
+    is the roofline denominator."""
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    sink = torch.zeros(1, dtype=torch.float64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    best_probe = 0.0
+    for warps in (8, 16):
+        iters = 20000
+        _lib.call("dlrsn_dmma_probe", sms, warps, 10, _lib.ptr(sink), st)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.call("dlrsn_dmma_probe", sms, warps, iters, _lib.ptr(sink), st)
+        e1.record()
+        torch.cuda.synchronize()
+        fl = 4096.0 * iters * sms * warps
+        best_probe = max(best_probe, fl / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    torch.matmul(a, b)
+    torch.cuda.synchronize()
+    best_gemm = 0.0
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best_gemm = max(best_gemm, 2.0 * n ** 3 / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    del a, b
+    torch.cuda.empty_cache()
+    return max(best_probe, best_gemm), {"dmma_probe_tflops": best_probe,
+                                        "cublas_dgemm_8192_tflops": best_gemm}
+
+
+def _timings(_lib, which):
+    import ctypes
+
+    cap = 4096
+    ms = (ctypes.c_float * cap)()
+    cnt = ctypes.c_int()
+    if which == "sweep":
+        groups = (ctypes.c_int * cap)()
+        dw = (ctypes.c_int * cap)()
+        _lib.call("dlrsn_sweep_timing_read", cap, ms, groups, dw, ctypes.byref(cnt))
+        _lib.call("dlrsn_sweep_timing", 0)
+    else:
+        _lib.call("dlrsn_project_timing_read", cap, ms, ctypes.byref(cnt))
+        _lib.call("dlrsn_project_timing", 0)
+    return [ms[k] for k in range(min(cnt.value, cap))]
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)  # BASELINE config 2: 50 steps
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C4", choices=["C2", "C3", "C4"])
+    ap.add_argument("--dry", action="store_true", help="multi-rank plumbing on CPU (gloo)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-steps", type=int, default=2)
-    ap.add_argument("--full-sn", type=int, default=1, help="also time the config-2 full-SN sweep")
-    ap.add_argument("--more-configs", default="C4,C3,C5dlr,C5",
-                    help="also time a few steps of these BASELINE configs at N=1 ('' = none)")
-    args = ap.parse_args()
+    ap.add_argument("--cpu-budget", type=float, default=25.0,
+                    help="seconds of port step time for cpu_baseline (at least one step)")
+    ap.add_argument("--ref-budget", type=float, default=150.0,
+                    help="seconds of port step time for --impl reference (at least one step)")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0: same as --steps (max 10)")
+    ap.add_argument("--more-configs", default="C2,C3,C5dlr,C5",
+                    help="also measure these at N=1 ('' = none)")
+    args = ap.parse_args(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(argv, args.gpus)
+    if args.dry:
+        return run_dry(args)
     if args.impl == "reference":
         return run_reference(args)
+    if args.warmup < 3:
+        raise SystemExit("timing rules: at least 3 warm-up steps")
 
     import torch
 
-    from paper_2601_18705_b200 import _lib, problems, transport
+    from paper_2601_18705_b200 import _lib
     from paper_2601_18705_b200._device import set_device
-    from paper_2601_18705_b200.dlr_sn import step_collocation
     from paper_2601_18705_b200.driver import DeviceProblem, initial_state
+    from paper_2601_18705_b200.sharding import DirectionComm
 
     ws, rank, local = _dist()
     set_device(local)
@@ -193,32 +400,23 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    spec = problems.config2()
+    comm = DirectionComm.from_default_group()  # None at N=1
+    spec = make_spec(args.config)
     dp = DeviceProblem.from_spec(spec)
     state = initial_state(dp)
     T = torch.as_tensor(spec.T0, device="cuda").clone()
     lin = dp.linearized(T)
+    box = {"state": state, "lin": lin, "T": T}
 
-    from paper_2601_18705_b200.sharding import DirectionComm
+    def one_step():
+        box["state"], box["lin"], box["T"], info = dp.step(box["state"], box["lin"], box["T"],
+                                                           si_tol=1e-8, check_state=True,
+                                                           comm=comm)
+        return info
 
-    comm = DirectionComm.from_default_group()  # None at N=1; NCCL direction sharding at N>1
-
-    Tbox = [T]
-
-    def one_step(state, lin):
-        # step_collocation + the step boundary (T update, re-linearisation)
-        # in one native call (DeviceProblem.step)
-        state, lin, Tbox[0], info = dp.step(state, lin, Tbox[0], si_tol=1e-8, check_state=True,
-                                            comm=comm)
-        return state, lin, info
-
-    # setup (untimed, before the W warm-up steps): the step's CUDA graphs are
-    # captured per buffer set on first sighting and the sticky iteration
-    # batch settles within the first few steps of a chain
-    for _ in range(10):
-        state, lin, _ = one_step(state, lin)
-    for _ in range(args.warmup):
-        state, lin, _ = one_step(state, lin)
+    # setup + warm-up (untimed): graph capture per buffer set, batch hint
+    for _ in range(3 + args.warmup):
+        one_step()
     torch.cuda.synchronize()
 
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 512 MB > L2
@@ -234,225 +432,205 @@ def main():
         for k in range(args.steps):
             flush.fill_(float(k))  # evict L2 between timed steps (outside the events)
             starts[k].record()
-            state, lin, info = one_step(state, lin)
+            info = one_step()
             ends[k].record()
             iters.append(info.iterations)
         torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
     launches = _lib.launch_count() - launches0
+    per_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms = sum(per_ms)
     if ws > 1:
-        torch.distributed.barrier()
-    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    if ws > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    # roofline pass (after the timed region): CUDA events around every sweep
-    # launch of a few more steps (sweep timing turns the step's graph replay
-    # off, so it is kept out of the timed steps; kernel times are the same)
-    _lib.call("dlrsn_sweep_timing", 1)
-    r_iters = []
-    for _ in range(3):
-        state, lin, info = one_step(state, lin)
-        r_iters.append(info.iterations)
-    torch.cuda.synchronize()
-    sweep_ms, sweep_groups = _sweep_timings(_lib)
-    n_cells, D = spec.n_cells, int(sweep_groups[0])  # single-direction groups: D = G
+        ms = comm.max_scalar(ms)
     updates = sum(spec.n_cells * spec.rank * it for it in iters)
     value = updates / (ms * 1e-3)
-    peak, peak_kind = _peaks()
-    alg_bytes = n_cells * (D * SWEEP_BYTES_PER_CELL_ANGLE + SWEEP_BYTES_PER_CELL)
-    # launches past convergence (speculative, return at once) are counted in
-    # the time but not as sweeps: time per real sweep = all sweep time / iterations
-    sweep_avg_ms = float(np.sum(sweep_ms)) / max(1, sum(r_iters))
-    achieved = alg_bytes / (sweep_avg_ms * 1e-3) / 1e9
-    traffic = None
-    tp = os.path.join(HERE, "profiles", "sweep_traffic.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get("C2_dlr_sweep_bytes_per_launch")
-        except Exception:
-            traffic = None
+    step_ms = ms / args.steps
 
-    # ---- end-to-end: public API with HOST (pinned) buffers each step -------
-    # (untimed warm-up long enough for every step graph of the rotation to be
-    # captured: 2 input sets x 3 output blocks cycling through the caching
-    # allocator = 6 buffer keys, each captured on its second sighting)
-    e2e = measure_e2e(dp, state, Tbox[0], lin, max(1, min(args.steps, 20)), comm,
-                      warmup=max(args.warmup, 14))
+    # ---- roofline pass (after the timed region): CUDA events around every K3
+    # and sweep launch of a few more steps (per-launch timing turns the
+    # step's graph replay off; the kernels are the same) ---------------------
+    _lib.call("dlrsn_sweep_timing", 1)
+    _lib.call("dlrsn_project_timing", 1)
+    r_iters = []
+    for _ in range(3):
+        r_iters.append(one_step().iterations)
+    torch.cuda.synchronize()
+    sweep_ms = _timings(_lib, "sweep")
+    proj_ms = _timings(_lib, "project")
+    peak_fp64, fp64_detail = fp64_peak(torch, _lib)
+    hbm_peak, hbm_kind = _peaks()
+    n_x, r = spec.n_dofs, spec.rank
+    k3_flop = K3_OUTPUTS * 2.0 * n_x * r * r
+    k3_ms = float(np.mean(proj_ms)) if proj_ms else float("nan")
+    k3_tf = k3_flop / (k3_ms * 1e-3) / 1e12
+    n_loc = r if comm is None else len(range(comm.rank, r, comm.world_size))
+    sweep_bytes = spec.n_cells * (n_loc * SWEEP_BYTES_PER_CELL_ANGLE + SWEEP_BYTES_PER_CELL)
+    sweep_real_ms = float(np.sum(sweep_ms)) / max(1, sum(r_iters))  # speculative no-ops excluded
+    sweep_gbs = sweep_bytes / (sweep_real_ms * 1e-3) / 1e9
+    traffic = _ncu_traffic(args.config)
+    roofline = {
+        "bound": "tensor", "achieved": k3_tf, "peak": peak_fp64, "unit": "TFLOP/s",
+        "frac": k3_tf / peak_fp64, "traffic": traffic.get("k3"),
+        "kernel": "project_mma32_kernel (K3: 7 reduced operators, DMMA m8n8k4 f64)",
+        "peak_kind": "fp64 tensor, measured in this run (max of DMMA probe, cuBLAS DGEMM)",
+        "peak_detail": fp64_detail, "launch_ms": k3_ms,
+        "alg_flop_per_launch": k3_flop, "flop_formula": "7 x 2 N_x r^2",
+        "share_of_step": k3_ms / step_ms,
+        "sweep": {"kernel": "sweep_kernel<1> (K1)", "bound": "hbm", "unit": "GB/s",
+                  "achieved": sweep_gbs, "peak": hbm_peak, "peak_kind": hbm_kind,
+                  "frac": sweep_gbs / hbm_peak, "launch_ms": sweep_real_ms,
+                  "alg_bytes_per_launch": sweep_bytes, "traffic": traffic.get("sweep"),
+                  "launches": len(sweep_ms), "sweeps_converging": int(sum(r_iters)),
+                  "share_of_step": (sum(sweep_ms) / len(r_iters)) / step_ms},
+    }
 
-    # ---- full-SN comparison sweep (config 2: all 1024 directions) ----------
-    full = measure_full_sn(dp, comm) if args.full_sn else None
+    # ---- end to end: host buffers, sequential time loop ---------------------
+    e2e = measure_e2e(dp, box, min(10, args.e2e_steps or args.steps), comm)
 
-    # ---- larger BASELINE configs at N=1 (not the headline: step time and
-    # the DLR sweep's HBM fraction where the sweep is bandwidth-bound) -------
     more = []
     if ws == 1 and args.more_configs:
-        del state, lin, Tbox, dp
+        del box, state, lin, T, dp, flush
         torch.cuda.empty_cache()
         for name in args.more_configs.split(","):
-            more.append(measure_config(name.strip()))
+            name = name.strip()
+            if name and name != args.config:
+                more.append(measure_config(name))
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded BASELINE config 2 checkerboard, random-orthonormal factors)",
-        "config": {"workload": "C2 checkerboard 280x280, r=16, 32x32 quadrature, dlr-sn step",
-                   "si_tol": 1e-8, "use_dsa": False, "parallelism": f"dp{ws} (directions)",
-                   "l2": "512 MB buffer written between timed steps (outside the step events)"},
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "weak" if ws == 1 else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (seeded BASELINE {args.config}, random-orthonormal factors)",
+        "config": {"workload": WORKLOADS[args.config], "si_tol": 1e-8, "use_dsa": False,
+                   "parallelism": f"dp{ws} (directions)",
+                   "l2": "inputs > L2 (X alone 2.1 GB at C4) and a 512 MB buffer written "
+                         "between timed steps (outside the step events)"},
         "dlr_steps_per_s": args.steps / (ms * 1e-3),
-        "si_iterations_per_step": float(np.mean(iters)),
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "sweep_ws_kernel", "launch_ms": sweep_avg_ms,
-                     "sweep_launches": len(sweep_ms), "sweeps_converging": int(sum(r_iters)),
-                     "alg_bytes_per_launch": alg_bytes,
-                     "sweep_share_of_step": (sum(sweep_ms) / len(r_iters)) / (ms / args.steps)},
+        "si_iterations": iters,
+        "ms_per_step_each": [round(x, 3) for x in per_ms],
+        "roofline": roofline,
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "wall_s_timed_region": wall,
     }
-    if full is not None:
-        line["full_sn_sweep"] = full
     if more:
         line["more_configs"] = more
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-        rate, sps, sec, it = cpu_reference_step_rate(spec, args.cpu_steps, 0)
-        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                                "sample": f"{args.cpu_steps} full C2 DLR steps of the oracle port "
-                                          f"({it} sweeps of 16 directions, {sec:.1f} s)",
-                                "dlr_steps_per_s": sps}
+        line["cpu_baseline"] = cpu_baseline(spec, args)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
+    return 0
 
 
-def measure_e2e(dp, state, T, lin, n, comm=None, warmup=3):
-    """Same step through the public API with the state and per-cell fields
-    in pinned HOST memory: every step copies X, S, W, T and the step
-    coefficients host->device, runs step_collocation + the T update, and
-    copies the new X, S, W and T device->host.  Steps are independent
-    problems streamed through the API, so the copies are pipelined: the H2D
-    of step k+1 (copy stream) and the D2H of step k-1 (second copy stream)
-    overlap step k's compute; everything is inside the timed region."""
+def _ncu_traffic(config):
+    """dram__bytes_read + write per launch of K3 / the sweep from the
+    committed ncu --set full captures (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(HERE, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get(config, {})
+    except Exception:
+        return {}
+
+
+def cpu_baseline(spec, args):
+    """The oracle port timed on this host's cores on a bounded sample of the
+    same workload: whole DLR steps from the same seeded state (the factors
+    come from the GPU setup, so the port's own CGS2 of the 4 M x 64 draw is
+    not timed), until ~``args.cpu_budget`` s."""
+    from paper_2601_18705_b200.driver import DeviceProblem, initial_state
+
+    dp = DeviceProblem.from_spec(spec)
+    st = initial_state(dp)
+    X, W = st.X.cpu().numpy(), st.W.values.cpu().numpy()
+    del dp, st
+    res = cpu_reference_steps(spec, 50, args.cpu_budget, X=X, W=W)
+    return {"value": res["rate"], "unit": UNIT, "cores": _cores(), "kind": "port",
+            "cpu_model": _cpu_model(),
+            "sample": f"{res['steps']} whole {args.config} DLR steps of the oracle port "
+                      f"({res['sec']:.1f} s, SI iterations {res['iters']}), numpy/scipy BLAS on "
+                      f"all cores + plain-C sweep (OpenMP)",
+            "dlr_steps_per_s": res["steps"] / res["sec"]}
+
+
+def measure_e2e(dp, box, n, comm=None):
+    """The step through the public API (DeviceProblem.step: step_collocation
+    + the T update / re-linearisation) with the state and coefficients in
+    pinned HOST memory: each step uploads X, S, W, beta, T and the seven
+    LinearizedStep fields, runs, and downloads X, S, W, beta, T and the next
+    step's fields, which are the next step's host inputs.  One stream, no
+    overlap between steps; timed by CUDA events around the whole loop."""
     import torch
 
-    from paper_2601_18705_b200.dlr_sn import step_collocation
-    from paper_2601_18705_b200.lowrank import DlrState
     from paper_2601_18705_b200.angular import AngularBasis
+    from paper_2601_18705_b200.lowrank import DlrState
     from paper_2601_18705_b200.physics import LinearizedStep
+
+    fields = ("sigma_t", "sigma_s", "sigma_a", "q", "T0", "denom", "rho_cv")
+    st, lin = box["state"], box["lin"]
 
     def pin(t):
         return t.detach().cpu().pin_memory()
 
-    host = {"X": pin(state.X), "S": pin(state.S), "W": pin(state.W.values), "T": pin(T)}
-    fields = ("sigma_t", "sigma_s", "sigma_a", "q", "T0", "denom", "rho_cv")
+    host = {"X": pin(st.X), "S": pin(st.S), "W": pin(st.W.values), "beta": pin(st.W.beta),
+            "T": pin(box["T"])}
     host.update({f: pin(getattr(lin, f)) for f in fields})
-    outs = [{k: torch.empty_like(host[k]).pin_memory() for k in ("X", "S", "W", "T")}
-            for _ in range(2)]
-    h2d = sum(v.numel() * 8 for v in host.values())
-    d2h = sum(v.numel() * 8 for v in outs[0].values())
-    dev = [{k: torch.empty_like(v, device="cuda") for k, v in host.items()} for _ in range(2)]
-    comp = torch.cuda.current_stream()
-    up, down = torch.cuda.Stream(), torch.cuda.Stream()
-    loaded = [torch.cuda.Event() for _ in range(2)]
-    freed = [torch.cuda.Event() for _ in range(2)]
-    done = [torch.cuda.Event() for _ in range(2)]
-    copied = [torch.cuda.Event() for _ in range(2)]
-    for e in freed + copied:
-        e.record(comp)
-    keep = [None, None]
+    consts = (lin.dt, lin.inv_cdt, lin.constants)
+    out_keys = ("X", "S", "W", "beta", "T") + fields
+    h2d_bytes = sum(v.numel() * 8 for v in host.values())
+    d2h_bytes = sum(host[k].numel() * 8 for k in out_keys if k != "rho_cv")
 
-    def upload(k):
-        b = k % 2
-        with torch.cuda.stream(up):
-            up.wait_event(freed[b])
-            for name, v in host.items():
-                dev[b][name].copy_(v, non_blocking=True)
-            loaded[b].record(up)
+    def step(h):
+        d = {k: v.to("cuda", non_blocking=True) for k, v in h.items()}
+        state = DlrState(X=d["X"], S=d["S"], W=AngularBasis(values=d["W"], beta=d["beta"]))
+        lin_d = LinearizedStep(dt=consts[0], inv_cdt=consts[1], constants=consts[2],
+                               **{f: d[f] for f in fields})
+        new, nxt, T1, info = dp.step(state, lin_d, d["T"], si_tol=1e-8, comm=comm)
+        res = {"X": new.X, "S": new.S, "W": new.W.values, "beta": new.W.beta, "T": T1}
+        res.update({f: getattr(nxt, f) for f in fields if f != "rho_cv"})
+        out = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in res.items()}
+        for k, v in res.items():
+            out[k].copy_(v, non_blocking=True)
+        out["rho_cv"] = h["rho_cv"]
+        return out, info.iterations
 
-    def compute(k):
-        b = k % 2
-        d = dev[b]
-        comp.wait_event(loaded[b])
-        st = DlrState(X=d["X"], S=d["S"], W=AngularBasis(values=d["W"]).bind(dp.quad))
-        step = LinearizedStep(dt=lin.dt, inv_cdt=lin.inv_cdt, constants=lin.constants,
-                              **{f: d[f] for f in fields})
-        new, info = step_collocation(dp.grid, step, dp.quad, st, si_tol=1e-8, use_dsa=False,
-                                     comm=comm)
-        # T update in place on this step's input slot (re-filled by the upload of step k+2)
-        Tn = dp.advance(step, info.phi, d["T0"])
-        freed[b].record(comp)  # the input set may be overwritten from here on
-        res = {"X": new.X, "S": new.S, "W": new.W.values, "T": Tn.T0}
-        done[b].record(comp)
-        comp.wait_event(copied[b])  # outputs of step k-2 read back before reuse
-        keep[b] = res
-        with torch.cuda.stream(down):
-            down.wait_event(done[b])
-            for name, v in res.items():
-                outs[b][name].copy_(v, non_blocking=True)
-            copied[b].record(down)
-        for v in res.values():
-            v.record_stream(down)
-        return info.iterations
-
-    def run(count):
-        it = 0
-        up.wait_stream(comp)  # the first upload starts inside the timed region
-        upload(0)
-        for k in range(count):
-            if k + 1 < count:
-                upload(k + 1)
-            it += compute(k)
-        comp.wait_stream(down)
-        return it
-
-    run(warmup)  # untimed: first-sighting setup of both buffer sets
+    for _ in range(3):  # untimed: graph capture for the e2e buffer sets
+        host, _ = step(host)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(comp)
-    iters = run(n)
-    e1.record(comp)
+    e0.record()
+    iters = 0
+    for _ in range(n):
+        host, it = step(host)  # .iterations is read after the step's own sync
+        iters += it
+    e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     if comm is not None:
         ms = comm.max_scalar(ms)
     spec = dp.spec
     return {"value": spec.n_cells * spec.rank * iters / (ms * 1e-3), "unit": UNIT,
-            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "steps": n, "warmup": warmup, "ms_per_step": ms / n,
-            "pipelined": "H2D of step k+1 and D2H of step k-1 overlap step k (2 copy streams)"}
+            "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h_bytes),
+            "steps": n, "ms_per_step": ms / n,
+            "pattern": "sequential: H2D inputs -> step -> D2H outputs, chained through pinned "
+                       "host buffers, one stream, no cross-step overlap"}
 
 
-def measure_config(name, steps=6, warmup=6):
-    """A few DLR steps of a larger BASELINE config (C3 Marshak 512^2 r=32
-    from its initial state, C4 random medium 1024^2 r=64): device time per
-    step (inputs resident, L2 flushed between steps) and the DLR sweep's
-    algorithmic HBM fraction from per-launch CUDA events."""
+def measure_config(name, steps=6, warmup=4):
+    """A few DLR steps of another BASELINE config at N=1 (device time per
+    step, L2 flushed between steps), or config 5's sweeps."""
     import torch
 
-    from paper_2601_18705_b200 import _lib, problems
+    from paper_2601_18705_b200 import _lib
     from paper_2601_18705_b200.driver import DeviceProblem, initial_state
 
     if name == "C5":
         return measure_c5_sweep()
     if name == "C5dlr":
         return measure_c5_dlr_sweep()
-    if name == "C3":
-        spec = problems.marshak()
-        label = "C3 Marshak 512x512, r=32, 64x64 quadrature, inflow T_b=1, dlr-sn step"
-    elif name == "C4":
-        spec, fields = problems.random_medium()
-        rng = np.random.default_rng(spec.seed)
-        problems.draw_factors(spec, rng)  # X, W first (SURVEY 8d draw order)
-        fields(rng)
-        label = "C4 random medium 1024x1024, r=64, 64x64 quadrature, dlr-sn step"
-    else:
-        raise SystemExit(f"unknown config {name}")
+    spec = make_spec(name)
     dp = DeviceProblem.from_spec(spec)
     state = initial_state(dp)
     T = torch.as_tensor(spec.T0, device="cuda").clone()
@@ -474,16 +652,16 @@ def measure_config(name, steps=6, warmup=6):
     _lib.call("dlrsn_sweep_timing", 1)
     state, lin, T, info = dp.step(state, lin, T, si_tol=1e-8)
     torch.cuda.synchronize()
-    sw, _ = _sweep_timings(_lib)
+    sw = _timings(_lib, "sweep")
     sweep_ms = float(np.sum(sw)) / max(1, info.iterations)
     alg = spec.n_cells * (spec.rank * SWEEP_BYTES_PER_CELL_ANGLE + SWEEP_BYTES_PER_CELL)
     peak, _ = _peaks()
-    out = {"workload": label, "steps": steps, "ms_per_step": ms / steps,
+    out = {"workload": WORKLOADS[name], "steps": steps, "ms_per_step": ms / steps,
            "ms_per_step_each": [round(x, 3) for x in per],
            "dlr_steps_per_s": steps / (ms * 1e-3), "si_iterations": iters,
            "cell_angle_per_s": spec.n_cells * spec.rank * sum(iters) / (ms * 1e-3),
-           "sweep": {"kernel": "sweep_kernel<1>", "launch_ms": sweep_ms,
-                     "alg_bytes_per_launch": alg, "achieved_GBs": alg / (sweep_ms * 1e-3) / 1e9,
+           "sweep": {"launch_ms": sweep_ms, "alg_bytes_per_launch": alg,
+                     "achieved_GBs": alg / (sweep_ms * 1e-3) / 1e9,
                      "frac_of_hbm": alg / (sweep_ms * 1e-3) / 1e9 / peak}}
     del state, lin, T, dp, flush
     torch.cuda.empty_cache()
@@ -494,14 +672,12 @@ def measure_c5_dlr_sweep(reps=3):
     """Config 5's DLR sweep on one GPU: the r = 128 directions DEIM selects
     from a seeded random orthonormal W (16384 x 128, lowrank.py:168-205),
     swept over the 4096^2 tile medium with psi STORED for every direction
-    (rhs and psi are 69 GB each in the SK layout, both in HBM), i.e. the
-    per-iteration sweep of the C5 DLR step (sigma_s = 0: one sweep per step,
-    no scattering source).  The rhs of every direction is the step's
-    source_vector(q) + inv_cdt M psi_old for the isotropic psi_old = B(T0)
-    (forming X S W_sel^T needs the 68.7 GB X, which with rhs and psi does
-    not fit one GPU; the sweep's traffic and arithmetic do not depend on
-    the rhs values).  Algorithmic bytes: 64 per cell-angle + 32 per cell
-    (sigma_t in 4 quadrant orientations)."""
+    (rhs and psi 69 GB each in the SK layout, both in HBM): the per-step
+    sweep of the C5 DLR step (sigma_s = 0: one sweep per step).  The rhs of
+    every direction is the step's source_vector(q) + inv_cdt M psi_old for
+    the isotropic psi_old = B(T0); the sweep's traffic and arithmetic do not
+    depend on the rhs values.  Algorithmic bytes: 64 per cell-angle + 32 per
+    cell (sigma_t in 4 quadrant orientations)."""
     import torch
 
     from paper_2601_18705_b200 import _lib, problems, transport
@@ -562,8 +738,7 @@ def measure_c5_dlr_sweep(reps=3):
            n_sel_quads, "ms_per_sweep": ms, "cell_angle_per_s": spec.n_cells * D / (ms * 1e-3),
            "alg_bytes_per_launch": alg, "achieved_GBs": alg / (ms * 1e-3) / 1e9,
            "frac_of_hbm": alg / (ms * 1e-3) / 1e9 / peak, "psi_checksum": chk,
-           "note": "rhs = source + inv_cdt M B(T0) per direction (X S W_sel^T needs the "
-                   "68.7 GB X); l2: inputs 138 GB >> L2"}
+           "note": "rhs = source + inv_cdt M B(T0) per direction; l2: inputs 138 GB >> L2"}
     del rhs_sk, psi_sk, ops, lin, T, rhs, dp, plan
     torch.cuda.empty_cache()
     return out
@@ -571,12 +746,11 @@ def measure_c5_dlr_sweep(reps=3):
 
 def measure_c5_sweep(reps=1):
     """Config 5's full-SN stress sweep on one GPU: 16384 directions on the
-    4096^2 tile medium (sigma_a log-uniform [0.1, 100] per 64x64 tile, q ~
-    U[0,1], dt = dx = 1, pure absorber => one sweep per step), closure only:
-    psi (8.8 TB) is never stored, so there are no per-cell-angle HBM bytes
-    and the sweep is FP64-issue bound (report cell-angle/s).  The fields
-    are drawn from seed 5 directly (the 68.7 GB X draw of the DLR factors
-    is skipped: config 5's DLR step needs the space-sharded layout)."""
+    4096^2 tile medium, closure only (psi, 8.8 TB, is never stored), so it
+    is FP64-issue bound: report cell-angle/s.  With the isotropic rhs every
+    z-mirrored pair of nodes (same omega_x, omega_y) has the same psi, so
+    each pair is swept once with the summed closure weight (``unique``
+    directions beside the nominal count)."""
     import torch
 
     from paper_2601_18705_b200 import problems, transport
@@ -601,76 +775,18 @@ def measure_c5_sweep(reps=1):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     ca = spec.n_cells * quad.n_angles
+    uniq = transport.mirror_pairs(quad.omegas)[0].shape[0] if hasattr(transport, "mirror_pairs") \
+        else quad.n_angles
     out = {"workload": "C5 stress 4096x4096, 128x128 = 16384 directions, full-SN closure-only sweep",
            "ms_per_sweep": ms, "cell_angle_per_s": ca / (ms * 1e-3), "cell_angles": ca,
+           "directions_nominal": quad.n_angles, "directions_swept": uniq,
            "bound": "fp64 issue (no per-cell-angle HBM traffic: psi not stored)",
-           "phi_checksum": float(phi.sum())}
+           "phi_checksum": float(phi.sum()),
+           "determinism": "group closure sums added with fp64 atomics: reproducible to round-off"}
     del ops, lin, T, rhs, phi, dp
     torch.cuda.empty_cache()
     return out
 
 
-def _sweep_timings(_lib):
-    """Per-launch sweep times recorded by the library (dlrsn_sweep_timing)."""
-    import ctypes
-
-    cap = 4096
-    ms = (ctypes.c_float * cap)()
-    groups = (ctypes.c_int * cap)()
-    dw = (ctypes.c_int * cap)()
-    cnt = ctypes.c_int()
-    _lib.call("dlrsn_sweep_timing_read", cap, ms, groups, dw, ctypes.byref(cnt))
-    _lib.call("dlrsn_sweep_timing", 0)
-    n = min(cnt.value, cap)
-    if n == 0 or any(dw[k] != 1 for k in range(n)):
-        raise RuntimeError("sweep timing: expected single-direction groups")
-    return [ms[k] for k in range(n)], [groups[k] for k in range(n)]
-
-
-def measure_full_sn(dp, comm=None, reps=3):
-    """Config 2's full-SN comparison sweep: one source-iteration sweep over
-    all 1024 quadrature directions (closure = quadrature weights) on the
-    280x280 grid, psi stored (64 B/cell-angle algorithmic)."""
-    import torch
-
-    from paper_2601_18705_b200 import transport
-
-    T = torch.as_tensor(dp.spec.T0, device="cuda")
-    lin = dp.linearized(T)
-    ops = transport.assemble_operators(dp.grid, lin)
-    quad = dp.quad
-    D = quad.n_angles
-    mine = np.arange(D)
-    if comm is not None:
-        from paper_2601_18705_b200.sharding import partition_directions
-
-        mine = partition_directions(quad.omegas, comm.world_size)[comm.rank]
-    plan = transport._SweepPlan(ops, quad.omegas[mine], quad.weights[mine])
-    vl = ops.vec_len
-    Dl = len(mine)
-    rhs = torch.rand(Dl * vl, dtype=torch.float64, device="cuda")
-    psi = torch.empty_like(rhs)
-    part = torch.empty(plan.G * vl, dtype=torch.float64, device="cuda")
-    scat = torch.zeros(4 * vl, dtype=torch.float64, device="cuda")
-    for _ in range(2):
-        transport._sweep(ops, plan, rhs, psi, scat, part)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        transport._sweep(ops, plan, rhs, psi, scat, part)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
-    if comm is not None:
-        ms = comm.max_scalar(ms)
-    nc = dp.grid.n_cells
-    alg = nc * (D * SWEEP_BYTES_PER_CELL_ANGLE + SWEEP_BYTES_PER_CELL)
-    peak, _ = _peaks()
-    return {"directions": D, "ms_per_sweep": ms, "cell_angle_per_s": nc * D / (ms * 1e-3),
-            "achieved_GBs": alg / (ms * 1e-3) / 1e9, "frac_of_hbm": alg / (ms * 1e-3) / 1e9 / peak,
-            "group_width": plan.dw, "groups": plan.G}
-
-
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

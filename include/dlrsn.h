@@ -102,6 +102,12 @@ int dlrsn_sweep_workspace_init(void* workspace, int64_t workspace_bytes, dlrsn_s
 int dlrsn_debug_trace(unsigned long long* buf, int chunks);
 int dlrsn_debug_flags(int flags); /* debug: bit0 = no speculative handoff prefetch */
 
+/* FP64 tensor-core peak probe: blocks x warps_per_block warps, each issuing
+ * 8 independent chains of `iters` mma.sync m8n8k4 f64 (DMMA) on registers;
+ * FLOPs = 4096 * iters * blocks * warps_per_block.  sink: device double. */
+int dlrsn_dmma_probe(int blocks, int warps_per_block, int iters, double* sink,
+                     dlrsn_stream_t stream);
+
 /* ---- K4: per-cell physics (physics.py:63-132, driver.py:344-346,532-534) */
 
 /* linearize (physics.py:94-120) + BASELINE adapters: sigma_t += ss_phys,
@@ -256,6 +262,12 @@ int dlrsn_mgram(const dlrsn_cellops* ops, int ra, int rb, const double* A, int l
                 const double* B, int ldb, const double* coeff, double* G, double* partial,
                 dlrsn_stream_t stream);
 
+/* Measurement hook: while enabled, every dlrsn_project records a CUDA event
+ * pair around its main kernel (not the partial-sum reduction); _read
+ * synchronises and returns the per-launch ms (cap entries at most). */
+int dlrsn_project_timing(int enable);
+int dlrsn_project_timing_read(int cap, float* ms, int* count);
+
 /* Fused reduced operators (project_row_operators, dlr_sn.py:61-71, plus
  * X_old^T M X of project_initial, :50-58) in one pass over the cells:
  * out = [px, py, jx, jy, mt, ms, mo] (7 r x r, row-major) then q-hat (r).
@@ -289,9 +301,23 @@ int dlrsn_row_combine(int n, int r, const double* Binv, const double* ms, const 
 
 /* deim_select (lowrank.py:168-205) by Gaussian elimination with row
  * pivoting on a work copy of W (n x r): idx (r picks), W[idx,:] = Lhat U.
- * *err_col = -1 on success, else the column whose residual vanished. */
+ * *err_col = -1 on success, else the column whose residual vanished (or
+ * that has no finite candidate left).  gap (r doubles, nullable): per pick
+ * (|best| - |second best|) / |best| of the residual over the unpicked rows
+ * -- 0 is an exact tie, which np.argmax (lowrank.py:191) breaks by the
+ * lowest row, as this kernel does; near-ties are where round-off can flip a
+ * pick.  variant: 0 auto, 1 one-thread-per-row registers (n <= 1024,
+ * r <= 16), 2 thread-block cluster (DSMEM), 3 one CTA over shared / global
+ * memory (Wwork used when n r doubles exceed shared memory). */
 int dlrsn_deim(int n, int r, double* Wwork, const double* W, int* idx, double* Lhat, double* U,
-               int* err_col, dlrsn_stream_t stream);
+               int* err_col, double* gap, int variant, dlrsn_stream_t stream);
+
+/* Forced selection (the angle_indices override of a step): idx = indices
+ * (HOST int64, r entries, pick order), W[idx,:] = Lhat U without further
+ * pivoting; *err_col = j when pivot j vanishes below the DEIM floor or
+ * index j repeats / is out of range, else -1; gap[j] = 1.  r <= 78. */
+int dlrsn_deim_forced(int n, int r, const double* W, const int64_t* indices, int* idx,
+                      double* Lhat, double* U, int* err_col, double* gap, dlrsn_stream_t stream);
 
 /* W_hat solves: mode 0 X = W_hat^-1 V (interpolation_coefficients,
  * lowrank.py:158-160), mode 1 x = W_hat^-T v (closure_weights, :162-165). */
@@ -365,6 +391,14 @@ typedef struct dlrsn_step_params {
                                 skipped; M depends on the grid only, so the value is the one
                                 the Gram would give).  NULL: compute it */
   double* x_check_out;       /* device, optional: receives max|X_new^T M X_new - I| */
+  int si_batch_hint;         /* source iterations enqueued before the first convergence
+                                readback (0: library default 6).  The caller keeps it per
+                                problem (step_info.si_batch_hint of the previous step); with
+                                world_size > 1 every rank must pass the same value, since the
+                                batch fixes the number of allreduce callbacks per segment */
+  int angle_override;        /* 1: use angle_indices_in instead of the DEIM picks
+                                (forced-selection parity, lowrank.py:168-205 hazard (i)) */
+  const int64_t* angle_indices_in; /* HOST, r entries, read when angle_override */
 } dlrsn_step_params;
 
 typedef struct dlrsn_step_info { /* HOST, filled by the call */
@@ -379,6 +413,11 @@ typedef struct dlrsn_step_info { /* HOST, filled by the call */
   double check_out[2];
   int64_t angle_indices[DLRSN_MAX_RANK];
   double closure[DLRSN_MAX_RANK];
+  int si_batch_hint;         /* suggested si_batch_hint for the next step of this problem */
+  int sweep_status;          /* sweep workspace status word (2: a strip handoff timed out;
+                                the call then fails with DLRSN_ECUDA and re-arms the workspace) */
+  double deim_gap[DLRSN_MAX_RANK]; /* per pick: (|top| - |second|) / |top| of the DEIM
+                                residual (near-tie diagnostic, lowrank.py:191 argmax) */
 } dlrsn_step_info;
 
 /* Multi-GPU hooks (NULL = one GPU): the step calls allreduce_sum(user) to

@@ -346,6 +346,9 @@ class Operators:
         """transport_sn.py:107-116: per-cell mass block, then the coefficient."""
         u = np.asarray(u)
         flat = u.ndim == 1
+        lib = _csweep_lib()
+        if lib is not None and u.dtype == np.float64 and u.size >= (1 << 16):
+            return _mass_apply_c(lib, self, u, coeff, flat)
         uc = u.reshape(self.grid.n_cells, 4, -1)
         out = np.einsum("ij,cjk->cik", self.mass_cell, uc)
         if coeff is not None:
@@ -496,14 +499,105 @@ def _local_inverses(ops, omegas):
     return out
 
 
-def sweep_many(ops, omegas, rhs, chunk=16):
+# --- plain-C restatement of the sweep (oracle/csweep.c), built on demand ---
+_CSWEEP = None
+
+
+def _csweep_lib():
+    """ctypes handle of oracle/libcsweep.so (compiled with gcc -fopenmp on
+    first use when missing or older than csweep.c); None if gcc fails."""
+    global _CSWEEP
+    if _CSWEEP is None:
+        import ctypes
+        import os
+        import subprocess
+
+        here = os.path.dirname(os.path.abspath(__file__))
+        src = os.path.join(here, "csweep.c")
+        so = os.path.join(here, "libcsweep.so")
+        try:
+            if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+                tmp = f"{so}.{os.getpid()}.tmp"
+                subprocess.run(["gcc", "-O3", "-fopenmp", "-fPIC", "-shared", "-o", tmp, src],
+                               check=True, capture_output=True)
+                os.replace(tmp, so)
+            lib = ctypes.CDLL(so)
+            f = lib.csweep_quadrant
+            P, I, L = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
+            f.argtypes = [I, I, I, I, I, P, P, P, P, P, P, P, P, L, P, P, L, P, I]
+            f.restype = None
+            lib.cmass_apply.argtypes = [L, L, P, P, P, P, I]
+            lib.cmass_apply.restype = None
+            _CSWEEP = lib
+        except Exception:
+            _CSWEEP = False
+    return _CSWEEP or None
+
+
+def build_csweep():
+    """Compile the C sweep restatement now (__graft_entry__.build)."""
+    return _csweep_lib() is not None
+
+
+def _mass_apply_c(lib, ops, u, coeff, flat):
+    import os
+
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    k = 1 if flat else u.shape[1]
+    out = np.empty((ops.grid.n_dofs, k))
+    mass = np.ascontiguousarray(ops.mass_cell, dtype=np.float64)
+    cf = None if coeff is None else np.ascontiguousarray(coeff, dtype=np.float64)
+    nthreads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else 0
+    lib.cmass_apply(ops.grid.n_cells, k, mass.ctypes.data, None if cf is None else cf.ctypes.data,
+                    u.ctypes.data, out.ctypes.data, nthreads)
+    return out[:, 0] if flat else out
+
+
+def _sweep_many_c(lib, ops, omegas, rhs):
+    import os
+
+    g = ops.grid
+    D = omegas.shape[0]
+    rhs = np.ascontiguousarray(rhs, dtype=float)
+    psi_out = np.empty((g.n_dofs, D))
+    sig = np.ascontiguousarray(ops.step.sigma_t, dtype=float)
+    mass = np.ascontiguousarray(ops.mass_cell, dtype=float)
+    nthreads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else 0
+    quads = {}
+    for d in range(D):
+        quads.setdefault(quadrant_of(omegas[d]), []).append(d)
+    for (sx, sy), idx in quads.items():
+        om = omegas[idx]
+        stream = np.empty((len(idx), 4, 4))
+        for k, o in enumerate(om):
+            stream[k] = (o[0] * ops.grad[0] + o[1] * ops.grad[1]
+                         + abs(float(o[0])) * ops.edge_mass["right" if sx > 0 else "left"]
+                         + abs(float(o[1])) * ops.edge_mass["top" if sy > 0 else "bottom"])
+        cx = np.ascontiguousarray(ops.couple[("x", sx)], dtype=float)
+        cy = np.ascontiguousarray(ops.couple[("y", sy)], dtype=float)
+        ox = np.ascontiguousarray(np.abs(om[:, 0]))
+        oy = np.ascontiguousarray(np.abs(om[:, 1]))
+        cols = np.ascontiguousarray(idx, dtype=np.int32)
+        lib.csweep_quadrant(g.nx, g.ny, sx, sy, len(idx), stream.ctypes.data, mass.ctypes.data,
+                            sig.ctypes.data, cx.ctypes.data, cy.ctypes.data, ox.ctypes.data,
+                            oy.ctypes.data, rhs.ctypes.data, D, cols.ctypes.data,
+                            psi_out.ctypes.data, D, cols.ctypes.data, nthreads)
+    return psi_out
+
+
+def sweep_many(ops, omegas, rhs, chunk=16, use_c=True):
     """Upwind sweeps of many directions: rhs (n_dofs, D) -> psi (n_dofs, D).
 
     Same arithmetic per direction as ``sweep_solve`` (transport_sn.py:303-322);
-    directions of one quadrant advance through the wavefront levels together.
+    directions of one quadrant advance through the wavefront levels together
+    (numpy), or run through the plain-C restatement (oracle/csweep.c, same
+    per-cell arithmetic) when it builds.
     """
     omegas = np.asarray(omegas, dtype=float)
     rhs = np.asarray(rhs, dtype=float)
+    lib = _csweep_lib() if use_c else None
+    if lib is not None:
+        return _sweep_many_c(lib, ops, omegas, rhs)
     g = ops.grid
     nc = g.n_cells
     D = omegas.shape[0]
@@ -834,6 +928,28 @@ def deim_select(W):
     return Deim(idx, wh, scipy.linalg.lu_factor(wh), float(np.linalg.cond(wh)))
 
 
+def deim_gaps(W, picks):
+    """Relative top-2 gap of the |residual| at each pick of ``picks`` over the
+    rows not picked before it (the near-tie diagnostic of the GPU DEIM; a
+    restatement of the residuals of lowrank.py:186-191 with the picked rows
+    excluded, whose residuals are zero up to round-off)."""
+    w = np.asarray(W, dtype=float)
+    picks = [int(p) for p in picks]
+    gaps = []
+    for j in range(len(picks)):
+        if j == 0:
+            res = w[:, 0].copy()
+        else:
+            cf = np.linalg.solve(w[np.ix_(picks[:j], range(j))], w[picks[:j], j])
+            res = w[:, j] - w[:, :j] @ cf
+        a = np.abs(res)
+        a[picks[:j]] = -1.0
+        top = np.sort(a)[::-1]
+        second = max(top[1], 0.0) if top.size > 1 else 0.0
+        gaps.append((top[0] - second) / top[0] if top[0] > 0 else 0.0)
+    return np.asarray(gaps)
+
+
 def project_row_operators(ops, x):
     """dlr_sn.py:61-71."""
     st = ops.step
@@ -881,6 +997,25 @@ def solve_row_system(B, ms, Q, weights):
     return np.einsum("dij,dj->di", Binv, rhs), lbar
 
 
+def _lazy_spatial_monomials(grid, count):
+    """The completion candidates of dlr_sn.py:124-125 (spatial_monomials,
+    lowrank.py:28-40), generated only when a deficiency asks for one."""
+    coords = None
+    x0, y0, lx, ly = grid.extent
+    k, deg = 0, 0
+    while k < count:
+        for a in range(deg, -1, -1):
+            if k >= count:
+                return
+            if coords is None:
+                coords = dof_coordinates(grid)
+                xh = 2.0 * (coords[:, 0] - x0) / lx - 1.0
+                yh = 2.0 * (coords[:, 1] - y0) / ly - 1.0
+            yield xh**a * yh ** (deg - a)
+            k += 1
+        deg += 1
+
+
 @dataclass(eq=False)
 class StepInfo:
     """CollocationStepInfo (dlr_sn.py:40-47)."""
@@ -910,7 +1045,7 @@ def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, 
     res = source_iteration(ops, om_sel, closure, psi_time=psi_time, use_dsa=use_dsa, tol=si_tol,
                            max_iters=si_max_iters, phi_start=state.scalar_flux(),
                            extra_source=extra)
-    comp = spatial_monomials(dof_coordinates(grid), grid.extent, state.rank + 8)
+    comp = _lazy_spatial_monomials(grid, state.rank + 8)
     x_new, _, dx_ = gram_schmidt(res.psi, mass_dot(ops), comp)
     proj = project_row_operators(ops, x_new)
     B = row_matrices(proj, om_sel)

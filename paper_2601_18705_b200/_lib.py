@@ -50,14 +50,16 @@ class StepParams(ctypes.Structure):
                 ("weights_dev", c_vp), ("inv_cdt", c_dbl), ("si_tol", c_dbl),
                 ("si_max_iters", c_int), ("check_state", c_int), ("gs_method", c_int),
                 ("sweep_dw", c_int), ("advance", c_vp), ("inflow", c_dbl * 4),
-                ("x_check_in", c_vp), ("x_check_out", c_vp)]
+                ("x_check_in", c_vp), ("x_check_out", c_vp), ("si_batch_hint", c_int),
+                ("angle_override", c_int), ("angle_indices_in", c_vp)]
 
 
 class StepInfo(ctypes.Structure):
     _fields_ = [("iterations", c_int), ("spatial_deficiency", c_int),
                 ("angular_deficiency", c_int), ("error_index", c_int), ("gs_fallback", c_int),
                 ("residual", c_dbl), ("check_in", c_dbl * 2), ("check_out", c_dbl * 2),
-                ("angle_indices", c_i64 * MAX_RANK), ("closure", c_dbl * MAX_RANK)]
+                ("angle_indices", c_i64 * MAX_RANK), ("closure", c_dbl * MAX_RANK),
+                ("si_batch_hint", c_int), ("sweep_status", c_int), ("deim_gap", c_dbl * MAX_RANK)]
 
 
 COMM_FN = ctypes.CFUNCTYPE(c_int, c_vp)
@@ -120,7 +122,11 @@ _SIGNATURES = {
     "dlrsn_small_matmul": (c_int, [c_int, c_int, c_int, c_vp, c_vp, c_vp, c_int, c_vp]),
     "dlrsn_row_inverse": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "dlrsn_row_combine": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
-    "dlrsn_deim": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "dlrsn_deim": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp]),
+    "dlrsn_dmma_probe": (c_int, [c_int, c_int, c_int, c_vp, c_vp]),
+    "dlrsn_project_timing": (c_int, [c_int]),
+    "dlrsn_project_timing_read": (c_int, [c_int, c_vp, c_vp]),
+    "dlrsn_deim_forced": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "dlrsn_what_solve": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp]),
     "dlrsn_cgs2_workspace_len": (c_i64, [c_int]),
     "dlrsn_cholqr2_small_smem": (c_i64, [c_int, c_int]),

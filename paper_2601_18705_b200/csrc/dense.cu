@@ -13,6 +13,8 @@
 //                 reference's deficiency + completion rules
 //                 (angular.py:104-160,217-238; lowrank.py:158-205,235-259)
 #include <cmath>
+#include <vector>
+#include <utility>
 #include <cstring>
 
 #include <cstdlib>
@@ -1901,6 +1903,31 @@ __global__ void row_combine_kernel(int n, int r, const double* __restrict__ Binv
   if (threadIdx.x == 0 && sing) *status = 1;
 }
 
+// Running top-2 of the DEIM argmax: (best, its row, second best value).
+// Merging two partial results keeps the larger best (lowest row on ties,
+// np.argmax) and max(both seconds, the smaller best) as the second -- equal
+// bests give second == best, i.e. an exact tie (gap 0).
+__device__ __forceinline__ void top2_merge(double& b, int& i, double& s, double ob, int oi,
+                                           double os) {
+  s = fmax(fmax(s, os), fmin(b, ob));
+  if (ob > b || (ob == b && oi < i)) {
+    b = ob;
+    i = oi;
+  }
+}
+__device__ __forceinline__ void top2_warp(double& b, int& i, double& s) {
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(kFull, b, o);
+    const int oi = __shfl_xor_sync(kFull, i, o);
+    const double os = __shfl_xor_sync(kFull, s, o);
+    top2_merge(b, i, s, ob, oi, os);
+  }
+}
+// relative top-2 gap of a pick (near-tie diagnostic; 0 = exact tie)
+__device__ __forceinline__ double top2_gap(double b, double s) {
+  return b > 0.0 ? (b - fmax(s, 0.0)) / b : 0.0;
+}
+
 // DEIM (lowrank.py:168-205) as Gaussian elimination with row pivoting on a
 // working copy of W (n x r): column j's Schur-complement column is exactly
 // the interpolation residual W[:,j] - W[:,:j] W[p,:j]^-1 W[p,j]; the pivot is
@@ -1911,7 +1938,7 @@ __global__ void __launch_bounds__(1024) deim_kernel(int n, int r,
                                                    const double* __restrict__ W,
                                                    int* __restrict__ idx, double* __restrict__ Lhat,
                                                    double* __restrict__ U, int* err_col,
-                                                   int in_smem) {
+                                                   int in_smem, double* __restrict__ gap) {
   // Column-major work copy (smem when it fits).  Per column: block argmax
   // of |residual| (first index on ties) with two barriers; the picked row is
   // read-only during the elimination (its own update would zero it exactly,
@@ -1919,7 +1946,7 @@ __global__ void __launch_bounds__(1024) deim_kernel(int n, int r,
   extern __shared__ double dsm[];
   double* Wk = in_smem ? dsm : Wk_global;
   unsigned char* picked = reinterpret_cast<unsigned char*>(in_smem ? dsm + (size_t)n * r : nullptr);
-  __shared__ double bv[2][32];
+  __shared__ double bv[2][32], bs[2][32];
   __shared__ int bi[2][32];
   __shared__ double s_floor[32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -1948,27 +1975,27 @@ __global__ void __launch_bounds__(1024) deim_kernel(int n, int r,
   int fail = -1;
   for (int j = 0; j < r; ++j) {
     const int buf = j & 1;
-    double best = -1.0;
+    double best = -1.0, second = -1.0;
     int bidx = 0x7fffffff;
     const double* col = Wk + (int64_t)j * n;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      // (global variant: earlier picks hold exact zeros from here on)
       if (picked && picked[i]) continue;
       const double v = fabs(col[i]);
-      if (v > best) { best = v; bidx = i; }  // rows ascend per thread: first max kept
+      if (v > best) { second = best; best = v; bidx = i; }  // rows ascend: first max kept
+      else if (v > second) second = v;
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(kFull, best, o);
-      const int oi = __shfl_xor_sync(kFull, bidx, o);
-      if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
-    }
-    if (lane == 0) { bv[buf][w] = best; bi[buf][w] = bidx; }
+    top2_warp(best, bidx, second);
+    if (lane == 0) { bv[buf][w] = best; bi[buf][w] = bidx; bs[buf][w] = second; }
     __syncthreads();
-    double b = -1.0;
+    double b = -1.0, sb = -1.0;
     int p = 0x7fffffff;
-    for (int q = 0; q < nw; ++q)
-      if (bv[buf][q] > b || (bv[buf][q] == b && bi[buf][q] < p)) { b = bv[buf][q]; p = bi[buf][q]; }
-    if (p < 0 || p >= n) p = 0;  // all-NaN column: still a valid row
-    const double pv = col[p];
+    for (int q = 0; q < nw; ++q) top2_merge(b, p, sb, bv[buf][q], bi[buf][q], bs[buf][q]);
+    // no finite unpicked candidate (all NaN): fail like a vanished residual
+    const bool none = p < 0 || p >= n;
+    if (none) p = 0;
+    const double pv = none ? 0.0 : col[p];
+    if (gap && threadIdx.x == 0) gap[j] = top2_gap(b, sb);
     bool bad = !(fabs(pv) > floor_);
     if (!picked)
       for (int q = 0; q < j; ++q) bad |= idx[q] == p;  // (global-memory variant)
@@ -2012,10 +2039,11 @@ __global__ void __launch_bounds__(1024) deim_kernel(int n, int r,
 template <int RT>
 __global__ void __launch_bounds__(1024) deim_reg_kernel(int n, int r, const double* __restrict__ W,
                                                         int* __restrict__ idx, double* __restrict__ Lhat,
-                                                        double* __restrict__ U, int* __restrict__ err_col) {
+                                                        double* __restrict__ U, int* __restrict__ err_col,
+                                                        double* __restrict__ gap) {
   // double-buffered by pick parity: two block barriers per pick, and every
   // warp reduces the per-warp candidates itself (no serial pass)
-  __shared__ double bv[2][32];
+  __shared__ double bv[2][32], bs[2][32];
   __shared__ int bi[2][32];
   __shared__ double prow[2][RT];
   const int i = threadIdx.x, lane = i & 31, wid = i >> 5, nw = (blockDim.x + 31) >> 5;
@@ -2038,34 +2066,31 @@ __global__ void __launch_bounds__(1024) deim_reg_kernel(int n, int r, const doub
   for (int j = 0; j < RT; ++j) {
     if (j >= r) break;
     const int buf = j & 1;
-    double best = -1.0;
+    double best = -1.0, second = -1.0;
     int bidx = 0x7fffffff;
     if (row && myq < 0) {
       best = fabs(w[j]);
       bidx = i;
       if (!(best > -1.0)) { best = -1.0; bidx = 0x7fffffff; }  // NaN: never a candidate
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(kFull, best, o);
-      const int oi = __shfl_xor_sync(kFull, bidx, o);
-      if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
-    }
-    if (lane == 0) { bv[buf][wid] = best; bi[buf][wid] = bidx; }
+    top2_warp(best, bidx, second);
+    if (lane == 0) { bv[buf][wid] = best; bi[buf][wid] = bidx; bs[buf][wid] = second; }
     __syncthreads();
     best = lane < nw ? bv[buf][lane] : -1.0;
     bidx = lane < nw ? bi[buf][lane] : 0x7fffffff;
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(kFull, best, o);
-      const int oi = __shfl_xor_sync(kFull, bidx, o);
-      if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
-    }
-    const int p = (bidx < 0 || bidx >= n) ? 0 : bidx;  // all-NaN column: still a valid row
-    if (i == p) {
+    second = lane < nw ? bs[buf][lane] : -1.0;
+    top2_warp(best, bidx, second);
+    // no finite unpicked candidate (all NaN): fail like a vanished residual
+    // (row 0 may already be picked, so it is not a fallback)
+    const bool none = bidx < 0 || bidx >= n;
+    const int p = none ? 0 : bidx;
+    if (i == p && !none) {
 #pragma unroll
       for (int k = 0; k < RT; ++k) prow[buf][k] = w[k];
     }
     __syncthreads();
-    const double pv = prow[buf][j];
+    const double pv = none ? 0.0 : prow[buf][j];
+    if (gap && i == 0) gap[j] = top2_gap(best, second);
     if (!(fabs(pv) > floor_)) {  // InterpolationError (lowrank.py:192-199)
       if (i == 0) { idx[j] = p; *err_col = j; }
       return;
@@ -2104,18 +2129,19 @@ __global__ void __launch_bounds__(kDeimCT) deim_cluster_kernel(int n, int r, int
                                                               const double* __restrict__ W,
                                                               int* __restrict__ idx,
                                                               double* __restrict__ Lhat,
-                                                              double* __restrict__ U, int* err_col) {
+                                                              double* __restrict__ U, int* err_col,
+                                                              double* __restrict__ gap) {
   cg::cluster_group cl = cg::this_cluster();
   const int crank = (int)cl.block_rank(), cs = (int)cl.num_blocks();
   extern __shared__ double dsm[];
   const int i0 = crank * nl;
   const int nloc = max(0, min(nl, n - i0));
-  const int ls = r + 2;                    // slot stride: value, row, entries
+  const int ls = r + 3;                    // slot stride: value, row, second, entries
   double* Wk = dsm;                        // r x nl, Wk[k * nl + i]
   double* slot = Wk + (size_t)r * nl;      // 2 x ls
   double* prow = slot + 2 * ls;            // r: the pivot row
   unsigned char* picked = reinterpret_cast<unsigned char*>(prow + r);
-  __shared__ double wv[kDeimCT / 32];
+  __shared__ double wv[kDeimCT / 32], ws2[kDeimCT / 32];
   __shared__ int wi[kDeimCT / 32];
   __shared__ int s_idx[DLRSN_MAX_RANK];
   __shared__ int s_p, s_fail;
@@ -2143,56 +2169,55 @@ __global__ void __launch_bounds__(kDeimCT) deim_cluster_kernel(int n, int r, int
     if (lane == 0) s_floor = 1e-14 * fmax(1.0, m);
   }
   // local argmax of column 0
-  double best = -1.0;
+  double best = -1.0, second = -1.0;
   int bidx = 0x7fffffff;
   for (int i = tid; i < nloc; i += kDeimCT) {
     const double v = fabs(Wk[i]);
-    if (v > best) { best = v; bidx = i0 + i; }
+    if (v > best) { second = best; best = v; bidx = i0 + i; }
+    else if (v > second) second = v;
   }
   int fail = -1;
   for (int j = 0; j < r; ++j) {
     double* my = slot + ((j + 1) & 1) * ls;  // step 0 uses slot 1 (slot 0 held the max)
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(kFull, best, o);
-      const int oi = __shfl_xor_sync(kFull, bidx, o);
-      if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
-    }
-    if (lane == 0) { wv[w] = best; wi[w] = bidx; }
+    top2_warp(best, bidx, second);
+    if (lane == 0) { wv[w] = best; wi[w] = bidx; ws2[w] = second; }
     __syncthreads();
     if (w == 0) {
       double b = lane < nw ? wv[lane] : -1.0;
       int bi = lane < nw ? wi[lane] : 0x7fffffff;
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(kFull, b, o);
-        const int oi = __shfl_xor_sync(kFull, bi, o);
-        if (ov > b || (ov == b && oi < bi)) { b = ov; bi = oi; }
-      }
-      if (lane == 0) { my[0] = b; my[1] = (double)bi; }
+      double sb = lane < nw ? ws2[lane] : -1.0;
+      top2_warp(b, bi, sb);
+      if (lane == 0) { my[0] = b; my[1] = (double)bi; my[2] = sb; }
       const bool have = bi >= i0 && bi < i0 + nloc;
-      for (int k = j + lane; k < r; k += 32) my[2 + k] = have ? Wk[k * nl + (bi - i0)] : 0.0;
+      for (int k = j + lane; k < r; k += 32) my[3 + k] = have ? Wk[k * nl + (bi - i0)] : 0.0;
     }
     cl.sync();
     if (w == 0) {
       const double* rs = lane < cs ? cl.map_shared_rank(my, lane) : nullptr;
       double b = rs ? rs[0] : -1.0;
       int bi = rs ? (int)rs[1] : 0x7fffffff;
+      double sb = rs ? rs[2] : -1.0;
       int src = lane;
       for (int o = 16; o > 0; o >>= 1) {
         const double ov = __shfl_xor_sync(kFull, b, o);
         const int oi = __shfl_xor_sync(kFull, bi, o);
+        const double osb = __shfl_xor_sync(kFull, sb, o);
         const int os = __shfl_xor_sync(kFull, src, o);
-        if (ov > b || (ov == b && oi < bi)) { b = ov; bi = oi; src = os; }
+        const bool take = ov > b || (ov == b && oi < bi);
+        top2_merge(b, bi, sb, ov, oi, osb);
+        if (take) src = os;
       }
       const bool valid = bi >= 0 && bi < n;
       if (valid) {
         const double* win = cl.map_shared_rank(my, src);
-        for (int k = j + lane; k < r; k += 32) prow[k] = win[2 + k];
+        for (int k = j + lane; k < r; k += 32) prow[k] = win[3 + k];
       }
       __syncwarp();
       if (lane == 0) {
         const double pv = valid ? prow[j] : 0.0;
         s_p = valid ? bi : 0;
         s_fail = !(valid && fabs(pv) > s_floor);
+        if (gap && crank == 0) gap[j] = top2_gap(b, sb);
       }
     }
     __syncthreads();
@@ -2205,7 +2230,7 @@ __global__ void __launch_bounds__(kDeimCT) deim_cluster_kernel(int n, int r, int
     const double pv = prow[j];
     const int pl = p - i0;
     if (tid == 0 && pl >= 0 && pl < nloc) picked[pl] = 1;
-    best = -1.0;
+    best = second = -1.0;
     bidx = 0x7fffffff;
     for (int i = tid; i < nloc; i += kDeimCT) {
       if (i == pl || picked[i]) continue;
@@ -2214,7 +2239,8 @@ __global__ void __launch_bounds__(kDeimCT) deim_cluster_kernel(int n, int r, int
       for (int k = j + 1; k < r; ++k) Wk[k * nl + i] -= l * prow[k];
       if (j + 1 < r) {
         const double v = fabs(Wk[(j + 1) * nl + i]);
-        if (v > best) { best = v; bidx = i0 + i; }
+        if (v > best) { second = best; best = v; bidx = i0 + i; }
+        else if (v > second) second = v;
       }
     }
     // the next step's slot write happens after the __syncthreads of its
@@ -2491,6 +2517,45 @@ int dlrsn_mgram(const dlrsn_cellops* ops, int ra, int rb, const double* A, int l
   return DLRSN_OK;
 }
 
+}  // extern "C"
+
+namespace dlrsn {
+// optional CUDA-event timing of the K3 kernel launches (bench.py roofline)
+static bool g_proj_timing = false;
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_proj_events;
+static size_t g_proj_used = 0;
+static std::pair<cudaEvent_t, cudaEvent_t>* proj_timer() {
+  if (!g_proj_timing) return nullptr;
+  if (g_proj_used == g_proj_events.size()) {
+    std::pair<cudaEvent_t, cudaEvent_t> e;
+    if (cudaEventCreate(&e.first) != cudaSuccess || cudaEventCreate(&e.second) != cudaSuccess)
+      return nullptr;
+    g_proj_events.push_back(e);
+  }
+  return &g_proj_events[g_proj_used++];
+}
+bool project_timing_enabled() { return g_proj_timing; }
+}  // namespace dlrsn
+
+extern "C" {
+
+int dlrsn_project_timing(int enable) {
+  g_proj_timing = enable != 0;
+  g_proj_used = 0;
+  return DLRSN_OK;
+}
+
+int dlrsn_project_timing_read(int cap, float* ms, int* count) {
+  int n = 0;
+  for (size_t k = 0; k < g_proj_used; ++k, ++n) {
+    if (n >= cap) continue;
+    DLRSN_TRY_CUDA(cudaEventSynchronize(g_proj_events[k].second));
+    DLRSN_TRY_CUDA(cudaEventElapsedTime(&ms[n], g_proj_events[k].first, g_proj_events[k].second));
+  }
+  *count = n;
+  return DLRSN_OK;
+}
+
 int dlrsn_project(const dlrsn_cellops* ops, int r, const double* X, const double* Xold,
                   const double* sigma_t, const double* sigma_s, const double* q, double* out,
                   double* partial, dlrsn_stream_t stream) {
@@ -2515,8 +2580,11 @@ int dlrsn_project(const dlrsn_cellops* ops, int r, const double* X, const double
     DLRSN_TRY_CUDA(cudaFuncSetAttribute(project_mma32_kernel,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)kProj32Smem));
+    auto* tm = proj_timer();
+    if (tm) DLRSN_TRY_CUDA(cudaEventRecord(tm->first, st));
     project_mma32_kernel<<<dim3(tiles32, nblk32), 256, kProj32Smem, st>>>(pa, *ops);
     DLRSN_CHECK_LAUNCH("project_mma32_kernel");
+    if (tm) DLRSN_TRY_CUDA(cudaEventRecord(tm->second, st));
     const int64_t len32 = 7 * (int64_t)r * r + r;
     reduce_partials_kernel<<<(unsigned)((len32 + 31) / 32), 1024, 0, st>>>(nblk32, len32, partial,
                                                                            out, 1.0);
@@ -2525,6 +2593,8 @@ int dlrsn_project(const dlrsn_cellops* ops, int r, const double* X, const double
   }
   // partial slots not written by some tiles must be zero
   DLRSN_TRY_CUDA(zero_async(partial, sizeof(double) * (size_t)nblk * (7 * (size_t)r * r + r), st));
+  auto* tm = proj_timer();
+  if (tm) DLRSN_TRY_CUDA(cudaEventRecord(tm->first, st));
   if (simt && simt[0] == '1') {
     project_kernel<<<dim3(nblk, tiles), kTile * kTile, 0, st>>>(pa, *ops);
     DLRSN_CHECK_LAUNCH("project_kernel");
@@ -2532,6 +2602,7 @@ int dlrsn_project(const dlrsn_cellops* ops, int r, const double* X, const double
     project_mma_kernel<<<dim3(nblk, tiles), 256, 0, st>>>(pa, *ops);
     DLRSN_CHECK_LAUNCH("project_mma_kernel");
   }
+  if (tm) DLRSN_TRY_CUDA(cudaEventRecord(tm->second, st));
   const int64_t len = 7 * (int64_t)r * r + r;
   reduce_partials_kernel<<<(unsigned)((len + 31) / 32), 1024, 0, st>>>(nblk, len, partial, out, 1.0);
   DLRSN_CHECK_LAUNCH("reduce_partials_kernel");
@@ -2611,14 +2682,17 @@ int dlrsn_row_combine(int n, int r, const double* Binv, const double* ms, const 
 }
 
 int dlrsn_deim(int n, int r, double* Wwork, const double* W, int* idx, double* Lhat, double* U,
-               int* err_col, dlrsn_stream_t stream) {
+               int* err_col, double* gap, int variant, dlrsn_stream_t stream) {
   DLRSN_REQUIRE(r <= n, "rank %d exceeds the %d available nodes", r, n);
   DLRSN_REQUIRE(r <= DLRSN_MAX_RANK, "rank %d exceeds DLRSN_MAX_RANK", r);
+  DLRSN_REQUIRE(variant >= 0 && variant <= 3, "unknown DEIM variant %d", variant);
   static const char* ereg = getenv("DLRSN_DEIM_REG");
-  if (n <= 1024 && r <= 16 && !(ereg && ereg[0] == '0')) {
+  const bool reg_ok = n <= 1024 && r <= 16;
+  DLRSN_REQUIRE(variant != 1 || reg_ok, "register DEIM needs n <= 1024, r <= 16");
+  if (variant == 1 || (variant == 0 && reg_ok && !(ereg && ereg[0] == '0'))) {
     // register variant: 46 -> 36 us per step on config 2 (n = 1024, r = 16)
     deim_reg_kernel<16><<<1, (n + 31) / 32 * 32, 0, as_stream(stream)>>>(n, r, W, idx, Lhat, U,
-                                                                       err_col);
+                                                                       err_col, gap);
     DLRSN_CHECK_LAUNCH("deim_reg_kernel");
     return DLRSN_OK;
   }
@@ -2630,7 +2704,7 @@ int dlrsn_deim(int n, int r, double* Wwork, const double* W, int* idx, double* L
   else while (cs < 16 && cs * 256 < n) cs *= 2;
   auto csmem = [&](int c) {
     const int64_t nl = (n + c - 1) / c;
-    return (nl * r + 2 * (r + 2) + r) * (int64_t)sizeof(double) + nl;
+    return (nl * r + 2 * (r + 3) + r) * (int64_t)sizeof(double) + nl;
   };
   while (cs < 16 && csmem(cs) > 200 * 1024) cs *= 2;
   static int max_cs = 0;
@@ -2655,7 +2729,9 @@ int dlrsn_deim(int n, int r, double* Wwork, const double* W, int* idx, double* L
       max_cs = 16;
     cudaGetLastError();
   }
-  if (cs >= 1 && cs <= max_cs && csmem(cs) <= 200 * 1024) {
+  const bool cl_ok = cs >= 1 && cs <= max_cs && csmem(cs) <= 200 * 1024;
+  DLRSN_REQUIRE(variant != 2 || cl_ok, "cluster DEIM does not fit n = %d, r = %d", n, r);
+  if (variant == 2 || (variant == 0 && cl_ok)) {
     const int nl = (n + cs - 1) / cs;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(cs);
@@ -2668,7 +2744,8 @@ int dlrsn_deim(int n, int r, double* Wwork, const double* W, int* idx, double* L
     la.val.clusterDim.y = la.val.clusterDim.z = 1;
     lc.attrs = &la;
     lc.numAttrs = 1;
-    DLRSN_TRY_CUDA(cudaLaunchKernelEx(&lc, deim_cluster_kernel, n, r, nl, W, idx, Lhat, U, err_col));
+    DLRSN_TRY_CUDA(cudaLaunchKernelEx(&lc, deim_cluster_kernel, n, r, nl, W, idx, Lhat, U, err_col,
+                                      gap));
     DLRSN_CHECK_LAUNCH("deim_cluster_kernel");
     return DLRSN_OK;
   }
@@ -2679,8 +2756,9 @@ int dlrsn_deim(int n, int r, double* Wwork, const double* W, int* idx, double* L
                                         (int)smem));
   static const char* dt = getenv("DLRSN_DEIM_THREADS");
   const int threads = dt ? atoi(dt) : 256;  // 256 / 512 equal, 1024 slower (C2)
+  DLRSN_REQUIRE(in_smem || Wwork, "DEIM needs a work copy of W for n = %d, r = %d", n, r);
   deim_kernel<<<1, threads, in_smem ? smem : 0, as_stream(stream)>>>(n, r, Wwork, W, idx, Lhat, U,
-                                                                 err_col, in_smem);
+                                                                 err_col, in_smem, gap);
   DLRSN_CHECK_LAUNCH("deim_kernel");
   return DLRSN_OK;
 }

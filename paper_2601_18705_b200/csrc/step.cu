@@ -228,6 +228,76 @@ __global__ void pack_kernel(PackList l, unsigned* __restrict__ dst) {
     for (int w = threadIdx.x; w < l.words[k]; w += blockDim.x) dst[l.off[k] + w] = l.src[k][w];
 }
 
+// Forced DEIM selection (the angle_indices override of a step): the picks
+// come from the caller, W_hat = W[idx, :] is factored as Lhat U without
+// further pivoting (the factorisation DEIM's elimination produces when it
+// picks these rows in this order); err_col = j if pivot j vanishes below the
+// DEIM floor (lowrank.py:185,192-199) or an index repeats / is out of range.
+struct ForcedPicks {
+  int idx[DLRSN_MAX_RANK];
+};
+__global__ void deim_forced_kernel(int n, int r, const double* __restrict__ W, ForcedPicks fp,
+                                   int* __restrict__ idx_out, double* __restrict__ Lhat,
+                                   double* __restrict__ U, int* __restrict__ err_col,
+                                   double* __restrict__ gap) {
+  extern __shared__ double a[];  // r x r, row q = W[idx[q], :]
+  __shared__ double s_mx;
+  __shared__ int s_bad;
+  const int t = threadIdx.x;
+  if (t == 0) {
+    s_bad = -1;
+    for (int q = 0; q < r && s_bad < 0; ++q) {
+      bool bad = fp.idx[q] < 0 || fp.idx[q] >= n;
+      for (int e = 0; e < q; ++e) bad |= fp.idx[e] == fp.idx[q];
+      if (bad) s_bad = q;
+    }
+  }
+  double mx = 0.0;
+  for (int64_t e = t; e < (int64_t)n * r; e += blockDim.x) mx = fmax(mx, fabs(W[e]));
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
+  if (t == 0) s_mx = 0.0;
+  __syncthreads();
+  if ((t & 31) == 0) atomicMax(reinterpret_cast<unsigned long long*>(&s_mx),
+                               (unsigned long long)__double_as_longlong(mx));
+  __syncthreads();
+  const double floor_ = 1e-14 * fmax(1.0, s_mx);  // lowrank.py:185
+  int fail = s_bad;
+  if (fail < 0) {
+    for (int e = t; e < r * r; e += blockDim.x) a[e] = W[(int64_t)fp.idx[e / r] * r + e % r];
+    __syncthreads();
+    for (int j = 0; j < r; ++j) {  // Doolittle, rows in pick order
+      const double pv = a[j * r + j];
+      if (!(fabs(pv) > floor_)) { fail = j; break; }
+      for (int e = t; e < (r - j - 1) * (r - j); e += blockDim.x) {
+        const int q = j + 1 + e / (r - j), k = j + e % (r - j);
+        const double l = a[q * r + j] / pv;
+        if (k == j) continue;
+        a[q * r + k] -= l * a[j * r + k];
+      }
+      __syncthreads();
+      for (int q = j + 1 + t; q < r; q += blockDim.x) a[q * r + j] /= pv;
+      __syncthreads();
+    }
+  }
+  if (fail >= 0) {
+    if (t == 0) {
+      *err_col = fail;
+      for (int q = 0; q < r; ++q) idx_out[q] = fp.idx[q] >= 0 && fp.idx[q] < n ? fp.idx[q] : 0;
+    }
+    return;
+  }
+  for (int e = t; e < r * r; e += blockDim.x) {
+    const int q = e / r, k = e % r;
+    Lhat[e] = k < q ? a[e] : (k == q ? 1.0 : 0.0);
+    U[e] = k >= q ? a[e] : 0.0;
+  }
+  for (int q = t; q < r; q += blockDim.x) {
+    idx_out[q] = fp.idx[q];
+    if (gap) gap[q] = 1.0;  // forced: no argmax, no tie
+  }
+  if (t == 0) *err_col = -1;
+}
+
 // ---- workspace arena ---------------------------------------------------------
 struct Arena {
   char* base;
@@ -253,7 +323,7 @@ struct Upload {
 
 struct StepBufs {
   int *err_idx, *flags, *rowstat, *defw, *statw, *defx, *statx, *cholflag;
-  double *Wk, *Lhat, *U, *closure, *chk_in, *chk_out;
+  double *Wk, *Lhat, *U, *closure, *chk_in, *chk_out, *deimgap;
   double *sig4, *rhs_sk, *psi_sk, *phi_part, *scat, *psi_time, *phi0, *phi1, *norms, *red_ws;
   double *om_sel, *K, *Sb, *psi, *G, *R1, *R1inv, *ratio, *ratio2, *X1, *R2, *R2inv, *Rtot;
   double *part, *proj, *Binv, *L, *lbar, *T, *qall, *gamma, *lfull, *Rang, *cgsws;
@@ -287,6 +357,7 @@ static size_t carve(Arena& ar, StepBufs& b, int nx, int ny, int r, int no, int w
   b.statx = ar.take<int>(1);
   b.cholflag = ar.take<int>(2);
   b.Wk = ar.take<double>((size_t)no * r);
+  b.deimgap = ar.take<double>(r);
   b.Lhat = ar.take<double>((size_t)r * r);
   b.U = ar.take<double>((size_t)r * r);
   b.closure = ar.take<double>(r);
@@ -383,6 +454,8 @@ struct StepStatus {
   int statw, statx;
   double ratio[2 * DLRSN_MAX_RANK], ratiow[2 * DLRSN_MAX_RANK];
   int cholflag[2], cholw[2];
+  int sweep_status;                 // sweep workspace word 1 (2: handoff timeout)
+  double deim_gap[DLRSN_MAX_RANK];
 };
 
 // pinned, device-mapped host copy of the status block (one per host thread;
@@ -405,7 +478,8 @@ static int status_block(StepStatus** out) {
 }
 
 // pack kernel + one device-to-host copy of the status block
-static int enqueue_status(cudaStream_t st, const StepBufs& b, int r, StepStatus* hs) {
+static int enqueue_status(cudaStream_t st, const StepBufs& b, int r, StepStatus* hs,
+                          const void* sweep_ws) {
   PackList l;
   l.n = 0;
   StepStatus* dev = reinterpret_cast<StepStatus*>(b.rbdev);
@@ -430,6 +504,8 @@ static int enqueue_status(cudaStream_t st, const StepBufs& b, int r, StepStatus*
   add(b.ratiow, 2 * r * sizeof(double), dev->ratiow);
   add(b.cholflag, 2 * sizeof(int), dev->cholflag);
   add(b.cholw, 2 * sizeof(int), dev->cholw);
+  add(reinterpret_cast<const int*>(sweep_ws) + 1, sizeof(int), &dev->sweep_status);
+  add(b.deimgap, r * sizeof(double), dev->deim_gap);
   (void)hs;
   pack_kernel<<<1, 256, 0, st>>>(l, reinterpret_cast<unsigned*>(g_status_dev));
   DLRSN_CHECK_LAUNCH("pack_kernel");
@@ -708,8 +784,6 @@ static int grid_n(int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
 }
 
-// source-iteration batch size hint: the largest count seen (+1)
-static thread_local int g_si_hint = 0;
 // X_new of the previous successful step: a step whose X is it is part of a
 // driver loop, whose buffers come back, so its graph is captured at once
 static thread_local const void* g_last_xnew = nullptr;
@@ -719,6 +793,20 @@ static thread_local const void* g_last_xnew = nullptr;
 using namespace dlrsn;
 
 extern "C" {
+
+int dlrsn_deim_forced(int n, int r, const double* W, const int64_t* indices, int* idx,
+                      double* Lhat, double* U, int* err_col, double* gap, dlrsn_stream_t stream) {
+  DLRSN_REQUIRE(r >= 1 && r <= n && r <= DLRSN_MAX_RANK, "rank %d outside [1, min(%d, %d)]", r, n,
+                DLRSN_MAX_RANK);
+  DLRSN_REQUIRE((size_t)r * r * sizeof(double) <= 48 * 1024, "forced selection needs r <= 78");
+  DLRSN_REQUIRE(indices, "null angle indices");
+  ForcedPicks fp;
+  for (int d = 0; d < r; ++d) fp.idx[d] = (indices[d] >= 0 && indices[d] < n) ? (int)indices[d] : -1;
+  deim_forced_kernel<<<1, 256, (size_t)r * r * sizeof(double), as_stream(stream)>>>(
+      n, r, W, fp, idx, Lhat, U, err_col, gap);
+  DLRSN_CHECK_LAUNCH("deim_forced_kernel");
+  return DLRSN_OK;
+}
 
 int64_t dlrsn_step_workspace_bytes(int nx, int ny, int r, int n_omega, int world_size) {
   StepBufs b;
@@ -761,6 +849,16 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
   const bool ang_fast = r <= 32 && dlrsn_cholqr2_small_smem(no, r) <= 200 * 1024;
   StepStatus* hs = nullptr;
   DLRSN_RET(status_block(&hs));
+  ForcedPicks forced;
+  memset(&forced, 0, sizeof(forced));
+  if (p->angle_override) {
+    DLRSN_REQUIRE(p->angle_indices_in, "angle_override without angle_indices_in");
+    DLRSN_REQUIRE((size_t)r * r * sizeof(double) <= 48 * 1024, "forced selection needs r <= 78");
+    for (int d = 0; d < r; ++d) {
+      const int64_t v = p->angle_indices_in[d];
+      forced.idx[d] = (v >= 0 && v < no) ? (int)v : -1;
+    }
+  }
   double* P[2] = {b.phi0, b.phi1};
   Inflow4 infl;
   bool has_inflow = false;
@@ -818,7 +916,13 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
       DLRSN_RET(dlrsn_cells_to_sk4(ops, sigma_t, b.sig4, ss2));
     }
     // 1. DEIM, closure weights (errors reported at the readback)
-    DLRSN_RET(dlrsn_deim(no, r, b.Wk, W, b.err_idx + 1, b.Lhat, b.U, b.err_idx, s));
+    if (p->angle_override) {
+      deim_forced_kernel<<<1, 256, (size_t)r * r * sizeof(double), st>>>(
+          no, r, W, forced, b.err_idx + 1, b.Lhat, b.U, b.err_idx, b.deimgap);
+      DLRSN_CHECK_LAUNCH("deim_forced_kernel");
+    } else {
+      DLRSN_RET(dlrsn_deim(no, r, b.Wk, W, b.err_idx + 1, b.Lhat, b.U, b.err_idx, b.deimgap, 0, s));
+    }
     DLRSN_RET(dlrsn_what_solve(r, 1, b.Lhat, b.U, beta, b.closure, 1, s));
     const int width = world > 1 ? comm->gather_width : 1;
     plan_kernel<<<1, DLRSN_MAX_RANK, 0, st>>>(r, no, world, rank_id, b.err_idx, b.err_idx + 1,
@@ -961,13 +1065,16 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
       ortho_residual_kernel<<<1, 256, 0, st>>>(r, b.G, b.wg, b.chk_out, nullptr, p->x_check_out);
       DLRSN_CHECK_LAUNCH("ortho_residual_kernel");
     }
-    return enqueue_status(st, b, r, hs);
+    return enqueue_status(st, b, r, hs, sweep_ws);
   };
 
   int exact = p->gs_method == 1 ? 1 : 0;
   int exact_w = 0;
-  // iteration batch: sticky (only grows), so the graph keys stay stable
-  const int batch0 = std::min(std::max(g_si_hint + 1, 6), 24);
+  // iteration batch: the caller's per-problem hint (the largest iteration
+  // count of its earlier steps + 1, so it only grows and the graph keys stay
+  // stable); every rank of a sharded step passes the same value
+  const int batch0 = std::min(std::max(p->si_batch_hint, 6), 24);
+  info->si_batch_hint = batch0;
   int it_next = std::min(p->si_max_iters, batch0) + 1;
   // ---- segment 1 (the whole step in the common case): replayed as a CUDA
   // graph when the same buffers come back (world 1; see graph_cache)
@@ -978,7 +1085,9 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
       return enqueue_tail(st, exact, exact_w, false);
     };
     GraphKey key;
-    const bool graphed = world == 1 && graphs_enabled() && !sweep_timing_enabled();
+    const bool graphed = world == 1 && graphs_enabled() && !sweep_timing_enabled() &&
+                         !project_timing_enabled() &&
+                         !p->angle_override;
     if (graphed) {
       key.set(ops, p, X, S, W, beta, sigma_t, sigma_s, q, X_new, S_new, W_new, beta_new, phi_out,
               si_phi, workspace, sweep_ws, sweep_ws_bytes, batch0, exact, exact_w);
@@ -988,6 +1097,7 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     }
   }
   DLRSN_TRY_CUDA(cudaStreamSynchronize(st0));
+  for (int d = 0; d < r; ++d) info->deim_gap[d] = hs->deim_gap[d];
   // errors of the reference's order (dlr_sn.py:99-109)
   if (hs->err_idx[0] >= 0) {  // InterpolationError (lowrank.py:192-199)
     info->error_index = hs->err_idx[0];
@@ -1010,6 +1120,14 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
   // exact Gram-Schmidt pass (a CholQR2 guard failed) -- rare, not graphed
   int batch = batch0;
   for (int guard = 0; guard < 1 << 20; ++guard) {
+    info->sweep_status = hs->sweep_status;
+    if (hs->sweep_status) {  // a strip handoff timed out: psi is not trustworthy
+      DLRSN_RET(dlrsn_sweep_workspace_init(sweep_ws, sweep_ws_bytes, st0));
+      DLRSN_TRY_CUDA(cudaStreamSynchronize(st0));
+      set_error("sweep strip handoff timed out (status %d); workspace re-armed",
+                hs->sweep_status);
+      return DLRSN_ECUDA;
+    }
     for (int d = 0; d < r; ++d) info->closure[d] = hs->closure[d];
     info->residual = hs->ctl.change;
     if (!hs->ctl.done) {
@@ -1028,9 +1146,9 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
       continue;
     }
     info->iterations = hs->ctl.iters;
-    // batch hint: the iteration count, decaying by one per step (stable
+    // next step's batch hint: grows to cover this step's count (stable
     // batches keep the graph keys stable; a shortfall costs one more segment)
-    g_si_hint = std::max(hs->ctl.iters, g_si_hint);
+    info->si_batch_hint = std::max(batch0, hs->ctl.iters + 1);
     if (!exact) {
       // CholQR's R_kk is accurate to ~eps/rel^2: keep it only when every
       // column retains >= 1e-6 of its M-norm and sits 100x above the

@@ -109,6 +109,7 @@ __device__ __forceinline__ void solve4(double* a, double* b, double* x) {
 int launch_sweep_ws(const SweepArgs& a, int max_ctas, cudaStream_t st);
 
 bool sweep_timing_enabled();
+bool project_timing_enabled();
 int advance_launch(const dlrsn_advance* av, const double* phi, cudaStream_t st);  // physics.cu  // dlrsn_sweep_timing on (the step then skips graphs)
 
 // internal entry points of the step (step.cu); the public C-ABI calls pass

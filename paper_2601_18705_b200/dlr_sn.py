@@ -40,9 +40,11 @@ from .lowrank import (
     _cgs2_flags,
     _row_solve_async,
     cgs2_spatial_async,
+    check_ties,
     cholqr2_speculative,
     cholqr_guard_ok,
     deim_finish,
+    deim_forced_launch,
     deim_launch,
     evaluate_rows,
     raise_row_status,
@@ -51,6 +53,9 @@ from .lowrank import (
 from .transport import assemble_operators, inflow_values, source_iteration
 
 FOUR_PI = 4.0 * np.pi
+# DEIM picks closer to a tie than this (relative top-2 residual gap) raise
+# InterpolationTieError unless the selection is forced (SURVEY 8c hazard (i))
+DEIM_TIE_TOL = 1e-10
 
 
 @dataclass(eq=False)
@@ -117,7 +122,8 @@ def project_initial(state, x_new, ops):
 
 def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, use_dsa=True,
                      dsa_penalty="simplified", threads=0, check_state=True, gs_method="cholqr2",
-                     sweep_dw=None, comm=None, engine="native", inflow=None, _advance=None):
+                     sweep_dw=None, comm=None, engine="native", inflow=None, angle_indices=None,
+                     deim_tie_tol=DEIM_TIE_TOL, _advance=None):
     """Advance one linearised step; returns (new DlrState, CollocationStepInfo).
 
     ``engine="native"`` issues the whole step from C++ through the single
@@ -137,6 +143,12 @@ def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, 
     |omega.n| psi_b (e2 row sums) on the wall edge dofs joins each selected
     direction's sweep rhs and, projected on X_new, its reduced row source
     (BASELINE config 3; restated in oracle/port.py ``inflow_load``).
+
+    ``angle_indices`` (an extension) forces the DEIM selection (r node
+    indices, in pick order) -- e.g. the reference's own picks for a basis
+    with near-ties.  Otherwise each pick's relative top-2 residual gap is
+    checked against ``deim_tie_tol`` (InterpolationTieError below it; 0
+    disables) and reported as ``info.deim_gaps``.
     """
     if gs_method not in ("cholqr2", "cgs2"):
         raise ConfigurationError(f"unknown gs_method {gs_method!r}")
@@ -148,27 +160,33 @@ def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, 
         if dsa_penalty not in ("simplified", "collocation"):
             raise ContractViolation(f"unknown dsa penalty variant {dsa_penalty!r}")
         return _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state,
-                            gs_method, sweep_dw, comm, _advance, inflow_values(inflow))
+                            gs_method, sweep_dw, comm, _advance, inflow_values(inflow),
+                            angle_indices, deim_tie_tol)
     if inflow_values(inflow) is not None:
         raise ConfigurationError("inflow boundaries need the native engine")
     if _advance is not None:
         raise ConfigurationError("the fused step boundary needs the native engine")
     r = state.rank
     # ---- DEIM + closure + input checks: one readback ------------------------
-    selection, err_idx = deim_launch(state.W.values)
+    if angle_indices is not None:
+        selection, err_idx = deim_forced_launch(state.W.values, angle_indices)
+    else:
+        selection, err_idx = deim_launch(state.W.values)
     closure = selection.closure_weights(state.W.beta)
     ops = assemble_operators(grid, step, dsa_penalty=dsa_penalty, validate=False)
     bad_sigma = (step.sigma_t - step.sigma_s <= 0).any().to(torch.float64).reshape(1)
-    parts = [err_idx.to(torch.float64), closure, bad_sigma]
+    parts = [err_idx.to(torch.float64), closure, bad_sigma, selection.gap_dev]
     if check_state:
         parts.append(state.check_values(ops, quad))
     host = torch.cat(parts).cpu().numpy()
-    deim_finish(selection, host[:r + 1])                       # InterpolationError
+    deim_finish(selection, host[:r + 1], host[2 * r + 2:3 * r + 2])  # InterpolationError
     closure_host = host[r + 1:2 * r + 1].copy()
     if host[2 * r + 1]:                                        # transport_sn.py:208-209
         raise ContractViolation("pseudo absorption sigma_t - sigma_s must stay positive")
     if check_state:
-        state.raise_check(host[2 * r + 2:])                    # lowrank.py:68-81
+        state.raise_check(host[3 * r + 2:])                    # lowrank.py:68-81
+    if angle_indices is None:
+        check_ties(selection.gaps, deim_tie_tol)
     omegas_sel = quad.omegas[selection.indices]
     if dsa_penalty == "collocation":
         ops.penalty_closure = (omegas_sel, closure_host)
@@ -196,6 +214,7 @@ def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, 
         angular_deficiency=tail["adef"],
         si_phi=result.phi,
     )
+    info.deim_gaps = selection.gaps
     return new_state, info
 
 
@@ -404,6 +423,9 @@ class _NativeCtx:
         self.shapes = [(n, r), (r, r), (no, r), (r,), (n,), (n,)]
         self.strides = [(r, 1), (r, 1), (r, 1), (1,), (1,), (1,)]
         self.fn = lib.dlrsn_step_collocation
+        # source iterations enqueued before the first readback: per problem,
+        # so every rank of a sharded run (same steps, same ctx history) agrees
+        self.si_hint = 0
 
 
 _CTX = {}
@@ -421,7 +443,7 @@ def _native_ctx(grid, quad, r, comm):
 
 
 def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_method, sweep_dw,
-                 comm, advance=None, inflow=None):
+                 comm, advance=None, inflow=None, angle_indices=None, deim_tie_tol=DEIM_TIE_TOL):
     r = state.rank
     no = quad.n_angles
     n = grid.n_dofs
@@ -446,6 +468,15 @@ def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_
     p.gs_method = 0 if gs_method == "cholqr2" else 1
     p.advance = ctypes.addressof(advance) if advance is not None else None
     p.inflow[:] = inflow if inflow is not None else (0.0, 0.0, 0.0, 0.0)
+    p.si_batch_hint = ctx.si_hint
+    forced = None
+    if angle_indices is not None:
+        forced = np.ascontiguousarray(angle_indices, dtype=np.int64).reshape(-1)
+        if forced.shape != (r,):
+            raise ContractViolation(f"angle_indices must hold {r} node indices")
+        p.angle_override, p.angle_indices_in = 1, forced.ctypes.data
+    else:
+        p.angle_override, p.angle_indices_in = 0, None
     # DlrState.check of an X this library produced and already checked (same
     # tensor, not modified since): the input Gram is not recomputed
     xc = getattr(state, "_xcheck", None)
@@ -465,6 +496,9 @@ def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_
         ob + 8 * ctx.offs[0], ob + 8 * ctx.offs[1], ob + 8 * ctx.offs[2], ob + 8 * ctx.offs[3],
         ob + 8 * ctx.offs[4], ob + 8 * ctx.offs[5], ctx.ws.data_ptr(), ctx.ws.numel(),
         ctx.sws.data_ptr(), ctx.sws.numel(), ctx.comm_ref, ctypes.byref(info), stream())
+    p.angle_override, p.angle_indices_in = 0, None
+    if rc == 0 or rc == -7:
+        ctx.si_hint = max(ctx.si_hint, int(info.si_batch_hint))
     if hooks is not None and hooks.error is not None:
         raise hooks.error
     if rc != 0:
@@ -482,6 +516,9 @@ def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_
             raise ContractViolation(msg)
         raise RuntimeError(f"dlrsn CUDA failure ({rc}): {msg}")
     indices = np.frombuffer(info.angle_indices, dtype=np.int64, count=r).copy()
+    gaps = np.frombuffer(info.deim_gap, dtype=np.float64, count=r).copy()
+    if forced is None:
+        check_ties(gaps, deim_tie_tol)
     basis = AngularBasis(values=W_new, beta=beta_new)
     new_state = DlrState(X=X_new, S=S_new, W=basis)
     if check_state:
@@ -496,4 +533,5 @@ def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_
         si_phi=si_phi,
     )
     res.gs_fallback = int(info.gs_fallback)
+    res.deim_gaps = gaps
     return new_state, res

@@ -19,7 +19,7 @@ import torch
 from . import _lib
 from ._device import as_device, cached_upload, device, empty, stream, to_numpy, zeros
 from .angular import AngularBasis
-from .errors import ContractViolation, InterpolationError, SolverError
+from .errors import ContractViolation, InterpolationError, InterpolationTieError, SolverError
 from .mesh import cellops_struct
 
 FOUR_PI = 4.0 * np.pi
@@ -259,6 +259,8 @@ class DeimSelection:
     w_hat: torch.Tensor
     lhat: torch.Tensor
     u: torch.Tensor
+    gap_dev: torch.Tensor | None = None  # per pick relative top-2 residual gap (device)
+    gaps: np.ndarray | None = None       # the same on the host, after deim_finish
 
     @property
     def rank(self):
@@ -286,42 +288,87 @@ class DeimSelection:
         return x[:, 0]
 
 
-def deim_select(basis_values):
+DEIM_VARIANTS = {"auto": 0, "register": 1, "cluster": 2, "block": 3}
+
+
+def deim_select(basis_values, *, variant="auto", tie_tol=0.0):
     """Greedy DEIM point selection over quadrature nodes (lowrank.py:168-205);
-    ties take the lowest node index."""
+    ties take the lowest node index.  ``selection.gaps`` holds each pick's
+    relative top-2 residual gap; ``tie_tol`` > 0 raises InterpolationTieError
+    for a pick closer to a tie than that (an extension: the reference breaks
+    every tie silently).  ``variant`` pins the kernel (tests)."""
     W = as_device(basis_values)
     if W.ndim != 2:
         raise ContractViolation("deim_select expects an (n_angles, rank) array")
     n, r = W.shape
     if r > n:
         raise ContractViolation(f"rank {r} exceeds the {n} available nodes")
-    sel, err_idx = deim_launch(W)
-    return deim_finish(sel, err_idx.cpu().numpy())
+    sel, err_idx = deim_launch(W, variant=variant)
+    host = torch.cat([err_idx.to(torch.float64), sel.gap_dev]).cpu().numpy()
+    sel = deim_finish(sel, host[:r + 1].astype(np.int64), host[r + 1:])
+    check_ties(sel.gaps, tie_tol)
+    return sel
 
 
-def deim_launch(W):
-    """Launch DEIM without a host sync: (selection with device-side factors,
-    int32 [err_col, idx...]) -- see deim_finish."""
+def deim_launch(W, variant="auto"):
+    """Launch DEIM without a host sync: (selection with device-side factors
+    and top-2 gaps, int32 [err_col, idx...]) -- see deim_finish."""
     W = as_device(W).contiguous()
     n, r = W.shape
     work = empty(n, r)
     err_idx = _i32(r + 1)
     lhat, u = empty(r, r), empty(r, r)
+    gap = empty(r)
     _lib.call("dlrsn_deim", n, r, _lib.ptr(work), _lib.ptr(W), _lib.ptr(err_idx[1:]),
-              _lib.ptr(lhat), _lib.ptr(u), _lib.ptr(err_idx[:1]), stream())
+              _lib.ptr(lhat), _lib.ptr(u), _lib.ptr(err_idx[:1]), _lib.ptr(gap),
+              DEIM_VARIANTS[variant], stream())
     idx_dev = err_idx[1:].to(torch.int64)
     sel = DeimSelection(indices=None, indices_dev=idx_dev, w_hat=W[idx_dev].contiguous(),
-                        lhat=lhat, u=u)
+                        lhat=lhat, u=u, gap_dev=gap)
     return sel, err_idx
 
 
-def deim_finish(sel, host_err_idx):
+def deim_forced_launch(W, indices):
+    """DEIM factors for a forced selection (``angle_indices`` of a step):
+    W_hat = W[indices] = Lhat U in the given order, err_col set when a pivot
+    vanishes or an index repeats / is out of range (no host sync)."""
+    W = as_device(W).contiguous()
+    n, r = W.shape
+    idx_h = np.ascontiguousarray(indices, dtype=np.int64).reshape(-1)
+    if idx_h.shape != (r,):
+        raise ContractViolation(f"angle_indices must hold {r} node indices")
+    err_idx = _i32(r + 1)
+    lhat, u = empty(r, r), empty(r, r)
+    gap = empty(r)
+    _lib.call("dlrsn_deim_forced", n, r, _lib.ptr(W), idx_h.ctypes.data, _lib.ptr(err_idx[1:]),
+              _lib.ptr(lhat), _lib.ptr(u), _lib.ptr(err_idx[:1]), _lib.ptr(gap), stream())
+    idx_dev = err_idx[1:].to(torch.int64)
+    sel = DeimSelection(indices=None, indices_dev=idx_dev, w_hat=W[idx_dev].contiguous(),
+                        lhat=lhat, u=u, gap_dev=gap)
+    return sel, err_idx
+
+
+def deim_finish(sel, host_err_idx, host_gaps=None):
     """Raise InterpolationError (lowrank.py:192-199) or attach host indices."""
     if host_err_idx[0] >= 0:
         raise InterpolationError("interpolation residual vanished; basis is rank deficient",
                                  column=int(host_err_idx[0]))
     sel.indices = np.asarray(host_err_idx[1:], dtype=np.int64)
+    if host_gaps is not None:
+        sel.gaps = np.asarray(host_gaps, dtype=float)
     return sel
+
+
+def check_ties(gaps, tie_tol):
+    """InterpolationTieError for the first pick whose relative top-2 gap is
+    below ``tie_tol`` (hazard (i) of SURVEY 8c: a near-tie is decided by
+    round-off, so a GPU and a CPU run may pick different nodes)."""
+    if tie_tol and gaps is not None:
+        bad = np.flatnonzero(np.asarray(gaps) < tie_tol)
+        if bad.size:
+            j = int(bad[0])
+            raise InterpolationTieError("near-tie DEIM pick; pass angle_indices= to force the "
+                                        "selection", column=j, gap=float(gaps[j]))
 
 
 @dataclass(eq=False)

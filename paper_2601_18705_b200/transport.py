@@ -298,6 +298,21 @@ def closure_sweep(ops, omegas, closure, rhs, *, scat_phi=None, dw=4, ws_limit=8 
     return phi
 
 
+def sweep_status_word(workspace):
+    """Device view of the sweep workspace's sticky status (word 1; 2 = a
+    strip handoff wait timed out, include/dlrsn.h)."""
+    return workspace[4:8].view(torch.int32)
+
+
+def raise_sweep_status(status, workspace):
+    """A timed-out strip handoff leaves psi wrong: re-arm the workspace and
+    fail loudly instead of returning it."""
+    if int(status):
+        _lib.call("dlrsn_sweep_workspace_init", _lib.ptr(workspace), workspace.numel(), stream())
+        raise RuntimeError(f"dlrsn sweep strip handoff timed out (status {int(status)}); "
+                           "workspace re-armed")
+
+
 def _to_canonical(ops, plan, psi_sk, out=None):
     g = ops.grid
     psi = out if out is not None else empty(g.n_dofs, plan.D)
@@ -319,7 +334,9 @@ def sweep_solve(ops, omega, rhs, _key=None):
     _lib.call("dlrsn_rhs_build", ops.cellops_ptr, 1, _lib.ptr(plan.quads_dev), _lib.ptr(zero_q),
               0.0, None, 1, _lib.ptr(rhs), 1, _lib.ptr(rhs_sk), stream())
     _sweep(ops, plan, rhs_sk, psi_sk)
-    return _to_canonical(ops, plan, psi_sk)[:, 0].contiguous()
+    out = _to_canonical(ops, plan, psi_sk)[:, 0].contiguous()
+    raise_sweep_status(sweep_status_word(plan.workspace).item(), plan.workspace)
+    return out
 
 
 def source_iteration(ops, omegas, closure, psi_time=None, *, use_dsa=True, tol=1e-8,
@@ -387,7 +404,7 @@ def source_iteration(ops, omegas, closure, psi_time=None, *, use_dsa=True, tol=1
     nb = (g.n_cells + 255) // 256
     red_ws = ops.buffer("red_ws", 256 // 8 + 2 * nb + 8, zero=True)
     norms = zeros(2)
-    host = torch.empty(3, dtype=torch.float64, pin_memory=True)
+    host = torch.empty(4, dtype=torch.float64, pin_memory=True)
     dsa = _DsaState(ops) if use_dsa else None
     change = math.inf
     for it in range(1, max_iters + 1):
@@ -426,9 +443,13 @@ def source_iteration(ops, omegas, closure, psi_time=None, *, use_dsa=True, tol=1
         host[:2].copy_(norms, non_blocking=True)
         if it == 1:
             host[2:3].copy_(flags.to(torch.float64), non_blocking=True)
+        if plan:
+            host[3:4].copy_(sweep_status_word(plan.workspace).to(torch.float64), non_blocking=True)
         if dsa is not None:
             dsa.stage_info()
         torch.cuda.current_stream(device()).synchronize()
+        if plan:
+            raise_sweep_status(host[3].item(), plan.workspace)
         if dsa is not None:
             dsa.raise_on_failure()
         phi, phi_new = phi_new, phi
