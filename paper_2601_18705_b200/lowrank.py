@@ -361,10 +361,14 @@ def deim_finish(sel, host_err_idx, host_gaps=None):
 
 def check_ties(gaps, tie_tol):
     """InterpolationTieError for the first pick whose relative top-2 gap is
-    below ``tie_tol`` (hazard (i) of SURVEY 8c: a near-tie is decided by
-    round-off, so a GPU and a CPU run may pick different nodes)."""
+    positive but below ``tie_tol`` (hazard (i) of SURVEY 8c: a near-tie is
+    decided by round-off, so a GPU and a CPU run may pick different nodes).
+    An exact tie (gap 0: bitwise-equal maxima, e.g. the constant completion
+    column of a deficient angular basis) follows the reference's stated rule,
+    the lowest node index (lowrank.py:176, np.argmax), as the kernels do."""
     if tie_tol and gaps is not None:
-        bad = np.flatnonzero(np.asarray(gaps) < tie_tol)
+        g = np.asarray(gaps)
+        bad = np.flatnonzero((g > 0.0) & (g < tie_tol))
         if bad.size:
             j = int(bad[0])
             raise InterpolationTieError("near-tie DEIM pick; pass angle_indices= to force the "

@@ -258,8 +258,10 @@ def gen_sn():
     save("sn", **out)
 
 
-def run_checker(tag, per, r, nq, nsteps, seed):
-    """Reference dlr-sn loop on a checkerboard (SURVEY App. B adapters)."""
+def run_checker(tag, per, r, nq, nsteps, seed, compact=False):
+    """Reference dlr-sn loop on a checkerboard (SURVEY App. B adapters).
+    ``compact``: BASELINE-size runs (config 2) keep phi, T and the sketches
+    but not the quadrature flux, and skip the dense energy rows."""
     spec = problems.checkerboard(per, rank=r, n_polar=nq, n_azimuthal=nq, seed=seed)
     rng = np.random.default_rng(spec.seed)
     Xr, Wr = problems.draw_factors(spec, rng)
@@ -286,14 +288,18 @@ def run_checker(tag, per, r, nq, nsteps, seed):
                                               use_dsa=False)
         raw = physics.update_temperature(driver.dofs_to_cells(g, info.phi), lin, -np.inf)
         Tn = np.maximum(raw, 1e-6)
-        row = diag_row(g, quad, spec, T, Tn, raw, state.reconstruct(), e_prev)
-        e_prev = (row[0], row[1])
+        if not compact:
+            row = diag_row(g, quad, spec, T, Tn, raw, state.reconstruct(), e_prev)
+            e_prev = (row[0], row[1])
+            out[f"s{s}_diag"] = row
+            out[f"s{s}_phiq"] = state.scalar_flux()
         T = Tn
         out.update({f"s{s}_idx": info.angle_indices, f"s{s}_iters": info.iterations,
-                    f"s{s}_diag": row,
                     f"s{s}_cond": info.interpolation_condition, f"s{s}_phi": info.phi,
-                    f"s{s}_T": T, f"s{s}_phiq": state.scalar_flux(),
+                    f"s{s}_T": T, f"s{s}_S": state.S, f"s{s}_W": state.W.values,
                     f"s{s}_sketch": sketch(state.X, state.S, state.W.values),
+                    f"s{s}_xsketch": np.random.default_rng(19).standard_normal(
+                        (12, state.X.shape[0])) @ state.X,
                     f"s{s}_sdef": info.spatial_deficiency, f"s{s}_adef": info.angular_deficiency})
         print(tag, "step", s, info.iterations, info.angle_indices)
     if per <= 3:
@@ -431,6 +437,10 @@ if __name__ == "__main__":
     import importlib
 
     sys.modules["helpers_ref"] = importlib.import_module("helpers")
+    if len(sys.argv) > 1 and sys.argv[1] == "dlr_c2":
+        # BASELINE config 2 itself, one step of the real reference (~1 min)
+        run_checker("dlr_c2", per=40, r=16, nq=32, nsteps=1, seed=2, compact=True)
+        sys.exit(0)
     gen_physics()
     gen_quadrature()
     gen_sweep()
