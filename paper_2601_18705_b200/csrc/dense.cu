@@ -1360,6 +1360,319 @@ __global__ void __launch_bounds__(256, 1) project_mma32_kernel(ProjArgs pa, dlrs
     out[7 * (int64_t)r * r + j0 + threadIdx.x] = qacc;
 }
 
+// Output groups of the split launch: GROUP 0 = {px, py, jx, jy} (volume and
+// face terms), GROUP 1 = {mt, ms, mo} + q-hat.  Each CTA stages only its
+// group's planes and holds only its group's accumulators (4 or 3 outputs x
+// 2x2 fragments instead of 7), so two CTAs (16 warps) fit per SM and the
+// dependent DMMA chains of one warp are covered by the others.
+constexpr size_t kProj32RedG0 = (4 + 2) * 32 * 33;
+constexpr size_t kProj32RedG1 = 3 * 32 * 33;
+constexpr size_t kProj32SmemG =
+    (kProj32Stage > kProj32RedG0 ? kProj32Stage : kProj32RedG0) * sizeof(double);
+
+template <int GROUP>
+__device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_cellops& ops,
+                                                double* sm32) {
+  constexpr int C = kPC32, kLS = kLS32, kRow = kRow32;
+  constexpr int NO = GROUP == 0 ? 4 : 3;  // accumulated outputs
+  double* sX = sm32;             // [C][4][kLS] i-side
+  double* sXo = sX + C * kRow;   // [C][4][kLS] i-side (group 1)
+  double* sU = sXo + C * kRow;   // [C][4][kLS] i-side: ux0 ux1 uy0 uy1 (group 0)
+  double* sMX = sU + C * kRow;   // [C][4][kLS] j-side (group 1)
+  double* sGX = sMX + C * kRow;  // [C][4][kLS] (group 0)
+  double* sGY = sGX + C * kRow;  // [C][4][kLS] (group 0)
+  double* sF = sGY + C * kRow;   // [C][8][kLS] (group 0)
+  double* sQ = sF + 2 * C * kRow;  // [C][32] (group 1)
+  double* sC = sQ + C * kT32;      // [C][2] (group 1)
+  __shared__ double so[64];
+  if (threadIdx.x < 16) {
+    so[threadIdx.x] = ops.mass[threadIdx.x];
+    so[16 + threadIdx.x] = ops.gx[threadIdx.x];
+    so[32 + threadIdx.x] = ops.gy[threadIdx.x];
+  } else if (threadIdx.x < 20) {
+    so[48 + threadIdx.x - 16] = ops.e2x[threadIdx.x - 16];
+    so[52 + threadIdx.x - 16] = ops.e2y[threadIdx.x - 16];
+    so[56 + threadIdx.x - 16] = ops.src_row[threadIdx.x - 16];
+  }
+  const double* e2x = so + 48;
+  const double* e2y = so + 52;
+  const int r = pa.r, nx = pa.nx, ny = pa.ny;
+  const int ncell = nx * ny;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3, kk = q & 1, second = q >> 1;
+  const int mp = warp & 1, np = (warp >> 1) & 1, hf = warp >> 2;
+  const int tiles_j = (r + kT32 - 1) / kT32;
+  const int i0 = (blockIdx.x / tiles_j) * kT32, j0 = (blockIdx.x % tiles_j) * kT32;
+  const int c_begin = blockIdx.y * pa.cells_per_block;
+  const int c_end = min(ncell, c_begin + pa.cells_per_block);
+  double acc[NO][2][2][2];
+#pragma unroll
+  for (int o = 0; o < NO; ++o)
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) acc[o][a][b][0] = acc[o][a][b][1] = 0.0;
+  double qacc = 0.0;
+  const double* X = pa.X;
+  int ca[2], cb[2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    ca[a] = 8 * (2 * mp + a) + g;
+    cb[a] = 8 * (2 * np + a) + g;
+  }
+  const int side = threadIdx.x / (C * kT32);
+  const int scl = (threadIdx.x % (C * kT32)) / kT32, scol = threadIdx.x % kT32;
+  const int sgcol = (side == 0 ? i0 : j0) + scol;
+  struct Raw {
+    double x[4];
+    double y[4];  // group 0: x-left / y-below neighbour edge dofs; group 1: X_old (i-side)
+    double qc, st, ss;
+  };
+  auto fetch = [&](int cc0, Raw& w) {
+    const int c = cc0 + scl;
+    const bool live = cc0 < c_end && c < c_end;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) w.x[l] = live ? ldx(X, r, (int64_t)c * 4 + l, sgcol) : 0.0;
+    if constexpr (GROUP == 0) {
+      const int ci = c % nx, cj = c / nx;
+      const bool lx = live && ci > 0, ly = live && cj > 0;
+      w.y[0] = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 1, sgcol) : 0.0;
+      w.y[1] = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 3, sgcol) : 0.0;
+      w.y[2] = ly ? ldx(X, r, (int64_t)(c - nx) * 4 + 2, sgcol) : 0.0;
+      w.y[3] = ly ? ldx(X, r, (int64_t)(c - nx) * 4 + 3, sgcol) : 0.0;
+    } else {
+#pragma unroll
+      for (int l = 0; l < 4; ++l)
+        w.y[l] = (live && side == 0 && pa.Xold) ? ldx(pa.Xold, r, (int64_t)c * 4 + l, sgcol) : 0.0;
+      w.qc = (live && side == 1) ? __ldg(pa.q + c) : 0.0;
+      const int cs = cc0 + (int)threadIdx.x;
+      w.st = (cc0 < c_end && threadIdx.x < C && cs < c_end) ? __ldg(pa.sigma_t + cs) : 0.0;
+      w.ss = (cc0 < c_end && threadIdx.x < C && cs < c_end) ? __ldg(pa.sigma_s + cs) : 0.0;
+    }
+  };
+  Raw cur;
+  fetch(c_begin, cur);
+  for (int c0 = c_begin; c0 < c_end; c0 += C) {
+    const int nc = min(C, c_end - c0);
+    __syncthreads();  // the previous chunk's fragments are consumed
+    {
+      const double* x = cur.x;
+      const int base = scl * kRow + scol;
+      if constexpr (GROUP == 0) {
+        const double ux0 = cur.y[0] - x[0], ux1 = cur.y[1] - x[2];
+        const double vx0 = cur.y[0] + x[0], vx1 = cur.y[1] + x[2];
+        const double uy0 = cur.y[2] - x[0], uy1 = cur.y[3] - x[1];
+        const double vy0 = cur.y[2] + x[0], vy1 = cur.y[3] + x[1];
+        if (side == 0) {
+#pragma unroll
+          for (int l = 0; l < 4; ++l) sX[base + kLS * l] = x[l];
+          sU[base] = ux0;
+          sU[base + kLS] = ux1;
+          sU[base + 2 * kLS] = uy0;
+          sU[base + 3 * kLS] = uy1;
+        } else {
+#pragma unroll
+          for (int l = 0; l < 4; ++l) {
+            double gx = 0.0, gy = 0.0;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+              gx = fma(so[16 + 4 * l + p], x[p], gx);
+              gy = fma(so[32 + 4 * l + p], x[p], gy);
+            }
+            sGX[base + kLS * l] = gx;
+            sGY[base + kLS * l] = gy;
+          }
+          double* f = sF + 2 * scl * kRow + scol;
+          f[0] = 0.5 * (e2x[0] * vx0 + e2x[1] * vx1);
+          f[kLS] = 0.5 * (e2x[2] * vx0 + e2x[3] * vx1);
+          f[2 * kLS] = 0.5 * (e2y[0] * vy0 + e2y[1] * vy1);
+          f[3 * kLS] = 0.5 * (e2y[2] * vy0 + e2y[3] * vy1);
+          f[4 * kLS] = 0.5 * (e2x[0] * ux0 + e2x[1] * ux1);
+          f[5 * kLS] = 0.5 * (e2x[2] * ux0 + e2x[3] * ux1);
+          f[6 * kLS] = 0.5 * (e2y[0] * uy0 + e2y[1] * uy1);
+          f[7 * kLS] = 0.5 * (e2y[2] * uy0 + e2y[3] * uy1);
+        }
+      } else {
+        if (side == 0) {
+#pragma unroll
+          for (int l = 0; l < 4; ++l) {
+            sX[base + kLS * l] = x[l];
+            sXo[base + kLS * l] = cur.y[l];
+          }
+        } else {
+#pragma unroll
+          for (int l = 0; l < 4; ++l) {
+            double m = 0.0;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) m = fma(so[4 * l + p], x[p], m);
+            sMX[base + kLS * l] = m;
+          }
+          double sq = 0.0;
+#pragma unroll
+          for (int l = 0; l < 4; ++l) sq = fma(so[56 + l], x[l], sq);
+          sQ[scl * kT32 + scol] = cur.qc * sq;  // q-hat (dlr_sn.py:70)
+        }
+        if (threadIdx.x < C) {
+          sC[2 * threadIdx.x] = cur.st;
+          sC[2 * threadIdx.x + 1] = cur.ss;
+        }
+      }
+    }
+    __syncthreads();
+    fetch(c0 + C, cur);  // next chunk's loads in flight during the MMAs
+    // ---- volume terms: the 2 cells of this warp's half
+#pragma unroll
+    for (int k = 0; k < C / 2; ++k) {
+      const int cl = hf * (C / 2) + k;
+      double xa[2];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) xa[a] = sX[cl * kRow + q * kLS + ca[a]];
+      if constexpr (GROUP == 0) {
+        double gx[2], gy[2];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          gx[b] = sGX[cl * kRow + q * kLS + cb[b]];
+          gy[b] = sGY[cl * kRow + q * kLS + cb[b]];
+        }
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            dmma(acc[0][a][b][0], acc[0][a][b][1], xa[a], gx[b]);  // px (volume)
+            dmma(acc[1][a][b][0], acc[1][a][b][1], xa[a], gy[b]);  // py (volume)
+          }
+      } else {
+        const double stc = sC[2 * cl], ssc = sC[2 * cl + 1];
+        double xo[2], mx[2];
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          xo[a] = sXo[cl * kRow + q * kLS + ca[a]];
+          mx[a] = sMX[cl * kRow + q * kLS + cb[a]];
+        }
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          const double xs = stc * xa[a], xss = ssc * xa[a];
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            dmma(acc[0][a][b][0], acc[0][a][b][1], xs, mx[b]);     // mt
+            dmma(acc[1][a][b][0], acc[1][a][b][1], xss, mx[b]);    // ms
+            dmma(acc[2][a][b][0], acc[2][a][b][1], xo[a], mx[b]);  // mo
+          }
+        }
+      }
+    }
+    if constexpr (GROUP == 0) {
+      // ---- face terms: the cell pair of this half; k slot q -> cell cl + q / 2,
+      // face dof q % 2
+      const int cl = hf * (C / 2) + second;
+      double uxa[2], uya[2], fx[2], fy[2], fux[2], fuy[2];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        uxa[a] = sU[cl * kRow + kk * kLS + ca[a]];
+        uya[a] = sU[cl * kRow + (2 + kk) * kLS + ca[a]];
+        const double* f = sF + 2 * cl * kRow + cb[a];
+        fx[a] = f[kk * kLS];
+        fy[a] = f[(2 + kk) * kLS];
+        fux[a] = f[(4 + kk) * kLS];
+        fuy[a] = f[(6 + kk) * kLS];
+      }
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          dmma(acc[0][a][b][0], acc[0][a][b][1], uxa[a], fx[b]);   // px (faces)
+          dmma(acc[1][a][b][0], acc[1][a][b][1], uya[a], fy[b]);   // py (faces)
+          dmma(acc[2][a][b][0], acc[2][a][b][1], uxa[a], fux[b]);  // jx
+          dmma(acc[3][a][b][0], acc[3][a][b][1], uya[a], fuy[b]);  // jy
+        }
+    } else {
+      if (i0 == 0 && threadIdx.x < kT32)
+        for (int cl = 0; cl < nc; ++cl) qacc += sQ[cl * kT32 + threadIdx.x];
+    }
+  }
+  __syncthreads();  // staging planes are dead: reuse them for the reduction
+  double* red = sm32;               // [NO][32][33]: half 1's accumulators
+  double* bnd = red + NO * 32 * 33;  // [2][32][33]: right / top domain-boundary faces (group 0)
+  if constexpr (GROUP == 0) {
+    // ---- right / top domain-boundary faces (a = own right/top edge, b = 0)
+    for (int e = threadIdx.x; e < kT32 * kT32; e += blockDim.x) {
+      const int ti = e >> 5, tj = e & 31;
+      const int i = i0 + ti, j = j0 + tj;
+      double bx = 0.0, by = 0.0;
+      if (i < r && j < r) {
+        const int first_right = c_begin + ((nx - 1 - c_begin % nx) % nx + nx) % nx;
+        for (int c = first_right; c < c_end; c += nx) {
+          const int64_t r1 = (int64_t)c * 4 + 1, r3 = (int64_t)c * 4 + 3;
+          const double ai0 = ldx(X, r, r1, i), ai1 = ldx(X, r, r3, i);
+          const double aj0 = ldx(X, r, r1, j), aj1 = ldx(X, r, r3, j);
+          bx += ai0 * (0.5 * (e2x[0] * aj0 + e2x[1] * aj1)) + ai1 * (0.5 * (e2x[2] * aj0 + e2x[3] * aj1));
+        }
+        for (int c = max(c_begin, (ny - 1) * nx); c < c_end; ++c) {
+          const int64_t r2 = (int64_t)c * 4 + 2, r3 = (int64_t)c * 4 + 3;
+          const double ai0 = ldx(X, r, r2, i), ai1 = ldx(X, r, r3, i);
+          const double aj0 = ldx(X, r, r2, j), aj1 = ldx(X, r, r3, j);
+          by += ai0 * (0.5 * (e2y[0] * aj0 + e2y[1] * aj1)) + ai1 * (0.5 * (e2y[2] * aj0 + e2y[3] * aj1));
+        }
+      }
+      bnd[ti * 33 + tj] = bx;
+      bnd[32 * 33 + ti * 33 + tj] = by;
+    }
+  }
+  if (hf == 1) {
+#pragma unroll
+    for (int o = 0; o < NO; ++o)
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int row = 8 * (2 * mp + a) + g, col = 8 * (2 * np + b) + 2 * q;
+          red[(o * 32 + row) * 33 + col] = acc[o][a][b][0];
+          red[(o * 32 + row) * 33 + col + 1] = acc[o][a][b][1];
+        }
+  }
+  __syncthreads();
+  // ---- fixed-order reduction: (half 0 + half 1) + boundary
+  const int64_t stride = 7 * (int64_t)r * r + r;
+  double* out = pa.part + (int64_t)blockIdx.y * stride;
+  if (hf == 0) {
+#pragma unroll
+    for (int o = 0; o < NO; ++o)
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int row = 8 * (2 * mp + a) + g, col = 8 * (2 * np + b) + 2 * q + h;
+            const int i = i0 + row, j = j0 + col;
+            if (i >= r || j >= r) continue;
+            double v = acc[o][a][b][h] + red[(o * 32 + row) * 33 + col];
+            int slot;
+            if constexpr (GROUP == 0) {
+              if (o == 0 || o == 2) v += bnd[row * 33 + col];            // px, jx
+              if (o == 1 || o == 3) v += bnd[32 * 33 + row * 33 + col];  // py, jy
+              slot = o;  // px py jx jy
+            } else {
+              slot = 4 + o;  // mt ms mo
+            }
+            out[(int64_t)slot * r * r + (int64_t)i * r + j] = v;
+          }
+  }
+  if constexpr (GROUP == 1)
+    if (i0 == 0 && threadIdx.x < kT32 && j0 + (int)threadIdx.x < r)
+      out[7 * (int64_t)r * r + j0 + threadIdx.x] = qacc;
+}
+
+// grid (tiles, cell blocks, 2 groups): both groups in one launch, so the
+// CTAs of the two groups share the SMs and the tail of one overlaps the other
+__global__ void __launch_bounds__(256, 2) project_mma32g_kernel(ProjArgs pa, dlrsn_cellops ops) {
+  extern __shared__ __align__(16) double sm32g[];
+  if (blockIdx.z == 0)
+    project32_group<0>(pa, ops, sm32g);
+  else
+    project32_group<1>(pa, ops, sm32g);
+}
+
 // ---------------------------------------------------------------------------
 // Small dense kernels: one CTA, matrices in global memory (L2 resident).
 
@@ -2436,6 +2749,16 @@ static int cells_per_block(int ncell, int tiles) {
   return cpb < kChunk ? kChunk : cpb;
 }
 
+// cells per block of project_mma32g_kernel: about 4 waves of 2 CTAs per SM
+// over all 32x32 output tiles and both output groups, whole chunks
+static int project32g_cells_per_block(int ncell, int r) {
+  const int tiles32 = ((r + kT32 - 1) / kT32) * ((r + kT32 - 1) / kT32);
+  const int target = (4 * 2 * 148 + 2 * tiles32 - 1) / (2 * tiles32);
+  int cpb = (ncell + target - 1) / target;
+  cpb = (cpb + kPC32 - 1) / kPC32 * kPC32;
+  return cpb < kPC32 ? kPC32 : cpb;
+}
+
 // cells per block of project_mma32_kernel: one block per SM (148) over all
 // 32x32 output tiles
 static int project32_cells_per_block(int ncell, int r) {
@@ -2478,6 +2801,9 @@ int64_t dlrsn_partials_len(int ncell, int ra, int rb, int kind) {
   const int cpb32 = project32_cells_per_block(ncell, ra);
   const int64_t nblk32 = (ncell + cpb32 - 1) / cpb32;
   if (nblk32 > nblk) nblk = nblk32;
+  const int cpbg = project32g_cells_per_block(ncell, ra);
+  const int64_t nblkg = (ncell + cpbg - 1) / cpbg;
+  if (nblkg > nblk) nblk = nblkg;
   return nblk * (7 * (int64_t)ra * ra + ra);
 }
 
@@ -2576,15 +2902,40 @@ int dlrsn_project(const dlrsn_cellops* ops, int r, const double* X, const double
     const int cpb32 = project32_cells_per_block(ncell, r);
     const int nblk32 = (ncell + cpb32 - 1) / cpb32;
     pa.cells_per_block = cpb32;
-    DLRSN_TRY_CUDA(zero_async(partial, sizeof(double) * (size_t)nblk32 * (7 * (size_t)r * r + r), st));
-    DLRSN_TRY_CUDA(cudaFuncSetAttribute(project_mma32_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)kProj32Smem));
+    static const char* fused = getenv("DLRSN_PROJECT_FUSED");
     auto* tm = proj_timer();
-    if (tm) DLRSN_TRY_CUDA(cudaEventRecord(tm->first, st));
-    project_mma32_kernel<<<dim3(tiles32, nblk32), 256, kProj32Smem, st>>>(pa, *ops);
-    DLRSN_CHECK_LAUNCH("project_mma32_kernel");
-    if (tm) DLRSN_TRY_CUDA(cudaEventRecord(tm->second, st));
+    if (fused && fused[0] == '1') {
+      DLRSN_TRY_CUDA(zero_async(partial, sizeof(double) * (size_t)nblk32 * (7 * (size_t)r * r + r), st));
+      DLRSN_TRY_CUDA(cudaFuncSetAttribute(project_mma32_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)kProj32Smem));
+      if (tm) DLRSN_TRY_CUDA(cudaEventRecord(tm->first, st));
+      project_mma32_kernel<<<dim3(tiles32, nblk32), 256, kProj32Smem, st>>>(pa, *ops);
+      DLRSN_CHECK_LAUNCH("project_mma32_kernel");
+      if (tm) DLRSN_TRY_CUDA(cudaEventRecord(tm->second, st));
+    } else {
+      static bool attr = false;
+      if (!attr) {
+        DLRSN_TRY_CUDA(cudaFuncSetAttribute(project_mma32g_kernel,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)kProj32SmemG));
+        attr = true;
+      }
+      // both output groups in one grid (z = group); cell blocks of about
+      // 4 waves over 2 CTAs per SM, so the unequal group costs even out
+      const int cpbg = project32g_cells_per_block(ncell, r);
+      const int nblkg = (ncell + cpbg - 1) / cpbg;
+      pa.cells_per_block = cpbg;
+      DLRSN_TRY_CUDA(zero_async(partial, sizeof(double) * (size_t)nblkg * (7 * (size_t)r * r + r), st));
+      if (tm) DLRSN_TRY_CUDA(cudaEventRecord(tm->first, st));
+      project_mma32g_kernel<<<dim3(tiles32, nblkg, 2), 256, kProj32SmemG, st>>>(pa, *ops);
+      DLRSN_CHECK_LAUNCH("project_mma32g_kernel");
+      if (tm) DLRSN_TRY_CUDA(cudaEventRecord(tm->second, st));
+      reduce_partials_kernel<<<(unsigned)((7 * (int64_t)r * r + r + 31) / 32), 1024, 0, st>>>(
+          nblkg, 7 * (int64_t)r * r + r, partial, out, 1.0);
+      DLRSN_CHECK_LAUNCH("reduce_partials_kernel");
+      return DLRSN_OK;
+    }
     const int64_t len32 = 7 * (int64_t)r * r + r;
     reduce_partials_kernel<<<(unsigned)((len32 + 31) / 32), 1024, 0, st>>>(nblk32, len32, partial,
                                                                            out, 1.0);
