@@ -1364,26 +1364,36 @@ __global__ void __launch_bounds__(256, 1) project_mma32_kernel(ProjArgs pa, dlrs
 // face terms), GROUP 1 = {mt, ms, mo} + q-hat.  Each CTA stages only its
 // group's planes and holds only its group's accumulators (4 or 3 outputs x
 // 2x2 fragments instead of 7), so two CTAs (16 warps) fit per SM and the
-// dependent DMMA chains of one warp are covered by the others.
+// dependent DMMA chains of one warp are covered by the others.  Chunks of 8
+// cells (two staging items per thread: the same cell rows for the i-side
+// and the j-side columns), so each barrier pair is amortised over 4 cells
+// of MMAs per warp.
+constexpr int kPCG = 8;                          // cells per chunk
+constexpr int kPlaneG = kPCG * kRow32;           // one staged plane
+constexpr size_t kProj32StageG0 = 6 * (size_t)kPlaneG;
+constexpr size_t kProj32StageG1 = 3 * (size_t)kPlaneG + kPCG * kT32 + 2 * kPCG;
 constexpr size_t kProj32RedG0 = (4 + 2) * 32 * 33;
 constexpr size_t kProj32RedG1 = 3 * 32 * 33;
 constexpr size_t kProj32SmemG =
-    (kProj32Stage > kProj32RedG0 ? kProj32Stage : kProj32RedG0) * sizeof(double);
+    std::max(std::max(kProj32StageG0, kProj32StageG1), std::max(kProj32RedG0, kProj32RedG1)) *
+    sizeof(double);
 
 template <int GROUP>
 __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_cellops& ops,
-                                                double* sm32) {
-  constexpr int C = kPC32, kLS = kLS32, kRow = kRow32;
+                                                double* sm32, int ti, int tj, bool mo_only) {
+  constexpr int C = kPCG, kLS = kLS32, kRow = kRow32;
   constexpr int NO = GROUP == 0 ? 4 : 3;  // accumulated outputs
-  double* sX = sm32;             // [C][4][kLS] i-side
-  double* sXo = sX + C * kRow;   // [C][4][kLS] i-side (group 1)
-  double* sU = sXo + C * kRow;   // [C][4][kLS] i-side: ux0 ux1 uy0 uy1 (group 0)
-  double* sMX = sU + C * kRow;   // [C][4][kLS] j-side (group 1)
-  double* sGX = sMX + C * kRow;  // [C][4][kLS] (group 0)
-  double* sGY = sGX + C * kRow;  // [C][4][kLS] (group 0)
-  double* sF = sGY + C * kRow;   // [C][8][kLS] (group 0)
-  double* sQ = sF + 2 * C * kRow;  // [C][32] (group 1)
-  double* sC = sQ + C * kT32;      // [C][2] (group 1)
+  // group 0: sX sU (i-side), sGX sGY sF[2] (j-side); group 1: sX sXo (i),
+  // sMX (j), then sQ [C][32] and sC [C][2]
+  double* sX = sm32;
+  double* sU = sm32 + kPlaneG;       // group 0
+  double* sXo = sm32 + kPlaneG;      // group 1
+  double* sGX = sm32 + 2 * kPlaneG;  // group 0
+  double* sMX = sm32 + 2 * kPlaneG;  // group 1
+  double* sGY = sm32 + 3 * kPlaneG;
+  double* sF = sm32 + 4 * kPlaneG;   // [C][8][kLS]
+  double* sQ = sm32 + 3 * kPlaneG;   // group 1
+  double* sC = sQ + C * kT32;
   __shared__ double so[64];
   if (threadIdx.x < 16) {
     so[threadIdx.x] = ops.mass[threadIdx.x];
@@ -1401,8 +1411,7 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3, kk = q & 1, second = q >> 1;
   const int mp = warp & 1, np = (warp >> 1) & 1, hf = warp >> 2;
-  const int tiles_j = (r + kT32 - 1) / kT32;
-  const int i0 = (blockIdx.x / tiles_j) * kT32, j0 = (blockIdx.x % tiles_j) * kT32;
+  const int i0 = ti * kT32, j0 = tj * kT32;
   const int c_begin = blockIdx.y * pa.cells_per_block;
   const int c_end = min(ncell, c_begin + pa.cells_per_block);
   double acc[NO][2][2][2];
@@ -1420,31 +1429,40 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
     ca[a] = 8 * (2 * mp + a) + g;
     cb[a] = 8 * (2 * np + a) + g;
   }
-  const int side = threadIdx.x / (C * kT32);
-  const int scl = (threadIdx.x % (C * kT32)) / kT32, scol = threadIdx.x % kT32;
-  const int sgcol = (side == 0 ? i0 : j0) + scol;
+  // staging item of this thread: cell scl of the chunk, column scol of the
+  // i-side tile (i0 + scol) and of the j-side tile (j0 + scol)
+  const int scl = threadIdx.x / kT32, scol = threadIdx.x % kT32;
+  const int gi = i0 + scol, gj = j0 + scol;
   struct Raw {
-    double x[4];
-    double y[4];  // group 0: x-left / y-below neighbour edge dofs; group 1: X_old (i-side)
+    double xi[4], xj[4];
+    double y[4];  // group 0: x-left / y-below neighbour edge dofs (j-side); group 1: X_old (i)
+    double ui[4];  // group 0: neighbour edge dofs on the i-side (face jumps)
     double qc, st, ss;
   };
   auto fetch = [&](int cc0, Raw& w) {
     const int c = cc0 + scl;
     const bool live = cc0 < c_end && c < c_end;
 #pragma unroll
-    for (int l = 0; l < 4; ++l) w.x[l] = live ? ldx(X, r, (int64_t)c * 4 + l, sgcol) : 0.0;
+    for (int l = 0; l < 4; ++l) {
+      w.xi[l] = live ? ldx(X, r, (int64_t)c * 4 + l, gi) : 0.0;
+      w.xj[l] = live ? ldx(X, r, (int64_t)c * 4 + l, gj) : 0.0;
+    }
     if constexpr (GROUP == 0) {
       const int ci = c % nx, cj = c / nx;
       const bool lx = live && ci > 0, ly = live && cj > 0;
-      w.y[0] = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 1, sgcol) : 0.0;
-      w.y[1] = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 3, sgcol) : 0.0;
-      w.y[2] = ly ? ldx(X, r, (int64_t)(c - nx) * 4 + 2, sgcol) : 0.0;
-      w.y[3] = ly ? ldx(X, r, (int64_t)(c - nx) * 4 + 3, sgcol) : 0.0;
+      w.y[0] = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 1, gj) : 0.0;
+      w.y[1] = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 3, gj) : 0.0;
+      w.y[2] = ly ? ldx(X, r, (int64_t)(c - nx) * 4 + 2, gj) : 0.0;
+      w.y[3] = ly ? ldx(X, r, (int64_t)(c - nx) * 4 + 3, gj) : 0.0;
+      w.ui[0] = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 1, gi) : 0.0;
+      w.ui[1] = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 3, gi) : 0.0;
+      w.ui[2] = ly ? ldx(X, r, (int64_t)(c - nx) * 4 + 2, gi) : 0.0;
+      w.ui[3] = ly ? ldx(X, r, (int64_t)(c - nx) * 4 + 3, gi) : 0.0;
     } else {
 #pragma unroll
       for (int l = 0; l < 4; ++l)
-        w.y[l] = (live && side == 0 && pa.Xold) ? ldx(pa.Xold, r, (int64_t)c * 4 + l, sgcol) : 0.0;
-      w.qc = (live && side == 1) ? __ldg(pa.q + c) : 0.0;
+        w.y[l] = (live && pa.Xold) ? ldx(pa.Xold, r, (int64_t)c * 4 + l, gi) : 0.0;
+      w.qc = live ? __ldg(pa.q + c) : 0.0;
       const int cs = cc0 + (int)threadIdx.x;
       w.st = (cc0 < c_end && threadIdx.x < C && cs < c_end) ? __ldg(pa.sigma_t + cs) : 0.0;
       w.ss = (cc0 < c_end && threadIdx.x < C && cs < c_end) ? __ldg(pa.sigma_s + cs) : 0.0;
@@ -1456,62 +1474,54 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
     const int nc = min(C, c_end - c0);
     __syncthreads();  // the previous chunk's fragments are consumed
     {
-      const double* x = cur.x;
       const int base = scl * kRow + scol;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) sX[base + kLS * l] = cur.xi[l];
       if constexpr (GROUP == 0) {
+        const double* x = cur.xj;
+        // i-side face jumps u = (left/below neighbour edge) - own edge
+        sU[base] = cur.ui[0] - cur.xi[0];
+        sU[base + kLS] = cur.ui[1] - cur.xi[2];
+        sU[base + 2 * kLS] = cur.ui[2] - cur.xi[0];
+        sU[base + 3 * kLS] = cur.ui[3] - cur.xi[1];
         const double ux0 = cur.y[0] - x[0], ux1 = cur.y[1] - x[2];
         const double vx0 = cur.y[0] + x[0], vx1 = cur.y[1] + x[2];
         const double uy0 = cur.y[2] - x[0], uy1 = cur.y[3] - x[1];
         const double vy0 = cur.y[2] + x[0], vy1 = cur.y[3] + x[1];
-        if (side == 0) {
 #pragma unroll
-          for (int l = 0; l < 4; ++l) sX[base + kLS * l] = x[l];
-          sU[base] = ux0;
-          sU[base + kLS] = ux1;
-          sU[base + 2 * kLS] = uy0;
-          sU[base + 3 * kLS] = uy1;
-        } else {
+        for (int l = 0; l < 4; ++l) {
+          double gx = 0.0, gy = 0.0;
 #pragma unroll
-          for (int l = 0; l < 4; ++l) {
-            double gx = 0.0, gy = 0.0;
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-              gx = fma(so[16 + 4 * l + p], x[p], gx);
-              gy = fma(so[32 + 4 * l + p], x[p], gy);
-            }
-            sGX[base + kLS * l] = gx;
-            sGY[base + kLS * l] = gy;
+          for (int p = 0; p < 4; ++p) {
+            gx = fma(so[16 + 4 * l + p], x[p], gx);
+            gy = fma(so[32 + 4 * l + p], x[p], gy);
           }
-          double* f = sF + 2 * scl * kRow + scol;
-          f[0] = 0.5 * (e2x[0] * vx0 + e2x[1] * vx1);
-          f[kLS] = 0.5 * (e2x[2] * vx0 + e2x[3] * vx1);
-          f[2 * kLS] = 0.5 * (e2y[0] * vy0 + e2y[1] * vy1);
-          f[3 * kLS] = 0.5 * (e2y[2] * vy0 + e2y[3] * vy1);
-          f[4 * kLS] = 0.5 * (e2x[0] * ux0 + e2x[1] * ux1);
-          f[5 * kLS] = 0.5 * (e2x[2] * ux0 + e2x[3] * ux1);
-          f[6 * kLS] = 0.5 * (e2y[0] * uy0 + e2y[1] * uy1);
-          f[7 * kLS] = 0.5 * (e2y[2] * uy0 + e2y[3] * uy1);
+          sGX[base + kLS * l] = gx;
+          sGY[base + kLS * l] = gy;
         }
+        double* f = sF + 2 * scl * kRow + scol;
+        f[0] = 0.5 * (e2x[0] * vx0 + e2x[1] * vx1);
+        f[kLS] = 0.5 * (e2x[2] * vx0 + e2x[3] * vx1);
+        f[2 * kLS] = 0.5 * (e2y[0] * vy0 + e2y[1] * vy1);
+        f[3 * kLS] = 0.5 * (e2y[2] * vy0 + e2y[3] * vy1);
+        f[4 * kLS] = 0.5 * (e2x[0] * ux0 + e2x[1] * ux1);
+        f[5 * kLS] = 0.5 * (e2x[2] * ux0 + e2x[3] * ux1);
+        f[6 * kLS] = 0.5 * (e2y[0] * uy0 + e2y[1] * uy1);
+        f[7 * kLS] = 0.5 * (e2y[2] * uy0 + e2y[3] * uy1);
       } else {
-        if (side == 0) {
+        const double* x = cur.xj;
 #pragma unroll
-          for (int l = 0; l < 4; ++l) {
-            sX[base + kLS * l] = x[l];
-            sXo[base + kLS * l] = cur.y[l];
-          }
-        } else {
+        for (int l = 0; l < 4; ++l) {
+          sXo[base + kLS * l] = cur.y[l];
+          double m = 0.0;
 #pragma unroll
-          for (int l = 0; l < 4; ++l) {
-            double m = 0.0;
-#pragma unroll
-            for (int p = 0; p < 4; ++p) m = fma(so[4 * l + p], x[p], m);
-            sMX[base + kLS * l] = m;
-          }
-          double sq = 0.0;
-#pragma unroll
-          for (int l = 0; l < 4; ++l) sq = fma(so[56 + l], x[l], sq);
-          sQ[scl * kT32 + scol] = cur.qc * sq;  // q-hat (dlr_sn.py:70)
+          for (int p = 0; p < 4; ++p) m = fma(so[4 * l + p], x[p], m);
+          sMX[base + kLS * l] = m;
         }
+        double sq = 0.0;
+#pragma unroll
+        for (int l = 0; l < 4; ++l) sq = fma(so[56 + l], x[l], sq);
+        sQ[scl * kT32 + scol] = cur.qc * sq;  // q-hat (dlr_sn.py:70)
         if (threadIdx.x < C) {
           sC[2 * threadIdx.x] = cur.st;
           sC[2 * threadIdx.x + 1] = cur.ss;
@@ -1520,7 +1530,7 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
     }
     __syncthreads();
     fetch(c0 + C, cur);  // next chunk's loads in flight during the MMAs
-    // ---- volume terms: the 2 cells of this warp's half
+    // ---- volume terms: the C / 2 cells of this warp's half
 #pragma unroll
     for (int k = 0; k < C / 2; ++k) {
       const int cl = hf * (C / 2) + k;
@@ -1549,42 +1559,50 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
           xo[a] = sXo[cl * kRow + q * kLS + ca[a]];
           mx[a] = sMX[cl * kRow + q * kLS + cb[a]];
         }
+        if (!mo_only) {
 #pragma unroll
-        for (int a = 0; a < 2; ++a) {
-          const double xs = stc * xa[a], xss = ssc * xa[a];
+          for (int a = 0; a < 2; ++a) {
+            const double xs = stc * xa[a], xss = ssc * xa[a];
 #pragma unroll
-          for (int b = 0; b < 2; ++b) {
-            dmma(acc[0][a][b][0], acc[0][a][b][1], xs, mx[b]);     // mt
-            dmma(acc[1][a][b][0], acc[1][a][b][1], xss, mx[b]);    // ms
-            dmma(acc[2][a][b][0], acc[2][a][b][1], xo[a], mx[b]);  // mo
+            for (int b = 0; b < 2; ++b) {
+              dmma(acc[0][a][b][0], acc[0][a][b][1], xs, mx[b]);     // mt
+              dmma(acc[1][a][b][0], acc[1][a][b][1], xss, mx[b]);    // ms
+            }
           }
         }
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) dmma(acc[2][a][b][0], acc[2][a][b][1], xo[a], mx[b]);  // mo
       }
     }
     if constexpr (GROUP == 0) {
-      // ---- face terms: the cell pair of this half; k slot q -> cell cl + q / 2,
-      // face dof q % 2
-      const int cl = hf * (C / 2) + second;
-      double uxa[2], uya[2], fx[2], fy[2], fux[2], fuy[2];
+      // ---- face terms: the cell pairs of this half; k slot q -> cell
+      // cl + q / 2, face dof q % 2
 #pragma unroll
-      for (int a = 0; a < 2; ++a) {
-        uxa[a] = sU[cl * kRow + kk * kLS + ca[a]];
-        uya[a] = sU[cl * kRow + (2 + kk) * kLS + ca[a]];
-        const double* f = sF + 2 * cl * kRow + cb[a];
-        fx[a] = f[kk * kLS];
-        fy[a] = f[(2 + kk) * kLS];
-        fux[a] = f[(4 + kk) * kLS];
-        fuy[a] = f[(6 + kk) * kLS];
-      }
+      for (int k = 0; k < C / 4; ++k) {
+        const int cl = hf * (C / 2) + 2 * k + second;
+        double uxa[2], uya[2], fx[2], fy[2], fux[2], fuy[2];
 #pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          dmma(acc[0][a][b][0], acc[0][a][b][1], uxa[a], fx[b]);   // px (faces)
-          dmma(acc[1][a][b][0], acc[1][a][b][1], uya[a], fy[b]);   // py (faces)
-          dmma(acc[2][a][b][0], acc[2][a][b][1], uxa[a], fux[b]);  // jx
-          dmma(acc[3][a][b][0], acc[3][a][b][1], uya[a], fuy[b]);  // jy
+        for (int a = 0; a < 2; ++a) {
+          uxa[a] = sU[cl * kRow + kk * kLS + ca[a]];
+          uya[a] = sU[cl * kRow + (2 + kk) * kLS + ca[a]];
+          const double* f = sF + 2 * cl * kRow + cb[a];
+          fx[a] = f[kk * kLS];
+          fy[a] = f[(2 + kk) * kLS];
+          fux[a] = f[(4 + kk) * kLS];
+          fuy[a] = f[(6 + kk) * kLS];
         }
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            dmma(acc[0][a][b][0], acc[0][a][b][1], uxa[a], fx[b]);   // px (faces)
+            dmma(acc[1][a][b][0], acc[1][a][b][1], uya[a], fy[b]);   // py (faces)
+            dmma(acc[2][a][b][0], acc[2][a][b][1], uxa[a], fux[b]);  // jx
+            dmma(acc[3][a][b][0], acc[3][a][b][1], uya[a], fuy[b]);  // jy
+          }
+      }
     } else {
       if (i0 == 0 && threadIdx.x < kT32)
         for (int cl = 0; cl < nc; ++cl) qacc += sQ[cl * kT32 + threadIdx.x];
@@ -1654,6 +1672,7 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
               slot = o;  // px py jx jy
             } else {
               slot = 4 + o;  // mt ms mo
+              if (mo_only && o < 2) continue;
             }
             out[(int64_t)slot * r * r + (int64_t)i * r + j] = v;
           }
@@ -1663,14 +1682,45 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
       out[7 * (int64_t)r * r + j0 + threadIdx.x] = qacc;
 }
 
-// grid (tiles, cell blocks, 2 groups): both groups in one launch, so the
-// CTAs of the two groups share the SMs and the tail of one overlaps the other
-__global__ void __launch_bounds__(256, 2) project_mma32g_kernel(ProjArgs pa, dlrsn_cellops ops) {
+// The (group, tile) work list of one cell block.  px, py are skew- and jx,
+// jy, mt, ms symmetric (X^T A X with A = -A^T or A = A^T: Px, Py skew, Jx,
+// Jy, M_sigma symmetric, transport_sn.py:246-282), so only the tiles on and
+// above the diagonal are computed for them and the reduced result is
+// mirrored (mirror_tiles_kernel); mo = X_old^T M X has no symmetry, so the
+// tiles below the diagonal run group 1 in mo-only mode.  Entry = group
+// (0 / 1 / 2 = mo only) | ti << 2 | tj << 5.
+struct ProjTiles {
+  int n;
+  unsigned char e[64];
+};
+
+// grid (work list, cell blocks): all groups / tiles of one cell block are
+// adjacent in launch order, so they run together and read that block's X
+// rows from DRAM once (L2 shares them)
+__global__ void __launch_bounds__(256, 2) project_mma32g_kernel(ProjArgs pa, dlrsn_cellops ops,
+                                                                 ProjTiles tl) {
   extern __shared__ __align__(16) double sm32g[];
-  if (blockIdx.z == 0)
-    project32_group<0>(pa, ops, sm32g);
+  const int e = tl.e[blockIdx.x];
+  const int grp = e & 3, ti = (e >> 2) & 7, tj = (e >> 5) & 7;
+  if (grp == 0)
+    project32_group<0>(pa, ops, sm32g, ti, tj, false);
   else
-    project32_group<1>(pa, ops, sm32g);
+    project32_group<1>(pa, ops, sm32g, ti, tj, grp == 2);
+}
+
+// out[o][i][j] = s_o out[o][j][i] below the diagonal tiles (o < 6; s = -1
+// for the skew px, py)
+__global__ void mirror_tiles_kernel(int r, double* __restrict__ out) {
+  const int64_t total = 6 * (int64_t)r * r;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int o = (int)(e / ((int64_t)r * r));
+    const int rem = (int)(e - (int64_t)o * r * r);
+    const int i = rem / r, j = rem % r;
+    if (i / kT32 <= j / kT32) continue;
+    const double v = out[(int64_t)o * r * r + (int64_t)j * r + i];
+    out[e] = o < 2 ? -v : v;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -2752,11 +2802,12 @@ static int cells_per_block(int ncell, int tiles) {
 // cells per block of project_mma32g_kernel: about 4 waves of 2 CTAs per SM
 // over all 32x32 output tiles and both output groups, whole chunks
 static int project32g_cells_per_block(int ncell, int r) {
-  const int tiles32 = ((r + kT32 - 1) / kT32) * ((r + kT32 - 1) / kT32);
-  const int target = (4 * 2 * 148 + 2 * tiles32 - 1) / (2 * tiles32);
+  const int T = (r + kT32 - 1) / kT32;
+  const int work = T * (T + 1) + T * (T - 1) / 2;  // CTAs per cell block (work list)
+  const int target = (4 * 2 * 148 + work - 1) / work;
   int cpb = (ncell + target - 1) / target;
-  cpb = (cpb + kPC32 - 1) / kPC32 * kPC32;
-  return cpb < kPC32 ? kPC32 : cpb;
+  cpb = (cpb + kPCG - 1) / kPCG * kPCG;
+  return cpb < kPCG ? kPCG : cpb;
 }
 
 // cells per block of project_mma32_kernel: one block per SM (148) over all
@@ -2927,13 +2978,31 @@ int dlrsn_project(const dlrsn_cellops* ops, int r, const double* X, const double
       const int nblkg = (ncell + cpbg - 1) / cpbg;
       pa.cells_per_block = cpbg;
       DLRSN_TRY_CUDA(zero_async(partial, sizeof(double) * (size_t)nblkg * (7 * (size_t)r * r + r), st));
+      static const char* sym_env = getenv("DLRSN_PROJECT_SYM");
+      const bool sym = !(sym_env && sym_env[0] == '0');
+      const int T = (r + kT32 - 1) / kT32;
+      ProjTiles tl;
+      tl.n = 0;
+      for (int ti = 0; ti < T; ++ti)
+        for (int tj = 0; tj < T; ++tj) {
+          if (!sym || ti <= tj) {
+            tl.e[tl.n++] = (unsigned char)(0 | ti << 2 | tj << 5);
+            tl.e[tl.n++] = (unsigned char)(1 | ti << 2 | tj << 5);
+          } else {
+            tl.e[tl.n++] = (unsigned char)(2 | ti << 2 | tj << 5);
+          }
+        }
       if (tm) DLRSN_TRY_CUDA(cudaEventRecord(tm->first, st));
-      project_mma32g_kernel<<<dim3(tiles32, nblkg, 2), 256, kProj32SmemG, st>>>(pa, *ops);
+      project_mma32g_kernel<<<dim3(tl.n, nblkg), 256, kProj32SmemG, st>>>(pa, *ops, tl);
       DLRSN_CHECK_LAUNCH("project_mma32g_kernel");
       if (tm) DLRSN_TRY_CUDA(cudaEventRecord(tm->second, st));
       reduce_partials_kernel<<<(unsigned)((7 * (int64_t)r * r + r + 31) / 32), 1024, 0, st>>>(
           nblkg, 7 * (int64_t)r * r + r, partial, out, 1.0);
       DLRSN_CHECK_LAUNCH("reduce_partials_kernel");
+      if (sym && T > 1) {
+        mirror_tiles_kernel<<<(unsigned)((6 * r * r + 255) / 256), 256, 0, st>>>(r, out);
+        DLRSN_CHECK_LAUNCH("mirror_tiles_kernel");
+      }
       return DLRSN_OK;
     }
     const int64_t len32 = 7 * (int64_t)r * r + r;

@@ -386,37 +386,78 @@ def test_deim_cluster_rank_deficient_raises():
     assert err.value.column == 4
 
 
-@pytest.mark.parametrize("per_block,r,n_polar,n_azimuthal", [(4, 64, 8, 16), (3, 40, 6, 12)])
-def test_wide_rank_steps_match_oracle(per_block, r, n_polar, n_azimuthal):
+def _wide_spec(kind, size, r, n_polar, n_azimuthal):
+    from paper_2601_18705_b200 import problems
+
+    if kind == "rm":  # BASELINE config 4's medium at a reduced size
+        spec, fields = problems.random_medium(n=size, rank=r, n_polar=n_polar,
+                                              n_azimuthal=n_azimuthal, n_steps=2, seed=13)
+        rng = np.random.default_rng(spec.seed)
+        problems.draw_factors(spec, rng)
+        fields(rng)
+        return spec
+    return problems.checkerboard(size, rank=r, n_polar=n_polar, n_azimuthal=n_azimuthal,
+                                 seed=13, n_steps=2)
+
+
+def _oracle_sensitivity(spec, X, W, ref, eps=1e-14):
+    """Round-off floor of the problem itself: the oracle rerun from X
+    perturbed by eps (relative, seeded) -- how far two CPU runs that differ
+    only in round-off drift apart after each step."""
+    from oracle import port as P
+    from oracle import runner as R
+
+    Xp = X * (1.0 + eps * np.random.default_rng(0).standard_normal(X.shape))
+    alt = []
+    R.run(spec, R.initial_state(spec, Xp, W), 2, record=lambda s, i, t: alt.append((s, i, t)))
+    return [max(rel_l2(ai.phi, ri.phi), rel_l2(at, rt),
+                P.lowrank_rel_diff(as_.X, as_.S, as_.W, rs.X, rs.S, rs.W))
+            for (rs, ri, rt), (as_, ai, at) in zip(ref, alt)]
+
+
+@pytest.mark.parametrize("kind,size,r,n_polar,n_azimuthal",
+                         [("rm", 48, 64, 16, 16), ("rm", 40, 40, 8, 12), ("cb", 4, 64, 8, 16),
+                          ("cb", 3, 40, 6, 12)])
+def test_wide_rank_steps_match_oracle(kind, size, r, n_polar, n_azimuthal):
     """Ranks above 32 take the wide kernels (rowmix_wide, mgram_wide with 32-
-    and 64-wide blocks, the row-block angular CholQR2, cluster DEIM): two
-    native steps against the oracle at 1e-11."""
+    and 64-wide blocks, the symmetric-tile K3, the row-block angular
+    CholQR2, cluster DEIM): two native steps against the oracle, 1e-11 on
+    phi, T and X S W^T at every step.
+
+    The small checkerboards at r >= 40 are ill-conditioned (r close to the
+    number of distinct angular modes the 6x12 / 8x16 quadrature resolves):
+    measured here, a 1e-14 relative perturbation of X moves the oracle's own
+    second step by up to ~1e-10 (scripts/ref_sensitivity.py found 4.6e-10
+    between the reference and the oracle, both CPU).  For those the bound
+    after step 1 is max(1e-11, 10 x that measured CPU-vs-CPU floor); the
+    random-medium cases (config 4's medium) are well conditioned (floor
+    ~1e-13) and are held to 1e-11 flat."""
     from oracle import port as P
     from oracle import runner as R
     from paper_2601_18705_b200 import problems
     from paper_2601_18705_b200.driver import DeviceProblem, initial_state, run
 
-    spec = problems.checkerboard(per_block, rank=r, n_polar=n_polar, n_azimuthal=n_azimuthal,
-                                 seed=13, n_steps=2)
+    spec = _wide_spec(kind, size, r, n_polar, n_azimuthal)
     rng = np.random.default_rng(spec.seed)
     Xr, Wr = problems.draw_factors(spec, rng)
     X, W = R.orthonormal_factors(spec, Xr, Wr)
     ref = []
     R.run(spec, R.initial_state(spec, X, W), 2, record=lambda s, i, t: ref.append((s, i, t)))
+    floor = _oracle_sensitivity(spec, X, W, ref)
     dp = DeviceProblem.from_spec(spec)
     got = []
     run(dp, initial_state(dp, X=X, W=W), 2, si_tol=1e-12, si_max_iters=400,
         record=lambda s, i, t: got.append((s, i, _np(t).copy())))
     for k, ((rs, ri, rt), (gs, gi, gt)) in enumerate(zip(ref, got)):
+        tol = 1e-11 if (kind == "rm" or k == 0) else max(1e-11, 10.0 * floor[k])
+        if kind == "rm":
+            assert floor[k] <= 1e-12, (k, floor[k])  # the case is as well conditioned as claimed
         assert list(gi.angle_indices) == list(ri.angle_indices), k
         assert gi.iterations == ri.iterations, k
-        assert rel_l2(_np(gi.phi), ri.phi) <= 1e-11, k
-        assert rel_l2(gt, rt) <= 1e-11, k
+        assert rel_l2(_np(gi.phi), ri.phi) <= tol, (k, tol)
+        assert rel_l2(gt, rt) <= tol, (k, tol)
         X2, S2, W2 = gs.to_numpy()
-        # the state itself is ill-conditioned here (columns retaining ~1e-6 of
-        # their norm): the reference and the oracle, both CPU, already differ
-        # by up to 4.6e-10 after one step (scripts/ref_sensitivity.py)
-        assert P.lowrank_rel_diff(X2, S2, W2, rs.X, rs.S, rs.W) <= (1e-11 if k == 0 else 1e-9), k
+        assert P.lowrank_rel_diff(X2, S2, W2, rs.X, rs.S, rs.W) <= tol, (k, tol)
 
 
 @pytest.mark.parametrize("gs_method", ["cholqr2", "cgs2"])
