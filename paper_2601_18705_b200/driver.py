@@ -205,14 +205,21 @@ def run(dp, state, n_steps, *, si_tol=1e-8, si_max_iters=200, check_state=True, 
 
 
 def run_sn(dp, n_steps, *, si_tol=1e-8, si_max_iters=200, use_dsa=True, dsa_penalty="simplified",
-           T=None, record=None, diagnostics=None, comm=None):
+           T=None, record=None, diagnostics=None, comm=None, dedup=True):
     """The reference driver's full discrete-ordinates method ("sn",
     driver.py:463-466, 492-504): psi0 = B(T0) on every quadrature node, then
     per step the source iteration over ALL directions with the previous
     intensity as psi_time (sweeps grouped DW directions per warp), the
     temperature update and the floor.  psi (n_dofs x N_Omega) stays on the
     device.  Returns (psi, phi, T, iterations per step); ``diagnostics``
-    as in ``run``."""
+    as in ``run``.
+
+    ``dedup`` (z-mirror deduplication): psi0 is isotropic, so
+    nodes with equal (omega_x, omega_y) start equal, sweep the same operator
+    (omega_z does not enter, transport_sn.py:143) with equal rhs, and stay
+    bitwise equal every step; only the distinct pairs (half the nodes) are
+    swept, with summed closure weights, and psi is expanded to every node
+    on output."""
     from . import transport
     from .physics import planck, update_temperature
 
@@ -220,9 +227,18 @@ def run_sn(dp, n_steps, *, si_tol=1e-8, si_max_iters=200, use_dsa=True, dsa_pena
     quad = dp.quad
     T = as_device(spec.T0 if T is None else T).clone()
     b0, _ = planck(T.repeat_interleave(4), dp.constants)
-    psi = b0[:, None].repeat(1, quad.n_angles).contiguous()
-    w = torch.as_tensor(np.array(quad.weights, dtype=float), device=device())
+    w_full = np.array(quad.weights, dtype=float)
+    if dedup:
+        om_sw, w_sw, inv = transport.dedup_mirrors(quad.omegas, w_full)
+        inv_dev = torch.as_tensor(inv, device=device())
+    else:
+        om_sw, w_sw, inv_dev = quad.omegas, w_full, None
+    psi = b0[:, None].repeat(1, om_sw.shape[0]).contiguous()
+    w = torch.as_tensor(w_sw, device=device())
     phi = psi @ w
+
+    def expand(p):
+        return p if inv_dev is None else p[:, inv_dev]
     ledger = None
     if diagnostics is not None:
         from .diagnostics import EnergyLedger, outflow_dense
@@ -232,7 +248,7 @@ def run_sn(dp, n_steps, *, si_tol=1e-8, si_max_iters=200, use_dsa=True, dsa_pena
     for step_no in range(1, n_steps + 1):
         lin = dp.linearized(T)
         ops = transport.assemble_operators(dp.grid, lin, dsa_penalty=dsa_penalty)
-        res = transport.source_iteration(ops, quad.omegas, quad.weights, psi_time=psi,
+        res = transport.source_iteration(ops, om_sw, w_sw, psi_time=psi,
                                          use_dsa=use_dsa, tol=si_tol, max_iters=si_max_iters,
                                          phi_start=phi, inflow=spec.inflow, comm=comm)
         psi, phi = res.psi, res.phi
@@ -241,7 +257,7 @@ def run_sn(dp, n_steps, *, si_tol=1e-8, si_max_iters=200, use_dsa=True, dsa_pena
         iters.append(res.iterations)
         if ledger is not None:
             diagnostics.append(ledger.row(step_no, res.iterations, 0.0, T, raw, psi @ w,
-                                          outflow_dense(dp.grid, psi, quad)))
+                                          outflow_dense(dp.grid, expand(psi), quad)))
         if record is not None:
-            record(psi, phi, T, res.iterations)
-    return psi, phi, T, iters
+            record(expand(psi), phi, T, res.iterations)
+    return expand(psi), phi, T, iters

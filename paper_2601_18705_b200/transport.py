@@ -244,7 +244,38 @@ def _sweep(ops, plan, rhs_sk, psi_sk, scat_sk4=None, phi_part=None, max_ctas=0):
         SWEEP_EVENTS.append((ev[0], ev[1], ops.grid.n_cells, plan.D, plan.G))
 
 
-def closure_sweep(ops, omegas, closure, rhs, *, scat_phi=None, dw=4, ws_limit=8 << 30):
+def mirror_pairs(omegas):
+    """z-mirror deduplication ("we need only
+    solving for half the angles" in xy geometry): omega_z does not enter a
+    2-D sweep, and the reference keys its per-direction operators on
+    (omega_x, omega_y) (transport_sn.py:143), so nodes with bitwise-equal
+    (omega_x, omega_y) sweep the same operator.  Returns (first index of each
+    distinct pair, in node order; the pair index of every node)."""
+    om = np.ascontiguousarray(np.asarray(omegas, dtype=float)[:, :2])
+    key = om.view(np.dtype((np.void, om.dtype.itemsize * 2))).ravel()
+    _, first, inverse = np.unique(key, return_index=True, return_inverse=True)
+    order = np.argsort(first, kind="stable")  # distinct pairs in node order
+    rank = np.empty_like(order)
+    rank[order] = np.arange(order.size)
+    return first[order], rank[inverse.ravel()]
+
+
+def dedup_mirrors(omegas, closure):
+    """(omegas of the distinct (omega_x, omega_y) pairs, their summed closure
+    weights, pair index per node): the sweep of a z-symmetric problem (every
+    node's rhs depends on (omega_x, omega_y) only) gives mirrored nodes the
+    same psi, so one sweep per pair with the summed weight has the same
+    closure flux (to round-off of the weight sum)."""
+    om = np.asarray(omegas, dtype=float)
+    clo = np.asarray(closure, dtype=float)
+    first, inv = mirror_pairs(om)
+    w = np.zeros(first.size)
+    np.add.at(w, inv, clo)
+    return om[first], w, inv
+
+
+def closure_sweep(ops, omegas, closure, rhs, *, scat_phi=None, dw=4, ws_limit=8 << 30,
+                  dedup=True):
     """One sweep of many directions that all see the same rhs, returning only
     the closure phi = sum_d closure_d psi_d (transport_sn.py:303-322 per
     direction, psi @ closure of :438) -- psi is never stored.  This is the
@@ -255,13 +286,18 @@ def closure_sweep(ops, omegas, closure, rhs, *, scat_phi=None, dw=4, ws_limit=8 
     M (sigma_s phi) / 4 pi.  Groups of ``dw`` directions add their closure
     sums with fp64 atomics (dlrsn_sweep_closure), so phi is reproducible to
     round-off only; the groups are launched in batches whose strip-handoff
-    workspace stays under ``ws_limit`` bytes."""
+    workspace stays under ``ws_limit`` bytes.  Every direction sees the same
+    rhs, so z-mirrored nodes have the same psi: with ``dedup`` each distinct
+    (omega_x, omega_y) is swept once with the summed closure weight (half of
+    a product quadrature's nodes)."""
     g = ops.grid
     st = ops.step
     om = np.asarray(omegas.cpu() if isinstance(omegas, torch.Tensor) else omegas, dtype=float)
     clo = np.asarray(closure.cpu() if isinstance(closure, torch.Tensor) else closure, dtype=float)
     if clo.shape != (om.shape[0],):
         raise ContractViolation("closure vector must have one entry per swept angle")
+    if dedup:
+        om, clo, _ = dedup_mirrors(om, clo)
     vl = ops.vec_len
     rhs = as_device(rhs).reshape(g.n_dofs, 1)
     cols = rhs.expand(-1, 4).contiguous()  # the same rhs in the 4 quadrant orientations

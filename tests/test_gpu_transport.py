@@ -288,11 +288,13 @@ def test_dsa_step_collocation_matches_reference(golden):
     assert np.abs(_np(new.X) - g["cold_newX"]).max() <= 1e-12
 
 
+@pytest.mark.parametrize("dedup", [True, False])
 @pytest.mark.parametrize("nx,ny,npol,naz,dw", [(40, 70, 4, 8, 8), (33, 29, 2, 6, 2), (70, 40, 4, 8, 1)])
-def test_closure_sweep_matches_oracle(nx, ny, npol, naz, dw):
+def test_closure_sweep_matches_oracle(nx, ny, npol, naz, dw, dedup):
     """Config 5's closure-only full-SN sweep (psi never stored, closure sums
-    added with fp64 atomics): phi against the oracle's sweeps of every
-    direction with the shared rhs, to round-off (the atomic order varies)."""
+    added with fp64 atomics): phi against the oracle's sweeps of EVERY
+    direction with the shared rhs, to round-off (the atomic order varies);
+    with ``dedup`` only the distinct (omega_x, omega_y) pairs are swept."""
     from oracle import port as P
     from paper_2601_18705_b200 import transport as Tr
     from paper_2601_18705_b200.angular import build_quadrature
@@ -307,7 +309,8 @@ def test_closure_sweep_matches_oracle(nx, ny, npol, naz, dw):
     ops = Tr.assemble_operators(grid, _manual_step(n, sig, 0 * sig, q, 1.0))
     psi_old = rng.uniform(0, 1, 4 * n)  # isotropic previous intensity
     rhs = ops.source_vector(q) + 1.0 * ops.mass_apply(psi_old)
-    phi = Tr.closure_sweep(ops, quad.omegas, quad.weights, rhs, dw=dw, ws_limit=1 << 13)
+    phi = Tr.closure_sweep(ops, quad.omegas, quad.weights, rhs, dw=dw, ws_limit=1 << 13,
+                           dedup=dedup)
     pg = P.Grid(nx, ny, 0.0, 0.0, float(nx), float(ny))
     pops = P.assemble_operators(pg, P.Step(sig, 0 * sig, sig - 1.0, q, np.zeros(n), np.ones(n),
                                            np.ones(n), 1.0, 1.0))

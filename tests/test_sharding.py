@@ -130,3 +130,23 @@ def test_allgather_columns_places_uneven_shards():
         mp.spawn(_gather_check, args=(2, _free_port(), out), nprocs=2, join=True)
         r = np.load(out)
         assert bool(r["ok"]) and float(r["mx"]) == 2.0
+
+
+def test_mirror_pairs_halve_product_quadratures():
+    """z-mirror dedup (transport.mirror_pairs): a Gauss-Legendre x uniform
+    azimuth product set has exactly two nodes per (omega_x, omega_y), the
+    pair index maps every node onto a pair with bitwise-equal components,
+    and the summed closure weights keep the total (4 pi)."""
+    import numpy as np
+
+    from paper_2601_18705_b200.angular import build_quadrature
+    from paper_2601_18705_b200.transport import dedup_mirrors, mirror_pairs
+
+    for n in (4, 16, 32, 128):
+        q = build_quadrature(n, n)
+        first, inv = mirror_pairs(q.omegas)
+        assert first.size * 2 == q.n_angles
+        assert np.array_equal(q.omegas[first[inv], :2], q.omegas[:, :2])
+        assert np.all(np.diff(first) > 0)
+        om, w, inv2 = dedup_mirrors(q.omegas, q.weights)
+        assert np.array_equal(inv, inv2) and abs(w.sum() - 4 * np.pi) <= 1e-12
