@@ -375,7 +375,7 @@ def main(argv=None):
     ap.add_argument("--ref-budget", type=float, default=150.0,
                     help="seconds of port step time for --impl reference (at least one step)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0: same as --steps (max 10)")
-    ap.add_argument("--more-configs", default="C2,C3,C5dlr,C5",
+    ap.add_argument("--more-configs", default="C2,C3,C5step,C5dlr,C5",
                     help="also measure these at N=1 ('' = none)")
     args = ap.parse_args(argv)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -630,6 +630,8 @@ def measure_config(name, steps=6, warmup=4):
         return measure_c5_sweep()
     if name == "C5dlr":
         return measure_c5_dlr_sweep()
+    if name == "C5step":
+        return measure_c5_dlr_step()
     spec = make_spec(name)
     dp = DeviceProblem.from_spec(spec)
     state = initial_state(dp)
@@ -664,6 +666,50 @@ def measure_config(name, steps=6, warmup=4):
                      "achieved_GBs": alg / (sweep_ms * 1e-3) / 1e9,
                      "frac_of_hbm": alg / (sweep_ms * 1e-3) / 1e9 / peak}}
     del state, lin, T, dp, flush
+    torch.cuda.empty_cache()
+    return out
+
+
+def measure_c5_dlr_step(steps=2, warmup=1):
+    """Config 5's DLR step on ONE GPU (4096^2, r = 128 of 128x128 directions,
+    pure absorber): the memory-lean engine (lean.py: chunked in-place sweeps,
+    in-place CholQR2; X and X_new are 68.7 GB each) plus the T update, from
+    device-generated seeded orthonormal factors (initial_state_device).  One
+    sweep per step (sigma_s = 0), so cell-angle updates per step = N_c r."""
+    import torch
+
+    from paper_2601_18705_b200 import problems
+    from paper_2601_18705_b200.driver import DeviceProblem, initial_state_device
+
+    spec, fields = problems.stress()
+    fields(np.random.default_rng(spec.seed))
+    dp = DeviceProblem.from_spec(spec)
+    torch.cuda.reset_peak_memory_stats()
+    state = initial_state_device(dp)
+    T = torch.as_tensor(spec.T0, device="cuda").clone()
+    lin = dp.linearized(T)
+    for _ in range(warmup):
+        state, lin, T, info = dp.step(state, lin, T, si_tol=1e-8, engine="lean")
+    torch.cuda.synchronize()
+    per = []
+    for _ in range(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        state, lin, T, info = dp.step(state, lin, T, si_tol=1e-8, engine="lean")
+        e1.record()
+        torch.cuda.synchronize()
+        per.append(e0.elapsed_time(e1))
+    ms = float(np.mean(per))
+    out = {"workload": "C5 stress 4096x4096, r=128 of 128x128 directions, dlr-sn step (lean "
+                       "engine, one GPU)",
+           "steps": steps, "warmup": warmup, "ms_per_step": ms,
+           "ms_per_step_each": [round(x, 1) for x in per],
+           "dlr_steps_per_s": 1e3 / ms,
+           "cell_angle_per_s": spec.n_cells * spec.rank / (ms * 1e-3),
+           "peak_hbm_GB": torch.cuda.max_memory_allocated() / 1e9,
+           "T_checksum": float(T.sum()),
+           "note": "factors drawn on the device (torch CUDA generator, seed 5), not numpy"}
+    del state, lin, T, dp
     torch.cuda.empty_cache()
     return out
 

@@ -156,8 +156,18 @@ def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, 
     """
     if gs_method not in ("cholqr2", "cgs2"):
         raise ConfigurationError(f"unknown gs_method {gs_method!r}")
-    if engine not in ("native", "python"):
+    if engine not in ("native", "python", "lean"):
         raise ConfigurationError(f"unknown engine {engine!r}")
+    if engine == "lean":  # pure absorbers at config-5 size (lean.py)
+        if use_dsa or inflow_values(inflow) is not None or comm is not None or _advance is not None \
+                or gs_method != "cholqr2":
+            raise ConfigurationError("the lean engine takes pure absorbers without DSA, inflow, "
+                                     "sharding or the fused step boundary (CholQR2 only)")
+        from .lean import step_lean
+
+        return step_lean(grid, step, quad, state, si_tol=si_tol, si_max_iters=si_max_iters,
+                         check_state=check_state, angle_indices=angle_indices,
+                         deim_tie_tol=deim_tie_tol)
     if (engine == "native" and not use_dsa and not state.W.pinned
             and state.rank <= _lib.MAX_RANK and (sweep_dw or 1) == 1
             and (comm is None or comm.world_size <= 8)):

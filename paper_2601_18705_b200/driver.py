@@ -92,7 +92,7 @@ class DeviceProblem:
 
 
     def step(self, state, lin, T, *, si_tol=1e-8, si_max_iters=200, check_state=True,
-             gs_method="cholqr2", comm=None):
+             gs_method="cholqr2", comm=None, engine="native"):
         """One DLR step and the step boundary (T update + re-linearisation)
         in a single native call (the fused form of step_collocation +
         advance, driver.py:486-487,532-534).  Returns (state, next
@@ -100,11 +100,11 @@ class DeviceProblem:
         step that raises leaves the caller's state as it was."""
         from .dlr_sn import step_collocation
 
-        if self.spec.frozen:
+        if self.spec.frozen or engine != "native":
             state, info = step_collocation(self.grid, lin, self.quad, state, si_tol=si_tol,
                                            si_max_iters=si_max_iters, use_dsa=False,
                                            check_state=check_state, gs_method=gs_method,
-                                           comm=comm, inflow=self.spec.inflow)
+                                           comm=comm, inflow=self.spec.inflow, engine=engine)
             T = T.clone()
             return state, self.advance(lin, info.phi, T), T, info
         n = self.spec.n_cells
@@ -159,6 +159,38 @@ def initial_state(dp, X=None, W=None, seed=None, T=None):
     b0 = b0.repeat_interleave(4).reshape(-1, 1)
     xb = mass_gram(cellops_struct(dp.grid), X, b0)[:, 0]
     S = torch.outer(xb, W.beta)
+    return DlrState(X=X, S=S, W=W)
+
+
+def initial_state_device(dp, seed=None, block_rows=1 << 22):
+    """Seeded random-orthonormal factors generated on the device, for sizes
+    whose N_x x r draw does not fit host memory comfortably (config 5: X is
+    68.7 GB): X ~ N(0, 1) from a CUDA generator seeded with the config seed,
+    M-orthonormalised by two in-place Cholesky-QR passes (a Gaussian block is
+    well conditioned); W from numpy's default_rng(seed) and the weighted
+    orthonormalisation; S = (X^T M b0) beta^T as in ``initial_state``.  The
+    draws differ from ``initial_state``'s host draws (stated in the bench)."""
+    from .lean import rowmix_inplace
+    from .lowrank import _chol
+
+    spec = dp.spec
+    seed = spec.seed if seed is None else seed
+    co = cellops_struct(dp.grid)
+    gen = torch.Generator(device=device()).manual_seed(int(seed))
+    X = torch.randn(spec.n_dofs, spec.rank, dtype=torch.float64, device=device(), generator=gen)
+    for _ in range(2):
+        _, Rinv, _, flag = _chol(mass_gram(co, X))
+        rowmix_inplace(X, Rinv, block_rows)
+    if int(flag.item()):
+        raise ContractViolation("random initial factors are rank deficient")
+    Wr = np.random.default_rng(seed).standard_normal((spec.n_angles, spec.rank))
+    W, _, dw = orthonormalize(as_device(Wr), dp.quad)
+    if dw:
+        raise ContractViolation("random initial factors are rank deficient")
+    T = as_device(spec.T0)
+    k = dp.constants
+    b0 = ((k.a_r * k.c / FOUR_PI) * (T * T) ** 2).repeat_interleave(4).reshape(-1, 1)
+    S = torch.outer(mass_gram(co, X, b0)[:, 0], W.beta)
     return DlrState(X=X, S=S, W=W)
 
 

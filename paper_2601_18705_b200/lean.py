@@ -1,0 +1,161 @@
+"""Memory-lean DLR-SN step for pure absorbers (BASELINE config 5 on one GPU).
+
+``step_collocation(..., engine="lean")`` runs the same algorithm as the
+reference (dlr_sn.py:86-151) for sigma_s = 0, where the source iteration is
+a single sweep whose flux is never used by the step (transport_sn.py:410,
+430-432; dlr_sn.py:111-150 reads only psi and the iteration count), with a
+working set of about 2 x N_x r doubles instead of the ~6 x N_x r of the
+one-call native step:
+
+* the selected directions are swept in chunks of ``chunk`` directions: the
+  chunk's psi_time = X (S W_sel^T)[:, chunk] (evaluate_rows,
+  lowrank.py:220-227) is formed in a chunk buffer, laid out as the sweep rhs
+  (transport_sn.py:403-407), swept IN PLACE (the rhs of a step is staged
+  before that step's psi is written), and its psi columns are written
+  straight into the N_x x r buffer Psi;
+* CholQR2 in the M inner product (K2) runs on Psi in place (row blocks
+  through a chunk buffer), so Psi becomes X_new;
+* the projections (K3) read X_new and the caller's X; everything else is
+  r x r or N_Omega x r.
+
+At config 5 (N_x = 67.1 M, r = 128) the step holds X (68.7 GB), Psi / X_new
+(68.7 GB) and ~18 GB of chunk buffers on one 180 GB B200.  The exact CGS2
+fallback of a failed CholQR2 guard needs a separate copy of Psi, which this
+mode does not have: it raises instead (the guard never fires on the
+BASELINE configs).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import empty, stream
+from .angular import AngularBasis, orthonormalize_async
+from .errors import ContractViolation, SolverError
+from .lowrank import (
+    DlrState,
+    _chol,
+    _row_solve_async,
+    _cgs2_flags,
+    check_ties,
+    cholqr_guard_ok,
+    deim_finish,
+    deim_forced_launch,
+    deim_launch,
+    mass_gram,
+    raise_row_status,
+    rowmix,
+)
+from .transport import _SweepPlan, _sweep, assemble_operators, raise_sweep_status, sweep_status_word
+
+
+def rowmix_inplace(A, K, block_rows):
+    """A <- A K (K square) through a row-block buffer (the rows of a block
+    are read before they are rewritten; no full-size temporary)."""
+    n = A.shape[0]
+    buf = None
+    for r0 in range(0, n, block_rows):
+        r1 = min(n, r0 + block_rows)
+        blk = A[r0:r1]
+        if buf is None or buf.shape[0] < r1 - r0:
+            buf = empty(min(block_rows, n), A.shape[1])
+        out = buf[:r1 - r0]
+        rowmix(blk, K, out=out)
+        blk.copy_(out)
+    return A
+
+
+def step_lean(grid, step, quad, state, *, si_tol, si_max_iters, check_state, chunk=16,
+              angle_indices=None, deim_tie_tol=0.0, block_rows=1 << 22):
+    from .dlr_sn import CollocationStepInfo, _NativeSelection, project_operators
+
+    r = state.rank
+    n = grid.n_dofs
+    X, S, W = state.X, state.S, state.W.values
+    beta = state.W.beta if state.W.beta is not None else state.W.bind(quad).beta
+    # ---- DEIM, closure weights, input checks (one readback) ---------------
+    if angle_indices is not None:
+        sel, err_idx = deim_forced_launch(W, angle_indices)
+    else:
+        sel, err_idx = deim_launch(W)
+    closure = sel.closure_weights(beta)
+    ops = assemble_operators(grid, step, validate=False)
+    st = ops.step
+    flags = torch.stack([(st.sigma_t - st.sigma_s <= 0).any(), (st.sigma_s != 0).any()])
+    parts = [err_idx.to(torch.float64), closure, flags.to(torch.float64), sel.gap_dev]
+    if check_state:
+        parts.append(state.check_values(ops, quad))
+    host = torch.cat(parts).cpu().numpy()
+    deim_finish(sel, host[:r + 1], host[2 * r + 3:3 * r + 3])
+    cw = host[r + 1:2 * r + 1].copy()
+    if host[2 * r + 1]:
+        raise ContractViolation("pseudo absorption sigma_t - sigma_s must stay positive")
+    if host[2 * r + 2]:
+        raise ContractViolation("the lean step is for pure absorbers (sigma_s = 0): one sweep "
+                                "per step (transport_sn.py:410,430-432)")
+    if check_state:
+        state.raise_check(host[3 * r + 3:])
+    if angle_indices is None:
+        check_ties(sel.gaps, deim_tie_tol)
+    om_sel = quad.omegas[sel.indices]
+    # ---- the sweep, chunk by chunk (dlr_sn.py:110-121) --------------------
+    K = S @ W[sel.indices_dev].T  # (r, r): psi_time = X K (evaluate_rows)
+    psi = empty(n, r)
+    vl = ops.vec_len
+    cbuf = empty(n * chunk)  # psi_time of a chunk, then the row-block buffer
+    skbuf = empty(chunk * vl)  # rhs -> psi (in place), SK layout
+    for c0 in range(0, r, chunk):
+        c1 = min(r, c0 + chunk)
+        D = c1 - c0
+        pt = cbuf[:n * D].view(n, D)
+        rowmix(X, K[:, c0:c1].contiguous(), out=pt)
+        plan = _SweepPlan(ops, om_sel[c0:c1], cw[c0:c1], dw=1)
+        sk = skbuf[:D * vl]
+        _lib.call("dlrsn_rhs_build", ops.cellops_ptr, D, _lib.ptr(plan.quads_dev), _lib.ptr(st.q),
+                  float(st.inv_cdt), _lib.ptr(pt), D, None, 1, _lib.ptr(sk), stream())
+        _sweep(ops, plan, sk, sk)
+        _lib.call("dlrsn_sk_to_canonical", ops.cellops_ptr, D, _lib.ptr(plan.quads_dev),
+                  _lib.ptr(sk), ctypes.c_void_p(psi.data_ptr() + 8 * c0), r, stream())
+        raise_sweep_status(sweep_status_word(plan.workspace).item(), plan.workspace)
+    del cbuf, skbuf
+    # ---- K2: CholQR2 in place (Psi -> X_new) ------------------------------
+    R1, R1inv, ratio, flag = _chol(mass_gram(ops, psi))
+    rowmix_inplace(psi, R1inv, block_rows)
+    R2, R2inv, _, flag2 = _chol(mass_gram(ops, psi))
+    rowmix_inplace(psi, R2inv, block_rows)
+    guard = torch.cat([ratio, (flag + flag2).to(torch.float64)]).cpu().numpy()
+    if not cholqr_guard_ok(guard, r):
+        raise SolverError("lean step: CholQR2 guard failed (a swept column keeps < 1e-6 of its "
+                          "M-norm); the exact CGS2 fallback needs the native engine")
+    x_new = psi
+    # ---- K3 + the reduced row system + the angular update (dlr_sn.py:126-141)
+    proj, packed = project_operators(ops, x_new, x_old=X)
+    w_sel = W[sel.indices_dev]
+    q_all = (proj["q"][None, :] + st.inv_cdt * (w_sel @ (S.T @ proj["mo"]))).contiguous()
+    om_dev = quad.omegas_device()[sel.indices_dev].contiguous()
+    l_nodes, l_bar, row_status = _row_solve_async(r, r, packed, om_dev, proj["ms"].contiguous(),
+                                                  q_all, closure)
+    gamma = sel.interpolation_coefficients(l_nodes)
+    l_full = rowmix(W, gamma)
+    basis_new, r_ang, defi_w, status_w = orthonormalize_async(l_full, quad)
+    new_state = DlrState(X=x_new, S=r_ang.T.contiguous(), W=basis_new)
+    parts = [row_status.to(torch.float64), defi_w[:r].to(torch.float64),
+             status_w.to(torch.float64)]
+    if check_state:
+        parts.append(new_state.check_values(ops, quad))
+    host = torch.cat(parts).cpu().numpy()
+    raise_row_status(host[:r + 1], r)
+    adef = host[r + 1:2 * r + 1]
+    _cgs2_flags(adef, [host[2 * r + 1]], r)
+    if check_state:
+        new_state.raise_check(host[2 * r + 2:])
+    info = CollocationStepInfo(
+        iterations=1, selection=_NativeSelection(sel.indices, W), angle_indices=sel.indices.copy(),
+        phi=rowmix(x_new, l_bar.reshape(-1, 1))[:, 0], spatial_deficiency=0,
+        angular_deficiency=int(np.count_nonzero(adef)))
+    info.deim_gaps = sel.gaps
+    return new_state, info
