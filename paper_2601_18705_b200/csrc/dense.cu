@@ -1730,11 +1730,12 @@ __global__ void mirror_tiles_kernel(int r, double* __restrict__ out) {
 // pivot is not positive; diag_ratio[k] = R_kk / max(sqrt(G_kk), 1) (the
 // reference's deficiency test quantity, angular.py:137).
 __global__ void chol_upper_kernel(int r, const double* __restrict__ G, double* __restrict__ R,
-                                  double* __restrict__ Rinv, double* __restrict__ diag_ratio,
-                                  int* flag) {
+                                  double* Rinv, double* __restrict__ diag_ratio, int* flag,
+                                  int inv_in_global) {
   extern __shared__ double sm[];
   double* a = sm;          // r*r working copy (becomes R)
-  double* inv = sm + r * r;
+  // r > 110: the inverse is built in place in Rinv (global, L2-resident)
+  double* inv = inv_in_global ? Rinv : sm + r * r;
   for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
     a[e] = G[e];
     inv[e] = 0.0;
@@ -1787,7 +1788,8 @@ __global__ void chol_upper_kernel(int r, const double* __restrict__ G, double* _
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < r * r; e += blockDim.x) Rinv[e] = inv[e];
+  if (!inv_in_global)
+    for (int e = threadIdx.x; e < r * r; e += blockDim.x) Rinv[e] = inv[e];
   if (threadIdx.x == 0 && flag) *flag = bad;
 }
 
@@ -2156,6 +2158,96 @@ __global__ void row_inverse_kernel(int r, const double* __restrict__ proj,
   }
 }
 
+// The same inverse without the augmented identity (r > ~110, where [B | I]
+// does not fit shared memory): in-place Gauss-Jordan with partial pivoting
+// -- column k of the working matrix holds column k of the inverse's
+// elimination once it is eliminated -- then the row interchanges undone as
+// column swaps in reverse order.  r x r doubles of shared memory.
+__global__ void row_inverse_inplace_kernel(int r, const double* __restrict__ proj,
+                                           const double* __restrict__ om_sel,
+                                           double* __restrict__ Binv, double* __restrict__ Bout,
+                                           int* status) {
+  extern __shared__ double sm[];
+  const int d = blockIdx.x;
+  double* a = sm;  // r x r
+  __shared__ int perm[DLRSN_MAX_RANK];
+  __shared__ int piv;
+  __shared__ int sing;
+  __shared__ double rowk[DLRSN_MAX_RANK], colk[DLRSN_MAX_RANK];
+  const double wx = om_sel ? om_sel[3 * d] : 0.0, wy = om_sel ? om_sel[3 * d + 1] : 0.0;
+  const int64_t rr = (int64_t)r * r;
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+    const double b = om_sel ? wx * proj[e] + wy * proj[rr + e] + fabs(wx) * proj[2 * rr + e] +
+                                  fabs(wy) * proj[3 * rr + e] + proj[4 * rr + e]
+                            : proj[d * rr + e];
+    a[e] = b;
+    if (Bout) Bout[(int64_t)d * rr + e] = b;
+  }
+  if (threadIdx.x == 0) sing = 0;
+  __syncthreads();
+  for (int k = 0; k < r; ++k) {
+    if (threadIdx.x == 0) {
+      int p = k;
+      double best = fabs(a[k * r + k]);
+      for (int i = k + 1; i < r; ++i) {
+        const double v = fabs(a[i * r + k]);
+        if (v > best) { best = v; p = i; }
+      }
+      piv = p;
+      perm[k] = p;
+      if (!(best > 0.0) || !isfinite(best)) sing = 1;
+    }
+    __syncthreads();
+    if (sing) break;
+    const int p = piv;
+    if (p != k)
+      for (int j = threadIdx.x; j < r; j += blockDim.x) {
+        const double t = a[k * r + j];
+        a[k * r + j] = a[p * r + j];
+        a[p * r + j] = t;
+      }
+    __syncthreads();
+    const double inv = 1.0 / a[k * r + k];
+    // pivot row scaled (its pivot slot becomes the inverse pivot), the
+    // pivot column saved as the multipliers
+    for (int j = threadIdx.x; j < r; j += blockDim.x) {
+      rowk[j] = j == k ? inv : a[k * r + j] * inv;
+      colk[j] = a[j * r + k];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+      const int i = e / r, j = e % r;
+      if (i == k) {
+        a[e] = rowk[j];
+      } else {
+        const double f = colk[i];
+        a[e] = j == k ? -f * inv : a[e] - f * rowk[j];
+      }
+    }
+    __syncthreads();
+  }
+  if (sing) {
+    if (threadIdx.x == 0) status[d] = 1;
+    return;
+  }
+  // undo the row interchanges as column swaps, last first
+  for (int k = r - 1; k >= 0; --k) {
+    const int p = perm[k];
+    if (p != k)
+      for (int i = threadIdx.x; i < r; i += blockDim.x) {
+        const double t = a[i * r + k];
+        a[i * r + k] = a[i * r + p];
+        a[i * r + p] = t;
+      }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+    const double v = a[e];
+    if (!isfinite(v)) status[d] = 1;
+    Binv[(int64_t)d * rr + e] = v;
+  }
+}
+
 // LU with partial pivoting of an n x n matrix in shared memory (one CTA)
 // and solve with nrhs right-hand sides stored column-major after it.
 __device__ void cta_lu_solve(int n, double* a, int lda, double* b, int ldb, int nrhs, int* perm,
@@ -2211,23 +2303,20 @@ __device__ void cta_lu_solve(int n, double* a, int lda, double* b, int ldb, int 
 //   lbar = solve(I - cbar ms / 4pi, zeta); L_d = Binv_d (Q_d + ms lbar / 4pi)
 __global__ void row_combine_kernel(int n, int r, const double* __restrict__ Binv,
                                    const double* __restrict__ ms, const double* __restrict__ Q,
-                                   const double* __restrict__ wts, double* __restrict__ L,
-                                   double* __restrict__ lbar, int* status) {
+                                   const double* __restrict__ wts, double* L,
+                                   double* __restrict__ lbar, int* status, int cbar_in_L) {
   extern __shared__ double sm[];
-  double* cbar = sm;              // r*r
-  double* lhs = cbar + r * r;     // r*r
-  double* zeta = lhs + r * r;     // r
+  // cbar_in_L (r > ~110, n >= r): cbar is staged in the output L (global),
+  // after zeta has consumed the per-node products kept there
+  double* lhs = sm;               // r*r
+  double* cbar = cbar_in_L ? L : lhs + r * r;  // r*r
+  double* zeta = cbar_in_L ? lhs + r * r : lhs + 2 * r * r;  // r
   double* msl = zeta + r;         // r
   int* perm = reinterpret_cast<int*>(msl + r);
   __shared__ int sing;
   const int64_t rr = (int64_t)r * r;
-  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
-    double s = 0.0;
-    for (int d = 0; d < n; ++d) s += wts[d] * Binv[d * rr + e];
-    cbar[e] = s;
-  }
   // zeta = sum_d w_d Binv_d q_d: the per-node products in parallel (stored
-  // in lhs as scratch), then the node sum in fixed order
+  // in L as scratch), then the node sum in fixed order
   for (int e = threadIdx.x; e < n * r; e += blockDim.x) {
     const int d = e / r, i = e % r;
     double bq = 0.0;
@@ -2240,6 +2329,12 @@ __global__ void row_combine_kernel(int n, int r, const double* __restrict__ Binv
     double s = 0.0;
     for (int d = 0; d < n; ++d) s += wts[d] * L[d * r + i];
     zeta[i] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+    double s = 0.0;
+    for (int d = 0; d < n; ++d) s += wts[d] * Binv[d * rr + e];
+    cbar[e] = s;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
@@ -2628,15 +2723,18 @@ __global__ void __launch_bounds__(kDeimCT) deim_cluster_kernel(int n, int r, int
 //   mode 1 (closure_weights):            x = W_hat^-T v   (v r)
 __global__ void what_solve_kernel(int r, int m, const double* __restrict__ Lhat,
                                   const double* __restrict__ U, const double* __restrict__ V,
-                                  double* __restrict__ X, int mode) {
+                                  double* __restrict__ X, int mode, int factors_global) {
   extern __shared__ double sw[];
-  double* sL = sw;               // r x r
-  double* sU = sL + r * r;       // r x r
-  double* sX = sU + r * r;       // r x m
-  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
-    cp_async8(sL + e, Lhat + e);
-    cp_async8(sU + e, U + e);
-  }
+  // factors_global (r x r factors too large to stage next to the rhs, r >
+  // ~110): the substitutions read Lhat / U from global memory (L1 / L2)
+  const double* sL = factors_global ? Lhat : sw;          // r x r
+  const double* sU = factors_global ? U : sw + r * r;     // r x r
+  double* sX = factors_global ? sw : sw + 2 * r * r;      // r x m
+  if (!factors_global)
+    for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+      cp_async8(sw + e, Lhat + e);
+      cp_async8(sw + r * r + e, U + e);
+    }
   for (int e = threadIdx.x; e < r * m; e += blockDim.x) cp_async8(sX + e, V + e);
   cp_async_wait_all();
   __syncthreads();
@@ -3032,7 +3130,7 @@ int dlrsn_project(const dlrsn_cellops* ops, int r, const double* X, const double
 int dlrsn_chol_upper(int r, const double* G, double* R, double* Rinv, double* diag_ratio,
                      int* flag, dlrsn_stream_t stream) {
   const size_t smem = 2 * (size_t)r * r * sizeof(double);
-  DLRSN_REQUIRE(smem <= 200 * 1024, "rank %d too large for chol_upper", r);
+  DLRSN_REQUIRE(r <= DLRSN_MAX_RANK, "rank %d too large for chol_upper", r);
   if (r <= 32) {
     if (r <= 16)
       chol_upper_warp_kernel<16><<<1, 32, 0, as_stream(stream)>>>(r, G, R, Rinv, diag_ratio, flag);
@@ -3041,8 +3139,12 @@ int dlrsn_chol_upper(int r, const double* G, double* R, double* Rinv, double* di
     DLRSN_CHECK_LAUNCH("chol_upper_warp_kernel");
     return DLRSN_OK;
   }
-  DLRSN_TRY_CUDA(cudaFuncSetAttribute(chol_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  chol_upper_kernel<<<1, 256, smem, as_stream(stream)>>>(r, G, R, Rinv, diag_ratio, flag);
+  const int inv_global = smem > 200 * 1024;
+  const size_t smem_used = inv_global ? smem / 2 : smem;
+  DLRSN_TRY_CUDA(cudaFuncSetAttribute(chol_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem_used));
+  chol_upper_kernel<<<1, 256, smem_used, as_stream(stream)>>>(r, G, R, Rinv, diag_ratio, flag,
+                                                              inv_global);
   DLRSN_CHECK_LAUNCH("chol_upper_kernel");
   return DLRSN_OK;
 }
@@ -3081,22 +3183,34 @@ int dlrsn_small_matmul(int m, int k, int n, const double* A, const double* B, do
 
 int dlrsn_row_inverse(int n, int r, const double* proj, const double* om_sel, double* Binv,
                       double* Bout, int* status, dlrsn_stream_t stream) {
+  DLRSN_REQUIRE(r >= 1 && r <= DLRSN_MAX_RANK, "rank %d too large for row_inverse", r);
   const size_t smem = 2 * (size_t)r * r * sizeof(double);
-  DLRSN_REQUIRE(smem <= 200 * 1024, "rank %d too large for row_inverse", r);
-  DLRSN_TRY_CUDA(cudaFuncSetAttribute(row_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (n == 0) return DLRSN_OK;
-  row_inverse_kernel<<<n, 256, smem, as_stream(stream)>>>(r, proj, om_sel, Binv, Bout, status);
-  DLRSN_CHECK_LAUNCH("row_inverse_kernel");
+  if (smem <= 200 * 1024) {
+    DLRSN_TRY_CUDA(cudaFuncSetAttribute(row_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    row_inverse_kernel<<<n, 256, smem, as_stream(stream)>>>(r, proj, om_sel, Binv, Bout, status);
+    DLRSN_CHECK_LAUNCH("row_inverse_kernel");
+  } else {
+    const size_t sm1 = (size_t)r * r * sizeof(double);
+    DLRSN_TRY_CUDA(cudaFuncSetAttribute(row_inverse_inplace_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+    row_inverse_inplace_kernel<<<n, 256, sm1, as_stream(stream)>>>(r, proj, om_sel, Binv, Bout,
+                                                                   status);
+    DLRSN_CHECK_LAUNCH("row_inverse_inplace_kernel");
+  }
   return DLRSN_OK;
 }
 
 int dlrsn_row_combine(int n, int r, const double* Binv, const double* ms, const double* Q,
                       const double* wts, double* L, double* lbar, int* status,
                       dlrsn_stream_t stream) {
-  const size_t smem = (2 * (size_t)r * r + 2 * r) * sizeof(double) + r * sizeof(int);
+  size_t smem = (2 * (size_t)r * r + 2 * r) * sizeof(double) + r * sizeof(int);
+  const int in_l = smem > 200 * 1024 && n >= r;
+  if (in_l) smem -= (size_t)r * r * sizeof(double);
   DLRSN_REQUIRE(smem <= 200 * 1024, "rank %d too large for row_combine", r);
   DLRSN_TRY_CUDA(cudaFuncSetAttribute(row_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  row_combine_kernel<<<1, 256, smem, as_stream(stream)>>>(n, r, Binv, ms, Q, wts, L, lbar, status);
+  row_combine_kernel<<<1, 256, smem, as_stream(stream)>>>(n, r, Binv, ms, Q, wts, L, lbar, status,
+                                                          in_l);
   DLRSN_CHECK_LAUNCH("row_combine_kernel");
   return DLRSN_OK;
 }
@@ -3185,11 +3299,13 @@ int dlrsn_deim(int n, int r, double* Wwork, const double* W, int* idx, double* L
 
 int dlrsn_what_solve(int r, int m, const double* Lhat, const double* U, const double* V,
                      double* X, int mode, dlrsn_stream_t stream) {
-  const size_t smem = (2 * (size_t)r * r + (size_t)r * m) * sizeof(double);
+  size_t smem = (2 * (size_t)r * r + (size_t)r * m) * sizeof(double);
+  const int fg = smem > 200 * 1024;
+  if (fg) smem = (size_t)r * m * sizeof(double);
   DLRSN_REQUIRE(smem <= 200 * 1024, "W_hat solve too large for shared memory");
   DLRSN_TRY_CUDA(cudaFuncSetAttribute(what_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
-  what_solve_kernel<<<1, 128, smem, as_stream(stream)>>>(r, m, Lhat, U, V, X, mode);
+  what_solve_kernel<<<1, 128, smem, as_stream(stream)>>>(r, m, Lhat, U, V, X, mode, fg);
   DLRSN_CHECK_LAUNCH("what_solve_kernel");
   return DLRSN_OK;
 }

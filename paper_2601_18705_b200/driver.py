@@ -71,10 +71,13 @@ class DeviceProblem:
         returns the next LinearizedStep."""
         n = self.spec.n_cells
         if self.spec.frozen:
+            # coefficients stay frozen (sigma_t, q; sigma_s = 0) but the next
+            # step linearises about the new T (T0, denom, sigma_a of the
+            # update_temperature formula, physics.py:94-132), as oracle/runner.py
             from .physics import update_temperature
 
             T.copy_(update_temperature(phi_dofs, lin, self.spec.t_floor))
-            return lin
+            return self.linearized(T.clone())
         # one allocation for the next step's coefficients; the kernel reads
         # this step's sigma_a / denom and writes the new ones out of place
         buf = empty(6, n)

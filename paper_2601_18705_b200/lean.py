@@ -28,6 +28,8 @@ BASELINE configs).
 from __future__ import annotations
 
 import ctypes
+import os
+import sys
 
 import numpy as np
 import torch
@@ -41,6 +43,7 @@ from .lowrank import (
     _chol,
     _row_solve_async,
     _cgs2_flags,
+    cgs2_spatial_async,
     check_ties,
     cholqr_guard_ok,
     deim_finish,
@@ -122,15 +125,27 @@ def step_lean(grid, step, quad, state, *, si_tol, si_max_iters, check_state, chu
                   _lib.ptr(sk), ctypes.c_void_p(psi.data_ptr() + 8 * c0), r, stream())
         raise_sweep_status(sweep_status_word(plan.workspace).item(), plan.workspace)
     del cbuf, skbuf
-    # ---- K2: CholQR2 in place (Psi -> X_new) ------------------------------
+    # ---- K2 in place (Psi -> X_new): CholQR2 when its guard holds (every
+    # column keeps >= 1e-6 of its M-norm, read back before Psi is touched),
+    # else the reference's exact CGS2 with deficiency / completion, in place
     R1, R1inv, ratio, flag = _chol(mass_gram(ops, psi))
-    rowmix_inplace(psi, R1inv, block_rows)
-    R2, R2inv, _, flag2 = _chol(mass_gram(ops, psi))
-    rowmix_inplace(psi, R2inv, block_rows)
-    guard = torch.cat([ratio, (flag + flag2).to(torch.float64)]).cpu().numpy()
-    if not cholqr_guard_ok(guard, r):
-        raise SolverError("lean step: CholQR2 guard failed (a swept column keeps < 1e-6 of its "
-                          "M-norm); the exact CGS2 fallback needs the native engine")
+    guard = torch.cat([ratio, flag.to(torch.float64)]).cpu().numpy()
+    sdef = 0
+    if cholqr_guard_ok(guard, r):
+        rowmix_inplace(psi, R1inv, block_rows)
+        R2, R2inv, _, flag2 = _chol(mass_gram(ops, psi))
+        rowmix_inplace(psi, R2inv, block_rows)
+        if int(flag2.item()):
+            raise SolverError("lean step: second CholQR pass lost positive definiteness")
+        gs_fallback = 0
+    else:
+        _, _, defi_x, status_x = cgs2_spatial_async(ops.cellops, psi, r + 8, True, out=psi)
+        hx = torch.cat([defi_x[:r].to(torch.float64), status_x.to(torch.float64)]).cpu().numpy()
+        sdef = len(_cgs2_flags(hx[:r], hx[r:], r))
+        gs_fallback = 1
+    if os.environ.get("DLRSN_GUARD_DEBUG"):
+        print(f"dlrsn lean guard: min ratio {guard[:r].min():.3e}, fallback {gs_fallback}",
+              file=sys.stderr)
     x_new = psi
     # ---- K3 + the reduced row system + the angular update (dlr_sn.py:126-141)
     proj, packed = project_operators(ops, x_new, x_old=X)
@@ -155,7 +170,8 @@ def step_lean(grid, step, quad, state, *, si_tol, si_max_iters, check_state, chu
         new_state.raise_check(host[2 * r + 2:])
     info = CollocationStepInfo(
         iterations=1, selection=_NativeSelection(sel.indices, W), angle_indices=sel.indices.copy(),
-        phi=rowmix(x_new, l_bar.reshape(-1, 1))[:, 0], spatial_deficiency=0,
+        phi=rowmix(x_new, l_bar.reshape(-1, 1))[:, 0], spatial_deficiency=sdef,
         angular_deficiency=int(np.count_nonzero(adef)))
     info.deim_gaps = sel.gaps
+    info.gs_fallback = gs_fallback
     return new_state, info

@@ -154,12 +154,14 @@ def cholqr_guard_ok(host_guard, m):
             and float(dec.min(initial=np.inf)) >= 1e-10)
 
 
-def cgs2_spatial_async(co, cols, completion_count, strict=True):
+def cgs2_spatial_async(co, cols, completion_count, strict=True, out=None):
+    """``out`` may be ``cols`` itself: column k is read before Q[:, k] is
+    written and only Q[:, :k] is read at step k, so the kernel runs in place."""
     n, m = cols.shape
     return _cgs2_async(n, m, cols, metric=1, ops=co, comp_kind=1,
                        comp_exp=np.asarray(spatial_monomial_exponents(completion_count), np.int32),
                        coords=np.asarray([co.x0, co.y0, co.nx * co.dx, co.ny * co.dy]),
-                       strict=strict)
+                       strict=strict, out=out)
 
 
 def _cgs2_flags(defi, status, m):
@@ -169,9 +171,9 @@ def _cgs2_flags(defi, status, m):
 
 
 def _cgs2_async(n, m, cols, *, metric, ops=None, weights=None, comp_kind, comp_exp, coords,
-                strict=True):
+                strict=True, out=None):
     """Exact CGS2 kernel without a host sync: (Q, R, deficient flags, status)."""
-    Q = zeros(n, m)
+    Q = zeros(n, m) if out is None else out
     R = zeros(m, m)
     defi = _i32(max(m, 1))
     status = _i32(1)
@@ -182,7 +184,7 @@ def _cgs2_async(n, m, cols, *, metric, ops=None, weights=None, comp_kind, comp_e
     if not isinstance(coords, torch.Tensor):
         c = np.asarray(coords, dtype=np.float64)
         coords = cached_upload(("coords", c.shape, c.tobytes()), lambda: c)
-    _lib.call("dlrsn_cgs2", n, m, _lib.ptr(cols), cols.stride(0), _lib.ptr(Q), m, _lib.ptr(R),
+    _lib.call("dlrsn_cgs2", n, m, _lib.ptr(cols), cols.stride(0), _lib.ptr(Q), Q.stride(0), _lib.ptr(R),
               _lib.ptr(defi), metric, _lib.ptr(weights), None if ops is None else _addr(ops),
               comp_kind, ncomp, _lib.ptr(exp_dev), _lib.ptr(coords), _lib.ptr(work),
               _lib.ptr(status), int(bool(strict)), stream())
