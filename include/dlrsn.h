@@ -276,6 +276,18 @@ int dlrsn_project(const dlrsn_cellops* ops, int r, const double* X, const double
                   const double* sigma_t, const double* sigma_s, const double* q, double* out,
                   double* partial, dlrsn_stream_t stream);
 
+/* dlrsn_project on one row slab of a larger grid (multi-GPU row slabs,
+ * slab.py): ops describes the slab (nx x ny_slab cells), halo (nullable) the
+ * X rows of the grid row just below the slab (4 nx x r) for the horizontal
+ * faces on the slab's bottom edge (NULL: the domain's bottom wall), and
+ * top_wall = 1 when the slab's top row is the domain's top wall (0: the face
+ * above is counted by the next slab).  Summing the outputs over the slabs of
+ * a grid gives dlrsn_project on the whole grid. */
+int dlrsn_project_slab(const dlrsn_cellops* ops, int r, const double* X, const double* Xold,
+                       const double* halo, int top_wall, const double* sigma_t,
+                       const double* sigma_s, const double* q, double* out, double* partial,
+                       dlrsn_stream_t stream);
+
 /* G = R^T R (R upper) and R^-1; diag_ratio (2r): [k] = R_kk / sqrt(G_kk)
  * (relative norm left after projection), [r+k] = R_kk / max(sqrt(G_kk), 1)
  * (the CGS2 deficiency quantity of angular.py:137); *flag = 1 on a

@@ -124,6 +124,8 @@ _SIGNATURES = {
     "dlrsn_row_combine": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "dlrsn_deim": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp]),
     "dlrsn_dmma_probe": (c_int, [c_int, c_int, c_int, c_vp, c_vp]),
+    "dlrsn_project_slab": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp,
+                                   c_vp, c_vp]),
     "dlrsn_project_timing": (c_int, [c_int]),
     "dlrsn_project_timing_read": (c_int, [c_int, c_vp, c_vp]),
     "dlrsn_deim_forced": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),

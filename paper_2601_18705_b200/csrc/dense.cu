@@ -608,10 +608,24 @@ struct ProjArgs {
   const double* q;
   double* part;  // [chunk][7*r*r + r]
   int cells_per_block;
+  // row-slab decomposition (multi-GPU, slab.py): X rows of the grid row just
+  // below this slab (4 nx x r, nullable: the bottom wall), and whether the
+  // slab's top row is the domain's top wall (else the face above belongs to
+  // the next slab, which sees this slab's top row as its halo)
+  const double* halo;
+  int top_wall;
 };
 
 __device__ inline double ldx(const double* X, int r, int64_t row, int col) {
   return col < r ? __ldg(X + row * r + col) : 0.0;
+}
+
+// local dof l of the cell below cell c = (ci, cj) of this slab: a slab row,
+// or the halo row below the slab, or 0 at the bottom wall (vacuum trace)
+__device__ inline double ld_below(const ProjArgs& pa, const double* X, int c, int ci, int cj, int l,
+                                  int col) {
+  if (cj > 0) return ldx(X, pa.r, (int64_t)(c - pa.nx) * 4 + l, col);
+  return pa.halo ? ldx(pa.halo, pa.r, (int64_t)ci * 4 + l, col) : 0.0;
 }
 
 __device__ inline double2 ld2s(const double* p) { return *reinterpret_cast<const double2*>(p); }
@@ -691,9 +705,9 @@ __global__ void __launch_bounds__(256, 2) project_kernel(ProjArgs pa, dlrsn_cell
         ax0 = ldx(X, r, (int64_t)(c - 1) * 4 + 1, gcol);
         ax1 = ldx(X, r, (int64_t)(c - 1) * 4 + 3, gcol);
       }
-      if (cj > 0) {
-        ay0 = ldx(X, r, (int64_t)(c - nx) * 4 + 2, gcol);
-        ay1 = ldx(X, r, (int64_t)(c - nx) * 4 + 3, gcol);
+      if (cj > 0 || pa.halo) {
+        ay0 = ld_below(pa, X, c, ci, cj, 2, gcol);
+        ay1 = ld_below(pa, X, c, ci, cj, 3, gcol);
       }
       const double ux0 = ax0 - x[0], ux1 = ax1 - x[2], vx0 = ax0 + x[0], vx1 = ax1 + x[2];
       const double uy0 = ay0 - x[0], uy1 = ay1 - x[1], vy0 = ay0 + x[0], vy1 = ay1 + x[1];
@@ -801,7 +815,7 @@ __global__ void __launch_bounds__(256, 2) project_kernel(ProjArgs pa, dlrsn_cell
         acc[2][q] += v[q];
       }
     }
-    for (int c = max(c_begin, (ny - 1) * nx) + g; c < c_end; c += 4) {
+    for (int c = max(c_begin, (ny - 1) * nx) + g; pa.top_wall && c < c_end; c += 4) {
       const int64_t r2 = (int64_t)c * 4 + 2, r3 = (int64_t)c * 4 + 3;
       const double2 a0 = make_double2(ldx(X, r, r2, ia), ldx(X, r, r2, ia + 1));
       const double2 a1 = make_double2(ldx(X, r, r3, ia), ldx(X, r, r3, ia + 1));
@@ -945,11 +959,11 @@ __global__ void __launch_bounds__(256, 2) project_mma_kernel(ProjArgs pa, dlrsn_
       w.x[l] = live ? ldx(X, r, (int64_t)c * 4 + l, sgcol) : 0.0;
       w.xo[l] = (live && side == 0 && pa.Xold) ? ldx(pa.Xold, r, (int64_t)c * 4 + l, sgcol) : 0.0;
     }
-    const bool lx = live && ci > 0, ly = live && cj > 0;
+    const bool lx = live && ci > 0, ly = live && (cj > 0 || pa.halo != nullptr);
     w.ax0 = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 1, sgcol) : 0.0;
     w.ax1 = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 3, sgcol) : 0.0;
-    w.ay0 = ly ? ldx(X, r, (int64_t)(c - nx) * 4 + 2, sgcol) : 0.0;
-    w.ay1 = ly ? ldx(X, r, (int64_t)(c - nx) * 4 + 3, sgcol) : 0.0;
+    w.ay0 = ly ? ld_below(pa, X, c, ci, cj, 2, sgcol) : 0.0;
+    w.ay1 = ly ? ld_below(pa, X, c, ci, cj, 3, sgcol) : 0.0;
     w.qc = (live && side == 1) ? __ldg(pa.q + c) : 0.0;
     const bool cst = live && threadIdx.x < C;  // sigma of cell cc0 + threadIdx.x
     const int cs = cc0 + (int)threadIdx.x;
@@ -1059,7 +1073,7 @@ __global__ void __launch_bounds__(256, 2) project_mma_kernel(ProjArgs pa, dlrsn_
         const double aj0 = ldx(X, r, r1, j), aj1 = ldx(X, r, r3, j);
         bx += ai0 * (0.5 * (e2x[0] * aj0 + e2x[1] * aj1)) + ai1 * (0.5 * (e2x[2] * aj0 + e2x[3] * aj1));
       }
-      for (int c = max(c_begin, (ny - 1) * nx); c < c_end; ++c) {
+      for (int c = max(c_begin, (ny - 1) * nx); pa.top_wall && c < c_end; ++c) {
         const int64_t r2 = (int64_t)c * 4 + 2, r3 = (int64_t)c * 4 + 3;
         const double ai0 = ldx(X, r, r2, i), ai1 = ldx(X, r, r3, i);
         const double aj0 = ldx(X, r, r2, j), aj1 = ldx(X, r, r3, j);
@@ -1174,11 +1188,11 @@ __global__ void __launch_bounds__(256, 1) project_mma32_kernel(ProjArgs pa, dlrs
       w.x[l] = live ? ldx(X, r, (int64_t)c * 4 + l, sgcol) : 0.0;
       w.xo[l] = (live && side == 0 && pa.Xold) ? ldx(pa.Xold, r, (int64_t)c * 4 + l, sgcol) : 0.0;
     }
-    const bool lx = live && ci > 0, ly = live && cj > 0;
+    const bool lx = live && ci > 0, ly = live && (cj > 0 || pa.halo != nullptr);
     w.ax0 = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 1, sgcol) : 0.0;
     w.ax1 = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 3, sgcol) : 0.0;
-    w.ay0 = ly ? ldx(X, r, (int64_t)(c - nx) * 4 + 2, sgcol) : 0.0;
-    w.ay1 = ly ? ldx(X, r, (int64_t)(c - nx) * 4 + 3, sgcol) : 0.0;
+    w.ay0 = ly ? ld_below(pa, X, c, ci, cj, 2, sgcol) : 0.0;
+    w.ay1 = ly ? ld_below(pa, X, c, ci, cj, 3, sgcol) : 0.0;
     w.qc = (live && side == 1) ? __ldg(pa.q + c) : 0.0;
     const int cs = cc0 + (int)threadIdx.x;
     w.st = (cc0 < c_end && threadIdx.x < C && cs < c_end) ? __ldg(pa.sigma_t + cs) : 0.0;
@@ -1312,7 +1326,7 @@ __global__ void __launch_bounds__(256, 1) project_mma32_kernel(ProjArgs pa, dlrs
         const double aj0 = ldx(X, r, r1, j), aj1 = ldx(X, r, r3, j);
         bx += ai0 * (0.5 * (e2x[0] * aj0 + e2x[1] * aj1)) + ai1 * (0.5 * (e2x[2] * aj0 + e2x[3] * aj1));
       }
-      for (int c = max(c_begin, (ny - 1) * nx); c < c_end; ++c) {
+      for (int c = max(c_begin, (ny - 1) * nx); pa.top_wall && c < c_end; ++c) {
         const int64_t r2 = (int64_t)c * 4 + 2, r3 = (int64_t)c * 4 + 3;
         const double ai0 = ldx(X, r, r2, i), ai1 = ldx(X, r, r3, i);
         const double aj0 = ldx(X, r, r2, j), aj1 = ldx(X, r, r3, j);
@@ -1449,15 +1463,15 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
     }
     if constexpr (GROUP == 0) {
       const int ci = c % nx, cj = c / nx;
-      const bool lx = live && ci > 0, ly = live && cj > 0;
+      const bool lx = live && ci > 0, ly = live && (cj > 0 || pa.halo != nullptr);
       w.y[0] = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 1, gj) : 0.0;
       w.y[1] = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 3, gj) : 0.0;
-      w.y[2] = ly ? ldx(X, r, (int64_t)(c - nx) * 4 + 2, gj) : 0.0;
-      w.y[3] = ly ? ldx(X, r, (int64_t)(c - nx) * 4 + 3, gj) : 0.0;
+      w.y[2] = ly ? ld_below(pa, X, c, ci, cj, 2, gj) : 0.0;
+      w.y[3] = ly ? ld_below(pa, X, c, ci, cj, 3, gj) : 0.0;
       w.ui[0] = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 1, gi) : 0.0;
       w.ui[1] = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 3, gi) : 0.0;
-      w.ui[2] = ly ? ldx(X, r, (int64_t)(c - nx) * 4 + 2, gi) : 0.0;
-      w.ui[3] = ly ? ldx(X, r, (int64_t)(c - nx) * 4 + 3, gi) : 0.0;
+      w.ui[2] = ly ? ld_below(pa, X, c, ci, cj, 2, gi) : 0.0;
+      w.ui[3] = ly ? ld_below(pa, X, c, ci, cj, 3, gi) : 0.0;
     } else {
 #pragma unroll
       for (int l = 0; l < 4; ++l)
@@ -1625,7 +1639,7 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
           const double aj0 = ldx(X, r, r1, j), aj1 = ldx(X, r, r3, j);
           bx += ai0 * (0.5 * (e2x[0] * aj0 + e2x[1] * aj1)) + ai1 * (0.5 * (e2x[2] * aj0 + e2x[3] * aj1));
         }
-        for (int c = max(c_begin, (ny - 1) * nx); c < c_end; ++c) {
+        for (int c = max(c_begin, (ny - 1) * nx); pa.top_wall && c < c_end; ++c) {
           const int64_t r2 = (int64_t)c * 4 + 2, r3 = (int64_t)c * 4 + 3;
           const double ai0 = ldx(X, r, r2, i), ai1 = ldx(X, r, r3, i);
           const double aj0 = ldx(X, r, r2, j), aj1 = ldx(X, r, r3, j);
@@ -3034,6 +3048,13 @@ int dlrsn_project_timing_read(int cap, float* ms, int* count) {
 int dlrsn_project(const dlrsn_cellops* ops, int r, const double* X, const double* Xold,
                   const double* sigma_t, const double* sigma_s, const double* q, double* out,
                   double* partial, dlrsn_stream_t stream) {
+  return dlrsn_project_slab(ops, r, X, Xold, nullptr, 1, sigma_t, sigma_s, q, out, partial, stream);
+}
+
+int dlrsn_project_slab(const dlrsn_cellops* ops, int r, const double* X, const double* Xold,
+                       const double* halo, int top_wall, const double* sigma_t,
+                       const double* sigma_s, const double* q, double* out, double* partial,
+                       dlrsn_stream_t stream) {
   const int ncell = ops->nx * ops->ny;
   const int tiles = ((r + kTile - 1) / kTile) * ((r + kTile - 1) / kTile);
   const int cpb = cells_per_block(ncell, tiles);
@@ -3042,6 +3063,8 @@ int dlrsn_project(const dlrsn_cellops* ops, int r, const double* X, const double
   pa.nx = ops->nx; pa.ny = ops->ny; pa.r = r;
   pa.X = X; pa.Xold = Xold; pa.sigma_t = sigma_t; pa.sigma_s = sigma_s; pa.q = q;
   pa.part = partial; pa.cells_per_block = cpb;
+  pa.halo = halo;
+  pa.top_wall = top_wall;
   cudaStream_t st = as_stream(stream);
   static const char* simt = getenv("DLRSN_PROJECT_SIMT");
   static const char* wide = getenv("DLRSN_PROJECT_WIDE");

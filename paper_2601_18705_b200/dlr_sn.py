@@ -317,6 +317,18 @@ class _NativeSelection:
 _STEP_WS = {}
 
 
+def release_workspaces():
+    """Drop the cached per-problem step workspaces, native contexts and sweep
+    workspaces (e.g. before a config-5 step that needs most of HBM)."""
+    from . import transport
+
+    _STEP_WS.clear()
+    _CTX.clear()
+    _HOOKS.clear()
+    transport._WS_CACHE.clear()
+    torch.cuda.empty_cache()
+
+
 def _grid_cellops(grid):
     co = grid.__dict__.get("_cellops")
     if co is None:
