@@ -367,7 +367,7 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="C4", choices=["C2", "C3", "C4"])
+    ap.add_argument("--config", default="C4", choices=["C2", "C3", "C4", "C5"])
     ap.add_argument("--dry", action="store_true", help="multi-rank plumbing on CPU (gloo)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=25.0,
@@ -375,6 +375,9 @@ def main(argv=None):
     ap.add_argument("--ref-budget", type=float, default=150.0,
                     help="seconds of port step time for --impl reference (at least one step)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0: same as --steps (max 10)")
+    ap.add_argument("--sharding", default="slab", choices=["slab", "directions"],
+                    help="N > 1: row slabs with direction-sharded sweeps (Option B, slab.py) "
+                         "or direction sharding with the Galerkin side replicated (Option A)")
     ap.add_argument("--more-configs", default="C2,C3,C5step,C5dlr,C5",
                     help="also measure these at N=1 ('' = none)")
     args = ap.parse_args(argv)
@@ -400,6 +403,10 @@ def main(argv=None):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.sharding == "slab":
+            return run_slab_bench(args, ws, rank, local)
+    if args.config == "C5":  # one GPU: the memory-lean engine (lean.py)
+        return run_slab_bench(args, ws, rank, local)
     comm = DirectionComm.from_default_group()  # None at N=1
     spec = make_spec(args.config)
     dp = DeviceProblem.from_spec(spec)
@@ -522,6 +529,99 @@ def main(argv=None):
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
+    return 0
+
+
+def run_slab_bench(args, ws, rank, local):
+    """N > 1 ranks, one per GPU (NCCL): the row-slab step (slab.py, Option B
+    of SURVEY 8e).  Every rank holds the full per-cell coefficient fields
+    (the sweep covers the whole grid) and its slab rows of X; after each
+    step the slabs' phi rows are all-reduced so every rank updates T and
+    re-linearises redundantly.  Timed: whole steps (step + T update), CUDA
+    events, max over ranks; strong scaling (the same problem over N GPUs)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_18705_b200.driver import DeviceProblem, initial_state, initial_state_device
+    from paper_2601_18705_b200.slab import AllReduce, Slab, run_dist, slab_rows, split_state, step_slab
+
+    spec = make_spec(args.config) if args.config != "C5" else None
+    if spec is None:
+        from paper_2601_18705_b200 import problems
+
+        spec, fields = problems.stress()
+        fields(np.random.default_rng(spec.seed))
+    dp = DeviceProblem.from_spec(spec)
+    slab = Slab(rank, ws, dp.grid, slab_rows(dp.grid.ny, ws))
+    full = initial_state_device(dp) if args.config == "C5" else initial_state(dp)
+    state = split_state(full, slab)
+    del full
+    torch.cuda.empty_cache()
+    T = torch.as_tensor(spec.T0, device="cuda").clone()
+    lin = dp.linearized(T)
+    if ws == 1:  # config 5 on one GPU: the lean engine (the slab step is not memory-lean)
+        def one_step():
+            nonlocal state, lin, T
+            state, lin, T, info = dp.step(state, lin, T, si_tol=1e-8, engine="lean")
+            return {"iterations": info.iterations}
+
+        dist = None
+    else:
+        import torch.distributed as dist
+
+    def slab_step_once():
+        nonlocal state, lin, T
+        state, info = run_dist(step_slab(slab, lin, dp.quad, state, si_tol=1e-8))
+        phi = torch.zeros(dp.grid.n_dofs, dtype=torch.float64, device="cuda")
+        phi[slab.d0:slab.d1] = info["phi"]
+        run_dist(iter([AllReduce(phi)]))
+        T = T.clone()
+        lin = dp.advance(lin, phi, T)
+        return info
+
+    if ws > 1:
+        one_step = slab_step_once
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    iters = []
+    wall0 = time.perf_counter()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            starts[k].record()
+            iters.append(one_step()["iterations"])
+            ends[k].record()
+        torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    per = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    t = torch.tensor([sum(per)], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = sum(spec.n_cells * spec.rank * it for it in iters) / (ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (seeded BASELINE {args.config})",
+        "config": {"workload": WORKLOADS.get(args.config, "C5 stress 4096x4096, r=128, dlr-sn step"),
+                   "si_tol": 1e-8, "use_dsa": False,
+                   "parallelism": (f"row slabs x{ws} + direction-sharded sweeps (Option B)"
+                                   if ws > 1 else "one GPU, lean engine"),
+                   "l2": "inputs > L2"},
+        "dlr_steps_per_s": args.steps / (ms * 1e-3), "si_iterations": iters,
+        "ms_per_step_each_rank0": [round(x, 3) for x in per],
+        "clocks": clk.summary(), "wall_s_timed_region": wall,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
     return 0
 
 

@@ -262,11 +262,14 @@ def _slab_step_fields(step, slab):
                           inv_cdt=step.inv_cdt, constants=step.constants)
 
 
-def step_slab(slab, step, quad, state, *, check_state=True, chunk=16, deim_tie_tol=1e-12):
-    """Generator: rank ``slab.rank``'s part of one pure-absorber DLR step
-    (dlr_sn.py:86-151) on row slabs.  ``step`` holds the FULL per-cell
-    fields (replicated), ``state`` the rank's slab rows of X with the
-    replicated S and W.  Returns (new slab state, info dict)."""
+def step_slab(slab, step, quad, state, *, check_state=True, chunk=16, deim_tie_tol=1e-12,
+              si_tol=1e-8, si_max_iters=200):
+    """Generator: rank ``slab.rank``'s part of one DLR step (dlr_sn.py:86-151)
+    on row slabs.  ``step`` holds the FULL per-cell fields (replicated),
+    ``state`` the rank's slab rows of X with the replicated S and W.  With
+    sigma_s = 0 one chunked in-place sweep; else the source iteration with
+    the closure flux all-reduced every iteration.  Returns (new slab state,
+    info dict)."""
     from .dlr_sn import project_operators  # noqa: F401 (documentation link)
 
     P, me = slab.P, slab.rank
@@ -296,8 +299,7 @@ def step_slab(slab, step, quad, state, *, check_state=True, chunk=16, deim_tie_t
     cw = host[r + 1:2 * r + 1].copy()
     if host[2 * r + 1]:
         raise ContractViolation("pseudo absorption sigma_t - sigma_s must stay positive")
-    if host[2 * r + 2]:
-        raise ConfigurationError("the row-slab step is for pure absorbers (sigma_s = 0)")
+    pure = not host[2 * r + 2]  # sigma_s == 0: one sweep (transport_sn.py:410)
     if check_state:
         rx, rw = float(host[3 * r + 3]), float(host[3 * r + 4])
         if rx > 1e-10 or rw > 1e-10:
@@ -312,24 +314,30 @@ def step_slab(slab, step, quad, state, *, check_state=True, chunk=16, deim_tie_t
     Y = rowmix(X, K)  # (N_p, r): this slab's rows of psi_time for every direction
     pt = yield from rows_to_direction_columns(Y, owners, slab)  # (N, |mine|)
     del Y
-    # ---- 3. sweep my directions over the whole grid (chunks) --------------
+    # ---- 3. sweep my directions over the whole grid -----------------------
     n = grid.n_dofs
-    psi_mine = empty(n, len(mine))
-    vl = ops.vec_len
-    for c0 in range(0, len(mine), chunk):
-        c1 = min(len(mine), c0 + chunk)
-        D = c1 - c0
-        cols = pt[:, c0:c1].contiguous()
-        plan = _SweepPlan(ops, om_sel[mine[c0:c1]], cw[mine[c0:c1]], dw=1)
-        sk = empty(D * vl)
-        _lib.call("dlrsn_rhs_build", ops.cellops_ptr, D, _lib.ptr(plan.quads_dev), _lib.ptr(st.q),
-                  float(st.inv_cdt), _lib.ptr(cols), D, None, 1, _lib.ptr(sk), stream())
-        _sweep(ops, plan, sk, sk)
-        _lib.call("dlrsn_sk_to_canonical", ops.cellops_ptr, D, _lib.ptr(plan.quads_dev),
-                  _lib.ptr(sk), ctypes.c_void_p(psi_mine.data_ptr() + 8 * c0), len(mine),
-                  stream())
-        raise_sweep_status(sweep_status_word(plan.workspace).item(), plan.workspace)
-        del sk, cols
+    if pure:  # one sweep, in place, chunked (transport_sn.py:410,430-432)
+        psi_mine = empty(n, len(mine))
+        vl = ops.vec_len
+        for c0 in range(0, len(mine), chunk):
+            c1 = min(len(mine), c0 + chunk)
+            D = c1 - c0
+            cols = pt[:, c0:c1].contiguous()
+            plan = _SweepPlan(ops, om_sel[mine[c0:c1]], cw[mine[c0:c1]], dw=1)
+            sk = empty(D * vl)
+            _lib.call("dlrsn_rhs_build", ops.cellops_ptr, D, _lib.ptr(plan.quads_dev),
+                      _lib.ptr(st.q), float(st.inv_cdt), _lib.ptr(cols), D, None, 1, _lib.ptr(sk),
+                      stream())
+            _sweep(ops, plan, sk, sk)
+            _lib.call("dlrsn_sk_to_canonical", ops.cellops_ptr, D, _lib.ptr(plan.quads_dev),
+                      _lib.ptr(sk), ctypes.c_void_p(psi_mine.data_ptr() + 8 * c0), len(mine),
+                      stream())
+            raise_sweep_status(sweep_status_word(plan.workspace).item(), plan.workspace)
+            del sk, cols
+        iters = 1
+    else:
+        psi_mine, iters = yield from _source_iteration_slabs(ops, slab, om_sel, cw, mine, pt, X,
+                                                            S, beta, si_tol, si_max_iters)
     del pt
     # ---- 4. swept columns back to the slabs, selection order ---------------
     psi = yield from direction_columns_to_rows(psi_mine, owners, slab, r)
@@ -392,10 +400,72 @@ def step_slab(slab, step, quad, state, *, check_state=True, chunk=16, deim_tie_t
             raise ContractViolation(f"factor orthonormality violated: spatial {rx:.2e}, "
                                     f"angular {rw:.2e}")
     phi = rowmix(x_new, l_bar.reshape(-1, 1))[:, 0]  # slab rows of info.phi
-    info = {"angle_indices": sel.indices.copy(), "iterations": 1, "phi": phi,
+    info = {"angle_indices": sel.indices.copy(), "iterations": iters, "phi": phi,
             "spatial_deficiency": sdef, "angular_deficiency": int(np.count_nonzero(adef)),
             "selection": sel, "deim_gaps": sel.gaps, "gs_fallback": int(fallback)}
     return new_state, info
+
+
+def _source_iteration_slabs(ops, slab, om_sel, cw, mine, pt, X, S, beta, tol, max_iters):
+    """Generator: the collocated source iteration (transport_sn.py:377-450)
+    with my directions swept over the whole grid and the closure flux
+    all-reduced each iteration (N_x doubles); the norms and the next
+    scattering source come from the summed flux, so every rank takes the
+    same convergence decision.  The starting flux phi_start = X S beta
+    (lowrank.py:60-62) is assembled from the slabs.  Returns (psi of my
+    directions, N_x x |mine|; iterations)."""
+    import math
+
+    from .errors import IterationLimitError
+
+    g = ops.grid
+    st = ops.step
+    n = g.n_dofs
+    phi = torch.zeros(n, dtype=torch.float64, device=X.device)
+    phi[slab.d0:slab.d1] = rowmix(X, (S @ beta).reshape(-1, 1))[:, 0]
+    yield AllReduce(phi)  # the slabs' rows of phi_start, every rank holds all
+    vl = ops.vec_len
+    D = len(mine)
+    plan = _SweepPlan(ops, om_sel[mine], cw[mine], dw=1) if D else None
+    rhs_sk = empty(max(D, 1) * vl)
+    psi_sk = empty(max(D, 1) * vl)
+    if D:
+        cols = pt.contiguous()
+        _lib.call("dlrsn_rhs_build", ops.cellops_ptr, D, _lib.ptr(plan.quads_dev), _lib.ptr(st.q),
+                  float(st.inv_cdt), _lib.ptr(cols), D, None, 1, _lib.ptr(rhs_sk), stream())
+        del cols
+    scat = empty(4 * vl)
+    flags = zeros(1, dtype=torch.int32)
+    _lib.call("dlrsn_scatter_source", ops.cellops_ptr, _lib.ptr(phi), _lib.ptr(st.sigma_s),
+              _lib.ptr(scat), _lib.ptr(flags), stream())
+    phi_new = empty(n)
+    nb = (g.n_cells + 255) // 256
+    red_ws = zeros(256 // 8 + 2 * nb + 8)
+    norms = zeros(2)
+    change = math.inf
+    for it in range(1, max_iters + 1):
+        if D:
+            _sweep(ops, plan, rhs_sk, psi_sk, scat, None)
+            _lib.call("dlrsn_phi_combine", ops.cellops_ptr, plan.G, _lib.ptr(plan.groups_dev), None,
+                      _lib.ptr(psi_sk), _lib.ptr(phi), _lib.ptr(st.sigma_s), _lib.ptr(phi_new),
+                      None, _lib.ptr(norms), _lib.ptr(red_ws), stream())
+        else:
+            phi_new.zero_()
+        yield AllReduce(phi_new)
+        _lib.call("dlrsn_phi_finish", ops.cellops_ptr, _lib.ptr(phi_new), _lib.ptr(phi),
+                  _lib.ptr(st.sigma_s), _lib.ptr(scat), _lib.ptr(norms), _lib.ptr(red_ws), stream())
+        host = norms.cpu().numpy()
+        if D:
+            raise_sweep_status(sweep_status_word(plan.workspace).item(), plan.workspace)
+        phi, phi_new = phi_new, phi
+        change = math.sqrt(host[0]) / max(math.sqrt(host[1]), 1e-300)
+        if change <= tol:
+            psi_mine = empty(n, D)
+            if D:
+                _lib.call("dlrsn_sk_to_canonical", ops.cellops_ptr, D, _lib.ptr(plan.quads_dev),
+                          _lib.ptr(psi_sk), _lib.ptr(psi_mine), D, stream())
+            return psi_mine, it
+    raise IterationLimitError("source iteration did not converge", max_iters, change)
 
 
 def _cgs2_slabs(sops, cols, m, slab, strict=True):
@@ -465,7 +535,7 @@ def _cgs2_slabs(sops, cols, m, slab, strict=True):
     return Q, ndef
 
 
-def run_slabs_local(P, grid, quad, step, state, n_steps=1, advance=None, **kw):
+def run_slabs_local(P, grid, quad, step, state, n_steps=1, advance=None, **kw):  # noqa: D401
     """Convenience for tests: split a full state into P row slabs, run
     ``n_steps`` slab steps as virtual ranks in one process and gather the
     result (X rows concatenated; S, W from rank 0 -- identical on all)."""

@@ -104,3 +104,40 @@ def test_slab_projections_sum_to_whole_grid():
             a = total[i * r * r:(i + 1) * r * r].cpu().numpy()
             assert rel_l2(a, whole[k].cpu().numpy().ravel()) <= 1e-13, (nx, r, k)
         assert rel_l2(total[7 * r * r:].cpu().numpy(), whole["q"].cpu().numpy()) <= 1e-13
+
+
+@pytest.mark.parametrize("n,r,nq,P", [(40, 16, 8, 2), (48, 24, 12, 3)])
+def test_slab_steps_with_scattering_match_oracle(n, r, nq, P):
+    """Config 4's medium (sigma_s = 0.5 sigma_a: source iteration with the
+    closure flux all-reduced every iteration) at reduced size: identical
+    picks and iteration counts, 1e-11 on phi, T and X S W^T."""
+    from oracle import port as P_
+    from oracle import runner as R
+    from paper_2601_18705_b200 import problems
+    from paper_2601_18705_b200.driver import DeviceProblem, initial_state
+    from paper_2601_18705_b200.slab import run_slabs_local
+
+    spec, fields = problems.random_medium(n=n, rank=r, n_polar=nq, n_azimuthal=nq, seed=4)
+    rng = np.random.default_rng(spec.seed)
+    Xr, Wr = problems.draw_factors(spec, rng)
+    fields(rng)
+    X, W = R.orthonormal_factors(spec, Xr, Wr)
+    ref = []
+    R.run(spec, R.initial_state(spec, X, W), 2, record=lambda s, i, t: ref.append((s, i, t)))
+    dp = DeviceProblem.from_spec(spec)
+    st = initial_state(dp, X=X, W=W)
+    T = torch.as_tensor(spec.T0, device="cuda").clone()
+    lin = dp.linearized(T)
+    for k, (rs, ri, rt) in enumerate(ref):
+        st, infos, _ = run_slabs_local(P, dp.grid, dp.quad, lin, st, si_tol=1e-12,
+                                       si_max_iters=400)
+        info = infos[0]
+        assert all(list(i["angle_indices"]) == list(ri.angle_indices) for i in info), k
+        assert all(i["iterations"] == ri.iterations for i in info), k
+        phi = torch.cat([i["phi"] for i in info])
+        assert rel_l2(phi.cpu().numpy(), ri.phi) <= 1e-11, k
+        T = T.clone()
+        lin = dp.advance(lin, phi, T)
+        assert rel_l2(T.cpu().numpy(), rt) <= 1e-11, k
+        Xg, Sg, Wg = st.to_numpy()
+        assert P_.lowrank_rel_diff(Xg, Sg, Wg, rs.X, rs.S, rs.W) <= 1e-11, k
