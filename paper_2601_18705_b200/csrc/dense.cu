@@ -468,7 +468,8 @@ __global__ void __launch_bounds__(256, 1) mgram_wide_kernel(int ncell, int ra, i
                                                          const double* __restrict__ B, int ldb,
                                                          const double* __restrict__ coeff,
                                                          dlrsn_cellops ops, int cells_per_block,
-                                                         double* __restrict__ part, int vec) {
+                                                         double* __restrict__ part, int vec,
+                                                         int sym) {
   using P = MgramWide<TB>;
   constexpr int LD = P::LD, PL = P::PL, KP = P::KP, NWT = 8 / KP, CPK = kMgC / KP;
   constexpr int NCP = TB / 2;  // column pairs
@@ -479,7 +480,16 @@ __global__ void __launch_bounds__(256, 1) mgram_wide_kernel(int ncell, int ra, i
   const int wt = warp % NWT, kp = warp / NWT;
   const int wi = wt / (TB / 32), wj = wt % (TB / 32);
   const int tiles_j = (rb + TB - 1) / TB;
-  const int i0 = (blockIdx.y / tiles_j) * TB, j0 = (blockIdx.y % tiles_j) * TB;
+  int i0 = (blockIdx.y / tiles_j) * TB, j0 = (blockIdx.y % tiles_j) * TB;
+  if (sym) {  // symmetric Gram (A == B): blockIdx.y walks the tiles ti <= tj
+    int y = blockIdx.y, ti = 0;
+    while (y >= tiles_j - ti) {
+      y -= tiles_j - ti;
+      ++ti;
+    }
+    i0 = ti * TB;
+    j0 = (ti + y) * TB;
+  }
   const int c_begin = blockIdx.x * cells_per_block;
   const int c_end = min(ncell, c_begin + cells_per_block);
   const bool same = (A == B) && (lda == ldb) && (i0 == j0);
@@ -2955,9 +2965,35 @@ static MgramPlan mgram_plan(int ncell, int ra, int rb) {
   return pl;
 }
 
+// symmetric Gram plan: 32-wide upper tiles, about 2 CTAs per SM over them
+static MgramPlan mgram_plan_sym(int ncell, int r) {
+  MgramPlan pl;
+  const int T = (r + 31) / 32;
+  pl.tb = 32;
+  pl.tiles = T * (T + 1) / 2;
+  const int target = (2 * 148 + pl.tiles - 1) / pl.tiles;
+  int cpb = (ncell + target - 1) / target;
+  cpb = (cpb + kMgC - 1) / kMgC * kMgC;
+  pl.cpb = cpb < kMgC ? kMgC : cpb;
+  pl.nblk = (ncell + pl.cpb - 1) / pl.cpb;
+  return pl;
+}
+
+// G[i][j] = G[j][i] below the diagonal tiles of a symmetric Gram
+__global__ void mirror_gram_kernel(int r, int tb, double* __restrict__ G) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < r * r; e += gridDim.x * blockDim.x) {
+    const int i = e / r, j = e % r;
+    if (i / tb > j / tb) G[e] = G[j * r + i];
+  }
+}
+
 int64_t dlrsn_partials_len(int ncell, int ra, int rb, int kind) {
   // partial buffer (doubles) for mgram (kind 0) / project (kind 1)
-  if (kind == 0) return (int64_t)mgram_plan(ncell, ra, rb).nblk * ra * rb;
+  if (kind == 0) {
+    int64_t nb = mgram_plan(ncell, ra, rb).nblk;
+    if (ra == rb && ra > 32) nb = std::max<int64_t>(nb, mgram_plan_sym(ncell, ra).nblk);
+    return nb * ra * rb;
+  }
   const int tiles = ((ra + kTile - 1) / kTile) * ((rb + kTile - 1) / kTile);
   const int cpb = cells_per_block(ncell, tiles);
   int64_t nblk = (ncell + cpb - 1) / cpb;
@@ -2974,9 +3010,33 @@ int dlrsn_mgram(const dlrsn_cellops* ops, int ra, int rb, const double* A, int l
                 const double* B, int ldb, const double* coeff, double* G, double* partial,
                 dlrsn_stream_t stream) {
   const int ncell = ops->nx * ops->ny;
+  cudaStream_t st = as_stream(stream);
+  static const char* sym_env = getenv("DLRSN_MGRAM_SYM");
+  if (A == B && lda == ldb && ra == rb && ra > 32 && sym_env && sym_env[0] == '1') {
+    // symmetric Gram: the 32-wide tiles on and above the diagonal only
+    // (T (T + 1) / 2 of T^2), mirrored after the reduction.  Off by default:
+    // measured slower than the 64-wide kernel over all tiles (C4 1.51 vs
+    // 2.46 ms, r = 128 25.4 vs 34.3 ms): the 32-wide tiles stage and
+    // premultiply each operand column block once per tile pair
+    const int T = (ra + 31) / 32, tiles = T * (T + 1) / 2;
+    const MgramPlan pl = mgram_plan_sym(ncell, ra);
+    const int vec = ((reinterpret_cast<uintptr_t>(A) | (uintptr_t)lda * 8) & 15) == 0;
+    const size_t smem = MgramWide<32>::smem(false);
+    DLRSN_TRY_CUDA(cudaFuncSetAttribute(mgram_wide_kernel<32>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    mgram_wide_kernel<32><<<dim3(pl.nblk, tiles), 256, smem, st>>>(ncell, ra, rb, A, lda, B, ldb,
+                                                                   coeff, *ops, pl.cpb, partial,
+                                                                   vec, 1);
+    DLRSN_CHECK_LAUNCH("mgram_wide_kernel");
+    const int64_t len = (int64_t)ra * rb;
+    reduce_partials_kernel<<<(unsigned)((len + 31) / 32), 1024, 0, st>>>(pl.nblk, len, partial, G, 1.0);
+    DLRSN_CHECK_LAUNCH("reduce_partials_kernel");
+    mirror_gram_kernel<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(ra, 32, G);
+    DLRSN_CHECK_LAUNCH("mirror_gram_kernel");
+    return DLRSN_OK;
+  }
   const MgramPlan pl = mgram_plan(ncell, ra, rb);
   const int nblk = pl.nblk;
-  cudaStream_t st = as_stream(stream);
   if (pl.tb == 0) {
     mgram_mma_kernel<<<dim3(nblk, pl.tiles), kTile * kTile, 0, st>>>(ncell, ra, rb, A, lda, B, ldb,
                                                                      coeff, *ops, pl.cpb, partial);
@@ -2990,13 +3050,15 @@ int dlrsn_mgram(const dlrsn_cellops* ops, int ra, int rb, const double* A, int l
       DLRSN_TRY_CUDA(cudaFuncSetAttribute(mgram_wide_kernel<64>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       mgram_wide_kernel<64><<<dim3(nblk, pl.tiles), 256, smem, st>>>(ncell, ra, rb, A, lda, B, ldb,
-                                                                     coeff, *ops, pl.cpb, partial, vec);
+                                                                     coeff, *ops, pl.cpb, partial, vec,
+                                                                     0);
     } else {
       const size_t smem = MgramWide<32>::smem(same);
       DLRSN_TRY_CUDA(cudaFuncSetAttribute(mgram_wide_kernel<32>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       mgram_wide_kernel<32><<<dim3(nblk, pl.tiles), 256, smem, st>>>(ncell, ra, rb, A, lda, B, ldb,
-                                                                     coeff, *ops, pl.cpb, partial, vec);
+                                                                     coeff, *ops, pl.cpb, partial, vec,
+                                                                     0);
     }
     DLRSN_CHECK_LAUNCH("mgram_wide_kernel");
   }

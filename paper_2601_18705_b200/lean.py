@@ -72,10 +72,33 @@ def rowmix_inplace(A, K, block_rows):
     return A
 
 
+class _Phases:
+    """Optional per-phase device timing of the lean step (DLRSN_LEAN_PROFILE=1,
+    printed to stderr): synchronises between phases, so off by default."""
+
+    def __init__(self):
+        self.on = bool(os.environ.get("DLRSN_LEAN_PROFILE"))
+        self.marks = []
+
+    def mark(self, name):
+        if self.on:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self.marks.append((name, ev))
+
+    def report(self):
+        if self.on and len(self.marks) > 1:
+            torch.cuda.synchronize()
+            parts = [f"{b[0]} {a[1].elapsed_time(b[1]):.1f}" for a, b in zip(self.marks, self.marks[1:])]
+            print("dlrsn lean ms: " + ", ".join(parts), file=sys.stderr)
+
+
 def step_lean(grid, step, quad, state, *, si_tol, si_max_iters, check_state, chunk=16,
               angle_indices=None, deim_tie_tol=0.0, block_rows=1 << 22):
     from .dlr_sn import CollocationStepInfo, _NativeSelection, project_operators
 
+    ph = _Phases()
+    ph.mark("start")
     r = state.rank
     n = grid.n_dofs
     X, S, W = state.X, state.S, state.W.values
@@ -91,7 +114,15 @@ def step_lean(grid, step, quad, state, *, si_tol, si_max_iters, check_state, chu
     flags = torch.stack([(st.sigma_t - st.sigma_s <= 0).any(), (st.sigma_s != 0).any()])
     parts = [err_idx.to(torch.float64), closure, flags.to(torch.float64), sel.gap_dev]
     if check_state:
-        parts.append(state.check_values(ops, quad))
+        # DlrState.check (lowrank.py:68-81); the spatial residual of an X this
+        # engine produced and checked (same tensor, unmodified) is reused
+        xc = getattr(state, "_xcheck", None)
+        if xc is not None and xc[1] is X and xc[2] == X._version and not state.W.pinned:
+            eye = torch.eye(r, dtype=torch.float64, device=X.device)
+            wq = quad.weights_device()
+            parts.append(torch.stack([xc[0], ((W * wq[:, None]).T @ W - eye).abs().max()]))
+        else:
+            parts.append(state.check_values(ops, quad))
     host = torch.cat(parts).cpu().numpy()
     deim_finish(sel, host[:r + 1], host[2 * r + 3:3 * r + 3])
     cw = host[r + 1:2 * r + 1].copy()
@@ -105,6 +136,7 @@ def step_lean(grid, step, quad, state, *, si_tol, si_max_iters, check_state, chu
     if angle_indices is None:
         check_ties(sel.gaps, deim_tie_tol)
     om_sel = quad.omegas[sel.indices]
+    ph.mark("deim+checks")
     # ---- the sweep, chunk by chunk (dlr_sn.py:110-121) --------------------
     K = S @ W[sel.indices_dev].T  # (r, r): psi_time = X K (evaluate_rows)
     psi = empty(n, r)
@@ -116,13 +148,17 @@ def step_lean(grid, step, quad, state, *, si_tol, si_max_iters, check_state, chu
         D = c1 - c0
         pt = cbuf[:n * D].view(n, D)
         rowmix(X, K[:, c0:c1].contiguous(), out=pt)
+        ph.mark(f"rowmix{c0}")
         plan = _SweepPlan(ops, om_sel[c0:c1], cw[c0:c1], dw=1)
         sk = skbuf[:D * vl]
         _lib.call("dlrsn_rhs_build", ops.cellops_ptr, D, _lib.ptr(plan.quads_dev), _lib.ptr(st.q),
                   float(st.inv_cdt), _lib.ptr(pt), D, None, 1, _lib.ptr(sk), stream())
+        ph.mark(f"rhs{c0}")
         _sweep(ops, plan, sk, sk)
+        ph.mark(f"sweep{c0}")
         _lib.call("dlrsn_sk_to_canonical", ops.cellops_ptr, D, _lib.ptr(plan.quads_dev),
                   _lib.ptr(sk), ctypes.c_void_p(psi.data_ptr() + 8 * c0), r, stream())
+        ph.mark(f"tocanon{c0}")
         raise_sweep_status(sweep_status_word(plan.workspace).item(), plan.workspace)
     del cbuf, skbuf
     # ---- K2 in place (Psi -> X_new): CholQR2 when its guard holds (every
@@ -130,11 +166,15 @@ def step_lean(grid, step, quad, state, *, si_tol, si_max_iters, check_state, chu
     # else the reference's exact CGS2 with deficiency / completion, in place
     R1, R1inv, ratio, flag = _chol(mass_gram(ops, psi))
     guard = torch.cat([ratio, flag.to(torch.float64)]).cpu().numpy()
+    ph.mark("gram1")
     sdef = 0
     if cholqr_guard_ok(guard, r):
         rowmix_inplace(psi, R1inv, block_rows)
+        ph.mark("rowmix1")
         R2, R2inv, _, flag2 = _chol(mass_gram(ops, psi))
+        ph.mark("gram2")
         rowmix_inplace(psi, R2inv, block_rows)
+        ph.mark("rowmix2")
         if int(flag2.item()):
             raise SolverError("lean step: second CholQR pass lost positive definiteness")
         gs_fallback = 0
@@ -148,7 +188,9 @@ def step_lean(grid, step, quad, state, *, si_tol, si_max_iters, check_state, chu
               file=sys.stderr)
     x_new = psi
     # ---- K3 + the reduced row system + the angular update (dlr_sn.py:126-141)
+    ph.mark("k2")
     proj, packed = project_operators(ops, x_new, x_old=X)
+    ph.mark("k3")
     w_sel = W[sel.indices_dev]
     q_all = (proj["q"][None, :] + st.inv_cdt * (w_sel @ (S.T @ proj["mo"]))).contiguous()
     om_dev = quad.omegas_device()[sel.indices_dev].contiguous()
@@ -161,8 +203,12 @@ def step_lean(grid, step, quad, state, *, si_tol, si_max_iters, check_state, chu
     parts = [row_status.to(torch.float64), defi_w[:r].to(torch.float64),
              status_w.to(torch.float64)]
     if check_state:
-        parts.append(new_state.check_values(ops, quad))
+        out_check = new_state.check_values(ops, quad)
+        parts.append(out_check)
+        new_state._xcheck = (out_check[0].clone(), x_new, x_new._version)
     host = torch.cat(parts).cpu().numpy()
+    ph.mark("rows+angular+check")
+    ph.report()
     raise_row_status(host[:r + 1], r)
     adef = host[r + 1:2 * r + 1]
     _cgs2_flags(adef, [host[2 * r + 1]], r)
