@@ -320,7 +320,8 @@ int dlrsn_row_combine(int n, int r, const double* Binv, const double* ms, const 
  * lowest row, as this kernel does; near-ties are where round-off can flip a
  * pick.  variant: 0 auto, 1 one-thread-per-row registers (n <= 1024,
  * r <= 16), 2 thread-block cluster (DSMEM), 3 one CTA over shared / global
- * memory (Wwork used when n r doubles exceed shared memory). */
+ * memory (Wwork used when n r doubles exceed shared memory), 4 one
+ * cooperative grid over all SMs (Wwork holds the per-CTA candidate slots). */
 int dlrsn_deim(int n, int r, double* Wwork, const double* W, int* idx, double* Lhat, double* U,
                int* err_col, double* gap, int variant, dlrsn_stream_t stream);
 

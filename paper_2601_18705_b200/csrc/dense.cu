@@ -2742,6 +2742,155 @@ __global__ void __launch_bounds__(kDeimCT) deim_cluster_kernel(int n, int r, int
   cl.sync();  // no CTA leaves while its slots may still be read
 }
 
+// DEIM over the whole GPU (node sets too large for a cluster's shared
+// memory, e.g. config 5's 16384 x 128 basis): one cooperative launch, CTA b
+// keeps rows [b nl, (b+1) nl) of W in shared memory (column-major).  Per pick
+// one grid barrier: every CTA publishes its best unpicked row (|residual|,
+// row, second best, the row's trailing entries) in a double-buffered global
+// slot; after the barrier every CTA reads all slots in CTA order, takes the
+// same winner (largest |residual|, lowest row on ties; np.argmax) and
+// eliminates its own rows, computing the next column's local argmax in the
+// same pass.  Per element the arithmetic is deim_kernel's.
+constexpr int kDeimGT = 256;
+__global__ void __launch_bounds__(kDeimGT) deim_grid_kernel(int n, int r, int nl,
+                                                          const double* __restrict__ W,
+                                                          int* __restrict__ idx,
+                                                          double* __restrict__ Lhat,
+                                                          double* __restrict__ U, int* err_col,
+                                                          double* __restrict__ gap,
+                                                          double* __restrict__ slots) {
+  cg::grid_group grid = cg::this_grid();
+  const int G = (int)gridDim.x, me = (int)blockIdx.x;
+  extern __shared__ double dsm[];
+  const int i0 = me * nl;
+  const int nloc = max(0, min(nl, n - i0));
+  const int ls = r + 3;                    // slot stride: value, row, second, entries
+  double* Wk = dsm;                        // r x nl, Wk[k * nl + i]
+  double* prow = Wk + (size_t)r * nl;      // r: the pivot row
+  unsigned char* picked = reinterpret_cast<unsigned char*>(prow + r);
+  __shared__ double wv[kDeimGT / 32], ws2[kDeimGT / 32];
+  __shared__ int wi[kDeimGT / 32];
+  __shared__ int s_idx[DLRSN_MAX_RANK];
+  __shared__ int s_p, s_fail;
+  __shared__ double s_floor;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = kDeimGT / 32;
+  for (int e = tid; e < nloc * r; e += kDeimGT) cp_async8(Wk + (e % r) * nl + e / r, W + (int64_t)i0 * r + e);
+  for (int i = tid; i < nl; i += kDeimGT) picked[i] = 0;
+  cp_async_wait_all();
+  __syncthreads();
+  // floor = 1e-14 max(1, max |W|) (lowrank.py:182), via slot column 0
+  double mx = 0.0;
+  for (int e = tid; e < nloc * r; e += kDeimGT) mx = fmax(mx, fabs(Wk[(e % r) * nl + e / r]));
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
+  if (lane == 0) wv[w] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int q = 0; q < nw; ++q) m = fmax(m, wv[q]);
+    slots[(int64_t)2 * G * ls + me] = m;  // scratch after the two slot buffers
+  }
+  grid.sync();
+  if (w == 0) {
+    double m = 0.0;
+    for (int q = lane; q < G; q += 32) m = fmax(m, __ldcg(slots + (int64_t)2 * G * ls + q));
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(kFull, m, o));
+    if (lane == 0) s_floor = 1e-14 * fmax(1.0, m);
+  }
+  // local argmax of column 0
+  double best = -1.0, second = -1.0;
+  int bidx = 0x7fffffff;
+  for (int i = tid; i < nloc; i += kDeimGT) {
+    const double v = fabs(Wk[i]);
+    if (v > best) { second = best; best = v; bidx = i0 + i; }
+    else if (v > second) second = v;
+  }
+  int fail = -1;
+  for (int j = 0; j < r; ++j) {
+    double* mine = slots + ((int64_t)(j & 1) * G + me) * ls;
+    top2_warp(best, bidx, second);
+    if (lane == 0) { wv[w] = best; wi[w] = bidx; ws2[w] = second; }
+    __syncthreads();
+    if (w == 0) {
+      double b = lane < nw ? wv[lane] : -1.0;
+      int bi = lane < nw ? wi[lane] : 0x7fffffff;
+      double sb = lane < nw ? ws2[lane] : -1.0;
+      top2_warp(b, bi, sb);
+      if (lane == 0) { mine[0] = b; mine[1] = (double)bi; mine[2] = sb; }
+      const bool have = bi >= i0 && bi < i0 + nloc;
+      for (int k = j + lane; k < r; k += 32) mine[3 + k] = have ? Wk[k * nl + (bi - i0)] : 0.0;
+    }
+    grid.sync();
+    if (w == 0) {
+      // every CTA reduces the G slots in the same order: identical winner
+      double b = -1.0, sb = -1.0;
+      int bi = 0x7fffffff, src = 0;
+      for (int q = lane; q < G; q += 32) {
+        const double* sl = slots + ((int64_t)(j & 1) * G + q) * ls;
+        const double ob = __ldcg(sl), osb = __ldcg(sl + 2);
+        const int oi = (int)__ldcg(sl + 1);
+        const bool take = ob > b || (ob == b && oi < bi);
+        top2_merge(b, bi, sb, ob, oi, osb);
+        if (take) src = q;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(kFull, b, o);
+        const int oi = __shfl_xor_sync(kFull, bi, o);
+        const double osb = __shfl_xor_sync(kFull, sb, o);
+        const int os = __shfl_xor_sync(kFull, src, o);
+        const bool take = ov > b || (ov == b && oi < bi);
+        top2_merge(b, bi, sb, ov, oi, osb);
+        if (take) src = os;
+      }
+      const bool valid = bi >= 0 && bi < n;
+      if (valid) {
+        const double* win = slots + ((int64_t)(j & 1) * G + src) * ls;
+        for (int k = j + lane; k < r; k += 32) prow[k] = __ldcg(win + 3 + k);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const double pv = valid ? prow[j] : 0.0;
+        s_p = valid ? bi : 0;
+        s_fail = !(valid && fabs(pv) > s_floor);
+        if (gap && me == 0) gap[j] = top2_gap(b, sb);
+      }
+    }
+    __syncthreads();
+    const int p = s_p;
+    if (me == 0 && tid == 0) idx[j] = p;
+    if (tid == 0) s_idx[j] = p;
+    if (s_fail) { fail = j; break; }
+    if (me == 0)
+      for (int k = tid; k < r; k += kDeimGT) U[j * r + k] = k >= j ? prow[k] : 0.0;
+    const double pv = prow[j];
+    const int pl = p - i0;
+    if (tid == 0 && pl >= 0 && pl < nloc) picked[pl] = 1;
+    best = second = -1.0;
+    bidx = 0x7fffffff;
+    for (int i = tid; i < nloc; i += kDeimGT) {
+      if (i == pl || picked[i]) continue;
+      const double l = Wk[j * nl + i] / pv;
+      Wk[j * nl + i] = l;  // the multiplier column (Lhat entries)
+      for (int k = j + 1; k < r; ++k) Wk[k * nl + i] -= l * prow[k];
+      if (j + 1 < r) {
+        const double v = fabs(Wk[(j + 1) * nl + i]);
+        if (v > best) { second = best; best = v; bidx = i0 + i; }
+        else if (v > second) second = v;
+      }
+    }
+    __syncthreads();  // prow / picked of this pick are consumed
+  }
+  if (fail < 0) {
+    // Lhat[q, j] = multiplier of column j at the q-th picked row (unit lower)
+    for (int e = tid; e < r * r; e += kDeimGT) {
+      const int q = e / r, jj = e % r;
+      const int pl = s_idx[q] - i0;
+      if (pl < 0 || pl >= nloc) continue;
+      Lhat[e] = jj < q ? Wk[jj * nl + pl] : (jj == q ? 1.0 : 0.0);
+    }
+  }
+  if (me == 0 && tid == 0) *err_col = fail;
+}
+
 // Solves with W_hat = Lhat U (pick order):
 //   mode 0 (interpolation_coefficients): X = W_hat^-1 V   (V r x m)
 //   mode 1 (closure_weights):            x = W_hat^-T v   (v r)
@@ -3307,7 +3456,7 @@ int dlrsn_deim(int n, int r, double* Wwork, const double* W, int* idx, double* L
                int* err_col, double* gap, int variant, dlrsn_stream_t stream) {
   DLRSN_REQUIRE(r <= n, "rank %d exceeds the %d available nodes", r, n);
   DLRSN_REQUIRE(r <= DLRSN_MAX_RANK, "rank %d exceeds DLRSN_MAX_RANK", r);
-  DLRSN_REQUIRE(variant >= 0 && variant <= 3, "unknown DEIM variant %d", variant);
+  DLRSN_REQUIRE(variant >= 0 && variant <= 4, "unknown DEIM variant %d", variant);
   static const char* ereg = getenv("DLRSN_DEIM_REG");
   const bool reg_ok = n <= 1024 && r <= 16;
   DLRSN_REQUIRE(variant != 1 || reg_ok, "register DEIM needs n <= 1024, r <= 16");
@@ -3370,6 +3519,32 @@ int dlrsn_deim(int n, int r, double* Wwork, const double* W, int* idx, double* L
                                       gap));
     DLRSN_CHECK_LAUNCH("deim_cluster_kernel");
     return DLRSN_OK;
+  }
+  // grid variant: rows spread over the GPU's SMs (one cooperative launch)
+  {
+    static int sms = 0;
+    if (sms == 0) {
+      int dev = 0;
+      DLRSN_TRY_CUDA(cudaGetDevice(&dev));
+      DLRSN_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    int G = std::min(sms, std::max(1, (n + 63) / 64));
+    const int nl = (n + G - 1) / G;
+    G = (n + nl - 1) / nl;
+    const size_t gsm = ((size_t)nl * r + r) * sizeof(double) + nl;
+    const bool g_ok = gsm <= 200 * 1024 && Wwork != nullptr &&
+                      (int64_t)n * r >= (int64_t)2 * G * (r + 3) + G;
+    DLRSN_REQUIRE(variant != 4 || g_ok, "grid DEIM does not fit n = %d, r = %d", n, r);
+    if (variant == 4 || (variant == 0 && g_ok && (int64_t)n * r * 8 > 200 * 1024)) {
+      DLRSN_TRY_CUDA(cudaFuncSetAttribute(deim_grid_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
+      int nn = n, rr = r, nll = nl;
+      void* args[] = {&nn, &rr, &nll, (void*)&W, &idx, &Lhat, &U, &err_col, &gap, &Wwork};
+      DLRSN_TRY_CUDA(cudaLaunchCooperativeKernel((void*)deim_grid_kernel, dim3(G), dim3(kDeimGT),
+                                                 args, gsm, as_stream(stream)));
+      DLRSN_CHECK_LAUNCH("deim_grid_kernel");
+      return DLRSN_OK;
+    }
   }
   const size_t smem = (size_t)n * r * sizeof(double) + (size_t)n;
   const int in_smem = smem <= 200 * 1024;

@@ -290,7 +290,7 @@ class DeimSelection:
         return x[:, 0]
 
 
-DEIM_VARIANTS = {"auto": 0, "register": 1, "cluster": 2, "block": 3}
+DEIM_VARIANTS = {"auto": 0, "register": 1, "cluster": 2, "block": 3, "grid": 4}
 
 
 def deim_select(basis_values, *, variant="auto", tie_tol=0.0):
