@@ -56,20 +56,16 @@ from .lowrank import (
 from .transport import _SweepPlan, _sweep, assemble_operators, raise_sweep_status, sweep_status_word
 
 
-def rowmix_inplace(A, K, block_rows):
-    """A <- A K (K square) through a row-block buffer (the rows of a block
-    are read before they are rewritten; no full-size temporary)."""
-    n = A.shape[0]
-    buf = None
-    for r0 in range(0, n, block_rows):
-        r1 = min(n, r0 + block_rows)
-        blk = A[r0:r1]
-        if buf is None or buf.shape[0] < r1 - r0:
-            buf = empty(min(block_rows, n), A.shape[1])
-        out = buf[:r1 - r0]
-        rowmix(blk, K, out=out)
-        blk.copy_(out)
-    return A
+def rowmix_inplace(A, K, block_rows=None):
+    """A <- A K (K square) in place: the rowmix kernels load every row of a
+    warp's row tile (all kx columns, into registers) before writing that
+    tile's outputs, and no other warp touches those rows, so Y = X is safe
+    (each element is read once, then written once, by the same warp).  The
+    one-thread-per-element fallback (n < 64) is not: it goes through a copy."""
+    if A.shape[0] < 64 or A.shape[1] > 128:
+        A.copy_(rowmix(A, K))
+        return A
+    return rowmix(A, K, out=A)
 
 
 class _Phases:
@@ -93,8 +89,19 @@ class _Phases:
             print("dlrsn lean ms: " + ", ".join(parts), file=sys.stderr)
 
 
-def step_lean(grid, step, quad, state, *, si_tol, si_max_iters, check_state, chunk=16,
-              angle_indices=None, deim_tie_tol=0.0, block_rows=1 << 22):
+def _chunk_width(n, r, vl, limit=16):
+    """Directions per sweep chunk: as many as fit next to the chunk's two
+    buffers (psi_time n x D, SK rhs / psi D x vl) in the free device memory,
+    up to ``limit`` (each chunk re-reads X once; 32 at config 5 leaves too
+    little headroom for the projections' workspace)."""
+    free, _ = torch.cuda.mem_get_info()
+    per = 8 * (n + vl)
+    fit = int(0.9 * free) // per
+    return max(1, min(limit, r, fit))
+
+
+def step_lean(grid, step, quad, state, *, si_tol, si_max_iters, check_state, chunk=None,
+              angle_indices=None, deim_tie_tol=0.0, block_rows=None):
     from .dlr_sn import CollocationStepInfo, _NativeSelection, project_operators
 
     ph = _Phases()
@@ -141,6 +148,9 @@ def step_lean(grid, step, quad, state, *, si_tol, si_max_iters, check_state, chu
     K = S @ W[sel.indices_dev].T  # (r, r): psi_time = X K (evaluate_rows)
     psi = empty(n, r)
     vl = ops.vec_len
+    if chunk is None:
+        env = os.environ.get("DLRSN_LEAN_CHUNK")
+        chunk = int(env) if env else _chunk_width(n, r, vl)
     cbuf = empty(n * chunk)  # psi_time of a chunk, then the row-block buffer
     skbuf = empty(chunk * vl)  # rhs -> psi (in place), SK layout
     for c0 in range(0, r, chunk):
