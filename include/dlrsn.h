@@ -412,6 +412,10 @@ typedef struct dlrsn_step_params {
   int angle_override;        /* 1: use angle_indices_in instead of the DEIM picks
                                 (forced-selection parity, lowrank.py:168-205 hazard (i)) */
   const int64_t* angle_indices_in; /* HOST, r entries, read when angle_override */
+  double* x_new_host;        /* HOST pinned (n_dofs x r), optional: X_new is copied here on a
+                                copy stream as soon as it is final (after K2), overlapping the
+                                projections and the angular update; the call returns after the
+                                copy (a caller holding its state in host memory) */
 } dlrsn_step_params;
 
 typedef struct dlrsn_step_info { /* HOST, filled by the call */

@@ -51,7 +51,7 @@ class StepParams(ctypes.Structure):
                 ("si_max_iters", c_int), ("check_state", c_int), ("gs_method", c_int),
                 ("sweep_dw", c_int), ("advance", c_vp), ("inflow", c_dbl * 4),
                 ("x_check_in", c_vp), ("x_check_out", c_vp), ("si_batch_hint", c_int),
-                ("angle_override", c_int), ("angle_indices_in", c_vp)]
+                ("angle_override", c_int), ("angle_indices_in", c_vp), ("x_new_host", c_vp)]
 
 
 class StepInfo(ctypes.Structure):

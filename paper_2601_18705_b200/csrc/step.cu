@@ -559,6 +559,22 @@ static int join_from(const Fork* f, cudaStream_t st) {
   return DLRSN_OK;
 }
 
+// ---- X_new device-to-host copy overlapped with the rest of the step --------
+struct OutCopy {
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ready = nullptr, done = nullptr;
+};
+static int out_copy_stream(OutCopy** out) {
+  static thread_local OutCopy oc;
+  if (!oc.cs) {
+    DLRSN_TRY_CUDA(cudaStreamCreateWithFlags(&oc.cs, cudaStreamNonBlocking));
+    DLRSN_TRY_CUDA(cudaEventCreateWithFlags(&oc.ready, cudaEventDisableTiming));
+    DLRSN_TRY_CUDA(cudaEventCreateWithFlags(&oc.done, cudaEventDisableTiming));
+  }
+  *out = &oc;
+  return DLRSN_OK;
+}
+
 // ---- CUDA-graph replay of the step's first segment --------------------------
 // The segment's ~50 launches depend only on the buffers, the parameters and
 // the iteration batch; a driver loop hands the same buffers back every other
@@ -1016,6 +1032,15 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
       DLRSN_RET(dlrsn_cgs2((int)N, r, b.psi, r, X_new, r, b.Rtot, b.defx, 1, nullptr, ops, 1,
                            r + 8, b.up->sexp, b.up->extent, b.cgsws, b.statx, 1, s));
     }
+    OutCopy* oc = nullptr;
+    if (p->x_new_host) {  // X_new is final: its host copy runs under the rest of the step
+      DLRSN_RET(out_copy_stream(&oc));
+      DLRSN_TRY_CUDA(cudaEventRecord(oc->ready, st));
+      DLRSN_TRY_CUDA(cudaStreamWaitEvent(oc->cs, oc->ready, 0));
+      DLRSN_TRY_CUDA(cudaMemcpyAsync(p->x_new_host, X_new, (size_t)N * r * sizeof(double),
+                                     cudaMemcpyDeviceToHost, oc->cs));
+      DLRSN_TRY_CUDA(cudaEventRecord(oc->done, oc->cs));
+    }
     DLRSN_RET(dlrsn_project(ops, r, X_new, X, sigma_t, sigma_s, q, b.proj, b.part, s));
     if (has_inflow) DLRSN_RET(dlrsn_inflow_project(ops, r, X_new, r, p->inflow, b.hin, s));
     qall_kernel<<<1, 256, 0, st>>>(r, S, b.proj + 6 * r * r, b.proj + 7 * r * r, W, b.idx,
@@ -1065,6 +1090,7 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
       ortho_residual_kernel<<<1, 256, 0, st>>>(r, b.G, b.wg, b.chk_out, nullptr, p->x_check_out);
       DLRSN_CHECK_LAUNCH("ortho_residual_kernel");
     }
+    if (oc) DLRSN_TRY_CUDA(cudaStreamWaitEvent(st, oc->done, 0));  // join the host copy
     return enqueue_status(st, b, r, hs, sweep_ws);
   };
 

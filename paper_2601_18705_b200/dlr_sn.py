@@ -127,7 +127,7 @@ def project_initial(state, x_new, ops):
 def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, use_dsa=True,
                      dsa_penalty="simplified", threads=0, check_state=True, gs_method="cholqr2",
                      sweep_dw=None, comm=None, engine="native", inflow=None, angle_indices=None,
-                     deim_tie_tol=DEIM_TIE_TOL, _advance=None):
+                     deim_tie_tol=DEIM_TIE_TOL, _advance=None, _x_new_host=None):
     """Advance one linearised step; returns (new DlrState, CollocationStepInfo).
 
     ``engine="native"`` issues the whole step from C++ through the single
@@ -175,7 +175,7 @@ def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, 
             raise ContractViolation(f"unknown dsa penalty variant {dsa_penalty!r}")
         return _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state,
                             gs_method, sweep_dw, comm, _advance, inflow_values(inflow),
-                            angle_indices, deim_tie_tol)
+                            angle_indices, deim_tie_tol, _x_new_host)
     if inflow_values(inflow) is not None:
         raise ConfigurationError("inflow boundaries need the native engine")
     if _advance is not None:
@@ -469,7 +469,8 @@ def _native_ctx(grid, quad, r, comm):
 
 
 def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_method, sweep_dw,
-                 comm, advance=None, inflow=None, angle_indices=None, deim_tie_tol=DEIM_TIE_TOL):
+                 comm, advance=None, inflow=None, angle_indices=None, deim_tie_tol=DEIM_TIE_TOL,
+                 x_new_host=None):
     r = state.rank
     no = quad.n_angles
     n = grid.n_dofs
@@ -495,6 +496,13 @@ def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_
     p.advance = ctypes.addressof(advance) if advance is not None else None
     p.inflow[:] = inflow if inflow is not None else (0.0, 0.0, 0.0, 0.0)
     p.si_batch_hint = ctx.si_hint
+    if x_new_host is not None:
+        if (not x_new_host.is_pinned() or x_new_host.dtype != torch.float64
+                or tuple(x_new_host.shape) != (n, r) or not x_new_host.is_contiguous()):
+            raise ContractViolation("x_new_host must be a contiguous pinned fp64 (n_dofs, r) tensor")
+        p.x_new_host = x_new_host.data_ptr()
+    else:
+        p.x_new_host = None
     forced = None
     if angle_indices is not None:
         forced = np.ascontiguousarray(angle_indices, dtype=np.int64).reshape(-1)
@@ -523,6 +531,7 @@ def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_
         ob + 8 * ctx.offs[4], ob + 8 * ctx.offs[5], ctx.ws.data_ptr(), ctx.ws.numel(),
         ctx.sws.data_ptr(), ctx.sws.numel(), ctx.comm_ref, ctypes.byref(info), stream())
     p.angle_override, p.angle_indices_in = 0, None
+    p.x_new_host = None
     if rc == 0 or rc == -7:
         ctx.si_hint = max(ctx.si_hint, int(info.si_batch_hint))
     if hooks is not None and hooks.error is not None:

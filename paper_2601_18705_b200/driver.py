@@ -95,7 +95,7 @@ class DeviceProblem:
 
 
     def step(self, state, lin, T, *, si_tol=1e-8, si_max_iters=200, check_state=True,
-             gs_method="cholqr2", comm=None, engine="native"):
+             gs_method="cholqr2", comm=None, engine="native", x_new_host=None):
         """One DLR step and the step boundary (T update + re-linearisation)
         in a single native call (the fused form of step_collocation +
         advance, driver.py:486-487,532-534).  Returns (state, next
@@ -132,7 +132,8 @@ class DeviceProblem:
         state, info = step_collocation(self.grid, lin, self.quad, state, si_tol=si_tol,
                                        si_max_iters=si_max_iters, use_dsa=False,
                                        check_state=check_state, gs_method=gs_method, comm=comm,
-                                       inflow=self.spec.inflow, _advance=av)
+                                       inflow=self.spec.inflow, _advance=av,
+                                       _x_new_host=x_new_host)
         k = self.constants
         nxt = LinearizedStep(sigma_t=st, sigma_s=ss, sigma_a=sa, q=q, T0=T0, denom=den,
                              rho_cv=self.rho_cv, dt=float(self.spec.dt),

@@ -542,3 +542,24 @@ def test_projections_match_oracle_wide(nx, ny, r):
     ref["mo"] = Xo.T @ pops.mass_apply(X)
     for k in ("px", "py", "jx", "jy", "mt", "ms", "mo", "q"):
         assert rel_l2(_np(proj[k]), ref[k]) <= 1e-13, k
+
+
+def test_step_copies_x_new_to_host_inside_the_call():
+    """x_new_host: the native step reads X_new back on a copy stream as soon
+    as it is final; the host copy equals the device result bitwise, for a
+    graph-replayed chain of steps too."""
+    from paper_2601_18705_b200 import problems
+    from paper_2601_18705_b200.driver import DeviceProblem, initial_state
+
+    spec = problems.checkerboard(4, rank=8, n_polar=4, n_azimuthal=8, seed=9)
+    dp = DeviceProblem.from_spec(spec)
+    st = initial_state(dp)
+    T = torch.as_tensor(spec.T0, device="cuda").clone()
+    lin = dp.linearized(T)
+    bufs = [torch.empty(spec.n_dofs, spec.rank, dtype=torch.float64, pin_memory=True)
+            for _ in range(2)]
+    for k in range(6):
+        host = bufs[k % 2]
+        host.fill_(float("nan"))
+        st, lin, T, info = dp.step(st, lin, T, si_tol=1e-10, x_new_host=host)
+        assert torch.equal(host, st.X.cpu()), k
