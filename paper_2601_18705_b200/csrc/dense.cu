@@ -268,6 +268,98 @@ __global__ void __launch_bounds__(256, (4 * KS + 8 * NT <= 96) ? 2 : 1) rowmix_w
   }
 }
 
+// rowmix by an upper-triangular K (r x r, exact zeros below the diagonal:
+// the CholQR2 factors R^-1): Y = X K with the MMA k index in natural order
+// (lane quad q owns columns 4 ks + q), so k step ks meets column group nt
+// only when 4 ks <= 8 nt + 7 -- 72 of 128 DMMA fragments at r = 64.
+template <int KS, int NT>
+__global__ void __launch_bounds__(256, 1) rowmix_upper_kernel(int n, int r,
+                                                           const double* __restrict__ X, int ldx,
+                                                           const double* __restrict__ K, int ldk,
+                                                           double* __restrict__ Y, int ldy,
+                                                           int ldks) {
+  static_assert(4 * KS == 8 * NT, "square K tile");
+  extern __shared__ double sK[];  // (4 KS) x ldks
+  for (int e = threadIdx.x; e < 4 * KS * 8 * NT; e += blockDim.x) {
+    const int k = e / (8 * NT), col = e - k * (8 * NT);
+    sK[k * ldks + col] = (k < r && col < r) ? __ldg(K + (int64_t)k * ldk + col) : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int64_t tiles = ((int64_t)n + 7) / 8;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool vstore = ((ldy & 1) == 0) && ((reinterpret_cast<uintptr_t>(Y) & 15) == 0);
+  for (int64_t t0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 2; t0 < tiles;
+       t0 += 2 * nwarps) {
+    double af[2][KS];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t row = (t0 + u) * 8 + g;
+      const double* xr = X + row * ldx + q;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks)
+        af[u][ks] = (row < n && 4 * ks + q < r) ? __ldg(xr + 4 * ks) : 0.0;
+    }
+    double d[2][NT][2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) d[u][nt][0] = d[u][nt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const double* kr = sK + (4 * ks + q) * ldks + g;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        if (ks > 2 * nt + 1) continue;  // K rows 4 ks.. lie below columns 8 nt..8 nt + 7
+        const double b = kr[8 * nt];
+        dmma(d[0][nt][0], d[0][nt][1], af[0][ks], b);
+        dmma(d[1][nt][0], d[1][nt][1], af[1][ks], b);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t row = (t0 + u) * 8 + g;
+      if (row >= n) continue;
+      double* y = Y + row * ldy;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int c = 8 * nt + 2 * q;
+        if (vstore && c + 1 < r) {
+          *reinterpret_cast<double2*>(y + c) = make_double2(d[u][nt][0], d[u][nt][1]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+            if (c + i < r) y[c + i] = d[u][nt][i];
+        }
+      }
+    }
+  }
+}
+
+int rowmix_upper(int64_t n, int r, const double* X, int ldx, const double* K, int ldk, double* Y,
+                 int ldy, cudaStream_t st) {
+  if (r <= 16 || r > 64 || n < 64)
+    return dlrsn_rowmix(n, r, r, X, ldx, K, ldk, 0.0, Y, ldy, st);
+  const int64_t tiles = (n + 7) / 8;
+  int64_t blocks = (tiles + 15) / 16;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  if (r <= 32) {
+    constexpr int KS = 8, NT = 4;
+    const int ldks = 32 + 4;
+    const size_t smem = (size_t)4 * KS * ldks * sizeof(double);
+    rowmix_upper_kernel<KS, NT><<<(int)blocks, 256, smem, st>>>((int)n, r, X, ldx, K, ldk, Y, ldy, ldks);
+  } else {
+    constexpr int KS = 16, NT = 8;
+    const int ldks = 64 + 4;
+    const size_t smem = (size_t)4 * KS * ldks * sizeof(double);
+    DLRSN_TRY_CUDA(cudaFuncSetAttribute(rowmix_upper_kernel<KS, NT>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    rowmix_upper_kernel<KS, NT><<<(int)blocks, 256, smem, st>>>((int)n, r, X, ldx, K, ldk, Y, ldy, ldks);
+  }
+  DLRSN_CHECK_LAUNCH("rowmix_upper_kernel");
+  return DLRSN_OK;
+}
+
 // ---------------------------------------------------------------------------
 // mgram: G (ra x rb) = sum_c coeff_c * A_c^T M B_c; A_c = rows 4c..4c+3.
 // Block = one chunk of cells x one (TI x TJ) output tile; thread (i, j) of
@@ -481,7 +573,7 @@ __global__ void __launch_bounds__(256, 1) mgram_wide_kernel(int ncell, int ra, i
   const int wi = wt / (TB / 32), wj = wt % (TB / 32);
   const int tiles_j = (rb + TB - 1) / TB;
   int i0 = (blockIdx.y / tiles_j) * TB, j0 = (blockIdx.y % tiles_j) * TB;
-  if (sym) {  // symmetric Gram (A == B): blockIdx.y walks the tiles ti <= tj
+  if (sym & 1) {  // symmetric Gram (A == B): blockIdx.y walks the tiles ti <= tj
     int y = blockIdx.y, ti = 0;
     while (y >= tiles_j - ti) {
       y -= tiles_j - ti;
@@ -493,6 +585,9 @@ __global__ void __launch_bounds__(256, 1) mgram_wide_kernel(int ncell, int ra, i
   const int c_begin = blockIdx.x * cells_per_block;
   const int c_end = min(ncell, c_begin + cells_per_block);
   const bool same = (A == B) && (lda == ldb) && (i0 == j0);
+  // diagonal tile of a symmetric Gram (64-wide): upper 8 x 8 fragments only
+  // (36 of 64 DMMA fragments), the lower ones mirrored at the write-out
+  const bool fsym = TB == 64 && same && !(sym & 2);
   double* sA0 = smw;
   double* sBm = smw + 2 * PL;   // B' (premultiplied)
   double* sBr0 = smw + 3 * PL;  // raw B x2 (separate operands)
@@ -556,41 +651,96 @@ __global__ void __launch_bounds__(256, 1) mgram_wide_kernel(int ncell, int ra, i
       }
     }
     __syncthreads();
+    if (fsym && wt < 2) {
+      // symmetric diagonal tile, rows 16 wt .. 16 wt + 15 x columns 32..63
 #pragma unroll
-    for (int k = 0; k < CPK; ++k) {
-      const int cl = kp * CPK + k;
-      const double* ar = sA + (4 * cl + q) * LD + 32 * wi + g;
-      const double* br = sBm + (4 * cl + q) * LD + 32 * wj + g;
-      double af[4], bf[4];
+      for (int k = 0; k < CPK; ++k) {
+        const int cl = kp * CPK + k;
+        const double* ar = sA + (4 * cl + q) * LD + 16 * wt + g;
+        const double* br = sBm + (4 * cl + q) * LD + 32 + g;
+        double af[2], bf[4];
+        af[0] = ar[0];
+        af[1] = ar[8];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        af[t] = ar[8 * t];
-        bf[t] = br[8 * t];
+        for (int t = 0; t < 4; ++t) bf[t] = br[8 * t];
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) dmma(d[a][b][0], d[a][b][1], af[a], bf[b]);
       }
+    } else if (fsym) {
+      // symmetric diagonal tile, the diagonal 32 x 32 quadrant wt - 2: the
+      // 8 x 8 fragments on and above its diagonal
+      const int base = 32 * (wt - 2);
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int k = 0; k < CPK; ++k) {
+        const int cl = kp * CPK + k;
+        const double* ar = sA + (4 * cl + q) * LD + base + g;
+        const double* br = sBm + (4 * cl + q) * LD + base + g;
+        double af[4], bf[4];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) dmma(d[a][b][0], d[a][b][1], af[a], bf[b]);
+        for (int t = 0; t < 4; ++t) {
+          af[t] = ar[8 * t];
+          bf[t] = br[8 * t];
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = a; b < 4; ++b) dmma(d[a][b][0], d[a][b][1], af[a], bf[b]);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < CPK; ++k) {
+        const int cl = kp * CPK + k;
+        const double* ar = sA + (4 * cl + q) * LD + 32 * wi + g;
+        const double* br = sBm + (4 * cl + q) * LD + 32 * wj + g;
+        double af[4], bf[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          af[t] = ar[8 * t];
+          bf[t] = br[8 * t];
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) dmma(d[a][b][0], d[a][b][1], af[a], bf[b]);
+      }
     }
     __syncthreads();  // this chunk's planes are free for the next issue
   }
   double* red = smw;  // [KP][TB][TB + 1]
+  if (fsym) {
+    const int r0 = wt < 2 ? 16 * wt : 32 * (wt - 2), c0 = wt < 2 ? 32 : 32 * (wt - 2);
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
+      for (int b = 0; b < 4; ++b) {
+        if (wt < 2 ? a >= 2 : b < a) continue;
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
-        red[(kp * TB + 32 * wi + 8 * a + g) * (TB + 1) + 32 * wj + 8 * b + 2 * q + i] = d[a][b][i];
+        for (int i = 0; i < 2; ++i)
+          red[(kp * TB + r0 + 8 * a + g) * (TB + 1) + c0 + 8 * b + 2 * q + i] = d[a][b][i];
+      }
+  } else {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+          red[(kp * TB + 32 * wi + 8 * a + g) * (TB + 1) + 32 * wj + 8 * b + 2 * q + i] = d[a][b][i];
+  }
   __syncthreads();
   double* out = part + (int64_t)blockIdx.x * ra * rb;
   for (int e = threadIdx.x; e < TB * TB; e += 256) {
     const int ii = e / TB, jj = e % TB;
     const int i = i0 + ii, j = j0 + jj;
     if (i >= ra || j >= rb) continue;
+    // symmetric diagonal tile: fragments below the diagonal from their mirror
+    const bool low = fsym && (ii >> 3) > (jj >> 3);
+    const int si = low ? jj : ii, sj = low ? ii : jj;
     double v = 0.0;
 #pragma unroll
-    for (int p = 0; p < KP; ++p) v += red[(p * TB + ii) * (TB + 1) + jj];
+    for (int p = 0; p < KP; ++p) v += red[(p * TB + si) * (TB + 1) + sj];
     out[(int64_t)i * rb + j] = v;
   }
 }
@@ -1760,61 +1910,73 @@ __global__ void chol_upper_kernel(int r, const double* __restrict__ G, double* _
   double* a = sm;          // r*r working copy (becomes R)
   // r > 110: the inverse is built in place in Rinv (global, L2-resident)
   double* inv = inv_in_global ? Rinv : sm + r * r;
-  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
-    a[e] = G[e];
-    inv[e] = 0.0;
-  }
-  __syncthreads();
+  __shared__ double gdiag[DLRSN_MAX_RANK];  // G_kk (the deficiency test's norms)
+  __shared__ double rdiag[DLRSN_MAX_RANK];  // 1 / R_kk (0 for a failed pivot)
   __shared__ int bad;
-  if (threadIdx.x == 0) bad = 0;
+  const int tid = threadIdx.x, bs = blockDim.x;
+  for (int e = tid; e < r * r; e += bs) {
+    const int i = e / r, j = e % r;
+    const double g = G[e];
+    a[e] = g;
+    inv[e] = i == j ? 1.0 : 0.0;
+    if (i == j) gdiag[i] = g;
+  }
+  if (tid == 0) bad = 0;
   __syncthreads();
+  // Two barriers per column: (A) every thread reads the pivot and scales
+  // its part of row k; (B) the trailing update of the upper part, and the
+  // pivot's own entries written by thread 0.
+  const int warp = tid >> 5, lane = tid & 31, nw = bs >> 5;
   for (int k = 0; k < r; ++k) {
-    if (threadIdx.x == 0) {
-      const double d = a[k * r + k];
-      const double g = G[k * r + k];
-      if (!(d > 0.0)) {
-        bad = 1;
-        a[k * r + k] = 0.0;
-        diag_ratio[k] = 0.0;
-        diag_ratio[r + k] = 0.0;
-      } else {
-        a[k * r + k] = sqrt(d);
-        const double on = sqrt(fmax(g, 0.0));
-        diag_ratio[k] = on > 0.0 ? a[k * r + k] / on : 0.0;
-        diag_ratio[r + k] = a[k * r + k] / fmax(on, 1.0);
-      }
+    const double d = a[k * r + k];
+    const bool ok = d > 0.0;
+    const double rkk = ok ? sqrt(d) : 0.0;
+    for (int j = k + 1 + tid; j < r; j += bs) a[k * r + j] = rkk > 0 ? a[k * r + j] / rkk : 0.0;
+    __syncthreads();
+    if (tid == 0) {
+      a[k * r + k] = rkk;
+      rdiag[k] = ok ? 1.0 / rkk : 0.0;
+      if (!ok) bad = 1;
+      const double on = sqrt(fmax(gdiag[k], 0.0));
+      diag_ratio[k] = ok && on > 0.0 ? rkk / on : 0.0;
+      diag_ratio[r + k] = ok ? rkk / fmax(on, 1.0) : 0.0;
     }
-    __syncthreads();
-    const double rkk = a[k * r + k];
-    for (int j = k + 1 + threadIdx.x; j < r; j += blockDim.x) a[k * r + j] = rkk > 0 ? a[k * r + j] / rkk : 0.0;
-    __syncthreads();
-    // trailing update a[i][j] -= a[k][i] a[k][j], i,j > k (upper part only)
-    const int m = r - k - 1;
-    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-      const int i = k + 1 + e / m, j = k + 1 + e % m;
-      if (j >= i) a[i * r + j] -= a[k * r + i] * a[k * r + j];
+    // a[i][j] -= a[k][i] a[k][j] for k < i <= j (a warp per row)
+    for (int i = k + 1 + warp; i < r; i += nw) {
+      const double aki = a[k * r + i];
+      for (int j = i + lane; j < r; j += 32) a[i * r + j] -= aki * a[k * r + j];
     }
     __syncthreads();
   }
   // R: zero the strict lower part
-  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+  for (int e = tid; e < r * r; e += bs) {
     const int i = e / r, j = e % r;
     R[e] = j >= i ? a[e] : 0.0;
   }
+  // R^-1 by right-looking back substitution on B = I: at step k, row k of
+  // the inverse is final; rows i < k lose column k's contribution, and row
+  // k - 1 (whose last update this is) is scaled by 1 / R_{k-1,k-1}.  One
+  // barrier per column.
+  if (tid == 0) inv[(r - 1) * r + r - 1] *= rdiag[r - 1];
   __syncthreads();
-  // Rinv by columns: solve R x = e_j (back substitution), one thread/column
-  for (int j = threadIdx.x; j < r; j += blockDim.x) {
-    for (int i = j; i >= 0; --i) {
-      double s = (i == j) ? 1.0 : 0.0;
-      for (int p = i + 1; p <= j; ++p) s -= a[i * r + p] * inv[p * r + j];
-      const double d = a[i * r + i];
-      inv[i * r + j] = d > 0 ? s / d : 0.0;
+  for (int k = r - 1; k >= 1; --k) {
+    const int cols = r - k;
+    const double rk1 = rdiag[k - 1];
+    for (int e = tid; e <= k * cols; e += bs) {
+      if (e == k * cols) {
+        inv[(k - 1) * r + k - 1] *= rk1;
+        continue;
+      }
+      const int i = e / cols, j = k + e % cols;
+      double v = inv[i * r + j] - a[i * r + k] * inv[k * r + j];
+      if (i == k - 1) v *= rk1;
+      inv[i * r + j] = v;
     }
+    __syncthreads();
   }
-  __syncthreads();
   if (!inv_in_global)
-    for (int e = threadIdx.x; e < r * r; e += blockDim.x) Rinv[e] = inv[e];
-  if (threadIdx.x == 0 && flag) *flag = bad;
+    for (int e = tid; e < r * r; e += bs) Rinv[e] = inv[e];
+  if (tid == 0 && flag) *flag = bad;
 }
 
 // Asynchronous global -> shared copies (LDGSTS): a single-CTA kernel issues
@@ -2115,11 +2277,18 @@ __global__ void row_inverse_kernel(int r, const double* __restrict__ proj,
                                    const double* __restrict__ om_sel, double* __restrict__ Binv,
                                    double* __restrict__ Bout, int* status) {
   // om_sel == nullptr: proj holds the node matrices B_d directly (n x r x r)
+  // Gauss-Jordan on [B | I] with partial pivoting (first maximal |entry|,
+  // as a serial scan would pick), three barriers per column: pivot search
+  // by warp 0; swap + scale of the pivot row with column k saved; the
+  // rank-1 elimination of every other row.  Column k of the left block is
+  // never read again, so it is not cleared.
   extern __shared__ double sm[];
   const int d = blockIdx.x;
   const int w = 2 * r;
   double* a = sm;  // r x 2r augmented [B | I]
+  __shared__ double colk[DLRSN_MAX_RANK];
   __shared__ int piv;
+  __shared__ double pivval;
   __shared__ int sing;
   const double wx = om_sel ? om_sel[3 * d] : 0.0, wy = om_sel ? om_sel[3 * d + 1] : 0.0;
   const int64_t rr = (int64_t)r * r;
@@ -2134,41 +2303,46 @@ __global__ void row_inverse_kernel(int r, const double* __restrict__ proj,
   }
   if (threadIdx.x == 0) sing = 0;
   __syncthreads();
+  const int lane = threadIdx.x & 31;
   for (int k = 0; k < r; ++k) {
-    if (threadIdx.x == 0) {
-      int p = k;
-      double best = fabs(a[k * w + k]);
-      for (int i = k + 1; i < r; ++i) {
+    if (threadIdx.x < 32) {
+      double best = -1.0;
+      int p = r;
+      for (int i = k + lane; i < r; i += 32) {
         const double v = fabs(a[i * w + k]);
-        if (v > best) { best = v; p = i; }
+        if (v > best) { best = v; p = i; }  // lowest row of this lane's maximum
       }
-      piv = p;
-      if (!(best > 0.0) || !isfinite(best)) sing = 1;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(kFull, best, o);
+        const int op = __shfl_xor_sync(kFull, p, o);
+        if (ob > best || (ob == best && op < p)) { best = ob; p = op; }
+      }
+      if (lane == 0) {
+        piv = p < r ? p : k;
+        pivval = a[(p < r ? p : k) * w + k];
+        if (!(best > 0.0) || !isfinite(best)) sing = 1;
+      }
     }
     __syncthreads();
     if (sing) break;
     const int p = piv;
-    if (p != k)
-      for (int j = threadIdx.x; j < w; j += blockDim.x) {
-        const double t = a[k * w + j];
-        a[k * w + j] = a[p * w + j];
-        a[p * w + j] = t;
-      }
-    __syncthreads();
-    const double inv = 1.0 / a[k * w + k];
-    __syncthreads();
-    for (int j = threadIdx.x; j < w; j += blockDim.x) a[k * w + j] *= inv;
+    const double inv = 1.0 / pivval;
+    // new row k = row p / pivot, row p = old row k; colk = column k after
+    // the swap (the old a[k][k] for row p, handed over by the j == k thread)
+    for (int j = threadIdx.x; j < w; j += blockDim.x) {
+      const double tk = a[k * w + j], tp = a[p * w + j];
+      if (p != k) a[p * w + j] = tk;
+      a[k * w + j] = tp * inv;
+      if (j == k) colk[p] = p == k ? 0.0 : tk;
+    }
+    for (int i = threadIdx.x; i < r; i += blockDim.x)
+      if (i != k && i != p) colk[i] = a[i * w + k];
+    if (threadIdx.x == 0 && p != k) colk[k] = 0.0;
     __syncthreads();
     for (int e = threadIdx.x; e < r * w; e += blockDim.x) {
       const int i = e / w, j = e % w;
-      if (i != k) {
-        const double f = a[i * w + k];
-        if (j != k) a[i * w + j] -= f * a[k * w + j];
-      }
+      if (i != k && j > k) a[i * w + j] -= colk[i] * a[k * w + j];
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < r; i += blockDim.x)
-      if (i != k) a[i * w + k] = 0.0;
     __syncthreads();
   }
   if (sing) {
@@ -2383,6 +2557,93 @@ __global__ void row_combine_kernel(int n, int r, const double* __restrict__ Binv
     L[e] = s;
   }
   if (threadIdx.x == 0 && sing) *status = 1;
+}
+
+// The same combine spread over the GPU (the one-call step): the per-node
+// products and the node sums, which were the single-CTA kernel's cost (n r^2
+// L2 loads each), run as grids; only the r x r solve stays on one CTA.  Same
+// summation orders as row_combine_kernel, so the results are identical.
+// scratch: cbar (r*r) | zeta (r) | msl (r).
+__global__ void row_bq_kernel(int r, const double* __restrict__ Binv, const double* __restrict__ Q,
+                              const double* __restrict__ msl, double* __restrict__ out) {
+  // out[d][i] = sum_j Binv_d[i][j] (Q_d[j] + msl[j])   (msl null: + 0)
+  const int d = blockIdx.x;
+  const int64_t rr = (int64_t)r * r;
+  __shared__ double qd[DLRSN_MAX_RANK];
+  for (int j = threadIdx.x; j < r; j += blockDim.x) qd[j] = msl ? Q[d * r + j] + msl[j] : Q[d * r + j];
+  __syncthreads();
+  for (int i = threadIdx.x; i < r; i += blockDim.x) {
+    const double* row = Binv + d * rr + (int64_t)i * r;
+    double s = 0.0;
+    for (int j = 0; j < r; ++j) s += row[j] * qd[j];
+    out[d * r + i] = s;
+  }
+}
+
+__global__ void row_sums_kernel(int n, int r, const double* __restrict__ Binv,
+                                const double* __restrict__ BQ, const double* __restrict__ wts,
+                                double* __restrict__ scratch) {
+  const int64_t rr = (int64_t)r * r;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < rr) {
+    double s = 0.0;
+    for (int d = 0; d < n; ++d) s += wts[d] * Binv[d * rr + e];
+    scratch[e] = s;
+  } else if (e < rr + r) {
+    const int i = e - (int)rr;
+    double s = 0.0;
+    for (int d = 0; d < n; ++d) s += wts[d] * BQ[d * r + i];
+    scratch[e] = s;
+  }
+}
+
+__global__ void row_solve_kernel(int r, const double* __restrict__ ms, double* __restrict__ scratch,
+                                 double* __restrict__ lbar, int* status) {
+  extern __shared__ double sm[];
+  double* lhs = sm;           // r*r
+  double* cbar = lhs + r * r; // r*r
+  double* zeta = cbar + r * r;
+  int* perm = reinterpret_cast<int*>(zeta + r);
+  __shared__ int sing;
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) cbar[e] = scratch[e];
+  for (int i = threadIdx.x; i < r; i += blockDim.x) zeta[i] = scratch[r * r + i];
+  if (threadIdx.x == 0) sing = 0;
+  __syncthreads();
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+    const int i = e / r, j = e % r;
+    double s = 0.0;
+    for (int p = 0; p < r; ++p) s += cbar[i * r + p] * ms[p * r + j];
+    lhs[e] = (i == j ? 1.0 : 0.0) - s / kFourPi;
+  }
+  __syncthreads();
+  cta_lu_solve(r, lhs, r, zeta, 1, 1, perm, &sing);
+  double* msl = scratch + r * r + r;
+  for (int i = threadIdx.x; i < r; i += blockDim.x) {
+    lbar[i] = zeta[i];
+    double s = 0.0;
+    for (int p = 0; p < r; ++p) s += ms[i * r + p] * zeta[p];
+    msl[i] = s / kFourPi;
+  }
+  if (threadIdx.x == 0 && sing) *status = 1;
+}
+
+int row_combine_grid(int n, int r, const double* Binv, const double* ms, const double* Q,
+                     const double* wts, double* L, double* lbar, int* status, double* scratch,
+                     cudaStream_t st) {
+  const size_t smem = (2 * (size_t)r * r + r) * sizeof(double) + r * sizeof(int);
+  DLRSN_REQUIRE(smem <= 227 * 1024, "rank %d too large for row_combine", r);
+  row_bq_kernel<<<n, 128, 0, st>>>(r, Binv, Q, nullptr, L);  // L holds B_d^-1 Q_d here
+  DLRSN_CHECK_LAUNCH("row_bq_kernel");
+  const int len = r * r + r;
+  row_sums_kernel<<<(len + 127) / 128, 128, 0, st>>>(n, r, Binv, L, wts, scratch);
+  DLRSN_CHECK_LAUNCH("row_sums_kernel");
+  DLRSN_TRY_CUDA(cudaFuncSetAttribute(row_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+  row_solve_kernel<<<1, 256, smem, st>>>(r, ms, scratch, lbar, status);
+  DLRSN_CHECK_LAUNCH("row_solve_kernel");
+  row_bq_kernel<<<n, 128, 0, st>>>(r, Binv, Q, scratch + r * r + r, L);
+  DLRSN_CHECK_LAUNCH("row_bq_kernel");
+  return DLRSN_OK;
 }
 
 // Running top-2 of the DEIM argmax: (best, its row, second best value).
@@ -3189,6 +3450,7 @@ int dlrsn_mgram(const dlrsn_cellops* ops, int ra, int rb, const double* A, int l
   }
   const MgramPlan pl = mgram_plan(ncell, ra, rb);
   const int nblk = pl.nblk;
+  bool tsym = false;
   if (pl.tb == 0) {
     mgram_mma_kernel<<<dim3(nblk, pl.tiles), kTile * kTile, 0, st>>>(ncell, ra, rb, A, lda, B, ldb,
                                                                      coeff, *ops, pl.cpb, partial);
@@ -3201,9 +3463,17 @@ int dlrsn_mgram(const dlrsn_cellops* ops, int ra, int rb, const double* A, int l
       const size_t smem = MgramWide<64>::smem(same);
       DLRSN_TRY_CUDA(cudaFuncSetAttribute(mgram_wide_kernel<64>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      mgram_wide_kernel<64><<<dim3(nblk, pl.tiles), 256, smem, st>>>(ncell, ra, rb, A, lda, B, ldb,
-                                                                     coeff, *ops, pl.cpb, partial, vec,
-                                                                     0);
+      // DLRSN_MGRAM_FULL=1: diagonal tiles computed in full (A/B timing)
+      static const char* full_env = getenv("DLRSN_MGRAM_FULL");
+      const bool full = full_env && full_env[0] == '1';
+      // symmetric Gram over several tiles: the tiles ti <= tj only, the
+      // lower ones mirrored after the reduction
+      const int T = (ra + 63) / 64;
+      tsym = !full && A == B && lda == ldb && ra == rb && pl.tiles > 1;
+      const int gy = tsym ? T * (T + 1) / 2 : pl.tiles;
+      mgram_wide_kernel<64><<<dim3(nblk, gy), 256, smem, st>>>(ncell, ra, rb, A, lda, B, ldb,
+                                                               coeff, *ops, pl.cpb, partial, vec,
+                                                               (full ? 2 : 0) | (tsym ? 1 : 0));
     } else {
       const size_t smem = MgramWide<32>::smem(same);
       DLRSN_TRY_CUDA(cudaFuncSetAttribute(mgram_wide_kernel<32>,
@@ -3217,6 +3487,10 @@ int dlrsn_mgram(const dlrsn_cellops* ops, int ra, int rb, const double* A, int l
   const int64_t len = (int64_t)ra * rb;
   reduce_partials_kernel<<<(unsigned)((len + 31) / 32), 1024, 0, st>>>(nblk, len, partial, G, 1.0);
   DLRSN_CHECK_LAUNCH("reduce_partials_kernel");
+  if (tsym) {
+    mirror_gram_kernel<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(ra, 64, G);
+    DLRSN_CHECK_LAUNCH("mirror_gram_kernel");
+  }
   return DLRSN_OK;
 }
 

@@ -328,6 +328,7 @@ struct StepBufs {
   double *om_sel, *K, *Sb, *psi, *G, *R1, *R1inv, *ratio, *ratio2, *X1, *R2, *R2inv, *Rtot;
   double *part, *proj, *Binv, *L, *lbar, *T, *qall, *gamma, *lfull, *Rang, *cgsws;
   double *wpart, *wg;
+  double* rcs;  // row-combine scratch: cbar | zeta | msl
   int *idx, *quads, *mine;
   int64_t* place;
   double* cw_local;
@@ -417,6 +418,7 @@ static size_t carve(Arena& ar, StepBufs& b, int nx, int ny, int r, int no, int w
   b.ratiow2 = ar.take<double>(2 * r);
   b.lq1 = ar.take<double>((size_t)no * r);
   b.hin = ar.take<double>(4 * (size_t)r);
+  b.rcs = ar.take<double>((size_t)r * r + 2 * r);
   b.up = ar.take<Upload>(1);
   return ar.off;
 }
@@ -1024,10 +1026,10 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     if (!exact) {
       DLRSN_RET(dlrsn_mgram(ops, r, r, b.psi, r, b.psi, r, nullptr, b.G, b.part, s));
       DLRSN_RET(dlrsn_chol_upper(r, b.G, b.R1, b.R1inv, b.ratio, b.cholflag, s));
-      DLRSN_RET(dlrsn_rowmix(N, r, r, b.psi, r, b.R1inv, r, 0.0, b.X1, r, s));
+      DLRSN_RET(rowmix_upper(N, r, b.psi, r, b.R1inv, r, b.X1, r, st));
       DLRSN_RET(dlrsn_mgram(ops, r, r, b.X1, r, b.X1, r, nullptr, b.G, b.part, s));
       DLRSN_RET(dlrsn_chol_upper(r, b.G, b.R2, b.R2inv, b.ratio2, b.cholflag + 1, s));
-      DLRSN_RET(dlrsn_rowmix(N, r, r, b.X1, r, b.R2inv, r, 0.0, X_new, r, s));
+      DLRSN_RET(rowmix_upper(N, r, b.X1, r, b.R2inv, r, X_new, r, st));
     } else {
       DLRSN_RET(dlrsn_cgs2((int)N, r, b.psi, r, X_new, r, b.Rtot, b.defx, 1, nullptr, ops, 1,
                            r + 8, b.up->sexp, b.up->extent, b.cgsws, b.statx, 1, s));
@@ -1049,8 +1051,8 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     DLRSN_CHECK_LAUNCH("qall_kernel");
     DLRSN_TRY_CUDA(zero_async(b.rowstat, (r + 1) * sizeof(int), st));
     DLRSN_RET(dlrsn_row_inverse(r, r, b.proj, b.om_sel, b.Binv, nullptr, b.rowstat, s));
-    DLRSN_RET(dlrsn_row_combine(r, r, b.Binv, b.proj + 5 * r * r, b.qall, b.closure, b.L,
-                                b.lbar, b.rowstat + r, s));
+    DLRSN_RET(row_combine_grid(r, r, b.Binv, b.proj + 5 * r * r, b.qall, b.closure, b.L,
+                               b.lbar, b.rowstat + r, b.rcs, st));
     DLRSN_RET(dlrsn_what_solve(r, r, b.Lhat, b.U, b.L, b.gamma, 0, s));
     // two branches: the angular update (one CTA) on `st`; the flux of the
     // new state, the step boundary and the spatial check on the side stream

@@ -315,6 +315,240 @@ sweep_kernel(const SweepArgs a) {
 }
 
 
+// ---- single-direction sweep, factorisation off the critical path ---------
+// Same data flow as sweep_kernel<1> (TMA ring per warp, L2 strip handoff),
+// but the per-step work is split by what it depends on:
+//   phase 1 (independent across the chunk's C steps, ILP C): form A =
+//     sigma_t M + S_omega, LU-factor it, and keep the factors plus the
+//     source part of the rhs in registers -- all of it may run before the
+//     strip below has delivered the chunk's inflow;
+//   phase 2 (the dependent chain): add the upwind couplings to the rhs and
+//     run the forward / back substitutions with pre-scaled factors: ~8
+//     dependent FMAs per step instead of a whole factorisation (four
+//     reciprocals) per step.
+// Measured on C4 (1024^2, 64 directions): the chain-bound sweep_kernel<1>
+// spent ~1200 cycles per warp-step ('wait' + handoff spin stalls).
+struct Lu4 {
+  double l1, l2, l3, m2, m3, n3;  // unit-lower multipliers
+  double p0, p1, p2, p3;          // pivot reciprocals
+  double u1, u2, u3, u6, u7, u11; // strictly upper part, row-scaled by its pivot reciprocal
+  double b0, b1, b2, b3;          // source part of the rhs (rhs + scattering source)
+};
+
+template <int C>
+__device__ __forceinline__ void lu4_factor(const SweepArgs& a, const double* S, double sigma,
+                                           Lu4& f) {
+  double A[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) A[q] = fma(sigma, a.mass[q], S[q]);
+  f.p0 = rcp64(A[0]);
+  f.l1 = A[4] * f.p0; f.l2 = A[8] * f.p0; f.l3 = A[12] * f.p0;
+  A[5] -= f.l1 * A[1]; A[6] -= f.l1 * A[2]; A[7] -= f.l1 * A[3];
+  A[9] -= f.l2 * A[1]; A[10] -= f.l2 * A[2]; A[11] -= f.l2 * A[3];
+  A[13] -= f.l3 * A[1]; A[14] -= f.l3 * A[2]; A[15] -= f.l3 * A[3];
+  f.p1 = rcp64(A[5]);
+  f.m2 = A[9] * f.p1; f.m3 = A[13] * f.p1;
+  A[10] -= f.m2 * A[6]; A[11] -= f.m2 * A[7];
+  A[14] -= f.m3 * A[6]; A[15] -= f.m3 * A[7];
+  f.p2 = rcp64(A[10]);
+  f.n3 = A[14] * f.p2;
+  A[15] -= f.n3 * A[11];
+  f.p3 = rcp64(A[15]);
+  f.u1 = A[1] * f.p0; f.u2 = A[2] * f.p0; f.u3 = A[3] * f.p0;
+  f.u6 = A[6] * f.p1; f.u7 = A[7] * f.p1;
+  f.u11 = A[11] * f.p2;
+}
+
+template <int C, int P, int WPC>
+__global__ void __launch_bounds__(WPC * 32)
+sweep1s_kernel(const SweepArgs a) {
+  const bool skip = a.skip != nullptr && *a.skip != 0;
+  constexpr int SD = C * (32 + 128 + 128);  // doubles per stage: sigma | scat | rhs
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t bars[WPC][P];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  double* ring = smem + (size_t)wib * P * SD;
+  const int nx = a.nx, ny = a.ny, G = a.G;
+  const int T = nx + 31;
+  const int ns = (ny + 31) >> 5;
+  const int items = ns * G;
+  const int nchunks = (T + C - 1) / C;
+  const int hchunks = (nx + C - 1) / C;
+  const double empty = __longlong_as_double((long long)kEmpty);
+  const int flags = g_flags;  // debug bits, read once
+
+  if (lane == 0) {
+#pragma unroll
+    for (int st = 0; st < P; ++st) mbar_init(&bars[wib][st], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  uint32_t parity = 0;
+
+  for (;;) {
+    int item = 0;
+    if (lane == 0) {
+      item = skip ? items : atomicAdd(a.ticket, 1);
+      if (!skip && item == items + (int)(gridDim.x * blockDim.x / 32) - 1) atomicExch(a.ticket, 0);
+    }
+    item = __shfl_sync(kFull, item, 0);
+    if (item >= items) break;
+    const int s = item / G;
+    const int g = item - s * G;
+    const dlrsn_group* grp = a.groups + g;
+    const int quad = grp->quad;
+    const double ox = grp->ox[0], oy = grp->oy[0], cw = grp->cw[0];
+    double S[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) S[m] = ox * a.gxp[m] + oy * a.gyp[m];
+    const double cx0 = ox * a.ex[0], cx1 = ox * a.ex[1], cx2 = ox * a.ex[2], cx3 = ox * a.ex[3];
+    const double cy0 = oy * a.ey[0], cy1 = oy * a.ey[1], cy2 = oy * a.ey[2], cy3 = oy * a.ey[3];
+    const int64_t strip_vec = (int64_t)s * T * 128;
+    const int64_t slot_off = (int64_t)grp->slot[0] * a.vlen + strip_vec;
+    const double* sig = a.sigma_sk4 + (int64_t)quad * a.slen + (int64_t)s * T * 32;
+    const double* scat = a.scat_sk4 ? a.scat_sk4 + (int64_t)quad * a.vlen + strip_vec : nullptr;
+    const double* rhs = a.rhs_sk + slot_off;
+    double* phi_p = a.phi_sk ? a.phi_sk + (int64_t)g * a.vlen + strip_vec + 2 * lane : nullptr;
+    const uint32_t bytes_per_step = 256u + (scat ? 1024u : 0u) + 1024u;
+    __syncwarp();
+
+    auto issue = [&](int mm) {
+      const int st = mm % P, t0 = mm * C;
+      const uint32_t n = (uint32_t)min(C, T - t0);
+      double* buf = ring + st * SD;
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&bars[wib][st], n * bytes_per_step);
+      tma_load_1d(buf, sig + t0 * 32, n * 256u, &bars[wib][st]);
+      if (scat) tma_load_1d(buf + C * 32, scat + t0 * 128, n * 1024u, &bars[wib][st]);
+      tma_load_1d(buf + C * 160, rhs + t0 * 128, n * 1024u, &bars[wib][st]);
+    };
+    if (lane == 0)
+      for (int m = 0; m < P - 1 && m < nchunks; ++m) issue(m);
+
+    const bool row_ok = (s << 5) + lane < ny;
+    double2* hin = s > 0 ? reinterpret_cast<double2*>(a.handoff) + ((int64_t)(s - 1) * G + g) * nx
+                         : nullptr;
+    double2* hout = (s + 1 < ns) ? reinterpret_cast<double2*>(a.handoff) + ((int64_t)s * G + g) * nx
+                                 : nullptr;
+    const bool hlane = hin != nullptr && lane < C;
+    double2 h0 = make_double2(0.0, 0.0), h1 = h0, h2 = h0;
+    const bool spec = (flags & 1) == 0;
+    if (!spec) h0 = h1 = h2 = make_double2(empty, empty);
+    if (spec && hlane && lane < nx) h1 = __ldcg(hin + lane);
+    if (spec && hlane && C + lane < nx) h2 = __ldcg(hin + C + lane);
+    const bool take_y = lane == 0 && hin != nullptr && (flags & 2) == 0;
+
+    double xin0 = 0.0, xin1 = 0.0, yin0 = 0.0, yin1 = 0.0;
+    for (int m = 0; m < nchunks; ++m) {
+      if (lane == 0 && m + P - 1 < nchunks) issue(m + P - 1);
+      {
+        const int st = m % P;
+        mbar_wait_warp(&bars[wib][st], (parity >> st) & 1u);
+        parity ^= 1u << st;
+      }
+      __syncwarp();
+      const double* buf = ring + (m % P) * SD;
+      // phase 1: factors and source rhs of the chunk's C steps
+      Lu4 f[C];
+#pragma unroll
+      for (int tt = 0; tt < C; ++tt) {
+        const double sigma = buf[tt * 32 + lane];
+        const double2 u = reinterpret_cast<const double2*>(buf + C * 160 + tt * 128)[lane];
+        const double2 v = reinterpret_cast<const double2*>(buf + C * 160 + tt * 128 + 64)[lane];
+        f[tt].b0 = u.x; f[tt].b1 = u.y; f[tt].b2 = v.x; f[tt].b3 = v.y;
+        if (scat) {
+          const double2 su = reinterpret_cast<const double2*>(buf + C * 32 + tt * 128)[lane];
+          const double2 sv = reinterpret_cast<const double2*>(buf + C * 32 + tt * 128 + 64)[lane];
+          f[tt].b0 += su.x; f[tt].b1 += su.y; f[tt].b2 += sv.x; f[tt].b3 += sv.y;
+        }
+        lu4_factor<C>(a, S, sigma, f[tt]);
+      }
+      __syncwarp();  // every lane has read stage m % P before it is refilled
+      // the chunk's y-inflow of lane 0 (strip below, via L2)
+      h0 = h1;
+      h1 = h2;
+      {
+        const bool need = hlane && m < hchunks && m * C + lane < nx;
+        double2* slot = hin + (int64_t)m * C + lane;
+        int spins = 0;
+        while (__any_sync(kFull, need && (is_empty(h0.x) || is_empty(h0.y)))) {
+          __nanosleep(32);
+          if (need && (is_empty(h0.x) || is_empty(h0.y))) h0 = __ldcv(slot);
+          if (++spins > (1 << 26)) {
+            if (need) atomicOr(a.status, 2);
+            h0 = make_double2(0.0, 0.0);
+          }
+        }
+        if (need) __stcg(slot, make_double2(empty, empty));
+      }
+      if (spec && hlane && m + 2 < hchunks && (m + 2) * C + lane < nx)
+        h2 = __ldcg(hin + (int64_t)(m + 2) * C + lane);
+      // phase 2: the dependent chain
+#pragma unroll
+      for (int tt = 0; tt < C; ++tt) {
+        const int t = m * C + tt;
+        const int ip = t - lane;
+        const bool act = row_ok && ip >= 0 && ip < nx;
+        {
+          const double y0 = __shfl_sync(kFull, h0.x, tt);
+          const double y1 = __shfl_sync(kFull, h0.y, tt);
+          if (take_y) { yin0 = y0; yin1 = y1; }
+        }
+        const Lu4& F = f[tt];
+        const double v0 = fma(cy1, yin1, fma(cy0, yin0, fma(cx1, xin1, fma(cx0, xin0, F.b0))));
+        const double v1 = fma(cy3, yin1, fma(cy2, yin0, F.b1));
+        const double v2 = fma(cx3, xin1, fma(cx2, xin0, F.b2));
+        const double y1 = fma(-F.l1, v0, v1);
+        const double y2 = fma(-F.m2, y1, fma(-F.l2, v0, v2));
+        const double y3 = fma(-F.n3, y2, fma(-F.m3, y1, fma(-F.l3, v0, F.b3)));
+        const double x3 = y3 * F.p3;
+        const double x2 = fma(-F.u11, x3, y2 * F.p2);
+        const double x1 = fma(-F.u6, x2, fma(-F.u7, x3, y1 * F.p1));
+        const double x0 = fma(-F.u1, x1, fma(-F.u2, x2, fma(-F.u3, x3, v0 * F.p0)));
+        double yt0 = 0.0, yt1 = 0.0;
+        if (act) {
+          double2* po = reinterpret_cast<double2*>(a.psi_sk + slot_off + (int64_t)t * 128 + 2 * lane);
+          po[0] = make_double2(x0, x1);
+          po[32] = make_double2(x2, x3);
+          xin0 = x1; xin1 = x3;
+          yt0 = x2; yt1 = x3;
+          if (phi_p) {
+            double2* pp = reinterpret_cast<double2*>(phi_p + (int64_t)t * 128);
+            pp[0] = make_double2(cw * x0, cw * x1);
+            pp[32] = make_double2(cw * x2, cw * x3);
+          }
+          if (lane == 31 && hout) __stcg(hout + ip, make_double2(x2, x3));
+        }
+        const double u0 = __shfl_up_sync(kFull, yt0, 1);
+        const double u1 = __shfl_up_sync(kFull, yt1, 1);
+        if (lane > 0) { yin0 = u0; yin1 = u1; }
+      }
+    }
+  }
+}
+
+template <int C, int P, int WPC>
+int launch_sweep1s(const SweepArgs& a, int max_ctas, cudaStream_t st) {
+  constexpr size_t smem = (size_t)WPC * P * C * (32 + 128 + 128) * sizeof(double);
+  int dev = 0, sms = 0, occ = 0;
+  DLRSN_TRY_CUDA(cudaGetDevice(&dev));
+  DLRSN_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  DLRSN_TRY_CUDA(cudaFuncSetAttribute(sweep1s_kernel<C, P, WPC>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  DLRSN_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep1s_kernel<C, P, WPC>,
+                                                               WPC * 32, smem));
+  const int items = sk_strips(a.ny) * a.G;
+  int ctas = (items + WPC - 1) / WPC;
+  const int cap = sms * (occ > 0 ? occ : 1);
+  if (ctas > cap) ctas = cap;
+  if (max_ctas > 0 && ctas > max_ctas) ctas = max_ctas;
+  if (ctas < 1) ctas = 1;
+  sweep1s_kernel<C, P, WPC><<<ctas, WPC * 32, smem, st>>>(a);
+  DLRSN_CHECK_LAUNCH("sweep1s_kernel");
+  return DLRSN_OK;
+}
+
 __global__ void fill_empty_kernel(double* p, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = __longlong_as_double((long long)kEmpty);
@@ -1284,7 +1518,7 @@ static int sweep_launch_ex(const dlrsn_cellops* ops, int G, const dlrsn_group* g
   // crossover measured on B200 (scripts/sweep_bench.py, configs.py): WS wins
   // at 512 items (C3: 0.41 vs 0.63 ms) and 1024 items (1.31 vs 1.39 ms), the
   // multi-warp kernel at 1152 items (1.05 vs 1.13 ms) and 2048 (C4: 1.59 vs 2.57)
-  bool use_ws = items <= 7 * sms;
+  bool use_ws = items <= 4 * sms;
   if (ws_env) use_ws = ws_env[0] == '1';
   if (phi_part_sk) use_ws = false;  // the warp-specialised kernel writes no closure partials
   if (rhs_shared || phi_atomic) use_ws = false;
@@ -1297,7 +1531,16 @@ static int sweep_launch_ex(const dlrsn_cellops* ops, int G, const dlrsn_group* g
         rc = launch_sweep_ws(a, max_ctas, st);
         break;
       }
+      if (rhs_shared || phi_atomic) {  // closure-only sweeps: the general kernel
+        rc = launch_sweep<1, 0>(a, max_ctas, st);
+        break;
+      }
       switch (sweep1_variant()) {
+        case 0: rc = launch_sweep1s<4, 3, 2>(a, max_ctas, st); break;
+        case 10: rc = launch_sweep1s<2, 4, 2>(a, max_ctas, st); break;
+        case 11: rc = launch_sweep1s<4, 2, 2>(a, max_ctas, st); break;
+        case 12: rc = launch_sweep1s<2, 3, 4>(a, max_ctas, st); break;
+        case 9: rc = launch_sweep<1, 0>(a, max_ctas, st); break;
         case 1: rc = launch_sweep<1, 1>(a, max_ctas, st); break;
         case 2: rc = launch_sweep<1, 2>(a, max_ctas, st); break;
         case 3: rc = launch_sweep<1, 3>(a, max_ctas, st); break;
@@ -1305,7 +1548,7 @@ static int sweep_launch_ex(const dlrsn_cellops* ops, int G, const dlrsn_group* g
         case 5: rc = launch_sweep<1, 5>(a, max_ctas, st); break;
         case 6: rc = launch_sweep<1, 6>(a, max_ctas, st); break;
         case 7: rc = launch_sweep<1, 7>(a, max_ctas, st); break;
-        default: rc = launch_sweep<1, 0>(a, max_ctas, st); break;
+        default: rc = launch_sweep1s<4, 3, 2>(a, max_ctas, st); break;
       }
       break;
     case 2: rc = launch_sweep<2>(a, max_ctas, st); break;

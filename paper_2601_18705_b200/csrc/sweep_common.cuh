@@ -110,7 +110,14 @@ int launch_sweep_ws(const SweepArgs& a, int max_ctas, cudaStream_t st);
 
 bool sweep_timing_enabled();
 bool project_timing_enabled();
-int advance_launch(const dlrsn_advance* av, const double* phi, cudaStream_t st);  // physics.cu  // dlrsn_sweep_timing on (the step then skips graphs)
+int advance_launch(const dlrsn_advance* av, const double* phi, cudaStream_t st);
+// dense.cu: Y = X K for an upper-triangular r x r K (skips the zero blocks)
+int rowmix_upper(int64_t n, int r, const double* X, int ldx, const double* K, int ldk, double* Y,
+                 int ldy, cudaStream_t st);
+// dense.cu: the row-system combine as grids (scratch r*r + 2r doubles)
+int row_combine_grid(int n, int r, const double* Binv, const double* ms, const double* Q,
+                     const double* wts, double* L, double* lbar, int* status, double* scratch,
+                     cudaStream_t st);  // physics.cu  // dlrsn_sweep_timing on (the step then skips graphs)
 
 // internal entry points of the step (step.cu); the public C-ABI calls pass
 // skip / ctl = nullptr
