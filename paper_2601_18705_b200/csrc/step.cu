@@ -329,6 +329,9 @@ struct StepBufs {
   double *part, *proj, *Binv, *L, *lbar, *T, *qall, *gamma, *lfull, *Rang, *cgsws;
   double *wpart, *wg;
   double* rcs;  // row-combine scratch: cbar | zeta | msl
+  CgTable* cgtab;  // grouped sweep: direction groups
+  int* cg_quad;
+  double* cg_w;
   int *idx, *quads, *mine;
   int64_t* place;
   double* cw_local;
@@ -419,6 +422,9 @@ static size_t carve(Arena& ar, StepBufs& b, int nx, int ny, int r, int no, int w
   b.lq1 = ar.take<double>((size_t)no * r);
   b.hin = ar.take<double>(4 * (size_t)r);
   b.rcs = ar.take<double>((size_t)r * r + 2 * r);
+  b.cgtab = ar.take<CgTable>(1);
+  b.cg_quad = ar.take<int>(r);
+  b.cg_w = ar.take<double>(r);
   b.up = ar.take<Upload>(1);
   return ar.off;
 }
@@ -863,6 +869,16 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
   info->error_index = -1;
   const int nl = (r - rank_id + world - 1) / world;  // this rank's directions
   const int G = nl;                                  // single-direction groups
+  // grouped sweep with the fused closure: one GPU, enough direction-strips
+  // for the throughput kernel (the warp-specialised kernel below that)
+  int sms_count = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms_count, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const bool grouped = world == 1 && nl > 0 && sweep_group_width() > 0 &&
+                       sk_strips(ny) * G > 4 * sms_count;
   // full-rank fast path of the angular update: one-CTA weighted CholQR2
   const bool ang_fast = r <= 32 && dlrsn_cholqr2_small_smem(no, r) <= 200 * 1024;
   StepStatus* hs = nullptr;
@@ -947,6 +963,9 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
                                               p->omegas_dev, b.closure, b.idx, b.groups, b.quads,
                                               b.mine, b.place, N, width, b.cw_local);
     DLRSN_CHECK_LAUNCH("plan_kernel");
+    if (grouped)
+      DLRSN_RET(cgroup_plan_launch(G, b.groups, sweep_group_width(), r, b.cgtab, b.cg_quad, b.cg_w,
+                                   st));
     // 2. evaluate_rows (dlr_sn.py:110-121) and the sweep rhs
     ks_kernel<<<1, 256, 0, st>>>(r, S, W, b.idx, beta, b.K, nullptr, p->omegas_dev, b.om_sel);
     DLRSN_CHECK_LAUNCH("ks_kernel");
@@ -976,6 +995,17 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     for (int it = it_from; it <= it_to; ++it) {
       const double* phi = P[(it - 1) & 1];
       double* phin = P[it & 1];
+      if (grouped) {
+        // psi and the per-group closure partials in one pass, then the
+        // partial slabs summed per quadrant (fixed order) like swept columns
+        DLRSN_RET(sweep_grouped_launch(ops, G, b.groups, b.cgtab, b.sig4, b.scat, b.rhs_sk,
+                                       b.psi_sk, b.phi_part, sweep_ws, sweep_ws_bytes,
+                                       &b.ctl->done, st));
+        DLRSN_RET(phi_closure_launch(ops, r, b.cg_quad, b.cg_w, b.phi_part, b.phiq, phi, sigma_s,
+                                     phin, b.scat, b.norms, b.red_ws, b.ctl, it, p->si_tol,
+                                     b.flags + 1, nullptr, st));
+        continue;
+      }
       if (nl > 0)
         DLRSN_RET(sweep_launch(ops, G, b.groups, 1, b.sig4, b.scat, b.rhs_sk, b.psi_sk, nullptr,
                                sweep_ws, sweep_ws_bytes, 0, &b.ctl->done, st));

@@ -20,6 +20,7 @@
 //     accumulated in registers (deterministic, no atomics).
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "sweep_common.cuh"
@@ -549,6 +550,270 @@ int launch_sweep1s(const SweepArgs& a, int max_ctas, cudaStream_t st) {
   return DLRSN_OK;
 }
 
+// ---- grouped single-direction sweep with the closure fused --------------
+// One CTA = up to WPC directions of ONE quadrant on one 32-row strip, a warp
+// per direction, in lock step chunk by chunk: sigma_t and the scattering
+// source are staged once per CTA (they are per cell), each warp stages its
+// own rhs; after the dependent chain each warp leaves cw_d psi_d of the
+// chunk in shared memory and the CTA sums the group's directions in fixed
+// warp order into the group's closure partial (SK layout of the quadrant).
+// So the source iteration never re-reads psi for phi (the separate closure
+// pass read every swept direction once per iteration), and the reduction
+// order is fixed (deterministic).  One CTA barrier per chunk.
+template <int C, int P, int WPC>
+__global__ void __launch_bounds__(WPC * 32, 1)
+sweep1g_kernel(const SweepArgs a, const CgTable* __restrict__ tab, double* __restrict__ part) {
+  const bool skip = a.skip != nullptr && *a.skip != 0;
+  constexpr int SD = C * (32 + 128) + WPC * C * 128;  // sigma | scat | rhs x WPC
+  extern __shared__ __align__(128) double smem[];
+  double* ring = smem;                    // P x SD
+  double* phibuf = smem + (size_t)P * SD;  // 2 x WPC x C*128
+  __shared__ __align__(8) uint64_t bars[P];
+  __shared__ int s_item, s_ncg;
+  __shared__ int s_first[kMaxCg], s_count[kMaxCg], s_quad[kMaxCg];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int nx = a.nx, ny = a.ny;
+  const int T = nx + 31;
+  const int ns = (ny + 31) >> 5;
+  const int nchunks = (T + C - 1) / C;
+  const int hchunks = (nx + C - 1) / C;
+  const double empty = __longlong_as_double((long long)kEmpty);
+  const int flags = g_flags;
+  if (tid == 0) {
+    s_ncg = tab->ncg;
+#pragma unroll
+    for (int st = 0; st < P; ++st) mbar_init(&bars[st], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int ncg = s_ncg;
+  for (int c = tid; c < ncg; c += blockDim.x) {
+    s_first[c] = tab->first[c];
+    s_count[c] = tab->count[c];
+    s_quad[c] = tab->quad[c];
+  }
+  const int items = ns * ncg;
+  uint32_t parity = 0;
+  int mm_total = 0;  // chunks consumed by this CTA (phibuf parity)
+  for (;;) {
+    __syncthreads();  // previous item fully reduced; tables loaded
+    if (tid == 0) {
+      int item = skip ? items : atomicAdd(a.ticket, 1);
+      if (!skip && item == items + (int)gridDim.x - 1) atomicExch(a.ticket, 0);
+      s_item = item;
+    }
+    __syncthreads();
+    const int item = s_item;
+    if (item >= items) break;
+    const int s = item / ncg;
+    const int c = item - s * ncg;
+    const int quad = s_quad[c], first = s_first[c], count = s_count[c];
+    const bool active = w < count;
+    const int gi = first + (active ? w : 0);
+    const dlrsn_group* grp = a.groups + gi;
+    const double ox = grp->ox[0], oy = grp->oy[0], cw = active ? grp->cw[0] : 0.0;
+    double S[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) S[m] = ox * a.gxp[m] + oy * a.gyp[m];
+    const double cx0 = ox * a.ex[0], cx1 = ox * a.ex[1], cx2 = ox * a.ex[2], cx3 = ox * a.ex[3];
+    const double cy0 = oy * a.ey[0], cy1 = oy * a.ey[1], cy2 = oy * a.ey[2], cy3 = oy * a.ey[3];
+    const int64_t strip_vec = (int64_t)s * T * 128;
+    const int64_t slot_off = (int64_t)grp->slot[0] * a.vlen + strip_vec;
+    const double* sig = a.sigma_sk4 + (int64_t)quad * a.slen + (int64_t)s * T * 32;
+    const double* scat = a.scat_sk4 ? a.scat_sk4 + (int64_t)quad * a.vlen + strip_vec : nullptr;
+    double* pout = part + (int64_t)c * a.vlen + strip_vec;
+    __shared__ int64_t s_off[WPC];  // rhs offsets of the group's directions
+    if (lane == 0) s_off[w] = slot_off;
+    __syncthreads();
+
+    auto issue = [&](int mm) {  // thread 0
+      const int st = mm % P, t0 = mm * C;
+      const uint32_t n = (uint32_t)min(C, T - t0);
+      double* buf = ring + st * SD;
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&bars[st], n * (256u + (scat ? 1024u : 0u) + 1024u * count));
+      tma_load_1d(buf, sig + t0 * 32, n * 256u, &bars[st]);
+      if (scat) tma_load_1d(buf + C * 32, scat + t0 * 128, n * 1024u, &bars[st]);
+      for (int k = 0; k < count; ++k)
+        tma_load_1d(buf + C * 160 + k * C * 128, a.rhs_sk + s_off[k] + t0 * 128, n * 1024u, &bars[st]);
+    };
+    if (tid == 0)
+      for (int m = 0; m < P - 1 && m < nchunks; ++m) issue(m);
+
+    const bool row_ok = (s << 5) + lane < ny;
+    const int D = a.G;  // handoff columns: one per single-direction group
+    double2* hin = (active && s > 0)
+                       ? reinterpret_cast<double2*>(a.handoff) + ((int64_t)(s - 1) * D + gi) * nx
+                       : nullptr;
+    double2* hout = (active && s + 1 < ns)
+                        ? reinterpret_cast<double2*>(a.handoff) + ((int64_t)s * D + gi) * nx
+                        : nullptr;
+    const bool hlane = hin != nullptr && lane < C;
+    double2 h0 = make_double2(0.0, 0.0), h1 = h0, h2 = h0;
+    const bool spec = (flags & 1) == 0;
+    if (!spec) h0 = h1 = h2 = make_double2(empty, empty);
+    if (spec && hlane && lane < nx) h1 = __ldcg(hin + lane);
+    if (spec && hlane && C + lane < nx) h2 = __ldcg(hin + C + lane);
+    const bool take_y = lane == 0 && hin != nullptr && (flags & 2) == 0;
+
+    double xin0 = 0.0, xin1 = 0.0, yin0 = 0.0, yin1 = 0.0;
+    for (int m = 0; m < nchunks; ++m, ++mm_total) {
+      // stage (m + P - 1) % P was last read in chunk m - 1's phase 1, which
+      // every warp finished before that chunk's barrier
+      if (tid == 0 && m + P - 1 < nchunks) issue(m + P - 1);
+      {
+        const int st = m % P;
+        mbar_wait_warp(&bars[st], (parity >> st) & 1u);
+        parity ^= 1u << st;
+      }
+      __syncwarp();
+      const double* buf = ring + (m % P) * SD;
+      double* pb = phibuf + (size_t)(mm_total & 1) * WPC * C * 128 + (size_t)w * C * 128;
+      if (active) {
+        Lu4 f[C];
+#pragma unroll
+        for (int tt = 0; tt < C; ++tt) {
+          const double sigma = buf[tt * 32 + lane];
+          const double2 u = reinterpret_cast<const double2*>(buf + C * 160 + w * C * 128 + tt * 128)[lane];
+          const double2 v = reinterpret_cast<const double2*>(buf + C * 160 + w * C * 128 + tt * 128 + 64)[lane];
+          f[tt].b0 = u.x; f[tt].b1 = u.y; f[tt].b2 = v.x; f[tt].b3 = v.y;
+          if (scat) {
+            const double2 su = reinterpret_cast<const double2*>(buf + C * 32 + tt * 128)[lane];
+            const double2 sv = reinterpret_cast<const double2*>(buf + C * 32 + tt * 128 + 64)[lane];
+            f[tt].b0 += su.x; f[tt].b1 += su.y; f[tt].b2 += sv.x; f[tt].b3 += sv.y;
+          }
+          lu4_factor<C>(a, S, sigma, f[tt]);
+        }
+        h0 = h1;
+        h1 = h2;
+        {
+          const bool need = hlane && m < hchunks && m * C + lane < nx;
+          double2* slot = hin + (int64_t)m * C + lane;
+          int spins = 0;
+          while (__any_sync(kFull, need && (is_empty(h0.x) || is_empty(h0.y)))) {
+            __nanosleep(32);
+            if (need && (is_empty(h0.x) || is_empty(h0.y))) h0 = __ldcv(slot);
+            if (++spins > (1 << 26)) {
+              if (need) atomicOr(a.status, 2);
+              h0 = make_double2(0.0, 0.0);
+            }
+          }
+          if (need) __stcg(slot, make_double2(empty, empty));
+        }
+        if (spec && hlane && m + 2 < hchunks && (m + 2) * C + lane < nx)
+          h2 = __ldcg(hin + (int64_t)(m + 2) * C + lane);
+#pragma unroll
+        for (int tt = 0; tt < C; ++tt) {
+          const int t = m * C + tt;
+          const int ip = t - lane;
+          const bool act = row_ok && ip >= 0 && ip < nx;
+          {
+            const double y0 = __shfl_sync(kFull, h0.x, tt);
+            const double y1 = __shfl_sync(kFull, h0.y, tt);
+            if (take_y) { yin0 = y0; yin1 = y1; }
+          }
+          const Lu4& F = f[tt];
+          const double v0 = fma(cy1, yin1, fma(cy0, yin0, fma(cx1, xin1, fma(cx0, xin0, F.b0))));
+          const double v1 = fma(cy3, yin1, fma(cy2, yin0, F.b1));
+          const double v2 = fma(cx3, xin1, fma(cx2, xin0, F.b2));
+          const double y1 = fma(-F.l1, v0, v1);
+          const double y2 = fma(-F.m2, y1, fma(-F.l2, v0, v2));
+          const double y3 = fma(-F.n3, y2, fma(-F.m3, y1, fma(-F.l3, v0, F.b3)));
+          const double x3 = y3 * F.p3;
+          const double x2 = fma(-F.u11, x3, y2 * F.p2);
+          const double x1 = fma(-F.u6, x2, fma(-F.u7, x3, y1 * F.p1));
+          const double x0 = fma(-F.u1, x1, fma(-F.u2, x2, fma(-F.u3, x3, v0 * F.p0)));
+          double yt0 = 0.0, yt1 = 0.0;
+          double2 q0 = make_double2(0.0, 0.0), q1 = q0;
+          if (act) {
+            double2* po = reinterpret_cast<double2*>(a.psi_sk + slot_off + (int64_t)t * 128 + 2 * lane);
+            po[0] = make_double2(x0, x1);
+            po[32] = make_double2(x2, x3);
+            xin0 = x1; xin1 = x3;
+            yt0 = x2; yt1 = x3;
+            q0 = make_double2(cw * x0, cw * x1);
+            q1 = make_double2(cw * x2, cw * x3);
+            if (lane == 31 && hout) __stcg(hout + ip, make_double2(x2, x3));
+          }
+          reinterpret_cast<double2*>(pb + tt * 128)[lane] = q0;
+          reinterpret_cast<double2*>(pb + tt * 128 + 64)[lane] = q1;
+          const double u0 = __shfl_up_sync(kFull, yt0, 1);
+          const double u1 = __shfl_up_sync(kFull, yt1, 1);
+          if (lane > 0) { yin0 = u0; yin1 = u1; }
+        }
+      }
+      __syncthreads();  // the chunk's cw psi of every direction is in phibuf
+      {
+        // group closure partial: fixed warp order
+        const double* pbase = phibuf + (size_t)(mm_total & 1) * WPC * C * 128;
+        const int t0 = m * C;
+        const int nvalid = min(C, T - t0) * 128;
+        for (int e = tid; e < nvalid; e += WPC * 32) {
+          double v = 0.0;
+          for (int k = 0; k < count; ++k) v += pbase[(size_t)k * C * 128 + e];
+          pout[(int64_t)t0 * 128 + e] = v;
+        }
+      }
+    }
+  }
+}
+
+template <int C, int P, int WPC>
+int launch_sweep1g(const SweepArgs& a, const CgTable* tab, double* part, cudaStream_t st) {
+  constexpr size_t smem =
+      ((size_t)P * (C * (32 + 128) + WPC * C * 128) + 2 * (size_t)WPC * C * 128) * sizeof(double);
+  int dev = 0, sms = 0, occ = 0;
+  DLRSN_TRY_CUDA(cudaGetDevice(&dev));
+  DLRSN_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  DLRSN_TRY_CUDA(cudaFuncSetAttribute(sweep1g_kernel<C, P, WPC>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  DLRSN_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep1g_kernel<C, P, WPC>,
+                                                               WPC * 32, smem));
+  // items = strips x groups (known on the device only): one persistent
+  // wave, every CTA draws tickets until they run out
+  int ctas = sms * (occ > 0 ? occ : 1);
+  const int max_items = sk_strips(a.ny) * a.G;  // groups <= single directions
+  if (ctas > max_items) ctas = max_items;
+  if (ctas < 1) ctas = 1;
+  sweep1g_kernel<C, P, WPC><<<ctas, WPC * 32, smem, st>>>(a, tab, part);
+  DLRSN_CHECK_LAUNCH("sweep1g_kernel");
+  return DLRSN_OK;
+}
+
+// quadrant-ordered single-direction groups -> CTA groups of <= wpc
+// directions of one quadrant, sizes balanced within the quadrant; cg_quad /
+// cg_w (dmax entries) describe the partial slabs to the closure pass
+__global__ void cgroup_plan_kernel(int G, const dlrsn_group* __restrict__ groups, int wpc, int dmax,
+                                   CgTable* __restrict__ tab, int* __restrict__ cg_quad,
+                                   double* __restrict__ cg_w) {
+  if (threadIdx.x != 0) return;
+  int ncg = 0;
+  int i = 0;
+  while (i < G) {
+    const int q = groups[i].quad;
+    int j = i;
+    while (j < G && groups[j].quad == q) ++j;
+    const int n = j - i;
+    const int k = (n + wpc - 1) / wpc;
+    const int base = n / k, rem = n % k;
+    int f = i;
+    for (int c = 0; c < k && ncg < kMaxCg; ++c) {
+      const int cnt = base + (c < rem ? 1 : 0);
+      tab->first[ncg] = f;
+      tab->count[ncg] = cnt;
+      tab->quad[ncg] = q;
+      f += cnt;
+      ++ncg;
+    }
+    i = j;
+  }
+  tab->ncg = ncg;
+  for (int c = 0; c < dmax; ++c) {
+    cg_quad[c] = c < ncg ? tab->quad[c] : -1;
+    cg_w[c] = 1.0;
+  }
+}
+
 __global__ void fill_empty_kernel(double* p, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = __longlong_as_double((long long)kEmpty);
@@ -583,6 +848,9 @@ __device__ __forceinline__ void tr_diag_cell(int e, int& il, int& jl) {
   }
 }
 
+// Both transposes are software-pipelined over the 8-direction chunks: the
+// next chunk's loads are issued into registers (16 x 16 B per thread) before
+// the current chunk's store phase, so every thread keeps 256 B in flight.
 __global__ void __launch_bounds__(256) rhs_build_tiled_kernel(
     int nx, int ny, int D, const int* __restrict__ quad, const double* __restrict__ q,
     double inv_cdt, const double* __restrict__ pt, int ldp, const double* __restrict__ ex, int lde,
@@ -593,24 +861,44 @@ __global__ void __launch_bounds__(256) rhs_build_tiled_kernel(
   const int T = nx + 31;
   int il, jl;
   tr_diag_cell(threadIdx.x, il, jl);
+  // canonical loads: element e -> (cell, dof, direction pair), pairs fastest
+  // (64-byte runs of 8 directions); pt rows 16-byte aligned (ldp even)
+  constexpr int kLd = kTrCells * 4 * (kTrD / 2) / 256;  // 16 per thread
+  double2 R[kLd];
+  auto load = [&](int d0) {
+    const int dn = min(kTrD, D - d0);
+#pragma unroll
+    for (int u = 0; u < kLd; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      const int dp = e & 3, l = (e >> 2) & 3, cl = e >> 4;
+      const int ci = cl & (kTrI - 1), cj = cl >> 3;
+      double2 v = make_double2(0.0, 0.0);
+      if (ci < ti && cj < tj && 2 * dp < dn) {
+        const int64_t c = (int64_t)(j0 + cj) * nx + i0 + ci;
+        const double* src = pt + (4 * c + l) * ldp + d0 + 2 * dp;
+        if (2 * dp + 1 < dn) v = __ldg(reinterpret_cast<const double2*>(src));
+        else v.x = __ldg(src);
+      }
+      R[u] = v;
+    }
+  };
+  auto park = [&]() {
+#pragma unroll
+    for (int u = 0; u < kLd; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      const int dp = e & 3, l = (e >> 2) & 3, cl = e >> 4;
+      tr_sm[(l * kTrD + 2 * dp) * kTrS + cl] = R[u].x;
+      tr_sm[(l * kTrD + 2 * dp + 1) * kTrS + cl] = R[u].y;
+    }
+  };
+  if (pt) load(0);
   for (int d0 = 0; d0 < D; d0 += kTrD) {
     const int dn = min(kTrD, D - d0);
     if (pt) {
-      // canonical rows: e -> (cell, dof, dir) with dir fastest (64-byte runs);
-      // unrolled so that each thread has 8 loads in flight
-#pragma unroll 8
-      for (int e = threadIdx.x; e < kTrCells * 4 * kTrD; e += blockDim.x) {
-        const int dd = e & (kTrD - 1), l = (e >> 3) & 3, cl = e >> 5;
-        const int ci = cl & (kTrI - 1), cj = cl >> 3;
-        double v = 0.0;
-        if (ci < ti && cj < tj && dd < dn) {
-          const int64_t c = (int64_t)(j0 + cj) * nx + i0 + ci;
-          v = pt[(4 * c + l) * ldp + d0 + dd];
-        }
-        tr_sm[(l * kTrD + dd) * kTrS + cl] = v;
-      }
+      park();
+      __syncthreads();
+      if (d0 + kTrD < D) load(d0 + kTrD);  // in flight during the stores below
     }
-    __syncthreads();
     for (int dd = 0; dd < dn; ++dd) {
       const int d = d0 + dd;
       const int qd = quad[d];
@@ -660,33 +948,60 @@ __global__ void __launch_bounds__(256) sk_to_canonical_tiled_kernel(
   const int T = nx + 31;
   int il, jl;
   tr_diag_cell(threadIdx.x, il, jl);
-  for (int d0 = 0; d0 < D; d0 += kTrD) {
+  const bool in = il < ti && jl < tj;
+  const bool al = ((reinterpret_cast<uintptr_t>(psi) & 15) == 0) && (ld & 1) == 0;
+  // SK loads of this thread's cell: 2 x 16 B per direction of the chunk
+  double2 A[kTrD], B[kTrD];
+  auto load = [&](int d0) {
     const int dn = min(kTrD, D - d0);
-    for (int dd = 0; dd < dn; ++dd) {
-      const int d = d0 + dd;
-      const int qd = quad[d];
-      const int ci = (qd & 1) ? ti - 1 - il : il;
-      const int cj = (qd & 2) ? tj - 1 - jl : jl;
-      if (il < ti && jl < tj) {
-        const int cl = cj * kTrI + ci;
-        const int f = sk_flip(qd);
+#pragma unroll
+    for (int dd = 0; dd < kTrD; ++dd) {
+      A[dd] = B[dd] = make_double2(0.0, 0.0);
+      if (in && dd < dn) {
+        const int d = d0 + dd;
+        const int qd = quad[d];
+        const int ci = (qd & 1) ? ti - 1 - il : il;
+        const int cj = (qd & 2) ? tj - 1 - jl : jl;
         int s, t, lane;
         sk_locate(i0 + ci, j0 + cj, qd, nx, ny, s, t, lane);
         const double* src = sk + (int64_t)d * vlen;
-        const double2 a = *reinterpret_cast<const double2*>(src + sk_vec_off(T, s, t, 0, lane));
-        const double2 b = *reinterpret_cast<const double2*>(src + sk_vec_off(T, s, t, 1, lane));
-        const double o[4] = {a.x, a.y, b.x, b.y};
+        A[dd] = __ldcs(reinterpret_cast<const double2*>(src + sk_vec_off(T, s, t, 0, lane)));
+        B[dd] = __ldcs(reinterpret_cast<const double2*>(src + sk_vec_off(T, s, t, 1, lane)));
+      }
+    }
+  };
+  load(0);
+  for (int d0 = 0; d0 < D; d0 += kTrD) {
+    const int dn = min(kTrD, D - d0);
+#pragma unroll
+    for (int dd = 0; dd < kTrD; ++dd) {
+      if (in && dd < dn) {
+        const int qd = quad[d0 + dd];
+        const int ci = (qd & 1) ? ti - 1 - il : il;
+        const int cj = (qd & 2) ? tj - 1 - jl : jl;
+        const int cl = cj * kTrI + ci;
+        const int f = sk_flip(qd);
+        const double o[4] = {A[dd].x, A[dd].y, B[dd].x, B[dd].y};
 #pragma unroll
         for (int l = 0; l < 4; ++l) tr_sm[(l * kTrD + dd) * kTrS + cl] = o[l ^ f];
       }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < kTrCells * 4 * kTrD; e += blockDim.x) {
-      const int dd = e & (kTrD - 1), l = (e >> 3) & 3, cl = e >> 5;
+    if (d0 + kTrD < D) load(d0 + kTrD);  // in flight during the stores below
+    // canonical stores: (cell, dof, direction pair), 16 B each
+    for (int e = threadIdx.x; e < kTrCells * 4 * (kTrD / 2); e += blockDim.x) {
+      const int dp = e & 3, l = (e >> 2) & 3, cl = e >> 4;
       const int ci = cl & (kTrI - 1), cj = cl >> 3;
-      if (ci < ti && cj < tj && dd < dn) {
+      if (ci < ti && cj < tj && 2 * dp < dn) {
         const int64_t c = (int64_t)(j0 + cj) * nx + i0 + ci;
-        psi[(4 * c + l) * ld + d0 + dd] = tr_sm[(l * kTrD + dd) * kTrS + cl];
+        double* dst = psi + (4 * c + l) * ld + d0 + 2 * dp;
+        const double v0 = tr_sm[(l * kTrD + 2 * dp) * kTrS + cl];
+        if (2 * dp + 1 < dn && al) {
+          *reinterpret_cast<double2*>(dst) = make_double2(v0, tr_sm[(l * kTrD + 2 * dp + 1) * kTrS + cl]);
+        } else {
+          dst[0] = v0;
+          if (2 * dp + 1 < dn) dst[1] = tr_sm[(l * kTrD + 2 * dp + 1) * kTrS + cl];
+        }
       }
     }
     __syncthreads();
@@ -1281,7 +1596,7 @@ int dlrsn_rhs_build(const dlrsn_cellops* ops, int D, const int* quad, const doub
   DLRSN_REQUIRE(ops && D >= 0, "bad arguments to dlrsn_rhs_build");
   const int64_t n = (int64_t)ops->nx * ops->ny * D;
   if (n == 0) return DLRSN_OK;
-  if (tiled_transposes()) {
+  if (tiled_transposes() && (!psi_time || (((reinterpret_cast<uintptr_t>(psi_time) | (uintptr_t)ld_psi_time * 8) & 15) == 0))) {
     DLRSN_TRY_CUDA(cudaFuncSetAttribute(rhs_build_tiled_kernel,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrSmem));
     const dim3 grid((ops->nx + kTrI - 1) / kTrI, (ops->ny + kTrJ - 1) / kTrJ);
@@ -1555,6 +1870,76 @@ static int sweep_launch_ex(const dlrsn_cellops* ops, int G, const dlrsn_group* g
     case 4: rc = launch_sweep<4>(a, max_ctas, st); break;
     default: rc = launch_sweep<8>(a, max_ctas, st); break;
   }
+  if (tm && rc == DLRSN_OK) DLRSN_TRY_CUDA(cudaEventRecord(tm->stop, st));
+  return rc;
+}
+
+// directions per CTA group of the grouped sweep (DLRSN_SWEEP_GROUP: 4 or 8;
+// 0 = the ungrouped kernel + the separate closure pass).  Off by default:
+// measured on C4 (1024^2, 64 directions) the lock step costs more than the
+// closure pass it removes -- 32.0 (8 per group) / 32.5 ms (4) vs 30.0 ms
+// per 4-iteration step: a CTA barrier per chunk keeps every warp of an SM in
+// the same phase (all factorising, then all on the dependent chain), where
+// independent warps overlap one's chain with another's factorisation.
+int sweep_group_width() {
+  static const int v = [] {
+    const char* e = getenv("DLRSN_SWEEP_GROUP");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+int cgroup_plan_launch(int G, const dlrsn_group* groups, int wpc, int dmax, CgTable* tab,
+                       int* cg_quad, double* cg_w, cudaStream_t st) {
+  cgroup_plan_kernel<<<1, 32, 0, st>>>(G, groups, wpc, dmax, tab, cg_quad, cg_w);
+  DLRSN_CHECK_LAUNCH("cgroup_plan_kernel");
+  return DLRSN_OK;
+}
+
+int sweep_grouped_launch(const dlrsn_cellops* ops, int G, const dlrsn_group* groups,
+                         const CgTable* tab, const double* sigma_t_sk4, const double* scat_sk4,
+                         const double* rhs_sk, double* psi_sk, double* part, void* workspace,
+                         int64_t workspace_bytes, const int* skip, cudaStream_t st) {
+  DLRSN_REQUIRE(ops && groups && tab && sigma_t_sk4 && rhs_sk && psi_sk && part && workspace,
+                "null argument to the grouped sweep");
+  const int64_t need = dlrsn_sweep_workspace_bytes(ops->nx, ops->ny, G, 1);
+  DLRSN_REQUIRE(workspace_bytes >= need, "sweep workspace too small (%lld < %lld)",
+                (long long)workspace_bytes, (long long)need);
+  if (G == 0) return DLRSN_OK;
+  SweepArgs a;
+  memset(&a, 0, sizeof(a));
+  a.nx = ops->nx; a.ny = ops->ny; a.G = G;
+  a.groups = groups;
+  a.sigma_sk4 = sigma_t_sk4;
+  a.scat_sk4 = scat_sk4;
+  a.rhs_sk = rhs_sk;
+  a.psi_sk = psi_sk;
+  a.ticket = reinterpret_cast<int*>(workspace);
+  a.status = reinterpret_cast<int*>(workspace) + 1;
+  a.handoff = reinterpret_cast<double*>(reinterpret_cast<char*>(workspace) +
+                                        handoff_offset_bytes(ops->nx, ops->ny, G));
+  for (int m = 0; m < 16; ++m) {
+    a.mass[m] = ops->mass[m];
+    a.gxp[m] = ops->gx[m];
+    a.gyp[m] = ops->gy[m];
+  }
+  const int ix[2] = {1, 3}, iy[2] = {2, 3};
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 2; ++c) {
+      a.gxp[4 * ix[r] + ix[c]] += ops->e2x[2 * r + c];
+      a.gyp[4 * iy[r] + iy[c]] += ops->e2y[2 * r + c];
+    }
+  for (int m = 0; m < 4; ++m) {
+    a.ex[m] = ops->e2x[m];
+    a.ey[m] = ops->e2y[m];
+  }
+  a.vlen = sk_vec_len(ops->nx, ops->ny);
+  a.slen = sk_scalar_len(ops->nx, ops->ny);
+  a.skip = skip;
+  SweepTimer* tm = g_timing ? timer_slot(G, 1) : nullptr;
+  if (tm) DLRSN_TRY_CUDA(cudaEventRecord(tm->start, st));
+  const int rc = sweep_group_width() == 4 ? launch_sweep1g<4, 3, 4>(a, tab, part, st)
+                                          : launch_sweep1g<4, 3, 8>(a, tab, part, st);
   if (tm && rc == DLRSN_OK) DLRSN_TRY_CUDA(cudaEventRecord(tm->stop, st));
   return rc;
 }

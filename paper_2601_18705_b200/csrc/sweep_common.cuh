@@ -34,6 +34,19 @@ struct SweepArgs {
   double* phi_atomic;
 };
 
+// Direction groups of the grouped single-direction sweep (sweep1g_kernel):
+// up to kCgWarps directions of one quadrant swept by one CTA in lock step,
+// their closure summed in shared memory (one partial slab per group).
+// first/count index the quadrant-ordered single-direction group list.
+constexpr int kMaxCg = DLRSN_MAX_RANK + 4;
+struct CgTable {
+  int ncg;
+  int pad[3];
+  int first[kMaxCg];
+  int count[kMaxCg];
+  int quad[kMaxCg];
+};
+
 // isotropic inflow psi_b on the left, right, bottom, top walls (0: vacuum)
 struct Inflow4 {
   double v[4];
@@ -111,6 +124,15 @@ int launch_sweep_ws(const SweepArgs& a, int max_ctas, cudaStream_t st);
 bool sweep_timing_enabled();
 bool project_timing_enabled();
 int advance_launch(const dlrsn_advance* av, const double* phi, cudaStream_t st);
+// sweep.cu: the grouped single-direction sweep (psi + per-group closure
+// partials, one partial slab of sk_vec_len doubles per group)
+int sweep_grouped_launch(const dlrsn_cellops* ops, int G, const dlrsn_group* groups,
+                         const CgTable* tab, const double* sigma_t_sk4, const double* scat_sk4,
+                         const double* rhs_sk, double* psi_sk, double* part, void* workspace,
+                         int64_t workspace_bytes, const int* skip, cudaStream_t st);
+int cgroup_plan_launch(int G, const dlrsn_group* groups, int wpc, int dmax, CgTable* tab,
+                       int* cg_quad, double* cg_w, cudaStream_t st);
+int sweep_group_width();
 // dense.cu: Y = X K for an upper-triangular r x r K (skips the zero blocks)
 int rowmix_upper(int64_t n, int r, const double* X, int ldx, const double* K, int ldk, double* Y,
                  int ldy, cudaStream_t st);
