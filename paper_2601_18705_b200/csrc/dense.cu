@@ -555,7 +555,7 @@ struct MgramWide {
 };
 
 template <int TB>
-__global__ void __launch_bounds__(256, 1) mgram_wide_kernel(int ncell, int ra, int rb,
+__global__ void __launch_bounds__(256, TB == 64 ? 2 : 1) mgram_wide_kernel(int ncell, int ra, int rb,
                                                          const double* __restrict__ A, int lda,
                                                          const double* __restrict__ B, int ldb,
                                                          const double* __restrict__ coeff,
