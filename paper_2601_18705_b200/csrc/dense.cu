@@ -2448,49 +2448,98 @@ __global__ void row_inverse_inplace_kernel(int r, const double* __restrict__ pro
 
 // LU with partial pivoting of an n x n matrix in shared memory (one CTA)
 // and solve with nrhs right-hand sides stored column-major after it.
+__device__ __forceinline__ double pick4(const double (&v)[4], int k) {
+  return k == 0 ? v[0] : (k == 1 ? v[1] : (k == 2 ? v[2] : v[3]));
+}
+
 __device__ void cta_lu_solve(int n, double* a, int lda, double* b, int ldb, int nrhs, int* perm,
                              int* sing) {
+  // three barriers per column: pivot search by warp 0 (first maximal |entry|,
+  // as a serial scan picks it); row swap with the scaled multipliers saved;
+  // the rank-1 update.  n <= 128.
+  __shared__ double colk[DLRSN_MAX_RANK];
+  __shared__ double s_inv, s_akk;
+  const int tid = threadIdx.x, lane = tid & 31;
   for (int k = 0; k < n; ++k) {
     __syncthreads();
-    if (threadIdx.x == 0) {
-      int p = k;
-      double best = fabs(a[k * lda + k]);
-      for (int i = k + 1; i < n; ++i) {
+    if (tid < 32) {
+      double best = -1.0;
+      int p = n;
+      for (int i = k + lane; i < n; i += 32) {
         const double v = fabs(a[i * lda + k]);
         if (v > best) { best = v; p = i; }
       }
-      perm[k] = p;
-      if (!(best > 0.0)) *sing = 1;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(kFull, best, o);
+        const int op = __shfl_xor_sync(kFull, p, o);
+        if (ob > best || (ob == best && op < p)) { best = ob; p = op; }
+      }
+      if (lane == 0) {
+        if (p >= n) p = k;
+        perm[k] = p;
+        const double piv = a[p * lda + k];
+        s_inv = piv != 0.0 ? 1.0 / piv : 0.0;
+        s_akk = a[k * lda + k];  // moves to row p in the swap
+        if (!(best > 0.0)) *sing = 1;
+      }
     }
     __syncthreads();
     const int p = perm[k];
+    const double inv = s_inv;
     if (p != k) {
-      for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      for (int j = tid; j < n; j += blockDim.x) {
         const double t = a[k * lda + j]; a[k * lda + j] = a[p * lda + j]; a[p * lda + j] = t;
       }
-      for (int j = threadIdx.x; j < nrhs; j += blockDim.x) {
+      for (int j = tid; j < nrhs; j += blockDim.x) {
         const double t = b[k * ldb + j]; b[k * ldb + j] = b[p * ldb + j]; b[p * ldb + j] = t;
       }
     }
-    __syncthreads();
-    const double piv = a[k * lda + k];
-    for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) a[i * lda + k] = piv != 0.0 ? a[i * lda + k] / piv : 0.0;
+    // multipliers of the rows below; row p now holds the old row k, whose
+    // column-k entry was saved before the swap (rows != k, p are untouched)
+    for (int i = k + 1 + tid; i < n; i += blockDim.x)
+      colk[i] = (i == p ? s_akk : a[i * lda + k]) * inv;
     __syncthreads();
     const int m = n - k - 1;
-    for (int e = threadIdx.x; e < m * (m + nrhs); e += blockDim.x) {
-      const int i = k + 1 + e / (m + nrhs), jj = e % (m + nrhs);
-      const double l = a[i * lda + k];
-      if (jj < m) a[i * lda + k + 1 + jj] -= l * a[k * lda + k + 1 + jj];
+    for (int e = tid; e < m * (m + nrhs + 1); e += blockDim.x) {
+      const int i = k + 1 + e / (m + nrhs + 1), jj = e % (m + nrhs + 1);
+      const double l = colk[i];
+      if (jj == m + nrhs) a[i * lda + k] = l;
+      else if (jj < m) a[i * lda + k + 1 + jj] -= l * a[k * lda + k + 1 + jj];
       else b[i * ldb + (jj - m)] -= l * b[k * ldb + (jj - m)];
     }
   }
   __syncthreads();
-  // back substitution, one thread per rhs
-  for (int j = threadIdx.x; j < nrhs; j += blockDim.x) {
+  // back substitution: a warp per right-hand side, the column in registers
+  const int warp = tid >> 5, nw = blockDim.x >> 5;
+  for (int j = warp; j < nrhs; j += nw) {
+    double x[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = lane + 32 * q;
+      x[q] = i < n ? b[i * ldb + j] : 0.0;
+    }
     for (int i = n - 1; i >= 0; --i) {
-      double s = b[i * ldb + j];
-      for (int p = i + 1; p < n; ++p) s -= a[i * lda + p] * b[p * ldb + j];
-      b[i * ldb + j] = a[i * lda + i] != 0.0 ? s / a[i * lda + i] : 0.0;
+      double sacc = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = lane + 32 * q;
+        if (c > i && c < n) sacc = fma(a[i * lda + c], x[q], sacc);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(kFull, sacc, o);
+      if (lane == (i & 31)) {
+        const int q = i >> 5;
+        const double d = a[i * lda + i];
+        const double v = d != 0.0 ? (pick4(x, q) - sacc) / d : 0.0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (t == q) x[t] = v;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = lane + 32 * q;
+      if (i < n) b[i * ldb + j] = x[q];
     }
   }
   __syncthreads();
@@ -2597,7 +2646,7 @@ __global__ void row_sums_kernel(int n, int r, const double* __restrict__ Binv,
   }
 }
 
-__global__ void row_solve_kernel(int r, const double* __restrict__ ms, double* __restrict__ scratch,
+__global__ void __launch_bounds__(1024) row_solve_kernel(int r, const double* __restrict__ ms, double* __restrict__ scratch,
                                  double* __restrict__ lbar, int* status) {
   extern __shared__ double sm[];
   double* lhs = sm;           // r*r
@@ -2639,7 +2688,7 @@ int row_combine_grid(int n, int r, const double* Binv, const double* ms, const d
   DLRSN_CHECK_LAUNCH("row_sums_kernel");
   DLRSN_TRY_CUDA(cudaFuncSetAttribute(row_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
-  row_solve_kernel<<<1, 256, smem, st>>>(r, ms, scratch, lbar, status);
+  row_solve_kernel<<<1, 1024, smem, st>>>(r, ms, scratch, lbar, status);
   DLRSN_CHECK_LAUNCH("row_solve_kernel");
   row_bq_kernel<<<n, 128, 0, st>>>(r, Binv, Q, scratch + r * r + r, L);
   DLRSN_CHECK_LAUNCH("row_bq_kernel");
@@ -3155,74 +3204,95 @@ __global__ void __launch_bounds__(kDeimGT) deim_grid_kernel(int n, int r, int nl
 // Solves with W_hat = Lhat U (pick order):
 //   mode 0 (interpolation_coefficients): X = W_hat^-1 V   (V r x m)
 //   mode 1 (closure_weights):            x = W_hat^-T v   (v r)
-__global__ void what_solve_kernel(int r, int m, const double* __restrict__ Lhat,
-                                  const double* __restrict__ U, const double* __restrict__ V,
-                                  double* __restrict__ X, int mode, int factors_global) {
+// A warp per right-hand side: the solution column lives in registers (lane
+// l holds rows l, l + 32, ...), each substitution row is a warp dot product
+// of a factor row (contiguous, conflict-free) with the solved part.  For
+// mode 1 the factors are staged transposed so the rows stay contiguous.
+__global__ void __launch_bounds__(1024) what_solve_kernel(int r, int m, const double* __restrict__ Lhat,
+                                                          const double* __restrict__ U,
+                                                          const double* __restrict__ V,
+                                                          double* __restrict__ X, int mode,
+                                                          int factors_global) {
   extern __shared__ double sw[];
-  // factors_global (r x r factors too large to stage next to the rhs, r >
-  // ~110): the substitutions read Lhat / U from global memory (L1 / L2)
-  const double* sL = factors_global ? Lhat : sw;          // r x r
-  const double* sU = factors_global ? U : sw + r * r;     // r x r
-  double* sX = factors_global ? sw : sw + 2 * r * r;      // r x m
-  if (!factors_global)
-    for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
-      cp_async8(sw + e, Lhat + e);
-      cp_async8(sw + r * r + e, U + e);
+  // factors_global (r x r factors too large to stage, r > ~110): read from
+  // global memory (L1 / L2), transposed access for mode 1
+  double* sF = sw;  // [2][r][r]: mode 0: L, U; mode 1: U^T, L^T
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int64_t rr = (int64_t)r * r;
+  if (!factors_global) {
+    for (int e = tid; e < r * r; e += blockDim.x) {
+      const int i = e / r, j = e - (e / r) * r;
+      if (mode == 0) {
+        sF[e] = Lhat[e];
+        sF[rr + e] = U[e];
+      } else {
+        sF[i * r + j] = U[(int64_t)j * r + i];
+        sF[rr + i * r + j] = Lhat[(int64_t)j * r + i];
+      }
     }
-  for (int e = threadIdx.x; e < r * m; e += blockDim.x) cp_async8(sX + e, V + e);
-  cp_async_wait_all();
-  __syncthreads();
-  // one thread per right-hand side: sequential substitutions, the factor
-  // entries are warp-broadcast reads, the solution column is thread-private
-  // (two partial sums per row for a shorter dependency chain)
-  for (int c = threadIdx.x; c < m; c += blockDim.x) {
-    double* x = sX + c;
-    if (mode == 0) {
-      for (int i = 0; i < r; ++i) {  // L y = v
-        double s0 = 0.0, s1 = 0.0;
-        int p = 0;
-        for (; p + 1 < i; p += 2) {
-          s0 = fma(sL[i * r + p], x[p * m], s0);
-          s1 = fma(sL[i * r + p + 1], x[(p + 1) * m], s1);
-        }
-        if (p < i) s0 = fma(sL[i * r + p], x[p * m], s0);
-        x[i * m] -= s0 + s1;
+    __syncthreads();
+  }
+  // A[i][p]: first factor (forward, lower-triangular use), B: second (backward)
+  auto fa = [&](int i, int p) -> double {
+    if (!factors_global) return sF[i * r + p];
+    return mode == 0 ? Lhat[(int64_t)i * r + p] : U[(int64_t)p * r + i];
+  };
+  auto fb = [&](int i, int p) -> double {
+    if (!factors_global) return sF[rr + i * r + p];
+    return mode == 0 ? U[(int64_t)i * r + p] : Lhat[(int64_t)p * r + i];
+  };
+  const bool unit_a = mode == 0;  // L (mode 0) has a unit diagonal; U^T does not
+  for (int c = warp; c < m; c += nw) {
+    double x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = lane + 32 * k;
+      x[k] = i < r ? V[(int64_t)i * m + c] : 0.0;
+    }
+    // forward: A y = v, A lower triangular
+    for (int i = 0; i < r; ++i) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int p = lane + 32 * k;
+        if (p < i) sacc = fma(fa(i, p), x[k], sacc);
       }
-      for (int i = r - 1; i >= 0; --i) {  // U x = y
-        double s0 = 0.0, s1 = 0.0;
-        int p = i + 1;
-        for (; p + 1 < r; p += 2) {
-          s0 = fma(sU[i * r + p], x[p * m], s0);
-          s1 = fma(sU[i * r + p + 1], x[(p + 1) * m], s1);
-        }
-        if (p < r) s0 = fma(sU[i * r + p], x[p * m], s0);
-        x[i * m] = (x[i * m] - (s0 + s1)) / sU[i * r + i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(kFull, sacc, o);
+      if (lane == (i & 31)) {
+        const int k = i >> 5;
+        double v = pick4(x, k) - sacc;
+        if (!unit_a) v /= fa(i, i);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q == k) x[q] = v;
       }
-    } else {
-      for (int i = 0; i < r; ++i) {  // U^T y = v
-        double s0 = 0.0, s1 = 0.0;
-        int p = 0;
-        for (; p + 1 < i; p += 2) {
-          s0 = fma(sU[p * r + i], x[p * m], s0);
-          s1 = fma(sU[(p + 1) * r + i], x[(p + 1) * m], s1);
-        }
-        if (p < i) s0 = fma(sU[p * r + i], x[p * m], s0);
-        x[i * m] = (x[i * m] - (s0 + s1)) / sU[i * r + i];
+    }
+    // backward: B x = y, B upper triangular (U, or L^T with a unit diagonal)
+    for (int i = r - 1; i >= 0; --i) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int p = lane + 32 * k;
+        if (p > i && p < r) sacc = fma(fb(i, p), x[k], sacc);
       }
-      for (int i = r - 1; i >= 0; --i) {  // L^T x = y
-        double s0 = 0.0, s1 = 0.0;
-        int p = i + 1;
-        for (; p + 1 < r; p += 2) {
-          s0 = fma(sL[p * r + i], x[p * m], s0);
-          s1 = fma(sL[(p + 1) * r + i], x[(p + 1) * m], s1);
-        }
-        if (p < r) s0 = fma(sL[p * r + i], x[p * m], s0);
-        x[i * m] -= s0 + s1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(kFull, sacc, o);
+      if (lane == (i & 31)) {
+        const int k = i >> 5;
+        double v = pick4(x, k) - sacc;
+        if (mode == 0) v /= fb(i, i);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q == k) x[q] = v;
       }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = lane + 32 * k;
+      if (i < r) X[(int64_t)i * m + c] = x[k];
     }
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < r * m; e += blockDim.x) X[e] = sX[e];
 }
 
 }  // namespace dlrsn
@@ -3836,13 +3906,14 @@ int dlrsn_deim(int n, int r, double* Wwork, const double* W, int* idx, double* L
 
 int dlrsn_what_solve(int r, int m, const double* Lhat, const double* U, const double* V,
                      double* X, int mode, dlrsn_stream_t stream) {
-  size_t smem = (2 * (size_t)r * r + (size_t)r * m) * sizeof(double);
+  DLRSN_REQUIRE(r >= 1 && r <= DLRSN_MAX_RANK && m >= 1, "bad W_hat solve shape (%d, %d)", r, m);
+  size_t smem = 2 * (size_t)r * r * sizeof(double);
   const int fg = smem > 200 * 1024;
-  if (fg) smem = (size_t)r * m * sizeof(double);
-  DLRSN_REQUIRE(smem <= 200 * 1024, "W_hat solve too large for shared memory");
+  if (fg) smem = 0;
   DLRSN_TRY_CUDA(cudaFuncSetAttribute(what_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
-  what_solve_kernel<<<1, 128, smem, as_stream(stream)>>>(r, m, Lhat, U, V, X, mode, fg);
+  const int threads = 32 * std::min(32, m);
+  what_solve_kernel<<<1, threads, smem, as_stream(stream)>>>(r, m, Lhat, U, V, X, mode, fg);
   DLRSN_CHECK_LAUNCH("what_solve_kernel");
   return DLRSN_OK;
 }

@@ -127,23 +127,35 @@ __global__ void ortho_residual_kernel(int r, const double* __restrict__ Gx,
 // + sum_w max(-omega_d.n_w, 0) psi_b,w h[w][j]: the projected inflow load of
 // the selected direction d (isotropic inflow walls, h = X_new^T g_w; hin null
 // for vacuum walls, the reference's case)
-__global__ void qall_kernel(int r, const double* __restrict__ S, const double* __restrict__ mo,
+__global__ void __launch_bounds__(1024) qall_kernel(int r, const double* __restrict__ S, const double* __restrict__ mo,
                             const double* __restrict__ qhat, const double* __restrict__ W,
                             const int* __restrict__ idx, double inv_cdt, double* __restrict__ T,
                             double* __restrict__ qall, const double* __restrict__ hin,
-                            Inflow4 inflow, const double* __restrict__ om_sel) {
+                            Inflow4 inflow, const double* __restrict__ om_sel, int staged) {
+  // staged (3 r^2 doubles of shared memory): S, mo and T in shared memory
+  extern __shared__ double sq[];
+  const double* sS = staged ? sq : S;
+  const double* sM = staged ? sq + r * r : mo;
+  double* sT = staged ? sq + 2 * r * r : T;
+  if (staged) {
+    for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+      sq[e] = S[e];
+      sq[r * r + e] = mo[e];
+    }
+    __syncthreads();
+  }
   for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
     const int i = e / r, j = e % r;
     double s = 0.0;
-    for (int k = 0; k < r; ++k) s = fma(S[k * r + i], mo[k * r + j], s);
-    T[e] = s;
+    for (int k = 0; k < r; ++k) s = fma(sS[k * r + i], sM[k * r + j], s);
+    sT[e] = s;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
     const int d = e / r, j = e % r;
     const double* w = W + (int64_t)idx[d] * r;
     double s = 0.0;
-    for (int i = 0; i < r; ++i) s = fma(w[i], T[i * r + j], s);
+    for (int i = 0; i < r; ++i) s = fma(w[i], sT[i * r + j], s);
     double v = qhat[j] + inv_cdt * s;
     if (hin) {
       const double ox = om_sel[3 * d], oy = om_sel[3 * d + 1];
@@ -967,7 +979,7 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
       DLRSN_RET(cgroup_plan_launch(G, b.groups, sweep_group_width(), r, b.cgtab, b.cg_quad, b.cg_w,
                                    st));
     // 2. evaluate_rows (dlr_sn.py:110-121) and the sweep rhs
-    ks_kernel<<<1, 256, 0, st>>>(r, S, W, b.idx, beta, b.K, nullptr, p->omegas_dev, b.om_sel);
+    ks_kernel<<<1, 1024, 0, st>>>(r, S, W, b.idx, beta, b.K, nullptr, p->omegas_dev, b.om_sel);
     DLRSN_CHECK_LAUNCH("ks_kernel");
     DLRSN_RET(dlrsn_rowmix(N, r, r, X, r, b.K, r, 0.0, b.psi_time, r, s));
     const double* pt_local = b.psi_time;
@@ -1075,9 +1087,17 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     }
     DLRSN_RET(dlrsn_project(ops, r, X_new, X, sigma_t, sigma_s, q, b.proj, b.part, s));
     if (has_inflow) DLRSN_RET(dlrsn_inflow_project(ops, r, X_new, r, p->inflow, b.hin, s));
-    qall_kernel<<<1, 256, 0, st>>>(r, S, b.proj + 6 * r * r, b.proj + 7 * r * r, W, b.idx,
-                                   p->inv_cdt, b.T, b.qall, has_inflow ? b.hin : nullptr, infl,
-                                   b.om_sel);
+    {
+      const size_t qsm = 3 * (size_t)r * r * sizeof(double);
+      const int staged = qsm <= 160 * 1024;
+      if (staged)
+        DLRSN_TRY_CUDA(cudaFuncSetAttribute(qall_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)qsm));
+      qall_kernel<<<1, 1024, staged ? qsm : 0, st>>>(r, S, b.proj + 6 * r * r, b.proj + 7 * r * r,
+                                                     W, b.idx, p->inv_cdt, b.T, b.qall,
+                                                     has_inflow ? b.hin : nullptr, infl, b.om_sel,
+                                                     staged);
+    }
     DLRSN_CHECK_LAUNCH("qall_kernel");
     DLRSN_TRY_CUDA(zero_async(b.rowstat, (r + 1) * sizeof(int), st));
     DLRSN_RET(dlrsn_row_inverse(r, r, b.proj, b.om_sel, b.Binv, nullptr, b.rowstat, s));

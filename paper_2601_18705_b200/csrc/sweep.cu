@@ -336,8 +336,8 @@ struct Lu4 {
   double b0, b1, b2, b3;          // source part of the rhs (rhs + scattering source)
 };
 
-template <int C>
-__device__ __forceinline__ void lu4_factor(const SweepArgs& a, const double* S, double sigma,
+template <int C, class SA>
+__device__ __forceinline__ void lu4_factor(const SweepArgs& a, const SA& S, double sigma,
                                            Lu4& f) {
   double A[16];
 #pragma unroll
@@ -360,8 +360,10 @@ __device__ __forceinline__ void lu4_factor(const SweepArgs& a, const double* S, 
   f.u11 = A[11] * f.p2;
 }
 
-template <int C, int P, int WPC>
-__global__ void __launch_bounds__(WPC * 32)
+// MINB > 1: that many CTAs per SM (registers capped accordingly), the
+// direction's streaming operator S kept in shared memory instead of registers
+template <int C, int P, int WPC, int MINB = 1>
+__global__ void __launch_bounds__(WPC * 32, MINB)
 sweep1s_kernel(const SweepArgs a) {
   const bool skip = a.skip != nullptr && *a.skip != 0;
   constexpr int SD = C * (32 + 128 + 128);  // doubles per stage: sigma | scat | rhs
@@ -400,9 +402,16 @@ sweep1s_kernel(const SweepArgs a) {
     const dlrsn_group* grp = a.groups + g;
     const int quad = grp->quad;
     const double ox = grp->ox[0], oy = grp->oy[0], cw = grp->cw[0];
-    double S[16];
+    double S_reg[MINB > 1 ? 1 : 16];
+    __shared__ double s_S[WPC][16];
+    if constexpr (MINB > 1) {
+      __syncwarp();
+      if (lane < 16) s_S[wib][lane] = ox * a.gxp[lane] + oy * a.gyp[lane];
+      __syncwarp();
+    } else {
 #pragma unroll
-    for (int m = 0; m < 16; ++m) S[m] = ox * a.gxp[m] + oy * a.gyp[m];
+      for (int m = 0; m < 16; ++m) S_reg[m] = ox * a.gxp[m] + oy * a.gyp[m];
+    }
     const double cx0 = ox * a.ex[0], cx1 = ox * a.ex[1], cx2 = ox * a.ex[2], cx3 = ox * a.ex[3];
     const double cy0 = oy * a.ey[0], cy1 = oy * a.ey[1], cy2 = oy * a.ey[2], cy3 = oy * a.ey[3];
     const int64_t strip_vec = (int64_t)s * T * 128;
@@ -463,7 +472,10 @@ sweep1s_kernel(const SweepArgs a) {
           const double2 sv = reinterpret_cast<const double2*>(buf + C * 32 + tt * 128 + 64)[lane];
           f[tt].b0 += su.x; f[tt].b1 += su.y; f[tt].b2 += sv.x; f[tt].b3 += sv.y;
         }
-        lu4_factor<C>(a, S, sigma, f[tt]);
+        if constexpr (MINB > 1)
+          lu4_factor<C>(a, s_S[wib], sigma, f[tt]);
+        else
+          lu4_factor<C>(a, S_reg, sigma, f[tt]);
       }
       __syncwarp();  // every lane has read stage m % P before it is refilled
       // the chunk's y-inflow of lane 0 (strip below, via L2)
@@ -529,15 +541,15 @@ sweep1s_kernel(const SweepArgs a) {
   }
 }
 
-template <int C, int P, int WPC>
+template <int C, int P, int WPC, int MINB = 1>
 int launch_sweep1s(const SweepArgs& a, int max_ctas, cudaStream_t st) {
   constexpr size_t smem = (size_t)WPC * P * C * (32 + 128 + 128) * sizeof(double);
   int dev = 0, sms = 0, occ = 0;
   DLRSN_TRY_CUDA(cudaGetDevice(&dev));
   DLRSN_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  DLRSN_TRY_CUDA(cudaFuncSetAttribute(sweep1s_kernel<C, P, WPC>,
+  DLRSN_TRY_CUDA(cudaFuncSetAttribute(sweep1s_kernel<C, P, WPC, MINB>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  DLRSN_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep1s_kernel<C, P, WPC>,
+  DLRSN_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep1s_kernel<C, P, WPC, MINB>,
                                                                WPC * 32, smem));
   const int items = sk_strips(a.ny) * a.G;
   int ctas = (items + WPC - 1) / WPC;
@@ -545,7 +557,7 @@ int launch_sweep1s(const SweepArgs& a, int max_ctas, cudaStream_t st) {
   if (ctas > cap) ctas = cap;
   if (max_ctas > 0 && ctas > max_ctas) ctas = max_ctas;
   if (ctas < 1) ctas = 1;
-  sweep1s_kernel<C, P, WPC><<<ctas, WPC * 32, smem, st>>>(a);
+  sweep1s_kernel<C, P, WPC, MINB><<<ctas, WPC * 32, smem, st>>>(a);
   DLRSN_CHECK_LAUNCH("sweep1s_kernel");
   return DLRSN_OK;
 }
@@ -1855,6 +1867,10 @@ static int sweep_launch_ex(const dlrsn_cellops* ops, int G, const dlrsn_group* g
         case 10: rc = launch_sweep1s<2, 4, 2>(a, max_ctas, st); break;
         case 11: rc = launch_sweep1s<4, 2, 2>(a, max_ctas, st); break;
         case 12: rc = launch_sweep1s<2, 3, 4>(a, max_ctas, st); break;
+        // 12 warps per SM (167 registers, S in shared memory): C4 1.46 vs
+        // 1.32 ms, C5 29.9 vs 31.4 ms; 14-16 warps per SM (128 registers)
+        // spill and run 2-3x slower
+        case 15: rc = launch_sweep1s<2, 4, 2, 6>(a, max_ctas, st); break;
         case 9: rc = launch_sweep<1, 0>(a, max_ctas, st); break;
         case 1: rc = launch_sweep<1, 1>(a, max_ctas, st); break;
         case 2: rc = launch_sweep<1, 2>(a, max_ctas, st); break;
