@@ -774,6 +774,9 @@ struct ProjArgs {
   // the next slab, which sees this slab's top row as its halo)
   const double* halo;
   int top_wall;
+  // no scattering (sigma_s null, or *any_scat == 0 on the device): ms = 0
+  // exactly, its MMAs are skipped
+  const int* any_scat;
 };
 
 __device__ inline double ldx(const double* X, int r, int64_t row, int col) {
@@ -913,7 +916,7 @@ __global__ void __launch_bounds__(256, 2) project_kernel(ProjArgs pa, dlrsn_cell
     }
     for (int e = threadIdx.x; e < nc; e += blockDim.x) {
       sC[2 * e] = __ldg(pa.sigma_t + c0 + e);
-      sC[2 * e + 1] = __ldg(pa.sigma_s + c0 + e);
+      sC[2 * e + 1] = pa.sigma_s ? __ldg(pa.sigma_s + c0 + e) : 0.0;
     }
     __syncthreads();
     for (int cl = g; cl < nc; cl += 4) {
@@ -1128,7 +1131,7 @@ __global__ void __launch_bounds__(256, 2) project_mma_kernel(ProjArgs pa, dlrsn_
     const bool cst = live && threadIdx.x < C;  // sigma of cell cc0 + threadIdx.x
     const int cs = cc0 + (int)threadIdx.x;
     w.st = (cc0 < c_end && threadIdx.x < C && cs < c_end) ? __ldg(pa.sigma_t + cs) : 0.0;
-    w.ss = (cc0 < c_end && threadIdx.x < C && cs < c_end) ? __ldg(pa.sigma_s + cs) : 0.0;
+    w.ss = (pa.sigma_s && cc0 < c_end && threadIdx.x < C && cs < c_end) ? __ldg(pa.sigma_s + cs) : 0.0;
     (void)cst;
   };
   Raw cur;
@@ -1356,7 +1359,7 @@ __global__ void __launch_bounds__(256, 1) project_mma32_kernel(ProjArgs pa, dlrs
     w.qc = (live && side == 1) ? __ldg(pa.q + c) : 0.0;
     const int cs = cc0 + (int)threadIdx.x;
     w.st = (cc0 < c_end && threadIdx.x < C && cs < c_end) ? __ldg(pa.sigma_t + cs) : 0.0;
-    w.ss = (cc0 < c_end && threadIdx.x < C && cs < c_end) ? __ldg(pa.sigma_s + cs) : 0.0;
+    w.ss = (pa.sigma_s && cc0 < c_end && threadIdx.x < C && cs < c_end) ? __ldg(pa.sigma_s + cs) : 0.0;
   };
   Raw cur;
   fetch(c_begin, cur);
@@ -1581,6 +1584,7 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
   const double* e2x = so + 48;
   const double* e2y = so + 52;
   const int r = pa.r, nx = pa.nx, ny = pa.ny;
+  const bool no_ms = pa.sigma_s == nullptr || (pa.any_scat != nullptr && *pa.any_scat == 0);
   const int ncell = nx * ny;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3, kk = q & 1, second = q >> 1;
@@ -1639,7 +1643,7 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
       w.qc = live ? __ldg(pa.q + c) : 0.0;
       const int cs = cc0 + (int)threadIdx.x;
       w.st = (cc0 < c_end && threadIdx.x < C && cs < c_end) ? __ldg(pa.sigma_t + cs) : 0.0;
-      w.ss = (cc0 < c_end && threadIdx.x < C && cs < c_end) ? __ldg(pa.sigma_s + cs) : 0.0;
+      w.ss = (pa.sigma_s && cc0 < c_end && threadIdx.x < C && cs < c_end) ? __ldg(pa.sigma_s + cs) : 0.0;
     }
   };
   Raw cur;
@@ -1736,11 +1740,16 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
         if (!mo_only) {
 #pragma unroll
           for (int a = 0; a < 2; ++a) {
-            const double xs = stc * xa[a], xss = ssc * xa[a];
+            const double xs = stc * xa[a];
 #pragma unroll
-            for (int b = 0; b < 2; ++b) {
-              dmma(acc[0][a][b][0], acc[0][a][b][1], xs, mx[b]);     // mt
-              dmma(acc[1][a][b][0], acc[1][a][b][1], xss, mx[b]);    // ms
+            for (int b = 0; b < 2; ++b) dmma(acc[0][a][b][0], acc[0][a][b][1], xs, mx[b]);  // mt
+          }
+          if (!no_ms) {
+#pragma unroll
+            for (int a = 0; a < 2; ++a) {
+              const double xss = ssc * xa[a];
+#pragma unroll
+              for (int b = 0; b < 2; ++b) dmma(acc[1][a][b][0], acc[1][a][b][1], xss, mx[b]);  // ms
             }
           }
         }
@@ -3584,6 +3593,13 @@ static std::pair<cudaEvent_t, cudaEvent_t>* proj_timer() {
 bool project_timing_enabled() { return g_proj_timing; }
 }  // namespace dlrsn
 
+namespace dlrsn {
+int project_ex(const dlrsn_cellops* ops, int r, const double* X, const double* Xold,
+               const double* halo, int top_wall, const double* sigma_t, const double* sigma_s,
+               const double* q, double* out, double* partial, const int* any_scat,
+               cudaStream_t stream);
+}  // namespace dlrsn
+
 extern "C" {
 
 int dlrsn_project_timing(int enable) {
@@ -3613,6 +3629,17 @@ int dlrsn_project_slab(const dlrsn_cellops* ops, int r, const double* X, const d
                        const double* halo, int top_wall, const double* sigma_t,
                        const double* sigma_s, const double* q, double* out, double* partial,
                        dlrsn_stream_t stream) {
+  return dlrsn::project_ex(ops, r, X, Xold, halo, top_wall, sigma_t, sigma_s, q, out, partial,
+                           nullptr, as_stream(stream));
+}
+
+}  // extern "C"
+
+namespace dlrsn {
+int project_ex(const dlrsn_cellops* ops, int r, const double* X, const double* Xold,
+               const double* halo, int top_wall, const double* sigma_t, const double* sigma_s,
+               const double* q, double* out, double* partial, const int* any_scat,
+               cudaStream_t stream) {
   const int ncell = ops->nx * ops->ny;
   const int tiles = ((r + kTile - 1) / kTile) * ((r + kTile - 1) / kTile);
   const int cpb = cells_per_block(ncell, tiles);
@@ -3623,7 +3650,8 @@ int dlrsn_project_slab(const dlrsn_cellops* ops, int r, const double* X, const d
   pa.part = partial; pa.cells_per_block = cpb;
   pa.halo = halo;
   pa.top_wall = top_wall;
-  cudaStream_t st = as_stream(stream);
+  pa.any_scat = any_scat;
+  cudaStream_t st = stream;
   static const char* simt = getenv("DLRSN_PROJECT_SIMT");
   static const char* wide = getenv("DLRSN_PROJECT_WIDE");
   if (r > kTile && !(wide && wide[0] == '0') && !(simt && simt[0] == '1')) {
@@ -3707,6 +3735,9 @@ int dlrsn_project_slab(const dlrsn_cellops* ops, int r, const double* X, const d
   DLRSN_CHECK_LAUNCH("reduce_partials_kernel");
   return DLRSN_OK;
 }
+}  // namespace dlrsn
+
+extern "C" {
 
 int dlrsn_chol_upper(int r, const double* G, double* R, double* Rinv, double* diag_ratio,
                      int* flag, dlrsn_stream_t stream) {

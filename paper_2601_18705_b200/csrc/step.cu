@@ -1085,7 +1085,8 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
                                      cudaMemcpyDeviceToHost, oc->cs));
       DLRSN_TRY_CUDA(cudaEventRecord(oc->done, oc->cs));
     }
-    DLRSN_RET(dlrsn_project(ops, r, X_new, X, sigma_t, sigma_s, q, b.proj, b.part, s));
+    DLRSN_RET(project_ex(ops, r, X_new, X, nullptr, 1, sigma_t, sigma_s, q, b.proj, b.part,
+                         b.flags + 1, st));
     if (has_inflow) DLRSN_RET(dlrsn_inflow_project(ops, r, X_new, r, p->inflow, b.hin, s));
     {
       const size_t qsm = 3 * (size_t)r * r * sizeof(double);
@@ -1143,6 +1144,22 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
       DLRSN_CHECK_LAUNCH("ortho_residual_kernel");
     }
     if (oc) DLRSN_TRY_CUDA(cudaStreamWaitEvent(st, oc->done, 0));  // join the host copy
+    return enqueue_status(st, b, r, hs, sweep_ws);
+  };
+
+  // angular-only fallback: the exact CGS2 of W gamma (still in lfull) and
+  // what depends on it; X_new, the projections, phi and T stay as they are
+  auto enqueue_angular = [&](cudaStream_t st) -> int {
+    DLRSN_TRY_CUDA(zero_async(b.statw, sizeof(int), st));
+    DLRSN_RET(dlrsn_cgs2(no, r, b.lfull, r, W_new, r, b.Rang, b.defw, 0, p->weights_dev, nullptr,
+                         0, r + 8, b.up->aexp, p->omegas_dev, b.cgsws, b.statw, 1, st));
+    DLRSN_RET(wgram(no, r, W_new, p->weights_dev, b.wpart, b.wg, st));
+    finish_kernel<<<1, 256, 0, st>>>(r, b.Rang, b.wg, S_new, beta_new);
+    DLRSN_CHECK_LAUNCH("finish_kernel");
+    if (p->check_state) {
+      ortho_residual_kernel<<<1, 256, 0, st>>>(r, b.G, b.wg, b.chk_out, nullptr, p->x_check_out);
+      DLRSN_CHECK_LAUNCH("ortho_residual_kernel");
+    }
     return enqueue_status(st, b, r, hs, sweep_ws);
   };
 
@@ -1266,7 +1283,7 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
       if (!ok) {
         info->gs_fallback |= 2;
         exact_w = 1;
-        DLRSN_RET(enqueue_tail(st0, exact, exact_w, true));
+        DLRSN_RET(enqueue_angular(st0));
         DLRSN_TRY_CUDA(cudaStreamSynchronize(st0));
         continue;
       }

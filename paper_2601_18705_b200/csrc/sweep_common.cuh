@@ -133,6 +133,12 @@ int sweep_grouped_launch(const dlrsn_cellops* ops, int G, const dlrsn_group* gro
 int cgroup_plan_launch(int G, const dlrsn_group* groups, int wpc, int dmax, CgTable* tab,
                        int* cg_quad, double* cg_w, cudaStream_t st);
 int sweep_group_width();
+// dense.cu: dlrsn_project_slab with the device scattering flag (ms = 0 and
+// its MMAs skipped when *any_scat == 0)
+int project_ex(const dlrsn_cellops* ops, int r, const double* X, const double* Xold,
+               const double* halo, int top_wall, const double* sigma_t, const double* sigma_s,
+               const double* q, double* out, double* partial, const int* any_scat,
+               cudaStream_t stream);
 // dense.cu: Y = X K for an upper-triangular r x r K (skips the zero blocks)
 int rowmix_upper(int64_t n, int r, const double* X, int ldx, const double* K, int ldk, double* Y,
                  int ldy, cudaStream_t st);

@@ -80,10 +80,12 @@ class CollocationStepInfo:
         return self.selection.cond
 
 
-def project_operators(ops, x, x_old=None):
+def project_operators(ops, x, x_old=None, no_scatter=False):
     """Fused reduced operators: dict px, py, jx, jy, mt, ms, mo (r x r) and q
     (project_row_operators dlr_sn.py:61-71; mo = X_old^T M x for
-    project_initial :50-58).  Returns (dict, packed device buffer)."""
+    project_initial :50-58).  Returns (dict, packed device buffer).
+    no_scatter: the caller has checked sigma_s == 0, so ms = 0 and its MMAs
+    are skipped (sigma_s passed as NULL)."""
     co = _cellops_of(ops)
     x = as_device(x).contiguous()
     r = x.shape[1]
@@ -93,7 +95,8 @@ def project_operators(ops, x, x_old=None):
     xo = None if x_old is None else as_device(x_old).contiguous()
     st = ops.step
     _lib.call("dlrsn_project", _addr(co), r, _lib.ptr(x), _lib.ptr(xo), _lib.ptr(st.sigma_t),
-              _lib.ptr(st.sigma_s), _lib.ptr(st.q), _lib.ptr(out), _lib.ptr(part), stream())
+              None if no_scatter else _lib.ptr(st.sigma_s), _lib.ptr(st.q), _lib.ptr(out),
+              _lib.ptr(part), stream())
     mats = out[:7 * r * r].reshape(7, r, r)
     names = ("px", "py", "jx", "jy", "mt", "ms", "mo")
     proj = {k: mats[i] for i, k in enumerate(names)}

@@ -199,7 +199,7 @@ def step_lean(grid, step, quad, state, *, si_tol, si_max_iters, check_state, chu
     x_new = psi
     # ---- K3 + the reduced row system + the angular update (dlr_sn.py:126-141)
     ph.mark("k2")
-    proj, packed = project_operators(ops, x_new, x_old=X)
+    proj, packed = project_operators(ops, x_new, x_old=X, no_scatter=True)  # checked above
     ph.mark("k3")
     w_sel = W[sel.indices_dev]
     q_all = (proj["q"][None, :] + st.inv_cdt * (w_sel @ (S.T @ proj["mo"]))).contiguous()
