@@ -478,12 +478,12 @@ def main(argv=None):
     roofline = {
         "bound": "tensor", "achieved": k3_tf, "peak": peak_fp64, "unit": "TFLOP/s",
         "frac": k3_tf / peak_fp64, "traffic": traffic.get("k3"),
-        "kernel": "project_mma32_kernel (K3: 7 reduced operators, DMMA m8n8k4 f64)",
+        "kernel": "project_mma32g_kernel (K3: 7 reduced operators, DMMA m8n8k4 f64)",
         "peak_kind": "fp64 tensor, measured in this run (max of DMMA probe, cuBLAS DGEMM)",
         "peak_detail": fp64_detail, "launch_ms": k3_ms,
         "alg_flop_per_launch": k3_flop, "flop_formula": "7 x 2 N_x r^2",
         "share_of_step": k3_ms / step_ms,
-        "sweep": {"kernel": "sweep_kernel<1> (K1)", "bound": "hbm", "unit": "GB/s",
+        "sweep": {"kernel": "sweep1s_kernel<4,3,2> (K1, split-phase single-direction sweep)", "bound": "hbm", "unit": "GB/s",
                   "achieved": sweep_gbs, "peak": hbm_peak, "peak_kind": hbm_kind,
                   "frac": sweep_gbs / hbm_peak, "launch_ms": sweep_real_ms,
                   "alg_bytes_per_launch": sweep_bytes, "traffic": traffic.get("sweep"),
