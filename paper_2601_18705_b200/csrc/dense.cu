@@ -1548,7 +1548,7 @@ __global__ void __launch_bounds__(256, 1) project_mma32_kernel(ProjArgs pa, dlrs
 constexpr int kPCG = 8;                          // cells per chunk
 constexpr int kPlaneG = kPCG * kRow32;           // one staged plane
 constexpr size_t kProj32StageG0 = 6 * (size_t)kPlaneG;
-constexpr size_t kProj32StageG1 = 3 * (size_t)kPlaneG + kPCG * kT32 + 2 * kPCG;
+constexpr size_t kProj32StageG1 = 5 * (size_t)kPlaneG + kPCG * kT32;
 constexpr size_t kProj32RedG0 = (4 + 2) * 32 * 33;
 constexpr size_t kProj32RedG1 = 3 * 32 * 33;
 constexpr size_t kProj32SmemG =
@@ -1569,8 +1569,9 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
   double* sMX = sm32 + 2 * kPlaneG;  // group 1
   double* sGY = sm32 + 3 * kPlaneG;
   double* sF = sm32 + 4 * kPlaneG;   // [C][8][kLS]
-  double* sQ = sm32 + 3 * kPlaneG;   // group 1
-  double* sC = sQ + C * kT32;
+  double* sMXt = sm32 + 3 * kPlaneG;  // group 1: sigma_t M X (j-side)
+  double* sMXs = sm32 + 4 * kPlaneG;  // group 1: sigma_s M X (j-side)
+  double* sQ = sm32 + 5 * kPlaneG;    // group 1
   __shared__ double so[64];
   if (threadIdx.x < 16) {
     so[threadIdx.x] = ops.mass[threadIdx.x];
@@ -1641,9 +1642,9 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
       for (int l = 0; l < 4; ++l)
         w.y[l] = (live && pa.Xold) ? ldx(pa.Xold, r, (int64_t)c * 4 + l, gi) : 0.0;
       w.qc = live ? __ldg(pa.q + c) : 0.0;
-      const int cs = cc0 + (int)threadIdx.x;
-      w.st = (cc0 < c_end && threadIdx.x < C && cs < c_end) ? __ldg(pa.sigma_t + cs) : 0.0;
-      w.ss = (pa.sigma_s && cc0 < c_end && threadIdx.x < C && cs < c_end) ? __ldg(pa.sigma_s + cs) : 0.0;
+      // this staging item's own cell: the sigma-weighted mass planes
+      w.st = live ? __ldg(pa.sigma_t + c) : 0.0;
+      w.ss = (live && !no_ms) ? __ldg(pa.sigma_s + c) : 0.0;
     }
   };
   Raw cur;
@@ -1695,15 +1696,15 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
 #pragma unroll
           for (int p = 0; p < 4; ++p) m = fma(so[4 * l + p], x[p], m);
           sMX[base + kLS * l] = m;
+          // sigma folded into the B planes once per staged element (was a
+          // scaling of the A fragment per warp per MMA)
+          sMXt[base + kLS * l] = cur.st * m;
+          if (!no_ms) sMXs[base + kLS * l] = cur.ss * m;
         }
         double sq = 0.0;
 #pragma unroll
         for (int l = 0; l < 4; ++l) sq = fma(so[56 + l], x[l], sq);
         sQ[scl * kT32 + scol] = cur.qc * sq;  // q-hat (dlr_sn.py:70)
-        if (threadIdx.x < C) {
-          sC[2 * threadIdx.x] = cur.st;
-          sC[2 * threadIdx.x + 1] = cur.ss;
-        }
       }
     }
     __syncthreads();
@@ -1730,7 +1731,6 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
             dmma(acc[1][a][b][0], acc[1][a][b][1], xa[a], gy[b]);  // py (volume)
           }
       } else {
-        const double stc = sC[2 * cl], ssc = sC[2 * cl + 1];
         double xo[2], mx[2];
 #pragma unroll
         for (int a = 0; a < 2; ++a) {
@@ -1738,19 +1738,21 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
           mx[a] = sMX[cl * kRow + q * kLS + cb[a]];
         }
         if (!mo_only) {
+          double mxt[2];
 #pragma unroll
-          for (int a = 0; a < 2; ++a) {
-            const double xs = stc * xa[a];
+          for (int b = 0; b < 2; ++b) mxt[b] = sMXt[cl * kRow + q * kLS + cb[b]];
 #pragma unroll
-            for (int b = 0; b < 2; ++b) dmma(acc[0][a][b][0], acc[0][a][b][1], xs, mx[b]);  // mt
-          }
+          for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int b = 0; b < 2; ++b) dmma(acc[0][a][b][0], acc[0][a][b][1], xa[a], mxt[b]);  // mt
           if (!no_ms) {
+            double mxs[2];
 #pragma unroll
-            for (int a = 0; a < 2; ++a) {
-              const double xss = ssc * xa[a];
+            for (int b = 0; b < 2; ++b) mxs[b] = sMXs[cl * kRow + q * kLS + cb[b]];
 #pragma unroll
-              for (int b = 0; b < 2; ++b) dmma(acc[1][a][b][0], acc[1][a][b][1], xss, mx[b]);  // ms
-            }
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+              for (int b = 0; b < 2; ++b) dmma(acc[1][a][b][0], acc[1][a][b][1], xa[a], mxs[b]);  // ms
           }
         }
 #pragma unroll

@@ -89,7 +89,7 @@ class _Phases:
             print("dlrsn lean ms: " + ", ".join(parts), file=sys.stderr)
 
 
-def _chunk_width(n, r, vl, limit=16):
+def _chunk_width(n, r, vl, limit=24):
     """Directions per sweep chunk: as many as fit next to the chunk's two
     buffers (psi_time n x D, SK rhs / psi D x vl) in the free device memory,
     up to ``limit`` (each chunk re-reads X once; 32 at config 5 leaves too

@@ -118,11 +118,13 @@ def test_iteration_limit_error(golden):
 
 
 @pytest.mark.parametrize("nx,ny,ndir,dw", [(70, 70, 16, None), (3, 67, 9, 2), (45, 33, 24, 8),
-                                            (64, 100, 40, 4), (1, 1, 4, 1), (50, 330, 32, 1)])
+                                            (64, 100, 40, 4), (1, 1, 4, 1), (50, 330, 32, 1),
+                                            (40, 640, 32, 1), (33, 700, 30, 1)])
 def test_source_iteration_matches_oracle_random(nx, ny, ndir, dw):
-    """Multi-strip handoffs, partial strips, every group width, all quadrants;
-    (50, 330, 32, 1) has 352 single-direction work items, so it runs the
-    throughput kernel (sweep_kernel<1>) rather than the warp-specialised one."""
+    """Multi-strip handoffs, partial strips, every group width, all quadrants.
+    Single-direction groups above 4 x SM-count work items (strips x
+    directions: 640 and 660 here) run the split-phase throughput kernel
+    (sweep1s_kernel), below it the warp-specialised one (352 items)."""
     from oracle import port as P
     from paper_2601_18705_b200 import transport as Tr
     from paper_2601_18705_b200.mesh import build_grid
