@@ -421,8 +421,12 @@ def main(argv=None):
                                                            comm=comm)
         return info
 
-    # setup + warm-up (untimed): graph capture per buffer set, batch hint
-    for _ in range(3 + args.warmup):
+    # setup + warm-up (untimed): graph capture per buffer set, batch hint.
+    # The caching allocator hands the step's outputs back at a rotating set
+    # of addresses (about 8-14 distinct sets in a chained loop); every set is
+    # one CUDA graph, so the untimed settling runs past that period before
+    # the W warm-up steps proper
+    for _ in range(16 + args.warmup):
         one_step()
     torch.cuda.synchronize()
 

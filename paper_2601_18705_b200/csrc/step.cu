@@ -663,7 +663,7 @@ static int graph_run(const GraphKey& key, F&& enqueue, cudaStream_t st, bool cha
       break;
     }
   auto evict = [&]() {
-    if (cache.size() < 16) return;
+    if (cache.size() < 64) return;
     size_t lru = 0;
     for (size_t i = 1; i < cache.size(); ++i)
       if (cache[i].used < cache[lru].used) lru = i;
@@ -696,6 +696,15 @@ static int graph_run(const GraphKey& key, F&& enqueue, cudaStream_t st, bool cha
     seen = &cache.back();
   }
   if (!cs) DLRSN_TRY_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  {
+    static const bool dbg = getenv("DLRSN_GRAPH_DEBUG") != nullptr;
+    if (dbg) {
+      uint64_t h = 1469598103934665603ull;
+      for (size_t i = 0; i < sizeof(key.bytes); ++i) h = (h ^ key.bytes[i]) * 1099511628211ull;
+      fprintf(stderr, "dlrsn graph: capture #%zu key %016llx (chained %d)\n", cache.size(),
+              (unsigned long long)h, (int)chained);
+    }
+  }
   // capture on a private stream (the caller's may be the legacy default stream)
   DLRSN_TRY_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   const int64_t k0 = launch_counter().load();
