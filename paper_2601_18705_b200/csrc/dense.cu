@@ -1618,33 +1618,52 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
     double ui[4];  // group 0: neighbour edge dofs on the i-side (face jumps)
     double qc, st, ss;
   };
+  // the item's cell advances by C per chunk: its grid coordinates are kept
+  // incrementally (no division per chunk) and every load is a 32-bit offset
+  // from one row pointer (r doubles per dof row)
+  const bool ci_ok = gi < r, cj_ok = gj < r;
+  const int64_t rs = r;
+  int fc = c_begin + scl;           // the item's cell at the next fetch
+  int fci = fc % nx, fcj = fc / nx;  // its grid coordinates
   auto fetch = [&](int cc0, Raw& w) {
-    const int c = cc0 + scl;
+    const int c = fc;
+    const int ci = fci, cj = fcj;
     const bool live = cc0 < c_end && c < c_end;
+    const double* row = X + (int64_t)c * 4 * rs;  // dof row 4 c
+    const bool vi = live && ci_ok, vj = live && cj_ok;
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
-      w.xi[l] = live ? ldx(X, r, (int64_t)c * 4 + l, gi) : 0.0;
-      w.xj[l] = live ? ldx(X, r, (int64_t)c * 4 + l, gj) : 0.0;
+      w.xi[l] = vi ? __ldg(row + l * rs + gi) : 0.0;
+      w.xj[l] = vj ? __ldg(row + l * rs + gj) : 0.0;
     }
     if constexpr (GROUP == 0) {
-      const int ci = c % nx, cj = c / nx;
       const bool lx = live && ci > 0, ly = live && (cj > 0 || pa.halo != nullptr);
-      w.y[0] = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 1, gj) : 0.0;
-      w.y[1] = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 3, gj) : 0.0;
-      w.y[2] = ly ? ld_below(pa, X, c, ci, cj, 2, gj) : 0.0;
-      w.y[3] = ly ? ld_below(pa, X, c, ci, cj, 3, gj) : 0.0;
-      w.ui[0] = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 1, gi) : 0.0;
-      w.ui[1] = lx ? ldx(X, r, (int64_t)(c - 1) * 4 + 3, gi) : 0.0;
-      w.ui[2] = ly ? ld_below(pa, X, c, ci, cj, 2, gi) : 0.0;
-      w.ui[3] = ly ? ld_below(pa, X, c, ci, cj, 3, gi) : 0.0;
+      const double* left = row - 4 * rs;  // the cell to the left (c - 1)
+      const double* below = cj > 0 ? row - (int64_t)4 * nx * rs
+                                   : (pa.halo ? pa.halo + (int64_t)ci * 4 * rs : nullptr);
+      w.y[0] = (lx && cj_ok) ? __ldg(left + 1 * rs + gj) : 0.0;
+      w.y[1] = (lx && cj_ok) ? __ldg(left + 3 * rs + gj) : 0.0;
+      w.y[2] = (ly && cj_ok) ? __ldg(below + 2 * rs + gj) : 0.0;
+      w.y[3] = (ly && cj_ok) ? __ldg(below + 3 * rs + gj) : 0.0;
+      w.ui[0] = (lx && ci_ok) ? __ldg(left + 1 * rs + gi) : 0.0;
+      w.ui[1] = (lx && ci_ok) ? __ldg(left + 3 * rs + gi) : 0.0;
+      w.ui[2] = (ly && ci_ok) ? __ldg(below + 2 * rs + gi) : 0.0;
+      w.ui[3] = (ly && ci_ok) ? __ldg(below + 3 * rs + gi) : 0.0;
     } else {
+      const double* orow = pa.Xold ? pa.Xold + (int64_t)c * 4 * rs : nullptr;
 #pragma unroll
-      for (int l = 0; l < 4; ++l)
-        w.y[l] = (live && pa.Xold) ? ldx(pa.Xold, r, (int64_t)c * 4 + l, gi) : 0.0;
+      for (int l = 0; l < 4; ++l) w.y[l] = (vi && orow) ? __ldg(orow + l * rs + gi) : 0.0;
       w.qc = live ? __ldg(pa.q + c) : 0.0;
       // this staging item's own cell: the sigma-weighted mass planes
       w.st = live ? __ldg(pa.sigma_t + c) : 0.0;
       w.ss = (live && !no_ms) ? __ldg(pa.sigma_s + c) : 0.0;
+    }
+    // advance to the next chunk's cell
+    fc += C;
+    fci += C;
+    while (fci >= nx) {
+      fci -= nx;
+      ++fcj;
     }
   };
   Raw cur;
