@@ -1578,8 +1578,9 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
     so[16 + threadIdx.x] = ops.gx[threadIdx.x];
     so[32 + threadIdx.x] = ops.gy[threadIdx.x];
   } else if (threadIdx.x < 20) {
-    so[48 + threadIdx.x - 16] = ops.e2x[threadIdx.x - 16];
-    so[52 + threadIdx.x - 16] = ops.e2y[threadIdx.x - 16];
+    // halved edge masses: every face term carries the 1/2 of the average
+    so[48 + threadIdx.x - 16] = 0.5 * ops.e2x[threadIdx.x - 16];
+    so[52 + threadIdx.x - 16] = 0.5 * ops.e2y[threadIdx.x - 16];
     so[56 + threadIdx.x - 16] = ops.src_row[threadIdx.x - 16];
   }
   const double* e2x = so + 48;
@@ -1698,14 +1699,14 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
           sGY[base + kLS * l] = gy;
         }
         double* f = sF + 2 * scl * kRow + scol;
-        f[0] = 0.5 * (e2x[0] * vx0 + e2x[1] * vx1);
-        f[kLS] = 0.5 * (e2x[2] * vx0 + e2x[3] * vx1);
-        f[2 * kLS] = 0.5 * (e2y[0] * vy0 + e2y[1] * vy1);
-        f[3 * kLS] = 0.5 * (e2y[2] * vy0 + e2y[3] * vy1);
-        f[4 * kLS] = 0.5 * (e2x[0] * ux0 + e2x[1] * ux1);
-        f[5 * kLS] = 0.5 * (e2x[2] * ux0 + e2x[3] * ux1);
-        f[6 * kLS] = 0.5 * (e2y[0] * uy0 + e2y[1] * uy1);
-        f[7 * kLS] = 0.5 * (e2y[2] * uy0 + e2y[3] * uy1);
+        f[0] = (e2x[0] * vx0 + e2x[1] * vx1);
+        f[kLS] = (e2x[2] * vx0 + e2x[3] * vx1);
+        f[2 * kLS] = (e2y[0] * vy0 + e2y[1] * vy1);
+        f[3 * kLS] = (e2y[2] * vy0 + e2y[3] * vy1);
+        f[4 * kLS] = (e2x[0] * ux0 + e2x[1] * ux1);
+        f[5 * kLS] = (e2x[2] * ux0 + e2x[3] * ux1);
+        f[6 * kLS] = (e2y[0] * uy0 + e2y[1] * uy1);
+        f[7 * kLS] = (e2y[2] * uy0 + e2y[3] * uy1);
       } else {
         const double* x = cur.xj;
 #pragma unroll
@@ -1827,13 +1828,13 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
           const int64_t r1 = (int64_t)c * 4 + 1, r3 = (int64_t)c * 4 + 3;
           const double ai0 = ldx(X, r, r1, i), ai1 = ldx(X, r, r3, i);
           const double aj0 = ldx(X, r, r1, j), aj1 = ldx(X, r, r3, j);
-          bx += ai0 * (0.5 * (e2x[0] * aj0 + e2x[1] * aj1)) + ai1 * (0.5 * (e2x[2] * aj0 + e2x[3] * aj1));
+          bx += ai0 * ((e2x[0] * aj0 + e2x[1] * aj1)) + ai1 * ((e2x[2] * aj0 + e2x[3] * aj1));
         }
         for (int c = max(c_begin, (ny - 1) * nx); pa.top_wall && c < c_end; ++c) {
           const int64_t r2 = (int64_t)c * 4 + 2, r3 = (int64_t)c * 4 + 3;
           const double ai0 = ldx(X, r, r2, i), ai1 = ldx(X, r, r3, i);
           const double aj0 = ldx(X, r, r2, j), aj1 = ldx(X, r, r3, j);
-          by += ai0 * (0.5 * (e2y[0] * aj0 + e2y[1] * aj1)) + ai1 * (0.5 * (e2y[2] * aj0 + e2y[3] * aj1));
+          by += ai0 * ((e2y[0] * aj0 + e2y[1] * aj1)) + ai1 * ((e2y[2] * aj0 + e2y[3] * aj1));
         }
       }
       bnd[ti * 33 + tj] = bx;
