@@ -251,6 +251,13 @@ int dlrsn_sweep(const dlrsn_cellops* ops, int G, const dlrsn_group* groups, int 
 int dlrsn_rowmix(int64_t n, int kx, int ky, const double* X, int ldx, const double* K, int ldk,
                  double beta, double* Y, int ldy, dlrsn_stream_t stream);
 
+/* Y = X K for an upper-triangular r x r K (exact zeros below the diagonal:
+ * the CholQR2 factors R^-1, angular.py:104-160 restated as CholQR2), r <=
+ * 128: the zero blocks are skipped (72/128 of the MMAs at r = 64).  Y may
+ * alias X (in place, X's row stride = Y's). */
+int dlrsn_rowmix_upper(int64_t n, int r, const double* X, int ldx, const double* K, int ldk,
+                       double* Y, int ldy, dlrsn_stream_t stream);
+
 /* doubles of `partial` scratch needed by dlrsn_mgram (kind 0: ra x rb) or
  * dlrsn_project (kind 1: rank ra) */
 int64_t dlrsn_partials_len(int ncell, int ra, int rb, int kind);

@@ -115,6 +115,7 @@ _SIGNATURES = {
                                     c_int, c_vp]),
     "dlrsn_rowmix": (c_int, [c_i64, c_int, c_int, c_vp, c_int, c_vp, c_int, c_dbl, c_vp, c_int,
                              c_vp]),
+    "dlrsn_rowmix_upper": (c_int, [c_i64, c_int, c_vp, c_int, c_vp, c_int, c_vp, c_int, c_vp]),
     "dlrsn_partials_len": (c_i64, [c_int, c_int, c_int, c_int]),
     "dlrsn_mgram": (c_int, [c_vp, c_int, c_int, c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_vp]),
     "dlrsn_project": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),

@@ -270,18 +270,22 @@ __global__ void __launch_bounds__(256, (4 * KS + 8 * NT <= 96) ? 2 : 1) rowmix_w
 
 // rowmix by an upper-triangular K (r x r, exact zeros below the diagonal:
 // the CholQR2 factors R^-1): Y = X K with the MMA k index in natural order
-// (lane quad q owns columns 4 ks + q), so k step ks meets column group nt
-// only when 4 ks <= 8 nt + 7 -- 72 of 128 DMMA fragments at r = 64.
+// (lane quad q owns columns 4 ks + q), so k step ks meets column group
+// (c0 + 8 nt ..) only when 4 ks <= c0 + 8 nt + 7 -- 72 of 128 DMMA
+// fragments at r = 64, 272 of 512 at r = 128 (two 64-column passes).  Every
+// row of a warp's tile is loaded (all r columns) before any output of the
+// tile is written, so Y may alias X (in place).
 template <int KS, int NT>
 __global__ void __launch_bounds__(256, 1) rowmix_upper_kernel(int n, int r,
-                                                           const double* __restrict__ X, int ldx,
+                                                           const double* X, int ldx,
                                                            const double* __restrict__ K, int ldk,
-                                                           double* __restrict__ Y, int ldy,
-                                                           int ldks) {
-  static_assert(4 * KS == 8 * NT, "square K tile");
-  extern __shared__ double sK[];  // (4 KS) x ldks
-  for (int e = threadIdx.x; e < 4 * KS * 8 * NT; e += blockDim.x) {
-    const int k = e / (8 * NT), col = e - k * (8 * NT);
+                                                           double* Y, int ldy, int ldks) {
+  constexpr int KC = 4 * KS;    // K rows (padded r)
+  constexpr int CW = 8 * NT;    // columns per pass
+  constexpr int NP = KC / CW;   // passes (1 at r <= 64, 2 at r <= 128)
+  extern __shared__ double sK[];  // KC x ldks
+  for (int e = threadIdx.x; e < KC * KC; e += blockDim.x) {
+    const int k = e / KC, col = e - k * KC;
     sK[k * ldks + col] = (k < r && col < r) ? __ldg(K + (int64_t)k * ldk + col) : 0.0;
   }
   __syncthreads();
@@ -298,38 +302,43 @@ __global__ void __launch_bounds__(256, 1) rowmix_upper_kernel(int n, int r,
       const double* xr = X + row * ldx + q;
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks)
-        af[u][ks] = (row < n && 4 * ks + q < r) ? __ldg(xr + 4 * ks) : 0.0;
+        af[u][ks] = (row < n && 4 * ks + q < r) ? xr[4 * ks] : 0.0;
     }
-    double d[2][NT][2];
+    __syncwarp();  // every lane's reads of the tile precede the in-place writes
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+    for (int p = 0; p < NP; ++p) {
+      const int c0 = p * CW;
+      double d[2][NT][2];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) d[u][nt][0] = d[u][nt][1] = 0.0;
+      for (int u = 0; u < 2; ++u)
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const double* kr = sK + (4 * ks + q) * ldks + g;
+        for (int nt = 0; nt < NT; ++nt) d[u][nt][0] = d[u][nt][1] = 0.0;
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        if (ks > 2 * nt + 1) continue;  // K rows 4 ks.. lie below columns 8 nt..8 nt + 7
-        const double b = kr[8 * nt];
-        dmma(d[0][nt][0], d[0][nt][1], af[0][ks], b);
-        dmma(d[1][nt][0], d[1][nt][1], af[1][ks], b);
+      for (int ks = 0; ks < KS; ++ks) {
+        const double* kr = sK + (4 * ks + q) * ldks + c0 + g;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          if (4 * ks > c0 + 8 * nt + 7) continue;  // K rows 4 ks.. lie below these columns
+          const double b = kr[8 * nt];
+          dmma(d[0][nt][0], d[0][nt][1], af[0][ks], b);
+          dmma(d[1][nt][0], d[1][nt][1], af[1][ks], b);
+        }
       }
-    }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int64_t row = (t0 + u) * 8 + g;
-      if (row >= n) continue;
-      double* y = Y + row * ldy;
+      for (int u = 0; u < 2; ++u) {
+        const int64_t row = (t0 + u) * 8 + g;
+        if (row >= n) continue;
+        double* y = Y + row * ldy;
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int c = 8 * nt + 2 * q;
-        if (vstore && c + 1 < r) {
-          *reinterpret_cast<double2*>(y + c) = make_double2(d[u][nt][0], d[u][nt][1]);
-        } else {
+        for (int nt = 0; nt < NT; ++nt) {
+          const int c = c0 + 8 * nt + 2 * q;
+          if (vstore && c + 1 < r) {
+            *reinterpret_cast<double2*>(y + c) = make_double2(d[u][nt][0], d[u][nt][1]);
+          } else {
 #pragma unroll
-          for (int i = 0; i < 2; ++i)
-            if (c + i < r) y[c + i] = d[u][nt][i];
+            for (int i = 0; i < 2; ++i)
+              if (c + i < r) y[c + i] = d[u][nt][i];
+          }
         }
       }
     }
@@ -338,7 +347,7 @@ __global__ void __launch_bounds__(256, 1) rowmix_upper_kernel(int n, int r,
 
 int rowmix_upper(int64_t n, int r, const double* X, int ldx, const double* K, int ldk, double* Y,
                  int ldy, cudaStream_t st) {
-  if (r <= 16 || r > 64 || n < 64)
+  if (r <= 16 || r > 128 || n < 64)
     return dlrsn_rowmix(n, r, r, X, ldx, K, ldk, 0.0, Y, ldy, st);
   const int64_t tiles = (n + 7) / 8;
   int64_t blocks = (tiles + 15) / 16;
@@ -348,9 +357,16 @@ int rowmix_upper(int64_t n, int r, const double* X, int ldx, const double* K, in
     const int ldks = 32 + 4;
     const size_t smem = (size_t)4 * KS * ldks * sizeof(double);
     rowmix_upper_kernel<KS, NT><<<(int)blocks, 256, smem, st>>>((int)n, r, X, ldx, K, ldk, Y, ldy, ldks);
-  } else {
+  } else if (r <= 64) {
     constexpr int KS = 16, NT = 8;
     const int ldks = 64 + 4;
+    const size_t smem = (size_t)4 * KS * ldks * sizeof(double);
+    DLRSN_TRY_CUDA(cudaFuncSetAttribute(rowmix_upper_kernel<KS, NT>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    rowmix_upper_kernel<KS, NT><<<(int)blocks, 256, smem, st>>>((int)n, r, X, ldx, K, ldk, Y, ldy, ldks);
+  } else {
+    constexpr int KS = 32, NT = 8;
+    const int ldks = 128 + 4;
     const size_t smem = (size_t)4 * KS * ldks * sizeof(double);
     DLRSN_TRY_CUDA(cudaFuncSetAttribute(rowmix_upper_kernel<KS, NT>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -3337,6 +3353,12 @@ static int grid_for(int64_t n, int block = kRB) {
 }
 
 extern "C" {
+
+int dlrsn_rowmix_upper(int64_t n, int r, const double* X, int ldx, const double* K, int ldk,
+                       double* Y, int ldy, dlrsn_stream_t stream) {
+  DLRSN_REQUIRE(n >= 0 && r >= 1 && r <= DLRSN_MAX_RANK && X && K && Y, "bad dlrsn_rowmix_upper arguments");
+  return dlrsn::rowmix_upper(n, r, X, ldx, K, ldk, Y, ldy, as_stream(stream));
+}
 
 int dlrsn_rowmix(int64_t n, int kx, int ky, const double* X, int ldx, const double* K, int ldk,
                  double beta, double* Y, int ldy, dlrsn_stream_t stream) {

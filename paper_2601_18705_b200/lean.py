@@ -52,6 +52,7 @@ from .lowrank import (
     mass_gram,
     raise_row_status,
     rowmix,
+    rowmix_upper,
 )
 from .transport import _SweepPlan, _sweep, assemble_operators, raise_sweep_status, sweep_status_word
 
@@ -179,11 +180,12 @@ def step_lean(grid, step, quad, state, *, si_tol, si_max_iters, check_state, chu
     ph.mark("gram1")
     sdef = 0
     if cholqr_guard_ok(guard, r):
-        rowmix_inplace(psi, R1inv, block_rows)
+        # R^-1 is upper triangular: the in-place product skips its zero blocks
+        rowmix_upper(psi, R1inv, out=psi) if r <= 128 else rowmix_inplace(psi, R1inv, block_rows)
         ph.mark("rowmix1")
         R2, R2inv, _, flag2 = _chol(mass_gram(ops, psi))
         ph.mark("gram2")
-        rowmix_inplace(psi, R2inv, block_rows)
+        rowmix_upper(psi, R2inv, out=psi) if r <= 128 else rowmix_inplace(psi, R2inv, block_rows)
         ph.mark("rowmix2")
         if int(flag2.item()):
             raise SolverError("lean step: second CholQR pass lost positive definiteness")

@@ -74,6 +74,19 @@ def rowmix(X, K, out=None, beta=0.0):
     return out
 
 
+def rowmix_upper(X, K, out=None):
+    """out = X K for an upper-triangular square K (the CholQR2 factor R^-1:
+    its zero blocks are skipped); out may be X itself (in place)."""
+    X = as_device(X)
+    K = as_device(K).contiguous()
+    n, r = X.shape
+    if out is None:
+        out = empty(n, r)
+    _lib.call("dlrsn_rowmix_upper", n, r, _lib.ptr(X), X.stride(0), _lib.ptr(K), K.stride(0),
+              _lib.ptr(out), out.stride(0), stream())
+    return out
+
+
 def mass_inner(ops):
     """Inner product <u, v> = u^T M v on the device (lowrank.py:23-25)."""
     return lambda u, v: float(mass_gram(ops, as_device(u).reshape(-1, 1),

@@ -70,3 +70,21 @@ def test_mass_gram_matches_numpy(nx, ny, ra, rb, same, with_coeff):
     w = np.ones(g.n_cells) if coeff is None else coeff
     ref = np.einsum("c,cai,ab,cbj->ij", w, Ac, M, Bc)
     assert _rel(G, ref) <= 1e-13
+
+
+@pytest.mark.parametrize("n,r,inplace", [(1000, 17, False), (4099, 32, True), (5003, 33, False),
+                                        (100000, 64, True), (3001, 100, False), (2048, 128, True),
+                                        (777, 128, False), (70, 48, True)])
+def test_rowmix_upper_matches_numpy(n, r, inplace):
+    """The triangular product of the CholQR2 step (the zero blocks of R^-1
+    skipped), in place as the lean engine runs it and out of place."""
+    from paper_2601_18705_b200.lowrank import rowmix_upper
+
+    rng = np.random.default_rng(n + r)
+    X = rng.standard_normal((n, r))
+    K = np.triu(rng.standard_normal((r, r)))
+    Xd = torch.as_tensor(X, device="cuda").clone()
+    out = rowmix_upper(Xd, K, out=Xd if inplace else None)
+    if inplace:
+        assert out.data_ptr() == Xd.data_ptr()
+    assert _rel(out.cpu().numpy(), X @ K) <= 1e-14
