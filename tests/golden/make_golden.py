@@ -307,6 +307,45 @@ def run_checker(tag, per, r, nq, nsteps, seed, compact=False):
     save(tag, nsteps=nsteps, per=per, rank=r, nq=nq, seed=seed, **out)
 
 
+def run_c1_twenty():
+    """BASELINE config 1 in full: all 20 steps of the real reference's dlr-sn
+    loop (driver.py:485-539 restated as in run_checker), kept small: per step
+    the picks, SI count, T, S, W and random sketches of phi and X S W^T."""
+    tag, per, r, nq, nsteps, seed = "dlr_c1_20", 10, 8, 16, 20, 1
+    spec = problems.checkerboard(per, rank=r, n_polar=nq, n_azimuthal=nq, seed=seed)
+    rng = np.random.default_rng(spec.seed)
+    Xr, Wr = problems.draw_factors(spec, rng)
+    g = mesh.build_grid(spec.nx, spec.ny, spec.extent)
+    quad = angular.build_quadrature(nq, nq)
+    mass = driver.assemble_mass(g)
+    comp = lowrank.spatial_monomials(mesh.dof_coordinates(g), g.extent, r + 8)
+    X, _, _ = angular.gram_schmidt(Xr, lowrank.mass_inner(mass), comp)
+    Wb, _, _ = angular.orthonormalize(Wr, quad)
+    k = physics.PhysicsConstants(c=spec.c, a_r=spec.a_r)
+    b0, _ = physics.planck(driver.cells_to_dofs(g, spec.T0), k)
+    S = np.outer(X.T @ (mass @ b0), Wb.beta)
+    state = lowrank.DlrState(X=X, S=S, W=Wb)
+    proj = np.random.default_rng(23).standard_normal((12, g.n_dofs))
+    out = {}
+    T = spec.T0.copy()
+    for s in range(nsteps):
+        lin = physics.linearize(T, spec.sigma_a, spec.rho_cv, spec.dt, k)
+        lin.sigma_t = lin.sigma_t + spec.sigma_s_phys
+        lin.sigma_s = lin.sigma_s + spec.sigma_s_phys
+        lin.q = lin.q + spec.q_ext
+        state, info = dlr_sn.step_collocation(g, lin, quad, state, si_tol=1e-12, si_max_iters=400,
+                                              use_dsa=False)
+        raw = physics.update_temperature(driver.dofs_to_cells(g, info.phi), lin, -np.inf)
+        T = np.maximum(raw, 1e-6)
+        out.update({f"s{s}_idx": info.angle_indices, f"s{s}_iters": info.iterations,
+                    f"s{s}_phisk": proj @ info.phi, f"s{s}_T": T, f"s{s}_S": state.S,
+                    f"s{s}_W": state.W.values,
+                    f"s{s}_sketch": sketch(state.X, state.S, state.W.values),
+                    f"s{s}_sdef": info.spatial_deficiency, f"s{s}_adef": info.angular_deficiency})
+        print(tag, "step", s, info.iterations, info.angle_indices, flush=True)
+    save(tag, nsteps=nsteps, per=per, rank=r, nq=nq, seed=seed, proj_seed=23, **out)
+
+
 def ref_step_inflow(g, og, step, quad, state, inflow, si_tol):
     """step_collocation (dlr_sn.py:99-151) composed from the reference's own
     functions, plus the two inflow terms of the restatement (the reference
@@ -437,6 +476,10 @@ if __name__ == "__main__":
     import importlib
 
     sys.modules["helpers_ref"] = importlib.import_module("helpers")
+    if len(sys.argv) > 1 and sys.argv[1] == "dlr_c1_20":
+        # BASELINE config 1 itself, all 20 steps of the real reference
+        run_c1_twenty()
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "dlr_c2":
         # BASELINE config 2 itself, one step of the real reference (~1 min)
         run_checker("dlr_c2", per=40, r=16, nq=32, nsteps=1, seed=2, compact=True)

@@ -227,6 +227,35 @@ def test_dlr_steps_match_reference_golden(golden, name, gs_method):
         assert _lowrank_diff(X, S, W, g["final_X"], g["final_S"], g["final_W"]) <= 1e-11
 
 
+@pytest.mark.parametrize("gs_method", ["cholqr2", "cgs2"])
+def test_config1_twenty_steps_match_reference_golden(golden, gs_method):
+    """BASELINE config 1, ALL 20 steps, against the REAL reference's run
+    (tests/golden/dlr_c1_20.npz, make_golden.py dlr_c1_20): identical DEIM
+    picks, SI counts and deficiency counts every step; rel-L2 <= 1e-11 on
+    T, a 12-row random projection of info.phi, S, W and the sketch of
+    X S W^T at si_tol = 1e-12."""
+    g = golden("dlr_c1_20")
+    recs = _gpu_checker_run(g, gs_method)
+    assert len(recs) == int(g["nsteps"]) == 20
+    proj = None
+    for k, (s, info, T) in enumerate(recs):
+        assert list(info.angle_indices) == list(g[f"s{k}_idx"]), k
+        assert info.iterations == int(g[f"s{k}_iters"]), k
+        assert info.spatial_deficiency == int(g[f"s{k}_sdef"]), k
+        assert info.angular_deficiency == int(g[f"s{k}_adef"]), k
+        assert rel_l2(T, g[f"s{k}_T"]) <= 1e-11, k
+        phi = _np(info.phi)
+        if proj is None:
+            proj = np.random.default_rng(int(g["proj_seed"])).standard_normal((12, phi.shape[0]))
+        assert rel_l2(proj @ phi, g[f"s{k}_phisk"]) <= 1e-11, k
+        X, S, W = s.to_numpy()
+        assert rel_l2(W, g[f"s{k}_W"]) <= 1e-11 and rel_l2(S, g[f"s{k}_S"]) <= 1e-11, k
+        rng = np.random.default_rng(9)
+        phi_t = rng.standard_normal((X.shape[0], 12))
+        om_t = rng.standard_normal((W.shape[0], 12))
+        assert rel_l2((phi_t.T @ X) @ S @ (W.T @ om_t), g[f"s{k}_sketch"]) <= 1e-11, k
+
+
 @pytest.mark.slow
 def test_config1_twenty_steps_match_oracle():
     """BASELINE config 1 (70x70 checkerboard, r=8, 16x16, dt=0.01), all 20

@@ -250,6 +250,30 @@ def test_dlr_steps_match_reference(golden, name):
         assert P.lowrank_rel_diff(s.X, s.S, s.W, g["final_X"], g["final_S"], g["final_W"]) <= 1e-11
 
 
+def test_config1_twenty_steps_match_reference(golden):
+    """The oracle pinned on the real reference over BASELINE config 1 in full
+    (all 20 steps, dlr_c1_20.npz): picks, SI and deficiency counts every
+    step, 1e-11 on T, the phi projection, S, W and the X S W^T sketch."""
+    g = golden("dlr_c1_20")
+    spec, st0 = _run_checker(g)
+    recs = []
+    R.run(spec, st0, int(g["nsteps"]), record=lambda s, i, t: recs.append((s, i, t)))
+    assert len(recs) == 20
+    proj = np.random.default_rng(int(g["proj_seed"])).standard_normal((12, st0.X.shape[0]))
+    for k, (s, info, T) in enumerate(recs):
+        assert list(info.angle_indices) == list(g[f"s{k}_idx"]), k
+        assert info.iterations == int(g[f"s{k}_iters"]), k
+        assert info.spatial_deficiency == int(g[f"s{k}_sdef"]), k
+        assert info.angular_deficiency == int(g[f"s{k}_adef"]), k
+        assert rel_l2(T, g[f"s{k}_T"]) <= 1e-11, k
+        assert rel_l2(proj @ info.phi, g[f"s{k}_phisk"]) <= 1e-11, k
+        assert rel_l2(s.W, g[f"s{k}_W"]) <= 1e-11 and rel_l2(s.S, g[f"s{k}_S"]) <= 1e-11, k
+        rng = np.random.default_rng(9)
+        phi_t = rng.standard_normal((s.X.shape[0], 12))
+        om_t = rng.standard_normal((s.W.shape[0], 12))
+        assert rel_l2((phi_t.T @ s.X) @ s.S @ (s.W.T @ om_t), g[f"s{k}_sketch"]) <= 1e-11, k
+
+
 # ---- isotropic inflow boundary (config 3; a restatement, see port.inflow_load)
 
 
