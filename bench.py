@@ -87,9 +87,14 @@ def _cores():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region,
-    every 100 ms: at 20 ms the NVML queries occasionally stalled a timed
-    step by 10-120 ms (one outlier step in about half of the runs)."""
+    """SM clocks + throttle reasons sampled during the timed region.
+
+    In-process NVML reads at step boundaries (``tick()`` right after a
+    step's host synchronisation, outside its CUDA events): a polling
+    `nvidia-smi -lms 20` beside the run stalled single timed steps by up to
+    270 ms (scripts/outlier_probe.py: NVML queries contending with the
+    step's launches), at -lms 100 still by up to ~20 ms.  Falls back to
+    polling nvidia-smi every 100 ms without pynvml."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -99,8 +104,21 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.nvml = None
+        self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
 
     def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM))
+            self.tick()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -118,6 +136,18 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def tick(self):
+        """One NVML sample (call between timed steps; no-op for nvidia-smi)."""
+        if self.nvml is None:
+            return
+        nv = self.nvml
+        try:
+            sm = float(nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM))
+            reasons = int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle))
+            self.samples.append((sm, self.max_mhz, reasons))
+        except Exception:
+            pass
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
@@ -131,8 +161,21 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        sm, mx, reasons = [], 0.0, set()
+        if self.nvml is not None:
+            nv = self.nvml
+            bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+            for f, m, r in self.samples:
+                sm.append(f)
+                mx = max(mx, m)
+                for nm, b in zip(names, bits):
+                    if r & b:
+                        reasons.add(nm)
+            return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                    "reasons": sorted(reasons), "samples": len(sm),
+                    "how": "NVML at every timed step boundary"}
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 8:
@@ -146,7 +189,7 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "how": "nvidia-smi -lms 100"}
 
 
 def _dist():
@@ -445,8 +488,9 @@ def main(argv=None):
         for k in range(args.steps):
             flush.fill_(float(k))  # evict L2 between timed steps (outside the events)
             starts[k].record()
-            info = one_step()
+            info = one_step()  # ends with the step's host synchronisation
             ends[k].record()
+            clk.tick()
             iters.append(info.iterations)
         torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
@@ -601,6 +645,7 @@ def run_slab_bench(args, ws, rank, local):
             starts[k].record()
             iters.append(one_step()["iterations"])
             ends[k].record()
+            clk.tick()
         torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
     per = [a.elapsed_time(b) for a, b in zip(starts, ends)]

@@ -3391,7 +3391,12 @@ int dlrsn_rowmix(int64_t n, int kx, int ky, const double* X, int ldx, const doub
   const bool aligned = ((reinterpret_cast<uintptr_t>(X) | (uintptr_t)ldx * 8) & 15) == 0;
   if ((kx > 32 || ky > 16) && kx <= 128 && n >= 64) {
     const int ks = kx <= 16 ? 4 : (kx <= 32 ? 8 : (kx <= 64 ? 16 : 32));
-    const int nt = ky > 32 ? 8 : (ky > 16 ? 4 : (ky > 8 ? 2 : 1));
+    int nt = ky > 32 ? 8 : (ky > 16 ? 4 : (ky > 8 ? 2 : 1));
+    {  // A/B: DLRSN_ROWMIX_NT caps the column group (more CTAs per SM)
+      static const char* e = getenv("DLRSN_ROWMIX_NT");
+      const int cap = e ? atoi(e) : 0;
+      if (cap > 0 && nt > cap) nt = cap;
+    }
     const int kyp = (ky + 8 * nt - 1) / (8 * nt) * (8 * nt);
     const int ldks = kyp + ((4 - kyp % 16) + 16) % 16;
     const size_t smem = (size_t)4 * ks * ldks * sizeof(double);

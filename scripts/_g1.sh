@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT
 O=gpurun_out
-for rep in 1 2; do for f in 0 1; do DLRSN_STEP_FORK=$f timeout 900 python bench.py --steps 20 --warmup 5 --more-configs "C2,C3" --no-cpu-baseline --e2e-steps 1 2>/dev/null | tail -1 | python -c "
-import json,sys; d=json.loads(sys.stdin.read()); print('fork $f', round(d['ms_per_step'],3), max(d['ms_per_step_each']), [round(m['ms_per_step'],3) for m in d['more_configs']], d['clocks']['samples'])"; done; done > $O/fork2.log 2>&1
+for rep in 1 2 3 4; do DLRSN_GRAPH_DEBUG=1 timeout 600 python bench.py --steps 20 --warmup 5 --more-configs "" --no-cpu-baseline --e2e-steps 1 2> $O/clk_err_$rep.log | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step_each'], d['si_iterations'])"; grep -c capture $O/clk_err_$rep.log; done > $O/clk2.log 2>&1

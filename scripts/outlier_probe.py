@@ -10,7 +10,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
-def main(n=40):
+def main(n=40, lms=0):
     import bench
     from paper_2601_18705_b200.driver import DeviceProblem, initial_state
 
@@ -20,6 +20,13 @@ def main(n=40):
     T = torch.as_tensor(spec.T0, device="cuda").clone()
     lin = dp.linearized(T)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
+    proc = None
+    if lms:  # nvidia-smi polling as bench.ClockSampler does it
+        import subprocess
+        proc = subprocess.Popen(["nvidia-smi", "-i", "0", f"--query-gpu={bench.ClockSampler.Q}",
+                                 "--format=csv,noheader,nounits", "-lms", str(lms)],
+                                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        time.sleep(2.0)
     for k in range(n):
         flush.fill_(float(k))
         m0 = torch.cuda.memory_stats()
@@ -37,5 +44,9 @@ def main(n=40):
               f"retries +{m1['num_alloc_retries'] - m0['num_alloc_retries']}", flush=True)
 
 
+    if proc is not None:
+        proc.terminate()
+
+
 if __name__ == "__main__":
-    main(int(sys.argv[1]) if len(sys.argv) > 1 else 40)
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 40, int(sys.argv[2]) if len(sys.argv) > 2 else 0)
