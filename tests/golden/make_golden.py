@@ -346,6 +346,51 @@ def run_c1_twenty():
     save(tag, nsteps=nsteps, per=per, rank=r, nq=nq, seed=seed, proj_seed=23, **out)
 
 
+def run_c2_fifty():
+    """BASELINE config 2 in full: all 50 steps of the real reference (~40 s a
+    step here), stored as projections only (the fixture stays small): per
+    step the picks, SI and deficiency counts, S, and 12-row random
+    projections of T, info.phi, W and X S W^T."""
+    tag, per, r, nq, nsteps, seed = "dlr_c2_50", 40, 16, 32, 50, 2
+    spec = problems.checkerboard(per, rank=r, n_polar=nq, n_azimuthal=nq, seed=seed)
+    rng = np.random.default_rng(spec.seed)
+    Xr, Wr = problems.draw_factors(spec, rng)
+    g = mesh.build_grid(spec.nx, spec.ny, spec.extent)
+    quad = angular.build_quadrature(nq, nq)
+    mass = driver.assemble_mass(g)
+    comp = lowrank.spatial_monomials(mesh.dof_coordinates(g), g.extent, r + 8)
+    X, _, _ = angular.gram_schmidt(Xr, lowrank.mass_inner(mass), comp)
+    Wb, _, _ = angular.orthonormalize(Wr, quad)
+    k = physics.PhysicsConstants(c=spec.c, a_r=spec.a_r)
+    b0, _ = physics.planck(driver.cells_to_dofs(g, spec.T0), k)
+    S = np.outer(X.T @ (mass @ b0), Wb.beta)
+    state = lowrank.DlrState(X=X, S=S, W=Wb)
+    pr = np.random.default_rng(29)
+    pT = pr.standard_normal((12, g.n_cells))
+    pphi = pr.standard_normal((12, g.n_dofs))
+    pW = pr.standard_normal((12, quad.n_angles))
+    out = {}
+    T = spec.T0.copy()
+    for s in range(nsteps):
+        lin = physics.linearize(T, spec.sigma_a, spec.rho_cv, spec.dt, k)
+        lin.sigma_t = lin.sigma_t + spec.sigma_s_phys
+        lin.sigma_s = lin.sigma_s + spec.sigma_s_phys
+        lin.q = lin.q + spec.q_ext
+        state, info = dlr_sn.step_collocation(g, lin, quad, state, si_tol=1e-12, si_max_iters=400,
+                                              use_dsa=False)
+        raw = physics.update_temperature(driver.dofs_to_cells(g, info.phi), lin, -np.inf)
+        T = np.maximum(raw, 1e-6)
+        out.update({f"s{s}_idx": info.angle_indices, f"s{s}_iters": info.iterations,
+                    f"s{s}_Tp": pT @ T, f"s{s}_phip": pphi @ info.phi, f"s{s}_S": state.S,
+                    f"s{s}_Wp": pW @ state.W.values,
+                    f"s{s}_sketch": sketch(state.X, state.S, state.W.values),
+                    f"s{s}_sdef": info.spatial_deficiency, f"s{s}_adef": info.angular_deficiency})
+        print(tag, "step", s, info.iterations, info.angle_indices, flush=True)
+        if s % 10 == 9:  # checkpoint: a long run survives an interruption
+            save(tag, nsteps=s + 1, per=per, rank=r, nq=nq, seed=seed, proj_seed=29, **out)
+    save(tag, nsteps=nsteps, per=per, rank=r, nq=nq, seed=seed, proj_seed=29, **out)
+
+
 def ref_step_inflow(g, og, step, quad, state, inflow, si_tol):
     """step_collocation (dlr_sn.py:99-151) composed from the reference's own
     functions, plus the two inflow terms of the restatement (the reference
@@ -476,6 +521,10 @@ if __name__ == "__main__":
     import importlib
 
     sys.modules["helpers_ref"] = importlib.import_module("helpers")
+    if len(sys.argv) > 1 and sys.argv[1] == "dlr_c2_50":
+        # BASELINE config 2 itself, all 50 steps of the real reference (~35 min)
+        run_c2_fifty()
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "dlr_c1_20":
         # BASELINE config 1 itself, all 20 steps of the real reference
         run_c1_twenty()

@@ -10,7 +10,9 @@ si_tol = 1e-12 and use_dsa = False, and requires at EVERY step:
 identical DEIM picks and SI iteration counts, and rel-L2 <= 1e-11 on
 info.phi (the flux of the T update), on T and on X S W^T (stacked-QR norm,
 no cancellation floor).  The oracle itself is pinned to the real reference
-on config 1 (3 steps) and config 2 (1 step) by tests/test_oracle_golden.py.
+on config 1 (all 20 steps) and config 2 by tests/test_oracle_golden.py, and
+the GPU's 50 config-2 steps are also held to the real reference's own
+50-step run (projections, tests/golden/dlr_c2_50.npz).
 
 * C2 (280^2, r = 16, 32x32 quadrature): all 50 steps.
 * C3 (Marshak 512^2, r = 32, 64x64, left inflow T_b = 1) from its physical
@@ -39,9 +41,32 @@ def _need_gpu():
     build()
 
 
-def _lockstep(spec, n_steps, gs_method="cholqr2", check=None):
+def _golden_check(g, k, info, T, Xg, Sg, Wg):
+    """The GPU state of step k against the REAL reference's run of the same
+    config (make_golden.py dlr_c2_50: projections only)."""
+    if f"s{k}_idx" not in g:
+        return
+    assert list(info.angle_indices) == list(g[f"s{k}_idx"]), k
+    assert info.iterations == int(g[f"s{k}_iters"]), k
+    assert info.spatial_deficiency == int(g[f"s{k}_sdef"]), k
+    assert info.angular_deficiency == int(g[f"s{k}_adef"]), k
+    pr = np.random.default_rng(int(g["proj_seed"]))
+    pT = pr.standard_normal((12, T.shape[0]))
+    pphi = pr.standard_normal((12, Xg.shape[0]))
+    pW = pr.standard_normal((12, Wg.shape[0]))
+    assert rel_l2(pT @ T, g[f"s{k}_Tp"]) <= TOL, k
+    assert rel_l2(pphi @ info.phi.cpu().numpy(), g[f"s{k}_phip"]) <= TOL, k
+    assert rel_l2(Sg, g[f"s{k}_S"]) <= TOL and rel_l2(pW @ Wg, g[f"s{k}_Wp"]) <= TOL, k
+    rng = np.random.default_rng(9)
+    phi_t = rng.standard_normal((Xg.shape[0], 12))
+    om_t = rng.standard_normal((Wg.shape[0], 12))
+    assert rel_l2((phi_t.T @ Xg) @ Sg @ (Wg.T @ om_t), g[f"s{k}_sketch"]) <= TOL, k
+
+
+def _lockstep(spec, n_steps, gs_method="cholqr2", check=None, golden=None):
     """Run oracle and GPU side by side; returns the per-step records
-    [(picks equal, iters (gpu, ref), phi err, T err, XSW err, sdef (gpu, ref))]."""
+    [(picks equal, iters (gpu, ref), phi err, T err, XSW err, sdef (gpu, ref))].
+    ``golden``: also hold every GPU step to the real reference's run."""
     from oracle import port as P
     from oracle import runner as R
     from paper_2601_18705_b200 import problems
@@ -65,6 +90,8 @@ def _lockstep(spec, n_steps, gs_method="cholqr2", check=None):
         state, lin, T, info = dp.step(state, lin, T, si_tol=1e-12, si_max_iters=400,
                                       gs_method=gs_method)
         Xg, Sg, Wg = state.to_numpy()
+        if golden is not None:
+            _golden_check(golden, k, info, T.cpu().numpy(), Xg, Sg, Wg)
         rec = {
             "step": k,
             "picks": list(info.angle_indices) == list(rinfo.angle_indices),
@@ -93,11 +120,15 @@ def _strict(rec):
     assert rec["xsw"] <= TOL, (k, rec["xsw"])
 
 
-def test_config2_all_fifty_steps_match_oracle():
+def test_config2_all_fifty_steps_match_oracle(golden):
+    """All 50 steps against the oracle in lock step, and every step against
+    the real reference's own 50-step run (tests/golden/dlr_c2_50.npz)."""
     from paper_2601_18705_b200 import problems
 
     spec = problems.config2()
-    recs = _lockstep(spec, spec.n_steps, check=_strict)
+    g = golden("dlr_c2_50")
+    assert int(g["nsteps"]) == 50
+    recs = _lockstep(spec, spec.n_steps, check=_strict, golden=g)
     assert len(recs) == 50
 
 

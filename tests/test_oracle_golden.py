@@ -274,6 +274,31 @@ def test_config1_twenty_steps_match_reference(golden):
         assert rel_l2((phi_t.T @ s.X) @ s.S @ (s.W.T @ om_t), g[f"s{k}_sketch"]) <= 1e-11, k
 
 
+def test_config2_first_steps_match_reference_fifty_step_run(golden):
+    """The oracle against the real reference's 50-step config-2 run
+    (dlr_c2_50.npz, projections): its first 8 steps here on the CPU; the
+    GPU is held to all 50 in test_gpu_baseline_parity.py."""
+    g = golden("dlr_c2_50")
+    spec, st0 = _run_checker(g)
+    recs = []
+    R.run(spec, st0, 8, record=lambda s, i, t: recs.append((s, i, t)))
+    pr = np.random.default_rng(int(g["proj_seed"]))
+    pT = pr.standard_normal((12, spec.n_cells))
+    pphi = pr.standard_normal((12, st0.X.shape[0]))
+    pW = pr.standard_normal((12, st0.W.shape[0]))
+    for k, (s, info, T) in enumerate(recs):
+        assert list(info.angle_indices) == list(g[f"s{k}_idx"]), k
+        assert info.iterations == int(g[f"s{k}_iters"]), k
+        assert info.spatial_deficiency == int(g[f"s{k}_sdef"]), k
+        assert rel_l2(pT @ T, g[f"s{k}_Tp"]) <= 1e-11, k
+        assert rel_l2(pphi @ info.phi, g[f"s{k}_phip"]) <= 1e-11, k
+        assert rel_l2(s.S, g[f"s{k}_S"]) <= 1e-11 and rel_l2(pW @ s.W, g[f"s{k}_Wp"]) <= 1e-11, k
+        rng = np.random.default_rng(9)
+        phi_t = rng.standard_normal((s.X.shape[0], 12))
+        om_t = rng.standard_normal((s.W.shape[0], 12))
+        assert rel_l2((phi_t.T @ s.X) @ s.S @ (s.W.T @ om_t), g[f"s{k}_sketch"]) <= 1e-11, k
+
+
 # ---- isotropic inflow boundary (config 3; a restatement, see port.inflow_load)
 
 
