@@ -46,7 +46,8 @@ enum {
   DLRSN_ECUDA = -4,       /* CUDA runtime failure */
   DLRSN_EINTERP = -5,     /* InterpolationError */
   DLRSN_ECOMPLETION = -6, /* ContractViolation: ran out of completion vectors */
-  DLRSN_EITER = -7        /* IterationLimitError (info->iterations, info->residual) */
+  DLRSN_EITER = -7,       /* IterationLimitError (info->iterations, info->residual) */
+  DLRSN_ECG = -8          /* CgError: the DSA conjugate gradient hit its iteration cap */
 };
 
 #define DLRSN_MAX_RANK 128 /* largest rank r of the step-level entry point */
@@ -423,6 +424,16 @@ typedef struct dlrsn_step_params {
                                 copy stream as soon as it is final (after K2), overlapping the
                                 projections and the angular update; the call returns after the
                                 copy (a caller holding its state in host memory) */
+  int use_dsa;               /* 1: diffusion synthetic acceleration of every source iteration
+                                inside the call (transport_sn.py:439-441; K6 on the device, no
+                                host synchronisation per iteration) */
+  int dsa_penalty;           /* 0: "simplified" (kx = ky = 1/4), 1: "collocation" (1/2
+                                closure.|omega_x|/(4 pi) of the step's own DEIM selection,
+                                dlr_sn.py:104, transport_sn.py:183-188; formed on the device) */
+  double dsa_tol;            /* PCG relative tolerance (0: the reference's 1e-10) */
+  int dsa_max_iters;         /* PCG cap (0: the reference's 10 n_dofs) */
+  double* dsa_history;       /* device, optional: ||r_k|| of the (first failed, else last) PCG */
+  int dsa_hist_cap;
 } dlrsn_step_params;
 
 typedef struct dlrsn_step_info { /* HOST, filled by the call */
@@ -442,6 +453,8 @@ typedef struct dlrsn_step_info { /* HOST, filled by the call */
                                 the call then fails with DLRSN_ECUDA and re-arms the workspace) */
   double deim_gap[DLRSN_MAX_RANK]; /* per pick: (|top| - |second|) / |top| of the DEIM
                                 residual (near-tie diagnostic, lowrank.py:191 argmax) */
+  int dsa_iterations;        /* use_dsa: PCG iterations summed over the step's source iterations */
+  int dsa_solves;            /* use_dsa: diffusion solves that ran (zero-residual ones excluded) */
 } dlrsn_step_info;
 
 /* Multi-GPU hooks (NULL = one GPU): the step calls allreduce_sum(user) to

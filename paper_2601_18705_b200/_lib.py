@@ -51,7 +51,9 @@ class StepParams(ctypes.Structure):
                 ("si_max_iters", c_int), ("check_state", c_int), ("gs_method", c_int),
                 ("sweep_dw", c_int), ("advance", c_vp), ("inflow", c_dbl * 4),
                 ("x_check_in", c_vp), ("x_check_out", c_vp), ("si_batch_hint", c_int),
-                ("angle_override", c_int), ("angle_indices_in", c_vp), ("x_new_host", c_vp)]
+                ("angle_override", c_int), ("angle_indices_in", c_vp), ("x_new_host", c_vp),
+                ("use_dsa", c_int), ("dsa_penalty", c_int), ("dsa_tol", c_dbl),
+                ("dsa_max_iters", c_int), ("dsa_history", c_vp), ("dsa_hist_cap", c_int)]
 
 
 class StepInfo(ctypes.Structure):
@@ -59,7 +61,8 @@ class StepInfo(ctypes.Structure):
                 ("angular_deficiency", c_int), ("error_index", c_int), ("gs_fallback", c_int),
                 ("residual", c_dbl), ("check_in", c_dbl * 2), ("check_out", c_dbl * 2),
                 ("angle_indices", c_i64 * MAX_RANK), ("closure", c_dbl * MAX_RANK),
-                ("si_batch_hint", c_int), ("sweep_status", c_int), ("deim_gap", c_dbl * MAX_RANK)]
+                ("si_batch_hint", c_int), ("sweep_status", c_int), ("deim_gap", c_dbl * MAX_RANK),
+                ("dsa_iterations", c_int), ("dsa_solves", c_int)]
 
 
 COMM_FN = ctypes.CFUNCTYPE(c_int, c_vp)

@@ -51,6 +51,13 @@ struct DsaArgs {
   int* info;  // [0] iterations, [1] status (0 ok, 1 CG cap reached)
   double* history;
   int hist_cap;
+  // one-call step (dsa_correct_launch): penalty weights (kx, ky) read from
+  // the device, the launch returns at once when *skip is set (a converged
+  // source iteration), and info accumulates over the step's launches:
+  // [1] sticky failure, [2] total CG iterations, [3] launches that solved
+  const double* k_dev;
+  const int* skip;
+  int accumulate;
 };
 
 __device__ __forceinline__ void ld4(const double* v, int64_t c, double o[4]) {
@@ -189,11 +196,12 @@ __device__ void pt_mtinv_p_plus_j(const DsaArgs& a, const double* v, int i, int 
   for (int l = 0; l < 4; ++l) acc[l] += pen * jv[l];
 }
 
-__device__ void apply_a(const DsaArgs& a, const double* v, int i, int j, double out[4]) {
+__device__ void apply_a(const DsaArgs& a, double kx2, double ky2, const double* v, int i, int j,
+                        double out[4]) {
   const int64_t c = (int64_t)j * a.nx + i;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  pt_mtinv_p_plus_j<0>(a, v, i, j, a.kx2, acc);
-  pt_mtinv_p_plus_j<1>(a, v, i, j, a.ky2, acc);
+  pt_mtinv_p_plus_j<0>(a, v, i, j, kx2, acc);
+  pt_mtinv_p_plus_j<1>(a, v, i, j, ky2, acc);
   double vc[4];
   ld4(v, c, vc);
   const double sa = a.sigma_t[c] - a.sigma_s[c];
@@ -305,9 +313,12 @@ __device__ __forceinline__ void grid_total2(const double* part, double& t0, doub
 }
 
 __global__ void __launch_bounds__(kDsaT) dsa_pcg_kernel(const DsaArgs a) {
+  if (a.skip && *a.skip) return;  // uniform over the grid: no barrier is reached
   cg::grid_group grid = cg::this_grid();
   __shared__ double red[2 * (kDsaT / 32)];
   __shared__ double bc[2];
+  const double kx2 = a.k_dev ? 2.0 * a.k_dev[0] : a.kx2;
+  const double ky2 = a.k_dev ? 2.0 * a.k_dev[1] : a.ky2;
   const int nc = a.nx * a.ny;
   const int nth = gridDim.x * blockDim.x;
   const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
@@ -330,7 +341,7 @@ __global__ void __launch_bounds__(kDsaT) dsa_pcg_kernel(const DsaArgs a) {
     const double sa = a.sigma_t[c] - a.sigma_s[c];
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
-      const double d = diag_axis<0>(a, i, j, l, a.kx2) + diag_axis<1>(a, i, j, l, a.ky2) +
+      const double d = diag_axis<0>(a, i, j, l, kx2) + diag_axis<1>(a, i, j, l, ky2) +
                        sa * a.mass[5 * l];
       dv[l] = 1.0 / d;
       z[l] = dv[l] * b[l];
@@ -360,11 +371,13 @@ __global__ void __launch_bounds__(kDsaT) dsa_pcg_kernel(const DsaArgs a) {
     }
     if (t0 == 0) {
       a.info[0] = 0;
-      a.info[1] = 0;
+      if (!a.accumulate) a.info[1] = 0;
     }
     return;
   }
-  if (t0 == 0 && a.history && a.hist_cap > 0) a.history[0] = bnorm;
+  // the history of a step's first failed solve is kept (accumulate mode)
+  const bool hist_on = a.history && !(a.accumulate && a.info[1]);
+  if (t0 == 0 && hist_on && a.hist_cap > 0) a.history[0] = bnorm;
   int it = 1;
   bool done = false;
   for (; it <= a.max_iters; ++it) {
@@ -374,7 +387,7 @@ __global__ void __launch_bounds__(kDsaT) dsa_pcg_kernel(const DsaArgs a) {
     for (int c = t0; c < nc; c += nth) {
       const int i = c % a.nx, j = c / a.nx;
       double ap[4], pc[4];
-      apply_a(a, a.p, i, j, ap);
+      apply_a(a, kx2, ky2, a.p, i, j, ap);
       ld4(a.p, c, pc);
 #pragma unroll
       for (int l = 0; l < 4; ++l) s0 += pc[l] * ap[l];
@@ -420,7 +433,7 @@ __global__ void __launch_bounds__(kDsaT) dsa_pcg_kernel(const DsaArgs a) {
     double rr, rz_new;
     grid_total2(part1, rr, rz_new, bc);
     const double rnorm = sqrt(rr);
-    if (t0 == 0 && a.history && it < a.hist_cap) a.history[it] = rnorm;
+    if (t0 == 0 && hist_on && it < a.hist_cap) a.history[it] = rnorm;
     if (rnorm <= a.tol * bnorm) {
       done = true;
       break;
@@ -448,7 +461,13 @@ __global__ void __launch_bounds__(kDsaT) dsa_pcg_kernel(const DsaArgs a) {
   }
   if (t0 == 0) {
     a.info[0] = done ? it : a.max_iters;
-    a.info[1] = done ? 0 : 1;
+    if (!a.accumulate) {
+      a.info[1] = done ? 0 : 1;
+    } else {
+      if (!done) a.info[1] = 1;
+      a.info[2] += done ? it : a.max_iters;
+      a.info[3] += 1;
+    }
   }
 }
 
@@ -480,28 +499,13 @@ void inv4(const double* m, double* out) {
 }
 
 }  // namespace
-}  // namespace dlrsn
 
-using namespace dlrsn;
-
-extern "C" {
-
-int64_t dlrsn_dsa_workspace_len(int nx, int ny) {
-  const int64_t nd = 4 * (int64_t)nx * ny;
-  return 5 * nd + 4 * 148 * 8 + 64;
-}
-
-int dlrsn_dsa_correct(const dlrsn_cellops* ops, const double* sigma_t, const double* sigma_s,
-                      double kx, double ky, const double* phi_half, const double* phi_old,
-                      double* phi_out, double tol, int max_iters, double* workspace,
-                      int64_t workspace_len, int* info, double* history, int hist_cap,
-                      dlrsn_stream_t stream) {
-  DLRSN_REQUIRE(ops && sigma_t && sigma_s && phi_half && phi_old && phi_out && workspace && info,
-                "bad arguments to dlrsn_dsa_correct");
-  DLRSN_REQUIRE(max_iters >= 1, "max_iters must be positive");
+int dsa_correct_launch(const dlrsn_cellops* ops, const double* sigma_t, const double* sigma_s,
+                       double kx, double ky, const double* k_dev, const double* phi_half,
+                       const double* phi_old, double* phi_out, double tol, int max_iters,
+                       double* workspace, int* info, double* history, int hist_cap,
+                       const int* skip, int accumulate, cudaStream_t st) {
   const int64_t nd = 4 * (int64_t)ops->nx * ops->ny;
-  DLRSN_REQUIRE(workspace_len >= dlrsn_dsa_workspace_len(ops->nx, ops->ny),
-                "dsa workspace too small");
   DsaArgs a;
   a.nx = ops->nx;
   a.ny = ops->ny;
@@ -529,21 +533,55 @@ int dlrsn_dsa_correct(const dlrsn_cellops* ops, const double* sigma_t, const dou
   a.info = info;
   a.history = history;
   a.hist_cap = history ? hist_cap : 0;
-  int dev = 0, sms = 0, occ = 0;
+  a.k_dev = k_dev;
+  a.skip = skip;
+  a.accumulate = accumulate;
+  static thread_local int cached_dev = -1, cached_cap = 0;
+  int dev = 0;
   DLRSN_TRY_CUDA(cudaGetDevice(&dev));
-  DLRSN_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  DLRSN_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dsa_pcg_kernel, kDsaT, 0));
+  if (dev != cached_dev) {  // the occupancy query is not capturable: once per device
+    int sms = 0, occ = 0;
+    DLRSN_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    DLRSN_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dsa_pcg_kernel, kDsaT, 0));
+    cached_cap = sms * (occ < 1 ? 1 : (occ > 8 ? 8 : occ));
+    cached_dev = dev;
+  }
   const int nc = ops->nx * ops->ny;
   int blocks = (nc + kDsaT - 1) / kDsaT;
-  const int cap = sms * (occ < 1 ? 1 : (occ > 8 ? 8 : occ));
-  if (blocks > cap) blocks = cap;
+  if (blocks > cached_cap) blocks = cached_cap;
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks < 1) blocks = 1;
   void* params[] = {&a};
   launch_counter().fetch_add(1, std::memory_order_relaxed);
   DLRSN_TRY_CUDA(cudaLaunchCooperativeKernel((const void*)dsa_pcg_kernel, dim3(blocks),
-                                             dim3(kDsaT), params, 0, as_stream(stream)));
+                                             dim3(kDsaT), params, 0, st));
   return DLRSN_OK;
+}
+
+}  // namespace dlrsn
+
+using namespace dlrsn;
+
+extern "C" {
+
+int64_t dlrsn_dsa_workspace_len(int nx, int ny) {
+  const int64_t nd = 4 * (int64_t)nx * ny;
+  return 5 * nd + 4 * 148 * 8 + 64;
+}
+
+int dlrsn_dsa_correct(const dlrsn_cellops* ops, const double* sigma_t, const double* sigma_s,
+                      double kx, double ky, const double* phi_half, const double* phi_old,
+                      double* phi_out, double tol, int max_iters, double* workspace,
+                      int64_t workspace_len, int* info, double* history, int hist_cap,
+                      dlrsn_stream_t stream) {
+  DLRSN_REQUIRE(ops && sigma_t && sigma_s && phi_half && phi_old && phi_out && workspace && info,
+                "bad arguments to dlrsn_dsa_correct");
+  DLRSN_REQUIRE(max_iters >= 1, "max_iters must be positive");
+  DLRSN_REQUIRE(workspace_len >= dlrsn_dsa_workspace_len(ops->nx, ops->ny),
+                "dsa workspace too small");
+  return dsa_correct_launch(ops, sigma_t, sigma_s, kx, ky, nullptr, phi_half, phi_old, phi_out, tol,
+                            max_iters, workspace, info, history, hist_cap, nullptr, 0,
+                            as_stream(stream));
 }
 
 }  // extern "C"

@@ -355,6 +355,9 @@ struct StepBufs {
   int* cholw;
   double *Rw1, *Rw1inv, *Rw2, *Rw2inv, *ratiow2, *lq1;  // angular CholQR2, r > 32
   double* hin;  // X_new^T of the unit inflow load per wall (4 x r)
+  // DSA inside the step: phi_half, the PCG workspace, {kx, ky}, the info words
+  double *dsa_half, *dsa_ws, *dsa_k;
+  int* dsa_info;
   Upload* up;
 };
 
@@ -437,6 +440,10 @@ static size_t carve(Arena& ar, StepBufs& b, int nx, int ny, int r, int no, int w
   b.cgtab = ar.take<CgTable>(1);
   b.cg_quad = ar.take<int>(r);
   b.cg_w = ar.take<double>(r);
+  b.dsa_half = ar.take<double>(N);
+  b.dsa_ws = ar.take<double>(dlrsn_dsa_workspace_len(nx, ny));
+  b.dsa_k = ar.take<double>(2);
+  b.dsa_info = ar.take<int>(4);
   b.up = ar.take<Upload>(1);
   return ar.off;
 }
@@ -476,6 +483,7 @@ struct StepStatus {
   int cholflag[2], cholw[2];
   int sweep_status;                 // sweep workspace word 1 (2: handoff timeout)
   double deim_gap[DLRSN_MAX_RANK];
+  int dsa[4];  // last CG iterations, failure, total CG iterations, solves
 };
 
 // pinned, device-mapped host copy of the status block (one per host thread;
@@ -526,6 +534,7 @@ static int enqueue_status(cudaStream_t st, const StepBufs& b, int r, StepStatus*
   add(b.cholw, 2 * sizeof(int), dev->cholw);
   add(reinterpret_cast<const int*>(sweep_ws) + 1, sizeof(int), &dev->sweep_status);
   add(b.deimgap, r * sizeof(double), dev->deim_gap);
+  add(b.dsa_info, 4 * sizeof(int), dev->dsa);
   (void)hs;
   pack_kernel<<<1, 256, 0, st>>>(l, reinterpret_cast<unsigned*>(g_status_dev));
   DLRSN_CHECK_LAUNCH("pack_kernel");
@@ -824,6 +833,17 @@ __global__ void si_select_kernel(int64_t n, const SiCtl* __restrict__ ctl,
     out[e] = src[e];
 }
 
+// DSA "collocation" penalty weights of the step's own selection
+// (transport_sn.py:186-188): k = 1/2 closure.|omega_{x,y}| / (4 pi)
+__global__ void dsa_penalty_kernel(int r, const double* __restrict__ closure,
+                                   const double* __restrict__ om_sel, double* __restrict__ k) {
+  if (threadIdx.x < 2) {
+    double acc = 0.0;
+    for (int d = 0; d < r; ++d) acc += closure[d] * fabs(om_sel[3 * d + threadIdx.x]);
+    k[threadIdx.x] = 0.5 * acc / (4.0 * 3.14159265358979323846);
+  }
+}
+
 static int grid_n(int64_t n) {
   int64_t b = (n + 255) / 256;
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
@@ -871,6 +891,8 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
   DLRSN_REQUIRE(r >= 1 && r <= DLRSN_MAX_RANK, "rank %d outside [1, %d]", r, DLRSN_MAX_RANK);
   DLRSN_REQUIRE(r <= no, "rank %d exceeds the %d available nodes", r, no);
   DLRSN_REQUIRE(p->sweep_dw <= 1, "the one-call step sweeps single-direction groups (sweep_dw 1)");
+  DLRSN_REQUIRE(!p->use_dsa || p->dsa_penalty == 0 || p->dsa_penalty == 1,
+                "unknown dsa penalty variant %d", p->dsa_penalty);
   const int world = comm ? comm->world_size : 1;
   const int rank_id = comm ? comm->rank : 0;
   DLRSN_REQUIRE(world >= 1 && world <= 8 && rank_id >= 0 && rank_id < world,
@@ -898,7 +920,7 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms_count, cudaDevAttrMultiProcessorCount, dev);
   }
-  const bool grouped = world == 1 && nl > 0 && sweep_group_width() > 0 &&
+  const bool grouped = world == 1 && nl > 0 && !p->use_dsa && sweep_group_width() > 0 &&
                        sk_strips(ny) * G > 4 * sms_count;
   // full-rank fast path of the angular update: one-CTA weighted CholQR2
   const bool ang_fast = r <= 32 && dlrsn_cholqr2_small_smem(no, r) <= 200 * 1024;
@@ -990,6 +1012,13 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     // 2. evaluate_rows (dlr_sn.py:110-121) and the sweep rhs
     ks_kernel<<<1, 1024, 0, st>>>(r, S, W, b.idx, beta, b.K, nullptr, p->omegas_dev, b.om_sel);
     DLRSN_CHECK_LAUNCH("ks_kernel");
+    if (p->use_dsa) {
+      DLRSN_TRY_CUDA(zero_async(b.dsa_info, 4 * sizeof(int), st));
+      if (p->dsa_penalty == 1) {
+        dsa_penalty_kernel<<<1, 32, 0, st>>>(r, b.closure, b.om_sel, b.dsa_k);
+        DLRSN_CHECK_LAUNCH("dsa_penalty_kernel");
+      }
+    }
     DLRSN_RET(dlrsn_rowmix(N, r, r, X, r, b.K, r, 0.0, b.psi_time, r, s));
     const double* pt_local = b.psi_time;
     int ld_pt = r;
@@ -1011,6 +1040,16 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
   // 3. source iterations it_from..it_to (transport_sn.py:408-447): the
   // convergence test runs on the device (si_decide) and iterations past it
   // return at once; then the converged flux / swept columns are selected
+  const double dsa_tol = p->dsa_tol > 0.0 ? p->dsa_tol : 1e-10;  // pcg defaults, :325-328
+  const int dsa_cap = p->dsa_max_iters > 0
+                          ? p->dsa_max_iters
+                          : (int)std::min<int64_t>(10 * N, (int64_t)INT32_MAX);
+  auto dsa_launch = [&](double* phi_half, const double* phi_old, cudaStream_t st) -> int {
+    return dsa_correct_launch(ops, sigma_t, sigma_s, 0.25, 0.25,
+                              p->dsa_penalty == 1 ? b.dsa_k : nullptr, phi_half, phi_old, phi_half,
+                              dsa_tol, dsa_cap, b.dsa_ws, b.dsa_info, p->dsa_history,
+                              p->dsa_hist_cap, &b.ctl->done, 1, st);
+  };
   auto enqueue_si = [&](cudaStream_t st, int it_from, int it_to) -> int {
     void* s = st;
     for (int it = it_from; it <= it_to; ++it) {
@@ -1030,7 +1069,17 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
       if (nl > 0)
         DLRSN_RET(sweep_launch(ops, G, b.groups, 1, b.sig4, b.scat, b.rhs_sk, b.psi_sk, nullptr,
                                sweep_ws, sweep_ws_bytes, 0, &b.ctl->done, st));
-      if (world == 1) {
+      if (world == 1 && p->use_dsa) {
+        // phi_half = psi closure, phi_half += delta (K6, one cooperative
+        // launch, skipped on the device once converged), then the norms and
+        // the next scattering source from the corrected flux (:439-446)
+        DLRSN_RET(phi_closure_launch(ops, nl, b.quads, b.cw_local, b.psi_sk, b.phiq, phi, sigma_s,
+                                     nullptr, nullptr, b.norms, b.red_ws, b.ctl, -1, p->si_tol,
+                                     nullptr, b.dsa_half, st));
+        DLRSN_RET(dsa_launch(b.dsa_half, phi, st));
+        DLRSN_RET(phi_finish_launch(ops, b.dsa_half, phin, phi, sigma_s, b.scat, b.norms, b.red_ws,
+                                    b.ctl, it, p->si_tol, b.flags + 1, st));
+      } else if (world == 1) {
         DLRSN_RET(phi_closure_launch(ops, nl, b.quads, b.cw_local, b.psi_sk, b.phiq, phi, sigma_s,
                                      phin, b.scat, b.norms, b.red_ws, b.ctl, it, p->si_tol,
                                      b.flags + 1, nullptr, st));
@@ -1045,6 +1094,8 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
           set_error("allreduce of the closure flux failed");
           return DLRSN_ECUDA;
         }
+        // DSA replicated on every rank from the summed flux
+        if (p->use_dsa) DLRSN_RET(dsa_launch(comm->reduce_buf, phi, st));
         DLRSN_RET(phi_finish_launch(ops, comm->reduce_buf, phin, phi, sigma_s, b.scat, b.norms,
                                     b.red_ws, b.ctl, it, p->si_tol, b.flags + 1, st));
       }
@@ -1234,6 +1285,13 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     }
     for (int d = 0; d < r; ++d) info->closure[d] = hs->closure[d];
     info->residual = hs->ctl.change;
+    info->dsa_iterations = p->use_dsa ? hs->dsa[2] : 0;
+    info->dsa_solves = p->use_dsa ? hs->dsa[3] : 0;
+    if (p->use_dsa && hs->dsa[1]) {  // CgError (transport_sn.py:350)
+      info->iterations = dsa_cap;
+      set_error("dsa failed to reach tol %g", dsa_tol);
+      return DLRSN_ECG;
+    }
     if (!hs->ctl.done) {
       if (it_next > p->si_max_iters) {
         info->iterations = p->si_max_iters;
@@ -1252,7 +1310,10 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     info->iterations = hs->ctl.iters;
     // next step's batch hint: grows to cover this step's count (stable
     // batches keep the graph keys stable; a shortfall costs one more segment)
-    info->si_batch_hint = std::max(batch0, hs->ctl.iters + 1);
+    // (rounded up to a multiple of 4: a slowly growing count -- the Marshak
+    // wave's 15, 16, 19, 20 -- re-captures the graphs once, not every step;
+    // iterations past convergence return at once)
+    info->si_batch_hint = std::max(batch0, (hs->ctl.iters + 1 + 3) / 4 * 4);
     if (!exact) {
       // CholQR's R_kk is accurate to ~eps/rel^2: keep it only when every
       // column retains >= 1e-6 of its M-norm and sits 100x above the

@@ -166,6 +166,14 @@ int phi_closure_launch(const dlrsn_cellops* ops, int D, const int* quads, const 
                        const double* sigma_s, double* phi_new, double* scat_sk4, double* norms,
                        void* partial_ws, SiCtl* ctl, int it, double tol, const int* any_scat,
                        double* partial_out, cudaStream_t st);
+// K6 inside the one-call step (dsa.cu): phi_out = phi_half + delta; k_dev
+// (device, nullable) overrides (kx, ky); *skip != 0 returns at once; with
+// accumulate, info = {last iterations, sticky failure, total iterations, solves}
+int dsa_correct_launch(const dlrsn_cellops* ops, const double* sigma_t, const double* sigma_s,
+                       double kx, double ky, const double* k_dev, const double* phi_half,
+                       const double* phi_old, double* phi_out, double tol, int max_iters,
+                       double* workspace, int* info, double* history, int hist_cap,
+                       const int* skip, int accumulate, cudaStream_t st);
 int phi_finish_launch(const dlrsn_cellops* ops, const double* phi_src, double* phi_dst,
                       const double* phi_old, const double* sigma_s, double* scat_sk4,
                       double* norms, void* partial_ws, SiCtl* ctl, int it, double tol,

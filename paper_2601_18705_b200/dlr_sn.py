@@ -27,6 +27,7 @@ from . import _lib
 from ._device import as_device, device, empty, stream
 from .angular import AngularBasis, orthonormalize_async
 from .errors import (
+    CgError,
     ConfigurationError,
     ContractViolation,
     InterpolationError,
@@ -136,7 +137,10 @@ def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, 
     ``engine="native"`` issues the whole step from C++ through the single
     C-ABI call ``dlrsn_step_collocation`` (include/dlrsn.h); ``"python"``
     orchestrates the same kernels from Python (kept as a cross-check and for
-    the cases the native call does not take: DSA, a pinned constant column).
+    the case the native call does not take: a pinned constant column).
+    ``use_dsa=True`` (the reference default) runs inside the native call
+    too: K6 (matrix-free Jacobi-PCG, one cooperative launch) after every
+    sweep, skipped on the device once the iteration has converged.
 
     Host synchronisations: one before the source iteration (DEIM picks,
     closure weights and the input checks come back together), one per source
@@ -171,14 +175,15 @@ def step_collocation(grid, step, quad, state, *, si_tol=1e-8, si_max_iters=200, 
         return step_lean(grid, step, quad, state, si_tol=si_tol, si_max_iters=si_max_iters,
                          check_state=check_state, angle_indices=angle_indices,
                          deim_tie_tol=deim_tie_tol)
-    if (engine == "native" and not use_dsa and not state.W.pinned
+    if (engine == "native" and not state.W.pinned
             and state.rank <= _lib.MAX_RANK and (sweep_dw or 1) == 1
             and (comm is None or comm.world_size <= 8)):
         if dsa_penalty not in ("simplified", "collocation"):
             raise ContractViolation(f"unknown dsa penalty variant {dsa_penalty!r}")
         return _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state,
                             gs_method, sweep_dw, comm, _advance, inflow_values(inflow),
-                            angle_indices, deim_tie_tol, _x_new_host)
+                            angle_indices, deim_tie_tol, _x_new_host,
+                            dsa=dsa_penalty if use_dsa else None)
     if inflow_values(inflow) is not None:
         raise ConfigurationError("inflow boundaries need the native engine")
     if _advance is not None:
@@ -318,6 +323,8 @@ class _NativeSelection:
 
 
 _STEP_WS = {}
+_DSA_HIST = 4096
+_DSA_MAX_ITERS = 0  # PCG cap of the native step (0: the reference's 10 n_dofs)
 
 
 def release_workspaces():
@@ -455,6 +462,7 @@ class _NativeCtx:
         # source iterations enqueued before the first readback: per problem,
         # so every rank of a sharded run (same steps, same ctx history) agrees
         self.si_hint = 0
+        self.dsa_hist = None  # PCG residual history (device), allocated on first DSA step
 
 
 _CTX = {}
@@ -473,7 +481,7 @@ def _native_ctx(grid, quad, r, comm):
 
 def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_method, sweep_dw,
                  comm, advance=None, inflow=None, angle_indices=None, deim_tie_tol=DEIM_TIE_TOL,
-                 x_new_host=None):
+                 x_new_host=None, dsa=None):
     r = state.rank
     no = quad.n_angles
     n = grid.n_dofs
@@ -499,6 +507,16 @@ def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_
     p.advance = ctypes.addressof(advance) if advance is not None else None
     p.inflow[:] = inflow if inflow is not None else (0.0, 0.0, 0.0, 0.0)
     p.si_batch_hint = ctx.si_hint
+    # DSA inside the call (K6 per source iteration, no host round trips)
+    p.use_dsa = 0 if dsa is None else 1
+    p.dsa_penalty = 1 if dsa == "collocation" else 0
+    p.dsa_tol, p.dsa_max_iters = 0.0, int(_DSA_MAX_ITERS)  # 0: the reference's pcg defaults
+    if dsa is not None:
+        if ctx.dsa_hist is None:
+            ctx.dsa_hist = torch.zeros(_DSA_HIST, dtype=torch.float64, device=X.device)
+        p.dsa_history, p.dsa_hist_cap = ctx.dsa_hist.data_ptr(), _DSA_HIST
+    else:
+        p.dsa_history, p.dsa_hist_cap = None, 0
     if x_new_host is not None:
         if (not x_new_host.is_pinned() or x_new_host.dtype != torch.float64
                 or tuple(x_new_host.shape) != (n, r) or not x_new_host.is_contiguous()):
@@ -548,6 +566,10 @@ def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_
         if rc == -7:
             raise IterationLimitError("source iteration did not converge", int(info.iterations),
                                       float(info.residual))
+        if rc == -8:  # transport_sn.py:350
+            cap = int(info.iterations)
+            hist = ctx.dsa_hist[:min(cap + 1, _DSA_HIST)].cpu().numpy().tolist()
+            raise CgError("dsa failed to reach tol 1e-10", cap, hist)
         if rc in (-2, -3):
             raise SolverError(msg)
         if rc in (-1, -6):
@@ -584,4 +606,7 @@ def _step_native(grid, step, quad, state, si_tol, si_max_iters, check_state, gs_
     )
     res.gs_fallback = int(info.gs_fallback)
     res.deim_gaps = gaps
+    if dsa is not None:
+        res.dsa_iterations = int(info.dsa_iterations)
+        res.dsa_solves = int(info.dsa_solves)
     return new_state, res

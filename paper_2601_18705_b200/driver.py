@@ -95,7 +95,8 @@ class DeviceProblem:
 
 
     def step(self, state, lin, T, *, si_tol=1e-8, si_max_iters=200, check_state=True,
-             gs_method="cholqr2", comm=None, engine="native", x_new_host=None):
+             gs_method="cholqr2", comm=None, engine="native", x_new_host=None, use_dsa=False,
+             dsa_penalty="simplified"):
         """One DLR step and the step boundary (T update + re-linearisation)
         in a single native call (the fused form of step_collocation +
         advance, driver.py:486-487,532-534).  Returns (state, next
@@ -105,7 +106,8 @@ class DeviceProblem:
 
         if self.spec.frozen or engine != "native":
             state, info = step_collocation(self.grid, lin, self.quad, state, si_tol=si_tol,
-                                           si_max_iters=si_max_iters, use_dsa=False,
+                                           si_max_iters=si_max_iters, use_dsa=use_dsa,
+                                           dsa_penalty=dsa_penalty,
                                            check_state=check_state, gs_method=gs_method,
                                            comm=comm, inflow=self.spec.inflow, engine=engine)
             T = T.clone()
@@ -130,7 +132,8 @@ class DeviceProblem:
         av.T_out, av.sigma_a, av.sigma_t = T0.data_ptr(), sa.data_ptr(), st.data_ptr()
         av.sigma_s, av.q, av.denom = ss.data_ptr(), q.data_ptr(), den.data_ptr()
         state, info = step_collocation(self.grid, lin, self.quad, state, si_tol=si_tol,
-                                       si_max_iters=si_max_iters, use_dsa=False,
+                                       si_max_iters=si_max_iters, use_dsa=use_dsa,
+                                       dsa_penalty=dsa_penalty,
                                        check_state=check_state, gs_method=gs_method, comm=comm,
                                        inflow=self.spec.inflow, _advance=av,
                                        _x_new_host=x_new_host)
@@ -199,7 +202,8 @@ def initial_state_device(dp, seed=None, block_rows=1 << 22):
 
 
 def run(dp, state, n_steps, *, si_tol=1e-8, si_max_iters=200, check_state=True, T=None,
-        record=None, gs_method="cholqr2", engine="native", comm=None, diagnostics=None):
+        record=None, gs_method="cholqr2", engine="native", comm=None, diagnostics=None,
+        use_dsa=False, dsa_penalty="simplified"):
     """n_steps of the dlr-sn loop; returns (state, T, infos).  With a list
     as ``diagnostics``, the reference driver's energy rows (driver.py:
     521-553, DIAGNOSTIC_COLUMNS order) are appended to it, evaluated on the
@@ -220,10 +224,12 @@ def run(dp, state, n_steps, *, si_tol=1e-8, si_max_iters=200, check_state=True, 
         lin_used = lin
         if engine == "native":  # step + boundary in one native call
             state, lin, T, info = dp.step(state, lin, T, si_tol=si_tol, si_max_iters=si_max_iters,
-                                          check_state=check_state, gs_method=gs_method, comm=comm)
+                                          check_state=check_state, gs_method=gs_method, comm=comm,
+                                          use_dsa=use_dsa, dsa_penalty=dsa_penalty)
         else:
             state, info = step_collocation(dp.grid, lin, dp.quad, state, si_tol=si_tol,
-                                           si_max_iters=si_max_iters, use_dsa=False,
+                                           si_max_iters=si_max_iters, use_dsa=use_dsa,
+                                           dsa_penalty=dsa_penalty,
                                            check_state=check_state, gs_method=gs_method,
                                            engine=engine, comm=comm, inflow=dp.spec.inflow)
             lin = dp.advance(lin, info.phi, T)

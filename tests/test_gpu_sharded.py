@@ -135,3 +135,42 @@ def test_sharded_dlr_steps_match_unsharded(engine):
     for X, S, W, T in out:
         assert lowrank_rel_diff(X, S, W, ref[0], ref[1], ref[2]) <= 1e-12
         assert rel_l2(T, ref[3]) <= 1e-12
+
+
+def test_sharded_dsa_steps_match_unsharded():
+    """use_dsa=True in the sharded native step: the diffusion correction runs
+    replicated on every rank from the all-reduced flux.  The constant is put
+    in span(W) so the reference's DSA converges."""
+    from oracle import runner as R
+    from paper_2601_18705_b200 import problems
+    from paper_2601_18705_b200.dlr_sn import step_collocation
+    from paper_2601_18705_b200.driver import DeviceProblem, initial_state
+
+    spec = problems.checkerboard(12, rank=6, n_polar=4, n_azimuthal=6, seed=9, blocks=3)
+    spec.sigma_s_phys = np.where(spec.sigma_a > 0, 0.0, 30.0)
+    Xr, Wr = problems.draw_factors(spec, np.random.default_rng(21))
+    Wr[:, 0] = 1.0
+    X0, W0 = R.orthonormal_factors(spec, Xr, Wr)
+
+    def run(comm):
+        dp = DeviceProblem.from_spec(spec)
+        state = initial_state(dp, X=X0, W=W0)
+        T = torch.as_tensor(spec.T0, device="cuda").clone()
+        lin = dp.linearized(T)
+        its = []
+        for _ in range(2):
+            state, info = step_collocation(dp.grid, lin, dp.quad, state, si_tol=1e-12,
+                                           si_max_iters=400, use_dsa=True, comm=comm)
+            its.append(info.iterations)
+            lin = dp.advance(lin, info.phi, T)
+        X, S, W = state.to_numpy()
+        return X, S, W, T.cpu().numpy(), its
+
+    ref = run(None)
+    out = _run_ranks(run)
+    from oracle.port import lowrank_rel_diff, rel_l2
+
+    for X, S, W, T, its in out:
+        assert its == ref[4]
+        assert lowrank_rel_diff(X, S, W, ref[0], ref[1], ref[2]) <= 1e-12
+        assert rel_l2(T, ref[3]) <= 1e-12
