@@ -272,6 +272,22 @@ def cpu_reference_steps(spec, max_steps, budget_s, X=None, W=None):
             "sec": sec, "iters": iters, "per_step_s": per, "setup_s": setup}
 
 
+def arm_config(args, ws):
+    """The `config` object of the repo arm for this command line; the
+    reference arm prints the same object (it times the same workload)."""
+    slab = args.config == "C5" or (ws > 1 and args.sharding == "slab")
+    if slab:
+        return {"workload": WORKLOADS.get(args.config, "C5 stress 4096x4096, r=128, dlr-sn step"),
+                "si_tol": 1e-8, "use_dsa": False,
+                "parallelism": (f"row slabs x{ws} + direction-sharded sweeps (Option B)"
+                                if ws > 1 else "one GPU, lean engine"),
+                "l2": "inputs > L2"}
+    return {"workload": WORKLOADS[args.config], "si_tol": 1e-8, "use_dsa": False,
+            "parallelism": f"dp{ws} (directions)",
+            "l2": "inputs > L2 (X alone 2.1 GB at C4) and a 512 MB buffer written "
+                  "between timed steps (outside the step events)"}
+
+
 def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
@@ -288,9 +304,11 @@ def run_reference(args):
     line = {
         "metric": METRIC, "value": res["rate"], "unit": UNIT, "n_gpus": args.gpus,
         "steps": res["steps"], "warmup": 0, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "weak" if args.gpus == 1 else "strong", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (seeded BASELINE {args.config})", "impl": "reference",
-        "config": {"workload": WORKLOADS[args.config], "si_tol": 1e-8, "use_dsa": False},
+        "config": arm_config(args, args.gpus),
+        "config_note": "the repo arm's config object (both arms time this workload); its "
+                       "parallelism / l2 entries describe the GPU arm",
         "dlr_steps_per_s": res["steps"] / res["sec"],
         "si_iterations": res["iters"],
         "cpu_baseline": {"value": res["rate"], "unit": UNIT, "cores": cores, "kind": "port",
@@ -558,10 +576,7 @@ def main(argv=None):
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
         "scaling": "weak" if ws == 1 else "strong", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (seeded BASELINE {args.config}, random-orthonormal factors)",
-        "config": {"workload": WORKLOADS[args.config], "si_tol": 1e-8, "use_dsa": False,
-                   "parallelism": f"dp{ws} (directions)",
-                   "l2": "inputs > L2 (X alone 2.1 GB at C4) and a 512 MB buffer written "
-                         "between timed steps (outside the step events)"},
+        "config": arm_config(args, ws),
         "dlr_steps_per_s": args.steps / (ms * 1e-3),
         "si_iterations": iters,
         "ms_per_step_each": [round(x, 3) for x in per_ms],
@@ -660,11 +675,7 @@ def run_slab_bench(args, ws, rank, local):
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (seeded BASELINE {args.config})",
-        "config": {"workload": WORKLOADS.get(args.config, "C5 stress 4096x4096, r=128, dlr-sn step"),
-                   "si_tol": 1e-8, "use_dsa": False,
-                   "parallelism": (f"row slabs x{ws} + direction-sharded sweeps (Option B)"
-                                   if ws > 1 else "one GPU, lean engine"),
-                   "l2": "inputs > L2"},
+        "config": arm_config(args, ws),
         "dlr_steps_per_s": args.steps / (ms * 1e-3), "si_iterations": iters,
         "ms_per_step_each_rank0": [round(x, 3) for x in per],
         "clocks": clk.summary(), "wall_s_timed_region": wall,
