@@ -1903,13 +1903,398 @@ __device__ __forceinline__ void project32_group(const ProjArgs& pa, const dlrsn_
       out[7 * (int64_t)r * r + j0 + threadIdx.x] = qacc;
 }
 
+// ---------------------------------------------------------------------------
+// K3 on a DIAGONAL 64-column block (columns c0 .. c0 + 63 on both sides).
+// One CTA per output group and cell block computes the whole 64 x 64 block:
+//  * the i-side and j-side columns coincide, so every X element is staged
+//    once (the 32 x 32 tiling stages it in 3 tiles x 2 sides per group);
+//  * px, py are skew and jx, jy, mt, ms symmetric, so only the 36 of 64 8x8
+//    fragments on and above the diagonal are computed (mirrored after the
+//    reduction); the 8 warps hold 5 or 4 of them each (rows a and 7 - a
+//    share a warp pair), every warp over all cells of a chunk -- no
+//    cross-warp reduction;
+//  * mo = X_old^T M X has no symmetry: warp w owns fragment row w.
+// Chunks of 4 cells (256 staging items = 4 cells x 64 columns).
+constexpr int kPC64 = 4;
+constexpr int kLS64 = 68;  // row stride of the staged planes (conflict-free fragments)
+// cell strides = 8 mod 16 doubles: the face MMAs read two cells per k-step
+// (lanes q >> 1), which must land in different banks
+constexpr int kRow64 = 4 * kLS64 + 8;   // [cell][4 rows][kLS]
+constexpr int kFace64 = 8 * kLS64 + 8;  // [cell][8 rows][kLS]
+constexpr int kPlane64 = kPC64 * kRow64;
+constexpr size_t kProj64Smem =
+    (4 * (size_t)kPlane64 + std::max(kPC64 * kFace64, kPlane64 + kPC64 * 64)) * sizeof(double);
+constexpr int kProjBndBlocks = 32;  // partial slots of the boundary-face kernel
+
+template <int GROUP, bool HOIST>
+__device__ __forceinline__ void project64d_group(const ProjArgs& pa, const dlrsn_cellops& ops,
+                                                 double* sm, int t64) {
+  constexpr int C = kPC64, kLS = kLS64, kRow = kRow64;
+  constexpr int NS = GROUP == 0 ? 4 : 2;  // symmetric / skew outputs of the group
+  double* sX = sm;
+  double* sU = sm + kPlane64;        // group 0: face jumps
+  double* sXo = sm + kPlane64;       // group 1: X_old
+  double* sGX = sm + 2 * kPlane64;   // group 0
+  double* sMX = sm + 2 * kPlane64;   // group 1
+  double* sGY = sm + 3 * kPlane64;   // group 0
+  double* sMXt = sm + 3 * kPlane64;  // group 1
+  double* sF = sm + 4 * kPlane64;    // group 0: [C][kFace64]
+  double* sMXs = sm + 4 * kPlane64;  // group 1
+  double* sQ = sm + 5 * kPlane64;    // group 1: [C][64]
+  constexpr int kFace = kFace64;
+  __shared__ double so[64];
+  if (threadIdx.x < 16) {
+    so[threadIdx.x] = ops.mass[threadIdx.x];
+    so[16 + threadIdx.x] = ops.gx[threadIdx.x];
+    so[32 + threadIdx.x] = ops.gy[threadIdx.x];
+  } else if (threadIdx.x < 20) {
+    so[48 + threadIdx.x - 16] = 0.5 * ops.e2x[threadIdx.x - 16];
+    so[52 + threadIdx.x - 16] = 0.5 * ops.e2y[threadIdx.x - 16];
+    so[56 + threadIdx.x - 16] = ops.src_row[threadIdx.x - 16];
+  }
+  const double* e2x = so + 48;
+  const double* e2y = so + 52;
+  const int r = pa.r, nx = pa.nx, ny = pa.ny;
+  const bool no_ms = pa.sigma_s == nullptr || (pa.any_scat != nullptr && *pa.any_scat == 0);
+  const int ncell = nx * ny;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3, kk = q & 1, second = q >> 1;
+  const int col0 = 64 * t64;
+  const int rloc = min(64, r - col0);  // live columns of this block
+  const int c_begin = blockIdx.y * pa.cells_per_block;
+  const int c_end = min(ncell, c_begin + pa.cells_per_block);
+  // fragment list of this warp: rows a_lo (the first n_lo fragments) and
+  // a_hi = 7 - a_lo; 36 = 4 x (5 + 4)
+  const int pr = warp >> 1, odd = warp & 1;
+  const int a_lo = pr, a_hi = 7 - pr;
+  // even warp: row a_lo, columns a_lo .. a_lo + 4; odd warp: the rest of row
+  // a_lo (3 - pr fragments) and row a_hi (pr + 1 fragments)
+  // per fragment k: ob[k] = 8 b + g (its B column of this lane), bit k of lom
+  // = row a_lo (else a_hi), bit k of onm = live
+  int ob[5];
+  unsigned lom = 0, onm = 0;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    int a, b;
+    if (!odd) {
+      a = a_lo;
+      b = a_lo + k;
+    } else if (k < 3 - pr) {
+      a = a_lo;
+      b = a_lo + 5 + k;
+    } else {
+      a = a_hi;
+      b = a_hi + (k - (3 - pr));
+    }
+    const bool live = b < 8 && (odd ? k < 4 : true);
+    ob[k] = (live ? 8 * b : 0) + g;
+    if (a == a_lo) lom |= 1u << k;
+    if (live && 8 * b < rloc) onm |= 1u << k;
+  }
+  double acc[NS][5][2];
+#pragma unroll
+  for (int o = 0; o < NS; ++o)
+#pragma unroll
+    for (int k = 0; k < 5; ++k) acc[o][k][0] = acc[o][k][1] = 0.0;
+  double amo[GROUP == 1 ? 8 : 1][2];
+#pragma unroll
+  for (int b = 0; b < (GROUP == 1 ? 8 : 1); ++b) amo[b][0] = amo[b][1] = 0.0;
+  const bool mo_row = 8 * warp < rloc;
+  double qacc = 0.0;
+  const double* X = pa.X;
+  // staging item of this thread: cell scl of the chunk, column col0 + scol
+  const int scl = threadIdx.x >> 6, scol = threadIdx.x & 63;
+  const int gc = col0 + scol;
+  const bool c_ok = gc < r;
+  const int64_t rs = r;
+  struct Raw {
+    double x[4];
+    double y[4];  // group 0: left / below neighbour edge dofs; group 1: X_old
+    double qc, st, ss;
+  };
+  int fc = c_begin + scl;
+  int fci = fc % nx, fcj = fc / nx;
+  auto fetch = [&](int cc0, Raw& w) {
+    const int c = fc;
+    const int ci = fci, cj = fcj;
+    const bool live = cc0 < c_end && c < c_end;
+    const double* row = X + (int64_t)c * 4 * rs;
+    const bool v = live && c_ok;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) w.x[l] = v ? __ldg(row + l * rs + gc) : 0.0;
+    if constexpr (GROUP == 0) {
+      const bool lx = v && ci > 0, ly = v && (cj > 0 || pa.halo != nullptr);
+      const double* left = row - 4 * rs;
+      const double* below = cj > 0 ? row - (int64_t)4 * nx * rs
+                                   : (pa.halo ? pa.halo + (int64_t)ci * 4 * rs : nullptr);
+      w.y[0] = lx ? __ldg(left + 1 * rs + gc) : 0.0;
+      w.y[1] = lx ? __ldg(left + 3 * rs + gc) : 0.0;
+      w.y[2] = ly ? __ldg(below + 2 * rs + gc) : 0.0;
+      w.y[3] = ly ? __ldg(below + 3 * rs + gc) : 0.0;
+    } else {
+      const double* orow = pa.Xold ? pa.Xold + (int64_t)c * 4 * rs : nullptr;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) w.y[l] = (v && orow) ? __ldg(orow + l * rs + gc) : 0.0;
+      w.qc = live ? __ldg(pa.q + c) : 0.0;
+      w.st = live ? __ldg(pa.sigma_t + c) : 0.0;
+      w.ss = (live && !no_ms) ? __ldg(pa.sigma_s + c) : 0.0;
+    }
+    fc += C;
+    fci += C;
+    while (fci >= nx) {
+      fci -= nx;
+      ++fcj;
+    }
+  };
+  Raw cur;
+  fetch(c_begin, cur);
+  const int oa_lo = 8 * a_lo + g, oa_hi = 8 * a_hi + g;
+  for (int c0 = c_begin; c0 < c_end; c0 += C) {
+    const int nc = min(C, c_end - c0);
+    __syncthreads();  // the previous chunk's fragments are consumed
+    {
+      const int base = scl * kRow + scol;
+      const double* x = cur.x;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) sX[base + kLS * l] = x[l];
+      if constexpr (GROUP == 0) {
+        const double ux0 = cur.y[0] - x[0], ux1 = cur.y[1] - x[2];
+        const double vx0 = cur.y[0] + x[0], vx1 = cur.y[1] + x[2];
+        const double uy0 = cur.y[2] - x[0], uy1 = cur.y[3] - x[1];
+        const double vy0 = cur.y[2] + x[0], vy1 = cur.y[3] + x[1];
+        sU[base] = ux0;
+        sU[base + kLS] = ux1;
+        sU[base + 2 * kLS] = uy0;
+        sU[base + 3 * kLS] = uy1;
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+          double gx = 0.0, gy = 0.0;
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            gx = fma(so[16 + 4 * l + p], x[p], gx);
+            gy = fma(so[32 + 4 * l + p], x[p], gy);
+          }
+          sGX[base + kLS * l] = gx;
+          sGY[base + kLS * l] = gy;
+        }
+        double* f = sF + scl * kFace + scol;
+        f[0] = (e2x[0] * vx0 + e2x[1] * vx1);
+        f[kLS] = (e2x[2] * vx0 + e2x[3] * vx1);
+        f[2 * kLS] = (e2y[0] * vy0 + e2y[1] * vy1);
+        f[3 * kLS] = (e2y[2] * vy0 + e2y[3] * vy1);
+        f[4 * kLS] = (e2x[0] * ux0 + e2x[1] * ux1);
+        f[5 * kLS] = (e2x[2] * ux0 + e2x[3] * ux1);
+        f[6 * kLS] = (e2y[0] * uy0 + e2y[1] * uy1);
+        f[7 * kLS] = (e2y[2] * uy0 + e2y[3] * uy1);
+      } else {
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+          sXo[base + kLS * l] = cur.y[l];
+          double m = 0.0;
+#pragma unroll
+          for (int p = 0; p < 4; ++p) m = fma(so[4 * l + p], x[p], m);
+          sMX[base + kLS * l] = m;
+          sMXt[base + kLS * l] = cur.st * m;
+          if (!no_ms) sMXs[base + kLS * l] = cur.ss * m;
+        }
+        double sq = 0.0;
+#pragma unroll
+        for (int l = 0; l < 4; ++l) sq = fma(so[56 + l], x[l], sq);
+        sQ[scl * 64 + scol] = cur.qc * sq;  // q-hat (dlr_sn.py:70)
+      }
+    }
+    __syncthreads();
+    fetch(c0 + C, cur);  // next chunk's loads in flight during the MMAs
+    // ---- volume terms, every cell of the chunk
+#pragma unroll
+    for (int cl = 0; cl < C; ++cl) {
+      const double* xr = sX + cl * kRow + q * kLS;
+      const double xlo = xr[oa_lo], xhi = xr[oa_hi];
+      if constexpr (GROUP == 0) {
+        const double* gxr = sGX + cl * kRow + q * kLS;
+        const double* gyr = sGY + cl * kRow + q * kLS;
+        double bgx[5], bgy[5];  // HOIST: every operand load ahead of the MMAs
+        if constexpr (HOIST) {
+#pragma unroll
+          for (int k = 0; k < 5; ++k) {
+            bgx[k] = gxr[ob[k]];
+            bgy[k] = gyr[ob[k]];
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 5; ++k)
+          if ((onm >> k) & 1u) {
+            const double xa = ((lom >> k) & 1u) ? xlo : xhi;
+            dmma(acc[0][k][0], acc[0][k][1], xa, HOIST ? bgx[k] : gxr[ob[k]]);  // px (volume)
+            dmma(acc[1][k][0], acc[1][k][1], xa, HOIST ? bgy[k] : gyr[ob[k]]);  // py (volume)
+          }
+      } else {
+        const double* mtr = sMXt + cl * kRow + q * kLS;
+        const double* msr = sMXs + cl * kRow + q * kLS;
+        double bt[5], bs[5];
+        if constexpr (HOIST) {
+#pragma unroll
+          for (int k = 0; k < 5; ++k) {
+            bt[k] = mtr[ob[k]];
+            bs[k] = no_ms ? 0.0 : msr[ob[k]];
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 5; ++k)
+          if ((onm >> k) & 1u) {
+            const double xa = ((lom >> k) & 1u) ? xlo : xhi;
+            dmma(acc[0][k][0], acc[0][k][1], xa, HOIST ? bt[k] : mtr[ob[k]]);  // mt
+            if (!no_ms) dmma(acc[1][k][0], acc[1][k][1], xa, HOIST ? bs[k] : msr[ob[k]]);  // ms
+          }
+        const double xo = sXo[cl * kRow + q * kLS + 8 * warp + g];
+        const double* mr = sMX + cl * kRow + q * kLS + g;
+        if (mo_row) {
+#pragma unroll
+          for (int hb = 0; hb < 2; ++hb) {
+            double bm[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) bm[b] = mr[8 * (4 * hb + b)];
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              if (8 * (4 * hb + b) < rloc) dmma(amo[4 * hb + b][0], amo[4 * hb + b][1], xo, bm[b]);  // mo
+          }
+        }
+      }
+    }
+    if constexpr (GROUP == 0) {
+      // ---- face terms: k slot q -> cell 2 kp + q / 2, face dof q % 2
+#pragma unroll
+      for (int kp = 0; kp < C / 2; ++kp) {
+        const int cl = 2 * kp + second;
+        const double* ur = sU + cl * kRow;
+        const double uxlo = ur[kk * kLS + oa_lo], uxhi = ur[kk * kLS + oa_hi];
+        const double uylo = ur[(2 + kk) * kLS + oa_lo], uyhi = ur[(2 + kk) * kLS + oa_hi];
+        const double* f = sF + cl * kFace;
+        // two passes (x faces, then y faces): 10 operands in flight each
+#pragma unroll
+        for (int ax = 0; ax < 2; ++ax) {
+          double f0[5], f1[5];
+          if constexpr (HOIST) {
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+              f0[k] = f[(2 * ax + kk) * kLS + ob[k]];
+              f1[k] = f[(4 + 2 * ax + kk) * kLS + ob[k]];
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 5; ++k)
+            if ((onm >> k) & 1u) {
+              const bool lo = (lom >> k) & 1u;
+              const double ua = ax == 0 ? (lo ? uxlo : uxhi) : (lo ? uylo : uyhi);
+              dmma(acc[ax][k][0], acc[ax][k][1], ua,
+                   HOIST ? f0[k] : f[(2 * ax + kk) * kLS + ob[k]]);  // px / py (faces)
+              dmma(acc[2 + ax][k][0], acc[2 + ax][k][1], ua,
+                   HOIST ? f1[k] : f[(4 + 2 * ax + kk) * kLS + ob[k]]);  // jx / jy
+            }
+        }
+      }
+    } else {
+      if (threadIdx.x < 64)
+        for (int cl = 0; cl < nc; ++cl) qacc += sQ[cl * 64 + threadIdx.x];
+    }
+  }
+  const int64_t stride = 7 * (int64_t)r * r + r;
+  double* out = pa.part + (int64_t)blockIdx.y * stride;
+  // (the right / top domain-boundary faces of the diagonal blocks are added
+  // by project_bnd64_kernel into partial slots of their own)
+#pragma unroll
+  for (int o = 0; o < NS; ++o)
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      if (!((onm >> k) & 1u)) continue;
+      const int i = col0 + (((lom >> k) & 1u) ? oa_lo : oa_hi);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = col0 + (ob[k] - g) + 2 * q + h;
+        if (i >= r || j >= r) continue;
+        const int slot = GROUP == 0 ? o : 4 + o;  // px py jx jy | mt ms
+        out[(int64_t)slot * r * r + (int64_t)i * r + j] = acc[o][k][h];
+      }
+    }
+  if constexpr (GROUP == 1) {
+    if (mo_row) {
+      const int i = col0 + 8 * warp + g;
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int j = col0 + 8 * b + 2 * q + h;
+          if (i < r && j < r) out[6 * (int64_t)r * r + (int64_t)i * r + j] = amo[b][h];
+        }
+    }
+    if (threadIdx.x < 64 && col0 + (int)threadIdx.x < r)
+      out[7 * (int64_t)r * r + col0 + threadIdx.x] = qacc;
+  }
+}
+
+// Right / top domain-boundary faces of the diagonal 64-blocks (own right /
+// top edge against a zero exterior): X_e^T (1/2 e2) X_e per boundary cell,
+// added to px, jx (right wall) and py, jy (top wall).  The boundary cells
+// (ny right-wall cells, then nx top-wall cells when top_wall) are split over
+// gridDim.x CTAs, each writing one partial slot (slot_base + blockIdx.x).
+__global__ void __launch_bounds__(256) project_bnd64_kernel(ProjArgs pa, dlrsn_cellops ops,
+                                                            int nb64, int slot_base) {
+  __shared__ double sa[2][64];
+  const int r = pa.r, nx = pa.nx, ny = pa.ny;
+  const int nright = ny, ntop = pa.top_wall ? nx : 0, total = nright + ntop;
+  const int per = (total + gridDim.x - 1) / gridDim.x;
+  const int b0 = blockIdx.x * per, b1 = min(total, b0 + per);
+  const int64_t stride = 7 * (int64_t)r * r + r;
+  double* out = pa.part + (int64_t)(slot_base + blockIdx.x) * stride;
+  for (int blk = 0; blk < nb64; ++blk) {
+    const int col0 = 64 * blk;
+    double ax[16], ay[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) ax[e] = ay[e] = 0.0;
+    for (int bc = b0; bc < b1; ++bc) {
+      const bool right = bc < nright;
+      const int c = right ? bc * nx + nx - 1 : (ny - 1) * nx + (bc - nright);
+      const int d0 = right ? 1 : 2;  // edge dofs: right (1, 3), top (2, 3)
+      __syncthreads();
+      if (threadIdx.x < 128) {
+        const int w = threadIdx.x >> 6, col = col0 + (threadIdx.x & 63);
+        sa[w][threadIdx.x & 63] = ldx(pa.X, r, (int64_t)c * 4 + (w ? 3 : d0), col);
+      }
+      __syncthreads();
+      const double* e2 = right ? ops.e2x : ops.e2y;
+      const double e00 = 0.5 * e2[0], e01 = 0.5 * e2[1], e10 = 0.5 * e2[2], e11 = 0.5 * e2[3];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int idx = threadIdx.x + 256 * e, i = idx >> 6, j = idx & 63;
+        const double v = sa[0][i] * (e00 * sa[0][j] + e01 * sa[1][j]) +
+                         sa[1][i] * (e10 * sa[0][j] + e11 * sa[1][j]);
+        if (right) ax[e] += v;
+        else ay[e] += v;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int idx = threadIdx.x + 256 * e, i = col0 + (idx >> 6), j = col0 + (idx & 63);
+      if (i >= r || j >= r) continue;
+      const int64_t o = (int64_t)i * r + j;
+      out[o] = ax[e];                           // px
+      out[2 * (int64_t)r * r + o] = ax[e];      // jx
+      out[(int64_t)r * r + o] = ay[e];          // py
+      out[3 * (int64_t)r * r + o] = ay[e];      // jy
+    }
+  }
+}
+
 // The (group, tile) work list of one cell block.  px, py are skew- and jx,
 // jy, mt, ms symmetric (X^T A X with A = -A^T or A = A^T: Px, Py skew, Jx,
 // Jy, M_sigma symmetric, transport_sn.py:246-282), so only the tiles on and
 // above the diagonal are computed for them and the reduced result is
 // mirrored (mirror_tiles_kernel); mo = X_old^T M X has no symmetry, so the
-// tiles below the diagonal run group 1 in mo-only mode.  Entry = group
-// (0 / 1 / 2 = mo only) | ti << 2 | tj << 5.
+// tiles below the diagonal run group 1 in mo-only mode.  With diagonal
+// 64-column blocks (project64d_group, r > 32) the diagonal blocks are one
+// CTA per group and only the off-diagonal 64-blocks use 32 x 32 tiles.
+// CTA per group (project_mma64d_kernel) and only the off-diagonal 64-blocks
+// are in this list.  Entry = kind (0 / 1 = group, 2 = mo only) | ti << 3 | tj << 5.
 struct ProjTiles {
   int n;
   unsigned char e[64];
@@ -1922,23 +2307,51 @@ __global__ void __launch_bounds__(256, 2) project_mma32g_kernel(ProjArgs pa, dlr
                                                                  ProjTiles tl) {
   extern __shared__ __align__(16) double sm32g[];
   const int e = tl.e[blockIdx.x];
-  const int grp = e & 3, ti = (e >> 2) & 7, tj = (e >> 5) & 7;
+  const int grp = e & 7, ti = (e >> 3) & 3, tj = (e >> 5) & 3;
   if (grp == 0)
     project32_group<0>(pa, ops, sm32g, ti, tj, false);
   else
     project32_group<1>(pa, ops, sm32g, ti, tj, grp == 2);
 }
 
+// the diagonal 64-column blocks: grid (2 x blocks, cell blocks), group =
+// blockIdx.x & 1 (the two groups of a cell block are adjacent: shared X rows)
+// seq = 1: grid (1, cell ranges), every CTA runs both groups of every
+// diagonal block on its range one after the other -- identical work per
+// CTA, so 2 x SM-count equal ranges are balanced without a tail
+template <bool HOIST>
+__global__ void __launch_bounds__(256, 2) project_mma64d_kernel(ProjArgs pa, dlrsn_cellops ops,
+                                                                 int nb64, int seq) {
+  extern __shared__ __align__(16) double sm64d[];
+  if (seq) {
+    for (int b = 0; b < nb64; ++b) {
+      project64d_group<0, HOIST>(pa, ops, sm64d, b);
+      __syncthreads();
+      project64d_group<1, HOIST>(pa, ops, sm64d, b);
+      __syncthreads();
+    }
+    return;
+  }
+  if ((blockIdx.x & 1) == 0)
+    project64d_group<0, HOIST>(pa, ops, sm64d, blockIdx.x >> 1);
+  else
+    project64d_group<1, HOIST>(pa, ops, sm64d, blockIdx.x >> 1);
+}
+
 // out[o][i][j] = s_o out[o][j][i] below the diagonal tiles (o < 6; s = -1
 // for the skew px, py)
-__global__ void mirror_tiles_kernel(int r, double* __restrict__ out) {
+__global__ void mirror_tiles_kernel(int r, double* __restrict__ out, int d64) {
   const int64_t total = 6 * (int64_t)r * r;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int o = (int)(e / ((int64_t)r * r));
     const int rem = (int)(e - (int64_t)o * r * r);
     const int i = rem / r, j = rem % r;
-    if (i / kT32 <= j / kT32) continue;
+    // computed: 32 x 32 tiles on / above the diagonal; with diagonal 64-blocks
+    // the 8 x 8 fragments on / above the diagonal inside them
+    const bool low = d64 ? ((i >> 6) > (j >> 6) || ((i >> 6) == (j >> 6) && (i >> 3) > (j >> 3)))
+                         : (i / kT32 > j / kT32);
+    if (!low) continue;
     const double v = out[(int64_t)o * r * r + (int64_t)j * r + i];
     out[e] = o < 2 ? -v : v;
   }
@@ -3461,9 +3874,55 @@ static int cells_per_block(int ncell, int tiles) {
 
 // cells per block of project_mma32g_kernel: about 4 waves of 2 CTAs per SM
 // over all 32x32 output tiles and both output groups, whole chunks
-static int project32g_cells_per_block(int ncell, int r) {
+// diagonal 64-column blocks (project64d_group) for r > 32 (DLRSN_K3_D64=0: the
+// 32 x 32 tiling everywhere)
+static bool project_d64(int r) {
+  static const bool on = [] {
+    const char* e = getenv("DLRSN_K3_D64");
+    return !(e && e[0] == '0');
+  }();
+  return on && r > kT32;
+}
+
+// the work list of one cell block (see ProjTiles)
+static ProjTiles project_tiles(int r, bool sym) {
+  ProjTiles tl;
+  tl.n = 0;
   const int T = (r + kT32 - 1) / kT32;
-  const int work = T * (T + 1) + T * (T - 1) / 2;  // CTAs per cell block (work list)
+  const bool d64 = sym && project_d64(r);
+  auto add = [&](int kind, int ti, int tj) {
+    tl.e[tl.n++] = (unsigned char)(kind | ti << 3 | tj << 5);
+  };
+  for (int ti = 0; ti < T; ++ti)
+    for (int tj = 0; tj < T; ++tj) {
+      if (d64 && ti / 2 == tj / 2) continue;  // inside a diagonal 64-block
+      if (!sym || ti <= tj) {
+        add(0, ti, tj);
+        add(1, ti, tj);
+      } else {
+        add(2, ti, tj);
+      }
+    }
+  return tl;
+}
+
+static int project32g_cells_per_block(int ncell, int r) {
+  static const char* sym_env = getenv("DLRSN_PROJECT_SYM");
+  const bool sym = !(sym_env && sym_env[0] == '0');
+  const bool d64 = sym && project_d64(r);
+  // CTAs per cell block (the work list, plus the diagonal 64-block CTAs)
+  const int work = project_tiles(r, sym).n + (d64 ? 2 * ((r + 63) / 64) : 0);
+  if (d64) {
+    // diagonal 64-blocks: every cell costs the same, so one cell range per
+    // SM (the two group CTAs of a range share an SM and its X rows) is
+    // balanced without a tail and needs only 148 partial slots
+    (void)work;
+    static const int nr = getenv("DLRSN_K3_RANGES") ? atoi(getenv("DLRSN_K3_RANGES")) : 296;
+    const int target = nr;
+    int cpb = (ncell + target - 1) / target;
+    cpb = (cpb + kPCG - 1) / kPCG * kPCG;
+    return cpb < kPCG ? kPCG : cpb;
+  }
   // ~16 waves: the CTAs of one cell block finish close together and share
   // its X rows through L2 (C4: 10.0 -> 9.5 ms; 4 waves re-read X 3x from DRAM)
   static const int waves = getenv("DLRSN_K3_WAVES") ? atoi(getenv("DLRSN_K3_WAVES")) : 16;
@@ -3544,6 +4003,7 @@ int64_t dlrsn_partials_len(int ncell, int ra, int rb, int kind) {
   const int cpbg = project32g_cells_per_block(ncell, ra);
   const int64_t nblkg = (ncell + cpbg - 1) / cpbg;
   if (nblkg > nblk) nblk = nblkg;
+  nblk += kProjBndBlocks;  // the boundary-face slots of the diagonal 64-block path
   return nblk * (7 * (int64_t)ra * ra + ra);
 }
 
@@ -3726,6 +4186,12 @@ int project_ex(const dlrsn_cellops* ops, int r, const double* X, const double* X
         DLRSN_TRY_CUDA(cudaFuncSetAttribute(project_mma32g_kernel,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)kProj32SmemG));
+        DLRSN_TRY_CUDA(cudaFuncSetAttribute(project_mma64d_kernel<true>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)kProj64Smem));
+        DLRSN_TRY_CUDA(cudaFuncSetAttribute(project_mma64d_kernel<false>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)kProj64Smem));
         attr = true;
       }
       // both output groups in one grid (z = group); cell blocks of about
@@ -3733,30 +4199,40 @@ int project_ex(const dlrsn_cellops* ops, int r, const double* X, const double* X
       const int cpbg = project32g_cells_per_block(ncell, r);
       const int nblkg = (ncell + cpbg - 1) / cpbg;
       pa.cells_per_block = cpbg;
-      DLRSN_TRY_CUDA(zero_async(partial, sizeof(double) * (size_t)nblkg * (7 * (size_t)r * r + r), st));
+      DLRSN_TRY_CUDA(zero_async(partial,
+                                sizeof(double) * (size_t)(nblkg + kProjBndBlocks) * (7 * (size_t)r * r + r),
+                                st));
       static const char* sym_env = getenv("DLRSN_PROJECT_SYM");
       const bool sym = !(sym_env && sym_env[0] == '0');
       const int T = (r + kT32 - 1) / kT32;
-      ProjTiles tl;
-      tl.n = 0;
-      for (int ti = 0; ti < T; ++ti)
-        for (int tj = 0; tj < T; ++tj) {
-          if (!sym || ti <= tj) {
-            tl.e[tl.n++] = (unsigned char)(0 | ti << 2 | tj << 5);
-            tl.e[tl.n++] = (unsigned char)(1 | ti << 2 | tj << 5);
-          } else {
-            tl.e[tl.n++] = (unsigned char)(2 | ti << 2 | tj << 5);
-          }
-        }
+      const ProjTiles tl = project_tiles(r, sym);
+      const bool d64 = sym && project_d64(r);
       if (tm) DLRSN_TRY_CUDA(cudaEventRecord(tm->first, st));
-      project_mma32g_kernel<<<dim3(tl.n, nblkg), 256, kProj32SmemG, st>>>(pa, *ops, tl);
-      DLRSN_CHECK_LAUNCH("project_mma32g_kernel");
+      int nslots = nblkg;
+      if (d64) {
+        static const bool hoist = getenv("DLRSN_K3_HOIST") && getenv("DLRSN_K3_HOIST")[0] == '1';
+        static const bool seq = !(getenv("DLRSN_K3_SEQ") && getenv("DLRSN_K3_SEQ")[0] == '0');
+        const int nb64 = (r + 63) / 64;
+        const dim3 g64(seq ? 1 : 2 * nb64, nblkg);
+        if (hoist)
+          project_mma64d_kernel<true><<<g64, 256, kProj64Smem, st>>>(pa, *ops, nb64, seq ? 1 : 0);
+        else
+          project_mma64d_kernel<false><<<g64, 256, kProj64Smem, st>>>(pa, *ops, nb64, seq ? 1 : 0);
+        DLRSN_CHECK_LAUNCH("project_mma64d_kernel");
+        project_bnd64_kernel<<<kProjBndBlocks, 256, 0, st>>>(pa, *ops, (r + 63) / 64, nblkg);
+        DLRSN_CHECK_LAUNCH("project_bnd64_kernel");
+        nslots += kProjBndBlocks;
+      }
+      if (tl.n > 0) {
+        project_mma32g_kernel<<<dim3(tl.n, nblkg), 256, kProj32SmemG, st>>>(pa, *ops, tl);
+        DLRSN_CHECK_LAUNCH("project_mma32g_kernel");
+      }
       if (tm) DLRSN_TRY_CUDA(cudaEventRecord(tm->second, st));
       reduce_partials_kernel<<<(unsigned)((7 * (int64_t)r * r + r + 31) / 32), 1024, 0, st>>>(
-          nblkg, 7 * (int64_t)r * r + r, partial, out, 1.0);
+          nslots, 7 * (int64_t)r * r + r, partial, out, 1.0);
       DLRSN_CHECK_LAUNCH("reduce_partials_kernel");
       if (sym && T > 1) {
-        mirror_tiles_kernel<<<(unsigned)((6 * r * r + 255) / 256), 256, 0, st>>>(r, out);
+        mirror_tiles_kernel<<<(unsigned)((6 * r * r + 255) / 256), 256, 0, st>>>(r, out, d64 ? 1 : 0);
         DLRSN_CHECK_LAUNCH("mirror_tiles_kernel");
       }
       return DLRSN_OK;
