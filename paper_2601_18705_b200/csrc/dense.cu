@@ -1926,6 +1926,119 @@ constexpr size_t kProj64Smem =
     (4 * (size_t)kPlane64 + std::max(kPC64 * kFace64, kPlane64 + kPC64 * 64)) * sizeof(double);
 constexpr int kProjBndBlocks = 32;  // partial slots of the boundary-face kernel
 
+// the MMAs of one staged chunk: NF = fragments of this warp (5 even / 4 odd
+// warps), EVEN = every fragment in row a_lo (no operand select), PRED = per
+// fragment liveness tests (ragged last block, r % 64 != 0)
+template <int GROUP, bool HOIST, int NF, bool EVEN, bool PRED>
+__device__ __forceinline__ void d64_mma(double (&acc)[GROUP == 0 ? 4 : 2][5][2],
+                                        double (&amo)[GROUP == 1 ? 8 : 1][2], const double* sm,
+                                        int q, int g, int warp, int oa_lo, int oa_hi,
+                                        const int (&ob)[5], unsigned lom, unsigned onm, bool no_ms,
+                                        bool mo_row, int rloc) {
+  constexpr int C = kPC64, kLS = kLS64, kRow = kRow64, kFace = kFace64;
+  const double* sX = sm;
+  const double* sU = sm + kPlane64;
+  const double* sXo = sm + kPlane64;
+  const double* sGX = sm + 2 * kPlane64;
+  const double* sMX = sm + 2 * kPlane64;
+  const double* sGY = sm + 3 * kPlane64;
+  const double* sMXt = sm + 3 * kPlane64;
+  const double* sF = sm + 4 * kPlane64;
+  const double* sMXs = sm + 4 * kPlane64;
+  const int kk = q & 1, second = q >> 1;
+  (void)sU; (void)sXo; (void)sGX; (void)sMX; (void)sGY; (void)sMXt; (void)sF; (void)sMXs;
+  (void)kk; (void)second; (void)warp; (void)mo_row; (void)rloc; (void)no_ms; (void)amo;
+    // ---- volume terms, every cell of the chunk
+#pragma unroll
+    for (int cl = 0; cl < C; ++cl) {
+      const double* xr = sX + cl * kRow + q * kLS;
+      const double xlo = xr[oa_lo], xhi = xr[oa_hi];
+      if constexpr (GROUP == 0) {
+        const double* gxr = sGX + cl * kRow + q * kLS;
+        const double* gyr = sGY + cl * kRow + q * kLS;
+        double bgx[5], bgy[5];  // HOIST: every operand load ahead of the MMAs
+        if constexpr (HOIST) {
+#pragma unroll
+          for (int k = 0; k < NF; ++k) {
+            bgx[k] = gxr[ob[k]];
+            bgy[k] = gyr[ob[k]];
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < NF; ++k)
+          if (!PRED || ((onm >> k) & 1u)) {
+            const double xa = (EVEN || ((lom >> k) & 1u)) ? xlo : xhi;
+            dmma(acc[0][k][0], acc[0][k][1], xa, HOIST ? bgx[k] : gxr[ob[k]]);  // px (volume)
+            dmma(acc[1][k][0], acc[1][k][1], xa, HOIST ? bgy[k] : gyr[ob[k]]);  // py (volume)
+          }
+      } else {
+        const double* mtr = sMXt + cl * kRow + q * kLS;
+        const double* msr = sMXs + cl * kRow + q * kLS;
+        double bt[5], bs[5];
+        if constexpr (HOIST) {
+#pragma unroll
+          for (int k = 0; k < NF; ++k) {
+            bt[k] = mtr[ob[k]];
+            bs[k] = no_ms ? 0.0 : msr[ob[k]];
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < NF; ++k)
+          if (!PRED || ((onm >> k) & 1u)) {
+            const double xa = (EVEN || ((lom >> k) & 1u)) ? xlo : xhi;
+            dmma(acc[0][k][0], acc[0][k][1], xa, HOIST ? bt[k] : mtr[ob[k]]);  // mt
+            if (!no_ms) dmma(acc[1][k][0], acc[1][k][1], xa, HOIST ? bs[k] : msr[ob[k]]);  // ms
+          }
+        const double xo = sXo[cl * kRow + q * kLS + 8 * warp + g];
+        const double* mr = sMX + cl * kRow + q * kLS + g;
+        if (mo_row) {
+#pragma unroll
+          for (int hb = 0; hb < 2; ++hb) {
+            double bm[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) bm[b] = mr[8 * (4 * hb + b)];
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              if (!PRED || 8 * (4 * hb + b) < rloc) dmma(amo[4 * hb + b][0], amo[4 * hb + b][1], xo, bm[b]);  // mo
+          }
+        }
+      }
+    }
+    if constexpr (GROUP == 0) {
+      // ---- face terms: k slot q -> cell 2 kp + q / 2, face dof q % 2
+#pragma unroll
+      for (int kp = 0; kp < C / 2; ++kp) {
+        const int cl = 2 * kp + second;
+        const double* ur = sU + cl * kRow;
+        const double uxlo = ur[kk * kLS + oa_lo], uxhi = ur[kk * kLS + oa_hi];
+        const double uylo = ur[(2 + kk) * kLS + oa_lo], uyhi = ur[(2 + kk) * kLS + oa_hi];
+        const double* f = sF + cl * kFace;
+        // two passes (x faces, then y faces): 10 operands in flight each
+#pragma unroll
+        for (int ax = 0; ax < 2; ++ax) {
+          double f0[5], f1[5];
+          if constexpr (HOIST) {
+#pragma unroll
+            for (int k = 0; k < NF; ++k) {
+              f0[k] = f[(2 * ax + kk) * kLS + ob[k]];
+              f1[k] = f[(4 + 2 * ax + kk) * kLS + ob[k]];
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < NF; ++k)
+            if (!PRED || ((onm >> k) & 1u)) {
+              const bool lo = EVEN || ((lom >> k) & 1u);
+              const double ua = ax == 0 ? (lo ? uxlo : uxhi) : (lo ? uylo : uyhi);
+              dmma(acc[ax][k][0], acc[ax][k][1], ua,
+                   HOIST ? f0[k] : f[(2 * ax + kk) * kLS + ob[k]]);  // px / py (faces)
+              dmma(acc[2 + ax][k][0], acc[2 + ax][k][1], ua,
+                   HOIST ? f1[k] : f[(4 + 2 * ax + kk) * kLS + ob[k]]);  // jx / jy
+            }
+        }
+      }
+    }
+}
+
 template <int GROUP, bool HOIST>
 __device__ __forceinline__ void project64d_group(const ProjArgs& pa, const dlrsn_cellops& ops,
                                                  double* sm, int t64) {
@@ -1958,7 +2071,7 @@ __device__ __forceinline__ void project64d_group(const ProjArgs& pa, const dlrsn
   const bool no_ms = pa.sigma_s == nullptr || (pa.any_scat != nullptr && *pa.any_scat == 0);
   const int ncell = nx * ny;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, q = lane & 3, kk = q & 1, second = q >> 1;
+  const int g = lane >> 2, q = lane & 3;
   const int col0 = 64 * t64;
   const int rloc = min(64, r - col0);  // live columns of this block
   const int c_begin = blockIdx.y * pa.cells_per_block;
@@ -2105,98 +2218,23 @@ __device__ __forceinline__ void project64d_group(const ProjArgs& pa, const dlrsn
     }
     __syncthreads();
     fetch(c0 + C, cur);  // next chunk's loads in flight during the MMAs
-    // ---- volume terms, every cell of the chunk
-#pragma unroll
-    for (int cl = 0; cl < C; ++cl) {
-      const double* xr = sX + cl * kRow + q * kLS;
-      const double xlo = xr[oa_lo], xhi = xr[oa_hi];
-      if constexpr (GROUP == 0) {
-        const double* gxr = sGX + cl * kRow + q * kLS;
-        const double* gyr = sGY + cl * kRow + q * kLS;
-        double bgx[5], bgy[5];  // HOIST: every operand load ahead of the MMAs
-        if constexpr (HOIST) {
-#pragma unroll
-          for (int k = 0; k < 5; ++k) {
-            bgx[k] = gxr[ob[k]];
-            bgy[k] = gyr[ob[k]];
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < 5; ++k)
-          if ((onm >> k) & 1u) {
-            const double xa = ((lom >> k) & 1u) ? xlo : xhi;
-            dmma(acc[0][k][0], acc[0][k][1], xa, HOIST ? bgx[k] : gxr[ob[k]]);  // px (volume)
-            dmma(acc[1][k][0], acc[1][k][1], xa, HOIST ? bgy[k] : gyr[ob[k]]);  // py (volume)
-          }
-      } else {
-        const double* mtr = sMXt + cl * kRow + q * kLS;
-        const double* msr = sMXs + cl * kRow + q * kLS;
-        double bt[5], bs[5];
-        if constexpr (HOIST) {
-#pragma unroll
-          for (int k = 0; k < 5; ++k) {
-            bt[k] = mtr[ob[k]];
-            bs[k] = no_ms ? 0.0 : msr[ob[k]];
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < 5; ++k)
-          if ((onm >> k) & 1u) {
-            const double xa = ((lom >> k) & 1u) ? xlo : xhi;
-            dmma(acc[0][k][0], acc[0][k][1], xa, HOIST ? bt[k] : mtr[ob[k]]);  // mt
-            if (!no_ms) dmma(acc[1][k][0], acc[1][k][1], xa, HOIST ? bs[k] : msr[ob[k]]);  // ms
-          }
-        const double xo = sXo[cl * kRow + q * kLS + 8 * warp + g];
-        const double* mr = sMX + cl * kRow + q * kLS + g;
-        if (mo_row) {
-#pragma unroll
-          for (int hb = 0; hb < 2; ++hb) {
-            double bm[4];
-#pragma unroll
-            for (int b = 0; b < 4; ++b) bm[b] = mr[8 * (4 * hb + b)];
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-              if (8 * (4 * hb + b) < rloc) dmma(amo[4 * hb + b][0], amo[4 * hb + b][1], xo, bm[b]);  // mo
-          }
-        }
-      }
-    }
-    if constexpr (GROUP == 0) {
-      // ---- face terms: k slot q -> cell 2 kp + q / 2, face dof q % 2
-#pragma unroll
-      for (int kp = 0; kp < C / 2; ++kp) {
-        const int cl = 2 * kp + second;
-        const double* ur = sU + cl * kRow;
-        const double uxlo = ur[kk * kLS + oa_lo], uxhi = ur[kk * kLS + oa_hi];
-        const double uylo = ur[(2 + kk) * kLS + oa_lo], uyhi = ur[(2 + kk) * kLS + oa_hi];
-        const double* f = sF + cl * kFace;
-        // two passes (x faces, then y faces): 10 operands in flight each
-#pragma unroll
-        for (int ax = 0; ax < 2; ++ax) {
-          double f0[5], f1[5];
-          if constexpr (HOIST) {
-#pragma unroll
-            for (int k = 0; k < 5; ++k) {
-              f0[k] = f[(2 * ax + kk) * kLS + ob[k]];
-              f1[k] = f[(4 + 2 * ax + kk) * kLS + ob[k]];
-            }
-          }
-#pragma unroll
-          for (int k = 0; k < 5; ++k)
-            if ((onm >> k) & 1u) {
-              const bool lo = (lom >> k) & 1u;
-              const double ua = ax == 0 ? (lo ? uxlo : uxhi) : (lo ? uylo : uyhi);
-              dmma(acc[ax][k][0], acc[ax][k][1], ua,
-                   HOIST ? f0[k] : f[(2 * ax + kk) * kLS + ob[k]]);  // px / py (faces)
-              dmma(acc[2 + ax][k][0], acc[2 + ax][k][1], ua,
-                   HOIST ? f1[k] : f[(4 + 2 * ax + kk) * kLS + ob[k]]);  // jx / jy
-            }
-        }
-      }
+    // ---- the chunk's MMAs (volume terms of every cell, then the faces)
+    if (rloc == 64) {
+      if (!odd)
+        d64_mma<GROUP, HOIST, 5, true, false>(acc, amo, sm, q, g, warp, oa_lo, oa_hi, ob, lom, onm,
+                                              no_ms, mo_row, rloc);
+      else
+        d64_mma<GROUP, HOIST, 4, false, false>(acc, amo, sm, q, g, warp, oa_lo, oa_hi, ob, lom, onm,
+                                               no_ms, mo_row, rloc);
     } else {
+      d64_mma<GROUP, HOIST, 5, false, true>(acc, amo, sm, q, g, warp, oa_lo, oa_hi, ob, lom, onm,
+                                            no_ms, mo_row, rloc);
+    }
+    if constexpr (GROUP == 1) {
       if (threadIdx.x < 64)
         for (int cl = 0; cl < nc; ++cl) qacc += sQ[cl * 64 + threadIdx.x];
     }
+
   }
   const int64_t stride = 7 * (int64_t)r * r + r;
   double* out = pa.part + (int64_t)blockIdx.y * stride;
@@ -2323,19 +2361,13 @@ template <bool HOIST>
 __global__ void __launch_bounds__(256, 2) project_mma64d_kernel(ProjArgs pa, dlrsn_cellops ops,
                                                                  int nb64, int seq) {
   extern __shared__ __align__(16) double sm64d[];
-  if (seq) {
-    for (int b = 0; b < nb64; ++b) {
-      project64d_group<0, HOIST>(pa, ops, sm64d, b);
-      __syncthreads();
-      project64d_group<1, HOIST>(pa, ops, sm64d, b);
-      __syncthreads();
-    }
-    return;
+  (void)seq;
+  for (int b = 0; b < nb64; ++b) {
+    project64d_group<0, HOIST>(pa, ops, sm64d, b);
+    __syncthreads();
+    project64d_group<1, HOIST>(pa, ops, sm64d, b);
+    __syncthreads();
   }
-  if ((blockIdx.x & 1) == 0)
-    project64d_group<0, HOIST>(pa, ops, sm64d, blockIdx.x >> 1);
-  else
-    project64d_group<1, HOIST>(pa, ops, sm64d, blockIdx.x >> 1);
 }
 
 // out[o][i][j] = s_o out[o][j][i] below the diagonal tiles (o < 6; s = -1
@@ -4211,9 +4243,9 @@ int project_ex(const dlrsn_cellops* ops, int r, const double* X, const double* X
       int nslots = nblkg;
       if (d64) {
         static const bool hoist = getenv("DLRSN_K3_HOIST") && getenv("DLRSN_K3_HOIST")[0] == '1';
-        static const bool seq = !(getenv("DLRSN_K3_SEQ") && getenv("DLRSN_K3_SEQ")[0] == '0');
+        const bool seq = true;
         const int nb64 = (r + 63) / 64;
-        const dim3 g64(seq ? 1 : 2 * nb64, nblkg);
+        const dim3 g64(1, nblkg);
         if (hoist)
           project_mma64d_kernel<true><<<g64, 256, kProj64Smem, st>>>(pa, *ops, nb64, seq ? 1 : 0);
         else
