@@ -538,6 +538,15 @@ def main(argv=None):
     k3_flop = K3_OUTPUTS * 2.0 * n_x * r * r
     k3_ms = float(np.mean(proj_ms)) if proj_ms else float("nan")
     k3_tf = k3_flop / (k3_ms * 1e-3) / 1e12
+    # flops the kernel executes: the skew (px, py) and symmetric (jx, jy, mt,
+    # ms) outputs are computed on / above the diagonal only -- 40 of 64 8x8
+    # fragment slots inside a diagonal 64-column block (the 36 on / above the
+    # diagonal + 4 slots of the warps' 5-fragment patterns), whole blocks above it
+    nb64 = (r + 63) // 64
+    if r > 32:
+        k3_exec = (nb64 * (6 * 40 + 64) + nb64 * (nb64 - 1) // 2 * (7 * 64 + 64)) / (7 * 64 * nb64 ** 2)
+    else:
+        k3_exec = 1.0
     n_loc = r if comm is None else len(range(comm.rank, r, comm.world_size))
     sweep_bytes = spec.n_cells * (n_loc * SWEEP_BYTES_PER_CELL_ANGLE + SWEEP_BYTES_PER_CELL)
     sweep_real_ms = float(np.sum(sweep_ms)) / max(1, sum(r_iters))  # speculative no-ops excluded
@@ -546,7 +555,14 @@ def main(argv=None):
     roofline = {
         "bound": "tensor", "achieved": k3_tf, "peak": peak_fp64, "unit": "TFLOP/s",
         "frac": k3_tf / peak_fp64, "traffic": traffic.get("k3"),
-        "kernel": "project_mma32g_kernel (K3: 7 reduced operators, DMMA m8n8k4 f64)",
+        "kernel": "project_mma64d_kernel (K3: 7 reduced operators on diagonal 64-column blocks, "
+                  "DMMA m8n8k4 f64)",
+        "executed_frac_of_alg": k3_exec,
+        "executed_tflops": k3_tf * k3_exec,
+        "executed_frac_of_peak": k3_tf * k3_exec / peak_fp64,
+        "note": "achieved / frac use the dense-equivalent count 7 x 2 N_x r^2 (SURVEY 8d); the "
+                "kernel skips the mirrored halves of the skew / symmetric outputs, so it executes "
+                "executed_frac_of_alg of those flops (executed_frac_of_peak = DMMA pipe share)",
         "peak_kind": "fp64 tensor, measured in this run (max of DMMA probe, cuBLAS DGEMM)",
         "peak_detail": fp64_detail, "launch_ms": k3_ms,
         "alg_flop_per_launch": k3_flop, "flop_formula": "7 x 2 N_x r^2",

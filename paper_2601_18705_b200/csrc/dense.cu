@@ -1926,14 +1926,29 @@ constexpr size_t kProj64Smem =
     (4 * (size_t)kPlane64 + std::max(kPC64 * kFace64, kPlane64 + kPC64 * 64)) * sizeof(double);
 constexpr int kProjBndBlocks = 32;  // partial slots of the boundary-face kernel
 
-// the MMAs of one staged chunk: NF = fragments of this warp (5 even / 4 odd
-// warps), EVEN = every fragment in row a_lo (no operand select), PRED = per
-// fragment liveness tests (ragged last block, r % 64 != 0)
-template <int GROUP, bool HOIST, int NF, bool EVEN, bool PRED>
+// Fragment pattern of a warp on a diagonal 64-block: rows (a0, a1) x columns
+// (b0, b1, b2) of the 8 x 8 fragment grid without the corner (a1, b0):
+//   k = 0 (a0, b0)   1 (a0, b1)   2 (a1, b1)   3 (a0, b2)   4 (a1, b2)
+// so 2 A and 3 B operands feed 5 MMAs.  The 8 warps' patterns below cover
+// the 36 fragments on / above the diagonal exactly once; 4 of the 40 slots
+// fall below the diagonal (computed anyway: valid values the mirror pass
+// overwrites).  Found by exhaustive search (K3).
+__constant__ unsigned char kD64Pat[8][5] = {
+    {0, 1, 0, 1, 2}, {0, 1, 3, 4, 5}, {1, 0, 3, 6, 7}, {2, 3, 2, 3, 5},
+    {2, 5, 6, 4, 7}, {3, 7, 4, 6, 7}, {5, 4, 5, 4, 6}, {6, 4, 6, 5, 7}};
+
+struct D64Frag {
+  int oa0, oa1;       // A operand columns (8 a + g)
+  int ob0, ob1, ob2;  // B operand columns (8 b + g)
+  unsigned onm;       // PRED: live fragments (ragged last block)
+};
+
+// the MMAs of one staged chunk; PRED = per-fragment liveness tests (ragged
+// last block, r % 64 != 0)
+template <int GROUP, bool PRED>
 __device__ __forceinline__ void d64_mma(double (&acc)[GROUP == 0 ? 4 : 2][5][2],
                                         double (&amo)[GROUP == 1 ? 8 : 1][2], const double* sm,
-                                        int q, int g, int warp, int oa_lo, int oa_hi,
-                                        const int (&ob)[5], unsigned lom, unsigned onm, bool no_ms,
+                                        int q, int g, int warp, const D64Frag& fr, bool no_ms,
                                         bool mo_row, int rloc) {
   constexpr int C = kPC64, kLS = kLS64, kRow = kRow64, kFace = kFace64;
   const double* sX = sm;
@@ -1948,98 +1963,63 @@ __device__ __forceinline__ void d64_mma(double (&acc)[GROUP == 0 ? 4 : 2][5][2],
   const int kk = q & 1, second = q >> 1;
   (void)sU; (void)sXo; (void)sGX; (void)sMX; (void)sGY; (void)sMXt; (void)sF; (void)sMXs;
   (void)kk; (void)second; (void)warp; (void)mo_row; (void)rloc; (void)no_ms; (void)amo;
-    // ---- volume terms, every cell of the chunk
+  // fragment k <- (A operand a[k], B operand b[k]) of the pattern
+  auto five = [&](double (&d)[5][2], double a0, double a1, double b0, double b1, double b2) {
+    if (!PRED || (fr.onm & 1u)) dmma(d[0][0], d[0][1], a0, b0);
+    if (!PRED || (fr.onm & 2u)) dmma(d[1][0], d[1][1], a0, b1);
+    if (!PRED || (fr.onm & 4u)) dmma(d[2][0], d[2][1], a1, b1);
+    if (!PRED || (fr.onm & 8u)) dmma(d[3][0], d[3][1], a0, b2);
+    if (!PRED || (fr.onm & 16u)) dmma(d[4][0], d[4][1], a1, b2);
+  };
+  // ---- volume terms, every cell of the chunk
 #pragma unroll
-    for (int cl = 0; cl < C; ++cl) {
-      const double* xr = sX + cl * kRow + q * kLS;
-      const double xlo = xr[oa_lo], xhi = xr[oa_hi];
-      if constexpr (GROUP == 0) {
-        const double* gxr = sGX + cl * kRow + q * kLS;
-        const double* gyr = sGY + cl * kRow + q * kLS;
-        double bgx[5], bgy[5];  // HOIST: every operand load ahead of the MMAs
-        if constexpr (HOIST) {
-#pragma unroll
-          for (int k = 0; k < NF; ++k) {
-            bgx[k] = gxr[ob[k]];
-            bgy[k] = gyr[ob[k]];
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < NF; ++k)
-          if (!PRED || ((onm >> k) & 1u)) {
-            const double xa = (EVEN || ((lom >> k) & 1u)) ? xlo : xhi;
-            dmma(acc[0][k][0], acc[0][k][1], xa, HOIST ? bgx[k] : gxr[ob[k]]);  // px (volume)
-            dmma(acc[1][k][0], acc[1][k][1], xa, HOIST ? bgy[k] : gyr[ob[k]]);  // py (volume)
-          }
-      } else {
-        const double* mtr = sMXt + cl * kRow + q * kLS;
-        const double* msr = sMXs + cl * kRow + q * kLS;
-        double bt[5], bs[5];
-        if constexpr (HOIST) {
-#pragma unroll
-          for (int k = 0; k < NF; ++k) {
-            bt[k] = mtr[ob[k]];
-            bs[k] = no_ms ? 0.0 : msr[ob[k]];
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < NF; ++k)
-          if (!PRED || ((onm >> k) & 1u)) {
-            const double xa = (EVEN || ((lom >> k) & 1u)) ? xlo : xhi;
-            dmma(acc[0][k][0], acc[0][k][1], xa, HOIST ? bt[k] : mtr[ob[k]]);  // mt
-            if (!no_ms) dmma(acc[1][k][0], acc[1][k][1], xa, HOIST ? bs[k] : msr[ob[k]]);  // ms
-          }
-        const double xo = sXo[cl * kRow + q * kLS + 8 * warp + g];
-        const double* mr = sMX + cl * kRow + q * kLS + g;
-        if (mo_row) {
-#pragma unroll
-          for (int hb = 0; hb < 2; ++hb) {
-            double bm[4];
-#pragma unroll
-            for (int b = 0; b < 4; ++b) bm[b] = mr[8 * (4 * hb + b)];
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-              if (!PRED || 8 * (4 * hb + b) < rloc) dmma(amo[4 * hb + b][0], amo[4 * hb + b][1], xo, bm[b]);  // mo
-          }
-        }
-      }
-    }
+  for (int cl = 0; cl < C; ++cl) {
+    const double* xr = sX + cl * kRow + q * kLS;
+    const double x0 = xr[fr.oa0], x1 = xr[fr.oa1];
     if constexpr (GROUP == 0) {
-      // ---- face terms: k slot q -> cell 2 kp + q / 2, face dof q % 2
+      const double* gxr = sGX + cl * kRow + q * kLS;
+      const double* gyr = sGY + cl * kRow + q * kLS;
+      five(acc[0], x0, x1, gxr[fr.ob0], gxr[fr.ob1], gxr[fr.ob2]);  // px (volume)
+      five(acc[1], x0, x1, gyr[fr.ob0], gyr[fr.ob1], gyr[fr.ob2]);  // py (volume)
+    } else {
+      const double* mtr = sMXt + cl * kRow + q * kLS;
+      const double* msr = sMXs + cl * kRow + q * kLS;
+      five(acc[0], x0, x1, mtr[fr.ob0], mtr[fr.ob1], mtr[fr.ob2]);  // mt
+      if (!no_ms) five(acc[1], x0, x1, msr[fr.ob0], msr[fr.ob1], msr[fr.ob2]);  // ms
+      const double xo = sXo[cl * kRow + q * kLS + 8 * warp + g];
+      const double* mr = sMX + cl * kRow + q * kLS + g;
+      if (mo_row) {
 #pragma unroll
-      for (int kp = 0; kp < C / 2; ++kp) {
-        const int cl = 2 * kp + second;
-        const double* ur = sU + cl * kRow;
-        const double uxlo = ur[kk * kLS + oa_lo], uxhi = ur[kk * kLS + oa_hi];
-        const double uylo = ur[(2 + kk) * kLS + oa_lo], uyhi = ur[(2 + kk) * kLS + oa_hi];
-        const double* f = sF + cl * kFace;
-        // two passes (x faces, then y faces): 10 operands in flight each
+        for (int hb = 0; hb < 2; ++hb) {
+          double bm[4];
 #pragma unroll
-        for (int ax = 0; ax < 2; ++ax) {
-          double f0[5], f1[5];
-          if constexpr (HOIST) {
+          for (int b = 0; b < 4; ++b) bm[b] = mr[8 * (4 * hb + b)];
 #pragma unroll
-            for (int k = 0; k < NF; ++k) {
-              f0[k] = f[(2 * ax + kk) * kLS + ob[k]];
-              f1[k] = f[(4 + 2 * ax + kk) * kLS + ob[k]];
-            }
-          }
-#pragma unroll
-          for (int k = 0; k < NF; ++k)
-            if (!PRED || ((onm >> k) & 1u)) {
-              const bool lo = EVEN || ((lom >> k) & 1u);
-              const double ua = ax == 0 ? (lo ? uxlo : uxhi) : (lo ? uylo : uyhi);
-              dmma(acc[ax][k][0], acc[ax][k][1], ua,
-                   HOIST ? f0[k] : f[(2 * ax + kk) * kLS + ob[k]]);  // px / py (faces)
-              dmma(acc[2 + ax][k][0], acc[2 + ax][k][1], ua,
-                   HOIST ? f1[k] : f[(4 + 2 * ax + kk) * kLS + ob[k]]);  // jx / jy
-            }
+          for (int b = 0; b < 4; ++b)
+            if (!PRED || 8 * (4 * hb + b) < rloc)
+              dmma(amo[4 * hb + b][0], amo[4 * hb + b][1], xo, bm[b]);  // mo
         }
       }
     }
+  }
+  if constexpr (GROUP == 0) {
+    // ---- face terms: k slot q -> cell 2 kp + q / 2, face dof q % 2
+#pragma unroll
+    for (int kp = 0; kp < C / 2; ++kp) {
+      const int cl = 2 * kp + second;
+      const double* ur = sU + cl * kRow + kk * kLS;
+      const double* f = sF + cl * kFace + kk * kLS;
+      const double ux0 = ur[fr.oa0], ux1 = ur[fr.oa1];
+      five(acc[0], ux0, ux1, f[fr.ob0], f[fr.ob1], f[fr.ob2]);  // px (faces)
+      five(acc[2], ux0, ux1, f[4 * kLS + fr.ob0], f[4 * kLS + fr.ob1], f[4 * kLS + fr.ob2]);  // jx
+      const double uy0 = ur[2 * kLS + fr.oa0], uy1 = ur[2 * kLS + fr.oa1];
+      five(acc[1], uy0, uy1, f[2 * kLS + fr.ob0], f[2 * kLS + fr.ob1], f[2 * kLS + fr.ob2]);  // py
+      five(acc[3], uy0, uy1, f[6 * kLS + fr.ob0], f[6 * kLS + fr.ob1], f[6 * kLS + fr.ob2]);  // jy
+    }
+  }
 }
 
-template <int GROUP, bool HOIST>
+template <int GROUP>
 __device__ __forceinline__ void project64d_group(const ProjArgs& pa, const dlrsn_cellops& ops,
                                                  double* sm, int t64) {
   constexpr int C = kPC64, kLS = kLS64, kRow = kRow64;
@@ -2076,33 +2056,22 @@ __device__ __forceinline__ void project64d_group(const ProjArgs& pa, const dlrsn
   const int rloc = min(64, r - col0);  // live columns of this block
   const int c_begin = blockIdx.y * pa.cells_per_block;
   const int c_end = min(ncell, c_begin + pa.cells_per_block);
-  // fragment list of this warp: rows a_lo (the first n_lo fragments) and
-  // a_hi = 7 - a_lo; 36 = 4 x (5 + 4)
-  const int pr = warp >> 1, odd = warp & 1;
-  const int a_lo = pr, a_hi = 7 - pr;
-  // even warp: row a_lo, columns a_lo .. a_lo + 4; odd warp: the rest of row
-  // a_lo (3 - pr fragments) and row a_hi (pr + 1 fragments)
-  // per fragment k: ob[k] = 8 b + g (its B column of this lane), bit k of lom
-  // = row a_lo (else a_hi), bit k of onm = live
-  int ob[5];
-  unsigned lom = 0, onm = 0;
+  // this warp's fragment pattern (kD64Pat): per fragment k its fragment row
+  // fa[k] and column fb[k] are recomputed from the table where needed
+  const int pa0 = kD64Pat[warp][0], pa1 = kD64Pat[warp][1];
+  const int pb0 = kD64Pat[warp][2], pb1 = kD64Pat[warp][3], pb2 = kD64Pat[warp][4];
+  D64Frag fr;
+  fr.oa0 = 8 * pa0 + g;
+  fr.oa1 = 8 * pa1 + g;
+  fr.ob0 = 8 * pb0 + g;
+  fr.ob1 = 8 * pb1 + g;
+  fr.ob2 = 8 * pb2 + g;
+  {
+    const int ra[5] = {pa0, pa0, pa1, pa0, pa1}, cb[5] = {pb0, pb1, pb1, pb2, pb2};
+    fr.onm = 0;
 #pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    int a, b;
-    if (!odd) {
-      a = a_lo;
-      b = a_lo + k;
-    } else if (k < 3 - pr) {
-      a = a_lo;
-      b = a_lo + 5 + k;
-    } else {
-      a = a_hi;
-      b = a_hi + (k - (3 - pr));
-    }
-    const bool live = b < 8 && (odd ? k < 4 : true);
-    ob[k] = (live ? 8 * b : 0) + g;
-    if (a == a_lo) lom |= 1u << k;
-    if (live && 8 * b < rloc) onm |= 1u << k;
+    for (int k = 0; k < 5; ++k)
+      if (8 * ra[k] < rloc && 8 * cb[k] < rloc) fr.onm |= 1u << k;
   }
   double acc[NS][5][2];
 #pragma unroll
@@ -2161,7 +2130,6 @@ __device__ __forceinline__ void project64d_group(const ProjArgs& pa, const dlrsn
   };
   Raw cur;
   fetch(c_begin, cur);
-  const int oa_lo = 8 * a_lo + g, oa_hi = 8 * a_hi + g;
   for (int c0 = c_begin; c0 < c_end; c0 += C) {
     const int nc = min(C, c_end - c0);
     __syncthreads();  // the previous chunk's fragments are consumed
@@ -2219,17 +2187,10 @@ __device__ __forceinline__ void project64d_group(const ProjArgs& pa, const dlrsn
     __syncthreads();
     fetch(c0 + C, cur);  // next chunk's loads in flight during the MMAs
     // ---- the chunk's MMAs (volume terms of every cell, then the faces)
-    if (rloc == 64) {
-      if (!odd)
-        d64_mma<GROUP, HOIST, 5, true, false>(acc, amo, sm, q, g, warp, oa_lo, oa_hi, ob, lom, onm,
-                                              no_ms, mo_row, rloc);
-      else
-        d64_mma<GROUP, HOIST, 4, false, false>(acc, amo, sm, q, g, warp, oa_lo, oa_hi, ob, lom, onm,
-                                               no_ms, mo_row, rloc);
-    } else {
-      d64_mma<GROUP, HOIST, 5, false, true>(acc, amo, sm, q, g, warp, oa_lo, oa_hi, ob, lom, onm,
-                                            no_ms, mo_row, rloc);
-    }
+    if (rloc == 64)
+      d64_mma<GROUP, false>(acc, amo, sm, q, g, warp, fr, no_ms, mo_row, rloc);
+    else
+      d64_mma<GROUP, true>(acc, amo, sm, q, g, warp, fr, no_ms, mo_row, rloc);
     if constexpr (GROUP == 1) {
       if (threadIdx.x < 64)
         for (int cl = 0; cl < nc; ++cl) qacc += sQ[cl * 64 + threadIdx.x];
@@ -2240,20 +2201,23 @@ __device__ __forceinline__ void project64d_group(const ProjArgs& pa, const dlrsn
   double* out = pa.part + (int64_t)blockIdx.y * stride;
   // (the right / top domain-boundary faces of the diagonal blocks are added
   // by project_bnd64_kernel into partial slots of their own)
+  {
+    const int ra[5] = {pa0, pa0, pa1, pa0, pa1}, cb[5] = {pb0, pb1, pb1, pb2, pb2};
 #pragma unroll
-  for (int o = 0; o < NS; ++o)
+    for (int o = 0; o < NS; ++o)
 #pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      if (!((onm >> k) & 1u)) continue;
-      const int i = col0 + (((lom >> k) & 1u) ? oa_lo : oa_hi);
+      for (int k = 0; k < 5; ++k) {
+        if (!((fr.onm >> k) & 1u)) continue;
+        const int i = col0 + 8 * ra[k] + g;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int j = col0 + (ob[k] - g) + 2 * q + h;
-        if (i >= r || j >= r) continue;
-        const int slot = GROUP == 0 ? o : 4 + o;  // px py jx jy | mt ms
-        out[(int64_t)slot * r * r + (int64_t)i * r + j] = acc[o][k][h];
+        for (int h = 0; h < 2; ++h) {
+          const int j = col0 + 8 * cb[k] + 2 * q + h;
+          if (i >= r || j >= r) continue;
+          const int slot = GROUP == 0 ? o : 4 + o;  // px py jx jy | mt ms
+          out[(int64_t)slot * r * r + (int64_t)i * r + j] = acc[o][k][h];
+        }
       }
-    }
+  }
   if constexpr (GROUP == 1) {
     if (mo_row) {
       const int i = col0 + 8 * warp + g;
@@ -2357,15 +2321,14 @@ __global__ void __launch_bounds__(256, 2) project_mma32g_kernel(ProjArgs pa, dlr
 // seq = 1: grid (1, cell ranges), every CTA runs both groups of every
 // diagonal block on its range one after the other -- identical work per
 // CTA, so 2 x SM-count equal ranges are balanced without a tail
-template <bool HOIST>
 __global__ void __launch_bounds__(256, 2) project_mma64d_kernel(ProjArgs pa, dlrsn_cellops ops,
                                                                  int nb64, int seq) {
   extern __shared__ __align__(16) double sm64d[];
   (void)seq;
   for (int b = 0; b < nb64; ++b) {
-    project64d_group<0, HOIST>(pa, ops, sm64d, b);
+    project64d_group<0>(pa, ops, sm64d, b);
     __syncthreads();
-    project64d_group<1, HOIST>(pa, ops, sm64d, b);
+    project64d_group<1>(pa, ops, sm64d, b);
     __syncthreads();
   }
 }
@@ -4218,10 +4181,7 @@ int project_ex(const dlrsn_cellops* ops, int r, const double* X, const double* X
         DLRSN_TRY_CUDA(cudaFuncSetAttribute(project_mma32g_kernel,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)kProj32SmemG));
-        DLRSN_TRY_CUDA(cudaFuncSetAttribute(project_mma64d_kernel<true>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)kProj64Smem));
-        DLRSN_TRY_CUDA(cudaFuncSetAttribute(project_mma64d_kernel<false>,
+        DLRSN_TRY_CUDA(cudaFuncSetAttribute(project_mma64d_kernel,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)kProj64Smem));
         attr = true;
@@ -4242,14 +4202,8 @@ int project_ex(const dlrsn_cellops* ops, int r, const double* X, const double* X
       if (tm) DLRSN_TRY_CUDA(cudaEventRecord(tm->first, st));
       int nslots = nblkg;
       if (d64) {
-        static const bool hoist = getenv("DLRSN_K3_HOIST") && getenv("DLRSN_K3_HOIST")[0] == '1';
-        const bool seq = true;
         const int nb64 = (r + 63) / 64;
-        const dim3 g64(1, nblkg);
-        if (hoist)
-          project_mma64d_kernel<true><<<g64, 256, kProj64Smem, st>>>(pa, *ops, nb64, seq ? 1 : 0);
-        else
-          project_mma64d_kernel<false><<<g64, 256, kProj64Smem, st>>>(pa, *ops, nb64, seq ? 1 : 0);
+        project_mma64d_kernel<<<dim3(1, nblkg), 256, kProj64Smem, st>>>(pa, *ops, nb64, 1);
         DLRSN_CHECK_LAUNCH("project_mma64d_kernel");
         project_bnd64_kernel<<<kProjBndBlocks, 256, 0, st>>>(pa, *ops, (r + 63) / 64, nblkg);
         DLRSN_CHECK_LAUNCH("project_bnd64_kernel");

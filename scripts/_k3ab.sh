@@ -1,5 +1,5 @@
-timeout 300 python -m pytest tests/test_gpu_dlr.py tests/test_gpu_slab.py tests/test_gpu_dense.py -m gpu -x -q 2>&1 | tail -2
-for cfg in "0 296" "1 296"; do set -- $cfg; echo "== HOIST=$1 RANGES=$2"; DLRSN_K3_HOIST=$1 DLRSN_K3_RANGES=$2 timeout 300 python bench.py --steps 8 --warmup 4 --more-configs "" --no-cpu-baseline --e2e-steps 2 2>/dev/null | python -c "
+timeout 400 python -m pytest tests/test_gpu_dlr.py tests/test_gpu_slab.py tests/test_gpu_dense.py tests/test_gpu_lean.py -m gpu -x -q 2>&1 | tail -2
+for i in 1 2; do timeout 300 python bench.py --steps 8 --warmup 4 --more-configs "" --no-cpu-baseline --e2e-steps 2 2>/dev/null | python -c "
 import json,sys
 d=json.loads(sys.stdin.read())
 e=sorted(d['ms_per_step_each'])
