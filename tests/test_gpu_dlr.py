@@ -544,11 +544,13 @@ def test_marshak_multistrip_matches_oracle():
 
 
 @pytest.mark.parametrize("nx,ny,r", [(37, 29, 24), (31, 33, 48), (20, 17, 64), (9, 40, 128),
-                                     (33, 35, 16)])
+                                     (33, 35, 16), (12, 11, 100), (8, 13, 72), (7, 9, 40)])
 def test_projections_match_oracle_wide(nx, ny, r):
-    """K3 at every tile width: r <= 16 (16x16 tiles), r > 16 (32x32 tiles,
-    partial edge tiles at 24 and 48): px, py, jx, jy, mt, ms, q-hat and
-    mo = X_old^T M X against the oracle's assembled sparse operators."""
+    """K3 at every tile width: r <= 16 (16x16 tiles), 16 < r <= 32 (32x32
+    tiles), r > 32 (diagonal 64-column blocks: full at 64 and 128, ragged --
+    the predicated fragment path -- at 40, 48, 72 and 100; 32x32 tiles off the
+    diagonal for r > 64): px, py, jx, jy, mt, ms, q-hat and mo = X_old^T M X
+    against the oracle's assembled sparse operators."""
     from oracle import port as P
     from paper_2601_18705_b200 import transport as Tr
     from paper_2601_18705_b200.dlr_sn import project_operators
