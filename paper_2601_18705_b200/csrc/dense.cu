@@ -199,13 +199,18 @@ __global__ void __launch_bounds__(256, (4 * KS + 8 * NT <= 96) ? 2 : 1) rowmix_w
                                                           const double* __restrict__ X, int ldx,
                                                           const double* __restrict__ K, int ldk,
                                                           double beta, double* __restrict__ Y,
-                                                          int ldy, int kyp, int ldks, int vec) {
+                                                          int ldy, int kyp, int ldks, int vec,
+                                                          const double* __restrict__ V,
+                                                          double* __restrict__ YV) {
   extern __shared__ double sK[];  // (4 KS) x ldks
+  __shared__ double sV[4 * KS];   // optional extra column: YV = X V in the same pass over X
   for (int e = threadIdx.x; e < 4 * KS * kyp; e += blockDim.x) {
     const int pr = e / kyp, col = e - pr * kyp;
     const int k = (pr & 3) * KS + (pr >> 2);
     sK[pr * ldks + col] = (k < kx && col < ky) ? __ldg(K + (int64_t)k * ldk + col) : 0.0;
   }
+  if (V)
+    for (int e = threadIdx.x; e < 4 * KS; e += blockDim.x) sV[e] = e < kx ? __ldg(V + e) : 0.0;
   __syncthreads();
   const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
   const int64_t tiles = ((int64_t)n + 7) / 8;
@@ -229,6 +234,18 @@ __global__ void __launch_bounds__(256, (4 * KS + 8 * NT <= 96) ? 2 : 1) rowmix_w
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks)
           af[u][ks] = (row < n && q * KS + ks < kx) ? __ldg(xr + ks) : 0.0;
+      }
+    }
+    if (V) {  // lane quad q holds columns q KS .. q KS + KS - 1 of its rows
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        double acc = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) acc = fma(af[u][ks], sV[q * KS + ks], acc);
+        acc += __shfl_xor_sync(kFull, acc, 1);
+        acc += __shfl_xor_sync(kFull, acc, 2);
+        const int64_t row = (t0 + u) * 8 + g;
+        if (q == 0 && row < n) YV[row] = acc;
       }
     }
     for (int c0 = 0; c0 < ky; c0 += 8 * NT) {
@@ -3760,6 +3777,12 @@ static int grid_for(int64_t n, int block = kRB) {
   return (int)(b < 1 ? 1 : b);
 }
 
+namespace dlrsn {
+int rowmix_vec(int64_t n, int kx, int ky, const double* X, int ldx, const double* K, int ldk,
+               double beta, double* Y, int ldy, const double* v, double* yv,
+               dlrsn_stream_t stream);
+}
+
 extern "C" {
 
 int dlrsn_rowmix_upper(int64_t n, int r, const double* X, int ldx, const double* K, int ldk,
@@ -3770,8 +3793,27 @@ int dlrsn_rowmix_upper(int64_t n, int r, const double* X, int ldx, const double*
 
 int dlrsn_rowmix(int64_t n, int kx, int ky, const double* X, int ldx, const double* K, int ldk,
                  double beta, double* Y, int ldy, dlrsn_stream_t stream) {
+  return dlrsn::rowmix_vec(n, kx, ky, X, ldx, K, ldk, beta, Y, ldy, nullptr, nullptr, stream);
+}
+
+}  // extern "C"
+
+namespace dlrsn {
+// Y = X K (+ beta Y) and, with v / yv, yv = X v from the same pass over X
+// (the wide DMMA kernel; otherwise a second launch)
+int rowmix_vec(int64_t n, int kx, int ky, const double* X, int ldx, const double* K, int ldk,
+               double beta, double* Y, int ldy, const double* v, double* yv,
+               dlrsn_stream_t stream) {
   DLRSN_REQUIRE(kx >= 0 && ky >= 0 && kx * ky <= 48 * 1024 / 8 * 4, "rowmix operand too large");
   if (n == 0 || ky == 0) return DLRSN_OK;
+  const double* V = v;
+  double* YV = yv;
+  if (v && !((kx > 32 || ky > 16) && kx <= 128 && n >= 64)) {  // not the wide kernel
+    const int rc = dlrsn_rowmix(n, kx, 1, X, ldx, v, 1, 0.0, yv, 1, stream);
+    if (rc != DLRSN_OK) return rc;
+    V = nullptr;
+    YV = nullptr;
+  }
   if (kx <= 32 && ky <= 16 && n >= 64) {
     const int64_t tiles = (n + 7) / 8;
     int64_t blocks = (tiles + 7) / 8;
@@ -3813,7 +3855,7 @@ int dlrsn_rowmix(int64_t n, int kx, int ky, const double* X, int ldx, const doub
     int64_t blocks = (tiles + 15) / 16;
     if (blocks > 148 * 4) blocks = 148 * 4;
     cudaStream_t st = as_stream(stream);
-#define DLRSN_ROWMIX_WIDE(KS, NT)                                                                do {                                                                                             if (smem > 48 * 1024)                                                                            DLRSN_TRY_CUDA(cudaFuncSetAttribute(rowmix_wide_kernel<KS, NT>,                                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));     rowmix_wide_kernel<KS, NT><<<(int)blocks, 256, smem, st>>>((int)n, kx, ky, X, ldx, K, ldk, beta,                                                                Y, ldy, kyp, ldks, vec);          } while (0)
+#define DLRSN_ROWMIX_WIDE(KS, NT)                                                                do {                                                                                             if (smem > 48 * 1024)                                                                            DLRSN_TRY_CUDA(cudaFuncSetAttribute(rowmix_wide_kernel<KS, NT>,                                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));     rowmix_wide_kernel<KS, NT><<<(int)blocks, 256, smem, st>>>((int)n, kx, ky, X, ldx, K, ldk, beta,                                                                Y, ldy, kyp, ldks, vec, V, YV);          } while (0)
     if (ks == 4) {
       if (nt == 8) DLRSN_ROWMIX_WIDE(4, 8);
       else if (nt == 4) DLRSN_ROWMIX_WIDE(4, 4);
@@ -3857,6 +3899,9 @@ int dlrsn_rowmix(int64_t n, int kx, int ky, const double* X, int ldx, const doub
   DLRSN_CHECK_LAUNCH("rowmix_kernel");
   return DLRSN_OK;
 }
+}  // namespace dlrsn
+
+extern "C" {
 
 // cells per block of the cell-reduction kernels: about 4 CTAs per SM in
 // total over all output tiles, in whole smem chunks

@@ -985,11 +985,6 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
                                                  b.chk_in, p->x_check_in);
         DLRSN_CHECK_LAUNCH("ortho_residual_kernel");
       }
-      // scalar_flux (lowrank.py:60-62) -> the first scattering source
-      ks_kernel<<<1, 256, 0, sd>>>(r, S, W, nullptr, beta, nullptr, b.Sb, p->omegas_dev, nullptr);
-      DLRSN_CHECK_LAUNCH("ks_kernel");
-      DLRSN_RET(dlrsn_rowmix(N, r, 1, X, r, b.Sb, 1, 0.0, b.phi0, 1, ss2));
-      DLRSN_RET(dlrsn_scatter_source(ops, b.phi0, sigma_s, b.scat, b.flags + 1, ss2));
       DLRSN_RET(dlrsn_cells_to_sk4(ops, sigma_t, b.sig4, ss2));
     }
     // 1. DEIM, closure weights (errors reported at the readback)
@@ -1019,7 +1014,12 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
         DLRSN_CHECK_LAUNCH("dsa_penalty_kernel");
       }
     }
-    DLRSN_RET(dlrsn_rowmix(N, r, r, X, r, b.K, r, 0.0, b.psi_time, r, s));
+    // scalar_flux (lowrank.py:60-62) -> the first scattering source; phi0 = X
+    // (S beta) comes out of the same pass over X as psi_time = X K
+    ks_kernel<<<1, 256, 0, st>>>(r, S, W, nullptr, beta, nullptr, b.Sb, p->omegas_dev, nullptr);
+    DLRSN_CHECK_LAUNCH("ks_kernel");
+    DLRSN_RET(rowmix_vec(N, r, r, X, r, b.K, r, 0.0, b.psi_time, r, b.Sb, b.phi0, s));
+    DLRSN_RET(dlrsn_scatter_source(ops, b.phi0, sigma_s, b.scat, b.flags + 1, s));
     const double* pt_local = b.psi_time;
     int ld_pt = r;
     if (world > 1 && nl > 0) {

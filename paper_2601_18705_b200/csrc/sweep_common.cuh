@@ -140,6 +140,10 @@ int project_ex(const dlrsn_cellops* ops, int r, const double* X, const double* X
                const double* q, double* out, double* partial, const int* any_scat,
                cudaStream_t stream);
 // dense.cu: Y = X K for an upper-triangular r x r K (skips the zero blocks)
+// dense.cu: Y = X K (+ beta Y) and, with v / yv, yv = X v from the same pass over X
+int rowmix_vec(int64_t n, int kx, int ky, const double* X, int ldx, const double* K, int ldk,
+               double beta, double* Y, int ldy, const double* v, double* yv,
+               dlrsn_stream_t stream);
 int rowmix_upper(int64_t n, int r, const double* X, int ldx, const double* K, int ldk, double* Y,
                  int ldy, cudaStream_t st);
 // dense.cu: the row-system combine as grids (scratch r*r + 2r doubles)
