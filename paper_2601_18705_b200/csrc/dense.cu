@@ -594,7 +594,8 @@ __global__ void __launch_bounds__(256, TB == 64 ? 2 : 1) mgram_wide_kernel(int n
                                                          const double* __restrict__ coeff,
                                                          dlrsn_cellops ops, int cells_per_block,
                                                          double* __restrict__ part, int vec,
-                                                         int sym) {
+                                                         int sym, const double* __restrict__ VV,
+                                                         double* __restrict__ YV) {
   using P = MgramWide<TB>;
   constexpr int LD = P::LD, PL = P::PL, KP = P::KP, NWT = 8 / KP, CPK = kMgC / KP;
   constexpr int NCP = TB / 2;  // column pairs
@@ -667,6 +668,21 @@ __global__ void __launch_bounds__(256, TB == 64 ? 2 : 1) mgram_wide_kernel(int n
       double2 v[4];
 #pragma unroll
       for (int l = 0; l < 4; ++l) v[l] = *reinterpret_cast<const double2*>(sBsrc + (4 * cl + l) * LD + 2 * cp);
+      if constexpr (TB == 64) {
+        // optional extra output YV = B VV from the staged rows (single-tile
+        // Grams, j0 = 0: a warp holds all 64 columns of one cell's 4 dof rows)
+        if (VV) {
+          const double v0 = 2 * cp < rb ? __ldg(VV + 2 * cp) : 0.0;
+          const double v1 = 2 * cp + 1 < rb ? __ldg(VV + 2 * cp + 1) : 0.0;
+#pragma unroll
+          for (int l = 0; l < 4; ++l) {
+            double dsum = fma(v[l].x, v0, v[l].y * v1);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(kFull, dsum, o);
+            if (cp == 0 && c0 + cl < c_end) YV[4 * (int64_t)(c0 + cl) + l] = dsum;
+          }
+        }
+      }
       const double w = (coeff && c0 + cl < c_end) ? __ldg(coeff + c0 + cl) : 1.0;
 #pragma unroll
       for (int l = 0; l < 4; ++l) {
@@ -3781,6 +3797,9 @@ namespace dlrsn {
 int rowmix_vec(int64_t n, int kx, int ky, const double* X, int ldx, const double* K, int ldk,
                double beta, double* Y, int ldy, const double* v, double* yv,
                dlrsn_stream_t stream);
+int mgram_vec(const dlrsn_cellops* ops, int ra, int rb, const double* A, int lda, const double* B,
+              int ldb, const double* coeff, double* G, double* partial, const double* v,
+              double* yv, dlrsn_stream_t stream);
 }
 
 extern "C" {
@@ -4050,6 +4069,18 @@ int64_t dlrsn_partials_len(int ncell, int ra, int rb, int kind) {
 int dlrsn_mgram(const dlrsn_cellops* ops, int ra, int rb, const double* A, int lda,
                 const double* B, int ldb, const double* coeff, double* G, double* partial,
                 dlrsn_stream_t stream) {
+  return dlrsn::mgram_vec(ops, ra, rb, A, lda, B, ldb, coeff, G, partial, nullptr, nullptr, stream);
+}
+
+}  // extern "C"
+
+namespace dlrsn {
+// dlrsn_mgram and, with v / yv, yv = B v (n_dofs) from the rows the Gram
+// stages anyway (single-tile symmetric Grams, 32 < r <= 64; otherwise a
+// separate rowmix launch)
+int mgram_vec(const dlrsn_cellops* ops, int ra, int rb, const double* A, int lda, const double* B,
+              int ldb, const double* coeff, double* G, double* partial, const double* v,
+              double* yv, dlrsn_stream_t stream) {
   const int ncell = ops->nx * ops->ny;
   cudaStream_t st = as_stream(stream);
   static const char* sym_env = getenv("DLRSN_MGRAM_SYM");
@@ -4067,13 +4098,14 @@ int dlrsn_mgram(const dlrsn_cellops* ops, int ra, int rb, const double* A, int l
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     mgram_wide_kernel<32><<<dim3(pl.nblk, tiles), 256, smem, st>>>(ncell, ra, rb, A, lda, B, ldb,
                                                                    coeff, *ops, pl.cpb, partial,
-                                                                   vec, 1);
+                                                                   vec, 1, nullptr, nullptr);
     DLRSN_CHECK_LAUNCH("mgram_wide_kernel");
     const int64_t len = (int64_t)ra * rb;
     reduce_partials_kernel<<<(unsigned)((len + 31) / 32), 1024, 0, st>>>(pl.nblk, len, partial, G, 1.0);
     DLRSN_CHECK_LAUNCH("reduce_partials_kernel");
     mirror_gram_kernel<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(ra, 32, G);
     DLRSN_CHECK_LAUNCH("mirror_gram_kernel");
+    if (v) return dlrsn_rowmix(4 * (int64_t)ncell, rb, 1, B, ldb, v, 1, 0.0, yv, 1, stream);
     return DLRSN_OK;
   }
   const MgramPlan pl = mgram_plan(ncell, ra, rb);
@@ -4099,16 +4131,19 @@ int dlrsn_mgram(const dlrsn_cellops* ops, int ra, int rb, const double* A, int l
       const int T = (ra + 63) / 64;
       tsym = !full && A == B && lda == ldb && ra == rb && pl.tiles > 1;
       const int gy = tsym ? T * (T + 1) / 2 : pl.tiles;
+      const bool fuse = v != nullptr && same;  // one tile: every CTA stages all columns
       mgram_wide_kernel<64><<<dim3(nblk, gy), 256, smem, st>>>(ncell, ra, rb, A, lda, B, ldb,
                                                                coeff, *ops, pl.cpb, partial, vec,
-                                                               (full ? 2 : 0) | (tsym ? 1 : 0));
+                                                               (full ? 2 : 0) | (tsym ? 1 : 0),
+                                                               fuse ? v : nullptr, fuse ? yv : nullptr);
+      if (fuse) v = nullptr;
     } else {
       const size_t smem = MgramWide<32>::smem(same);
       DLRSN_TRY_CUDA(cudaFuncSetAttribute(mgram_wide_kernel<32>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       mgram_wide_kernel<32><<<dim3(nblk, pl.tiles), 256, smem, st>>>(ncell, ra, rb, A, lda, B, ldb,
                                                                      coeff, *ops, pl.cpb, partial, vec,
-                                                                     0);
+                                                                     0, nullptr, nullptr);
     }
     DLRSN_CHECK_LAUNCH("mgram_wide_kernel");
   }
@@ -4119,8 +4154,12 @@ int dlrsn_mgram(const dlrsn_cellops* ops, int ra, int rb, const double* A, int l
     mirror_gram_kernel<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(ra, 64, G);
     DLRSN_CHECK_LAUNCH("mirror_gram_kernel");
   }
+  if (v) return dlrsn_rowmix(4 * (int64_t)ncell, rb, 1, B, ldb, v, 1, 0.0, yv, 1, stream);
   return DLRSN_OK;
 }
+}  // namespace dlrsn
+
+extern "C" {
 
 }  // extern "C"
 

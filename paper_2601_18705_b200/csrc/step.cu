@@ -1173,9 +1173,13 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     {
       cudaStream_t sd = fk->side;
       void* ss2 = sd;
-      DLRSN_RET(dlrsn_rowmix(N, r, 1, X_new, r, b.lbar, 1, 0.0, phi_out, 1, ss2));
+      // the flux of the new state phi = X_new lbar comes out of the spatial
+      // check's pass over X_new (single-tile Gram, r <= 64; else its own launch)
+      if (p->check_state)
+        DLRSN_RET(mgram_vec(ops, r, r, X_new, r, X_new, r, nullptr, b.G, b.part, b.lbar, phi_out, ss2));
+      else
+        DLRSN_RET(dlrsn_rowmix(N, r, 1, X_new, r, b.lbar, 1, 0.0, phi_out, 1, ss2));
       if (p->advance) DLRSN_RET(advance_launch(p->advance, phi_out, sd));
-      if (p->check_state) DLRSN_RET(dlrsn_mgram(ops, r, r, X_new, r, X_new, r, nullptr, b.G, b.part, ss2));
     }
     DLRSN_RET(dlrsn_rowmix(no, r, r, W, r, b.gamma, r, 0.0, b.lfull, r, s));
     if (!exact_w && ang_fast) {

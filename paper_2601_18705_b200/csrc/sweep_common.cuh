@@ -144,6 +144,10 @@ int project_ex(const dlrsn_cellops* ops, int r, const double* X, const double* X
 int rowmix_vec(int64_t n, int kx, int ky, const double* X, int ldx, const double* K, int ldk,
                double beta, double* Y, int ldy, const double* v, double* yv,
                dlrsn_stream_t stream);
+// dense.cu: dlrsn_mgram and, with v / yv, yv = B v from the rows the Gram stages
+int mgram_vec(const dlrsn_cellops* ops, int ra, int rb, const double* A, int lda, const double* B,
+              int ldb, const double* coeff, double* G, double* partial, const double* v,
+              double* yv, dlrsn_stream_t stream);
 int rowmix_upper(int64_t n, int r, const double* X, int ldx, const double* K, int ldk, double* Y,
                  int ldy, cudaStream_t st);
 // dense.cu: the row-system combine as grids (scratch r*r + 2r doubles)
