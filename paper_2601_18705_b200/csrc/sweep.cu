@@ -1293,6 +1293,7 @@ __global__ void phi_combine_kernel(dlrsn_cellops ops, int G, const dlrsn_group* 
 // same cell for every direction of that quadrant -- sums cw_k psi_k over the
 // quadrant's slots in slot order (loads of 32 lanes contiguous) and writes
 // the quadrant partial of that cell, canonical dofs, one 32-byte sector.
+template <int UNR>
 __global__ void __launch_bounds__(256) phi_quadrant_kernel(
     int nx, int ny, int D, const int* __restrict__ quads, const double* __restrict__ cw,
     const double* __restrict__ psi, int64_t vlen, double* __restrict__ phiq, int64_t nd,
@@ -1326,11 +1327,30 @@ __global__ void __launch_bounds__(256) phi_quadrant_kernel(
   const int64_t off = sk_vec_off(T, s, t, 0, lane);
   double p[4] = {0.0, 0.0, 0.0, 0.0};
   if (n > 0) {
-#pragma unroll 4
-    for (int m = 0; m < n; ++m) {
+    // batches of UNR directions: 2 UNR 16-byte loads in flight per thread,
+    // then the sums in slot order
+    int m = 0;
+    for (; m + UNR <= n; m += UNR) {
+      double2 a[UNR], b[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const double* src = psi + (int64_t)s_k[m + u] * vlen + off;
+        a[u] = __ldcs(reinterpret_cast<const double2*>(src));
+        b[u] = __ldcs(reinterpret_cast<const double2*>(src + 64));
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const double w = s_w[m + u];
+        p[0] += w * a[u].x;
+        p[1] += w * a[u].y;
+        p[2] += w * b[u].x;
+        p[3] += w * b[u].y;
+      }
+    }
+    for (; m < n; ++m) {
       const double* src = psi + (int64_t)s_k[m] * vlen + off;
-      const double2 a = __ldcg(reinterpret_cast<const double2*>(src));
-      const double2 b = __ldcg(reinterpret_cast<const double2*>(src + 64));
+      const double2 a = __ldcs(reinterpret_cast<const double2*>(src));
+      const double2 b = __ldcs(reinterpret_cast<const double2*>(src + 64));
       const double w = s_w[m];
       p[0] += w * a.x;
       p[1] += w * a.y;
@@ -1565,8 +1585,14 @@ int phi_closure_launch(const dlrsn_cellops* ops, int D, const int* quads, const 
   const int nx = ops->nx, ny = ops->ny, ns = (ny + 31) / 32;
   const int64_t nd = 4 * (int64_t)nx * ny;
   const int64_t elems = (int64_t)ns * (nx + 31) * 32;
-  phi_quadrant_kernel<<<dim3((unsigned)((elems + 255) / 256), 4), 256, 0, st>>>(
-      nx, ny, D, quads, cw, psi_sk, sk_vec_len(nx, ny), phiq, nd, ctl);
+  static const int unr = getenv("DLRSN_PHIQ_UNR") ? atoi(getenv("DLRSN_PHIQ_UNR")) : 4;
+  const dim3 gq((unsigned)((elems + 255) / 256), 4);
+  if (unr >= 16)
+    phi_quadrant_kernel<16><<<gq, 256, 0, st>>>(nx, ny, D, quads, cw, psi_sk, sk_vec_len(nx, ny), phiq, nd, ctl);
+  else if (unr >= 8)
+    phi_quadrant_kernel<8><<<gq, 256, 0, st>>>(nx, ny, D, quads, cw, psi_sk, sk_vec_len(nx, ny), phiq, nd, ctl);
+  else
+    phi_quadrant_kernel<4><<<gq, 256, 0, st>>>(nx, ny, D, quads, cw, psi_sk, sk_vec_len(nx, ny), phiq, nd, ctl);
   DLRSN_CHECK_LAUNCH("phi_quadrant_kernel");
   const int nb = (nx * ny + 255) / 256;
   unsigned* counter = reinterpret_cast<unsigned*>(partial_ws);
