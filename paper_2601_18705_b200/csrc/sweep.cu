@@ -1197,6 +1197,54 @@ __global__ void scatter_source_kernel(dlrsn_cellops ops, const double* __restric
   write_scat4(ops, c, p, s, scat, vlen);
 }
 
+// The next iteration's scattering source M (sigma_s phi) / 4 pi in the 4
+// quadrant SK slabs, written in SK order: thread = one SK element (strip,
+// step, lane) of quadrant blockIdx.y, so a warp stores two contiguous 512-byte
+// runs (the per-cell kernel above scatters 16-byte pieces over the 4 slabs:
+// half-written sectors).  phi is read by cell (one 32-byte sector, from L2
+// for the quadrants after the first).  Skipped once the iteration converged.
+__global__ void __launch_bounds__(256) scat_quadrant_kernel(dlrsn_cellops ops,
+                                                            const double* __restrict__ phi,
+                                                            const double* __restrict__ ss,
+                                                            double* __restrict__ scat, int64_t vlen,
+                                                            const SiCtl* ctl) {
+  if (ctl != nullptr && ctl->done != 0) return;
+  const int nx = ops.nx, ny = ops.ny, T = nx + 31;
+  const int qd = blockIdx.y;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (s, t, lane)
+  const int lane = (int)(e & 31);
+  const int64_t st = e >> 5;
+  const int s = (int)(st / T), t = (int)(st - (int64_t)s * T);
+  const int ip = t - lane, jp = 32 * s + lane;
+  if (jp >= ny || ip < 0 || ip >= nx) return;
+  const int i = (qd & 1) ? nx - 1 - ip : ip;
+  const int j = (qd & 2) ? ny - 1 - jp : jp;
+  const int64_t c = (int64_t)j * nx + i;
+  const double2 a = __ldg(reinterpret_cast<const double2*>(phi) + 2 * c);
+  const double2 b = __ldg(reinterpret_cast<const double2*>(phi) + 2 * c + 1);
+  const double sg = __ldg(ss + c);
+  const double u[4] = {sg * a.x, sg * a.y, sg * b.x, sg * b.y};
+  double w[4];
+#pragma unroll
+  for (int l = 0; l < 4; ++l)
+    w[l] = (ops.mass[4 * l] * u[0] + ops.mass[4 * l + 1] * u[1] + ops.mass[4 * l + 2] * u[2] +
+            ops.mass[4 * l + 3] * u[3]) / kFourPi;
+  const int f = sk_flip(qd);
+  double2* o = reinterpret_cast<double2*>(scat + qd * vlen);
+  o[sk_vec_off(T, s, t, 0, lane) >> 1] = make_double2(w[0 ^ f], w[1 ^ f]);
+  o[sk_vec_off(T, s, t, 1, lane) >> 1] = make_double2(w[2 ^ f], w[3 ^ f]);
+}
+
+static int scat_quadrant_launch(const dlrsn_cellops* ops, const double* phi, const double* sigma_s,
+                                double* scat_sk4, const SiCtl* ctl, cudaStream_t st) {
+  const int nx = ops->nx, ny = ops->ny, ns = (ny + 31) / 32;
+  const int64_t elems = (int64_t)ns * (nx + 31) * 32;
+  scat_quadrant_kernel<<<dim3((unsigned)((elems + 255) / 256), 4), 256, 0, st>>>(
+      *ops, phi, sigma_s, scat_sk4, sk_vec_len(nx, ny), ctl);
+  DLRSN_CHECK_LAUNCH("scat_quadrant_kernel");
+  return DLRSN_OK;
+}
+
 // convergence test of transport_sn.py:430-447 on the device
 __device__ void si_decide(SiCtl* ctl, const double* w, int it, double tol, const int* any_scat) {
   const double change = sqrt(w[0]) / fmax(sqrt(w[1]), 1e-300);
@@ -1597,10 +1645,12 @@ int phi_closure_launch(const dlrsn_cellops* ops, int D, const int* quads, const 
   const int nb = (nx * ny + 255) / 256;
   unsigned* counter = reinterpret_cast<unsigned*>(partial_ws);
   double* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(partial_ws) + 256);
-  phi_sum_kernel<<<nb, 256, 0, st>>>(*ops, phiq, nd, phi_old, sigma_s, phi_new, scat_sk4,
+  phi_sum_kernel<<<nb, 256, 0, st>>>(*ops, phiq, nd, phi_old, sigma_s, phi_new, nullptr,
                                      sk_vec_len(nx, ny), norms, partials, counter, ctl, it, tol,
                                      any_scat, partial_out);
   DLRSN_CHECK_LAUNCH("phi_sum_kernel");
+  // the next scattering source in SK order (skipped when this iteration converged)
+  if (scat_sk4 && !partial_out) return scat_quadrant_launch(ops, phi_new, sigma_s, scat_sk4, ctl, st);
   return DLRSN_OK;
 }
 
@@ -1612,10 +1662,11 @@ int phi_finish_launch(const dlrsn_cellops* ops, const double* phi_src, double* p
   const int nb = (n + 255) / 256;
   unsigned* counter = reinterpret_cast<unsigned*>(partial_ws);
   double* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(partial_ws) + 256);
-  phi_finish_kernel<<<nb, 256, 0, st>>>(*ops, phi_src, phi_dst, phi_old, sigma_s, scat_sk4,
+  phi_finish_kernel<<<nb, 256, 0, st>>>(*ops, phi_src, phi_dst, phi_old, sigma_s, nullptr,
                                         sk_vec_len(ops->nx, ops->ny), norms, partials, counter,
                                         ctl, it, tol, any_scat);
   DLRSN_CHECK_LAUNCH("phi_finish_kernel");
+  if (scat_sk4) return scat_quadrant_launch(ops, phi_dst, sigma_s, scat_sk4, ctl, st);
   return DLRSN_OK;
 }
 
