@@ -1183,25 +1183,11 @@ __device__ inline void write_scat4(const dlrsn_cellops& ops, int c, const double
   }
 }
 
-__global__ void scatter_source_kernel(dlrsn_cellops ops, const double* __restrict__ phi,
-                                      const double* __restrict__ ss, double* __restrict__ scat,
-                                      int64_t vlen, int* any) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= ops.nx * ops.ny) return;
-  const double s = ss[c];
-  if (s != 0.0 && any) atomicOr(any, 1);
-  double p[4];
-  const double2 a = reinterpret_cast<const double2*>(phi)[2 * c];
-  const double2 b = reinterpret_cast<const double2*>(phi)[2 * c + 1];
-  p[0] = a.x; p[1] = a.y; p[2] = b.x; p[3] = b.y;
-  write_scat4(ops, c, p, s, scat, vlen);
-}
-
 // The next iteration's scattering source M (sigma_s phi) / 4 pi in the 4
 // quadrant SK slabs, written in SK order: thread = one SK element (strip,
 // step, lane) of quadrant blockIdx.y, so a warp stores two contiguous 512-byte
-// runs (the per-cell kernel above scatters 16-byte pieces over the 4 slabs:
-// half-written sectors).  phi is read by cell (one 32-byte sector, from L2
+// runs (writing by cell scatters 16-byte pieces over the 4 slabs: half-written
+// sectors).  phi is read by cell (one 32-byte sector, from L2
 // for the quadrants after the first).  Skipped once the iteration converged.
 __global__ void __launch_bounds__(256) scat_quadrant_kernel(dlrsn_cellops ops,
                                                             const double* __restrict__ phi,
@@ -1233,6 +1219,14 @@ __global__ void __launch_bounds__(256) scat_quadrant_kernel(dlrsn_cellops ops,
   double2* o = reinterpret_cast<double2*>(scat + qd * vlen);
   o[sk_vec_off(T, s, t, 0, lane) >> 1] = make_double2(w[0 ^ f], w[1 ^ f]);
   o[sk_vec_off(T, s, t, 1, lane) >> 1] = make_double2(w[2 ^ f], w[3 ^ f]);
+}
+
+// *any |= (some v[i] != 0)  (the pure-absorber test of transport_sn.py:410)
+__global__ void any_nonzero_kernel(int n, const double* __restrict__ v, int* any) {
+  int nz = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    if (v[i] != 0.0) nz = 1;
+  if (__any_sync(kFull, nz) && (threadIdx.x & 31) == 0) atomicOr(any, 1);
 }
 
 static int scat_quadrant_launch(const dlrsn_cellops* ops, const double* phi, const double* sigma_s,
@@ -1744,10 +1738,14 @@ int dlrsn_cells_to_sk4(const dlrsn_cellops* ops, const double* cell_values, doub
 int dlrsn_scatter_source(const dlrsn_cellops* ops, const double* phi, const double* sigma_s,
                          double* scat_sk4, int* any_scatter, dlrsn_stream_t stream) {
   const int n = ops->nx * ops->ny;
-  scatter_source_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(
-      *ops, phi, sigma_s, scat_sk4, sk_vec_len(ops->nx, ops->ny), any_scatter);
-  DLRSN_CHECK_LAUNCH("scatter_source_kernel");
-  return DLRSN_OK;
+  // any_scatter from a scan of sigma_s, the slabs in SK order (coalesced)
+  if (any_scatter) {
+    const int nb = (n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024;
+    any_nonzero_kernel<<<nb, 256, 0, as_stream(stream)>>>(
+        n, sigma_s, any_scatter);
+    DLRSN_CHECK_LAUNCH("any_nonzero_kernel");
+  }
+  return scat_quadrant_launch(ops, phi, sigma_s, scat_sk4, nullptr, as_stream(stream));
 }
 
 int dlrsn_phi_combine(const dlrsn_cellops* ops, int G, const dlrsn_group* groups,
