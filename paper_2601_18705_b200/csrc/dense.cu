@@ -286,9 +286,9 @@ __global__ void __launch_bounds__(256, (4 * KS + 8 * NT <= 96) ? 2 : 1) rowmix_w
 }
 
 // rowmix by an upper-triangular K (r x r, exact zeros below the diagonal:
-// the CholQR2 factors R^-1): Y = X K with the MMA k index in natural order
-// (lane quad q owns columns 4 ks + q), so k step ks meets column group
-// (c0 + 8 nt ..) only when 4 ks <= c0 + 8 nt + 7 -- 72 of 128 DMMA
+// the CholQR2 factors R^-1): Y = X K with the MMA k index grouped by
+// 8-column blocks (see the kernel), so k step ks meets column group
+// (c0 + 8 nt ..) only when 8 (ks / 2) <= c0 + 8 nt + 7 -- 72 of 128 DMMA
 // fragments at r = 64, 272 of 512 at r = 128 (two 64-column passes).  Every
 // row of a warp's tile is loaded (all r columns) before any output of the
 // tile is written, so Y may alias X (in place).
@@ -300,26 +300,45 @@ __global__ void __launch_bounds__(256, 1) rowmix_upper_kernel(int n, int r,
   constexpr int KC = 4 * KS;    // K rows (padded r)
   constexpr int CW = 8 * NT;    // columns per pass
   constexpr int NP = KC / CW;   // passes (1 at r <= 64, 2 at r <= 128)
+  // k-step ks, lane quad q <-> column 8 (ks / 2) + 2 q + (ks & 1): the two
+  // k-steps of an 8-column block read adjacent columns per lane (one 16-byte
+  // load for both), and a k-step still lies inside one 8-column block, so the
+  // triangle's zero blocks are skipped as before.  sK row 4 ks + q holds that
+  // K row (fragment loads as in rowmix_wide).
   extern __shared__ double sK[];  // KC x ldks
   for (int e = threadIdx.x; e < KC * KC; e += blockDim.x) {
-    const int k = e / KC, col = e - k * KC;
-    sK[k * ldks + col] = (k < r && col < r) ? __ldg(K + (int64_t)k * ldk + col) : 0.0;
+    const int pr = e / KC, col = e - pr * KC;
+    const int ks = pr >> 2, qq = pr & 3;
+    const int k = 8 * (ks >> 1) + 2 * qq + (ks & 1);
+    sK[pr * ldks + col] = (k < r && col < r) ? __ldg(K + (int64_t)k * ldk + col) : 0.0;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
   const int64_t tiles = ((int64_t)n + 7) / 8;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const bool vstore = ((ldy & 1) == 0) && ((reinterpret_cast<uintptr_t>(Y) & 15) == 0);
+  const bool vload = ((ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) && r == KC;
   for (int64_t t0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 2; t0 < tiles;
        t0 += 2 * nwarps) {
     double af[2][KS];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int64_t row = (t0 + u) * 8 + g;
-      const double* xr = X + row * ldx + q;
+      const double* xr = X + row * ldx + 2 * q;
+      if (vload && row < n) {
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks)
-        af[u][ks] = (row < n && 4 * ks + q < r) ? xr[4 * ks] : 0.0;
+        for (int m = 0; m < KS / 2; ++m) {
+          const double2 v = *reinterpret_cast<const double2*>(xr + 8 * m);
+          af[u][2 * m] = v.x;
+          af[u][2 * m + 1] = v.y;
+        }
+      } else {
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const int c = 8 * (ks >> 1) + 2 * q + (ks & 1);
+          af[u][ks] = (row < n && c < r) ? X[row * ldx + c] : 0.0;
+        }
+      }
     }
     __syncwarp();  // every lane's reads of the tile precede the in-place writes
 #pragma unroll
@@ -335,7 +354,7 @@ __global__ void __launch_bounds__(256, 1) rowmix_upper_kernel(int n, int r,
         const double* kr = sK + (4 * ks + q) * ldks + c0 + g;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          if (4 * ks > c0 + 8 * nt + 7) continue;  // K rows 4 ks.. lie below these columns
+          if (8 * (ks >> 1) > c0 + 8 * nt + 7) continue;  // these K rows lie below the columns
           const double b = kr[8 * nt];
           dmma(d[0][nt][0], d[0][nt][1], af[0][ks], b);
           dmma(d[1][nt][0], d[1][nt][1], af[1][ks], b);
