@@ -2286,6 +2286,96 @@ __device__ __forceinline__ void project64d_group(const ProjArgs& pa, const dlrsn
   }
 }
 
+// Symmetric Gram G = X^T M X for 32 < r <= 64 with the diagonal-block K3's
+// layout: one CTA per cell range, every X element staged once from
+// registers together with M x (no separate premultiply pass: two barriers
+// per chunk), the 8 warps' 2 x 3-minus-corner fragment patterns (kD64Pat)
+// over all cells of a chunk -- no cross-warp reduction.  Chunks of 16 cells
+// (4 staging items per thread).  Columns >= r are staged as zeros.
+constexpr int kGC = 16;
+constexpr size_t kMgram64sSmem = 2 * (size_t)kGC * kRow64 * sizeof(double);
+
+__global__ void __launch_bounds__(256, 2) mgram64s_kernel(int ncell, int r,
+                                                          const double* __restrict__ X, int ldx,
+                                                          dlrsn_cellops ops, int cells_per_block,
+                                                          double* __restrict__ part) {
+  constexpr int kLS = kLS64, kRow = kRow64;
+  extern __shared__ __align__(16) double smg[];
+  double* sX = smg;
+  double* sMX = smg + kGC * kRow;
+  __shared__ double sm_m[16];
+  if (threadIdx.x < 16) sm_m[threadIdx.x] = ops.mass[threadIdx.x];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int pa0 = kD64Pat[warp][0], pa1 = kD64Pat[warp][1];
+  const int pb0 = kD64Pat[warp][2], pb1 = kD64Pat[warp][3], pb2 = kD64Pat[warp][4];
+  const int oa0 = 8 * pa0 + g, oa1 = 8 * pa1 + g;
+  const int ob0 = 8 * pb0 + g, ob1 = 8 * pb1 + g, ob2 = 8 * pb2 + g;
+  const int c_begin = blockIdx.x * cells_per_block;
+  const int c_end = min(ncell, c_begin + cells_per_block);
+  const int scl = threadIdx.x >> 6, scol = threadIdx.x & 63;
+  const bool c_ok = scol < r;
+  double acc[5][2];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) acc[k][0] = acc[k][1] = 0.0;
+  // the slot entries no fragment pattern covers (below the diagonal) stay
+  // zero; the mirror pass fills them after the reduction
+  for (int e = threadIdx.x; e < r * r; e += 256) part[(int64_t)blockIdx.x * r * r + e] = 0.0;
+  double raw[4][4];
+  auto fetch = [&](int c0) {
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int c = c0 + scl + 4 * m;
+      const bool live = c_ok && c < c_end;
+      const double* row = X + (int64_t)c * 4 * ldx + scol;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) raw[m][l] = live ? __ldg(row + (int64_t)l * ldx) : 0.0;
+    }
+  };
+  fetch(c_begin);
+  for (int c0 = c_begin; c0 < c_end; c0 += kGC) {
+    __syncthreads();  // the previous chunk's fragments are consumed
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int base = (scl + 4 * m) * kRow + scol;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        sX[base + kLS * l] = raw[m][l];
+        double v = 0.0;
+#pragma unroll
+        for (int p2 = 0; p2 < 4; ++p2) v = fma(sm_m[4 * l + p2], raw[m][p2], v);
+        sMX[base + kLS * l] = v;
+      }
+    }
+    __syncthreads();
+    fetch(c0 + kGC);  // next chunk's loads in flight during the MMAs
+#pragma unroll
+    for (int cl = 0; cl < kGC; ++cl) {
+      const double* xr = sX + cl * kRow + q * kLS;
+      const double* mr = sMX + cl * kRow + q * kLS;
+      const double x0 = xr[oa0], x1 = xr[oa1];
+      const double b0 = mr[ob0], b1 = mr[ob1], b2 = mr[ob2];
+      dmma(acc[0][0], acc[0][1], x0, b0);
+      dmma(acc[1][0], acc[1][1], x0, b1);
+      dmma(acc[2][0], acc[2][1], x1, b1);
+      dmma(acc[3][0], acc[3][1], x0, b2);
+      dmma(acc[4][0], acc[4][1], x1, b2);
+    }
+  }
+  __syncthreads();  // the zero fill above precedes every fragment store
+  double* out = part + (int64_t)blockIdx.x * r * r;
+  const int ra[5] = {pa0, pa0, pa1, pa0, pa1}, cb[5] = {pb0, pb1, pb1, pb2, pb2};
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int i = 8 * ra[k] + g;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = 8 * cb[k] + 2 * q + h;
+      if (i < r && j < r) out[(int64_t)i * r + j] = acc[k][h];
+    }
+  }
+}
+
 // Right / top domain-boundary faces of the diagonal 64-blocks (own right /
 // top edge against a zero exterior): X_e^T (1/2 e2) X_e per boundary cell,
 // added to px, jx (right wall) and py, jy (top wall).  The boundary cells
@@ -4129,6 +4219,28 @@ int mgram_vec(const dlrsn_cellops* ops, int ra, int rb, const double* A, int lda
   }
   const MgramPlan pl = mgram_plan(ncell, ra, rb);
   const int nblk = pl.nblk;
+  {
+    // symmetric single-block Gram (the CholQR2 Grams at 32 < r <= 64): the
+    // diagonal-block layout (DLRSN_MGRAM64S=0: the tiled kernel)
+    static const bool on = !(getenv("DLRSN_MGRAM64S") && getenv("DLRSN_MGRAM64S")[0] == '0');
+    if (on && A == B && lda == ldb && ra == rb && ra > 32 && ra <= 64 && !coeff && !v) {
+      static bool attr = false;
+      if (!attr) {
+        DLRSN_TRY_CUDA(cudaFuncSetAttribute(mgram64s_kernel,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)kMgram64sSmem));
+        attr = true;
+      }
+      mgram64s_kernel<<<nblk, 256, kMgram64sSmem, st>>>(ncell, ra, A, lda, *ops, pl.cpb, partial);
+      DLRSN_CHECK_LAUNCH("mgram64s_kernel");
+      const int64_t len = (int64_t)ra * rb;
+      reduce_partials_kernel<<<(unsigned)((len + 31) / 32), 1024, 0, st>>>(nblk, len, partial, G, 1.0);
+      DLRSN_CHECK_LAUNCH("reduce_partials_kernel");
+      mirror_gram_kernel<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(ra, 8, G);
+      DLRSN_CHECK_LAUNCH("mirror_gram_kernel");
+      return DLRSN_OK;
+    }
+  }
   bool tsym = false;
   if (pl.tb == 0) {
     mgram_mma_kernel<<<dim3(nblk, pl.tiles), kTile * kTile, 0, st>>>(ncell, ra, rb, A, lda, B, ldb,
