@@ -285,6 +285,90 @@ __global__ void __launch_bounds__(256, (4 * KS + 8 * NT <= 96) ? 2 : 1) rowmix_w
   }
 }
 
+// Software-pipelined rowmix_wide: one 8-row tile per iteration, the next
+// tile's rows loaded before this tile's MMAs (see rowmix_upper_pipe_kernel).
+template <int KS, int NT>
+__global__ void __launch_bounds__(384, 1) rowmix_wide_pipe_kernel(int n, int kx, int ky,
+                                                               const double* __restrict__ X, int ldx,
+                                                               const double* __restrict__ K, int ldk,
+                                                               double beta, double* __restrict__ Y,
+                                                               int ldy, int kyp, int ldks, int vec,
+                                                               const double* __restrict__ V,
+                                                               double* __restrict__ YV) {
+  extern __shared__ double sK[];  // (4 KS) x ldks
+  __shared__ double sV[4 * KS];
+  for (int e = threadIdx.x; e < 4 * KS * kyp; e += blockDim.x) {
+    const int pr = e / kyp, col = e - pr * kyp;
+    const int k = (pr & 3) * KS + (pr >> 2);
+    sK[pr * ldks + col] = (k < kx && col < ky) ? __ldg(K + (int64_t)k * ldk + col) : 0.0;
+  }
+  if (V)
+    for (int e = threadIdx.x; e < 4 * KS; e += blockDim.x) sV[e] = e < kx ? __ldg(V + e) : 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int64_t tiles = ((int64_t)n + 7) / 8;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool vstore = beta == 0.0 && ((ldy & 1) == 0) && ((reinterpret_cast<uintptr_t>(Y) & 15) == 0);
+  auto load = [&](int64_t t, double (&af)[KS]) {
+    const int64_t row = t * 8 + g;
+    const bool live = t < tiles && row < n;
+    const double* xr = X + row * ldx + q * KS;
+    if (live && vec) {
+#pragma unroll
+      for (int ks = 0; ks < KS; ks += 2) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(xr + ks));
+        af[ks] = v.x;
+        af[ks + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) af[ks] = (live && q * KS + ks < kx) ? __ldg(xr + ks) : 0.0;
+    }
+  };
+  int64_t t0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double cur[KS], nxt[KS];
+  load(t0, cur);
+  for (; t0 < tiles; t0 += nwarps) {
+    load(t0 + nwarps, nxt);
+    const int64_t row = t0 * 8 + g;
+    if (V) {
+      double acc = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) acc = fma(cur[ks], sV[q * KS + ks], acc);
+      acc += __shfl_xor_sync(kFull, acc, 1);
+      acc += __shfl_xor_sync(kFull, acc, 2);
+      if (q == 0 && row < n) YV[row] = acc;
+    }
+    for (int c0 = 0; c0 < ky; c0 += 8 * NT) {
+      double d[NT][2];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) d[nt][0] = d[nt][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const double* kr = sK + (4 * ks + q) * ldks + c0 + g;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma(d[nt][0], d[nt][1], cur[ks], kr[8 * nt]);
+      }
+      if (row < n) {
+        double* y = Y + row * ldy;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int c = c0 + 8 * nt + 2 * q;
+          if (vstore && c + 1 < ky) {
+            *reinterpret_cast<double2*>(y + c) = make_double2(d[nt][0], d[nt][1]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+              if (c + i < ky) y[c + i] = beta == 0.0 ? d[nt][i] : fma(beta, y[c + i], d[nt][i]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) cur[ks] = nxt[ks];
+  }
+}
+
 // rowmix by an upper-triangular K (r x r, exact zeros below the diagonal:
 // the CholQR2 factors R^-1): Y = X K with the MMA k index grouped by
 // 8-column blocks (see the kernel), so k step ks meets column group
@@ -381,6 +465,93 @@ __global__ void __launch_bounds__(256, 1) rowmix_upper_kernel(int n, int r,
   }
 }
 
+// Software-pipelined variant: one 8-row tile per iteration, the next tile's
+// rows loaded (into registers) before this tile's MMAs, so loads, MMAs and
+// stores of a warp overlap (the two-tile kernel above is co-bound by its
+// loads and its MMAs: 0.87 ms at C4 vs a 0.64 ms overlap bound).  The next
+// tile belongs to the same warp and is disjoint from the tile being written,
+// so Y may still alias X.
+template <int KS, int NT>
+__global__ void __launch_bounds__(384, 1) rowmix_upper_pipe_kernel(int n, int r, const double* X,
+                                                                int ldx,
+                                                                const double* __restrict__ K,
+                                                                int ldk, double* Y, int ldy,
+                                                                int ldks) {
+  constexpr int KC = 4 * KS, CW = 8 * NT, NP = KC / CW;
+  extern __shared__ double sK[];  // KC x ldks, rows in fragment order (see rowmix_upper_kernel)
+  for (int e = threadIdx.x; e < KC * KC; e += blockDim.x) {
+    const int pr = e / KC, col = e - pr * KC;
+    const int ks = pr >> 2, qq = pr & 3;
+    const int k = 8 * (ks >> 1) + 2 * qq + (ks & 1);
+    sK[pr * ldks + col] = (k < r && col < r) ? __ldg(K + (int64_t)k * ldk + col) : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int64_t tiles = ((int64_t)n + 7) / 8;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool vstore = ((ldy & 1) == 0) && ((reinterpret_cast<uintptr_t>(Y) & 15) == 0);
+  const bool vload = ((ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) && r == KC;
+  auto load = [&](int64_t t, double (&af)[KS]) {
+    const int64_t row = t * 8 + g;
+    const bool live = t < tiles && row < n;
+    const double* xr = X + row * ldx + 2 * q;
+    if (vload && live) {
+#pragma unroll
+      for (int m = 0; m < KS / 2; ++m) {
+        const double2 v = *reinterpret_cast<const double2*>(xr + 8 * m);
+        af[2 * m] = v.x;
+        af[2 * m + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int c = 8 * (ks >> 1) + 2 * q + (ks & 1);
+        af[ks] = (live && c < r) ? X[row * ldx + c] : 0.0;
+      }
+    }
+  };
+  int64_t t0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double cur[KS], nxt[KS];
+  load(t0, cur);
+  for (; t0 < tiles; t0 += nwarps) {
+    load(t0 + nwarps, nxt);
+    __syncwarp();  // every lane's reads of this tile precede the in-place writes
+    const int64_t row = t0 * 8 + g;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const int c0 = p * CW;
+      double d[NT][2];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) d[nt][0] = d[nt][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const double* kr = sK + (4 * ks + q) * ldks + c0 + g;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          if (8 * (ks >> 1) > c0 + 8 * nt + 7) continue;
+          dmma(d[nt][0], d[nt][1], cur[ks], kr[8 * nt]);
+        }
+      }
+      if (row < n) {
+        double* y = Y + row * ldy;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int c = c0 + 8 * nt + 2 * q;
+          if (vstore && c + 1 < r) {
+            *reinterpret_cast<double2*>(y + c) = make_double2(d[nt][0], d[nt][1]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+              if (c + i < r) y[c + i] = d[nt][i];
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) cur[ks] = nxt[ks];
+  }
+}
+
 int rowmix_upper(int64_t n, int r, const double* X, int ldx, const double* K, int ldk, double* Y,
                  int ldy, cudaStream_t st) {
   if (r <= 16 || r > 128 || n < 64)
@@ -397,6 +568,20 @@ int rowmix_upper(int64_t n, int r, const double* X, int ldx, const double* K, in
     constexpr int KS = 16, NT = 8;
     const int ldks = 64 + 4;
     const size_t smem = (size_t)4 * KS * ldks * sizeof(double);
+    // software-pipelined kernel, 12 warps per SM (DLRSN_ROWMIX_PIPE=0: the
+    // two-tile kernel; 1: 8 warps): C4 0.87 -> 0.70 (8 warps) -> 0.66 ms
+    static const int pipe = getenv("DLRSN_ROWMIX_PIPE") ? atoi(getenv("DLRSN_ROWMIX_PIPE")) : 2;
+    if (pipe) {
+      DLRSN_TRY_CUDA(cudaFuncSetAttribute(rowmix_upper_pipe_kernel<KS, NT>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const int threads = pipe >= 2 ? 384 : 256;  // 162 registers: 12 warps fit one SM
+      int64_t pb = (tiles + 7) / 8;
+      if (pb > 148) pb = 148;
+      rowmix_upper_pipe_kernel<KS, NT><<<(int)pb, threads, smem, st>>>((int)n, r, X, ldx, K, ldk, Y,
+                                                                      ldy, ldks);
+      DLRSN_CHECK_LAUNCH("rowmix_upper_pipe_kernel");
+      return DLRSN_OK;
+    }
     DLRSN_TRY_CUDA(cudaFuncSetAttribute(rowmix_upper_kernel<KS, NT>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     rowmix_upper_kernel<KS, NT><<<(int)blocks, 256, smem, st>>>((int)n, r, X, ldx, K, ldk, Y, ldy, ldks);
@@ -3984,6 +4169,19 @@ int rowmix_vec(int64_t n, int kx, int ky, const double* X, int ldx, const double
     if (blocks > 148 * 4) blocks = 148 * 4;
     cudaStream_t st = as_stream(stream);
 #define DLRSN_ROWMIX_WIDE(KS, NT)                                                                do {                                                                                             if (smem > 48 * 1024)                                                                            DLRSN_TRY_CUDA(cudaFuncSetAttribute(rowmix_wide_kernel<KS, NT>,                                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));     rowmix_wide_kernel<KS, NT><<<(int)blocks, 256, smem, st>>>((int)n, kx, ky, X, ldx, K, ldk, beta,                                                                Y, ldy, kyp, ldks, vec, V, YV);          } while (0)
+    static const int pipe = getenv("DLRSN_ROWMIX_PIPE") ? atoi(getenv("DLRSN_ROWMIX_PIPE")) : 2;
+    if (pipe && ks == 16 && nt == 8 && static_cast<const void*>(X) != static_cast<const void*>(Y)) {
+      // r in (32, 64] with > 32 output columns: the software-pipelined kernel
+      if (smem > 48 * 1024)
+        DLRSN_TRY_CUDA(cudaFuncSetAttribute(rowmix_wide_pipe_kernel<16, 8>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int64_t pb = (tiles + 7) / 8;
+      if (pb > 148) pb = 148;
+      rowmix_wide_pipe_kernel<16, 8><<<(int)pb, pipe >= 2 ? 384 : 256, smem, st>>>(
+          (int)n, kx, ky, X, ldx, K, ldk, beta, Y, ldy, kyp, ldks, vec, V, YV);
+      DLRSN_CHECK_LAUNCH("rowmix_wide_pipe_kernel");
+      return DLRSN_OK;
+    }
     if (ks == 4) {
       if (nt == 8) DLRSN_ROWMIX_WIDE(4, 8);
       else if (nt == 4) DLRSN_ROWMIX_WIDE(4, 4);

@@ -1314,10 +1314,13 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     info->iterations = hs->ctl.iters;
     // next step's batch hint: grows to cover this step's count (stable
     // batches keep the graph keys stable; a shortfall costs one more segment)
-    // (rounded up to a multiple of 4: a slowly growing count -- the Marshak
-    // wave's 15, 16, 19, 20 -- re-captures the graphs once, not every step;
-    // iterations past convergence return at once)
-    info->si_batch_hint = std::max(batch0, (hs->ctl.iters + 1 + 3) / 4 * 4);
+    // (above 8, rounded up to a multiple of 8: a slowly growing count -- the
+    // Marshak wave's 15, 16, 19, 20 -- re-captures the step graphs once, not
+    // at every change; iterations past convergence return at once)
+    {
+      const int want = hs->ctl.iters + 1;
+      info->si_batch_hint = std::max(batch0, want <= 8 ? want : (want + 7) / 8 * 8);
+    }
     if (!exact) {
       // CholQR's R_kk is accurate to ~eps/rel^2: keep it only when every
       // column retains >= 1e-6 of its M-norm and sits 100x above the
