@@ -3121,9 +3121,17 @@ __global__ void row_inverse_kernel(int r, const double* __restrict__ proj,
       if (i != k && i != p) colk[i] = a[i * w + k];
     if (threadIdx.x == 0 && p != k) colk[k] = 0.0;
     __syncthreads();
-    for (int e = threadIdx.x; e < r * w; e += blockDim.x) {
-      const int i = e / w, j = e % w;
-      if (i != k && j > k) a[i * w + j] -= colk[i] * a[k * w + j];
+    // rank-1 elimination: a warp per row, lanes across the columns j > k (no
+    // index division; the pivot row's entries are read once per lane)
+    {
+      const int wid = threadIdx.x >> 5, nwp = blockDim.x >> 5;
+      for (int j0 = k + 1; j0 < w; j0 += 32) {
+        const int j = j0 + lane;
+        const double akj = j < w ? a[k * w + j] : 0.0;
+        if (j < w)
+          for (int i = wid; i < r; i += nwp)
+            if (i != k) a[i * w + j] = fma(-colk[i], akj, a[i * w + j]);
+      }
     }
     __syncthreads();
   }
