@@ -3043,7 +3043,8 @@ __global__ void __launch_bounds__(256) cholqr2_small_kernel(int n, int m,
 __global__ void small_matmul_kernel(int m, int k, int n, const double* __restrict__ A,
                                     const double* __restrict__ B, double* __restrict__ C,
                                     int transA) {
-  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
+  // entries spread over the grid (same per-entry summation order as one CTA)
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m * n; e += gridDim.x * blockDim.x) {
     const int i = e / n, j = e % n;
     double s = 0.0;
     for (int p = 0; p < k; ++p) s = fma(transA ? A[p * m + i] : A[i * k + p], B[p * n + j], s);
@@ -4720,7 +4721,8 @@ int dlrsn_cholqr2_small(int n, int m, const double* W, int ldw, const double* w,
 
 int dlrsn_small_matmul(int m, int k, int n, const double* A, const double* B, double* C,
                        int transA, dlrsn_stream_t stream) {
-  small_matmul_kernel<<<1, 256, 0, as_stream(stream)>>>(m, k, n, A, B, C, transA);
+  const int blocks = (m * n + 255) / 256 < 64 ? (m * n + 255) / 256 : 64;
+  small_matmul_kernel<<<blocks < 1 ? 1 : blocks, 256, 0, as_stream(stream)>>>(m, k, n, A, B, C, transA);
   DLRSN_CHECK_LAUNCH("small_matmul_kernel");
   return DLRSN_OK;
 }

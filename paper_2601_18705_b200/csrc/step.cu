@@ -24,21 +24,29 @@ __global__ void ks_kernel(int r, const double* __restrict__ S, const double* __r
                           const int* __restrict__ idx, const double* __restrict__ beta,
                           double* __restrict__ K, double* __restrict__ Sb,
                           const double* __restrict__ omegas, double* __restrict__ om_sel) {
+  // a warp per output, lanes along the contraction index (coalesced row
+  // reads of S and of the gathered W rows; a thread per output made every
+  // warp load touch 32 different rows of W); rows spread over the CTAs
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if (K)
-    for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
-      const int i = e / r, d = e % r;
-      const double* w = W + (int64_t)idx[d] * r;
-      double s = 0.0;
-      for (int j = 0; j < r; ++j) s = fma(S[i * r + j], w[j], s);
-      K[e] = s;
-    }
+    for (int i = blockIdx.x; i < r; i += gridDim.x)
+      for (int d = warp; d < r; d += nw) {
+        const double* w = W + (int64_t)idx[d] * r;
+        double s = 0.0;
+        for (int j = lane; j < r; j += 32) s = fma(S[i * r + j], w[j], s);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+        if (lane == 0) K[i * r + d] = s;
+      }
   if (Sb)
-    for (int i = threadIdx.x; i < r; i += blockDim.x) {
+    for (int i = blockIdx.x * nw + warp; i < r; i += gridDim.x * nw) {
       double s = 0.0;
-      for (int j = 0; j < r; ++j) s = fma(S[i * r + j], beta[j], s);
-      Sb[i] = s;
+      for (int j = lane; j < r; j += 32) s = fma(S[i * r + j], beta[j], s);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+      if (lane == 0) Sb[i] = s;
     }
-  if (om_sel)
+  if (om_sel && blockIdx.x == 0)
     for (int e = threadIdx.x; e < 3 * r; e += blockDim.x)
       om_sel[e] = omegas[(int64_t)idx[e / 3] * 3 + e % 3];
 }
@@ -1005,7 +1013,7 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
       DLRSN_RET(cgroup_plan_launch(G, b.groups, sweep_group_width(), r, b.cgtab, b.cg_quad, b.cg_w,
                                    st));
     // 2. evaluate_rows (dlr_sn.py:110-121) and the sweep rhs
-    ks_kernel<<<1, 1024, 0, st>>>(r, S, W, b.idx, beta, b.K, nullptr, p->omegas_dev, b.om_sel);
+    ks_kernel<<<r, 256, 0, st>>>(r, S, W, b.idx, beta, b.K, nullptr, p->omegas_dev, b.om_sel);
     DLRSN_CHECK_LAUNCH("ks_kernel");
     if (p->use_dsa) {
       DLRSN_TRY_CUDA(zero_async(b.dsa_info, 4 * sizeof(int), st));
@@ -1016,7 +1024,7 @@ int dlrsn_step_collocation(const dlrsn_cellops* ops, const dlrsn_step_params* p,
     }
     // scalar_flux (lowrank.py:60-62) -> the first scattering source; phi0 = X
     // (S beta) comes out of the same pass over X as psi_time = X K
-    ks_kernel<<<1, 256, 0, st>>>(r, S, W, nullptr, beta, nullptr, b.Sb, p->omegas_dev, nullptr);
+    ks_kernel<<<(r + 7) / 8, 256, 0, st>>>(r, S, W, nullptr, beta, nullptr, b.Sb, p->omegas_dev, nullptr);
     DLRSN_CHECK_LAUNCH("ks_kernel");
     DLRSN_RET(rowmix_vec(N, r, r, X, r, b.K, r, 0.0, b.psi_time, r, b.Sb, b.phi0, s));
     DLRSN_RET(dlrsn_scatter_source(ops, b.phi0, sigma_s, b.scat, b.flags + 1, s));
