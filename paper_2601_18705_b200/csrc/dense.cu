@@ -4178,7 +4178,7 @@ int rowmix_vec(int64_t n, int kx, int ky, const double* X, int ldx, const double
     if (blocks > 148 * 4) blocks = 148 * 4;
     cudaStream_t st = as_stream(stream);
 #define DLRSN_ROWMIX_WIDE(KS, NT)                                                                do {                                                                                             if (smem > 48 * 1024)                                                                            DLRSN_TRY_CUDA(cudaFuncSetAttribute(rowmix_wide_kernel<KS, NT>,                                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));     rowmix_wide_kernel<KS, NT><<<(int)blocks, 256, smem, st>>>((int)n, kx, ky, X, ldx, K, ldk, beta,                                                                Y, ldy, kyp, ldks, vec, V, YV);          } while (0)
-    static const int pipe = getenv("DLRSN_ROWMIX_PIPE") ? atoi(getenv("DLRSN_ROWMIX_PIPE")) : 2;
+    static const int pipe = getenv("DLRSN_ROWMIX_WIDE_PIPE") ? atoi(getenv("DLRSN_ROWMIX_WIDE_PIPE")) : 0;
     if (pipe && ks == 16 && nt == 8 && static_cast<const void*>(X) != static_cast<const void*>(Y)) {
       // r in (32, 64] with > 32 output columns: the software-pipelined kernel
       if (smem > 48 * 1024)
