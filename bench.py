@@ -489,20 +489,33 @@ def main(argv=None):
     # of addresses (about 8-14 distinct sets in a chained loop); every set is
     # one CUDA graph, so the untimed settling runs past that period before
     # the W warm-up steps proper
-    for _ in range(16 + args.warmup):
-        one_step()
-    torch.cuda.synchronize()
-
+    # (the L2-flush buffer and the events are allocated BEFORE the settling
+    # steps: an allocation between warm-up and the timed region shifts the
+    # caching allocator's rotation, and a buffer set first seen inside the
+    # timed region costs one graph capture there -- a ~70-90 ms step)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 512 MB > L2
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    # NVML is initialised and queried during the settling steps too: on a
+    # fresh box the first queries disturbed the step after them (one ~80 ms
+    # step at index 1 of the timed region in the first bench run of a box)
+    clk = ClockSampler(local)
+    clk.__enter__()
+    for k in range(16 + args.warmup):
+        flush.fill_(float(k))
+        one_step()
+        clk.tick()
+    torch.cuda.synchronize()
+    clk.samples.clear()
+    clk.lines.clear()
+
     iters = []
     launches0 = _lib.launch_count()
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     wall0 = time.perf_counter()
-    with ClockSampler(local) as clk:
+    try:
         for k in range(args.steps):
             flush.fill_(float(k))  # evict L2 between timed steps (outside the events)
             starts[k].record()
@@ -511,6 +524,8 @@ def main(argv=None):
             clk.tick()
             iters.append(info.iterations)
         torch.cuda.synchronize()
+    finally:
+        clk.__exit__(None, None, None)
     wall = time.perf_counter() - wall0
     launches = _lib.launch_count() - launches0
     per_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
@@ -825,9 +840,9 @@ def measure_config(name, steps=6, warmup=None):
     state = initial_state(dp)
     T = torch.as_tensor(spec.T0, device="cuda").clone()
     lin = dp.linearized(T)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")  # before the warm-up
     for _ in range(warmup):
         state, lin, T, _ = dp.step(state, lin, T, si_tol=1e-8)
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
     ms, iters, per = 0.0, [], []
     for k in range(steps):
         flush.fill_(float(k))
